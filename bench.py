@@ -1,0 +1,316 @@
+#!/usr/bin/env python3
+"""Benchmark of the correction-step hot path (BASELINE.json configs[1], "cfg2").
+
+Workload (one step): the operator micro-benchmark of BASELINE.json configs[1] --
+A = 1/2 K + M_V - sigma M (sigma = -0.5) on the Kuhn-split P1 mesh of a 128^3 vertex
+grid over [-10,10]^3 (2,000,376 interior DOFs, 29.6 M interior nonzeros), V = -sum of
+4 seeded Gaussians, and a block of N = 16 seeded N(0,1) right-hand sides driven through
+exactly 200 iterations of the multi-RHS preconditioned CG (Jacobi). FP64.
+value = interior DOFs * 16 orbitals * 200 iterations / step time  [DOF*orbital*iter/s].
+
+Arms: default = the B200 path (libksb.so kernels); --impl reference = the CPU oracle's
+restatement of the reference's own algorithm (SGS-PCG, proj/src/solver.cpp:57-111) on the
+host cores (the reference itself cannot be built here: SURVEY.md section 8c).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "fine-solve DOF*orbital*iter/s; correction-step time; SpMM % of HBM peak"
+UNIT = "DOF*orbital*iter/s"
+N_RHS = 16
+ITERS = 200
+GRID = 127  # cells per axis -> 128^3 vertices
+BOX = 10.0
+SEED = 20210304
+
+
+def gaussians(seed=SEED):
+    """4 seeded wells: centres U[-3,3]^3, widths U(0.5,1.5), depths U(1,5); V = -sum d exp(-|x-c|^2/(2 w^2))."""
+    rng = np.random.default_rng(seed)
+    c = rng.uniform(-3.0, 3.0, (4, 3))
+    w = rng.uniform(0.5, 1.5, 4)
+    d = rng.uniform(1.0, 5.0, 4)
+    return np.column_stack([d, w, c])
+
+
+def rhs_block(ni, seed=SEED + 1):
+    return np.random.default_rng(seed).standard_normal((ni, N_RHS))
+
+
+def measured_peak():
+    try:
+        j = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+        return float(j["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = tempfile.mktemp(suffix=".csv")
+
+    def __enter__(self):
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+            self.f.close()
+
+    def summary(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = []
+        for line in open(self.path):
+            p = [x.strip() for x in line.split(",")]
+            if len(p) >= 7:
+                try:
+                    rows.append((float(p[0]), float(p[1]), p[3:7]))
+                except ValueError:
+                    pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, r in rows for i in range(4) if r[i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median([r[0] for r in rows])), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+def dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ----------------------------------------------------------------------------------- CPU legs
+def cpu_leg(iters_sample: int):
+    """Oracle SGS-PCG (reference algorithm) on the same operator; a bounded sample: 16 columns x iters_sample."""
+    from oracle import OMesh, Oracle
+    t0 = time.time()
+    m = OMesh.box([-BOX] * 3, [BOX] * 3, GRID)
+    orc = Oracle([[1.0, 0, 0, 0]])
+    orc.push(m)
+    op = orc.operator(0, c_s=0.5, c_m=0.5, potential=(1, gaussians()), precond=0)
+    B = rhs_block(op.ni)
+    setup = time.time() - t0
+    t1 = time.perf_counter()
+    op.pcg(B, fixed=iters_sample)
+    dt = time.perf_counter() - t1
+    return op.ni, dt, setup
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    sample = args.cpu_iters
+    from oracle import OMesh, Oracle
+    m = OMesh.box([-BOX] * 3, [BOX] * 3, GRID)
+    orc = Oracle([[1.0, 0, 0, 0]])
+    orc.push(m)
+    op = orc.operator(0, c_s=0.5, c_m=0.5, potential=(1, gaussians()), precond=0)
+    B = rhs_block(op.ni)
+    for _ in range(max(0, args.warmup)):
+        op.pcg(B, fixed=1)
+    times = []
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        op.pcg(B, fixed=sample)
+        times.append(time.perf_counter() - t)
+    dt = float(np.mean(times))
+    value = op.ni * N_RHS * sample / dt
+    used = min(cores, N_RHS)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 * ITERS / sample,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "cfg2 operator micro-benchmark: 128^3 Kuhn P1, A=1/2K+M_V+0.5M, N=16, 200 CG its",
+                       "n_interior": op.ni, "n_rhs": N_RHS, "iterations": ITERS, "l2": "inputs larger than L2"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": used, "kind": "port",
+                             "sample": f"oracle SGS-PCG (reference algorithm), 16 columns x {sample} iterations per "
+                                       f"step, OpenMP over columns"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------------- GPU leg
+def run_b200(args, world, rank, local):
+    import torch
+
+    import paper_2103_02824_b200 as kb
+    torch.cuda.set_device(local)
+    ctx = kb.Context(local)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
+
+    t0 = time.time()
+    mesh = kb.Mesh.box([-BOX] * 3, [BOX] * 3, GRID)
+    h = kb.Hierarchy()
+    h.push(mesh)
+    L = kb.Level(ctx, h, 0)
+    L.assemble(kb.MAT_USER0, c_s=0.5, c_m=0.5, potential=(kb.POT_GAUSSIAN, gaussians()))
+    setup_s = time.time() - t0
+    ni = L.ni
+    B = rhs_block(ni)
+    dB = ctx.to_device(B)
+    dX = ctx.empty((ni, N_RHS))
+    opts = L.cg_options(fixed_iterations=ITERS)
+
+    def step():
+        return L.cg_solve(kb.MAT_USER0, dB, dX, N_RHS, opts=opts)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    ctx.sync()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = ctx.launches()
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            stats = step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    launches = ctx.launches() - launches0
+    ms = ev0.elapsed_time(ev1) / args.steps
+    ms = max_over_ranks(ms, world)
+    value = world * ni * N_RHS * ITERS / (ms * 1e-3)
+    breakdown_cols = sum(1 for s in stats if s.breakdown)
+
+    # dominant kernel: the fused SpMM (Ap = A p + p.Ap partials), timed per launch with events on its stream
+    ctx.reset_counters()
+    ctx.set_profiling(True)
+    step()
+    ctx.set_profiling(False)
+    spmm_ms, spmm_n = ctx.kernel_time("spmm")
+    upd_ms, upd_n = ctx.kernel_time("cg_update")
+    spmm_avg = spmm_ms / max(1, spmm_n)
+    bytes_spmm = 12 * L.nnz_ii + 4 * (ni + 1) + 16 * ni * N_RHS
+    achieved = bytes_spmm / (spmm_avg * 1e-3) / 1e9
+    peak, peak_kind = measured_peak()
+
+    # end to end through the C-ABI with pinned host buffers (H2D of B, D2H of X inside the timed region)
+    hB = torch.empty((ni, N_RHS), dtype=torch.float64, pin_memory=True)
+    hX = torch.empty((ni, N_RHS), dtype=torch.float64, pin_memory=True)
+    hB.numpy()[:] = B
+    for _ in range(2):
+        L.cg_solve_host(kb.MAT_USER0, hB.numpy(), N_RHS, opts=opts, out=hX.numpy())
+    barrier(world)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        L.cg_solve_host(kb.MAT_USER0, hB.numpy(), N_RHS, opts=opts, out=hX.numpy())
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
+    e2e = world * ni * N_RHS * ITERS / (e2e_ms * 1e-3)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count() or 1))
+        cni, cdt, _ = cpu_leg(args.cpu_iters)
+        cpu = {"value": cni * N_RHS * args.cpu_iters / cdt, "unit": UNIT,
+               "cores": min(os.cpu_count() or 1, N_RHS), "kind": "port",
+               "sample": f"oracle SGS-PCG (reference algorithm) on the same operator: 16 columns x {args.cpu_iters} "
+                         f"iterations ({cdt:.1f} s), OpenMP over columns"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded Gaussians and N(0,1) RHS)",
+            "config": {"workload": "cfg2 operator micro-benchmark: 128^3 Kuhn P1, A=1/2K+M_V+0.5M, N=16, 200 CG its",
+                       "n_interior": ni, "nnz_interior": L.nnz_ii, "n_rhs": N_RHS, "iterations": ITERS,
+                       "preconditioner": "jacobi", "parallelism": f"replicas{world}",
+                       "l2": "inputs larger than L2 (256 MB blocks, 363 MB operator)",
+                       "breakdown_columns": breakdown_cols, "setup_s": round(setup_s, 2)},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": None, "kernel": "k_spmm_dot", "bytes_per_launch": bytes_spmm,
+                         "avg_launch_ms": spmm_avg, "peak_kind": peak_kind},
+            "spmm_hbm_frac": achieved / peak,
+            "cg_update_avg_ms": upd_ms / max(1, upd_n),
+            "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": B.nbytes, "d2h_bytes_per_step": B.nbytes,
+                    "ms_per_step": e2e_ms},
+            "gpu_launches": launches // max(1, args.steps) * args.steps,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    L.close()
+    ctx.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--cpu-iters", type=int, default=8, help="CPU oracle sample: iterations per 16-column block")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    world, rank, local = dist_init()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_b200(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,163 @@
+/*
+ * ksb.h -- C-ABI of the B200-native correction-step hot path of the
+ * multilevel-correction adaptive FEM for Kohn-Sham (arXiv 2103.02824).
+ *
+ * Drop-in boundary. The reference exposes the path as a C++ namespace API
+ * (no FFI of its own); each entry point below names the reference interface it
+ * replaces (file:line under /root/reference/proj). Conventions:
+ *   - every function returns an int status; codes are 1:1 with the reference's
+ *     ksafem::Error string codes (proj/include/ksafem/types.hpp:20-32);
+ *     ksb_last_error() returns the message of the last failure on this thread;
+ *   - no exceptions cross the ABI; plain pointers and sizes only;
+ *   - "d_" pointers are device pointers, "h_" pointers host pointers;
+ *   - one CUDA stream per context; a context is driven by one host thread;
+ *   - reductions are fixed-order (no floating-point atomics): reruns are bitwise stable.
+ * Vector layout: orbital blocks are row-major (rows = dofs, ld >= N columns), so a
+ * gathered row is N contiguous doubles.
+ */
+#ifndef KSB_H
+#define KSB_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (reference proj/include/ksafem/types.hpp:20-32) */
+#define KSB_OK 0
+#define KSB_NONCONVERGENCE 1
+#define KSB_MISMATCHED_SPACES 2
+#define KSB_SINGULAR_QUADRATURE 3
+#define KSB_AMBIGUOUS_SELECTION 4
+#define KSB_INTERNAL 5
+#define KSB_INVALID_ARGUMENT 6
+#define KSB_INVALID_DOMAIN 7
+#define KSB_HIERARCHY 8
+#define KSB_IO 9
+#define KSB_CUDA 10
+
+typedef struct ksb_mesh ksb_mesh;
+typedef struct ksb_hier ksb_hier;
+typedef struct ksb_ctx ksb_ctx;
+typedef struct ksb_level ksb_level;
+
+const char* ksb_last_error(void);
+const char* ksb_code_name(int code);
+int ksb_version(void);
+
+/* ---------------- host mesh pipeline (bit-exact index data) ----------------
+ * replaces mesh::build_box_mesh / uniform_refine / adapt_refine
+ * (proj/include/ksafem/mesh.hpp:93-105, proj/src/mesh.cpp:281-368) */
+int ksb_mesh_box(const double lo[3], const double hi[3], int n_per_axis, ksb_mesh** out);
+int ksb_mesh_uniform_refine(const ksb_mesh* m, ksb_mesh** out);
+int ksb_mesh_adapt_refine(const ksb_mesh* m, const int32_t* marked, int64_t n_marked, ksb_mesh** out);
+void ksb_mesh_free(ksb_mesh* m);
+/* sizes[0..7] = n_vertices, n_tets, n_boundary_faces, n_interior_faces, level,
+ * n_parent_vertices, 0, 0 */
+int ksb_mesh_sizes(const ksb_mesh* m, int64_t sizes[8]);
+/* what: 0 xyz(double n*3) 1 tets(int32 T*4) 2 tuple(int32 T*4) 3 tag(int8 T)
+ *       4 parent(int32 T) 5 vparent(int32 n*2) 6 on_boundary(uint8 n)
+ *       7 boundary faces(int32 nbf*3) 8 interior faces(int32 nif*3)
+ *       9 interior face tets(int32 nif*2) 10 interior face geometry(double nif*5) */
+int ksb_mesh_get(const ksb_mesh* m, int what, void* h_dst);
+
+/* ---------------- hierarchy (fem::SpaceHierarchy, proj/include/ksafem/fespace.hpp:65-81) */
+int ksb_hier_create(ksb_hier** out);
+int ksb_hier_push(ksb_hier* h, const ksb_mesh* m); /* copies the mesh handle (shared) */
+void ksb_hier_free(ksb_hier* h);
+int ksb_hier_levels(const ksb_hier* h);
+/* composite prolongation P(0, level): per vertex <=4 (level-0 vertex, value), -1 padded.
+ * replaces SpaceHierarchy::prolongation (proj/src/fespace.cpp:64-74) */
+int ksb_hier_prolongation(const ksb_hier* h, int level, int32_t* h_col, double* h_val);
+
+/* ---------------- device context ---------------- */
+int ksb_ctx_create(int device, ksb_ctx** out);
+void ksb_ctx_destroy(ksb_ctx* c);
+int ksb_ctx_stream(ksb_ctx* c, void** stream); /* cudaStream_t of the context */
+int ksb_ctx_sync(ksb_ctx* c);
+/* per-kernel CUDA-event instrumentation (off by default); names: "spmm", "cg_update",
+ * "assemble", ... ms = summed device time, count = launches since reset */
+int ksb_ctx_set_profiling(ksb_ctx* c, int on);
+int ksb_ctx_kernel_time(ksb_ctx* c, const char* name, double* ms, int64_t* count);
+int ksb_ctx_kernel_launches(ksb_ctx* c, int64_t* total); /* all kernels launched since reset */
+int ksb_ctx_reset_counters(ksb_ctx* c);
+int ksb_malloc(ksb_ctx* c, void** d_ptr, int64_t bytes);
+int ksb_free(ksb_ctx* c, void* d_ptr);
+int ksb_memcpy_h2d(ksb_ctx* c, void* d_dst, const void* h_src, int64_t bytes); /* async on ctx stream */
+int ksb_memcpy_d2h(ksb_ctx* c, void* h_dst, const void* d_src, int64_t bytes); /* async on ctx stream */
+
+/* ---------------- fine level on the device ----------------
+ * Uploads the FE space split, interior CSR patterns, the deterministic assembly
+ * gather lists, P_int and the coarse-ancestor grouping of level `level` of `h`.
+ * replaces FESpace + EllipticSolver's pattern gather (proj/src/fespace.cpp:7-18,
+ * proj/src/solver.cpp:11-48) */
+int ksb_level_create(ksb_ctx* c, const ksb_hier* h, int level, ksb_level** out);
+void ksb_level_destroy(ksb_level* l);
+/* sizes[0..9] = n, n_interior, n_boundary, n_tets, nnz_ii, nnz_ib, n_coarse_interior,
+ * n_coarse_tets, n_coarse_vertices, 0 */
+int ksb_level_sizes(const ksb_level* l, int64_t sizes[10]);
+/* host copies of index data for bit-exactness checks: what 0 ii.ptr 1 ii.col 2 ib.ptr
+ * 3 ib.col 4 interior vertex ids 5 P_int cols (ni*4) 6 P_int vals (double ni*4) */
+int ksb_level_index(const ksb_level* l, int what, void* h_dst);
+
+/* ---------------- operators (interior blocks stored on the shared pattern) ----------------
+ * A matrix is an id in the level's operator table. The interior-interior values live
+ * on the ii pattern and the interior-boundary values on the ib pattern. */
+#define KSB_MAT_S 0        /* stiffness (grad, grad), assemble_stiffness proj/src/assembly.cpp:93-105 */
+#define KSB_MAT_M 1        /* unit mass, assemble_mass proj/src/assembly.cpp:135-138 */
+#define KSB_MAT_AOP 2      /* a_op = 1/2 S + M_ext, make_level_ops proj/src/driver.cpp:41-43 */
+#define KSB_MAT_USER0 8    /* free ids 8..31 */
+
+/* analytic potential descriptor, evaluated at quadrature points */
+#define KSB_POT_COULOMB 0  /* params (Z, x, y, z) per center; -sum Z/r, r<1e-12 -> 1e-10 (proj/src/ks_model.cpp:33-41) */
+#define KSB_POT_GAUSSIAN 1 /* params (depth, width, x, y, z) per center; -sum d exp(-|x-c|^2/(2 w^2)) */
+
+/* values(mat) = c_s*S + c_m*M + c_p*M_{pot} + c_w*M_{w}, each term assembled by the
+ * 11-point Keast rule (proj/src/assembly.cpp:109-131) and combined slot-wise.
+ * pot may be NULL (c_p ignored); d_w (nodal weight, length n, device) may be NULL. */
+int ksb_mat_assemble(ksb_level* l, int mat, double c_s, double c_m, int pot_kind, int n_centers,
+                     const double* h_pot_params, double c_p, const double* d_w, double c_w);
+/* values(dst) = a*values(x) + b*values(y) */
+int ksb_mat_axpby(ksb_level* l, int dst, double a, int x, double b, int y);
+/* host copies of values: part 0 = ii (nnz_ii), part 1 = ib (nnz_ib) */
+int ksb_mat_values(ksb_level* l, int mat, int part, double* h_dst);
+
+/* Y = A_ii X on interior blocks (ni x N, row-major, ld >= N). replaces A_ii_ * p
+ * (proj/src/solver.cpp:72) -- the K-SpMM kernel */
+int ksb_spmm(ksb_level* l, int mat, const double* d_X, int N, int ldx, double* d_Y, int ldy);
+
+/* ---------------- multi-RHS conjugate gradients ----------------
+ * N independent preconditioned CG recurrences sharing one SpMM per iteration.
+ * Per column: x0 = 0, zero-rhs exit, breakdown on !(pAp > 0), convergence on the
+ * recursive residual confirmed by the true residual (else restart), as
+ * EllipticSolver::pcg (proj/src/solver.cpp:57-111). Operator of column j is
+ * A + sigma_j * B (B = shift_mat, may be -1 when no shifts). */
+typedef struct {
+    double tol;            /* relative residual (SolverOptions::tol, default 1e-9) */
+    int max_iterations;    /* SolverOptions::max_iterations (default 20000) */
+    int fixed_iterations;  /* >0: run exactly this many iterations, no stopping test (benchmark) */
+    int precond;           /* 0 = Jacobi (default) */
+    int check_every;       /* host polls convergence flags every k iterations (default 8) */
+} ksb_cg_opts;
+
+typedef struct {
+    int iterations;
+    double relative_residual;
+    int converged;
+    int breakdown;
+} ksb_cg_stats;
+
+int ksb_cg_defaults(ksb_cg_opts* o);
+/* d_B, d_X: interior blocks ni x N (ld). h_sigma: N shifts or NULL. stats: N entries (host). */
+int ksb_cg_solve(ksb_level* l, int mat, int shift_mat, const double* h_sigma, const double* d_B,
+                 double* d_X, int N, int ld, const ksb_cg_opts* o, ksb_cg_stats* h_stats);
+/* same with host buffers (H2D of B and D2H of X inside the call): the e2e entry point */
+int ksb_cg_solve_host(ksb_level* l, int mat, int shift_mat, const double* h_sigma, const double* h_B,
+                      double* h_X, int N, int ld, const ksb_cg_opts* o, ksb_cg_stats* h_stats);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KSB_H */

@@ -1,0 +1,299 @@
+// CPU ORACLE -- TEST INFRASTRUCTURE ONLY.
+//
+// Clean-room, Eigen-free restatement of the reference implementation's hot path
+// (/root/reference/proj, "ksafem"), used as the parity checker and as the CPU
+// baseline. Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+// reference legs may load it. The product (paper_2103_02824_b200) never does.
+//
+// Parity pin: the reference cannot be compiled here (Eigen3, doctest and CLI11 are
+// absent, no network). The reference ships no golden vectors.
+// This oracle is therefore pinned by restated versions of the reference's own
+// known-answer / identity tests (tests/test_oracle_pins.py, citing
+// proj/tests/*.cpp line by line), not by reference outputs.
+//
+// Each function cites the reference file:line whose semantics it follows.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace orc {
+
+struct OrcError : std::runtime_error {
+    int code;
+    OrcError(int c, const std::string& w) : std::runtime_error(w), code(c) {}
+};
+[[noreturn]] void fail(int code, const std::string& what);
+
+enum { E_NONCONV = 1, E_MISMATCH = 2, E_SINGULAR = 3, E_AMBIG = 4, E_INTERNAL = 5, E_ARG = 6, E_DOMAIN = 7, E_HIER = 8 };
+
+using Vec = std::vector<double>;
+struct V3 {
+    double x[3];
+    double& operator[](int i) { return x[i]; }
+    double operator[](int i) const { return x[i]; }
+};
+
+// ------------------------------------------------------------------ mesh (proj/src/mesh.cpp)
+struct Mesh {
+    std::vector<V3> verts;
+    std::vector<std::array<int, 4>> tets, tuple;
+    std::vector<int8_t> tag;
+    std::vector<int> parent;
+    std::vector<std::array<int, 2>> vparent;
+    int n_parent_vertices = 0, level = 0;
+    V3 lo{{-1, -1, -1}}, hi{{1, 1, 1}};
+    std::vector<std::array<int, 3>> bfaces, ifaces;
+    std::vector<std::array<int, 2>> iface_tets;
+    std::vector<char> on_boundary;
+    mutable unsigned long long quad_cells = 0;  // QuadCounter (proj/include/ksafem/mesh.hpp:25-32)
+
+    int nv() const { return int(verts.size()); }
+    int nt() const { return int(tets.size()); }
+    double tet_volume(int t) const;  // signed
+    void finalize();
+    bool conforming(std::string* why) const;
+};
+using MeshP = std::shared_ptr<const Mesh>;
+MeshP box_mesh(const V3& lo, const V3& hi, int n);
+MeshP uniform_refine(const Mesh& m);
+MeshP adapt_refine(const Mesh& m, std::vector<int> marked);
+
+// ------------------------------------------------------------------ sparse (Eigen SparseMatrix semantics)
+struct Trip {
+    int r, c;
+    double v;
+};
+/// column-major compressed matrix; setFromTriplets sums duplicates in insertion order
+struct Csc {
+    int rows = 0, cols = 0;
+    std::vector<int> ptr, idx;
+    Vec val;
+    static Csc from_triplets(int rows, int cols, const std::vector<Trip>& t);
+    double coeff(int r, int c) const;
+    Vec mul(const Vec& x) const;  // y = A x, column sweep
+    Csc transpose() const;
+    int64_t nnz() const { return ptr.empty() ? 0 : ptr.back(); }
+};
+Csc add(const Csc& a, double s, const Csc& b);  // a + s*b
+Csc scale(const Csc& a, double s);
+Csc matmul(const Csc& a, const Csc& b);
+double dot(const Vec& a, const Vec& b);
+double norm2(const Vec& a);
+
+// ------------------------------------------------------------------ FE space + hierarchy (proj/src/fespace.cpp)
+struct Space {
+    MeshP mesh;
+    std::vector<int> interior, boundary, iidx;
+    explicit Space(MeshP m);
+    int n() const { return mesh->nv(); }
+    int ni() const { return int(interior.size()); }
+};
+using SpaceP = std::shared_ptr<const Space>;
+Csc prolongation_step(const Mesh& fine);
+struct Hier {
+    std::vector<SpaceP> spaces;
+    std::vector<Csc> steps;
+    void push(MeshP m);
+    Csc prolongation(int from, int to) const;
+    Vec prolong(const Vec& c, int from, int to) const;
+};
+
+// ------------------------------------------------------------------ quadrature (proj/src/quadrature.cpp)
+struct QP {
+    double b[4];
+    double w;
+};
+const std::vector<QP>& keast();
+
+// ------------------------------------------------------------------ assembly (proj/src/assembly.cpp)
+struct Geo {
+    V3 x[4];
+    double g[4][3];
+    double vol;
+};
+Geo tet_geo(const Mesh& m, int t);
+Csc assemble_stiffness(const Space& V);
+Csc assemble_mass(const Space& V);
+Csc assemble_mass_nodal(const Space& V, const Vec& w);
+struct Potential {
+    int kind = 0;  // 0 coulomb (Z,x,y,z), 1 gaussian (d,w,x,y,z)
+    std::vector<double> p;
+    double operator()(const V3& x) const;
+};
+Csc assemble_mass_pot(const Space& V, const Potential& pot);
+Vec load_nodal(const Space& V, const Vec& f);
+double l2_norm(const Space& V, const Vec& f);
+double h1_seminorm(const Space& V, const Vec& f);
+double h1_norm(const Space& V, const Vec& f);
+Csc interior_block(const Csc& A, const Space& V);
+
+// ------------------------------------------------------------------ solver (proj/src/solver.cpp)
+struct SolveStats {
+    int iterations = 0;
+    double relres = 0;
+    bool converged = false, breakdown = false;
+};
+struct Elliptic {
+    SpaceP V;
+    Csc Aii, Aib;
+    Vec diag;
+    double min_diag = 0;
+    int precond = 0;  // 0 = SGS (reference), 1 = Jacobi (the GPU path's choice)
+    Elliptic(const Csc& A, SpaceP V, int precond = 0);
+    Vec apply_prec(const Vec& r) const;
+    Vec pcg(const Vec& rhs, double tol, int maxit, SolveStats* st, int fixed_iterations = 0) const;
+    Vec solve(const Vec& b, const Vec& bc, double tol, SolveStats* st) const;
+};
+
+// ------------------------------------------------------------------ physics (proj/src/ks_model.cpp, hartree.cpp)
+struct System {
+    std::vector<double> atoms;  // (Z, x, y, z) per nucleus
+    int n_pairs = 1;
+    double occ = 2.0;
+    int xc_kind = 2;  // 0 none, 1 x-alpha, 2 lda pz81
+    double alpha = 0.77298, p_exch = 1.0 / 3.0;
+    bool hartree_on = true, xc_on = true;
+};
+double v_ext(const System& s, const V3& x);
+Vec density(const std::vector<Vec>& orb, double occ);
+double xc_energy_density(const System& s, double rho);
+double xc_potential(const System& s, double rho);
+Vec xc_field(const System& s, const Vec& rho);
+struct Energy {
+    double kinetic = 0, external = 0, hartree = 0, xc = 0, total = 0;
+};
+Energy total_energy(const System& s, const Space& V, const std::vector<Vec>& orb, const Vec& w);
+struct Moments {
+    double q = 0;
+    V3 c{{0, 0, 0}}, dip{{0, 0, 0}};
+    double Q[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+};
+Moments compute_moments(const Space& V, const Vec& rho);
+double multipole(const Moments& m, const V3& x);
+Vec boundary_values(const Moments& m, const Space& V);
+Vec squared_density_load(const Space& V, const std::vector<Vec>& orb, double occ);
+Vec solve_hartree_exact(const Elliptic& S, const Space& V, const std::vector<Vec>& orb, double occ, const Vec& bc,
+                        double tol);
+
+// ------------------------------------------------------------------ dense linear algebra
+struct Dense {
+    int n = 0, m = 0;  // rows, cols (column-major)
+    Vec a;
+    Dense() = default;
+    Dense(int r, int c) : n(r), m(c), a(size_t(r) * c, 0.0) {}
+    double& operator()(int i, int j) { return a[size_t(j) * n + i]; }
+    double operator()(int i, int j) const { return a[size_t(j) * n + i]; }
+};
+Dense dense_of(const Csc& A);
+bool cholesky(Dense& A);  // in place lower; false if not PD
+/// generalized symmetric-definite eigenproblem A x = l B x: ascending, B-orthonormal columns
+bool gen_eig(const Dense& A, const Dense& B, Vec& vals, Dense& vecs);
+void normalize_sign(Dense& V);
+
+struct Bordered {
+    const Dense* A = nullptr;
+    const Dense* M = nullptr;
+    Vec b, c;
+    double beta = 0, gamma = 0;
+};
+struct BorderedResult {
+    double lambda = 0, theta = 0, score = 0;
+    Vec phi;
+    int scanned = 0;
+};
+BorderedResult solve_bordered(const Bordered& s, int nev_scan, double score_floor);
+
+// ------------------------------------------------------------------ correction (proj/src/correction.cpp)
+struct LevelOps {
+    SpaceP V;
+    Csc S, M, a_op;
+    std::unique_ptr<Elliptic> stiff;
+    Csc P_full;
+};
+struct ShiftLog {
+    std::vector<int> attempt;  // per orbital: -1 unshifted, k = ladder rung
+    std::vector<int> iterations;
+};
+struct Outer {
+    SpaceP V;
+    const Csc* M;
+    Csc H;
+    std::unique_ptr<Elliptic> solver;
+    double tol;
+    int precond;
+    std::vector<std::unique_ptr<Elliptic>> shifted;
+    std::vector<double> sigmas;
+    Outer(SpaceP V, const Csc& a_op, const Csc* M, const Vec& w_hat, const Vec& v_xc, double tol, int precond);
+    Vec solve_orbital(double lambda, const Vec& phi, int* attempt, int* iters);
+};
+struct Blocks {
+    SpaceP VH, Vh;
+    Csc P_int;
+    int n = 0;
+    double occ = 2;
+    bool hartree_on = true;
+    Dense A_H1, A_H3, A_H4, M_H, C_H;
+    Vec d_Hh, lift_load;
+    double zeta = 0, lift_load0 = 0;
+    std::vector<Dense> A_h4;
+    std::vector<Vec> b_H1, b_H3, b_H4, rhs, c_Hh, d_phi, phi_tilde;
+    Vec beta1, beta3, beta4, gamma, zeta_phi;
+    Vec w_tilde0, ell;
+    Dense CH_chol;
+    Vec hartree_u;
+    double hartree_schur = 0;
+    const Mesh* fine_mesh = nullptr;
+};
+Blocks prepare_blocks(SpaceP VH, SpaceP Vh, const Csc& P_full, const Csc& S_f, const Csc& M_f, const Csc& a_f,
+                      const std::vector<Vec>& phi_tilde, const Vec& w_tilde, const Vec& v_xc, double occ,
+                      bool hartree_on, const Vec& bc);
+struct AState {
+    Vec lambda, theta2, w_H;
+    std::vector<Vec> phi_H;
+    double theta1 = 0;
+};
+AState pure_state(const Blocks& B, const Vec& lambda);
+Dense assemble_A_H2(const Blocks& B, const Vec& w_H);
+Vec assemble_f_H(const Blocks& B, const AState& s);
+double assemble_g(const Blocks& B, const AState& s);
+struct InnerResult {
+    AState state;
+    int iterations = 0;
+    std::vector<double> history;
+};
+InnerResult inner_scf(const Blocks& B, const AState& init, double tol, int max_it, double score_floor, int pad);
+void expand(const AState& s, const Blocks& B, std::vector<Vec>& orb, Vec& w);
+
+// ------------------------------------------------------------------ driver pieces (proj/src/driver.cpp, scf.cpp)
+LevelOps make_level_ops(const Hier& h, int level, const System& s);
+struct ScfResult {
+    Vec lambdas;
+    std::vector<Vec> orbitals;
+    Vec hartree, rho;
+    int iterations = 0;
+};
+ScfResult self_consistent_solve(const System& s, SpaceP V, double tol, int max_it, double mixing, double tol_eig);
+
+struct StepConfig {
+    double tol_linear = 1e-9, tol_inner = 1e-8, score_floor = 1e-8;
+    int max_inner = 400, nev_pad = 4;
+    int precond = 0;  // linear-solve preconditioner used by the oracle (0 SGS = reference)
+};
+struct StepLog {
+    ShiftLog shifts;
+    int hartree_iterations = 0;
+    int inner_iterations = 0;
+    double delta = 0;
+    double t_bvp = 0, t_hartree = 0, t_blocks = 0, t_inner = 0, t_total = 0;
+    int64_t cg_iterations = 0;  // summed over orbitals and attempts
+};
+/// one outer iteration of solve_level_corrected (proj/src/driver.cpp:106-150)
+void correction_step(const System& s, const Hier& h, const LevelOps& ops, const StepConfig& cfg, Vec& lambdas,
+                     std::vector<Vec>& orbitals, Vec& w, StepLog* log);
+
+} // namespace orc

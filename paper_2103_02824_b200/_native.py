@@ -1,0 +1,103 @@
+"""ctypes binding of libksb.so (the C-ABI declared in include/ksb.h).
+
+The product path has no CPU fallback: if the in-tree library is missing this
+module raises at import time, and every compute entry point runs on the GPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+_HERE = Path(__file__).resolve().parent
+LIB_PATH = _HERE / "_lib" / "libksb.so"
+
+if not LIB_PATH.exists():
+    raise ImportError(
+        f"libksb.so not found at {LIB_PATH}; build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+        " (there is no CPU fallback for the product path)")
+
+lib = C.CDLL(str(LIB_PATH), mode=os.RTLD_GLOBAL if hasattr(os, "RTLD_GLOBAL") else 0)
+
+P = C.c_void_p
+PP = C.POINTER(C.c_void_p)
+I = C.c_int
+I64 = C.c_int64
+D = C.c_double
+DP = C.POINTER(C.c_double)
+IP = C.POINTER(C.c_int32)
+I64P = C.POINTER(C.c_int64)
+CP = C.c_char_p
+
+
+class CgOpts(C.Structure):
+    _fields_ = [("tol", D), ("max_iterations", I), ("fixed_iterations", I), ("precond", I), ("check_every", I)]
+
+
+class CgStats(C.Structure):
+    _fields_ = [("iterations", I), ("relative_residual", D), ("converged", I), ("breakdown", I)]
+
+
+# name -> (restype, argtypes); mirrors include/ksb.h exactly (checked by tests/test_abi.py)
+PROTOTYPES = {
+    "ksb_last_error": (CP, []),
+    "ksb_code_name": (CP, [I]),
+    "ksb_version": (I, []),
+    "ksb_mesh_box": (I, [DP, DP, I, PP]),
+    "ksb_mesh_uniform_refine": (I, [P, PP]),
+    "ksb_mesh_adapt_refine": (I, [P, IP, I64, PP]),
+    "ksb_mesh_free": (None, [P]),
+    "ksb_mesh_sizes": (I, [P, I64P]),
+    "ksb_mesh_get": (I, [P, I, P]),
+    "ksb_hier_create": (I, [PP]),
+    "ksb_hier_push": (I, [P, P]),
+    "ksb_hier_free": (None, [P]),
+    "ksb_hier_levels": (I, [P]),
+    "ksb_hier_prolongation": (I, [P, I, IP, DP]),
+    "ksb_ctx_create": (I, [I, PP]),
+    "ksb_ctx_destroy": (None, [P]),
+    "ksb_ctx_stream": (I, [P, PP]),
+    "ksb_ctx_sync": (I, [P]),
+    "ksb_ctx_set_profiling": (I, [P, I]),
+    "ksb_ctx_kernel_time": (I, [P, CP, DP, I64P]),
+    "ksb_ctx_kernel_launches": (I, [P, I64P]),
+    "ksb_ctx_reset_counters": (I, [P]),
+    "ksb_malloc": (I, [P, PP, I64]),
+    "ksb_free": (I, [P, P]),
+    "ksb_memcpy_h2d": (I, [P, P, P, I64]),
+    "ksb_memcpy_d2h": (I, [P, P, P, I64]),
+    "ksb_level_create": (I, [P, P, I, PP]),
+    "ksb_level_destroy": (None, [P]),
+    "ksb_level_sizes": (I, [P, I64P]),
+    "ksb_level_index": (I, [P, I, P]),
+    "ksb_mat_assemble": (I, [P, I, D, D, I, I, DP, D, P, D]),
+    "ksb_mat_axpby": (I, [P, I, D, I, D, I]),
+    "ksb_mat_values": (I, [P, I, I, DP]),
+    "ksb_spmm": (I, [P, I, P, I, I, P, I]),
+    "ksb_cg_defaults": (I, [C.POINTER(CgOpts)]),
+    "ksb_cg_solve": (I, [P, I, I, DP, P, P, I, I, C.POINTER(CgOpts), C.POINTER(CgStats)]),
+    "ksb_cg_solve_host": (I, [P, I, I, DP, P, P, I, I, C.POINTER(CgOpts), C.POINTER(CgStats)]),
+}
+
+for _name, (_res, _args) in PROTOTYPES.items():
+    _f = getattr(lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+CODE_NAMES = {0: "ok", 1: "nonconvergence", 2: "mismatched-spaces", 3: "singular-quadrature",
+              4: "ambiguous-selection", 5: "internal", 6: "invalid-argument", 7: "invalid-domain",
+              8: "hierarchy", 9: "io", 10: "cuda"}
+
+
+class KsbError(RuntimeError):
+    """Mirror of ksafem::Error: `code` is the reference's machine code string."""
+
+    def __init__(self, status: int, message: str):
+        self.status = status
+        self.code = CODE_NAMES.get(status, "unknown")
+        super().__init__(message)
+
+
+def check(status: int) -> None:
+    if status != 0:
+        raise KsbError(status, lib.ksb_last_error().decode())

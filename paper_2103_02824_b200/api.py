@@ -1,0 +1,307 @@
+"""Python face of the B200 correction-step library.
+
+Mirrors the reference's C++ namespace API for the hot path (names and argument
+meaning follow /root/reference/proj/include/ksafem/*.hpp) on top of the C-ABI in
+include/ksb.h. Host arrays are numpy; device arrays are `DeviceArray`s owned by
+a `Context`.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from ._native import check, lib
+
+MAT_S, MAT_M, MAT_AOP, MAT_USER0 = 0, 1, 2, 8
+POT_COULOMB, POT_GAUSSIAN = 0, 1
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(N.DP)
+
+
+def _ip(a: np.ndarray):
+    return a.ctypes.data_as(N.IP)
+
+
+# ----------------------------------------------------------------------------- mesh
+class Mesh:
+    """Host tetrahedral mesh (reference mesh::TetMesh, proj/include/ksafem/mesh.hpp:43-87)."""
+
+    _ARR = {  # what -> (dtype, columns, size index)
+        "xyz": (0, np.float64, 3, 0), "tets": (1, np.int32, 4, 1), "tuple": (2, np.int32, 4, 1),
+        "tag": (3, np.int8, 1, 1), "parent": (4, np.int32, 1, 1), "vparent": (5, np.int32, 2, 0),
+        "on_boundary": (6, np.uint8, 1, 0), "boundary_faces": (7, np.int32, 3, 2),
+        "interior_faces": (8, np.int32, 3, 3), "interior_face_tets": (9, np.int32, 2, 3),
+        "interior_face_geom": (10, np.float64, 5, 3),
+    }
+
+    def __init__(self, handle):
+        self._h = handle
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.ksb_mesh_free(self._h)
+            self._h = None
+
+    @staticmethod
+    def box(lo, hi, n: int) -> "Mesh":
+        """build_box_mesh (proj/src/mesh.cpp:281-331)."""
+        lo = np.ascontiguousarray(lo, np.float64)
+        hi = np.ascontiguousarray(hi, np.float64)
+        h = C.c_void_p()
+        check(lib.ksb_mesh_box(_dp(lo), _dp(hi), int(n), C.byref(h)))
+        return Mesh(h)
+
+    def uniform_refine(self) -> "Mesh":
+        """uniform_refine (proj/src/mesh.cpp:333-343)."""
+        h = C.c_void_p()
+        check(lib.ksb_mesh_uniform_refine(self._h, C.byref(h)))
+        return Mesh(h)
+
+    def adapt_refine(self, marked) -> "Mesh":
+        """adapt_refine (proj/src/mesh.cpp:345-368)."""
+        m = np.ascontiguousarray(marked, np.int32)
+        h = C.c_void_p()
+        check(lib.ksb_mesh_adapt_refine(self._h, _ip(m), len(m), C.byref(h)))
+        return Mesh(h)
+
+    def sizes(self):
+        s = (C.c_int64 * 8)()
+        check(lib.ksb_mesh_sizes(self._h, s))
+        return list(s)
+
+    @property
+    def n_vertices(self):
+        return self.sizes()[0]
+
+    @property
+    def n_tets(self):
+        return self.sizes()[1]
+
+    @property
+    def level(self):
+        return self.sizes()[4]
+
+    def array(self, name: str) -> np.ndarray:
+        what, dt, cols, si = self._ARR[name]
+        rows = self.sizes()[si]
+        out = np.empty((rows, cols) if cols > 1 else (rows,), dt)
+        check(lib.ksb_mesh_get(self._h, what, out.ctypes.data_as(C.c_void_p)))
+        return out
+
+
+class Hierarchy:
+    """fem::SpaceHierarchy (proj/include/ksafem/fespace.hpp:65-81)."""
+
+    def __init__(self):
+        h = C.c_void_p()
+        check(lib.ksb_hier_create(C.byref(h)))
+        self._h = h
+        self.meshes = []
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.ksb_hier_free(self._h)
+            self._h = None
+
+    def push(self, m: Mesh) -> None:
+        check(lib.ksb_hier_push(self._h, m._h))
+        self.meshes.append(m)
+
+    @property
+    def n_levels(self):
+        return lib.ksb_hier_levels(self._h)
+
+    def prolongation(self, level: int):
+        n = self.meshes[level].n_vertices
+        col = np.empty((n, 4), np.int32)
+        val = np.empty((n, 4), np.float64)
+        check(lib.ksb_hier_prolongation(self._h, level, _ip(col), _dp(val)))
+        return col, val
+
+
+# ----------------------------------------------------------------------------- device
+class Context:
+    """One device, one stream (include/ksb.h ksb_ctx)."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        check(lib.ksb_ctx_create(int(device), C.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.ksb_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    @property
+    def stream(self) -> int:
+        s = C.c_void_p()
+        check(lib.ksb_ctx_stream(self._h, C.byref(s)))
+        return s.value or 0
+
+    def sync(self):
+        check(lib.ksb_ctx_sync(self._h))
+
+    def set_profiling(self, on: bool):
+        check(lib.ksb_ctx_set_profiling(self._h, int(bool(on))))
+
+    def kernel_time(self, name: str):
+        ms = C.c_double()
+        cnt = C.c_int64()
+        check(lib.ksb_ctx_kernel_time(self._h, name.encode(), C.byref(ms), C.byref(cnt)))
+        return ms.value, cnt.value
+
+    def launches(self) -> int:
+        n = C.c_int64()
+        check(lib.ksb_ctx_kernel_launches(self._h, C.byref(n)))
+        return n.value
+
+    def reset_counters(self):
+        check(lib.ksb_ctx_reset_counters(self._h))
+
+    def empty(self, shape, dtype=np.float64) -> "DeviceArray":
+        return DeviceArray(self, shape, dtype)
+
+    def to_device(self, a: np.ndarray) -> "DeviceArray":
+        d = DeviceArray(self, a.shape, a.dtype)
+        d.upload(a)
+        return d
+
+
+class DeviceArray:
+    def __init__(self, ctx: Context, shape, dtype=np.float64):
+        self.ctx = ctx
+        self.shape = tuple(int(s) for s in (shape if isinstance(shape, (tuple, list)) else (shape,)))
+        self.dtype = np.dtype(dtype)
+        self.nbytes = int(np.prod(self.shape)) * self.dtype.itemsize
+        p = C.c_void_p()
+        check(lib.ksb_malloc(ctx._h, C.byref(p), self.nbytes))
+        self.ptr = p
+
+    def __del__(self):
+        if getattr(self, "ptr", None) and getattr(self.ctx, "_h", None):
+            lib.ksb_free(self.ctx._h, self.ptr)
+            self.ptr = None
+
+    def upload(self, a: np.ndarray):
+        a = np.ascontiguousarray(a, self.dtype)
+        assert a.nbytes == self.nbytes
+        check(lib.ksb_memcpy_h2d(self.ctx._h, self.ptr, a.ctypes.data_as(C.c_void_p), self.nbytes))
+        self.ctx.sync()
+
+    def download(self) -> np.ndarray:
+        out = np.empty(self.shape, self.dtype)
+        check(lib.ksb_memcpy_d2h(self.ctx._h, out.ctypes.data_as(C.c_void_p), self.ptr, self.nbytes))
+        self.ctx.sync()
+        return out
+
+
+@dataclass
+class SolveStats:
+    """fem::SolveStats (proj/include/ksafem/solver.hpp:10-15)."""
+    iterations: int
+    relative_residual: float
+    converged: bool
+    breakdown: bool
+
+
+class Level:
+    """Device-resident fine level: FE space split, interior patterns, operators."""
+
+    def __init__(self, ctx: Context, hier: Hierarchy, level: int):
+        h = C.c_void_p()
+        check(lib.ksb_level_create(ctx._h, hier._h, int(level), C.byref(h)))
+        self._h = h
+        self.ctx = ctx
+        s = (C.c_int64 * 10)()
+        check(lib.ksb_level_sizes(self._h, s))
+        (self.n, self.ni, self.nb, self.nt, self.nnz_ii, self.nnz_ib, self.nH, self.nct, self.ncv, _) = list(s)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.ksb_level_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def index(self, what: str) -> np.ndarray:
+        spec = {"ii_ptr": (0, np.int32, self.ni + 1), "ii_col": (1, np.int32, self.nnz_ii),
+                "ib_ptr": (2, np.int32, self.ni + 1), "ib_col": (3, np.int32, self.nnz_ib),
+                "interior": (4, np.int32, self.ni), "pint_col": (5, np.int32, self.ni * 4),
+                "pint_val": (6, np.float64, self.ni * 4)}[what]
+        out = np.empty(spec[2], spec[1])
+        check(lib.ksb_level_index(self._h, spec[0], out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def assemble(self, mat: int, c_s=0.0, c_m=0.0, potential=None, c_p=1.0, w: DeviceArray | None = None, c_w=1.0):
+        """values(mat) = c_s S + c_m M + c_p M_pot + c_w M_w (Keast rule, proj/src/assembly.cpp:109-131).
+
+        potential: (kind, params[n_centers, 4 or 5]) or None.
+        """
+        if potential is not None:
+            kind, params = potential
+            params = np.ascontiguousarray(params, np.float64)
+            nc = params.shape[0]
+            pp = _dp(params.reshape(-1))
+        else:
+            kind, nc, pp = 0, 0, None
+        check(lib.ksb_mat_assemble(self._h, int(mat), float(c_s), float(c_m), int(kind), int(nc), pp,
+                                   float(c_p), w.ptr if w is not None else None, float(c_w)))
+
+    def axpby(self, dst: int, a: float, x: int, b: float, y: int):
+        check(lib.ksb_mat_axpby(self._h, dst, float(a), x, float(b), y))
+
+    def values(self, mat: int, part: int = 0) -> np.ndarray:
+        out = np.empty(self.nnz_ii if part == 0 else self.nnz_ib, np.float64)
+        check(lib.ksb_mat_values(self._h, mat, part, _dp(out)))
+        return out
+
+    def spmm(self, mat: int, X: DeviceArray, Y: DeviceArray, N: int, ldx: int | None = None, ldy: int | None = None):
+        check(lib.ksb_spmm(self._h, mat, X.ptr, int(N), int(ldx or N), Y.ptr, int(ldy or N)))
+
+    @staticmethod
+    def cg_options(tol=1e-9, max_iterations=20000, fixed_iterations=0, check_every=8) -> N.CgOpts:
+        o = N.CgOpts()
+        check(lib.ksb_cg_defaults(C.byref(o)))
+        o.tol = tol
+        o.max_iterations = max_iterations
+        o.fixed_iterations = fixed_iterations
+        o.check_every = check_every
+        return o
+
+    def cg_solve(self, mat: int, B: DeviceArray, X: DeviceArray, N: int, ld: int | None = None, opts=None,
+                 shift_mat: int = -1, sigma=None):
+        """Multi-RHS PCG on interior blocks; returns per-column SolveStats."""
+        opts = opts or self.cg_options()
+        st = (N.CgStats * N_cols(N))()
+        sig = np.ascontiguousarray(sigma, np.float64) if sigma is not None else None
+        check(lib.ksb_cg_solve(self._h, mat, shift_mat, _dp(sig) if sig is not None else None, B.ptr, X.ptr,
+                               int(N), int(ld or N), C.byref(opts), st))
+        return [SolveStats(s.iterations, s.relative_residual, bool(s.converged), bool(s.breakdown)) for s in st]
+
+    def cg_solve_host(self, mat: int, B: np.ndarray, N: int, ld: int | None = None, opts=None, shift_mat=-1,
+                      sigma=None, out: np.ndarray | None = None):
+        """Same as cg_solve with host buffers (H2D + D2H inside the call)."""
+        opts = opts or self.cg_options()
+        ld = int(ld or N)
+        B = np.ascontiguousarray(B, np.float64)
+        X = out if out is not None else np.empty_like(B)
+        st = (N.CgStats * N_cols(N))()
+        sig = np.ascontiguousarray(sigma, np.float64) if sigma is not None else None
+        check(lib.ksb_cg_solve_host(self._h, mat, shift_mat, _dp(sig) if sig is not None else None,
+                                    B.ctypes.data_as(C.c_void_p), X.ctypes.data_as(C.c_void_p), int(N), ld,
+                                    C.byref(opts), st))
+        return X, [SolveStats(s.iterations, s.relative_residual, bool(s.converged), bool(s.breakdown)) for s in st]
+
+
+def N_cols(n: int) -> int:
+    return max(1, int(n))

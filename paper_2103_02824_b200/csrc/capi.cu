@@ -1,0 +1,516 @@
+// C-ABI implementation (include/ksb.h). No exceptions cross this boundary.
+#include <cstring>
+#include <exception>
+#include <new>
+
+#include "device/cg.cuh"
+#include "device/level.cuh"
+#include "ksb.h"
+
+struct ksb_mesh {
+    ksb::MeshPtr m;
+};
+struct ksb_hier {
+    ksb::Hierarchy h;
+};
+struct ksb_ctx {
+    ksb::Ctx c;
+    ksb::CgWork cg;
+    ksb::DevBuf<double> io_b, io_x;  // staging for the host-buffer entry points
+};
+struct ksb_level {
+    ksb_ctx* owner = nullptr;
+    ksb::Level L;
+};
+
+namespace ksb {
+
+void axpby_values(Level& L, int dst, double a, int x, double b, int y);
+
+cudaEvent_t Ctx::take_event() {
+    if (!event_pool.empty()) {
+        cudaEvent_t e = event_pool.back();
+        event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    KSB_CUDA_CHECK(cudaEventCreate(&e));
+    return e;
+}
+
+void Ctx::begin(const char*, cudaEvent_t* e0) {
+    *e0 = take_event();
+    KSB_CUDA_CHECK(cudaEventRecord(*e0, stream));
+}
+
+void Ctx::end(const char* name, cudaEvent_t e0) {
+    cudaEvent_t e1 = take_event();
+    KSB_CUDA_CHECK(cudaEventRecord(e1, stream));
+    pending.push_back({name, {e0, e1}});
+    if (pending.size() > 4096) harvest();
+}
+
+void Ctx::harvest() {
+    if (pending.empty()) return;
+    KSB_CUDA_CHECK(cudaStreamSynchronize(stream));
+    for (auto& p : pending) {
+        float ms = 0.f;
+        KSB_CUDA_CHECK(cudaEventElapsedTime(&ms, p.second.first, p.second.second));
+        auto& t = timers[p.first];
+        t.ms += ms;
+        t.count += 1;
+        event_pool.push_back(p.second.first);
+        event_pool.push_back(p.second.second);
+    }
+    pending.clear();
+}
+
+} // namespace ksb
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <typename F>
+int guard(F&& f) {
+    try {
+        f();
+        return KSB_OK;
+    } catch (const ksb::Failure& e) {
+        g_last_error = std::string(ksb_code_name(e.code)) + ": " + e.what;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "internal: host allocation failed";
+        return KSB_INTERNAL;
+    } catch (const std::exception& e) {
+        g_last_error = std::string("internal: ") + e.what();
+        return KSB_INTERNAL;
+    }
+}
+
+void need(bool ok, const char* what) {
+    if (!ok) ksb::raise(KSB_INVALID_ARGUMENT, what);
+}
+
+} // namespace
+
+extern "C" {
+
+const char* ksb_last_error(void) { return g_last_error.c_str(); }
+
+const char* ksb_code_name(int code) {
+    switch (code) {
+        case KSB_OK: return "ok";
+        case KSB_NONCONVERGENCE: return "nonconvergence";
+        case KSB_MISMATCHED_SPACES: return "mismatched-spaces";
+        case KSB_SINGULAR_QUADRATURE: return "singular-quadrature";
+        case KSB_AMBIGUOUS_SELECTION: return "ambiguous-selection";
+        case KSB_INTERNAL: return "internal";
+        case KSB_INVALID_ARGUMENT: return "invalid-argument";
+        case KSB_INVALID_DOMAIN: return "invalid-domain";
+        case KSB_HIERARCHY: return "hierarchy";
+        case KSB_IO: return "io";
+        case KSB_CUDA: return "cuda";
+        default: return "unknown";
+    }
+}
+
+int ksb_version(void) { return 1; }
+
+// ---------------- mesh ----------------
+int ksb_mesh_box(const double lo[3], const double hi[3], int n, ksb_mesh** out) {
+    return guard([&] {
+        need(out && lo && hi, "null argument");
+        *out = new ksb_mesh{ksb::build_box_mesh(lo, hi, n)};
+    });
+}
+
+int ksb_mesh_uniform_refine(const ksb_mesh* m, ksb_mesh** out) {
+    return guard([&] {
+        need(m && out, "null argument");
+        *out = new ksb_mesh{ksb::uniform_refine(*m->m)};
+    });
+}
+
+int ksb_mesh_adapt_refine(const ksb_mesh* m, const int32_t* marked, int64_t n, ksb_mesh** out) {
+    return guard([&] {
+        need(m && out && (n == 0 || marked), "null argument");
+        *out = new ksb_mesh{ksb::adapt_refine(*m->m, marked, n)};
+    });
+}
+
+void ksb_mesh_free(ksb_mesh* m) { delete m; }
+
+int ksb_mesh_sizes(const ksb_mesh* m, int64_t s[8]) {
+    return guard([&] {
+        need(m && s, "null argument");
+        const auto& M = *m->m;
+        s[0] = M.n_vertices();
+        s[1] = M.n_tets();
+        s[2] = int64_t(M.bface.size() / 3);
+        s[3] = int64_t(M.iface.size() / 3);
+        s[4] = M.level;
+        s[5] = M.n_parent_vertices;
+        s[6] = s[7] = 0;
+    });
+}
+
+int ksb_mesh_get(const ksb_mesh* m, int what, void* dst) {
+    return guard([&] {
+        need(m && dst, "null argument");
+        const auto& M = *m->m;
+        auto put = [&](const auto& v) { std::memcpy(dst, v.data(), v.size() * sizeof(v[0])); };
+        switch (what) {
+            case 0: put(M.xyz); break;
+            case 1: put(M.tets); break;
+            case 2: put(M.tuple); break;
+            case 3: put(M.tag); break;
+            case 4: put(M.parent); break;
+            case 5: put(M.vparent); break;
+            case 6: put(M.on_boundary); break;
+            case 7: put(M.bface); break;
+            case 8: put(M.iface); break;
+            case 9: put(M.iface_tets); break;
+            case 10: put(M.iface_geom); break;
+            default: ksb::raise(KSB_INVALID_ARGUMENT, "unknown mesh array");
+        }
+    });
+}
+
+// ---------------- hierarchy ----------------
+int ksb_hier_create(ksb_hier** out) {
+    return guard([&] {
+        need(out, "null argument");
+        *out = new ksb_hier;
+    });
+}
+
+int ksb_hier_push(ksb_hier* h, const ksb_mesh* m) {
+    return guard([&] {
+        need(h && m, "null argument");
+        h->h.push(m->m);
+    });
+}
+
+void ksb_hier_free(ksb_hier* h) { delete h; }
+
+int ksb_hier_levels(const ksb_hier* h) { return h ? h->h.n_levels() : 0; }
+
+int ksb_hier_prolongation(const ksb_hier* h, int level, int32_t* col, double* val) {
+    return guard([&] {
+        need(h && col && val, "null argument");
+        if (level < 0 || level >= h->h.n_levels()) ksb::raise(KSB_HIERARCHY, "level out of range");
+        const auto& c = h->h.pcol(level);
+        const auto& v = h->h.pval(level);
+        std::memcpy(col, c.data(), c.size() * sizeof(int32_t));
+        std::memcpy(val, v.data(), v.size() * sizeof(double));
+    });
+}
+
+// ---------------- context ----------------
+int ksb_ctx_create(int device, ksb_ctx** out) {
+    return guard([&] {
+        need(out, "null argument");
+        int ndev = 0;
+        KSB_CUDA_CHECK(cudaGetDeviceCount(&ndev));
+        if (device < 0 || device >= ndev) ksb::raise(KSB_CUDA, "no such CUDA device");
+        KSB_CUDA_CHECK(cudaSetDevice(device));
+        auto* c = new ksb_ctx;
+        c->c.device = device;
+        cudaDeviceProp prop;
+        KSB_CUDA_CHECK(cudaGetDeviceProperties(&prop, device));
+        c->c.sm_count = prop.multiProcessorCount;
+        KSB_CUDA_CHECK(cudaStreamCreateWithFlags(&c->c.stream, cudaStreamNonBlocking));
+        *out = c;
+    });
+}
+
+void ksb_ctx_destroy(ksb_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->c.device);
+    cudaStreamSynchronize(c->c.stream);
+    for (auto& p : c->c.pending) {
+        cudaEventDestroy(p.second.first);
+        cudaEventDestroy(p.second.second);
+    }
+    for (auto e : c->c.event_pool) cudaEventDestroy(e);
+    cudaStreamDestroy(c->c.stream);
+    delete c;
+}
+
+int ksb_ctx_stream(ksb_ctx* c, void** s) {
+    return guard([&] {
+        need(c && s, "null argument");
+        *s = reinterpret_cast<void*>(c->c.stream);
+    });
+}
+
+int ksb_ctx_sync(ksb_ctx* c) {
+    return guard([&] {
+        need(c, "null argument");
+        KSB_CUDA_CHECK(cudaStreamSynchronize(c->c.stream));
+    });
+}
+
+int ksb_ctx_set_profiling(ksb_ctx* c, int on) {
+    return guard([&] {
+        need(c, "null argument");
+        c->c.harvest();
+        c->c.profiling = on != 0;
+    });
+}
+
+int ksb_ctx_kernel_time(ksb_ctx* c, const char* name, double* ms, int64_t* count) {
+    return guard([&] {
+        need(c && name && ms && count, "null argument");
+        c->c.harvest();
+        auto it = c->c.timers.find(name);
+        *ms = it == c->c.timers.end() ? 0.0 : it->second.ms;
+        *count = it == c->c.timers.end() ? 0 : it->second.count;
+    });
+}
+
+int ksb_ctx_kernel_launches(ksb_ctx* c, int64_t* total) {
+    return guard([&] {
+        need(c && total, "null argument");
+        *total = c->c.launches;
+    });
+}
+
+int ksb_ctx_reset_counters(ksb_ctx* c) {
+    return guard([&] {
+        need(c, "null argument");
+        c->c.harvest();
+        c->c.timers.clear();
+        c->c.launches = 0;
+    });
+}
+
+int ksb_malloc(ksb_ctx* c, void** p, int64_t bytes) {
+    return guard([&] {
+        need(c && p && bytes >= 0, "bad argument");
+        KSB_CUDA_CHECK(cudaSetDevice(c->c.device));
+        KSB_CUDA_CHECK(cudaMalloc(p, size_t(bytes > 0 ? bytes : 1)));
+    });
+}
+
+int ksb_free(ksb_ctx* c, void* p) {
+    return guard([&] {
+        need(c, "null argument");
+        KSB_CUDA_CHECK(cudaFree(p));
+    });
+}
+
+int ksb_memcpy_h2d(ksb_ctx* c, void* d, const void* h, int64_t bytes) {
+    return guard([&] {
+        need(c && d && h, "null argument");
+        KSB_CUDA_CHECK(cudaMemcpyAsync(d, h, size_t(bytes), cudaMemcpyHostToDevice, c->c.stream));
+    });
+}
+
+int ksb_memcpy_d2h(ksb_ctx* c, void* h, const void* d, int64_t bytes) {
+    return guard([&] {
+        need(c && d && h, "null argument");
+        KSB_CUDA_CHECK(cudaMemcpyAsync(h, d, size_t(bytes), cudaMemcpyDeviceToHost, c->c.stream));
+    });
+}
+
+// ---------------- level ----------------
+int ksb_level_create(ksb_ctx* c, const ksb_hier* h, int level, ksb_level** out) {
+    return guard([&] {
+        need(c && h && out, "null argument");
+        if (level < 0 || level >= h->h.n_levels()) ksb::raise(KSB_HIERARCHY, "level out of range");
+        KSB_CUDA_CHECK(cudaSetDevice(c->c.device));
+        auto* lv = new ksb_level;
+        lv->owner = c;
+        ksb::Level& L = lv->L;
+        L.ctx = &c->c;
+        try {
+            L.topo = ksb::build_topology(h->h, level);
+            const auto& T = *L.topo;
+            const auto& S = *T.space;
+            const auto& M = *S.mesh;
+            L.n = S.n();
+            L.ni = S.ni();
+            L.nb = S.nb();
+            L.nt = M.n_tets();
+            L.nnz_ii = T.ii.nnz();
+            L.nnz_ib = T.ib.nnz();
+            L.nH = T.coarse->ni();
+            L.nct = T.coarse->mesh->n_tets();
+            L.ncv = T.coarse->n();
+            ksb::Ctx& cx = c->c;
+            L.xyz.upload(cx, M.xyz);
+            L.tets.upload(cx, M.tets);
+            L.interior.upload(cx, S.interior);
+            L.boundary.upload(cx, S.boundary);
+            L.iidx.upload(cx, S.iidx);
+            L.ii_ptr.upload(cx, T.ii.ptr);
+            L.ii_col.upload(cx, T.ii.col);
+            L.ib_ptr.upload(cx, T.ib.ptr);
+            L.ib_col.upload(cx, T.ib.col);
+            L.diag_slot.upload(cx, T.diag_slot);
+            L.ii_gptr.upload(cx, T.ii_gptr);
+            L.ii_gent.upload(cx, T.ii_gent);
+            L.ib_gptr.upload(cx, T.ib_gptr);
+            L.ib_gent.upload(cx, T.ib_gent);
+            L.pint_col.upload(cx, T.pint_col);
+            L.pint_val.upload(cx, T.pint_val);
+            L.ancestor.upload(cx, T.ancestor);
+            L.anc_ptr.upload(cx, T.anc_ptr);
+            L.anc_tets.upload(cx, T.anc_tets);
+            L.flag.alloc(4);
+            KSB_CUDA_CHECK(cudaStreamSynchronize(cx.stream));
+        } catch (...) {
+            delete lv;
+            throw;
+        }
+        *out = lv;
+    });
+}
+
+void ksb_level_destroy(ksb_level* l) {
+    if (!l) return;
+    cudaStreamSynchronize(l->L.ctx->stream);
+    delete l;
+}
+
+int ksb_level_sizes(const ksb_level* l, int64_t s[10]) {
+    return guard([&] {
+        need(l && s, "null argument");
+        const auto& L = l->L;
+        s[0] = L.n;
+        s[1] = L.ni;
+        s[2] = L.nb;
+        s[3] = L.nt;
+        s[4] = L.nnz_ii;
+        s[5] = L.nnz_ib;
+        s[6] = L.nH;
+        s[7] = L.nct;
+        s[8] = L.ncv;
+        s[9] = 0;
+    });
+}
+
+int ksb_level_index(const ksb_level* l, int what, void* dst) {
+    return guard([&] {
+        need(l && dst, "null argument");
+        const auto& T = *l->L.topo;
+        auto put = [&](const auto& v) { std::memcpy(dst, v.data(), v.size() * sizeof(v[0])); };
+        switch (what) {
+            case 0: put(T.ii.ptr); break;
+            case 1: put(T.ii.col); break;
+            case 2: put(T.ib.ptr); break;
+            case 3: put(T.ib.col); break;
+            case 4: put(T.space->interior); break;
+            case 5: put(T.pint_col); break;
+            case 6: put(T.pint_val); break;
+            default: ksb::raise(KSB_INVALID_ARGUMENT, "unknown index array");
+        }
+    });
+}
+
+// ---------------- operators ----------------
+int ksb_mat_assemble(ksb_level* l, int mat, double c_s, double c_m, int pot_kind, int n_centers,
+                     const double* pot_params, double c_p, const double* d_w, double c_w) {
+    return guard([&] {
+        need(l, "null argument");
+        ksb::Potential pot;
+        const ksb::Potential* pp = nullptr;
+        if (pot_params && n_centers > 0) {
+            if (pot_kind != KSB_POT_COULOMB && pot_kind != KSB_POT_GAUSSIAN)
+                ksb::raise(KSB_INVALID_ARGUMENT, "unknown potential kind");
+            pot.kind = pot_kind;
+            pot.n = n_centers;
+            const int stride = pot_kind == KSB_POT_COULOMB ? 4 : 5;
+            pot.params.assign(pot_params, pot_params + size_t(stride) * n_centers);
+            pp = &pot;
+        }
+        ksb::assemble_into(l->L, mat, c_s, c_m, pp, c_p, d_w, c_w);
+    });
+}
+
+int ksb_mat_axpby(ksb_level* l, int dst, double a, int x, double b, int y) {
+    return guard([&] {
+        need(l, "null argument");
+        ksb::axpby_values(l->L, dst, a, x, b, y);
+    });
+}
+
+int ksb_mat_values(ksb_level* l, int mat, int part, double* dst) {
+    return guard([&] {
+        need(l && dst, "null argument");
+        auto& L = l->L;
+        if (mat < 0 || mat >= ksb::kMaxMats || !L.mats[mat].valid) ksb::raise(KSB_INVALID_ARGUMENT, "matrix not assembled");
+        const auto& buf = part == 0 ? L.mats[mat].ii : L.mats[mat].ib;
+        KSB_CUDA_CHECK(cudaMemcpyAsync(dst, buf.p, sizeof(double) * size_t(buf.n), cudaMemcpyDeviceToHost, L.ctx->stream));
+        KSB_CUDA_CHECK(cudaStreamSynchronize(L.ctx->stream));
+    });
+}
+
+int ksb_spmm(ksb_level* l, int mat, const double* X, int N, int ldx, double* Y, int ldy) {
+    return guard([&] {
+        need(l && X && Y, "null argument");
+        auto& L = l->L;
+        if (mat < 0 || mat >= ksb::kMaxMats || !L.mats[mat].valid) ksb::raise(KSB_INVALID_ARGUMENT, "matrix not assembled");
+        ksb::spmm(*L.ctx, L, L.mats[mat].ii.p, nullptr, nullptr, X, N, ldx, Y, ldy);
+    });
+}
+
+// ---------------- CG ----------------
+int ksb_cg_defaults(ksb_cg_opts* o) {
+    return guard([&] {
+        need(o, "null argument");
+        o->tol = 1e-9;
+        o->max_iterations = 20000;
+        o->fixed_iterations = 0;
+        o->precond = 0;
+        o->check_every = 8;
+    });
+}
+
+static void run_cg(ksb_level* l, int mat, int shift_mat, const double* h_sigma, const double* d_B, double* d_X, int N,
+                   int ld, const ksb_cg_opts* o, ksb_cg_stats* h_stats) {
+    need(l && d_B && d_X && o, "null argument");
+    if (o->precond != 0) ksb::raise(KSB_INVALID_ARGUMENT, "only the Jacobi preconditioner is available");
+    if (mat < 0 || mat >= ksb::kMaxMats || (shift_mat >= ksb::kMaxMats)) ksb::raise(KSB_INVALID_ARGUMENT, "bad matrix id");
+    ksb::CgOptions co;
+    co.tol = o->tol;
+    co.max_iterations = o->max_iterations;
+    co.fixed_iterations = o->fixed_iterations;
+    co.check_every = o->check_every;
+    std::vector<ksb::CgColumnStats> st(N);
+    ksb::cg_solve(*l->L.ctx, l->L, mat, shift_mat, h_sigma, d_B, d_X, N, ld, co, st.data(), l->owner->cg);
+    if (h_stats)
+        for (int j = 0; j < N; ++j) {
+            h_stats[j].iterations = st[j].iterations;
+            h_stats[j].relative_residual = st[j].relative_residual;
+            h_stats[j].converged = st[j].converged;
+            h_stats[j].breakdown = st[j].breakdown;
+        }
+}
+
+int ksb_cg_solve(ksb_level* l, int mat, int shift_mat, const double* h_sigma, const double* d_B, double* d_X, int N,
+                 int ld, const ksb_cg_opts* o, ksb_cg_stats* h_stats) {
+    return guard([&] { run_cg(l, mat, shift_mat, h_sigma, d_B, d_X, N, ld, o, h_stats); });
+}
+
+int ksb_cg_solve_host(ksb_level* l, int mat, int shift_mat, const double* h_sigma, const double* h_B, double* h_X,
+                      int N, int ld, const ksb_cg_opts* o, ksb_cg_stats* h_stats) {
+    return guard([&] {
+        need(l && h_B && h_X, "null argument");
+        auto& c = *l->L.ctx;
+        const size_t bytes = sizeof(double) * size_t(l->L.ni) * ld;
+        auto& dB = l->owner->io_b;
+        auto& dX = l->owner->io_x;
+        const int64_t cnt = int64_t(l->L.ni) * ld;
+        if (dB.n < cnt) dB.alloc(cnt);
+        if (dX.n < cnt) dX.alloc(cnt);
+        KSB_CUDA_CHECK(cudaMemcpyAsync(dB.p, h_B, bytes, cudaMemcpyHostToDevice, c.stream));
+        run_cg(l, mat, shift_mat, h_sigma, dB.p, dX.p, N, ld, o, h_stats);
+        KSB_CUDA_CHECK(cudaMemcpyAsync(h_X, dX.p, bytes, cudaMemcpyDeviceToHost, c.stream));
+        KSB_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    });
+}
+
+} // extern "C"

@@ -1,0 +1,561 @@
+// Multi-RHS preconditioned conjugate gradients (N independent recurrences, one SpMM per iteration).
+//
+// Per column this is EllipticSolver::pcg (reference proj/src/solver.cpp:57-111):
+//   x0 = 0; zero rhs -> converged with 0 iterations;
+//   breakdown when !(p.Ap > 0) (iterations = it, residual of the current r);
+//   recursive residual <= tol -> true residual b - A x; accept, or restart with p = z;
+// with the reference's SGS preconditioner replaced by Jacobi (fully parallel, fused into
+// the vector updates). The operator of column j is A + sigma_j B (level-shift ladder,
+// proj/src/correction.cpp:36-61).
+//
+// Kernel schedule per iteration (all reductions fixed-order; the last block of each
+// producer kernel folds the per-block partials and runs the per-column scalar logic):
+//   K1 spmm_dot : Ap = (A + sigma B) p, partial p.Ap            -> alpha / breakdown
+//   K2 update_xr: x += alpha p, r -= alpha Ap, partial r.r, r.z  -> rel, check flags, beta
+//   K3 trueres  : (only when some column flagged) t = b - A x    -> converge or restart
+//   K4 update_p : p = D^-1 r + beta p
+#include <algorithm>
+
+#include "cg.cuh"
+#include "spmm_core.cuh"
+
+namespace ksb {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+enum : int { kActive = 0, kConverged = 1, kBreakdown = 2 };
+enum : int { kIt = 0, kAnyCheck = 1, kTicket1 = 2, kTicket2 = 3, kTicket3 = 4, kTicket0 = 5, kNActive = 6 };
+
+struct Cols {
+    int N, ld;
+    double tol;
+    int fixed;
+};
+
+__device__ __forceinline__ double dinv_of(const double* dA, const double* dB, const double* sigma, int r, int c) {
+    double d = dA[r];
+    if (dB) d += sigma[c] * dB[r];
+    return d != 0.0 ? 1.0 / d : 1.0;
+}
+
+/// Grid-wide "last block" election; the returned block folds the partials.
+__device__ bool last_block(int* ticket) {
+    __shared__ bool am_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int t = atomicAdd(ticket, 1);
+        am_last = (t == int(gridDim.x) - 1);
+    }
+    __syncthreads();
+    if (am_last) {
+        __threadfence();
+        if (threadIdx.x == 0) *ticket = 0;
+    }
+    return am_last;
+}
+
+/// Deterministic fold of part[b*N + c] over b for every column into out[c] (one warp per column).
+__device__ void fold_partials(const double* part, int nblocks, int N, double* out_smem) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int c = warp; c < N; c += nw) {
+        double s = 0.0;
+        for (int b = lane; b < nblocks; b += 32) s += __ldcg(part + size_t(b) * N + c);
+        s = warp_sum(s);
+        if (lane == 0) out_smem[c] = s;
+    }
+    __syncthreads();
+}
+
+/// Column-lane layout for elementwise kernels: thread -> (row offset, column), rows strided.
+struct ElemMap {
+    int c, r0, rstep, valid;
+    __device__ ElemMap(int N) {
+        const int rb = max(1, int(blockDim.x) / N);
+        c = threadIdx.x % N;
+        const int rl = threadIdx.x / N;
+        valid = rl < rb;
+        r0 = blockIdx.x * rb + rl;
+        rstep = gridDim.x * rb;
+    }
+};
+
+/// block reduction of per-thread column partials (ElemMap layout) -> part[blockIdx*N + c]
+__device__ void block_cols(double v, int N, double* part, double* smem) {
+    const int rb = max(1, int(blockDim.x) / N);
+    if (threadIdx.x < rb * N) smem[threadIdx.x] = v;
+    __syncthreads();
+    if (threadIdx.x < N) {
+        double s = 0.0;
+        for (int k = 0; k < rb; ++k) s += smem[k * N + threadIdx.x];
+        part[size_t(blockIdx.x) * N + threadIdx.x] = s;
+    }
+    __syncthreads();
+}
+
+// ---------------- K0: init ----------------
+__global__ void __launch_bounds__(kThreads) k_init(int ni, Cols cc, const double* __restrict__ B, double* __restrict__ X,
+                                                   double* __restrict__ R, double* __restrict__ P, CgDev s) {
+    extern __shared__ double sm[];
+    const int N = cc.N, ld = cc.ld;
+    ElemMap em(N);
+    double bb = 0.0, rz = 0.0;
+    if (em.valid)
+        for (int r = em.r0; r < ni; r += em.rstep) {
+            const size_t i = size_t(r) * ld + em.c;
+            const double b = B[i];
+            const double z = dinv_of(s.diagA, s.diagB, s.sigma, r, em.c) * b;
+            X[i] = 0.0;
+            R[i] = b;
+            P[i] = z;
+            bb += b * b;
+            rz += b * z;
+        }
+    block_cols(bb, N, s.part0, sm);
+    block_cols(rz, N, s.part1, sm);
+    if (!last_block(s.ctl + kTicket0)) return;
+    fold_partials(s.part0, gridDim.x, N, sm);
+    fold_partials(s.part1, gridDim.x, N, sm + N);
+    if (threadIdx.x < N) {
+        const int c = threadIdx.x;
+        const double bn = sqrt(sm[c]);
+        s.bnorm[c] = bn;
+        s.rz[c] = sm[N + c];
+        s.rr[c] = sm[c];
+        s.alpha[c] = 0.0;
+        s.beta[c] = 0.0;
+        s.iters[c] = 0;
+        s.check[c] = 0;
+        s.relres[c] = 0.0;
+        s.status[c] = (bn == 0.0) ? kConverged : kActive;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        s.ctl[kIt] = 0;
+        s.ctl[kAnyCheck] = 0;
+        int na = 0;
+        for (int c = 0; c < N; ++c) na += s.status[c] == kActive;
+        s.ctl[kNActive] = na;
+    }
+}
+
+// ---------------- K1: Ap = A p, alpha ----------------
+template <int G, int CPL, bool SHIFT, bool SPLIT>
+__global__ void __launch_bounds__(kThreads) k_spmm_dot(int ni, Cols cc, const int32_t* __restrict__ ptr,
+                                                       const int32_t* __restrict__ col, const double* __restrict__ A,
+                                                       const double* __restrict__ Bv, const double* __restrict__ P,
+                                                       double* __restrict__ AP, CgDev s) {
+    extern __shared__ double sm[];
+    const int N = cc.N, ld = cc.ld;
+    const int lane = threadIdx.x & 31;
+    const int g = lane / G, l = lane % G;
+    const int gbase = g * G;
+    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << gbase);
+    const int rows_per_warp = 32 / G;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    const int c0 = SPLIT ? 0 : l * CPL;
+    double pd[CPL];
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) pd[q] = 0.0;
+    for (int r = warp * rows_per_warp + g; r < ni; r += nwarps * rows_per_warp) {
+        const int rb = __ldg(ptr + r), re = __ldg(ptr + r + 1);
+        double acc[CPL], accB[CPL];
+        if constexpr (SPLIT) {
+            double a = 0.0, b = 0.0;
+            for (int k = rb + l; k < re; k += G) {
+                const double x = P[size_t(__ldg(col + k)) * ld];
+                a = fma(__ldg(A + k), x, a);
+                if (SHIFT) b = fma(__ldg(Bv + k), x, b);
+            }
+#pragma unroll
+            for (int o = G / 2; o > 0; o >>= 1) {
+                a += __shfl_xor_sync(gmask, a, o);
+                if (SHIFT) b += __shfl_xor_sync(gmask, b, o);
+            }
+            acc[0] = a;
+            accB[0] = b;
+        } else {
+            row_product<G, CPL, SHIFT>(rb, re, col, A, Bv, P, ld, c0, N, l, gmask, gbase, acc, accB);
+        }
+        if (!SPLIT || l == 0) {
+            if (SHIFT) {
+#pragma unroll
+                for (int q = 0; q < CPL; ++q)
+                    if (c0 + q < N) acc[q] = fma(s.sigma[c0 + q], accB[q], acc[q]);
+            }
+            if (c0 < N) {
+                double p[CPL];
+                load_cols<CPL>(P + size_t(r) * ld + c0, c0, N, p);
+                store_cols<CPL>(AP + size_t(r) * ld + c0, c0, N, acc);
+#pragma unroll
+                for (int q = 0; q < CPL; ++q) pd[q] = fma(p[q], acc[q], pd[q]);
+            }
+        }
+    }
+    // block reduce: groups with equal l hold the same columns
+    const int ngroups = blockDim.x / G;
+    const int width = G * CPL;
+    const int gid = threadIdx.x / G;
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) sm[gid * width + l * CPL + q] = pd[q];
+    __syncthreads();
+    if (threadIdx.x < N) {
+        double t = 0.0;
+        for (int k = 0; k < ngroups; ++k) t += sm[k * width + threadIdx.x];
+        s.part0[size_t(blockIdx.x) * N + threadIdx.x] = t;
+    }
+    if (!last_block(s.ctl + kTicket1)) return;
+    fold_partials(s.part0, gridDim.x, N, sm);
+    if (threadIdx.x < N) {
+        const int c = threadIdx.x;
+        const double pap = sm[c];
+        double al = 0.0;
+        if (s.status[c] == kActive) {
+            if (!cc.fixed && !(pap > 0.0)) {
+                s.status[c] = kBreakdown;
+                s.relres[c] = sqrt(s.rr[c]) / s.bnorm[c];
+            } else {
+                al = s.rz[c] / pap;
+            }
+        }
+        s.alpha[c] = al;
+    }
+}
+
+// ---------------- K2: x, r update ----------------
+__global__ void __launch_bounds__(kThreads) k_update_xr(int ni, Cols cc, double* __restrict__ X, double* __restrict__ R,
+                                                        const double* __restrict__ P, const double* __restrict__ AP,
+                                                        CgDev s) {
+    extern __shared__ double sm[];
+    const int N = cc.N, ld = cc.ld;
+    ElemMap em(N);
+    double rr = 0.0, rz = 0.0;
+    if (em.valid) {
+        const double al = s.alpha[em.c];
+        const bool act = s.status[em.c] == kActive;
+        for (int r = em.r0; r < ni; r += em.rstep) {
+            const size_t i = size_t(r) * ld + em.c;
+            double rv = R[i];
+            if (act) {
+                X[i] = fma(al, P[i], X[i]);
+                rv = fma(-al, AP[i], rv);
+                R[i] = rv;
+            }
+            rr = fma(rv, rv, rr);
+            rz = fma(rv, dinv_of(s.diagA, s.diagB, s.sigma, r, em.c) * rv, rz);
+        }
+    }
+    block_cols(rr, N, s.part0, sm);
+    block_cols(rz, N, s.part1, sm);
+    if (!last_block(s.ctl + kTicket2)) return;
+    fold_partials(s.part0, gridDim.x, N, sm);
+    fold_partials(s.part1, gridDim.x, N, sm + N);
+    __shared__ int any;
+    if (threadIdx.x == 0) any = 0;
+    __syncthreads();
+    const int it = s.ctl[kIt];
+    if (threadIdx.x < N) {
+        const int c = threadIdx.x;
+        if (s.status[c] == kActive) {
+            const double rel = sqrt(sm[c]) / s.bnorm[c];
+            s.rr[c] = sm[c];
+            s.iters[c] = it + 1;
+            s.relres[c] = rel;
+            if (!cc.fixed && rel <= cc.tol) {
+                s.check[c] = 1;
+                atomicOr(&any, 1);
+            } else {
+                s.beta[c] = sm[N + c] / s.rz[c];
+                s.rz[c] = sm[N + c];
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        s.ctl[kIt] = it + 1;
+        s.ctl[kAnyCheck] = any;
+    }
+}
+
+// ---------------- K3: true residual for flagged columns ----------------
+template <int G, int CPL, bool SHIFT, bool SPLIT>
+__global__ void __launch_bounds__(kThreads) k_trueres(int ni, Cols cc, const int32_t* __restrict__ ptr,
+                                                      const int32_t* __restrict__ col, const double* __restrict__ A,
+                                                      const double* __restrict__ Bv, const double* __restrict__ Bb,
+                                                      const double* __restrict__ X, double* __restrict__ R, CgDev s) {
+    extern __shared__ double sm[];
+    if (s.ctl[kAnyCheck] == 0) return;  // uniform early exit: nothing flagged this iteration
+    const int N = cc.N, ld = cc.ld;
+    const int lane = threadIdx.x & 31;
+    const int g = lane / G, l = lane % G;
+    const int gbase = g * G;
+    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << gbase);
+    const int rows_per_warp = 32 / G;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    const int c0 = SPLIT ? 0 : l * CPL;
+    double tt[CPL], tz[CPL];
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) tt[q] = tz[q] = 0.0;
+    for (int r = warp * rows_per_warp + g; r < ni; r += nwarps * rows_per_warp) {
+        const int rb = __ldg(ptr + r), re = __ldg(ptr + r + 1);
+        double acc[CPL], accB[CPL];
+        if constexpr (SPLIT) {
+            double a = 0.0, b = 0.0;
+            for (int k = rb + l; k < re; k += G) {
+                const double x = X[size_t(__ldg(col + k)) * ld];
+                a = fma(__ldg(A + k), x, a);
+                if (SHIFT) b = fma(__ldg(Bv + k), x, b);
+            }
+#pragma unroll
+            for (int o = G / 2; o > 0; o >>= 1) {
+                a += __shfl_xor_sync(gmask, a, o);
+                if (SHIFT) b += __shfl_xor_sync(gmask, b, o);
+            }
+            acc[0] = a;
+            accB[0] = b;
+        } else {
+            row_product<G, CPL, SHIFT>(rb, re, col, A, Bv, X, ld, c0, N, l, gmask, gbase, acc, accB);
+        }
+        if ((!SPLIT || l == 0) && c0 < N) {
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) {
+                const int c = c0 + q;
+                if (c < N && s.check[c]) {
+                    const double ax = SHIFT ? fma(s.sigma[c], accB[q], acc[q]) : acc[q];
+                    const size_t i = size_t(r) * ld + c;
+                    const double t = Bb[i] - ax;
+                    R[i] = t;
+                    tt[q] = fma(t, t, tt[q]);
+                    tz[q] = fma(t, dinv_of(s.diagA, s.diagB, s.sigma, r, c) * t, tz[q]);
+                }
+            }
+        }
+    }
+    const int ngroups = blockDim.x / G;
+    const int width = G * CPL;
+    const int gid = threadIdx.x / G;
+    for (int pass = 0; pass < 2; ++pass) {
+#pragma unroll
+        for (int q = 0; q < CPL; ++q) sm[gid * width + l * CPL + q] = pass ? tz[q] : tt[q];
+        __syncthreads();
+        if (threadIdx.x < N) {
+            double t = 0.0;
+            for (int k = 0; k < ngroups; ++k) t += sm[k * width + threadIdx.x];
+            (pass ? s.part1 : s.part0)[size_t(blockIdx.x) * N + threadIdx.x] = t;
+        }
+        __syncthreads();
+    }
+    if (!last_block(s.ctl + kTicket3)) return;
+    fold_partials(s.part0, gridDim.x, N, sm);
+    fold_partials(s.part1, gridDim.x, N, sm + N);
+    if (threadIdx.x < N) {
+        const int c = threadIdx.x;
+        if (s.check[c]) {
+            const double rel = sqrt(sm[c]) / s.bnorm[c];
+            s.relres[c] = rel;
+            s.rr[c] = sm[c];
+            if (rel <= cc.tol) {
+                s.status[c] = kConverged;
+            } else {  // restart from the true residual: p = z
+                s.rz[c] = sm[N + c];
+                s.beta[c] = 0.0;
+            }
+            s.check[c] = 0;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        s.ctl[kAnyCheck] = 0;
+        int na = 0;
+        for (int c = 0; c < N; ++c) na += s.status[c] == kActive;
+        s.ctl[kNActive] = na;
+    }
+}
+
+// ---------------- K4: p update ----------------
+__global__ void __launch_bounds__(kThreads) k_update_p(int ni, Cols cc, const double* __restrict__ R,
+                                                       double* __restrict__ P, CgDev s) {
+    const int N = cc.N, ld = cc.ld;
+    ElemMap em(N);
+    if (!em.valid) return;
+    if (s.status[em.c] != kActive) return;
+    const double be = s.beta[em.c];
+    for (int r = em.r0; r < ni; r += em.rstep) {
+        const size_t i = size_t(r) * ld + em.c;
+        P[i] = fma(be, P[i], dinv_of(s.diagA, s.diagB, s.sigma, r, em.c) * R[i]);
+    }
+}
+
+__global__ void k_diag(int ni, const int32_t* __restrict__ dslot, const double* __restrict__ vals,
+                       double* __restrict__ d) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < ni; r += gridDim.x * blockDim.x) d[r] = vals[dslot[r]];
+}
+
+int elem_grid(const Ctx& c, int ni, int N) {
+    const int rb = std::max(1, kThreads / N);
+    const int64_t want = (int64_t(ni) + rb - 1) / rb;
+    return int(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(c.sm_count) * 8)));
+}
+
+struct Plan {
+    int G, CPL;
+    bool split;
+};
+
+Plan plan_for(int N) {
+    if (N == 1) return {8, 1, true};
+    if (N <= 8) return {4, 2, false};
+    if (N <= 16) return {8, 2, false};
+    if (N <= 32) return {16, 2, false};
+    if (N <= 64) return {32, 2, false};
+    return {32, 4, false};
+}
+
+template <int G, int CPL, bool SHIFT, bool SPLIT>
+void launch_iteration(Ctx& c, const Level& L, const CgWork& w, const Cols& cc, const double* A, const double* Bv,
+                      const double* Bb, double* X, int grid_s, int grid_e) {
+    const size_t sm_s = sizeof(double) * std::max<size_t>(size_t(kThreads / G) * G * CPL, 2 * size_t(cc.N));
+    const size_t sm_e = sizeof(double) * std::max<size_t>(kThreads, 2 * size_t(cc.N));
+    launch(c, "spmm", k_spmm_dot<G, CPL, SHIFT, SPLIT>, grid_s, kThreads, sm_s, L.ni, cc,
+           (const int32_t*)L.ii_ptr.p, (const int32_t*)L.ii_col.p, A, Bv, (const double*)w.P, w.AP, w.dev);
+    launch(c, "cg_update", k_update_xr, grid_e, kThreads, sm_e, L.ni, cc, X, w.R, (const double*)w.P,
+           (const double*)w.AP, w.dev);
+    if (!cc.fixed)
+        launch(c, "cg_trueres", k_trueres<G, CPL, SHIFT, SPLIT>, grid_s, kThreads, sm_s, L.ni, cc,
+               (const int32_t*)L.ii_ptr.p, (const int32_t*)L.ii_col.p, A, Bv, Bb, (const double*)X, w.R, w.dev);
+    launch(c, "cg_update", k_update_p, grid_e, kThreads, 0, L.ni, cc, (const double*)w.R, w.P, w.dev);
+}
+
+template <bool SHIFT>
+void iteration(Ctx& c, const Level& L, const CgWork& w, const Cols& cc, const double* A, const double* Bv,
+               const double* Bb, double* X, int grid_s, int grid_e) {
+    const Plan p = plan_for(cc.N);
+    if (p.split)
+        launch_iteration<8, 1, SHIFT, true>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e);
+    else if (p.G == 4)
+        launch_iteration<4, 2, SHIFT, false>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e);
+    else if (p.G == 8)
+        launch_iteration<8, 2, SHIFT, false>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e);
+    else if (p.G == 16)
+        launch_iteration<16, 2, SHIFT, false>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e);
+    else if (p.CPL == 2)
+        launch_iteration<32, 2, SHIFT, false>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e);
+    else
+        launch_iteration<32, 4, SHIFT, false>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e);
+}
+
+} // namespace
+
+void CgWork::ensure(int ni, int N, int ld, int max_blocks) {
+    const int64_t vec = int64_t(ni) * ld;
+    if (vec > cap_vec) {
+        rbuf.alloc(vec);
+        pbuf.alloc(vec);
+        apbuf.alloc(vec);
+        cap_vec = vec;
+    }
+    R = rbuf.p;
+    P = pbuf.p;
+    AP = apbuf.p;
+    if (N > cap_cols || max_blocks > cap_blocks) {
+        cap_cols = std::max(N, cap_cols);
+        cap_blocks = std::max(max_blocks, cap_blocks);
+        scal.alloc(int64_t(cap_cols) * 8);
+        ints.alloc(int64_t(cap_cols) * 4 + 16);
+        parts.alloc(int64_t(cap_blocks) * cap_cols * 2);
+    }
+}
+
+void cg_solve(Ctx& c, Level& L, int mat, int shift_mat, const double* h_sigma, const double* d_B, double* d_X, int N,
+              int ld, const CgOptions& o, CgColumnStats* stats, CgWork& w) {
+    if (N < 1 || N > 128) raise(KSB_INVALID_ARGUMENT, "cg: N must be in [1, 128]");
+    if (ld < N || (N > 1 && (ld & 1))) raise(KSB_INVALID_ARGUMENT, "cg: ld must be >= N and even for N > 1");
+    if (!L.mats[mat].valid) raise(KSB_INVALID_ARGUMENT, "cg: operator not assembled");
+    const bool shift = shift_mat >= 0;
+    if (shift && !L.mats[shift_mat].valid) raise(KSB_INVALID_ARGUMENT, "cg: shift operator not assembled");
+
+    const Plan p = plan_for(N);
+    const int rows_per_block = kThreads / p.G;
+    const int grid_s = int(std::max<int64_t>(
+        1, std::min<int64_t>((int64_t(L.ni) + rows_per_block - 1) / rows_per_block, int64_t(c.sm_count) * 8)));
+    const int grid_e = elem_grid(c, L.ni, N);
+    w.ensure(L.ni, N, ld, std::max(grid_s, grid_e));
+
+    CgDev& d = w.dev;
+    double* sc = w.scal.p;
+    const int cap = w.cap_cols;
+    d.bnorm = sc + 0 * cap;
+    d.rz = sc + 1 * cap;
+    d.rr = sc + 2 * cap;
+    d.alpha = sc + 3 * cap;
+    d.beta = sc + 4 * cap;
+    d.relres = sc + 5 * cap;
+    d.sigma = sc + 6 * cap;
+    d.status = w.ints.p;
+    d.check = w.ints.p + cap;
+    d.iters = w.ints.p + 2 * cap;
+    d.ctl = w.ints.p + 4 * cap;
+    d.part0 = w.parts.p;
+    d.part1 = w.parts.p + int64_t(w.cap_blocks) * cap;
+    if (w.diagA.n < L.ni) w.diagA.alloc(L.ni);
+    if (w.diagB.n < L.ni) w.diagB.alloc(L.ni);
+    launch(c, "cg_setup", k_diag, elem_grid(c, L.ni, 1), kThreads, 0, L.ni, (const int32_t*)L.diag_slot.p,
+           (const double*)L.mats[mat].ii.p, w.diagA.p);
+    d.diagA = w.diagA.p;
+    d.diagB = nullptr;
+    std::vector<double> sig(N, 0.0);
+    if (shift) {
+        launch(c, "cg_setup", k_diag, elem_grid(c, L.ni, 1), kThreads, 0, L.ni, (const int32_t*)L.diag_slot.p,
+               (const double*)L.mats[shift_mat].ii.p, w.diagB.p);
+        d.diagB = w.diagB.p;
+        if (h_sigma) std::copy(h_sigma, h_sigma + N, sig.begin());
+    }
+    KSB_CUDA_CHECK(cudaMemcpyAsync(d.sigma, sig.data(), sizeof(double) * N, cudaMemcpyHostToDevice, c.stream));
+    KSB_CUDA_CHECK(cudaMemsetAsync(d.ctl, 0, sizeof(int) * 16, c.stream));
+
+    Cols cc{N, ld, o.tol, o.fixed_iterations > 0 ? 1 : 0};
+    const size_t sm_e = sizeof(double) * std::max<size_t>(kThreads, 2 * size_t(N));
+    launch(c, "cg_setup", k_init, grid_e, kThreads, sm_e, L.ni, cc, d_B, d_X, w.R, w.P, d);
+
+    const double* A = L.mats[mat].ii.p;
+    const double* Bv = shift ? L.mats[shift_mat].ii.p : nullptr;
+    const int total = cc.fixed ? o.fixed_iterations : o.max_iterations;
+    const int every = std::max(1, o.check_every);
+    int done = 0;
+    while (done < total) {
+        const int chunk = std::min(every, total - done);
+        for (int k = 0; k < chunk; ++k) {
+            if (shift)
+                iteration<true>(c, L, w, cc, A, Bv, d_B, d_X, grid_s, grid_e);
+            else
+                iteration<false>(c, L, w, cc, A, nullptr, d_B, d_X, grid_s, grid_e);
+        }
+        done += chunk;
+        if (!cc.fixed) {
+            int ctl[16];
+            KSB_CUDA_CHECK(cudaMemcpyAsync(ctl, d.ctl, sizeof ctl, cudaMemcpyDeviceToHost, c.stream));
+            KSB_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+            if (ctl[kNActive] == 0) break;
+        }
+    }
+    if (stats) {
+        std::vector<int> st(N), it(N);
+        std::vector<double> rel(N);
+        KSB_CUDA_CHECK(cudaMemcpyAsync(st.data(), d.status, sizeof(int) * N, cudaMemcpyDeviceToHost, c.stream));
+        KSB_CUDA_CHECK(cudaMemcpyAsync(it.data(), d.iters, sizeof(int) * N, cudaMemcpyDeviceToHost, c.stream));
+        KSB_CUDA_CHECK(cudaMemcpyAsync(rel.data(), d.relres, sizeof(double) * N, cudaMemcpyDeviceToHost, c.stream));
+        KSB_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+        for (int j = 0; j < N; ++j) {
+            stats[j].iterations = it[j];
+            stats[j].relative_residual = rel[j];
+            stats[j].converged = st[j] == kConverged;
+            stats[j].breakdown = st[j] == kBreakdown;
+        }
+    }
+}
+
+} // namespace ksb

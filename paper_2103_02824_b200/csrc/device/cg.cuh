@@ -1,0 +1,43 @@
+// Multi-RHS CG driver interface (see cg.cu).
+#pragma once
+
+#include "level.cuh"
+
+namespace ksb {
+
+struct CgOptions {
+    double tol = 1e-9;
+    int max_iterations = 20000;
+    int fixed_iterations = 0;
+    int check_every = 8;
+};
+
+struct CgColumnStats {
+    int iterations = 0;
+    double relative_residual = 0.0;
+    int converged = 0;
+    int breakdown = 0;
+};
+
+/// device pointers of the per-column scalar state (passed by value to kernels)
+struct CgDev {
+    double *bnorm, *rz, *rr, *alpha, *beta, *relres, *sigma;
+    const double *diagA, *diagB;
+    int *status, *check, *iters, *ctl;
+    double *part0, *part1;
+};
+
+struct CgWork {
+    DevBuf<double> rbuf, pbuf, apbuf, scal, parts, diagA, diagB;
+    DevBuf<int> ints;
+    double *R = nullptr, *P = nullptr, *AP = nullptr;
+    int64_t cap_vec = 0;
+    int cap_cols = 0, cap_blocks = 0;
+    CgDev dev{};
+    void ensure(int ni, int N, int ld, int max_blocks);
+};
+
+void cg_solve(Ctx& c, Level& L, int mat, int shift_mat, const double* h_sigma, const double* d_B, double* d_X, int N,
+              int ld, const CgOptions& o, CgColumnStats* stats, CgWork& w);
+
+} // namespace ksb

@@ -1,0 +1,64 @@
+// Shared device utilities: error checks, launch accounting, warp reductions.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../host/mesh.hpp"
+
+namespace ksb {
+
+#define KSB_CUDA_CHECK(expr)                                                                  \
+    do {                                                                                      \
+        cudaError_t _e = (expr);                                                              \
+        if (_e != cudaSuccess)                                                                \
+            ::ksb::raise(KSB_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));       \
+    } while (0)
+
+constexpr int kSMs = 148;  // B200
+
+/// Device context: one stream, launch counters, optional per-kernel event timing.
+struct Ctx {
+    int device = 0;
+    int sm_count = kSMs;
+    cudaStream_t stream = nullptr;
+    bool profiling = false;
+    int64_t launches = 0;
+    struct Timer {
+        double ms = 0;
+        int64_t count = 0;
+    };
+    std::map<std::string, Timer> timers;
+    std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+    std::vector<cudaEvent_t> event_pool;
+
+    cudaEvent_t take_event();
+    void begin(const char* name, cudaEvent_t* e0);
+    void end(const char* name, cudaEvent_t e0);
+    void harvest();  // fold completed pending timings into timers (syncs the stream)
+};
+
+/// RAII-free launch helper: counts the launch and brackets it with events when profiling.
+template <typename Kernel, typename... Args>
+inline void launch(Ctx& c, const char* name, Kernel k, dim3 grid, dim3 block, size_t smem, Args... args) {
+    cudaEvent_t e0 = nullptr;
+    if (c.profiling) c.begin(name, &e0);
+    k<<<grid, block, smem, c.stream>>>(args...);
+    ++c.launches;
+    KSB_CUDA_CHECK(cudaGetLastError());
+    if (c.profiling) c.end(name, e0);
+}
+
+inline int ceil_div(int64_t a, int64_t b) { return int((a + b - 1) / b); }
+
+__device__ __forceinline__ double warp_sum(double v, unsigned mask = 0xffffffffu) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(mask, v, o);
+    return v;
+}
+
+} // namespace ksb

@@ -1,0 +1,76 @@
+// Device-resident fine level: index data uploaded once, operator values on the shared pattern.
+#pragma once
+
+#include "../host/topology.hpp"
+#include "common.cuh"
+
+namespace ksb {
+
+constexpr int kMaxMats = 32;
+
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    int64_t n = 0;
+    void alloc(int64_t count) {
+        release();
+        n = count;
+        if (count > 0) KSB_CUDA_CHECK(cudaMalloc(&p, sizeof(T) * size_t(count)));
+    }
+    void upload(Ctx& c, const std::vector<T>& h) {
+        alloc(int64_t(h.size()));
+        if (n) KSB_CUDA_CHECK(cudaMemcpyAsync(p, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice, c.stream));
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    ~DevBuf() { release(); }
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+};
+
+struct Mat {
+    DevBuf<double> ii, ib;
+    bool valid = false;
+};
+
+struct Level {
+    Ctx* ctx = nullptr;
+    std::shared_ptr<FineTopology> topo;
+    int n = 0, ni = 0, nb = 0, nt = 0;
+    int64_t nnz_ii = 0, nnz_ib = 0;
+    int nH = 0, nct = 0, ncv = 0;  // coarse interior dofs, coarse tets, coarse vertices
+
+    DevBuf<double> xyz;
+    DevBuf<int32_t> tets;
+    DevBuf<int32_t> interior, iidx, boundary;
+    DevBuf<int32_t> ii_ptr, ii_col, ib_ptr, ib_col, diag_slot;
+    DevBuf<int32_t> ii_gptr, ii_gent, ib_gptr, ib_gent;
+    DevBuf<int32_t> pint_col;
+    DevBuf<double> pint_val;
+    DevBuf<int32_t> ancestor, anc_ptr, anc_tets;
+    DevBuf<double> ebuf;      // element matrices, 16 per tet (scratch)
+    DevBuf<double> scratch;   // term accumulation scratch (nnz_ii + nnz_ib)
+    DevBuf<int> flag;         // device error flag (singular quadrature)
+    Mat mats[kMaxMats];
+
+    Mat& mat(int id);
+};
+
+// assembly (assemble.cu)
+struct Potential {
+    int kind = -1;
+    int n = 0;
+    std::vector<double> params;
+};
+void assemble_into(Level& L, int mat, double c_s, double c_m, const Potential* pot, double c_p,
+                   const double* d_w, double c_w);
+
+// SpMM (spmm.cu): Y = (A + sigma_j B) X on interior blocks; B may be null (sigma ignored)
+void spmm(Ctx& c, const Level& L, const double* A, const double* B, const double* d_sigma,
+          const double* X, int N, int ldx, double* Y, int ldy);
+
+} // namespace ksb

@@ -1,0 +1,254 @@
+// Host index builders for a fine level. See topology.hpp for reference anchors.
+#include "topology.hpp"
+
+#include <algorithm>
+#include <limits>
+
+namespace ksb {
+
+Space::Space(MeshPtr m) : mesh(std::move(m)) {
+    const int nv = mesh->n_vertices();
+    iidx.assign(nv, -1);
+    bidx.assign(nv, -1);
+    for (int v = 0; v < nv; ++v) {
+        if (mesh->on_boundary[v]) {
+            bidx[v] = int32_t(boundary.size());
+            boundary.push_back(v);
+        } else {
+            iidx[v] = int32_t(interior.size());
+            interior.push_back(v);
+        }
+    }
+}
+
+void Hierarchy::push(MeshPtr m) {
+    const int nv = m->n_vertices();
+    std::vector<int32_t> col(size_t(nv) * 4, -1);
+    std::vector<double> val(size_t(nv) * 4, 0.0);
+    std::vector<int32_t> anc(m->n_tets());
+    if (meshes_.empty()) {
+        for (int v = 0; v < nv; ++v) {
+            col[4 * v] = v;
+            val[4 * v] = 1.0;
+        }
+        for (int t = 0; t < m->n_tets(); ++t) anc[t] = t;
+    } else {
+        if (m->n_parent_vertices != meshes_.back()->n_vertices())
+            raise(KSB_HIERARCHY, "levels are not nested");
+        const auto& pc = pcol_.back();
+        const auto& pv = pval_.back();
+        const int np = m->n_parent_vertices;
+        std::copy(pc.begin(), pc.begin() + size_t(np) * 4, col.begin());
+        std::copy(pv.begin(), pv.begin() + size_t(np) * 4, val.begin());
+        // new vertices average their parent edge; parents precede children and
+        // every row is a convex combination of <= 4 coarse vertices (dyadic, exact)
+        for (int v = np; v < nv; ++v) {
+            const int a = m->vparent[2 * v], b = m->vparent[2 * v + 1];
+            int32_t c[8];
+            double w[8];
+            int cnt = 0;
+            auto add = [&](int src) {
+                for (int k = 0; k < 4 && col[4 * src + k] >= 0; ++k) {
+                    const int32_t cc = col[4 * src + k];
+                    const double ww = 0.5 * val[4 * src + k];
+                    int j = 0;
+                    while (j < cnt && c[j] != cc) ++j;
+                    if (j == cnt) {
+                        c[cnt] = cc;
+                        w[cnt] = ww;
+                        ++cnt;
+                    } else {
+                        w[j] += ww;
+                    }
+                }
+            };
+            add(a);
+            add(b);
+            if (cnt > 4) raise(KSB_INTERNAL, "prolongation row wider than one coarse tet");
+            // sort by coarse column
+            for (int i = 1; i < cnt; ++i)
+                for (int j = i; j > 0 && c[j - 1] > c[j]; --j) {
+                    std::swap(c[j - 1], c[j]);
+                    std::swap(w[j - 1], w[j]);
+                }
+            for (int k = 0; k < cnt; ++k) {
+                col[4 * v + k] = c[k];
+                val[4 * v + k] = w[k];
+            }
+        }
+        const auto& pa = anc_.back();
+        for (int t = 0; t < m->n_tets(); ++t) anc[t] = pa[m->parent[t]];
+    }
+    meshes_.push_back(std::move(m));
+    pcol_.push_back(std::move(col));
+    pval_.push_back(std::move(val));
+    anc_.push_back(std::move(anc));
+}
+
+namespace {
+
+void check_i32(int64_t x, const char* what) {
+    if (x > std::numeric_limits<int32_t>::max())
+        raise(KSB_INVALID_ARGUMENT, std::string(what) + " exceeds the int32 index range");
+}
+
+} // namespace
+
+std::shared_ptr<FineTopology> build_topology(const Hierarchy& h, int level) {
+    auto topo = std::make_shared<FineTopology>();
+    const Mesh& m = h.mesh(level);
+    topo->space = std::make_shared<Space>(h.mesh_ptr(level));
+    topo->coarse = std::make_shared<Space>(h.mesh_ptr(0));
+    const Space& S = *topo->space;
+    const int nv = S.n(), ni = S.ni(), nt = m.n_tets();
+    check_i32(int64_t(nt) * 16, "16 * n_tets");
+
+    // vertex -> incident tets, ascending tet id (counting sort)
+    std::vector<int32_t> vptr(size_t(nv) + 1, 0), vtet(size_t(nt) * 4);
+    for (int t = 0; t < nt; ++t)
+        for (int k = 0; k < 4; ++k) ++vptr[m.tets[4 * t + k] + 1];
+    for (int v = 0; v < nv; ++v) vptr[v + 1] += vptr[v];
+    {
+        std::vector<int32_t> fill(vptr.begin(), vptr.end() - 1);
+        for (int t = 0; t < nt; ++t)
+            for (int k = 0; k < 4; ++k) vtet[fill[m.tets[4 * t + k]]++] = t;
+    }
+
+    // interior-row patterns: all vertices sharing a tet with the row vertex
+    std::vector<std::vector<int32_t>> rowv(ni);
+#pragma omp parallel for schedule(dynamic, 1024)
+    for (int r = 0; r < ni; ++r) {
+        const int v = S.interior[r];
+        auto& nb = rowv[r];
+        nb.reserve(32);
+        for (int p = vptr[v]; p < vptr[v + 1]; ++p)
+            for (int k = 0; k < 4; ++k) nb.push_back(m.tets[4 * vtet[p] + k]);
+        std::sort(nb.begin(), nb.end());
+        nb.erase(std::unique(nb.begin(), nb.end()), nb.end());
+    }
+    auto& ii = topo->ii;
+    auto& ib = topo->ib;
+    ii.rows = ib.rows = ni;
+    ii.cols = ni;
+    ib.cols = S.nb();
+    ii.ptr.assign(size_t(ni) + 1, 0);
+    ib.ptr.assign(size_t(ni) + 1, 0);
+    {
+        int64_t ci = 0, cb = 0;
+        for (int r = 0; r < ni; ++r) {
+            for (int32_t c : rowv[r]) (S.iidx[c] >= 0 ? ci : cb)++;
+            check_i32(ci, "interior nnz");
+            ii.ptr[r + 1] = int32_t(ci);
+            ib.ptr[r + 1] = int32_t(cb);
+        }
+    }
+    ii.col.resize(ii.ptr.back());
+    ib.col.resize(ib.ptr.back());
+    topo->diag_slot.resize(ni);
+#pragma omp parallel for schedule(static)
+    for (int r = 0; r < ni; ++r) {
+        int32_t pi = ii.ptr[r], pb = ib.ptr[r];
+        for (int32_t c : rowv[r]) {
+            if (S.iidx[c] >= 0) {
+                if (c == S.interior[r]) topo->diag_slot[r] = pi;
+                ii.col[pi++] = S.iidx[c];
+            } else {
+                ib.col[pb++] = S.bidx[c];
+            }
+        }
+    }
+
+    // slot gather lists: element entry (t, li, lj) feeds slot (v[li], v[lj]) of an interior row.
+    // Walking a row's incident tets in ascending order yields the setFromTriplets fold order.
+    topo->ii_gptr.assign(size_t(ii.nnz()) + 1, 0);
+    topo->ib_gptr.assign(size_t(ib.nnz()) + 1, 0);
+    auto find_slot = [&](int r, int32_t vcol, bool& interior_col) -> int32_t {
+        if (S.iidx[vcol] >= 0) {
+            interior_col = true;
+            const int32_t key = S.iidx[vcol];
+            const int32_t* b = ii.col.data() + ii.ptr[r];
+            const int32_t* e = ii.col.data() + ii.ptr[r + 1];
+            return int32_t(std::lower_bound(b, e, key) - ii.col.data());
+        }
+        interior_col = false;
+        const int32_t key = S.bidx[vcol];
+        const int32_t* b = ib.col.data() + ib.ptr[r];
+        const int32_t* e = ib.col.data() + ib.ptr[r + 1];
+        return int32_t(std::lower_bound(b, e, key) - ib.col.data());
+    };
+#pragma omp parallel for schedule(dynamic, 1024)
+    for (int r = 0; r < ni; ++r) {
+        const int v = S.interior[r];
+        for (int p = vptr[v]; p < vptr[v + 1]; ++p) {
+            const int t = vtet[p];
+            for (int lj = 0; lj < 4; ++lj) {
+                bool in;
+                const int32_t s = find_slot(r, m.tets[4 * t + lj], in);
+                (in ? topo->ii_gptr : topo->ib_gptr)[s + 1]++;
+            }
+        }
+    }
+    for (size_t s = 0; s + 1 < topo->ii_gptr.size(); ++s) topo->ii_gptr[s + 1] += topo->ii_gptr[s];
+    for (size_t s = 0; s + 1 < topo->ib_gptr.size(); ++s) topo->ib_gptr[s + 1] += topo->ib_gptr[s];
+    topo->ii_gent.resize(topo->ii_gptr.back());
+    topo->ib_gent.resize(topo->ib_gptr.back());
+#pragma omp parallel for schedule(dynamic, 1024)
+    for (int r = 0; r < ni; ++r) {
+        const int v = S.interior[r];
+        // per-row fill cursors (slots of one row are private to this iteration)
+        std::vector<int32_t> fi(topo->ii_gptr.begin() + ii.ptr[r], topo->ii_gptr.begin() + ii.ptr[r + 1]);
+        std::vector<int32_t> fb(topo->ib_gptr.begin() + ib.ptr[r], topo->ib_gptr.begin() + ib.ptr[r + 1]);
+        for (int p = vptr[v]; p < vptr[v + 1]; ++p) {
+            const int t = vtet[p];
+            int li = 0;
+            while (m.tets[4 * t + li] != v) ++li;
+            for (int lj = 0; lj < 4; ++lj) {
+                bool in;
+                const int32_t s = find_slot(r, m.tets[4 * t + lj], in);
+                const int32_t e = t * 16 + li * 4 + lj;
+                if (in) topo->ii_gent[fi[s - ii.ptr[r]]++] = e;
+                else topo->ib_gent[fb[s - ib.ptr[r]]++] = e;
+            }
+        }
+    }
+
+    // composite prolongation restricted to interior coarse columns (P_int), interior fine rows
+    const Space& C = *topo->coarse;
+    const auto& pc = h.pcol(level);
+    const auto& pv = h.pval(level);
+    // fine boundary vertices interpolate coarse boundary vertices only, so their
+    // P_int rows vanish (this is what lets every fine operator live on interior rows)
+    for (int32_t v : S.boundary)
+        for (int k = 0; k < 4 && pc[4 * size_t(v) + k] >= 0; ++k)
+            if (C.iidx[pc[4 * size_t(v) + k]] >= 0)
+                raise(KSB_INTERNAL, "fine boundary vertex couples to a coarse interior vertex");
+    topo->pint_col.assign(size_t(ni) * 4, -1);
+    topo->pint_val.assign(size_t(ni) * 4, 0.0);
+    for (int r = 0; r < ni; ++r) {
+        const int v = S.interior[r];
+        int w = 0;
+        for (int k = 0; k < 4; ++k) {
+            const int32_t c = pc[4 * size_t(v) + k];
+            if (c < 0) break;
+            if (C.iidx[c] < 0) continue;
+            topo->pint_col[4 * size_t(r) + w] = C.iidx[c];
+            topo->pint_val[4 * size_t(r) + w] = pv[4 * size_t(v) + k];
+            ++w;
+        }
+    }
+
+    // fine tets grouped by coarse ancestor
+    topo->ancestor = h.ancestor(level);
+    const int nct = h.mesh(0).n_tets();
+    topo->anc_ptr.assign(size_t(nct) + 1, 0);
+    for (int t = 0; t < nt; ++t) ++topo->anc_ptr[topo->ancestor[t] + 1];
+    for (int c = 0; c < nct; ++c) topo->anc_ptr[c + 1] += topo->anc_ptr[c];
+    topo->anc_tets.resize(nt);
+    {
+        std::vector<int32_t> fill(topo->anc_ptr.begin(), topo->anc_ptr.end() - 1);
+        for (int t = 0; t < nt; ++t) topo->anc_tets[fill[topo->ancestor[t]]++] = t;
+    }
+    return topo;
+}
+
+} // namespace ksb

@@ -1,0 +1,74 @@
+// Host-side index data for one fine level: FE space split, composite
+// prolongation to the coarse level, CSR patterns and the deterministic
+// assembly gather lists the device kernels consume.
+//
+//   FESpace interior/boundary split   reference proj/src/fespace.cpp:7-18
+//   prolongation_matrix + chaining    reference proj/src/fespace.cpp:35-56,64-74
+//   interior_columns (P_int)          reference proj/src/correction.cpp:79-90
+//   EllipticSolver gather (A_ii,A_ib) reference proj/src/solver.cpp:11-24,28-48
+//   setFromTriplets duplicate order   reference proj/src/assembly.cpp:36-63
+#pragma once
+
+#include "mesh.hpp"
+
+namespace ksb {
+
+struct Space {
+    MeshPtr mesh;
+    std::vector<int32_t> interior;   // vertex ids, ascending
+    std::vector<int32_t> boundary;   // vertex ids, ascending
+    std::vector<int32_t> iidx;       // vertex -> interior position or -1
+    std::vector<int32_t> bidx;       // vertex -> boundary position or -1
+    explicit Space(MeshPtr m);
+    int n() const { return mesh->n_vertices(); }
+    int ni() const { return int(interior.size()); }
+    int nb() const { return int(boundary.size()); }
+};
+
+/// Nested sequence of meshes with composite transfer data to level 0.
+class Hierarchy {
+public:
+    void push(MeshPtr m);
+    int n_levels() const { return int(meshes_.size()); }
+    const Mesh& mesh(int k) const { return *meshes_.at(k); }
+    MeshPtr mesh_ptr(int k) const { return meshes_.at(k); }
+    /// composite prolongation row of vertex v of level k to level-0 vertices (<=4 entries, col ascending)
+    const std::vector<int32_t>& pcol(int k) const { return pcol_.at(k); }   // n_k*4, -1 padded
+    const std::vector<double>& pval(int k) const { return pval_.at(k); }    // n_k*4
+    const std::vector<int32_t>& ancestor(int k) const { return anc_.at(k); } // level-0 tet per tet
+
+private:
+    std::vector<MeshPtr> meshes_;
+    std::vector<std::vector<int32_t>> pcol_;
+    std::vector<std::vector<double>> pval_;
+    std::vector<std::vector<int32_t>> anc_;
+};
+
+/// CSR block over interior rows. Columns are in interior (ii) or boundary (ib) numbering.
+struct Csr {
+    int32_t rows = 0, cols = 0;
+    std::vector<int32_t> ptr;
+    std::vector<int32_t> col;
+    int64_t nnz() const { return ptr.empty() ? 0 : ptr.back(); }
+};
+
+/// Everything the device needs to know about a fine level's index structure.
+struct FineTopology {
+    std::shared_ptr<Space> space;      // fine space
+    std::shared_ptr<Space> coarse;     // level-0 space
+    Csr ii, ib;                        // interior x interior, interior x boundary patterns
+    std::vector<int32_t> diag_slot;    // ii slot of (r, r)
+    // slot -> element-matrix entries (t*16 + li*4 + lj), ascending t (setFromTriplets order)
+    std::vector<int32_t> ii_gptr, ib_gptr;
+    std::vector<int32_t> ii_gent, ib_gent;
+    // composite P_int restricted to fine interior rows: <=4 (coarse interior col, value) per row
+    std::vector<int32_t> pint_col;     // ni*4, -1 padded
+    std::vector<double> pint_val;      // ni*4
+    std::vector<int32_t> ancestor;     // per fine tet, level-0 tet
+    std::vector<int32_t> anc_ptr;      // coarse tet -> range in anc_tets
+    std::vector<int32_t> anc_tets;     // fine tets grouped by coarse ancestor, ascending inside a group
+};
+
+std::shared_ptr<FineTopology> build_topology(const Hierarchy& h, int level);
+
+} // namespace ksb

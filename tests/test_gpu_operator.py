@@ -1,0 +1,144 @@
+"""K-ASM / K-SpMM / multi-RHS CG through the C-ABI vs the CPU oracle."""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+import paper_2103_02824_b200 as kb
+from oracle import OMesh, Oracle
+
+pytestmark = pytest.mark.gpu
+
+ATOMS = np.array([[2.0, 0.31, -0.17, 0.05], [1.0, -0.6, 0.4, 0.9]])
+GAUSS = np.array([[3.0, 0.8, 0.2, -0.1, 0.3], [1.5, 1.2, -0.9, 0.5, -0.4]])
+
+
+def hierarchy(n=3, levels=1, adapt=0, lo=-4.0, hi=4.0, seed=5):
+    h = kb.Hierarchy()
+    orc = Oracle(ATOMS, n_pairs=2)
+    a, b = kb.Mesh.box([lo] * 3, [hi] * 3, n), OMesh.box([lo] * 3, [hi] * 3, n)
+    h.push(a)
+    orc.push(b)
+    for _ in range(levels):
+        a, b = a.uniform_refine(), b.uniform_refine()
+        h.push(a)
+        orc.push(b)
+    rng = np.random.default_rng(seed)
+    for _ in range(adapt):
+        marks = rng.integers(0, a.n_tets, 6)
+        a, b = a.adapt_refine(marks), b.adapt_refine(marks)
+        h.push(a)
+        orc.push(b)
+    return h, orc
+
+
+def csr_of_oracle(op):
+    ptr, idx, val = op.ii()
+    A = sp.csc_matrix((val, idx, ptr), shape=(op.ni, op.ni)).tocsr()
+    A.sort_indices()
+    return A
+
+
+@pytest.mark.parametrize("adapt", [0, 2])
+def test_assembly_matches_oracle(ctx, adapt):
+    h, orc = hierarchy(adapt=adapt)
+    lev = h.n_levels - 1
+    L = kb.Level(ctx, h, lev)
+    w = np.sin(orc.meshes[lev].array("xyz") @ np.array([0.3, -0.2, 0.5]))
+    dw = ctx.to_device(w)
+    cases = [
+        (dict(c_s=1.0), dict(c_s=1.0)),
+        (dict(c_m=1.0), dict(c_m=1.0)),
+        (dict(c_s=0.5, potential=(kb.POT_COULOMB, ATOMS)), dict(c_s=0.5, potential=(0, ATOMS))),
+        (dict(potential=(kb.POT_GAUSSIAN, GAUSS)), dict(potential=(1, GAUSS))),
+        (dict(w=dw), dict(w=w)),
+    ]
+    for gpu_kw, orc_kw in cases:
+        L.assemble(kb.MAT_USER0, **gpu_kw)
+        op = orc.operator(lev, **orc_kw)
+        A = csr_of_oracle(op)
+        assert np.array_equal(L.index("ii_ptr"), A.indptr), gpu_kw
+        assert np.array_equal(L.index("ii_col"), A.indices), gpu_kw
+        g = L.values(kb.MAT_USER0)
+        scale = np.abs(A.data).max()
+        assert np.abs(g - A.data).max() <= 1e-13 * scale, gpu_kw
+
+
+def test_spmm_matches_oracle(ctx):
+    h, orc = hierarchy(adapt=1)
+    lev = h.n_levels - 1
+    L = kb.Level(ctx, h, lev)
+    L.assemble(kb.MAT_USER0, c_s=0.5, c_m=0.5, potential=(kb.POT_GAUSSIAN, GAUSS))
+    op = orc.operator(lev, c_s=0.5, c_m=0.5, potential=(1, GAUSS))
+    rng = np.random.default_rng(1)
+    for N in [1, 2, 5, 16, 21, 64, 120]:
+        ld = N if N == 1 else N + (N & 1)
+        X = np.zeros((L.ni, ld))
+        X[:, :N] = rng.standard_normal((L.ni, N))
+        dX, dY = ctx.to_device(X), ctx.empty((L.ni, ld))
+        L.spmm(kb.MAT_USER0, dX, dY, N, ld, ld)
+        Y = dY.download()[:, :N]
+        ref = np.stack([op.spmv(X[:, j]) for j in range(N)], 1)
+        assert np.abs(Y - ref).max() <= 1e-12 * np.abs(ref).max(), N
+
+
+@pytest.mark.parametrize("N", [1, 4, 16])
+def test_cg_matches_oracle_jacobi(ctx, N):
+    h, orc = hierarchy(adapt=1)
+    lev = h.n_levels - 1
+    L = kb.Level(ctx, h, lev)
+    L.assemble(kb.MAT_USER0, c_s=0.5, c_m=2.0, potential=(kb.POT_COULOMB, ATOMS))
+    op = orc.operator(lev, c_s=0.5, c_m=2.0, potential=(0, ATOMS), precond=1)
+    rng = np.random.default_rng(2)
+    B = rng.standard_normal((L.ni, N))
+    if N > 1:
+        B[:, 1] = 0.0  # zero right-hand side: converged with 0 iterations (proj/src/solver.cpp:62-66)
+    X, st = L.cg_solve_host(kb.MAT_USER0, B, N, opts=L.cg_options(tol=1e-10))
+    Xo, sto = op.pcg(B, tol=1e-10)
+    for j in range(N):
+        assert st[j].converged == sto[j]["converged"]
+        assert abs(st[j].iterations - sto[j]["iterations"]) <= 1
+    assert np.linalg.norm(X - Xo) <= 1e-9 * np.linalg.norm(Xo)
+    if N > 1:
+        assert st[1].iterations == 0 and st[1].converged and np.all(X[:, 1] == 0.0)
+
+
+def test_cg_breakdown_on_indefinite_operator(ctx):
+    """a_op alone is indefinite (bound states): CG stops with breakdown like the reference."""
+    h, orc = hierarchy(levels=1)
+    L = kb.Level(ctx, h, 1)
+    L.assemble(kb.MAT_USER0, c_s=0.5, potential=(kb.POT_COULOMB, 30 * ATOMS[:1]))
+    op = orc.operator(1, c_s=0.5, potential=(0, 30 * ATOMS[:1]), precond=1)
+    rng = np.random.default_rng(4)
+    B = rng.standard_normal((L.ni, 2))
+    X, st = L.cg_solve_host(kb.MAT_USER0, B, 2, opts=L.cg_options(tol=1e-10, max_iterations=3000))
+    Xo, sto = op.pcg(B, tol=1e-10, maxit=3000)
+    for j in range(2):
+        assert st[j].breakdown == sto[j]["breakdown"]
+        assert st[j].converged == sto[j]["converged"]
+        if sto[j]["breakdown"]:
+            assert st[j].iterations == sto[j]["iterations"]
+
+
+def test_cg_fixed_iterations_and_shifts(ctx):
+    h, orc = hierarchy()
+    L = kb.Level(ctx, h, 1)
+    L.assemble(kb.MAT_AOP, c_s=0.5, potential=(kb.POT_COULOMB, ATOMS))
+    L.assemble(kb.MAT_M, c_m=1.0)
+    rng = np.random.default_rng(6)
+    N = 3
+    B = rng.standard_normal((L.ni, N + 1))[:, :N]
+    sig = np.array([1.0, 2.5, 4.0])
+    X, st = L.cg_solve_host(kb.MAT_AOP, np.ascontiguousarray(np.pad(B, ((0, 0), (0, 1)))), N, ld=4,
+                            opts=L.cg_options(tol=1e-11), shift_mat=kb.MAT_M, sigma=sig)
+    for j in range(N):
+        op = orc.operator(1, c_s=0.5, potential=(0, ATOMS), c_m=sig[j], precond=1)
+        xo, so = op.pcg(B[:, j], tol=1e-11)
+        assert st[j].converged and so[0]["converged"]
+        assert np.linalg.norm(X[:, j] - xo[:, 0]) <= 1e-9 * np.linalg.norm(xo)
+    # fixed-iteration benchmark mode runs exactly k iterations, no stopping test
+    X, st = L.cg_solve_host(kb.MAT_AOP, np.ascontiguousarray(np.pad(B, ((0, 0), (0, 1)))), N, ld=4,
+                            opts=L.cg_options(fixed_iterations=7), shift_mat=kb.MAT_M, sigma=sig)
+    assert all(s.iterations == 7 for s in st)
+    op = orc.operator(1, c_s=0.5, potential=(0, ATOMS), c_m=sig[0], precond=1)
+    xo, so = op.pcg(B[:, 0], fixed=7)
+    assert np.linalg.norm(X[:, 0] - xo[:, 0]) <= 1e-11 * np.linalg.norm(xo)
