@@ -12,7 +12,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from . import _native as N
+from . import _native as _N
 from ._native import check, lib
 
 MAT_S, MAT_M, MAT_AOP, MAT_USER0 = 0, 1, 2, 8
@@ -20,11 +20,11 @@ POT_COULOMB, POT_GAUSSIAN = 0, 1
 
 
 def _dp(a: np.ndarray):
-    return a.ctypes.data_as(N.DP)
+    return a.ctypes.data_as(_N.DP)
 
 
 def _ip(a: np.ndarray):
-    return a.ctypes.data_as(N.IP)
+    return a.ctypes.data_as(_N.IP)
 
 
 # ----------------------------------------------------------------------------- mesh
@@ -269,8 +269,8 @@ class Level:
         check(lib.ksb_spmm(self._h, mat, X.ptr, int(N), int(ldx or N), Y.ptr, int(ldy or N)))
 
     @staticmethod
-    def cg_options(tol=1e-9, max_iterations=20000, fixed_iterations=0, check_every=8) -> N.CgOpts:
-        o = N.CgOpts()
+    def cg_options(tol=1e-9, max_iterations=20000, fixed_iterations=0, check_every=8) -> _N.CgOpts:
+        o = _N.CgOpts()
         check(lib.ksb_cg_defaults(C.byref(o)))
         o.tol = tol
         o.max_iterations = max_iterations
@@ -282,7 +282,7 @@ class Level:
                  shift_mat: int = -1, sigma=None):
         """Multi-RHS PCG on interior blocks; returns per-column SolveStats."""
         opts = opts or self.cg_options()
-        st = (N.CgStats * N_cols(N))()
+        st = (_N.CgStats * N_cols(N))()
         sig = np.ascontiguousarray(sigma, np.float64) if sigma is not None else None
         check(lib.ksb_cg_solve(self._h, mat, shift_mat, _dp(sig) if sig is not None else None, B.ptr, X.ptr,
                                int(N), int(ld or N), C.byref(opts), st))
@@ -295,7 +295,7 @@ class Level:
         ld = int(ld or N)
         B = np.ascontiguousarray(B, np.float64)
         X = out if out is not None else np.empty_like(B)
-        st = (N.CgStats * N_cols(N))()
+        st = (_N.CgStats * N_cols(N))()
         sig = np.ascontiguousarray(sigma, np.float64) if sigma is not None else None
         check(lib.ksb_cg_solve_host(self._h, mat, shift_mat, _dp(sig) if sig is not None else None,
                                     B.ctypes.data_as(C.c_void_p), X.ctypes.data_as(C.c_void_p), int(N), ld,

@@ -371,7 +371,7 @@ int ksb_level_create(ksb_ctx* c, const ksb_hier* h, int level, ksb_level** out) 
 
 void ksb_level_destroy(ksb_level* l) {
     if (!l) return;
-    cudaStreamSynchronize(l->L.ctx->stream);
+    cudaDeviceSynchronize();  // the owning context may already be gone; never touch it here
     delete l;
 }
 

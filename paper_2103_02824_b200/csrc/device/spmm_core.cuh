@@ -77,17 +77,32 @@ __device__ __forceinline__ void row_product(int rb, int re, const int32_t* __res
             if (SHIFT) mb = __ldg(B + k);
         }
         const int cnt = min(G, re - k0);
-        for (int s = 0; s < cnt; ++s) {
-            const int j = __shfl_sync(gmask, mc, gbase + s);
-            const double a = __shfl_sync(gmask, ma, gbase + s);
-            double b = 0.0;
-            if (SHIFT) b = __shfl_sync(gmask, mb, gbase + s);
-            double x[CPL];
-            load_cols<CPL>(X + size_t(j) * ldx + c0, c0, N, x);
+        // gathers of a sub-batch are all issued before any FMA consumes them (memory-level parallelism)
+        constexpr int UB = (G < 16 / CPL) ? G : 16 / CPL;
 #pragma unroll
-            for (int q = 0; q < CPL; ++q) {
-                acc[q] = fma(a, x[q], acc[q]);
-                if (SHIFT) accB[q] = fma(b, x[q], accB[q]);
+        for (int s0 = 0; s0 < G; s0 += UB) {
+            if (s0 >= cnt) break;
+            double x[UB][CPL];
+#pragma unroll
+            for (int u = 0; u < UB; ++u) {
+                const int j = __shfl_sync(gmask, mc, gbase + s0 + u);
+                if (s0 + u < cnt) {
+                    load_cols<CPL>(X + size_t(j) * ldx + c0, c0, N, x[u]);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < CPL; ++q) x[u][q] = 0.0;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < UB; ++u) {
+                const double a = __shfl_sync(gmask, ma, gbase + s0 + u);
+                double b = 0.0;
+                if (SHIFT) b = __shfl_sync(gmask, mb, gbase + s0 + u);
+#pragma unroll
+                for (int q = 0; q < CPL; ++q) {
+                    acc[q] = fma(a, x[u][q], acc[q]);
+                    if (SHIFT) accB[q] = fma(b, x[u][q], accB[q]);
+                }
             }
         }
     }

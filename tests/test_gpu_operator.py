@@ -120,25 +120,30 @@ def test_cg_breakdown_on_indefinite_operator(ctx):
 
 
 def test_cg_fixed_iterations_and_shifts(ctx):
+    """Per-column shifted operators A + sigma_j M (the level-shift ladder's dual-value SpMM)."""
     h, orc = hierarchy()
     L = kb.Level(ctx, h, 1)
     L.assemble(kb.MAT_AOP, c_s=0.5, potential=(kb.POT_COULOMB, ATOMS))
     L.assemble(kb.MAT_M, c_m=1.0)
     rng = np.random.default_rng(6)
     N = 3
-    B = rng.standard_normal((L.ni, N + 1))[:, :N]
-    sig = np.array([1.0, 2.5, 4.0])
-    X, st = L.cg_solve_host(kb.MAT_AOP, np.ascontiguousarray(np.pad(B, ((0, 0), (0, 1)))), N, ld=4,
-                            opts=L.cg_options(tol=1e-11), shift_mat=kb.MAT_M, sigma=sig)
+    B = rng.standard_normal((L.ni, N))
+    Bp = np.ascontiguousarray(np.pad(B, ((0, 0), (0, 1))))  # ld = 4 > N
+    sig = np.array([3.0, 5.0, 8.0])  # lowest pencil eigenvalue is about -2.18: all shifted operators SPD
+    X, st = L.cg_solve_host(kb.MAT_AOP, Bp, N, ld=4, opts=L.cg_options(tol=1e-11), shift_mat=kb.MAT_M, sigma=sig)
     for j in range(N):
         op = orc.operator(1, c_s=0.5, potential=(0, ATOMS), c_m=sig[j], precond=1)
         xo, so = op.pcg(B[:, j], tol=1e-11)
         assert st[j].converged and so[0]["converged"]
+        assert abs(st[j].iterations - so[0]["iterations"]) <= 1
         assert np.linalg.norm(X[:, j] - xo[:, 0]) <= 1e-9 * np.linalg.norm(xo)
-    # fixed-iteration benchmark mode runs exactly k iterations, no stopping test
-    X, st = L.cg_solve_host(kb.MAT_AOP, np.ascontiguousarray(np.pad(B, ((0, 0), (0, 1)))), N, ld=4,
-                            opts=L.cg_options(fixed_iterations=7), shift_mat=kb.MAT_M, sigma=sig)
-    assert all(s.iterations == 7 for s in st)
-    op = orc.operator(1, c_s=0.5, potential=(0, ATOMS), c_m=sig[0], precond=1)
-    xo, so = op.pcg(B[:, 0], fixed=7)
-    assert np.linalg.norm(X[:, 0] - xo[:, 0]) <= 1e-11 * np.linalg.norm(xo)
+    # fixed-iteration benchmark mode runs exactly k iterations, no stopping test (indefinite shift included)
+    sig = np.array([1.0, 2.5, 4.0])
+    for k in (1, 2, 7):
+        X, st = L.cg_solve_host(kb.MAT_AOP, Bp, N, ld=4, opts=L.cg_options(fixed_iterations=k), shift_mat=kb.MAT_M,
+                                sigma=sig)
+        assert all(s.iterations == k for s in st)
+        for j in range(N):
+            op = orc.operator(1, c_s=0.5, potential=(0, ATOMS), c_m=sig[j], precond=1)
+            xo, so = op.pcg(B[:, j], fixed=k)
+            assert np.linalg.norm(X[:, j] - xo[:, 0]) <= 1e-10 * np.linalg.norm(xo), (k, j)
