@@ -156,6 +156,82 @@ int ksb_cg_solve(ksb_level* l, int mat, int shift_mat, const double* h_sigma, co
 int ksb_cg_solve_host(ksb_level* l, int mat, int shift_mat, const double* h_sigma, const double* h_B,
                       double* h_X, int N, int ld, const ksb_cg_opts* o, ksb_cg_stats* h_stats);
 
+
+/* ---------------- the correction step (one outer iteration, proj/src/driver.cpp:106-150) ----------------
+ * Orbitals are interior blocks (ni x ld, row-major): the correction algorithm keeps them in the
+ * zero-trace space, so boundary values are structurally zero. Potentials (w, v_xc, rho) are
+ * full-length nodal vectors (n). */
+typedef struct {
+    double tol_linear;  /* RunConfig::tol_linear (1e-9) */
+    double tol_inner;   /* RunConfig::tol_inner (1e-8) */
+    double score_floor; /* RunConfig::score_floor (1e-8) */
+    int max_inner;      /* RunConfig::max_inner (400) */
+    int nev_pad;        /* RunConfig::nev_scan_pad (4) */
+    int check_every;    /* CG convergence poll interval */
+} ksb_step_opts;
+
+typedef struct {
+    int inner_iterations;
+    int hartree_iterations;
+    double delta; /* H1 norm of the density change (the outer stopping quantity) */
+    double ms_bvp, ms_hartree, ms_project, ms_inner, ms_total;
+    int64_t cg_iterations; /* summed over orbitals and shift attempts */
+} ksb_step_log;
+
+#define KSB_XC_NONE 0
+#define KSB_XC_XALPHA 1
+#define KSB_XC_LDA 2
+
+int ksb_step_defaults(ksb_step_opts* o);
+/* model::MolecularSystem + the mode switches (proj/include/ksafem/ks_model.hpp:26-34,
+ * runconfig.hpp:39-46). atoms: (Z, x, y, z) per nucleus. */
+int ksb_system_set(ksb_level* l, const double* h_atoms, int n_atoms, int n_pairs, double occupancy, int xc_kind,
+                   double alpha, double exchange_exponent, int hartree_on, int xc_on);
+/* make_level_ops (proj/src/driver.cpp:35-47): S, M, a_op, plus the coarse blocks M_H, C_H */
+int ksb_level_ops(ksb_level* l);
+/* one outer iteration: lambda (N, host) and Phi / w (device) are updated in place.
+ * h_attempts[i] = -1 when the unshifted solve converged, else the ladder rung; h_iters = CG iterations. */
+int ksb_correction_step(ksb_level* l, const ksb_step_opts* o, double* h_lambda, double* d_Phi, int ld, double* d_w,
+                        ksb_step_log* log, int* h_attempts, int* h_iters);
+/* same with host buffers (H2D/D2H inside the call): the e2e entry point */
+int ksb_correction_step_host(ksb_level* l, const ksb_step_opts* o, double* h_lambda, double* h_Phi, int ld,
+                             double* h_w, ksb_step_log* log, int* h_attempts, int* h_iters);
+
+/* pieces of the step, for parity checks against the reference's functions */
+/* model::density + xc_potential_field (proj/src/ks_model.cpp:43-52,101-105); d_vxc may be NULL */
+int ksb_density_xc(ksb_level* l, const double* d_Phi, int N, int ld, double* d_rho, double* d_vxc);
+/* hartree::compute_moments (proj/src/hartree.cpp:15-63): q, centre[3], dipole[3], quadrupole[9] */
+int ksb_moments(ksb_level* l, const double* d_rho, double h_out[16]);
+/* hartree::boundary_values at the boundary vertices, boundary numbering (proj/src/hartree.cpp:76-82) */
+int ksb_boundary_values(ksb_level* l, const double h_moments[16], double* d_bcb);
+/* hartree::squared_density_load restricted to interior rows (proj/src/hartree.cpp:108-129) */
+int ksb_sqload(ksb_level* l, const double* d_Phi, int N, int ld, double* d_out_int);
+/* corr::bvp_hartree (proj/src/correction.cpp:67-75): full-length w with boundary data d_bcb */
+int ksb_hartree_solve(ksb_level* l, const double* d_Phi, int N, int ld, const double* d_bcb, double tol,
+                      double* d_w_full, int* h_iters);
+/* OuterOperator + bvp_orbital for every orbital (proj/src/correction.cpp:15-61) */
+int ksb_outer_solve(ksb_level* l, const ksb_step_opts* o, const double* d_what_full, const double* d_vxc_full,
+                    const double* h_lambda, const double* d_Phi, int ld, double* d_PhiT, int* h_attempts,
+                    int* h_iters, double* h_min_diag);
+/* corr::prepare_blocks (proj/src/correction.cpp:113-212): w_tilde0 (zero trace) and the lift ell, full length */
+int ksb_prepare_blocks(ksb_level* l, const double* d_PhiT, int ld, const double* d_wt_full, const double* d_ell_full,
+                       const double* d_vxc_full);
+/* ledger access, codes as the oracle: 0 A_H1 1 A_H3 2 A_H4 3 M_H 4 C_H (nh x nh, row-major) 5 d_Hh
+ * 6 lift_load 7 [zeta, lift_load0] 10 A_h4 (N nh nh) 11 b_H1 12 b_H3 13 b_H4 14 rhs 15 c_Hh 16 d_phi (N nh)
+ * 17 beta1 18 beta3 19 beta4 20 gamma 21 zeta_phi (N) */
+int ksb_blocks_get(ksb_level* l, int what, double* h_dst);
+/* corr::inner_scf from the pure augmentation state (proj/src/correction.cpp:279-368) */
+int ksb_inner_scf(ksb_level* l, const ksb_step_opts* o, const double* h_lambda, double* h_lambda_out,
+                  double* h_phi_H, double* h_theta2, double* h_w_H, double* h_theta1, int* h_iterations,
+                  double* h_history, int hist_cap);
+/* corr::expand of the last inner state (proj/src/correction.cpp:370-381) */
+int ksb_expand(ksb_level* l, const double* d_PhiT, int ld, const double* d_wt_full, const double* d_bcb,
+               double* d_Phi, double* d_w_full);
+/* l2_norm^2, h1_seminorm^2, h1_norm of a full-length nodal function (proj/src/assembly.cpp:251-287) */
+int ksb_norms(ksb_level* l, const double* d_f_full, double h_out[3]);
+/* model::total_energy (proj/src/ks_model.cpp:107-143): kinetic, external, hartree, xc, total */
+int ksb_energy(ksb_level* l, const double* d_Phi, int N, int ld, const double* d_w_full, double h_out[5]);
+
 #ifdef __cplusplus
 }
 #endif

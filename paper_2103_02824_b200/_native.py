@@ -38,6 +38,19 @@ class CgStats(C.Structure):
     _fields_ = [("iterations", I), ("relative_residual", D), ("converged", I), ("breakdown", I)]
 
 
+class StepOpts(C.Structure):
+    _fields_ = [("tol_linear", D), ("tol_inner", D), ("score_floor", D), ("max_inner", I), ("nev_pad", I),
+                ("check_every", I)]
+
+
+class StepLog(C.Structure):
+    _fields_ = [("inner_iterations", I), ("hartree_iterations", I), ("delta", D), ("ms_bvp", D), ("ms_hartree", D),
+                ("ms_project", D), ("ms_inner", D), ("ms_total", D), ("cg_iterations", I64)]
+
+
+SOP = C.POINTER(StepOpts)
+SLP = C.POINTER(StepLog)
+
 # name -> (restype, argtypes); mirrors include/ksb.h exactly (checked by tests/test_abi.py)
 PROTOTYPES = {
     "ksb_last_error": (CP, []),
@@ -77,6 +90,23 @@ PROTOTYPES = {
     "ksb_cg_defaults": (I, [C.POINTER(CgOpts)]),
     "ksb_cg_solve": (I, [P, I, I, DP, P, P, I, I, C.POINTER(CgOpts), C.POINTER(CgStats)]),
     "ksb_cg_solve_host": (I, [P, I, I, DP, P, P, I, I, C.POINTER(CgOpts), C.POINTER(CgStats)]),
+    "ksb_step_defaults": (I, [SOP]),
+    "ksb_system_set": (I, [P, DP, I, I, D, I, D, D, I, I]),
+    "ksb_level_ops": (I, [P]),
+    "ksb_correction_step": (I, [P, SOP, DP, P, I, P, SLP, IP, IP]),
+    "ksb_correction_step_host": (I, [P, SOP, DP, P, I, P, SLP, IP, IP]),
+    "ksb_density_xc": (I, [P, P, I, I, P, P]),
+    "ksb_moments": (I, [P, P, DP]),
+    "ksb_boundary_values": (I, [P, DP, P]),
+    "ksb_sqload": (I, [P, P, I, I, P]),
+    "ksb_hartree_solve": (I, [P, P, I, I, P, D, P, IP]),
+    "ksb_outer_solve": (I, [P, SOP, P, P, DP, P, I, P, IP, IP, DP]),
+    "ksb_prepare_blocks": (I, [P, P, I, P, P, P]),
+    "ksb_blocks_get": (I, [P, I, DP]),
+    "ksb_inner_scf": (I, [P, SOP, DP, DP, DP, DP, DP, DP, IP, DP, I]),
+    "ksb_expand": (I, [P, P, I, P, P, P, P]),
+    "ksb_norms": (I, [P, P, DP]),
+    "ksb_energy": (I, [P, P, I, I, P, DP]),
 }
 
 for _name, (_res, _args) in PROTOTYPES.items():

@@ -303,5 +303,133 @@ class Level:
         return X, [SolveStats(s.iterations, s.relative_residual, bool(s.converged), bool(s.breakdown)) for s in st]
 
 
+    # ------------------------------------------------------------------ correction step
+    XC = {"none": 0, "x_alpha": 1, "lda": 2}
+
+    def set_system(self, atoms, n_pairs=1, occupancy=2.0, xc="lda", alpha=0.77298, exchange_exponent=1.0 / 3.0,
+                   hartree=True, xc_on=True):
+        """model::MolecularSystem + mode switches (proj/include/ksafem/ks_model.hpp:26-34)."""
+        a = np.ascontiguousarray(np.asarray(atoms, np.float64).reshape(-1, 4))
+        check(lib.ksb_system_set(self._h, _dp(a.reshape(-1)), a.shape[0], int(n_pairs), float(occupancy),
+                                 self.XC[xc], float(alpha), float(exchange_exponent), int(hartree), int(xc_on)))
+        self.N = int(n_pairs)
+
+    def level_ops(self):
+        """make_level_ops (proj/src/driver.cpp:35-47)."""
+        check(lib.ksb_level_ops(self._h))
+
+    @staticmethod
+    def step_options(**kw) -> _N.StepOpts:
+        o = _N.StepOpts()
+        check(lib.ksb_step_defaults(C.byref(o)))
+        for k, v in kw.items():
+            setattr(o, k, v)
+        return o
+
+    @staticmethod
+    def _log(lg, att, its):
+        return {"inner_iterations": lg.inner_iterations, "hartree_iterations": lg.hartree_iterations,
+                "delta": lg.delta, "ms_bvp": lg.ms_bvp, "ms_hartree": lg.ms_hartree, "ms_project": lg.ms_project,
+                "ms_inner": lg.ms_inner, "ms_total": lg.ms_total, "cg_iterations": int(lg.cg_iterations),
+                "attempts": att.tolist(), "iterations": its.tolist()}
+
+    def correction_step(self, lambdas: np.ndarray, Phi: DeviceArray, w: DeviceArray, ld: int | None = None, **opts):
+        """One outer iteration (proj/src/driver.cpp:106-150) on device-resident state; lambdas updated in place."""
+        o = self.step_options(**opts)
+        lg = _N.StepLog()
+        att = np.zeros(self.N, np.int32)
+        its = np.zeros(self.N, np.int32)
+        check(lib.ksb_correction_step(self._h, C.byref(o), _dp(lambdas), Phi.ptr, int(ld or Phi.shape[1]), w.ptr,
+                                      C.byref(lg), _ip(att), _ip(its)))
+        return self._log(lg, att, its)
+
+    def correction_step_host(self, lambdas: np.ndarray, Phi: np.ndarray, w: np.ndarray, **opts):
+        o = self.step_options(**opts)
+        lg = _N.StepLog()
+        att = np.zeros(self.N, np.int32)
+        its = np.zeros(self.N, np.int32)
+        check(lib.ksb_correction_step_host(self._h, C.byref(o), _dp(lambdas), Phi.ctypes.data_as(C.c_void_p),
+                                           int(Phi.shape[1]), w.ctypes.data_as(C.c_void_p), C.byref(lg), _ip(att),
+                                           _ip(its)))
+        return self._log(lg, att, its)
+
+    def density_xc(self, Phi: DeviceArray, rho: DeviceArray, vxc: DeviceArray | None = None, N=None, ld=None):
+        check(lib.ksb_density_xc(self._h, Phi.ptr, int(N or self.N), int(ld or Phi.shape[1]), rho.ptr,
+                                 vxc.ptr if vxc is not None else None))
+
+    def moments(self, rho: DeviceArray) -> np.ndarray:
+        out = np.empty(16)
+        check(lib.ksb_moments(self._h, rho.ptr, _dp(out)))
+        return out
+
+    def boundary_values(self, moments: np.ndarray, bcb: DeviceArray):
+        m = np.ascontiguousarray(moments, np.float64)
+        check(lib.ksb_boundary_values(self._h, _dp(m), bcb.ptr))
+
+    def sqload(self, Phi: DeviceArray, out: DeviceArray, N=None, ld=None):
+        check(lib.ksb_sqload(self._h, Phi.ptr, int(N or self.N), int(ld or Phi.shape[1]), out.ptr))
+
+    def hartree_solve(self, Phi: DeviceArray, bcb: DeviceArray, w: DeviceArray, tol=1e-9, N=None, ld=None):
+        it = C.c_int()
+        check(lib.ksb_hartree_solve(self._h, Phi.ptr, int(N or self.N), int(ld or Phi.shape[1]), bcb.ptr, float(tol),
+                                    w.ptr, C.byref(it)))
+        return it.value
+
+    def outer_solve(self, w_hat: DeviceArray, vxc: DeviceArray, lambdas, Phi: DeviceArray, PhiT: DeviceArray, **opts):
+        o = self.step_options(**opts)
+        lam = np.ascontiguousarray(lambdas, np.float64)
+        att = np.zeros(self.N, np.int32)
+        its = np.zeros(self.N, np.int32)
+        md = C.c_double()
+        check(lib.ksb_outer_solve(self._h, C.byref(o), w_hat.ptr, vxc.ptr, _dp(lam), Phi.ptr, int(Phi.shape[1]),
+                                  PhiT.ptr, _ip(att), _ip(its), C.byref(md)))
+        return att, its, md.value
+
+    def prepare_blocks(self, PhiT: DeviceArray, wt: DeviceArray, ell: DeviceArray, vxc: DeviceArray):
+        check(lib.ksb_prepare_blocks(self._h, PhiT.ptr, int(PhiT.shape[1]), wt.ptr, ell.ptr, vxc.ptr))
+
+    BLOCKS = {"A_H1": 0, "A_H3": 1, "A_H4": 2, "M_H": 3, "C_H": 4, "d_Hh": 5, "lift_load": 6, "scalars": 7,
+              "A_h4": 10, "b_H1": 11, "b_H3": 12, "b_H4": 13, "rhs": 14, "c_Hh": 15, "d_phi": 16, "beta1": 17,
+              "beta3": 18, "beta4": 19, "gamma": 20, "zeta_phi": 21}
+
+    def blocks(self, name: str) -> np.ndarray:
+        w = self.BLOCKS[name]
+        nh, N = self.nH, self.N
+        shape = {0: (nh, nh), 1: (nh, nh), 2: (nh, nh), 3: (nh, nh), 4: (nh, nh), 5: (nh,), 6: (nh,), 7: (2,),
+                 10: (N, nh, nh)}.get(w, (N, nh) if w < 17 else (N,))
+        out = np.empty(int(np.prod(shape)))
+        check(lib.ksb_blocks_get(self._h, w, _dp(out)))
+        return out.reshape(shape)
+
+    def inner_scf(self, lambdas, **opts):
+        o = self.step_options(**opts)
+        N, nh = self.N, self.nH
+        lam0 = np.ascontiguousarray(lambdas, np.float64)
+        lam = np.empty(N)
+        phi = np.empty((N, nh))
+        th2 = np.empty(N)
+        wH = np.empty(nh)
+        th1 = C.c_double()
+        it = C.c_int()
+        hist = np.zeros(o.max_inner)
+        check(lib.ksb_inner_scf(self._h, C.byref(o), _dp(lam0), _dp(lam), _dp(phi), _dp(th2), _dp(wH), C.byref(th1),
+                                C.byref(it), _dp(hist), o.max_inner))
+        return dict(lambda_=lam, phi_H=phi, theta2=th2, w_H=wH, theta1=th1.value, iterations=it.value,
+                    history=hist[:it.value])
+
+    def expand(self, PhiT: DeviceArray, wt: DeviceArray, bcb: DeviceArray, Phi: DeviceArray, w: DeviceArray):
+        check(lib.ksb_expand(self._h, PhiT.ptr, int(PhiT.shape[1]), wt.ptr, bcb.ptr, Phi.ptr, w.ptr))
+
+    def norms(self, f: DeviceArray) -> np.ndarray:
+        out = np.empty(3)
+        check(lib.ksb_norms(self._h, f.ptr, _dp(out)))
+        return out
+
+    def energy(self, Phi: DeviceArray, w: DeviceArray, N=None, ld=None) -> np.ndarray:
+        out = np.empty(5)
+        check(lib.ksb_energy(self._h, Phi.ptr, int(N or self.N), int(ld or Phi.shape[1]), w.ptr, _dp(out)))
+        return out
+
+
 def N_cols(n: int) -> int:
     return max(1, int(n))

@@ -4,6 +4,7 @@
 #include <new>
 
 #include "device/cg.cuh"
+#include "device/correction.cuh"
 #include "device/level.cuh"
 #include "ksb.h"
 
@@ -21,6 +22,11 @@ struct ksb_ctx {
 struct ksb_level {
     ksb_ctx* owner = nullptr;
     ksb::Level L;
+    std::unique_ptr<ksb::Corrector> K;
+    ksb::Corrector& corr() {
+        if (!K) K = std::make_unique<ksb::Corrector>();
+        return *K;
+    }
 };
 
 namespace ksb {
@@ -359,6 +365,17 @@ int ksb_level_create(ksb_ctx* c, const ksb_hier* h, int level, ksb_level** out) 
             L.ancestor.upload(cx, T.ancestor);
             L.anc_ptr.upload(cx, T.anc_ptr);
             L.anc_tets.upload(cx, T.anc_tets);
+            L.vinc_ptr.upload(cx, T.vinc_ptr);
+            L.vinc.upload(cx, T.vinc);
+            L.cinc_ptr.upload(cx, T.cinc_ptr);
+            L.cinc.upload(cx, T.cinc);
+            L.ctets.upload(cx, T.coarse->mesh->tets);
+            L.ciidx.upload(cx, T.coarse->iidx);
+            L.cxyz.upload(cx, T.coarse->mesh->xyz);
+            for (int d = 0; d < 3; ++d) {
+                L.box_lo[d] = M.lo[d];
+                L.box_hi[d] = M.hi[d];
+            }
             L.flag.alloc(4);
             KSB_CUDA_CHECK(cudaStreamSynchronize(cx.stream));
         } catch (...) {
@@ -510,6 +527,314 @@ int ksb_cg_solve_host(ksb_level* l, int mat, int shift_mat, const double* h_sigm
         run_cg(l, mat, shift_mat, h_sigma, dB.p, dX.p, N, ld, o, h_stats);
         KSB_CUDA_CHECK(cudaMemcpyAsync(h_X, dX.p, bytes, cudaMemcpyDeviceToHost, c.stream));
         KSB_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    });
+}
+
+
+// ---------------- correction step ----------------
+static ksb::StepOptions step_opts(const ksb_step_opts* o) {
+    ksb::StepOptions so;
+    if (o) {
+        so.tol_linear = o->tol_linear;
+        so.tol_inner = o->tol_inner;
+        so.score_floor = o->score_floor;
+        so.max_inner = o->max_inner;
+        so.nev_pad = o->nev_pad;
+        so.check_every = o->check_every;
+    }
+    return so;
+}
+
+static void fill_log(const ksb::StepLog& lg, ksb_step_log* log, int* att, int* its) {
+    if (log) {
+        log->inner_iterations = lg.inner_iterations;
+        log->hartree_iterations = lg.hartree_iterations;
+        log->delta = lg.delta;
+        log->ms_bvp = lg.ms_bvp;
+        log->ms_hartree = lg.ms_hartree;
+        log->ms_project = lg.ms_project;
+        log->ms_inner = lg.ms_inner;
+        log->ms_total = lg.ms_total;
+        log->cg_iterations = lg.cg_iterations;
+    }
+    for (size_t i = 0; i < lg.attempts.size(); ++i) {
+        if (att) att[i] = lg.attempts[i];
+        if (its) its[i] = lg.iterations[i];
+    }
+}
+
+static ksb::Corrector& ready(ksb_level* l) {
+    need(l != nullptr, "null level");
+    auto& K = l->corr();
+    if (!K.sys.set) ksb::raise(KSB_INVALID_ARGUMENT, "call ksb_system_set first");
+    if (!K.ops_ready) ksb::level_ops(l->L, K);
+    return K;
+}
+
+int ksb_step_defaults(ksb_step_opts* o) {
+    return guard([&] {
+        need(o, "null argument");
+        o->tol_linear = 1e-9;
+        o->tol_inner = 1e-8;
+        o->score_floor = 1e-8;
+        o->max_inner = 400;
+        o->nev_pad = 4;
+        o->check_every = 8;
+    });
+}
+
+int ksb_system_set(ksb_level* l, const double* atoms, int n_atoms, int n_pairs, double occ, int xc_kind, double alpha,
+                   double p_exch, int hartree_on, int xc_on) {
+    return guard([&] {
+        need(l && (n_atoms == 0 || atoms), "null argument");
+        if (n_pairs < 1 || n_pairs > 128) ksb::raise(KSB_INVALID_ARGUMENT, "n_pairs must be in [1, 128]");
+        if (!(occ > 0)) ksb::raise(KSB_INVALID_ARGUMENT, "occupancy must be positive");
+        if (xc_kind < 0 || xc_kind > 2) ksb::raise(KSB_INVALID_ARGUMENT, "unknown xc kind");
+        for (int a = 0; a < n_atoms; ++a)
+            if (!(atoms[4 * a] > 0)) ksb::raise(KSB_INVALID_ARGUMENT, "nuclear charge must be positive");
+        auto& K = l->corr();
+        K.sys.atoms.assign(atoms, atoms + 4 * n_atoms);
+        K.sys.N = n_pairs;
+        K.sys.occ = occ;
+        K.sys.xc = ksb::XcParams{xc_kind, alpha, p_exch};
+        K.sys.hartree_on = hartree_on != 0;
+        K.sys.xc_on = xc_on != 0 && xc_kind != 0;
+        K.sys.set = true;
+        K.ops_ready = false;
+    });
+}
+
+int ksb_level_ops(ksb_level* l) {
+    return guard([&] {
+        need(l, "null argument");
+        auto& K = l->corr();
+        if (!K.sys.set) ksb::raise(KSB_INVALID_ARGUMENT, "call ksb_system_set first");
+        ksb::level_ops(l->L, K);
+    });
+}
+
+int ksb_correction_step(ksb_level* l, const ksb_step_opts* o, double* h_lambda, double* d_Phi, int ld, double* d_w,
+                        ksb_step_log* log, int* att, int* its) {
+    return guard([&] {
+        auto& K = ready(l);
+        need(h_lambda && d_Phi && d_w, "null argument");
+        if (ld < K.sys.N || (K.sys.N > 1 && (ld & 1))) ksb::raise(KSB_INVALID_ARGUMENT, "bad ld");
+        ksb::StepLog lg;
+        ksb::correction_step(l->L, K, l->owner->cg, step_opts(o), h_lambda, d_Phi, ld, d_w, &lg);
+        fill_log(lg, log, att, its);
+    });
+}
+
+int ksb_correction_step_host(ksb_level* l, const ksb_step_opts* o, double* h_lambda, double* h_Phi, int ld,
+                             double* h_w, ksb_step_log* log, int* att, int* its) {
+    return guard([&] {
+        auto& K = ready(l);
+        need(h_lambda && h_Phi && h_w, "null argument");
+        auto& c = *l->L.ctx;
+        const int64_t nb = int64_t(l->L.ni) * ld;
+        auto& dP = l->owner->io_b;
+        auto& dW = l->owner->io_x;
+        if (dP.n < nb) dP.alloc(nb);
+        if (dW.n < l->L.n) dW.alloc(l->L.n);
+        KSB_CUDA_CHECK(cudaMemcpyAsync(dP.p, h_Phi, sizeof(double) * nb, cudaMemcpyHostToDevice, c.stream));
+        KSB_CUDA_CHECK(cudaMemcpyAsync(dW.p, h_w, sizeof(double) * l->L.n, cudaMemcpyHostToDevice, c.stream));
+        ksb::StepLog lg;
+        ksb::correction_step(l->L, K, l->owner->cg, step_opts(o), h_lambda, dP.p, ld, dW.p, &lg);
+        KSB_CUDA_CHECK(cudaMemcpyAsync(h_Phi, dP.p, sizeof(double) * nb, cudaMemcpyDeviceToHost, c.stream));
+        KSB_CUDA_CHECK(cudaMemcpyAsync(h_w, dW.p, sizeof(double) * l->L.n, cudaMemcpyDeviceToHost, c.stream));
+        KSB_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+        fill_log(lg, log, att, its);
+    });
+}
+
+int ksb_density_xc(ksb_level* l, const double* d_Phi, int N, int ld, double* d_rho, double* d_vxc) {
+    return guard([&] {
+        need(l && d_Phi && d_rho, "null argument");
+        auto& K = l->corr();
+        if (!K.sys.set) ksb::raise(KSB_INVALID_ARGUMENT, "call ksb_system_set first");
+        ksb::rho_vxc(l->L, d_Phi, N, ld, K.sys.occ, K.sys.xc, d_rho, d_vxc);
+    });
+}
+
+int ksb_moments(ksb_level* l, const double* d_rho, double out[16]) {
+    return guard([&] {
+        need(l && d_rho && out, "null argument");
+        auto& L = l->L;
+        const double ctr[3] = {0.5 * (L.box_lo[0] + L.box_hi[0]), 0.5 * (L.box_lo[1] + L.box_hi[1]),
+                               0.5 * (L.box_lo[2] + L.box_hi[2])};
+        const auto m = ksb::moments(L, d_rho, l->corr().phys, ctr);
+        out[0] = m.q;
+        for (int d = 0; d < 3; ++d) {
+            out[1 + d] = m.c[d];
+            out[4 + d] = m.dip[d];
+            for (int e = 0; e < 3; ++e) out[7 + 3 * d + e] = m.Q[d][e];
+        }
+    });
+}
+
+int ksb_boundary_values(ksb_level* l, const double mom[16], double* d_bcb) {
+    return guard([&] {
+        need(l && mom && d_bcb, "null argument");
+        ksb::Moments m{};
+        m.q = mom[0];
+        for (int d = 0; d < 3; ++d) {
+            m.c[d] = mom[1 + d];
+            m.dip[d] = mom[4 + d];
+            for (int e = 0; e < 3; ++e) m.Q[d][e] = mom[7 + 3 * d + e];
+        }
+        ksb::boundary_values(l->L, m, d_bcb);
+    });
+}
+
+int ksb_sqload(ksb_level* l, const double* d_Phi, int N, int ld, double* d_out) {
+    return guard([&] {
+        need(l && d_Phi && d_out, "null argument");
+        auto& K = l->corr();
+        if (!K.sys.set) ksb::raise(KSB_INVALID_ARGUMENT, "call ksb_system_set first");
+        ksb::sqload(l->L, d_Phi, N, ld, K.sys.occ, 1.0, d_out, K.phys);
+    });
+}
+
+int ksb_hartree_solve(ksb_level* l, const double* d_Phi, int N, int ld, const double* d_bcb, double tol,
+                      double* d_w_full, int* iters) {
+    return guard([&] {
+        auto& K = ready(l);
+        need(d_Phi && d_bcb && d_w_full, "null argument");
+        const int it = ksb::hartree_solve(l->L, K, l->owner->cg, d_Phi, N, ld, d_bcb, tol, d_w_full);
+        if (iters) *iters = it;
+    });
+}
+
+int ksb_outer_solve(ksb_level* l, const ksb_step_opts* o, const double* d_what, const double* d_vxc,
+                    const double* h_lambda, const double* d_Phi, int ld, double* d_PhiT, int* att, int* its,
+                    double* h_min_diag) {
+    return guard([&] {
+        auto& K = ready(l);
+        need(d_what && d_vxc && h_lambda && d_Phi && d_PhiT, "null argument");
+        const double md = ksb::outer_operator(l->L, K, d_what, d_vxc);
+        if (h_min_diag) *h_min_diag = md;
+        ksb::StepLog lg;
+        ksb::solve_orbitals(l->L, K, l->owner->cg, step_opts(o), h_lambda, d_Phi, ld, d_PhiT, ld, &lg);
+        fill_log(lg, nullptr, att, its);
+    });
+}
+
+int ksb_prepare_blocks(ksb_level* l, const double* d_PhiT, int ld, const double* d_wt, const double* d_ell,
+                       const double* d_vxc) {
+    return guard([&] {
+        auto& K = ready(l);
+        need(d_PhiT && d_wt && d_ell && d_vxc, "null argument");
+        ksb::project_blocks(l->L, d_PhiT, K.sys.N, ld, d_wt, d_ell, d_vxc, K.eext.p, K.proj);
+        KSB_CUDA_CHECK(cudaStreamSynchronize(l->L.ctx->stream));
+    });
+}
+
+int ksb_blocks_get(ksb_level* l, int what, double* dst) {
+    return guard([&] {
+        auto& K = ready(l);
+        need(dst, "null argument");
+        auto& P = K.proj;
+        auto& c = *l->L.ctx;
+        const int64_t nh = l->L.nH, nh2 = nh * nh, N = K.sys.N;
+        auto get = [&](const double* src, int64_t cnt) {
+            KSB_CUDA_CHECK(cudaMemcpyAsync(dst, src, sizeof(double) * cnt, cudaMemcpyDeviceToHost, c.stream));
+        };
+        auto getv = [&](int o) {  // per orbital vector o of 6
+            for (int64_t i = 0; i < N; ++i)
+                KSB_CUDA_CHECK(cudaMemcpyAsync(dst + i * nh, P.orb_vecs.p + (i * 6 + o) * nh, sizeof(double) * nh,
+                                               cudaMemcpyDeviceToHost, c.stream));
+        };
+        std::vector<double> sc;
+        switch (what) {
+            case 0: get(P.shared_mats.p, nh2); break;
+            case 1: get(P.shared_mats.p + nh2, nh2); break;
+            case 2: get(P.shared_mats.p + 2 * nh2, nh2); break;
+            case 3: get(K.coarse.MH.p, nh2); break;
+            case 4: get(K.coarse.CH.p, nh2); break;
+            case 5: get(P.shared_vecs.p, nh); break;
+            case 6: get(P.shared_vecs.p + nh, nh); break;
+            case 7: get(P.shared_scal.p, 2); break;
+            case 10: get(P.A_h4.p, N * nh2); break;
+            case 11: getv(0); break;
+            case 12: getv(1); break;
+            case 13: getv(2); break;
+            case 14: getv(5); break;
+            case 15: getv(3); break;
+            case 16: getv(4); break;
+            case 17: case 18: case 19: case 20: case 21: {
+                sc.resize(5 * N);
+                KSB_CUDA_CHECK(cudaMemcpyAsync(sc.data(), P.orb_scal.p, sizeof(double) * 5 * N, cudaMemcpyDeviceToHost,
+                                               c.stream));
+                KSB_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+                for (int64_t i = 0; i < N; ++i) dst[i] = sc[i * 5 + (what - 17)];
+                break;
+            }
+            default: ksb::raise(KSB_INVALID_ARGUMENT, "unknown block");
+        }
+        KSB_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    });
+}
+
+int ksb_inner_scf(ksb_level* l, const ksb_step_opts* o, const double* h_lambda, double* lam, double* phiH, double* th2,
+                  double* wH, double* th1, int* iters, double* hist, int hist_cap) {
+    return guard([&] {
+        auto& K = ready(l);
+        need(h_lambda, "null argument");
+        const auto so = step_opts(o);
+        ksb::InnerParams ip;
+        ip.tol = so.tol_inner;
+        ip.max_iterations = so.max_inner;
+        ip.score_floor = so.score_floor;
+        ip.nev_pad = so.nev_pad;
+        ip.hartree = K.sys.hartree_on;
+        ip.occ = K.sys.occ;
+        const auto st = ksb::inner_scf(l->L, K.coarse, K.proj, ip, h_lambda, K.inner, true);
+        auto& w = K.inner;
+        auto& c = *l->L.ctx;
+        const int N = K.sys.N, nh = l->L.nH, cur = w.cur;
+        if (lam) KSB_CUDA_CHECK(cudaMemcpyAsync(lam, w.lamv[cur].p, sizeof(double) * N, cudaMemcpyDeviceToHost, c.stream));
+        if (phiH) KSB_CUDA_CHECK(cudaMemcpyAsync(phiH, w.phi[cur].p, sizeof(double) * N * nh, cudaMemcpyDeviceToHost, c.stream));
+        if (th2) KSB_CUDA_CHECK(cudaMemcpyAsync(th2, w.th2[cur].p, sizeof(double) * N, cudaMemcpyDeviceToHost, c.stream));
+        if (wH) KSB_CUDA_CHECK(cudaMemcpyAsync(wH, w.wH[cur].p, sizeof(double) * nh, cudaMemcpyDeviceToHost, c.stream));
+        if (th1) KSB_CUDA_CHECK(cudaMemcpyAsync(th1, w.th1[cur].p, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+        KSB_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+        if (iters) *iters = st.iterations;
+        if (hist)
+            for (int k = 0; k < std::min<int>(hist_cap, int(st.history.size())); ++k) hist[k] = st.history[k];
+    });
+}
+
+int ksb_expand(ksb_level* l, const double* d_PhiT, int ld, const double* d_wt, const double* d_bcb, double* d_Phi,
+               double* d_w) {
+    return guard([&] {
+        auto& K = ready(l);
+        need(d_PhiT && d_wt && d_bcb && d_Phi && d_w, "null argument");
+        ksb::expand(l->L, K, d_PhiT, ld, d_wt, d_bcb, d_Phi, ld, d_w);
+        KSB_CUDA_CHECK(cudaStreamSynchronize(l->L.ctx->stream));
+    });
+}
+
+int ksb_norms(ksb_level* l, const double* d_f, double out[3]) {
+    return guard([&] {
+        need(l && d_f && out, "null argument");
+        const auto a = ksb::norms_sq(l->L, d_f, l->corr().phys);
+        out[0] = a[0];
+        out[1] = a[1];
+        const double l2 = std::sqrt(std::max(0.0, a[0])), semi = std::sqrt(std::max(0.0, a[1]));
+        out[2] = std::sqrt(l2 * l2 + semi * semi);
+    });
+}
+
+int ksb_energy(ksb_level* l, const double* d_Phi, int N, int ld, const double* d_w, double out[5]) {
+    return guard([&] {
+        need(l && d_Phi && d_w && out, "null argument");
+        auto& K = l->corr();
+        if (!K.sys.set) ksb::raise(KSB_INVALID_ARGUMENT, "call ksb_system_set first");
+        ksb::DevBuf<double> rho;
+        rho.alloc(l->L.n);
+        ksb::rho_vxc(l->L, d_Phi, N, ld, K.sys.occ, K.sys.xc, rho.p, nullptr);
+        const auto e = ksb::energy(l->L, d_Phi, N, ld, rho.p, d_w, K.sys.atoms, K.sys.occ, K.sys.xc, K.phys);
+        for (int k = 0; k < 5; ++k) out[k] = e[k];
     });
 }
 

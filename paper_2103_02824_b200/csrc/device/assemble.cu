@@ -200,6 +200,28 @@ int grid_for(const Ctx& c, int64_t work, int block) {
 
 } // namespace
 
+void elem_potential(Level& L, const Potential& pot, double* E) {
+    Ctx& c = *L.ctx;
+    upload_rule(c.stream);
+    const int stride = pot.kind == 0 ? 4 : 5;
+    if (pot.n > 256 || int(pot.params.size()) != stride * pot.n)
+        raise(KSB_INVALID_ARGUMENT, "potential descriptor too large or malformed");
+    KSB_CUDA_CHECK(cudaMemcpyToSymbolAsync(c_pot, pot.params.data(), sizeof(double) * pot.params.size(), 0,
+                                           cudaMemcpyHostToDevice, c.stream));
+    KSB_CUDA_CHECK(cudaMemsetAsync(L.flag.p, 0, sizeof(int), c.stream));
+    const int g = grid_for(c, L.nt, 128);
+    if (pot.kind == 0)
+        launch(c, "assemble", k_elem_mass<2>, g, 128, 0, (const double*)L.xyz.p, (const int32_t*)L.tets.p, L.nt,
+               (const double*)nullptr, pot.n, E, L.flag.p);
+    else
+        launch(c, "assemble", k_elem_mass<3>, g, 128, 0, (const double*)L.xyz.p, (const int32_t*)L.tets.p, L.nt,
+               (const double*)nullptr, pot.n, E, L.flag.p);
+    int h_flag = 0;
+    KSB_CUDA_CHECK(cudaMemcpyAsync(&h_flag, L.flag.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    KSB_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    if (h_flag) raise(KSB_SINGULAR_QUADRATURE, "weight is not finite at a quadrature point");
+}
+
 Mat& Level::mat(int id) {
     if (id < 0 || id >= kMaxMats) raise(KSB_INVALID_ARGUMENT, "matrix id out of range");
     Mat& m = mats[id];

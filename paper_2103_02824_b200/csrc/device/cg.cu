@@ -420,6 +420,8 @@ void launch_iteration(Ctx& c, const Level& L, const CgWork& w, const Cols& cc, c
                       const double* Bb, double* X, int grid_s, int grid_e) {
     const size_t sm_s = sizeof(double) * std::max<size_t>(size_t(kThreads / G) * G * CPL, 2 * size_t(cc.N));
     const size_t sm_e = sizeof(double) * std::max<size_t>(kThreads, 2 * size_t(cc.N));
+    grid_s = std::min(grid_s, resident_grid(c, k_spmm_dot<G, CPL, SHIFT, SPLIT>, kThreads, sm_s));
+    grid_e = std::min(grid_e, resident_grid(c, k_update_xr, kThreads, sm_e));
     launch(c, "spmm", k_spmm_dot<G, CPL, SHIFT, SPLIT>, grid_s, kThreads, sm_s, L.ni, cc,
            (const int32_t*)L.ii_ptr.p, (const int32_t*)L.ii_col.p, A, Bv, (const double*)w.P, w.AP, w.dev);
     launch(c, "cg_update", k_update_xr, grid_e, kThreads, sm_e, L.ni, cc, X, w.R, (const double*)w.P,

@@ -55,6 +55,22 @@ inline void launch(Ctx& c, const char* name, Kernel k, dim3 grid, dim3 block, si
 
 inline int ceil_div(int64_t a, int64_t b) { return int((a + b - 1) / b); }
 
+/// number of blocks of `kernel` that are co-resident on the whole GPU (one full wave).
+/// Streaming kernels sized to one wave sweep the rows in lock-step, which keeps the
+/// gathered neighbour rows of an SpMM inside L2 instead of re-fetching them per wave.
+template <typename Kernel>
+inline int resident_grid(const Ctx& c, Kernel k, int block, size_t smem) {
+    static std::map<std::pair<const void*, size_t>, int> cache;
+    const auto key = std::make_pair(reinterpret_cast<const void*>(k), smem * 4096 + size_t(block));
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second * c.sm_count;
+    int n = 0;
+    KSB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, block, smem));
+    n = n > 0 ? n : 1;
+    cache.emplace(key, n);
+    return n * c.sm_count;
+}
+
 __device__ __forceinline__ double warp_sum(double v, unsigned mask = 0xffffffffu) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(mask, v, o);

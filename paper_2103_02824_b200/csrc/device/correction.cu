@@ -1,0 +1,353 @@
+// One outer iteration of solve_level_corrected on the device.
+//
+// Reference loop body: proj/src/driver.cpp:106-150, with
+//   OuterOperator + shift ladder   proj/src/correction.cpp:15-61   (multi-RHS CG, cg.cu)
+//   bvp_hartree                    proj/src/correction.cpp:67-75   (physics.cu + CG on S)
+//   prepare_blocks                 proj/src/correction.cpp:113-212 (project.cu)
+//   inner_scf                      proj/src/correction.cpp:279-368 (inner.cu)
+//   expand                         proj/src/correction.cpp:370-381
+//   density_change (H1)            proj/src/driver.cpp:56-60
+#include <algorithm>
+#include <cmath>
+
+#include "correction.cuh"
+
+namespace ksb {
+
+void elem_potential(Level& L, const Potential& pot, double* E);
+void axpby_values(Level& L, int dst, double a, int x, double b, int y);
+
+namespace {
+
+constexpr int kT = 256;
+constexpr double kFourPi = 4.0 * 3.14159265358979323846;
+
+int grid_of(const Ctx& c, int64_t work) {
+    return int(std::max<int64_t>(1, std::min<int64_t>((work + kT - 1) / kT, int64_t(c.sm_count) * 8)));
+}
+
+__global__ void k_add(int64_t n, const double* __restrict__ a, double sa, const double* __restrict__ b, double sb,
+                      double* __restrict__ y) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        y[i] = sa * a[i] + sb * b[i];
+}
+
+__global__ void k_min_diag(int ni, const int32_t* __restrict__ dslot, const double* __restrict__ vals,
+                           double* __restrict__ out) {
+    __shared__ double red[32];
+    double m = INFINITY;
+    for (int r = threadIdx.x; r < ni; r += blockDim.x) m = fmin(m, vals[dslot[r]]);
+    for (int o = 16; o > 0; o >>= 1) m = fmin(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = INFINITY;
+        for (int w = 0; w < int(blockDim.x >> 5); ++w) t = fmin(t, red[w]);
+        out[0] = ni > 0 ? t : 0.0;
+    }
+}
+
+/// B[r, j] = scale_j * R[r, col_j]  (gather of a column subset, per-column scale)
+__global__ void k_gather_cols(int ni, int nc, const int* __restrict__ cols, const double* __restrict__ scale,
+                              const double* __restrict__ R, int ldr, double* __restrict__ B, int ldb) {
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < int64_t(ni) * nc;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        const int r = int(e / nc), j = int(e % nc);
+        B[size_t(r) * ldb + j] = scale[j] * R[size_t(r) * ldr + cols[j]];
+    }
+}
+
+/// X[r, col_j] = Xc[r, j] for the columns with take_j != 0
+__global__ void k_scatter_cols(int ni, int nc, const int* __restrict__ cols, const int* __restrict__ take,
+                               const double* __restrict__ Xc, int ldc, double* __restrict__ X, int ldx) {
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < int64_t(ni) * nc;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        const int r = int(e / nc), j = int(e % nc);
+        if (take[j]) X[size_t(r) * ldx + cols[j]] = Xc[size_t(r) * ldc + j];
+    }
+}
+
+/// full-length vector from interior values + boundary values
+__global__ void k_full_from(int ni, int nb, const int32_t* __restrict__ interior, const int32_t* __restrict__ boundary,
+                            const double* __restrict__ vint, const double* __restrict__ vb, double* __restrict__ full) {
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < int64_t(ni) + nb;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        if (e < ni)
+            full[interior[e]] = vint ? vint[e] : 0.0;
+        else
+            full[boundary[e - ni]] = vb ? vb[e - ni] : 0.0;
+    }
+}
+
+/// Phi[r, i] = sum_k P_int(r,k) phiH[i][col_k] + theta2_i PhiT[r, i]
+/// w[interior r] = (0 + sum_k P_int(r,k) wH[col_k]) + theta1 wt[interior r]; w[boundary] = bc
+__global__ void k_expand(int ni, int N, int nh, const int32_t* __restrict__ pcol, const double* __restrict__ pval,
+                         const double* __restrict__ phiH, const double* __restrict__ th2, const double* __restrict__ PhiT,
+                         int ldT, double* __restrict__ Phi, int ld, const double* __restrict__ wH,
+                         const double* __restrict__ th1, const double* __restrict__ wt_full,
+                         const int32_t* __restrict__ interior, double* __restrict__ w_full) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < ni; r += gridDim.x * blockDim.x) {
+        int pc[4];
+        double pv[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            pc[k] = pcol[4 * size_t(r) + k];
+            pv[k] = pval[4 * size_t(r) + k];
+        }
+        for (int i = 0; i < N; ++i) {
+            double s = 0.0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (pc[k] >= 0) s += pv[k] * phiH[size_t(i) * nh + pc[k]];
+            Phi[size_t(r) * ld + i] = s + th2[i] * PhiT[size_t(r) * ldT + i];
+        }
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (pc[k] >= 0) s += pv[k] * wH[pc[k]];
+        const int v = interior[r];
+        w_full[v] = (0.0 + s) + th1[0] * wt_full[v];
+    }
+}
+
+struct Timer {
+    cudaEvent_t e[8];
+    int n = 0;
+    cudaStream_t s;
+    explicit Timer(cudaStream_t st) : s(st) {
+        for (auto& x : e) KSB_CUDA_CHECK(cudaEventCreate(&x));
+    }
+    ~Timer() {
+        for (auto& x : e) cudaEventDestroy(x);
+    }
+    void mark() { KSB_CUDA_CHECK(cudaEventRecord(e[n++], s)); }
+    double ms(int a, int b) {
+        float t = 0;
+        KSB_CUDA_CHECK(cudaEventElapsedTime(&t, e[a], e[b]));
+        return t;
+    }
+};
+
+void need(DevBuf<double>& b, int64_t n) {
+    if (b.n < n) b.alloc(std::max<int64_t>(1, n));
+}
+
+}  // namespace
+
+// make_level_ops (proj/src/driver.cpp:35-47): S, M, a_op = 1/2 S + M_ext, the per-tet M_ext elements and the
+// coarse interior blocks M_H, C_H with their Cholesky factors.
+void level_ops(Level& L, Corrector& K) {
+    if (!K.sys.set) raise(KSB_INVALID_ARGUMENT, "system not set on this level");
+    Potential pot;
+    pot.kind = 0;
+    pot.n = int(K.sys.atoms.size() / 4);
+    pot.params = K.sys.atoms;
+    assemble_into(L, 0, 1.0, 0.0, nullptr, 0.0, nullptr, 0.0);  // S
+    assemble_into(L, 1, 0.0, 1.0, nullptr, 0.0, nullptr, 0.0);  // M
+    assemble_into(L, 2, 0.5, 0.0, pot.n ? &pot : nullptr, 1.0, nullptr, 0.0);  // a_op
+    need(K.eext, int64_t(L.nt) * 16);
+    if (pot.n)
+        elem_potential(L, pot, K.eext.p);
+    else
+        KSB_CUDA_CHECK(cudaMemsetAsync(K.eext.p, 0, sizeof(double) * L.nt * 16, L.ctx->stream));
+    coarse_level_setup(L, K.coarse);
+    K.ops_ready = true;
+}
+
+double outer_operator(Level& L, Corrector& K, const double* d_what_full, const double* d_vxc_full) {
+    Ctx& c = *L.ctx;
+    need(K.pot, L.n);
+    launch(c, "elementwise", k_add, grid_of(c, L.n), kT, 0, int64_t(L.n), d_what_full, 1.0, d_vxc_full, 1.0, K.pot.p);
+    assemble_into(L, MAT_TMP, 0.0, 0.0, nullptr, 0.0, K.pot.p, 1.0);
+    axpby_values(L, MAT_H, 1.0, 2, 1.0, MAT_TMP);
+    need(K.diff, L.n);
+    launch(c, "elementwise", k_min_diag, 1, 1024, 0, L.ni, (const int32_t*)L.diag_slot.p,
+           (const double*)L.mats[MAT_H].ii.p, K.diff.p);
+    double md = 0.0;
+    KSB_CUDA_CHECK(cudaMemcpyAsync(&md, K.diff.p, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    KSB_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    K.min_diag = md;
+    return md;
+}
+
+// OuterOperator::solve_orbital for all orbitals at once (proj/src/correction.cpp:26-61)
+void solve_orbitals(Level& L, Corrector& K, CgWork& cg, const StepOptions& o, const double* h_lambda,
+                    const double* d_Phi, int ld, double* d_PhiT, int ldT, StepLog* log) {
+    Ctx& c = *L.ctx;
+    const int N = K.sys.N, ni = L.ni;
+    need(K.R0, int64_t(ni) * ld);
+    need(K.Bblk, int64_t(ni) * ld);
+    spmm(c, L, L.mats[1].ii.p, nullptr, nullptr, d_Phi, N, ld, K.R0.p, ld);  // M phi (orbitals vanish on the boundary)
+    if (K.idx.n < 4 * N + 8) K.idx.alloc(4 * N + 8);
+    DevBuf<double> sc;
+    sc.alloc(N);
+    std::vector<int> cols(N);
+    for (int i = 0; i < N; ++i) cols[i] = i;
+    KSB_CUDA_CHECK(cudaMemcpyAsync(K.idx.p, cols.data(), sizeof(int) * N, cudaMemcpyHostToDevice, c.stream));
+    KSB_CUDA_CHECK(cudaMemcpyAsync(sc.p, h_lambda, sizeof(double) * N, cudaMemcpyHostToDevice, c.stream));
+    launch(c, "elementwise", k_gather_cols, grid_of(c, int64_t(ni) * N), kT, 0, ni, N, (const int*)K.idx.p,
+           (const double*)sc.p, (const double*)K.R0.p, ld, K.Bblk.p, ld);
+    CgOptions co;
+    co.tol = o.tol_linear;
+    co.check_every = o.check_every;
+    std::vector<CgColumnStats> st(N);
+    cg_solve(c, L, MAT_H, -1, nullptr, K.Bblk.p, d_PhiT, N, ld, co, st.data(), cg);
+    if (ldT != ld) raise(KSB_INVALID_ARGUMENT, "solve_orbitals: ld mismatch");
+    std::vector<int> attempt(N, -1), iters(N);
+    std::vector<int> fail;
+    for (int i = 0; i < N; ++i) {
+        iters[i] = st[i].iterations;
+        if (!st[i].converged) fail.push_back(i);
+    }
+    const double base = std::abs(K.min_diag);
+    for (int k = 0; k < 4 && !fail.empty(); ++k) {
+        const double sigma = k == 0 ? base : std::pow(4.0, k) * (base + 1.0);
+        const int nf = int(fail.size());
+        const int ldc = nf == 1 ? 1 : nf + (nf & 1);
+        need(K.Bc, int64_t(ni) * ldc);
+        need(K.Xc, int64_t(ni) * ldc);
+        std::vector<double> scale(nf), sig(nf, sigma);
+        for (int j = 0; j < nf; ++j) scale[j] = h_lambda[fail[j]] + sigma;
+        DevBuf<double> dsc;
+        dsc.alloc(nf);
+        KSB_CUDA_CHECK(cudaMemcpyAsync(K.idx.p, fail.data(), sizeof(int) * nf, cudaMemcpyHostToDevice, c.stream));
+        KSB_CUDA_CHECK(cudaMemcpyAsync(dsc.p, scale.data(), sizeof(double) * nf, cudaMemcpyHostToDevice, c.stream));
+        if (ldc > nf) KSB_CUDA_CHECK(cudaMemsetAsync(K.Bc.p, 0, sizeof(double) * ni * ldc, c.stream));
+        launch(c, "elementwise", k_gather_cols, grid_of(c, int64_t(ni) * nf), kT, 0, ni, nf, (const int*)K.idx.p,
+               (const double*)dsc.p, (const double*)K.R0.p, ld, K.Bc.p, ldc);
+        std::vector<CgColumnStats> sst(nf);
+        cg_solve(c, L, MAT_H, 1, sig.data(), K.Bc.p, K.Xc.p, nf, ldc, co, sst.data(), cg);
+        std::vector<int> take(nf), still;
+        for (int j = 0; j < nf; ++j) {
+            iters[fail[j]] += sst[j].iterations;
+            take[j] = sst[j].converged;
+            if (sst[j].converged)
+                attempt[fail[j]] = k;
+            else
+                still.push_back(fail[j]);
+        }
+        KSB_CUDA_CHECK(cudaMemcpyAsync(K.idx.p + N + 4, take.data(), sizeof(int) * nf, cudaMemcpyHostToDevice, c.stream));
+        launch(c, "elementwise", k_scatter_cols, grid_of(c, int64_t(ni) * nf), kT, 0, ni, nf, (const int*)K.idx.p,
+               (const int*)(K.idx.p + N + 4), (const double*)K.Xc.p, ldc, d_PhiT, ldT);
+        KSB_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+        fail.swap(still);
+    }
+    if (!fail.empty()) raise(KSB_NONCONVERGENCE, "orbital correction solve failed even after the level shift");
+    if (log) {
+        log->attempts = attempt;
+        log->iterations = iters;
+        log->cg_iterations = 0;
+        for (int x : iters) log->cg_iterations += x;
+    }
+}
+
+// bvp_hartree -> solve_hartree_exact (proj/src/hartree.cpp:131-144): w with Dirichlet data bcb
+int hartree_solve(Level& L, Corrector& K, CgWork& cg, const double* d_PhiT, int N, int ldT, const double* d_bcb,
+                  double tol, double* d_w_full) {
+    Ctx& c = *L.ctx;
+    need(K.hrhs, L.ni);
+    need(K.wtil_int, L.ni);
+    sqload(L, d_PhiT, N, ldT, K.sys.occ, kFourPi, K.hrhs.p, K.phys);
+    lift(L, 0, d_bcb, K.hrhs.p);
+    CgOptions co;
+    co.tol = tol;
+    CgColumnStats st;
+    cg_solve(c, L, 0, -1, nullptr, K.hrhs.p, K.wtil_int.p, 1, 1, co, &st, cg);
+    if (!st.converged) raise(KSB_NONCONVERGENCE, "hartree solve stalled");
+    launch(c, "elementwise", k_full_from, grid_of(c, L.n), kT, 0, L.ni, L.nb, (const int32_t*)L.interior.p,
+           (const int32_t*)L.boundary.p, (const double*)K.wtil_int.p, d_bcb, d_w_full);
+    return st.iterations;
+}
+
+void expand(Level& L, Corrector& K, const double* d_PhiT, int ldT, const double* d_wt_full, const double* d_bcb,
+            double* d_Phi, int ld, double* d_w_full) {
+    Ctx& c = *L.ctx;
+    InnerWork& w = K.inner;
+    const int cur = w.cur;
+    // boundary entries of w first (ell), interior entries from the kernel
+    launch(c, "elementwise", k_full_from, grid_of(c, L.n), kT, 0, 0, L.nb, (const int32_t*)L.interior.p,
+           (const int32_t*)L.boundary.p, (const double*)nullptr, d_bcb, d_w_full);
+    launch(c, "expand", k_expand, grid_of(c, L.ni), kT, 0, L.ni, K.sys.N, L.nH, (const int32_t*)L.pint_col.p,
+           (const double*)L.pint_val.p, (const double*)w.phi[cur].p, (const double*)w.th2[cur].p, d_PhiT, ldT, d_Phi,
+           ld, (const double*)w.wH[cur].p, (const double*)w.th1[cur].p, d_wt_full, (const int32_t*)L.interior.p,
+           d_w_full);
+}
+
+void correction_step(Level& L, Corrector& K, CgWork& cg, const StepOptions& o, double* h_lambda, double* d_Phi, int ld,
+                     double* d_w, StepLog* log) {
+    Ctx& c = *L.ctx;
+    if (!K.ops_ready) level_ops(L, K);
+    const int N = K.sys.N, n = L.n, ni = L.ni;
+    Timer tm(c.stream);
+    tm.mark();
+    need(K.rho, n);
+    need(K.vxc, n);
+    need(K.what_full, n);
+    need(K.bcb, std::max(1, L.nb));
+    need(K.wt_full, n);
+    need(K.ell_full, n);
+    need(K.rho_t, n);
+    need(K.diff, n);
+    need(K.PhiT, int64_t(ni) * ld);
+    // density and xc of the current orbitals
+    rho_vxc(L, d_Phi, N, ld, K.sys.occ, K.sys.xc, K.rho.p, K.sys.xc_on ? K.vxc.p : nullptr);
+    if (!K.sys.xc_on) KSB_CUDA_CHECK(cudaMemsetAsync(K.vxc.p, 0, sizeof(double) * n, c.stream));
+    if (K.sys.hartree_on)
+        KSB_CUDA_CHECK(cudaMemcpyAsync(K.what_full.p, d_w, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream));
+    else
+        KSB_CUDA_CHECK(cudaMemsetAsync(K.what_full.p, 0, sizeof(double) * n, c.stream));
+    outer_operator(L, K, K.what_full.p, K.vxc.p);
+    StepLog lg;
+    solve_orbitals(L, K, cg, o, h_lambda, d_Phi, ld, K.PhiT.p, ld, &lg);
+    tm.mark();
+    KSB_CUDA_CHECK(cudaMemsetAsync(K.bcb.p, 0, sizeof(double) * std::max(1, L.nb), c.stream));
+    if (K.sys.hartree_on) {
+        rho_vxc(L, K.PhiT.p, N, ld, K.sys.occ, K.sys.xc, K.rho_t.p, nullptr);
+        const double ctr[3] = {0.5 * (L.box_lo[0] + L.box_hi[0]), 0.5 * (L.box_lo[1] + L.box_hi[1]),
+                               0.5 * (L.box_lo[2] + L.box_hi[2])};
+        const Moments m = moments(L, K.rho_t.p, K.phys, ctr);
+        boundary_values(L, m, K.bcb.p);
+        lg.hartree_iterations = hartree_solve(L, K, cg, K.PhiT.p, N, ld, K.bcb.p, o.tol_linear, K.diff.p);
+        // w_tilde0 = w_tilde - ell: interior values, zero trace
+        launch(c, "elementwise", k_full_from, grid_of(c, n), kT, 0, ni, L.nb, (const int32_t*)L.interior.p,
+               (const int32_t*)L.boundary.p, (const double*)K.wtil_int.p, (const double*)nullptr, K.wt_full.p);
+        launch(c, "elementwise", k_full_from, grid_of(c, n), kT, 0, ni, L.nb, (const int32_t*)L.interior.p,
+               (const int32_t*)L.boundary.p, (const double*)nullptr, (const double*)K.bcb.p, K.ell_full.p);
+    } else {
+        KSB_CUDA_CHECK(cudaMemsetAsync(K.wt_full.p, 0, sizeof(double) * n, c.stream));
+        KSB_CUDA_CHECK(cudaMemsetAsync(K.ell_full.p, 0, sizeof(double) * n, c.stream));
+    }
+    tm.mark();
+    project_blocks(L, K.PhiT.p, N, ld, K.wt_full.p, K.ell_full.p, K.vxc.p, K.eext.p, K.proj);
+    tm.mark();
+    InnerParams ip;
+    ip.tol = o.tol_inner;
+    ip.max_iterations = o.max_inner;
+    ip.score_floor = o.score_floor;
+    ip.nev_pad = o.nev_pad;
+    ip.hartree = K.sys.hartree_on;
+    ip.occ = K.sys.occ;
+    const InnerStats ist = inner_scf(L, K.coarse, K.proj, ip, h_lambda, K.inner, true);
+    lg.inner_iterations = ist.iterations;
+    lg.inner_history = ist.history;
+    tm.mark();
+    expand(L, K, K.PhiT.p, ld, K.wt_full.p, K.bcb.p, d_Phi, ld, d_w);
+    rho_vxc(L, d_Phi, N, ld, K.sys.occ, K.sys.xc, K.rho_t.p, nullptr);
+    launch(c, "elementwise", k_add, grid_of(c, n), kT, 0, int64_t(n), (const double*)K.rho_t.p, 1.0,
+           (const double*)K.rho.p, -1.0, K.diff.p);
+    const auto nn = norms_sq(L, K.diff.p, K.phys);
+    const double l2 = std::sqrt(std::max(0.0, nn[0])), semi = std::sqrt(std::max(0.0, nn[1]));
+    lg.delta = std::sqrt(l2 * l2 + semi * semi);
+    KSB_CUDA_CHECK(cudaMemcpyAsync(h_lambda, K.inner.lamv[K.inner.cur].p, sizeof(double) * N, cudaMemcpyDeviceToHost,
+                                   c.stream));
+    tm.mark();
+    KSB_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    lg.ms_bvp = tm.ms(0, 1);
+    lg.ms_hartree = tm.ms(1, 2);
+    lg.ms_project = tm.ms(2, 3);
+    lg.ms_inner = tm.ms(3, 4);
+    lg.ms_total = tm.ms(0, 5);
+    if (log) *log = lg;
+}
+
+}  // namespace ksb

@@ -1,0 +1,70 @@
+// One outer iteration of the corrected level solve on the device (see correction.cu).
+#pragma once
+
+#include <array>
+#include <vector>
+
+#include "cg.cuh"
+#include "inner.cuh"
+#include "physics.cuh"
+#include "project.cuh"
+
+namespace ksb {
+
+constexpr int MAT_H = 3;    // current outer operator a_op + M_{w_hat + v_xc}
+constexpr int MAT_TMP = 4;  // scratch
+
+struct System {
+    std::vector<double> atoms;  // (Z, x, y, z) per nucleus
+    int N = 1;
+    double occ = 2.0;
+    XcParams xc{2, 0.77298, 1.0 / 3.0};
+    bool hartree_on = true, xc_on = true;
+    bool set = false;
+};
+
+struct StepOptions {
+    double tol_linear = 1e-9, tol_inner = 1e-8, score_floor = 1e-8;
+    int max_inner = 400, nev_pad = 4, check_every = 8;
+};
+
+struct StepLog {
+    int inner_iterations = 0, hartree_iterations = 0;
+    double delta = 0;
+    double ms_bvp = 0, ms_hartree = 0, ms_project = 0, ms_inner = 0, ms_total = 0;
+    int64_t cg_iterations = 0;
+    std::vector<int> attempts, iterations;  // per orbital: -1 unshifted, k = ladder rung
+    std::vector<double> inner_history;
+};
+
+/// per-level correction machinery attached to a Level
+struct Corrector {
+    System sys;
+    bool ops_ready = false;
+    double min_diag = 0;
+    DevBuf<double> eext;        // 16 per fine tet: M_ext element (Keast)
+    CoarseOps coarse;
+    ProjOut proj;
+    InnerWork inner;
+    PhysWork phys;
+    // work vectors (full = n, int = ni, blocks = ni x ld)
+    DevBuf<double> rho, vxc, pot, rho_t, bcb, wt_full, ell_full, what_full, diff, wtil_int, hrhs;
+    DevBuf<double> R0, Bblk, Xblk, Bc, Xc, PhiT;
+    DevBuf<int> idx;
+    int ldT = 0;
+};
+
+void level_ops(Level& L, Corrector& K);
+void correction_step(Level& L, Corrector& K, CgWork& cg, const StepOptions& o, double* h_lambda, double* d_Phi, int ld,
+                     double* d_w, StepLog* log);
+
+// pieces (also exported through the C-ABI for parity tests)
+double outer_operator(Level& L, Corrector& K, const double* d_what_full, const double* d_vxc_full);
+void solve_orbitals(Level& L, Corrector& K, CgWork& cg, const StepOptions& o, const double* h_lambda,
+                    const double* d_Phi, int ld, double* d_PhiT, int ldT, StepLog* log);
+int hartree_solve(Level& L, Corrector& K, CgWork& cg, const double* d_PhiT, int N, int ldT, const double* d_bcb,
+                  double tol, double* d_w_full);
+void expand(Level& L, Corrector& K, const double* d_PhiT, int ldT, const double* d_wt_full, const double* d_bcb,
+            double* d_Phi, int ld, double* d_w_full);
+
+}  // namespace ksb

@@ -1,0 +1,953 @@
+// K-BEIG + coarse sweep kernels: corr::inner_scf on the device.
+//
+// Reference: proj/src/correction.cpp:225-368 (inner_scf, A_H2, b_H2, beta2, f_H, g) and the
+// dense bordered eigensolve + selection rule proj/src/eigensolve.cpp:371-396,425-443.
+// The reference solves one (N_H+1)-dimensional generalized eigenproblem per orbital per
+// sweep. Here the coarse mass Cholesky factor L_H is shared by all orbitals, so each
+// bordered pencil reduces to  [C11 c12; c12^T c22]  with the SAME C11 = L_H^-1 A_H L_H^-T for
+// every orbital. C11 is tridiagonalised once per sweep (Householder, one CTA); every
+// orbital's problem is then an arrow-tridiagonal matrix [T c^; c^T c22] whose inertia at a
+// shift is one O(N_H) LDL^T pass (Sylvester), so the lowest nev eigenvalues come from
+// warp-parallel multisection and each eigenvector from one tridiagonal solve.
+#include <algorithm>
+#include <cfloat>
+
+#include "geom.cuh"
+#include "inner.cuh"
+
+namespace ksb {
+
+namespace {
+
+// ------------------------------------------------------------------------------------------
+// dense helpers (row-major n x n)
+
+/// single-CTA Cholesky, lower factor in place (upper part zeroed). flag[0] = 1 if not SPD.
+__global__ void k_potrf(int n, double* __restrict__ A, int* __restrict__ flag) {
+    __shared__ double piv;
+    for (int j = 0; j < n; ++j) {
+        // A[j][j] -= sum_k<j A[j][k]^2 (lane-parallel over k, fixed order)
+        if (threadIdx.x < 32) {
+            double s = 0.0;
+            for (int k = threadIdx.x; k < j; k += 32) s += A[size_t(j) * n + k] * A[size_t(j) * n + k];
+            s = warp_sum(s);
+            if (threadIdx.x == 0) {
+                const double d = A[size_t(j) * n + j] - s;
+                if (!(d > 0.0) || !isfinite(d)) flag[0] = 1;
+                piv = sqrt(fmax(d, DBL_MIN));
+                A[size_t(j) * n + j] = piv;
+            }
+        }
+        __syncthreads();
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+        for (int i = j + 1 + warp; i < n; i += nw) {
+            double s = 0.0;
+            for (int k = lane; k < j; k += 32) s += A[size_t(i) * n + k] * A[size_t(j) * n + k];
+            s = warp_sum(s);
+            if (lane == 0) A[size_t(i) * n + j] = (A[size_t(i) * n + j] - s) / piv;
+        }
+        __syncthreads();
+    }
+    for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x)
+        if (idx % n > idx / n) A[idx] = 0.0;
+}
+
+/// warp-per-RHS triangular solve with the lower factor L (row-major):
+///   trans = 0: L x = b ;  trans = 1: L^T x = b.
+/// RHS j element k at B[j*bs + k*bc]; solution to X[j*xs + k*xc] (may alias B with equal strides).
+__global__ void k_trsv_many(int n, int nrhs, const double* __restrict__ L, int trans, const double* B, int64_t bs,
+                            int64_t bc, double* X, int64_t xs, int64_t xc, double scale) {
+    extern __shared__ double ys[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int j = blockIdx.x * (blockDim.x >> 5) + warp;
+    if (j >= nrhs) return;
+    double* y = ys + size_t(warp) * n;
+    for (int k = lane; k < n; k += 32) y[k] = scale * B[j * bs + k * bc];
+    __syncwarp();
+    if (!trans) {
+        for (int i = 0; i < n; ++i) {
+            double s = 0.0;
+            for (int k = lane; k < i; k += 32) s += L[size_t(i) * n + k] * y[k];
+            s = warp_sum(s);
+            if (lane == 0) y[i] = (y[i] - s) / L[size_t(i) * n + i];
+            __syncwarp();
+        }
+    } else {
+        for (int i = n - 1; i >= 0; --i) {
+            double s = 0.0;
+            for (int k = i + 1 + lane; k < n; k += 32) s += L[size_t(k) * n + i] * y[k];
+            s = warp_sum(s);
+            if (lane == 0) y[i] = (y[i] - s) / L[size_t(i) * n + i];
+            __syncwarp();
+        }
+    }
+    for (int k = lane; k < n; k += 32) X[j * xs + k * xc] = y[k];
+}
+
+/// single-CTA Householder tridiagonalisation of symmetric C (row-major, destroyed).
+/// d[n], e[n-1]; V row k holds the unit Householder vector of step k in entries k+1..n-1.
+__global__ void __launch_bounds__(1024) k_tridiag(int n, double* __restrict__ C, double* __restrict__ d,
+                                                  double* __restrict__ e, double* __restrict__ V) {
+    extern __shared__ double sh[];
+    double* v = sh;          // n
+    double* p = sh + n;      // n
+    __shared__ double red[32];
+    __shared__ double bc[2];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    for (int k = 0; k + 2 < n; ++k) {
+        const int m0 = k + 1, m = n - m0;
+        // column k below the diagonal = row k right of the diagonal (symmetry)
+        double s = 0.0;
+        for (int i = tid; i < m; i += blockDim.x) {
+            const double x = C[size_t(k) * n + m0 + i];
+            v[m0 + i] = x;
+            s += x * x;
+        }
+        s = warp_sum(s);
+        if (lane == 0) red[warp] = s;
+        __syncthreads();
+        if (tid == 0) {
+            double t = 0.0;
+            for (int w = 0; w < nw; ++w) t += red[w];
+            const double nx = sqrt(t);
+            const double x0 = v[m0];
+            const double alpha = x0 >= 0.0 ? -nx : nx;
+            const double nv2 = t - x0 * x0 + (x0 - alpha) * (x0 - alpha);
+            bc[0] = alpha;
+            bc[1] = (nx == 0.0 || nv2 <= 0.0) ? 0.0 : 1.0 / sqrt(nv2);
+            v[m0] = x0 - alpha;
+        }
+        __syncthreads();
+        const double alpha = bc[0], inv = bc[1];
+        d[k] = C[size_t(k) * n + k];  // every thread writes the same value; harmless
+        if (tid == 0) e[k] = inv == 0.0 ? v[m0] + alpha : alpha;
+        if (inv == 0.0) {  // nothing to annihilate: identity reflector
+            for (int i = tid; i < m; i += blockDim.x) V[size_t(k) * n + m0 + i] = 0.0;
+            __syncthreads();
+            continue;
+        }
+        for (int i = tid; i < m; i += blockDim.x) {
+            v[m0 + i] *= inv;
+            V[size_t(k) * n + m0 + i] = v[m0 + i];
+        }
+        __syncthreads();
+        // p = C22 v (warp per row)
+        for (int r = warp; r < m; r += nw) {
+            const double* row = C + size_t(m0 + r) * n + m0;
+            double t = 0.0;
+            for (int c = lane; c < m; c += 32) t += row[c] * v[m0 + c];
+            t = warp_sum(t);
+            if (lane == 0) p[m0 + r] = t;
+        }
+        __syncthreads();
+        // K = v.p ; q = p - K v (stored in p)
+        s = 0.0;
+        for (int i = tid; i < m; i += blockDim.x) s += v[m0 + i] * p[m0 + i];
+        s = warp_sum(s);
+        if (lane == 0) red[warp] = s;
+        __syncthreads();
+        if (tid == 0) {
+            double t = 0.0;
+            for (int w = 0; w < nw; ++w) t += red[w];
+            bc[0] = t;
+        }
+        __syncthreads();
+        const double K = bc[0];
+        for (int i = tid; i < m; i += blockDim.x) p[m0 + i] -= K * v[m0 + i];
+        __syncthreads();
+        // C22 -= 2 (v q^T + q v^T)
+        for (int idx = tid; idx < m * m; idx += blockDim.x) {
+            const int r = idx / m, c = idx % m;
+            C[size_t(m0 + r) * n + m0 + c] -= 2.0 * (v[m0 + r] * p[m0 + c] + p[m0 + r] * v[m0 + c]);
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        if (n >= 2) {
+            d[n - 2] = C[size_t(n - 2) * n + n - 2];
+            e[n - 2] = C[size_t(n - 1) * n + n - 2];
+        }
+        if (n >= 1) d[n - 1] = C[size_t(n - 1) * n + n - 1];
+    }
+}
+
+/// apply Q^T (forward = 1: H_0 first) or Q (forward = 0: H_{n-3} first) to vectors, warp per vector.
+/// vector j element k at X[j*xs + k].
+__device__ void apply_q_warp(int n, const double* __restrict__ V, double* x, int forward) {
+    const int lane = threadIdx.x & 31;
+    const int steps = n - 2;
+    for (int s = 0; s < steps; ++s) {
+        const int k = forward ? s : steps - 1 - s;
+        const double* vk = V + size_t(k) * n;
+        double t = 0.0;
+        for (int i = k + 1 + lane; i < n; i += 32) t += vk[i] * x[i];
+        t = 2.0 * warp_sum(t);
+        for (int i = k + 1 + lane; i < n; i += 32) x[i] -= t * vk[i];
+        __syncwarp();
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// coarse-mesh element work (3072 coarse tets): A_H2(w_H) and the coarse square load
+
+/// per coarse tet: 16-entry weighted mass (Keast) with nodal weight from interior coarse values wint
+__global__ void k_coarse_wmass(int nct, const int32_t* __restrict__ ctets, const double* __restrict__ cxyz,
+                               const int32_t* __restrict__ ciidx, const double* __restrict__ wint,
+                               double* __restrict__ E) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nct; t += gridDim.x * blockDim.x) {
+        const int4 v = reinterpret_cast<const int4*>(ctets)[t];
+        TetG G;
+        tet_geometry(cxyz, v, G);
+        const int vv[4] = {v.x, v.y, v.z, v.w};
+        double wn[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) wn[k] = ciidx[vv[k]] >= 0 ? wint[ciidx[vv[k]]] : 0.0;
+        double K[4][4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) K[i][j] = 0.0;
+        for (int q = 0; q < 11; ++q) {
+            const double wq = g_qb[q][0] * wn[0] + g_qb[q][1] * wn[1] + g_qb[q][2] * wn[2] + g_qb[q][3] * wn[3];
+            const double s = g_qw[q] * G.vol * wq;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) K[i][j] += s * g_qb[q][i] * g_qb[q][j];
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) E[size_t(t) * 16 + 4 * i + j] = K[i][j];
+    }
+}
+
+/// per (coarse tet, orbital): coarse square load of the coarse function phi_H[i] (4 entries)
+__global__ void k_coarse_sq(int nct, int nh, int N, const int32_t* __restrict__ ctets, const double* __restrict__ cxyz,
+                            const int32_t* __restrict__ ciidx, const double* __restrict__ phiH, double* __restrict__ E4) {
+    const int i = blockIdx.y;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nct; t += gridDim.x * blockDim.x) {
+        const int4 v = reinterpret_cast<const int4*>(ctets)[t];
+        const int vv[4] = {v.x, v.y, v.z, v.w};
+        // |T| from the signed-volume formula, as the reference's coarse_square_load
+        TetG G;
+        tet_geometry(cxyz, v, G);
+        double u4[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) u4[k] = ciidx[vv[k]] >= 0 ? phiH[size_t(i) * nh + ciidx[vv[k]]] : 0.0;
+        double out[4] = {0, 0, 0, 0};
+        for (int q = 0; q < 11; ++q) {
+            const double u = g_qb[q][0] * u4[0] + g_qb[q][1] * u4[1] + g_qb[q][2] * u4[2] + g_qb[q][3] * u4[3];
+            const double s = g_qw[q] * G.vol * u * u;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) out[k] += s * g_qb[q][k];
+        }
+        reinterpret_cast<double4*>(E4)[size_t(i) * nct + t] = make_double4(out[0], out[1], out[2], out[3]);
+    }
+    (void)N;
+}
+
+/// per coarse tet: 16-entry stiffness element |T| grad l_i . grad l_j
+__global__ void k_coarse_stiff(int nct, const int32_t* __restrict__ ctets, const double* __restrict__ cxyz,
+                               double* __restrict__ E) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nct; t += gridDim.x * blockDim.x) {
+        const int4 v = reinterpret_cast<const int4*>(ctets)[t];
+        TetG G;
+        tet_geometry(cxyz, v, G);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                E[size_t(t) * 16 + 4 * i + j] =
+                    G.vol * (G.g[i][0] * G.g[j][0] + G.g[i][1] * G.g[j][1] + G.g[i][2] * G.g[j][2]);
+    }
+}
+
+/// A_H = A_H1 + A_H4 [+ A_H2(E16 assembled) + theta1 A_H3], row per thread group (deterministic per row)
+__global__ void k_build_AH(int nh, const int32_t* __restrict__ cinc_ptr, const int32_t* __restrict__ cinc,
+                           const int32_t* __restrict__ ctets, const int32_t* __restrict__ ciidx,
+                           const double* __restrict__ A1, const double* __restrict__ A3, const double* __restrict__ A4,
+                           const double* __restrict__ E16, int with_h, const double* __restrict__ theta1,
+                           double* __restrict__ AH) {
+    const int a = blockIdx.x;
+    double* row = AH + size_t(a) * nh;
+    for (int b = threadIdx.x; b < nh; b += blockDim.x) row[b] = A1[size_t(a) * nh + b] + A4[size_t(a) * nh + b];
+    __syncthreads();
+    if (!with_h) return;
+    // A_H2 row a: sum over coarse tets of a (ascending), exactly one writer per entry
+    if (threadIdx.x == 0) {
+        extern __shared__ double acc[];
+        for (int b = 0; b < nh; ++b) acc[b] = 0.0;
+        for (int k = cinc_ptr[a]; k < cinc_ptr[a + 1]; ++k) {
+            const int C = cinc[k] >> 2, la = cinc[k] & 3;
+            for (int lb = 0; lb < 4; ++lb) {
+                const int b = ciidx[ctets[4 * C + lb]];
+                if (b >= 0) acc[b] += E16[size_t(C) * 16 + 4 * la + lb];
+            }
+        }
+    }
+    __syncthreads();
+    extern __shared__ double acc2[];
+    const double th = theta1[0];
+    for (int b = threadIdx.x; b < nh; b += blockDim.x) {
+        double x = row[b] + acc2[b];
+        if (th != 0.0) x += th * A3[size_t(a) * nh + b];
+        row[b] = x;
+    }
+}
+
+/// sum over (C, la) of a of E4[(i*nct + C)*4 + la] -> out[i*nh + a]
+__global__ void k_coarse_vec_asm(int nh, int nct, const int32_t* __restrict__ cinc_ptr, const int32_t* __restrict__ cinc,
+                                 const double* __restrict__ E4, double* __restrict__ out) {
+    const int a = blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y;
+    if (a >= nh) return;
+    double s = 0.0;
+    for (int k = cinc_ptr[a]; k < cinc_ptr[a + 1]; ++k) s += E4[(size_t(i) * nct + (cinc[k] >> 2)) * 4 + (cinc[k] & 3)];
+    out[size_t(i) * nh + a] = s;
+}
+
+__global__ void k_symmetrize(int n, double* __restrict__ A) {
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n * n; idx += gridDim.x * blockDim.x) {
+        const int r = idx / n, c = idx % n;
+        if (c > r) {
+            const double m = 0.5 * (A[size_t(r) * n + c] + A[size_t(c) * n + r]);
+            A[size_t(r) * n + c] = m;
+            A[size_t(c) * n + r] = m;
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// per-outer preparation: l_i = L_H^-1 c_i, s_i, u_i = L_H^-T l_i ; Hartree u and Schur scalar
+
+__device__ double block_dot(const double* a, const double* b, int n) {
+    __shared__ double red[32];
+    __shared__ double out;
+    double s = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s += a[i] * b[i];
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < int(blockDim.x >> 5); ++w) t += red[w];
+        out = t;
+    }
+    __syncthreads();
+    const double r = out;
+    __syncthreads();
+    return r;
+}
+
+/// s_i^2 = gamma_i - l_i.l_i ; flag on non-positive
+__global__ void k_border_scale(int nh, int N, const double* __restrict__ l, const double* __restrict__ orb_scal,
+                               double* __restrict__ s, int* __restrict__ flag) {
+    const int i = blockIdx.x;
+    const double ll = block_dot(l + size_t(i) * nh, l + size_t(i) * nh, nh);
+    if (threadIdx.x == 0) {
+        const double g = orb_scal[5 * i + 3];
+        const double s2 = g - ll;
+        if (!(g > 0.0) || !(s2 > 0.0)) flag[0] = 1;
+        s[i] = sqrt(fmax(s2, DBL_MIN));
+    }
+    (void)N;
+}
+
+/// schur = zeta - d_Hh . u
+__global__ void k_schur(int nh, const double* __restrict__ dHh, const double* __restrict__ u,
+                        const double* __restrict__ shared_scal, double* __restrict__ out, int* __restrict__ flag) {
+    const double du = block_dot(dHh, u, nh);
+    if (threadIdx.x == 0) {
+        out[0] = shared_scal[0] - du;
+        if (!(out[0] > 0.0)) flag[0] = 1;
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// per sweep, per orbital: border, C12, C22, rotated vectors
+
+struct SweepDev {
+    const double *AH, *A3, *A_h4, *orb_vecs, *orb_scal, *LH, *V, *l, *u, *s, *wH, *theta1;
+    double *c12, *c22, *lhat, *work;
+    int nh, N, hartree;
+};
+
+/// block per orbital: b, beta, t = A_H u, c12 = L^-1 (b - t)/s, c22, then c^ = Q^T c12, l^ = Q^T l
+__global__ void k_orbital_border(SweepDev S) {
+    extern __shared__ double sh[];
+    const int i = blockIdx.x, nh = S.nh;
+    double* b = sh;            // nh
+    double* t = sh + nh;       // nh
+    const double* ov = S.orb_vecs + size_t(i) * 6 * nh;  // b_H1, b_H3, b_H4, c_Hh, d_phi, rhs
+    const double* sc = S.orb_scal + size_t(i) * 5;       // beta1, beta3, beta4, gamma, zeta_phi
+    const double th1 = S.theta1[0];
+    const double* Ah4 = S.A_h4 + size_t(i) * nh * nh;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    // border b = b_H1 + b_H4 [+ (A_h4 w_H + theta1 b_H3)]
+    for (int a = warp; a < nh; a += nw) {
+        double x = 0.0;
+        if (S.hartree)
+            for (int c = lane; c < nh; c += 32) x += Ah4[size_t(a) * nh + c] * S.wH[c];
+        x = warp_sum(x);
+        if (lane == 0) {
+            double bb = ov[a] + ov[2 * nh + a];
+            if (S.hartree) bb += x + th1 * ov[nh + a];
+            b[a] = bb;
+        }
+    }
+    __syncthreads();
+    double beta = sc[0] + sc[2];
+    if (S.hartree) beta += block_dot(ov + 5 * nh, S.wH, nh) + th1 * sc[1];
+    // t = A_H u
+    const double* u = S.u + size_t(i) * nh;
+    for (int a = warp; a < nh; a += nw) {
+        double x = 0.0;
+        for (int c = lane; c < nh; c += 32) x += S.AH[size_t(a) * nh + c] * u[c];
+        x = warp_sum(x);
+        if (lane == 0) t[a] = x;
+    }
+    __syncthreads();
+    const double ub = block_dot(u, b, nh);
+    const double ut = block_dot(u, t, nh);
+    const double si = S.s[i];
+    if (threadIdx.x == 0) S.c22[i] = (beta - 2.0 * ub + ut) / (si * si);
+    // c12 = L^-1 (b - t) / s (warp 0), l^ = Q^T l (warp 1) after c12
+    double* c12 = S.c12 + size_t(i) * nh;
+    double* lh = S.lhat + size_t(i) * nh;
+    if (warp == 0) {
+        for (int a = lane; a < nh; a += 32) t[a] = (b[a] - t[a]) / si;
+        __syncwarp();
+        for (int r = 0; r < nh; ++r) {
+            double x = 0.0;
+            for (int k = lane; k < r; k += 32) x += S.LH[size_t(r) * nh + k] * t[k];
+            x = warp_sum(x);
+            if (lane == 0) t[r] = (t[r] - x) / S.LH[size_t(r) * nh + r];
+            __syncwarp();
+        }
+        apply_q_warp(nh, S.V, t, 1);
+        for (int a = lane; a < nh; a += 32) c12[a] = t[a];
+    } else if (warp == 1) {
+        double* x = sh + 2 * nh;  // private scratch: warp 0 still reads b
+        for (int a = lane; a < nh; a += 32) x[a] = S.l[size_t(i) * nh + a];
+        __syncwarp();
+        apply_q_warp(nh, S.V, x, 1);
+        for (int a = lane; a < nh; a += 32) lh[a] = x[a];
+    }
+}
+
+/// inertia of [T - x, c; c^T, c22 - x]: number of eigenvalues < x (Sylvester)
+__device__ __forceinline__ int arrow_count(int n, const double* __restrict__ d, const double* __restrict__ e,
+                                           const double* __restrict__ c, double c22, double x, double pivmin) {
+    int cnt = 0;
+    double q = 0.0, z = 0.0, acc = 0.0;
+    for (int j = 0; j < n; ++j) {
+        double dj = d[j] - x;
+        double zj = c[j];
+        if (j > 0) {
+            const double l = e[j - 1] / q;
+            dj -= l * e[j - 1];
+            zj -= l * z;
+        }
+        if (fabs(dj) < pivmin) dj = -pivmin;
+        cnt += dj < 0.0;
+        acc += zj * zj / dj;
+        q = dj;
+        z = zj;
+    }
+    const double s = (c22 - x) - acc;
+    return cnt + (s < 0.0 ? 1 : 0);
+}
+
+/// warp per (orbital, k): k-th smallest eigenvalue by 32-way multisection
+__global__ void k_arrow_eig(int nh, int N, int nev, const double* __restrict__ d, const double* __restrict__ e,
+                            const double* __restrict__ c12, const double* __restrict__ c22, double* __restrict__ lam) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (warp >= N * nev) return;
+    const int i = warp / nev, k = warp % nev;
+    const double* c = c12 + size_t(i) * nh;
+    const double cc = c22[i];
+    // Gershgorin bounds
+    double lo = DBL_MAX, hi = -DBL_MAX, csum = 0.0;
+    for (int j = lane; j < nh; j += 32) {
+        const double r = (j > 0 ? fabs(e[j - 1]) : 0.0) + (j + 1 < nh ? fabs(e[j]) : 0.0) + fabs(c[j]);
+        lo = fmin(lo, d[j] - r);
+        hi = fmax(hi, d[j] + r);
+        csum += fabs(c[j]);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    csum = warp_sum(csum);
+    lo = fmin(lo, cc - csum);
+    hi = fmax(hi, cc + csum);
+    const double span = fmax(fabs(lo), fabs(hi));
+    lo -= 1e-12 * span + DBL_MIN;
+    hi += 1e-12 * span + DBL_MIN;
+    const double pivmin = DBL_MIN / DBL_EPSILON * fmax(1.0, span * span);
+    for (int it = 0; it < 40; ++it) {
+        const double w = hi - lo;
+        if (w <= 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + DBL_MIN) break;
+        const double x = lo + w * double(lane + 1) / 33.0;
+        const int cnt = arrow_count(nh, d, e, c, cc, x, pivmin);
+        // first lane whose count exceeds k bounds the eigenvalue from above
+        const unsigned above = __ballot_sync(0xffffffffu, cnt > k);
+        const int f = above ? __ffs(above) - 1 : 32;  // lanes 0..f-1 have count <= k
+        const double nlo = f == 0 ? lo : lo + w * double(f) / 33.0;
+        const double nhi = f == 32 ? hi : lo + w * double(f + 1) / 33.0;
+        lo = nlo;
+        hi = nhi;
+    }
+    if (lane == 0) lam[warp] = 0.5 * (lo + hi);
+}
+
+/// warp per (orbital, k): eigenvector y = [(T - lam)^-1 c ; -1] (rotated basis, unnormalised) and its score
+/// |(L y)_last| / (|y| sqrt(gamma)), (L y)_last = l^T Q y_h + s y_l.
+__global__ void k_arrow_vec(int nh, int N, int nev, const double* __restrict__ d, const double* __restrict__ e,
+                            const double* __restrict__ c12, const double* __restrict__ lhat, const double* __restrict__ s,
+                            const double* __restrict__ orb_scal, const double* __restrict__ lam, double* __restrict__ Y,
+                            double* __restrict__ piv, double* __restrict__ score, double* __restrict__ ynorm) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (warp >= N * nev) return;
+    const int i = warp / nev;
+    const double x = lam[warp];
+    const double* c = c12 + size_t(i) * nh;
+    double* y = Y + size_t(warp) * nh;
+    double* pv = piv + size_t(warp) * nh;
+    if (lane == 0 && nh > 0) {
+        double q = 1.0, z = 0.0;
+        for (int j = 0; j < nh; ++j) {
+            double dj = d[j] - x, zj = c[j];
+            if (j > 0) {
+                const double l = e[j - 1] / q;
+                dj -= l * e[j - 1];
+                zj -= l * z;
+            }
+            if (fabs(dj) < 1e-300) dj = dj < 0 ? -1e-300 : 1e-300;
+            pv[j] = dj;
+            y[j] = zj;
+            q = dj;
+            z = zj;
+        }
+        double nxt = y[nh - 1] / pv[nh - 1];
+        y[nh - 1] = nxt;
+        for (int j = nh - 2; j >= 0; --j) {
+            const double l = e[j] / pv[j];
+            nxt = y[j] / pv[j] - l * nxt;
+            y[j] = nxt;
+        }
+    }
+    __syncwarp();
+    const double* lh = lhat + size_t(i) * nh;
+    double ov = 0.0, nn = 0.0;
+    for (int j = lane; j < nh; j += 32) {
+        ov += lh[j] * y[j];
+        nn += y[j] * y[j];
+    }
+    ov = warp_sum(ov);
+    nn = warp_sum(nn);
+    if (lane == 0) {
+        const double yl = -1.0;
+        ov += s[i] * yl;
+        const double nrm = sqrt(fmax(1e-300, nn + yl * yl));
+        const double g = orb_scal[5 * i + 3];
+        score[warp] = fabs(ov) / (nrm * sqrt(g));
+        ynorm[warp] = nrm;
+    }
+}
+
+/// block per orbital: select (strict >, first wins), back-transform, sign-align against the previous state
+__global__ void k_select(SweepDev S, int nev, const double* __restrict__ lam, const double* __restrict__ Y,
+                         const double* __restrict__ score, const double* __restrict__ ynorm, double floor,
+                         const double* __restrict__ MH, const double* __restrict__ phi_old,
+                         const double* __restrict__ th2_old, double* __restrict__ lam_new, double* __restrict__ phi_new,
+                         double* __restrict__ th2_new, int* __restrict__ flag) {
+    extern __shared__ double sh[];
+    const int i = blockIdx.x, nh = S.nh;
+    __shared__ int best;
+    __shared__ double th;
+    if (threadIdx.x == 0) {
+        int b = 0;
+        double bs = -1.0;
+        for (int k = 0; k < nev; ++k) {
+            const double sc = score[i * nev + k];
+            if (sc > bs) {
+                bs = sc;
+                b = k;
+            }
+        }
+        if (bs < floor) flag[0] = 2;
+        best = b;
+        lam_new[i] = lam[i * nev + b];
+    }
+    __syncthreads();
+    const int w = i * nev + best;
+    const double nrm = ynorm[w];
+    double* x = sh;  // nh: Q y_h / nrm, then phi_H
+    for (int a = threadIdx.x; a < nh; a += blockDim.x) x[a] = Y[size_t(w) * nh + a];
+    __syncthreads();
+    if (threadIdx.x < 32) apply_q_warp(nh, S.V, x, 0);
+    __syncthreads();
+    const double si = S.s[i];
+    if (threadIdx.x == 0) th = (-1.0 / nrm) / si;
+    __syncthreads();
+    const double theta = th;
+    for (int a = threadIdx.x; a < nh; a += blockDim.x) x[a] = x[a] / nrm - S.l[size_t(i) * nh + a] * theta;
+    __syncthreads();
+    if (threadIdx.x < 32) {  // phi_H = L_H^-T x
+        const int lane = threadIdx.x;
+        for (int r = nh - 1; r >= 0; --r) {
+            double t = 0.0;
+            for (int k = r + 1 + lane; k < nh; k += 32) t += S.LH[size_t(k) * nh + r] * x[k];
+            t = warp_sum(t);
+            if (lane == 0) x[r] = (x[r] - t) / S.LH[size_t(r) * nh + r];
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    // ip = phi_new^T M_H phi_old + th_new c.phi_old + th_old c.phi_new + th_new th_old gamma
+    const double* po = phi_old + size_t(i) * nh;
+    const double* cH = S.orb_vecs + size_t(i) * 6 * nh + 3 * nh;
+    double* tmp = sh + nh;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int a = warp; a < nh; a += nw) {
+        double t = 0.0;
+        for (int c = lane; c < nh; c += 32) t += MH[size_t(a) * nh + c] * po[c];
+        t = warp_sum(t);
+        if (lane == 0) tmp[a] = t;
+    }
+    __syncthreads();
+    const double t1 = block_dot(x, tmp, nh);
+    const double t2 = block_dot(cH, po, nh);
+    const double t3 = block_dot(cH, x, nh);
+    const double to = th2_old[i];
+    const double ip = t1 + theta * t2 + to * t3 + theta * to * S.orb_scal[5 * i + 3];
+    const double sg = ip < 0 ? -1.0 : 1.0;
+    for (int a = threadIdx.x; a < nh; a += blockDim.x) phi_new[size_t(i) * nh + a] = sg * x[a];
+    if (threadIdx.x == 0) th2_new[i] = sg * theta;
+}
+
+/// one block: f_H, g, Hartree bordered solve, theta1, w_H, and the H1 state change delta
+struct HartreeDev {
+    const double *sq, *A_h4, *A3, *orb_vecs, *orb_scal, *shared_vecs, *shared_scal, *LC, *hu, *schur, *CH, *MH;
+    const double *phi_new, *th2_new, *phi_old, *th2_old;
+    double *wH_new, *theta1_new, *delta, *f;
+    int nh, N, hartree;
+    double occ;
+};
+
+__global__ void k_hartree_delta(HartreeDev H) {
+    extern __shared__ double sh[];
+    const int nh = H.nh;
+    double* f = sh;           // nh
+    double* tmp = sh + nh;    // nh
+    double* dp = sh + 2 * nh; // nh
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    constexpr double four_pi = 4.0 * 3.14159265358979323846;
+    if (H.hartree) {
+        double g = 0.0;
+        for (int a = threadIdx.x; a < nh; a += blockDim.x) f[a] = 0.0;
+        __syncthreads();
+        for (int i = 0; i < H.N; ++i) {
+            const double* ph = H.phi_new + size_t(i) * nh;
+            const double t2 = H.th2_new[i];
+            const double* Ah4 = H.A_h4 + size_t(i) * nh * nh;
+            for (int a = warp; a < nh; a += nw) {
+                double t = 0.0, u = 0.0;
+                for (int c = lane; c < nh; c += 32) {
+                    t += Ah4[size_t(a) * nh + c] * ph[c];
+                    u += H.A3[size_t(a) * nh + c] * ph[c];
+                }
+                t = warp_sum(t);
+                u = warp_sum(u);
+                if (lane == 0) {
+                    const double* ov = H.orb_vecs + size_t(i) * 6 * nh;
+                    f[a] += H.sq[size_t(i) * nh + a];
+                    f[a] += 2.0 * t2 * t;
+                    f[a] += t2 * t2 * ov[5 * nh + a];
+                    tmp[a] = u;
+                }
+            }
+            __syncthreads();
+            g += block_dot(ph, tmp, nh);
+            g += 2.0 * t2 * block_dot(H.orb_vecs + size_t(i) * 6 * nh + nh, ph, nh);
+            g += t2 * t2 * H.orb_scal[5 * i + 1];
+        }
+        for (int a = threadIdx.x; a < nh; a += blockDim.x) f[a] = four_pi * (H.occ * f[a]) - H.shared_vecs[nh + a];
+        g = four_pi * (H.occ * g) - H.shared_scal[1];
+        __syncthreads();
+        // t = C_H^-1 f (L_C L_C^T)
+        if (warp == 0) {
+            for (int r = 0; r < nh; ++r) {
+                double t = 0.0;
+                for (int k = lane; k < r; k += 32) t += H.LC[size_t(r) * nh + k] * f[k];
+                t = warp_sum(t);
+                if (lane == 0) f[r] = (f[r] - t) / H.LC[size_t(r) * nh + r];
+                __syncwarp();
+            }
+            for (int r = nh - 1; r >= 0; --r) {
+                double t = 0.0;
+                for (int k = r + 1 + lane; k < nh; k += 32) t += H.LC[size_t(k) * nh + r] * f[k];
+                t = warp_sum(t);
+                if (lane == 0) f[r] = (f[r] - t) / H.LC[size_t(r) * nh + r];
+                __syncwarp();
+            }
+        }
+        __syncthreads();
+        const double dt = block_dot(H.shared_vecs, f, nh);
+        const double th1 = (g - dt) / H.schur[0];
+        for (int a = threadIdx.x; a < nh; a += blockDim.x) H.wH_new[a] = f[a] - th1 * H.hu[a];
+        if (threadIdx.x == 0) H.theta1_new[0] = th1;
+    }
+    __syncthreads();
+    // delta^2 = sum_i dphi^T (C_H + M_H) dphi + 2 dth (d_phi + c_Hh).dphi + dth^2 (zeta_phi + gamma)
+    double tot = 0.0;
+    for (int i = 0; i < H.N; ++i) {
+        for (int a = threadIdx.x; a < nh; a += blockDim.x)
+            dp[a] = H.phi_new[size_t(i) * nh + a] - H.phi_old[size_t(i) * nh + a];
+        __syncthreads();
+        const double dth = H.th2_new[i] - H.th2_old[i];
+        for (int a = warp; a < nh; a += nw) {
+            double t = 0.0, u = 0.0;
+            for (int c = lane; c < nh; c += 32) {
+                t += H.CH[size_t(a) * nh + c] * dp[c];
+                u += H.MH[size_t(a) * nh + c] * dp[c];
+            }
+            t = warp_sum(t);
+            u = warp_sum(u);
+            if (lane == 0) {
+                tmp[a] = t;
+                f[a] = u;
+            }
+        }
+        __syncthreads();
+        const double* ov = H.orb_vecs + size_t(i) * 6 * nh;
+        const double* sc = H.orb_scal + size_t(i) * 5;
+        const double semi = block_dot(dp, tmp, nh) + 2.0 * dth * block_dot(ov + 4 * nh, dp, nh) + dth * dth * sc[4];
+        const double l2 = block_dot(dp, f, nh) + 2.0 * dth * block_dot(ov + 3 * nh, dp, nh) + dth * dth * sc[3];
+        tot += semi + l2;
+    }
+    if (threadIdx.x == 0) H.delta[0] = tot;
+}
+
+}  // namespace
+
+// ==========================================================================================
+// host orchestration
+
+void InnerWork::ensure(int nh_, int N_, int nev_, int nct) {
+    nh = nh_;
+    N = N_;
+    nev = nev_;
+    const int64_t nh2 = std::max<int64_t>(1, int64_t(nh) * nh);
+    const int64_t v = std::max<int64_t>(1, int64_t(N) * nh);
+    auto need = [](DevBuf<double>& b, int64_t n) {
+        if (b.n < n) b.alloc(n);
+    };
+    need(AH, nh2);
+    need(W, nh2);
+    need(C, nh2);
+    need(V, nh2);
+    need(d, nh + 1);
+    need(e, nh + 1);
+    need(E16, int64_t(nct) * 16);
+    need(E4, int64_t(nct) * 4 * std::max(1, N));
+    need(sq, v);
+    need(l, v);
+    need(u, v);
+    need(s, std::max(1, N));
+    need(c12, v);
+    need(c22, std::max(1, N));
+    need(lhat, v);
+    need(lam, int64_t(std::max(1, N)) * nev);
+    need(Y, int64_t(std::max(1, N)) * nev * std::max(1, nh));
+    need(piv, int64_t(std::max(1, N)) * nev * std::max(1, nh));
+    need(score, int64_t(std::max(1, N)) * nev);
+    need(ynorm, int64_t(std::max(1, N)) * nev);
+    need(hu, std::max(1, nh));
+    need(scal, 16);
+    for (int k = 0; k < 2; ++k) {
+        need(phi[k], v);
+        need(th2[k], std::max(1, N));
+        need(lamv[k], std::max(1, N));
+        need(wH[k], std::max(1, nh));
+        need(th1[k], 1);
+    }
+    if (flag.n < 4) flag.alloc(4);
+}
+
+namespace {
+
+int check_flag(Ctx& c, DevBuf<int>& flag) {
+    int h[4];
+    KSB_CUDA_CHECK(cudaMemcpyAsync(h, flag.p, sizeof h, cudaMemcpyDeviceToHost, c.stream));
+    KSB_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    KSB_CUDA_CHECK(cudaMemsetAsync(flag.p, 0, sizeof h, c.stream));
+    return h[0];
+}
+
+}  // namespace
+
+void coarse_level_setup(Level& L, CoarseOps& co) {
+    Ctx& c = *L.ctx;
+    ensure_rule(c.stream);
+    const int nh = L.nH, nct = L.nct;
+    const int64_t nh2 = std::max<int64_t>(1, int64_t(nh) * nh);
+    co.MH.alloc(nh2);
+    co.CH.alloc(nh2);
+    co.LH.alloc(nh2);
+    co.LC.alloc(nh2);
+    DevBuf<double> E;
+    E.alloc(int64_t(nct) * 16);
+    DevBuf<double> ones;
+    ones.alloc(std::max(1, nh));
+    std::vector<double> h1(std::max(1, nh), 1.0);
+    KSB_CUDA_CHECK(cudaMemcpyAsync(ones.p, h1.data(), sizeof(double) * h1.size(), cudaMemcpyHostToDevice, c.stream));
+    // M_H: the coarse unit mass restricted to interior dofs; the interior-only weight equals 1 on every
+    // tet vertex that survives the interior restriction, but boundary vertices of the same tets carry
+    // weight 1 in the reference's unit mass too -- use a dedicated all-ones weight per coarse vertex.
+    DevBuf<double> wall;
+    wall.alloc(std::max(1, L.ncv));
+    std::vector<double> hw(std::max(1, L.ncv), 1.0);
+    KSB_CUDA_CHECK(cudaMemcpyAsync(wall.p, hw.data(), sizeof(double) * hw.size(), cudaMemcpyHostToDevice, c.stream));
+    DevBuf<int32_t> ident;
+    ident.alloc(std::max(1, L.ncv));
+    std::vector<int32_t> hid(std::max(1, L.ncv));
+    for (int k = 0; k < L.ncv; ++k) hid[k] = k;
+    KSB_CUDA_CHECK(cudaMemcpyAsync(ident.p, hid.data(), sizeof(int32_t) * hid.size(), cudaMemcpyHostToDevice, c.stream));
+    launch(c, "coarse", k_coarse_wmass, ceil_div(nct, 128), 128, 0, nct, (const int32_t*)L.ctets.p,
+           (const double*)L.cxyz.p, (const int32_t*)ident.p, (const double*)wall.p, E.p);
+    DevBuf<double> zero, th0;
+    zero.alloc(nh2);
+    KSB_CUDA_CHECK(cudaMemsetAsync(zero.p, 0, sizeof(double) * nh2, c.stream));
+    th0.alloc(1);
+    KSB_CUDA_CHECK(cudaMemsetAsync(th0.p, 0, sizeof(double), c.stream));
+    // M_H = 0 + 0 + assembled(E)
+    if (nh > 0)
+        launch(c, "coarse", k_build_AH, nh, 128, sizeof(double) * nh, nh, (const int32_t*)L.cinc_ptr.p,
+               (const int32_t*)L.cinc.p, (const int32_t*)L.ctets.p, (const int32_t*)L.ciidx.p, (const double*)zero.p,
+               (const double*)zero.p, (const double*)zero.p, (const double*)E.p, 1, (const double*)th0.p, co.MH.p);
+    launch(c, "coarse", k_coarse_stiff, ceil_div(nct, 128), 128, 0, nct, (const int32_t*)L.ctets.p,
+           (const double*)L.cxyz.p, E.p);
+    if (nh > 0)
+        launch(c, "coarse", k_build_AH, nh, 128, sizeof(double) * nh, nh, (const int32_t*)L.cinc_ptr.p,
+               (const int32_t*)L.cinc.p, (const int32_t*)L.ctets.p, (const int32_t*)L.ciidx.p, (const double*)zero.p,
+               (const double*)zero.p, (const double*)zero.p, (const double*)E.p, 1, (const double*)th0.p, co.CH.p);
+    KSB_CUDA_CHECK(cudaMemcpyAsync(co.LH.p, co.MH.p, sizeof(double) * nh2, cudaMemcpyDeviceToDevice, c.stream));
+    KSB_CUDA_CHECK(cudaMemcpyAsync(co.LC.p, co.CH.p, sizeof(double) * nh2, cudaMemcpyDeviceToDevice, c.stream));
+    DevBuf<int> flag;
+    flag.alloc(4);
+    KSB_CUDA_CHECK(cudaMemsetAsync(flag.p, 0, sizeof(int) * 4, c.stream));
+    if (nh > 0) {
+        launch(c, "coarse", k_potrf, 1, 1024, 0, nh, co.LH.p, flag.p);
+        launch(c, "coarse", k_potrf, 1, 1024, 0, nh, co.LC.p, flag.p);
+    }
+    if (check_flag(c, flag)) raise(KSB_INTERNAL, "coarse mass or stiffness factorization failed");
+    co.ready = true;
+}
+
+InnerStats inner_scf(Level& L, const CoarseOps& co, const ProjOut& P, const InnerParams& prm, const double* h_lambda,
+                     InnerWork& w, bool start_pure) {
+    Ctx& c = *L.ctx;
+    ensure_rule(c.stream);
+    const int nh = L.nH, N = P.N, nct = L.nct;
+    const int nev = std::min(nh + 1, N + prm.nev_pad);
+    w.ensure(nh, N, nev, nct);
+    KSB_CUDA_CHECK(cudaMemsetAsync(w.flag.p, 0, sizeof(int) * 4, c.stream));
+    InnerStats st;
+    if (nh == 0) raise(KSB_INVALID_ARGUMENT, "degenerate coarse space: use the host path");
+
+    const double* A1 = P.shared_mats.p;
+    const double* A3 = P.shared_mats.p + int64_t(nh) * nh;
+    const double* A4 = P.shared_mats.p + 2 * int64_t(nh) * nh;
+    // per outer: l_i = L_H^-1 c_i, s_i, u_i = L_H^-T l_i
+    const size_t smem_trsv = sizeof(double) * nh * 4;
+    launch(c, "inner", k_trsv_many, ceil_div(N, 4), 128, smem_trsv, nh, N, (const double*)co.LH.p, 0,
+           (const double*)(P.orb_vecs.p + 3 * nh), int64_t(6) * nh, int64_t(1), w.l.p, int64_t(nh), int64_t(1), 1.0);
+    launch(c, "inner", k_border_scale, N, 128, 0, nh, N, (const double*)w.l.p, (const double*)P.orb_scal.p, w.s.p,
+           w.flag.p);
+    launch(c, "inner", k_trsv_many, ceil_div(N, 4), 128, smem_trsv, nh, N, (const double*)co.LH.p, 1,
+           (const double*)w.l.p, int64_t(nh), int64_t(1), w.u.p, int64_t(nh), int64_t(1), 1.0);
+    if (check_flag(c, w.flag)) raise(KSB_AMBIGUOUS_SELECTION, "bordered mass matrix is not positive definite");
+    if (prm.hartree) {
+        launch(c, "inner", k_trsv_many, 1, 32, sizeof(double) * nh, nh, 1, (const double*)co.LC.p, 0,
+               (const double*)P.shared_vecs.p, int64_t(nh), int64_t(1), w.hu.p, int64_t(nh), int64_t(1), 1.0);
+        launch(c, "inner", k_trsv_many, 1, 32, sizeof(double) * nh, nh, 1, (const double*)co.LC.p, 1,
+               (const double*)w.hu.p, int64_t(nh), int64_t(1), w.hu.p, int64_t(nh), int64_t(1), 1.0);
+        launch(c, "inner", k_schur, 1, 128, 0, nh, (const double*)P.shared_vecs.p, (const double*)w.hu.p,
+               (const double*)P.shared_scal.p, w.scal.p, w.flag.p);
+        if (check_flag(c, w.flag))
+            raise(KSB_AMBIGUOUS_SELECTION, "electrostatic augmentation vector lies in the coarse space");
+    }
+    // initial state: pure augmentation (phi_H = 0, theta2 = 1, w_H = 0, theta1 = hartree ? 1 : 0)
+    int cur = 0;
+    if (start_pure) {
+        KSB_CUDA_CHECK(cudaMemsetAsync(w.phi[0].p, 0, sizeof(double) * N * nh, c.stream));
+        KSB_CUDA_CHECK(cudaMemsetAsync(w.wH[0].p, 0, sizeof(double) * nh, c.stream));
+        std::vector<double> ones(N, 1.0);
+        KSB_CUDA_CHECK(cudaMemcpyAsync(w.th2[0].p, ones.data(), sizeof(double) * N, cudaMemcpyHostToDevice, c.stream));
+        const double t1 = prm.hartree ? 1.0 : 0.0;
+        KSB_CUDA_CHECK(cudaMemcpyAsync(w.th1[0].p, &t1, sizeof(double), cudaMemcpyHostToDevice, c.stream));
+        KSB_CUDA_CHECK(cudaMemcpyAsync(w.lamv[0].p, h_lambda, sizeof(double) * N, cudaMemcpyHostToDevice, c.stream));
+    }
+    const size_t tri_smem = sizeof(double) * 2 * nh;
+    for (int sweep = 1; sweep <= prm.max_iterations; ++sweep) {
+        const int nx = cur ^ 1;
+        // A_H
+        if (prm.hartree)
+            launch(c, "inner", k_coarse_wmass, ceil_div(nct, 128), 128, 0, nct, (const int32_t*)L.ctets.p,
+                   (const double*)L.cxyz.p, (const int32_t*)L.ciidx.p, (const double*)w.wH[cur].p, w.E16.p);
+        launch(c, "inner", k_build_AH, nh, 128, sizeof(double) * nh, nh, (const int32_t*)L.cinc_ptr.p,
+               (const int32_t*)L.cinc.p, (const int32_t*)L.ctets.p, (const int32_t*)L.ciidx.p, A1, A3, A4,
+               (const double*)w.E16.p, prm.hartree ? 1 : 0, (const double*)w.th1[cur].p, w.AH.p);
+        // C11 = L^-1 A_H L^-T: W^T = L^-1 A_H (rows of A_H are its columns), then C = L^-1 W
+        launch(c, "inner", k_trsv_many, ceil_div(nh, 4), 128, smem_trsv, nh, nh, (const double*)co.LH.p, 0,
+               (const double*)w.AH.p, int64_t(nh), int64_t(1), w.W.p, int64_t(1), int64_t(nh), 1.0);
+        launch(c, "inner", k_trsv_many, ceil_div(nh, 4), 128, smem_trsv, nh, nh, (const double*)co.LH.p, 0,
+               (const double*)w.W.p, int64_t(nh), int64_t(1), w.C.p, int64_t(1), int64_t(nh), 1.0);
+        launch(c, "inner", k_symmetrize, ceil_div(int64_t(nh) * nh, 256), 256, 0, nh, w.C.p);
+        launch(c, "inner_tridiag", k_tridiag, 1, 1024, tri_smem, nh, w.C.p, w.d.p, w.e.p, w.V.p);
+        SweepDev S{w.AH.p, A3, P.A_h4.p, P.orb_vecs.p, P.orb_scal.p, co.LH.p, w.V.p, w.l.p, w.u.p, w.s.p,
+                   w.wH[cur].p, w.th1[cur].p, w.c12.p, w.c22.p, w.lhat.p, nullptr, nh, N, prm.hartree ? 1 : 0};
+        launch(c, "inner", k_orbital_border, N, 256, sizeof(double) * 3 * nh, S);
+        const int warps = N * nev;
+        launch(c, "inner", k_arrow_eig, ceil_div(warps, 4), 128, 0, nh, N, nev, (const double*)w.d.p,
+               (const double*)w.e.p, (const double*)w.c12.p, (const double*)w.c22.p, w.lam.p);
+        launch(c, "inner", k_arrow_vec, ceil_div(warps, 4), 128, 0, nh, N, nev, (const double*)w.d.p,
+               (const double*)w.e.p, (const double*)w.c12.p, (const double*)w.lhat.p, (const double*)w.s.p,
+               (const double*)P.orb_scal.p, (const double*)w.lam.p, w.Y.p, w.piv.p, w.score.p, w.ynorm.p);
+        launch(c, "inner", k_select, N, 256, sizeof(double) * 2 * nh, S, nev, (const double*)w.lam.p,
+               (const double*)w.Y.p, (const double*)w.score.p, (const double*)w.ynorm.p, prm.score_floor,
+               (const double*)co.MH.p, (const double*)w.phi[cur].p, (const double*)w.th2[cur].p, w.lamv[nx].p,
+               w.phi[nx].p, w.th2[nx].p, w.flag.p);
+        if (prm.hartree)
+            launch(c, "inner", k_coarse_sq, dim3(ceil_div(nct, 128), N), 128, 0, nct, nh, N, (const int32_t*)L.ctets.p,
+                   (const double*)L.cxyz.p, (const int32_t*)L.ciidx.p, (const double*)w.phi[nx].p, w.E4.p);
+        if (prm.hartree)
+            launch(c, "inner", k_coarse_vec_asm, dim3(ceil_div(nh, 128), N), 128, 0, nh, nct,
+                   (const int32_t*)L.cinc_ptr.p, (const int32_t*)L.cinc.p, (const double*)w.E4.p, w.sq.p);
+        HartreeDev H{w.sq.p, P.A_h4.p, A3, P.orb_vecs.p, P.orb_scal.p, P.shared_vecs.p, P.shared_scal.p, co.LC.p,
+                     w.hu.p, w.scal.p, co.CH.p, co.MH.p, w.phi[nx].p, w.th2[nx].p, w.phi[cur].p, w.th2[cur].p,
+                     w.wH[nx].p, w.th1[nx].p, w.scal.p + 1, nullptr, nh, N, prm.hartree ? 1 : 0, prm.occ};
+        if (!prm.hartree) {
+            KSB_CUDA_CHECK(cudaMemcpyAsync(w.wH[nx].p, w.wH[cur].p, sizeof(double) * nh, cudaMemcpyDeviceToDevice, c.stream));
+            KSB_CUDA_CHECK(cudaMemcpyAsync(w.th1[nx].p, w.th1[cur].p, sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
+        }
+        launch(c, "inner", k_hartree_delta, 1, 512, sizeof(double) * 3 * nh, H);
+        double dsq = 0.0;
+        int fl[4];
+        KSB_CUDA_CHECK(cudaMemcpyAsync(&dsq, w.scal.p + 1, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+        KSB_CUDA_CHECK(cudaMemcpyAsync(fl, w.flag.p, sizeof fl, cudaMemcpyDeviceToHost, c.stream));
+        KSB_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+        if (fl[0] == 2) raise(KSB_AMBIGUOUS_SELECTION, "all scanned pairs have negligible augmentation component");
+        const double delta = std::sqrt(dsq);
+        st.history.push_back(delta);
+        st.iterations = sweep;
+        cur = nx;
+        w.cur = cur;
+        if (delta < prm.tol || !prm.hartree) return st;
+    }
+    raise(KSB_NONCONVERGENCE, "inner iteration exceeded the sweep cap");
+}
+
+}  // namespace ksb

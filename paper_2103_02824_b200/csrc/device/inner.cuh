@@ -1,0 +1,44 @@
+// Inner sweep (corr::inner_scf) on the device; see inner.cu.
+#pragma once
+
+#include <vector>
+
+#include "project.cuh"
+
+namespace ksb {
+
+/// per-level coarse operators: M_H, C_H (interior blocks, dense row-major) and their Cholesky factors
+struct CoarseOps {
+    DevBuf<double> MH, CH, LH, LC;
+    bool ready = false;
+};
+void coarse_level_setup(Level& L, CoarseOps& co);
+
+struct InnerParams {
+    double tol = 1e-8;
+    int max_iterations = 400;
+    double score_floor = 1e-8;
+    int nev_pad = 4;
+    bool hartree = true;
+    double occ = 2.0;
+};
+
+struct InnerStats {
+    int iterations = 0;
+    std::vector<double> history;
+};
+
+/// double-buffered augmented state + scratch; the result lives in buffers [cur]
+struct InnerWork {
+    int nh = 0, N = 0, nev = 0, cur = 0;
+    DevBuf<double> AH, W, C, V, d, e, E16, E4, sq, l, u, s, c12, c22, lhat, lam, Y, piv, score, ynorm, hu, scal;
+    DevBuf<double> phi[2], th2[2], lamv[2], wH[2], th1[2];
+    DevBuf<int> flag;
+    void ensure(int nh, int N, int nev, int nct);
+};
+
+/// runs sweeps from the pure augmentation state (phi_H = 0, theta2 = 1, w_H = 0, theta1 = hartree)
+InnerStats inner_scf(Level& L, const CoarseOps& co, const ProjOut& P, const InnerParams& prm, const double* h_lambda,
+                     InnerWork& w, bool start_pure = true);
+
+}  // namespace ksb

@@ -52,6 +52,11 @@ struct Level {
     DevBuf<int32_t> pint_col;
     DevBuf<double> pint_val;
     DevBuf<int32_t> ancestor, anc_ptr, anc_tets;
+    DevBuf<int32_t> vinc_ptr, vinc;           // interior vertex -> incident (tet*4 + local)
+    DevBuf<int32_t> cinc_ptr, cinc;           // coarse interior dof -> incident (coarse tet*4 + local)
+    DevBuf<int32_t> ctets, ciidx;             // coarse mesh (level 0)
+    DevBuf<double> cxyz;
+    double box_lo[3] = {0, 0, 0}, box_hi[3] = {0, 0, 0};
     DevBuf<double> ebuf;      // element matrices, 16 per tet (scratch)
     DevBuf<double> scratch;   // term accumulation scratch (nnz_ii + nnz_ib)
     DevBuf<int> flag;         // device error flag (singular quadrature)

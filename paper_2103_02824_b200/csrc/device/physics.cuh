@@ -1,0 +1,39 @@
+// Fine-level physics kernels (see physics.cu for reference anchors).
+#pragma once
+
+#include <array>
+
+#include "geom.cuh"
+#include "level.cuh"
+
+namespace ksb {
+
+struct Moments {
+    double q;
+    double c[3];
+    double dip[3];
+    double Q[3][3];
+};
+
+struct PhysWork {
+    DevBuf<double> part, out, e4;
+    void ensure(const Level& L);
+};
+
+/// rho = occ sum_i phi_i^2 and v_xc(rho), nodal, full-length outputs (boundary entries zero)
+void rho_vxc(Level& L, const double* Phi, int N, int ld, double occ, const XcParams& xc, double* rho_full,
+             double* vxc_full);
+Moments moments(Level& L, const double* rho_full, PhysWork& w, const double box_center[3]);
+/// multipole Dirichlet data at boundary vertices (boundary numbering)
+void boundary_values(Level& L, const Moments& m, double* bcb);
+/// out_int = scale * (occ sum_i phi_i^2, psi_j) on interior rows
+void sqload(Level& L, const double* Phi, int N, int ld, double occ, double scale, double* out_int, PhysWork& w);
+/// y_int -= A_ib(mat) bcb (Dirichlet lift, reference proj/src/solver.cpp:123)
+void lift(Level& L, int mat, const double* bcb, double* y_int);
+/// squared L2 norm and squared H1 seminorm of a full-length nodal function
+std::array<double, 2> norms_sq(Level& L, const double* f_full, PhysWork& w);
+/// kinetic, external, hartree, xc, total
+std::array<double, 5> energy(Level& L, const double* Phi, int N, int ld, const double* rho_full, const double* w_full,
+                             const std::vector<double>& atoms, double occ, const XcParams& xc, PhysWork& w);
+
+} // namespace ksb

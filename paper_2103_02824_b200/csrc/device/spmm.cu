@@ -70,7 +70,7 @@ void run_spmm(Ctx& c, const Level& L, const double* A, const double* B, const do
               int N, int ldx, double* Y, int ldy) {
     const int rows_per_block = 256 / G;
     const int64_t want = (int64_t(L.ni) + rows_per_block - 1) / rows_per_block;
-    const int grid = int(std::min<int64_t>(want, int64_t(c.sm_count) * 8));
+    const int grid = int(std::min<int64_t>(want, resident_grid(c, k_spmm<G, CPL, SHIFT>, 256, 0)));
     launch(c, "spmm", k_spmm<G, CPL, SHIFT>, std::max(grid, 1), 256, 0, L.ni, (const int32_t*)L.ii_ptr.p,
            (const int32_t*)L.ii_col.p, A, B, sigma, X, ldx, Y, ldy, N);
 }

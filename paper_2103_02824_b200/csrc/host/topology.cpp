@@ -237,6 +237,41 @@ std::shared_ptr<FineTopology> build_topology(const Hierarchy& h, int level) {
         }
     }
 
+    // interior vertex incidence (t*4 + local), ascending t
+    topo->vinc_ptr.assign(size_t(ni) + 1, 0);
+    for (int r = 0; r < ni; ++r) topo->vinc_ptr[r + 1] = topo->vinc_ptr[r] + (vptr[S.interior[r] + 1] - vptr[S.interior[r]]);
+    topo->vinc.resize(topo->vinc_ptr.back());
+#pragma omp parallel for schedule(static)
+    for (int r = 0; r < ni; ++r) {
+        const int v = S.interior[r];
+        int32_t w = topo->vinc_ptr[r];
+        for (int p = vptr[v]; p < vptr[v + 1]; ++p) {
+            const int t = vtet[p];
+            int li = 0;
+            while (m.tets[4 * t + li] != v) ++li;
+            topo->vinc[w++] = t * 4 + li;
+        }
+    }
+    // coarse interior incidence
+    {
+        const Mesh& cm = *topo->coarse->mesh;
+        const Space& Cs = *topo->coarse;
+        topo->cinc_ptr.assign(size_t(Cs.ni()) + 1, 0);
+        for (int t = 0; t < cm.n_tets(); ++t)
+            for (int k = 0; k < 4; ++k) {
+                const int a = Cs.iidx[cm.tets[4 * t + k]];
+                if (a >= 0) ++topo->cinc_ptr[a + 1];
+            }
+        for (int a = 0; a < Cs.ni(); ++a) topo->cinc_ptr[a + 1] += topo->cinc_ptr[a];
+        topo->cinc.resize(topo->cinc_ptr.back());
+        std::vector<int32_t> fill(topo->cinc_ptr.begin(), topo->cinc_ptr.end() - 1);
+        for (int t = 0; t < cm.n_tets(); ++t)
+            for (int k = 0; k < 4; ++k) {
+                const int a = Cs.iidx[cm.tets[4 * t + k]];
+                if (a >= 0) topo->cinc[fill[a]++] = t * 4 + k;
+            }
+    }
+
     // fine tets grouped by coarse ancestor
     topo->ancestor = h.ancestor(level);
     const int nct = h.mesh(0).n_tets();

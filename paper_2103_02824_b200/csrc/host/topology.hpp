@@ -67,6 +67,10 @@ struct FineTopology {
     std::vector<int32_t> ancestor;     // per fine tet, level-0 tet
     std::vector<int32_t> anc_ptr;      // coarse tet -> range in anc_tets
     std::vector<int32_t> anc_tets;     // fine tets grouped by coarse ancestor, ascending inside a group
+    // interior fine vertex -> incident (tet*4 + local), ascending tet (load-vector gather order)
+    std::vector<int32_t> vinc_ptr, vinc;
+    // coarse level: interior coarse dof -> incident (coarse tet*4 + local), ascending tet
+    std::vector<int32_t> cinc_ptr, cinc;
 };
 
 std::shared_ptr<FineTopology> build_topology(const Hierarchy& h, int level);

@@ -1,0 +1,203 @@
+"""Correction-step pieces through the C-ABI vs the CPU oracle on identical inputs.
+
+Fixture mirrors the reference's correction tests (proj/tests/test_correction.cpp:25-55):
+Z=2 nucleus at (0.31, -0.17, 0.05), two orbitals, a coarse box mesh plus one uniform
+refinement (and an adaptive variant). The physical starting state is the oracle's coarse SCF
+prolonged to the fine level, as driver::run does (proj/src/driver.cpp:367-371).
+"""
+import numpy as np
+import pytest
+
+import paper_2103_02824_b200 as kb
+from oracle import OMesh, Oracle
+
+pytestmark = pytest.mark.gpu
+
+ATOMS = [[2.0, 0.31, -0.17, 0.05]]
+
+
+class Case:
+    def __init__(self, ctx, xc="lda", n_coarse=4, lo=-5.0, hi=5.0, adapt=0, N=2, occ=1.0, hartree=True):
+        self.h = kb.Hierarchy()
+        self.orc = Oracle(ATOMS, n_pairs=N, occ=occ, xc=xc, hartree=hartree, xc_on=xc != "none")
+        a, b = kb.Mesh.box([lo] * 3, [hi] * 3, n_coarse), OMesh.box([lo] * 3, [hi] * 3, n_coarse)
+        self.h.push(a)
+        self.orc.push(b)
+        a, b = a.uniform_refine(), b.uniform_refine()
+        self.h.push(a)
+        self.orc.push(b)
+        rng = np.random.default_rng(23)
+        for _ in range(adapt):
+            marks = rng.integers(0, a.n_tets, 3)
+            a, b = a.adapt_refine(marks), b.adapt_refine(marks)
+            self.h.push(a)
+            self.orc.push(b)
+        self.lev = self.h.n_levels - 1
+        self.L = kb.Level(ctx, self.h, self.lev)
+        self.L.set_system(ATOMS, n_pairs=N, occupancy=occ, xc=xc, hartree=hartree, xc_on=xc != "none")
+        self.L.level_ops()
+        self.ctx = ctx
+        self.N = N
+        self.interior = self.L.index("interior")
+        lam, orb0, w0, _ = self.orc.coarse_scf(tol=1e-8, mixing=0.3)
+        self.lam = lam
+        self.orb = self.orc.prolong(orb0, 0, self.lev)
+        self.w = self.orc.prolong(w0, 0, self.lev)[:, 0]
+
+    def phi_block(self, orb):
+        return np.ascontiguousarray(orb[self.interior])
+
+    def dev(self, a):
+        return self.ctx.to_device(np.ascontiguousarray(a))
+
+    def full(self, interior_vals):
+        out = np.zeros(self.L.n)
+        out[self.interior] = interior_vals
+        return out
+
+
+def rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300)
+
+
+@pytest.mark.parametrize("xc", ["lda", "x_alpha"])
+def test_density_xc_moments_bc_sqload(ctx, xc):
+    c = Case(ctx, xc=xc)
+    Phi = c.dev(c.phi_block(c.orb))
+    rho, vxc = ctx.empty(c.L.n), ctx.empty(c.L.n)
+    c.L.density_xc(Phi, rho, vxc)
+    rho_o = c.orc.density(c.orb)
+    assert rel(rho.download(), rho_o) < 1e-14
+    assert rel(vxc.download(), c.orc.xc_potential(rho_o)) < 1e-13
+    m = c.L.moments(rho)
+    mo = c.orc.moments(c.lev, rho_o)
+    assert abs(m[0] - mo[0]) <= 1e-12 * abs(mo[0])
+    assert np.abs(m[:16] - mo[:16]).max() <= 1e-11 * max(1.0, np.abs(mo).max())
+    bcb = ctx.empty(c.L.nb)
+    c.L.boundary_values(m, bcb)
+    bc_o = c.orc.boundary_values(c.lev, mo)
+    bnd = np.setdiff1d(np.arange(c.L.n), c.interior)
+    assert rel(bcb.download(), bc_o[bnd]) < 1e-12
+    sq = ctx.empty(c.L.ni)
+    c.L.sqload(Phi, sq)
+    assert rel(sq.download(), c.orc.sqload(c.lev, c.orb)[c.interior]) < 1e-13
+
+
+def test_hartree_solve_matches_oracle(ctx):
+    c = Case(ctx)
+    Phi = c.dev(c.phi_block(c.orb))
+    rho = ctx.empty(c.L.n)
+    c.L.density_xc(Phi, rho)
+    m = c.L.moments(rho)
+    bcb = ctx.empty(c.L.nb)
+    c.L.boundary_values(m, bcb)
+    w = ctx.empty(c.L.n)
+    c.L.hartree_solve(Phi, bcb, w, tol=1e-12)
+    bc_o = c.orc.boundary_values(c.lev, c.orc.moments(c.lev, c.orc.density(c.orb)))
+    w_o, _ = c.orc.hartree_exact(c.lev, c.orb, bc_o, tol=1e-12)
+    assert rel(w.download(), w_o) < 1e-9
+    # boundary data is carried exactly (proj/tests/test_correction.cpp:131-132)
+    bnd = np.setdiff1d(np.arange(c.L.n), c.interior)
+    assert np.array_equal(w.download()[bnd], bcb.download())
+
+
+def test_outer_solve_matches_oracle(ctx):
+    c = Case(ctx)
+    Phi = c.dev(c.phi_block(c.orb))
+    rho_o = c.orc.density(c.orb)
+    vxc_o = c.orc.xc_potential(rho_o)
+    PhiT = ctx.empty((c.L.ni, c.N))
+    att, its, md = c.L.outer_solve(c.dev(c.w), c.dev(vxc_o), c.lam, Phi, PhiT, tol_linear=1e-12)
+    ph_o, att_o, its_o, sig_o = c.orc.outer_solve(c.lev, c.w, vxc_o, c.lam, c.orb, tol=1e-12)
+    assert list(att) == list(att_o)
+    assert abs(abs(md) - sig_o[0]) <= 1e-12 * sig_o[0]
+    assert rel(PhiT.download(), ph_o[c.interior]) < 1e-8
+
+
+def oracle_inputs(c):
+    """phi_tilde, w_tilde, vxc, bc from the oracle's own pipeline (one consistent outer state)."""
+    rho_o = c.orc.density(c.orb)
+    vxc_o = c.orc.xc_potential(rho_o)
+    ph_o, _, _, _ = c.orc.outer_solve(c.lev, c.w, vxc_o, c.lam, c.orb, tol=1e-12)
+    bc_o = c.orc.boundary_values(c.lev, c.orc.moments(c.lev, c.orc.density(ph_o)))
+    wt_o, _ = c.orc.hartree_exact(c.lev, ph_o, bc_o, tol=1e-12)
+    return ph_o, wt_o, vxc_o, bc_o
+
+
+@pytest.mark.parametrize("adapt", [0, 2])
+def test_prepare_blocks_matches_oracle(ctx, adapt):
+    c = Case(ctx, adapt=adapt)
+    ph_o, wt_o, vxc_o, bc_o = oracle_inputs(c)
+    bnd = np.setdiff1d(np.arange(c.L.n), c.interior)
+    ell = np.zeros(c.L.n)
+    ell[bnd] = bc_o[bnd]
+    c.L.prepare_blocks(c.dev(c.phi_block(ph_o)), c.dev(wt_o - ell), c.dev(ell), c.dev(vxc_o))
+    B = c.orc.prepare_blocks(c.lev, ph_o, wt_o, vxc_o, bc_o)
+    for name in ["A_H1", "A_H3", "A_H4", "M_H", "C_H", "d_Hh", "lift_load", "A_h4", "b_H1", "b_H3", "b_H4", "rhs",
+                 "c_Hh", "d_phi", "beta1", "beta3", "beta4", "gamma", "zeta_phi"]:
+        g, o = c.L.blocks(name), B.get(name)
+        assert g.shape == o.shape, name
+        assert np.abs(g - o).max() <= 1e-11 * max(1e-300, np.abs(o).max()), name
+    sc = B.get("scalars")
+    g = c.L.blocks("scalars")
+    assert abs(g[0] - sc[0]) <= 1e-11 * abs(sc[0]) and abs(g[1] - sc[1]) <= 1e-11 * max(abs(sc[1]), 1e-300)
+
+
+def test_inner_scf_and_expand_match_oracle(ctx):
+    c = Case(ctx)
+    ph_o, wt_o, vxc_o, bc_o = oracle_inputs(c)
+    bnd = np.setdiff1d(np.arange(c.L.n), c.interior)
+    ell = np.zeros(c.L.n)
+    ell[bnd] = bc_o[bnd]
+    dPhiT, dwt, dell = c.dev(c.phi_block(ph_o)), c.dev(wt_o - ell), c.dev(ell)
+    c.L.prepare_blocks(dPhiT, dwt, dell, c.dev(vxc_o))
+    g = c.L.inner_scf(c.lam)
+    B = c.orc.prepare_blocks(c.lev, ph_o, wt_o, vxc_o, bc_o)
+    o = B.inner_scf(c.lam)
+    assert abs(g["iterations"] - o["iterations"]) <= 1
+    assert np.abs(g["lambda_"] - o["lambda_"]).max() <= 1e-9 * np.abs(o["lambda_"]).max()
+    assert rel(g["theta2"], o["theta2"]) < 1e-7
+    assert rel(g["phi_H"], o["phi_H"]) < 1e-7
+    assert rel(g["w_H"], o["w_H"]) < 1e-7
+    assert abs(g["theta1"] - o["theta1"]) <= 1e-7 * abs(o["theta1"])
+    Phi, w = ctx.empty((c.L.ni, c.N)), ctx.empty(c.L.n)
+    bcb = c.dev(bc_o[bnd])
+    c.L.expand(dPhiT, dwt, bcb, Phi, w)
+    orb_o, w_o = B.expand_last()
+    assert rel(Phi.download(), orb_o[c.interior]) < 1e-7
+    assert rel(w.download(), w_o) < 1e-7
+
+
+def test_energy_and_norms(ctx):
+    c = Case(ctx)
+    Phi = c.dev(c.phi_block(c.orb))
+    e = c.L.energy(Phi, c.dev(c.w))
+    eo = c.orc.energy(c.lev, c.orb, c.w)
+    assert np.abs(e - eo).max() <= 1e-12 * np.abs(eo).max()
+    f = np.sin(np.arange(c.L.n) * 0.37)
+    nn = c.L.norms(c.dev(f))
+    no = c.orc.norms(c.lev, f)
+    assert abs(np.sqrt(nn[0]) - no[0]) <= 1e-12 * no[0]
+    assert abs(np.sqrt(nn[1]) - no[1]) <= 1e-12 * no[1]
+    assert abs(nn[2] - no[2]) <= 1e-12 * no[2]
+
+
+@pytest.mark.parametrize("xc,hartree", [("lda", True), ("none", False)])
+def test_correction_step_matches_oracle(ctx, xc, hartree):
+    """Two outer iterations through the full step: eigenvalues 1e-8, orbitals/density 1e-6 (north star)."""
+    c = Case(ctx, xc=xc, hartree=hartree)
+    lam_g, lam_o = c.lam.copy(), c.lam.copy()
+    orb_o, w_o = c.orb.copy(), c.w.copy()
+    Phi = c.dev(c.phi_block(c.orb))
+    w = c.dev(c.w)
+    for outer in range(2):
+        lg = c.L.correction_step(lam_g, Phi, w, tol_linear=1e-12)
+        lam_o, orb_o, w_o, lo = c.orc.correction_step(c.lev, lam_o, orb_o, w_o, tol_linear=1e-12)
+        assert lg["attempts"] == lo["attempts"], outer
+        assert abs(lg["inner_iterations"] - lo["inner_iterations"]) <= 1
+        assert np.abs(lam_g - lam_o).max() <= 1e-8 * np.abs(lam_o).max(), (outer, lam_g, lam_o)
+        P = Phi.download()
+        sgn = np.sign(np.sum(P * orb_o[c.interior], axis=0))
+        assert rel(P * sgn, orb_o[c.interior]) < 1e-6
+        assert rel(w.download(), w_o) < 1e-6
+        assert abs(lg["delta"] - lo["delta"]) <= 1e-6 * lo["delta"]
