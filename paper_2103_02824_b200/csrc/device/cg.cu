@@ -223,6 +223,12 @@ __global__ void __launch_bounds__(kThreads) k_spmm_dot(int ni, Cols cc, const in
         }
         s.alpha[c] = al;
     }
+    __syncthreads();
+    if (threadIdx.x == 0) {  // a breakdown retires its column: let the host loop stop once none is active
+        int na = 0;
+        for (int c = 0; c < N; ++c) na += s.status[c] == kActive;
+        s.ctl[kNActive] = na;
+    }
 }
 
 // ---------------- K2: x, r update ----------------

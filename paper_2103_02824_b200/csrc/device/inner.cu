@@ -12,6 +12,8 @@
 #include <algorithm>
 #include <cfloat>
 
+#include <cooperative_groups.h>
+
 #include "geom.cuh"
 #include "inner.cuh"
 
@@ -169,6 +171,116 @@ __global__ void __launch_bounds__(1024) k_tridiag(int n, double* __restrict__ C,
         }
         if (n >= 1) d[n - 1] = C[size_t(n - 1) * n + n - 1];
     }
+}
+
+constexpr int kTriCluster = 8;
+
+/// Cluster-of-8 Householder tridiagonalisation: each CTA keeps a slab of rows of C in shared
+/// memory (343 x 343 doubles = 941 KB spread over 8 SMs); the Householder vector and p = C v
+/// move between CTAs through distributed shared memory, two cluster barriers per step.
+/// Every CTA recomputes the reflector redundantly (same inputs, same order), so all copies agree.
+__global__ void __cluster_dims__(kTriCluster, 1, 1) __launch_bounds__(512)
+    k_tridiag_cluster(int n, int R, const double* __restrict__ Cin, double* __restrict__ d, double* __restrict__ e,
+                      double* __restrict__ V) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    extern __shared__ double sh[];
+    const int q = int(cluster.block_rank());
+    const int r0 = q * R, r1 = min(n, r0 + R);
+    double* A = sh;               // R x n, rows r0..r1-1
+    double* v = sh + size_t(R) * n;
+    double* p = v + n;            // own segment of p (indices r0..r1-1 valid)
+    double* pf = p + n;           // full p / q
+    __shared__ double red[32];
+    __shared__ double bc[2];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    for (int idx = tid; idx < (r1 - r0) * n; idx += blockDim.x) A[idx] = Cin[size_t(r0) * n + idx];
+    cluster.sync();
+    for (int k = 0; k + 2 < n; ++k) {
+        const int m0 = k + 1, m = n - m0;
+        const int owner = k / R;
+        const double* rowk = cluster.map_shared_rank(A, owner) + size_t(k - owner * R) * n;
+        double s = 0.0;
+        for (int i = tid; i < m; i += blockDim.x) {
+            const double x = rowk[m0 + i];
+            v[m0 + i] = x;
+            s += x * x;
+        }
+        s = warp_sum(s);
+        if (lane == 0) red[warp] = s;
+        __syncthreads();
+        if (tid == 0) {
+            double t = 0.0;
+            for (int w = 0; w < nw; ++w) t += red[w];
+            const double nx = sqrt(t);
+            const double x0 = v[m0];
+            const double alpha = x0 >= 0.0 ? -nx : nx;
+            const double nv2 = t - x0 * x0 + (x0 - alpha) * (x0 - alpha);
+            bc[0] = alpha;
+            bc[1] = (nx == 0.0 || nv2 <= 0.0) ? 0.0 : 1.0 / sqrt(nv2);
+            v[m0] = x0 - alpha;
+            if (q == 0) {
+                d[k] = rowk[k];
+                e[k] = bc[1] == 0.0 ? v[m0] + alpha : alpha;
+            }
+        }
+        __syncthreads();
+        const double inv = bc[1];
+        if (inv == 0.0) {
+            if (q == 0)
+                for (int i = tid; i < m; i += blockDim.x) V[size_t(k) * n + m0 + i] = 0.0;
+            cluster.sync();  // keep the two-barrier rhythm identical across CTAs
+            cluster.sync();
+            continue;
+        }
+        for (int i = tid; i < m; i += blockDim.x) {
+            v[m0 + i] *= inv;
+            if (q == 0) V[size_t(k) * n + m0 + i] = v[m0 + i];
+        }
+        __syncthreads();
+        const int ra = max(m0, r0);
+        for (int r = ra + warp; r < r1; r += nw) {
+            const double* row = A + size_t(r - r0) * n;
+            double t = 0.0;
+            for (int c = m0 + lane; c < n; c += 32) t += row[c] * v[c];
+            t = warp_sum(t);
+            if (lane == 0) p[r] = t;
+        }
+        cluster.sync();  // every CTA's p segment is complete
+        s = 0.0;
+        for (int i = m0 + tid; i < n; i += blockDim.x) {
+            const double pi = cluster.map_shared_rank(p, i / R)[i];
+            pf[i] = pi;
+            s += v[i] * pi;
+        }
+        s = warp_sum(s);
+        if (lane == 0) red[warp] = s;
+        __syncthreads();
+        if (tid == 0) {
+            double t = 0.0;
+            for (int w = 0; w < nw; ++w) t += red[w];
+            bc[0] = t;
+        }
+        __syncthreads();
+        const double K = bc[0];
+        for (int i = m0 + tid; i < n; i += blockDim.x) pf[i] -= K * v[i];
+        __syncthreads();
+        const int nr = r1 - ra;
+        for (int idx = tid; idx < nr * m; idx += blockDim.x) {
+            const int rr = ra + idx / m, c = m0 + idx % m;
+            A[size_t(rr - r0) * n + c] -= 2.0 * (v[rr] * pf[c] + pf[rr] * v[c]);
+        }
+        cluster.sync();  // updated rows visible before the next step reads row k+1 remotely
+    }
+    if (q == 0 && tid == 0) {
+        auto at = [&](int r, int c) { return cluster.map_shared_rank(A, r / R)[size_t(r % R) * n + c]; };
+        if (n >= 2) {
+            d[n - 2] = at(n - 2, n - 2);
+            e[n - 2] = at(n - 1, n - 2);
+        }
+        if (n >= 1) d[n - 1] = at(n - 1, n - 1);
+    }
+    cluster.sync();  // keep remote shared memory alive until rank 0 has read it
 }
 
 /// apply Q^T (forward = 1: H_0 first) or Q (forward = 0: H_{n-3} first) to vectors, warp per vector.
@@ -862,19 +974,19 @@ InnerStats inner_scf(Level& L, const CoarseOps& co, const ProjOut& P, const Inne
     const double* A4 = P.shared_mats.p + 2 * int64_t(nh) * nh;
     // per outer: l_i = L_H^-1 c_i, s_i, u_i = L_H^-T l_i
     const size_t smem_trsv = sizeof(double) * nh * 4;
-    launch(c, "inner", k_trsv_many, ceil_div(N, 4), 128, smem_trsv, nh, N, (const double*)co.LH.p, 0,
+    launch(c, "inner:trsv_many", k_trsv_many, ceil_div(N, 4), 128, smem_trsv, nh, N, (const double*)co.LH.p, 0,
            (const double*)(P.orb_vecs.p + 3 * nh), int64_t(6) * nh, int64_t(1), w.l.p, int64_t(nh), int64_t(1), 1.0);
-    launch(c, "inner", k_border_scale, N, 128, 0, nh, N, (const double*)w.l.p, (const double*)P.orb_scal.p, w.s.p,
+    launch(c, "inner:border_scale", k_border_scale, N, 128, 0, nh, N, (const double*)w.l.p, (const double*)P.orb_scal.p, w.s.p,
            w.flag.p);
-    launch(c, "inner", k_trsv_many, ceil_div(N, 4), 128, smem_trsv, nh, N, (const double*)co.LH.p, 1,
+    launch(c, "inner:trsv_many", k_trsv_many, ceil_div(N, 4), 128, smem_trsv, nh, N, (const double*)co.LH.p, 1,
            (const double*)w.l.p, int64_t(nh), int64_t(1), w.u.p, int64_t(nh), int64_t(1), 1.0);
     if (check_flag(c, w.flag)) raise(KSB_AMBIGUOUS_SELECTION, "bordered mass matrix is not positive definite");
     if (prm.hartree) {
-        launch(c, "inner", k_trsv_many, 1, 32, sizeof(double) * nh, nh, 1, (const double*)co.LC.p, 0,
+        launch(c, "inner:trsv_many", k_trsv_many, 1, 32, sizeof(double) * nh, nh, 1, (const double*)co.LC.p, 0,
                (const double*)P.shared_vecs.p, int64_t(nh), int64_t(1), w.hu.p, int64_t(nh), int64_t(1), 1.0);
-        launch(c, "inner", k_trsv_many, 1, 32, sizeof(double) * nh, nh, 1, (const double*)co.LC.p, 1,
+        launch(c, "inner:trsv_many", k_trsv_many, 1, 32, sizeof(double) * nh, nh, 1, (const double*)co.LC.p, 1,
                (const double*)w.hu.p, int64_t(nh), int64_t(1), w.hu.p, int64_t(nh), int64_t(1), 1.0);
-        launch(c, "inner", k_schur, 1, 128, 0, nh, (const double*)P.shared_vecs.p, (const double*)w.hu.p,
+        launch(c, "inner:schur", k_schur, 1, 128, 0, nh, (const double*)P.shared_vecs.p, (const double*)w.hu.p,
                (const double*)P.shared_scal.p, w.scal.p, w.flag.p);
         if (check_flag(c, w.flag))
             raise(KSB_AMBIGUOUS_SELECTION, "electrostatic augmentation vector lies in the coarse space");
@@ -891,40 +1003,54 @@ InnerStats inner_scf(Level& L, const CoarseOps& co, const ProjOut& P, const Inne
         KSB_CUDA_CHECK(cudaMemcpyAsync(w.lamv[0].p, h_lambda, sizeof(double) * N, cudaMemcpyHostToDevice, c.stream));
     }
     const size_t tri_smem = sizeof(double) * 2 * nh;
+    const int cl_R = (nh + kTriCluster - 1) / kTriCluster;
+    const size_t cl_smem = sizeof(double) * (size_t(cl_R) * nh + 3 * size_t(nh));
+    if (cl_smem <= size_t(200) * 1024) {
+        static bool attr = false;
+        if (!attr) {
+            KSB_CUDA_CHECK(cudaFuncSetAttribute(k_tridiag_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                int(200 * 1024)));
+            attr = true;
+        }
+    }
     for (int sweep = 1; sweep <= prm.max_iterations; ++sweep) {
         const int nx = cur ^ 1;
         // A_H
         if (prm.hartree)
-            launch(c, "inner", k_coarse_wmass, ceil_div(nct, 128), 128, 0, nct, (const int32_t*)L.ctets.p,
+            launch(c, "inner:coarse_wmass", k_coarse_wmass, ceil_div(nct, 128), 128, 0, nct, (const int32_t*)L.ctets.p,
                    (const double*)L.cxyz.p, (const int32_t*)L.ciidx.p, (const double*)w.wH[cur].p, w.E16.p);
-        launch(c, "inner", k_build_AH, nh, 128, sizeof(double) * nh, nh, (const int32_t*)L.cinc_ptr.p,
+        launch(c, "inner:build_", k_build_AH, nh, 128, sizeof(double) * nh, nh, (const int32_t*)L.cinc_ptr.p,
                (const int32_t*)L.cinc.p, (const int32_t*)L.ctets.p, (const int32_t*)L.ciidx.p, A1, A3, A4,
                (const double*)w.E16.p, prm.hartree ? 1 : 0, (const double*)w.th1[cur].p, w.AH.p);
         // C11 = L^-1 A_H L^-T: W^T = L^-1 A_H (rows of A_H are its columns), then C = L^-1 W
-        launch(c, "inner", k_trsv_many, ceil_div(nh, 4), 128, smem_trsv, nh, nh, (const double*)co.LH.p, 0,
+        launch(c, "inner:trsv_many", k_trsv_many, ceil_div(nh, 4), 128, smem_trsv, nh, nh, (const double*)co.LH.p, 0,
                (const double*)w.AH.p, int64_t(nh), int64_t(1), w.W.p, int64_t(1), int64_t(nh), 1.0);
-        launch(c, "inner", k_trsv_many, ceil_div(nh, 4), 128, smem_trsv, nh, nh, (const double*)co.LH.p, 0,
+        launch(c, "inner:trsv_many", k_trsv_many, ceil_div(nh, 4), 128, smem_trsv, nh, nh, (const double*)co.LH.p, 0,
                (const double*)w.W.p, int64_t(nh), int64_t(1), w.C.p, int64_t(1), int64_t(nh), 1.0);
-        launch(c, "inner", k_symmetrize, ceil_div(int64_t(nh) * nh, 256), 256, 0, nh, w.C.p);
-        launch(c, "inner_tridiag", k_tridiag, 1, 1024, tri_smem, nh, w.C.p, w.d.p, w.e.p, w.V.p);
+        launch(c, "inner:symmetrize", k_symmetrize, ceil_div(int64_t(nh) * nh, 256), 256, 0, nh, w.C.p);
+        if (cl_smem <= size_t(200) * 1024)
+            launch(c, "inner_tridiag", k_tridiag_cluster, kTriCluster, 512, cl_smem, nh, cl_R, (const double*)w.C.p,
+                   w.d.p, w.e.p, w.V.p);
+        else
+            launch(c, "inner_tridiag", k_tridiag, 1, 1024, tri_smem, nh, w.C.p, w.d.p, w.e.p, w.V.p);
         SweepDev S{w.AH.p, A3, P.A_h4.p, P.orb_vecs.p, P.orb_scal.p, co.LH.p, w.V.p, w.l.p, w.u.p, w.s.p,
                    w.wH[cur].p, w.th1[cur].p, w.c12.p, w.c22.p, w.lhat.p, nullptr, nh, N, prm.hartree ? 1 : 0};
-        launch(c, "inner", k_orbital_border, N, 256, sizeof(double) * 3 * nh, S);
+        launch(c, "inner:orbital_border", k_orbital_border, N, 256, sizeof(double) * 3 * nh, S);
         const int warps = N * nev;
-        launch(c, "inner", k_arrow_eig, ceil_div(warps, 4), 128, 0, nh, N, nev, (const double*)w.d.p,
+        launch(c, "inner:arrow_eig", k_arrow_eig, ceil_div(warps, 4), 128, 0, nh, N, nev, (const double*)w.d.p,
                (const double*)w.e.p, (const double*)w.c12.p, (const double*)w.c22.p, w.lam.p);
-        launch(c, "inner", k_arrow_vec, ceil_div(warps, 4), 128, 0, nh, N, nev, (const double*)w.d.p,
+        launch(c, "inner:arrow_vec", k_arrow_vec, ceil_div(warps, 4), 128, 0, nh, N, nev, (const double*)w.d.p,
                (const double*)w.e.p, (const double*)w.c12.p, (const double*)w.lhat.p, (const double*)w.s.p,
                (const double*)P.orb_scal.p, (const double*)w.lam.p, w.Y.p, w.piv.p, w.score.p, w.ynorm.p);
-        launch(c, "inner", k_select, N, 256, sizeof(double) * 2 * nh, S, nev, (const double*)w.lam.p,
+        launch(c, "inner:select", k_select, N, 256, sizeof(double) * 2 * nh, S, nev, (const double*)w.lam.p,
                (const double*)w.Y.p, (const double*)w.score.p, (const double*)w.ynorm.p, prm.score_floor,
                (const double*)co.MH.p, (const double*)w.phi[cur].p, (const double*)w.th2[cur].p, w.lamv[nx].p,
                w.phi[nx].p, w.th2[nx].p, w.flag.p);
         if (prm.hartree)
-            launch(c, "inner", k_coarse_sq, dim3(ceil_div(nct, 128), N), 128, 0, nct, nh, N, (const int32_t*)L.ctets.p,
+            launch(c, "inner:coarse_sq", k_coarse_sq, dim3(ceil_div(nct, 128), N), 128, 0, nct, nh, N, (const int32_t*)L.ctets.p,
                    (const double*)L.cxyz.p, (const int32_t*)L.ciidx.p, (const double*)w.phi[nx].p, w.E4.p);
         if (prm.hartree)
-            launch(c, "inner", k_coarse_vec_asm, dim3(ceil_div(nh, 128), N), 128, 0, nh, nct,
+            launch(c, "inner:coarse_vec_asm", k_coarse_vec_asm, dim3(ceil_div(nh, 128), N), 128, 0, nh, nct,
                    (const int32_t*)L.cinc_ptr.p, (const int32_t*)L.cinc.p, (const double*)w.E4.p, w.sq.p);
         HartreeDev H{w.sq.p, P.A_h4.p, A3, P.orb_vecs.p, P.orb_scal.p, P.shared_vecs.p, P.shared_scal.p, co.LC.p,
                      w.hu.p, w.scal.p, co.CH.p, co.MH.p, w.phi[nx].p, w.th2[nx].p, w.phi[cur].p, w.th2[cur].p,
@@ -933,7 +1059,7 @@ InnerStats inner_scf(Level& L, const CoarseOps& co, const ProjOut& P, const Inne
             KSB_CUDA_CHECK(cudaMemcpyAsync(w.wH[nx].p, w.wH[cur].p, sizeof(double) * nh, cudaMemcpyDeviceToDevice, c.stream));
             KSB_CUDA_CHECK(cudaMemcpyAsync(w.th1[nx].p, w.th1[cur].p, sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
         }
-        launch(c, "inner", k_hartree_delta, 1, 512, sizeof(double) * 3 * nh, H);
+        launch(c, "inner:hartree_delta", k_hartree_delta, 1, 512, sizeof(double) * 3 * nh, H);
         double dsq = 0.0;
         int fl[4];
         KSB_CUDA_CHECK(cudaMemcpyAsync(&dsq, w.scal.p + 1, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
@@ -947,7 +1073,10 @@ InnerStats inner_scf(Level& L, const CoarseOps& co, const ProjOut& P, const Inne
         w.cur = cur;
         if (delta < prm.tol || !prm.hartree) return st;
     }
-    raise(KSB_NONCONVERGENCE, "inner iteration exceeded the sweep cap");
+    std::string msg = "inner iteration exceeded " + std::to_string(prm.max_iterations) + " sweeps; recent changes:";
+    for (size_t k = st.history.size() > 6 ? st.history.size() - 6 : 0; k < st.history.size(); ++k)
+        msg += " " + std::to_string(st.history[k]);
+    raise(KSB_NONCONVERGENCE, msg);
 }
 
 }  // namespace ksb
