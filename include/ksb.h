@@ -168,6 +168,7 @@ typedef struct {
     int max_inner;      /* RunConfig::max_inner (400) */
     int nev_pad;        /* RunConfig::nev_scan_pad (4) */
     int check_every;    /* CG convergence poll interval */
+    int fixed_sweeps;   /* > 0: inner loop runs exactly this many sweeps (diagnostics), else 0 */
 } ksb_step_opts;
 
 typedef struct {

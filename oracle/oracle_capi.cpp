@@ -513,7 +513,10 @@ int orc_inner_scf(orc_blocks* bh, const double* lambdas, double tol, int max_it,
     return guard([&] {
         const Blocks& B = bh->B;
         const int nh = B.M_H.n;
-        const auto r = inner_scf(B, pure_state(B, Vec(lambdas, lambdas + B.n)), tol, max_it, floor, pad);
+        // max_it < 0: run exactly -max_it sweeps and return the state (diagnostics)
+        const bool fixed = max_it < 0;
+        const auto r = inner_scf(B, pure_state(B, Vec(lambdas, lambdas + B.n)), tol, fixed ? -max_it : max_it, floor,
+                                 pad, fixed);
         bh->last = r.state;
         std::memcpy(lam, r.state.lambda.data(), sizeof(double) * B.n);
         for (int i = 0; i < B.n; ++i) std::memcpy(phi_H + size_t(i) * nh, r.state.phi_H[i].data(), sizeof(double) * nh);

@@ -1492,7 +1492,7 @@ double state_change_sq(const Blocks& B, const AState& a, const AState& b) {
 }  // namespace
 
 // proj/src/correction.cpp:279-368
-InnerResult inner_scf(const Blocks& B, const AState& init, double tol, int max_it, double floor, int pad) {
+InnerResult inner_scf(const Blocks& B, const AState& init, double tol, int max_it, double floor, int pad, bool fixed) {
     InnerResult out;
     out.state = init;
     const int n = B.n, nh = B.M_H.n;
@@ -1550,9 +1550,13 @@ InnerResult inner_scf(const Blocks& B, const AState& init, double tol, int max_i
         out.history.push_back(delta);
         out.state = std::move(next);
         out.iterations = sweep;
-        if (delta < tol || !B.hartree_on) return out;
+        if (!fixed && (delta < tol || !B.hartree_on)) return out;
     }
-    fail(E_NONCONV, "inner iteration exceeded the sweep cap");
+    if (fixed) return out;
+    std::string msg = "inner iteration exceeded " + std::to_string(max_it) + " sweeps; recent changes:";
+    for (size_t k = out.history.size() > 6 ? out.history.size() - 6 : 0; k < out.history.size(); ++k)
+        msg += " " + std::to_string(out.history[k]);
+    fail(E_NONCONV, msg);
 }
 
 // proj/src/correction.cpp:370-381

@@ -266,7 +266,8 @@ struct InnerResult {
     int iterations = 0;
     std::vector<double> history;
 };
-InnerResult inner_scf(const Blocks& B, const AState& init, double tol, int max_it, double score_floor, int pad);
+InnerResult inner_scf(const Blocks& B, const AState& init, double tol, int max_it, double score_floor, int pad,
+                      bool fixed = false);
 void expand(const AState& s, const Blocks& B, std::vector<Vec>& orb, Vec& w);
 
 // ------------------------------------------------------------------ driver pieces (proj/src/driver.cpp, scf.cpp)

@@ -40,7 +40,7 @@ class CgStats(C.Structure):
 
 class StepOpts(C.Structure):
     _fields_ = [("tol_linear", D), ("tol_inner", D), ("score_floor", D), ("max_inner", I), ("nev_pad", I),
-                ("check_every", I)]
+                ("check_every", I), ("fixed_sweeps", I)]
 
 
 class StepLog(C.Structure):

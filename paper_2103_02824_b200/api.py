@@ -411,9 +411,10 @@ class Level:
         wH = np.empty(nh)
         th1 = C.c_double()
         it = C.c_int()
-        hist = np.zeros(o.max_inner)
+        cap = max(o.max_inner, o.fixed_sweeps)
+        hist = np.zeros(cap)
         check(lib.ksb_inner_scf(self._h, C.byref(o), _dp(lam0), _dp(lam), _dp(phi), _dp(th2), _dp(wH), C.byref(th1),
-                                C.byref(it), _dp(hist), o.max_inner))
+                                C.byref(it), _dp(hist), cap))
         return dict(lambda_=lam, phi_H=phi, theta2=th2, w_H=wH, theta1=th1.value, iterations=it.value,
                     history=hist[:it.value])
 

@@ -541,6 +541,7 @@ static ksb::StepOptions step_opts(const ksb_step_opts* o) {
         so.max_inner = o->max_inner;
         so.nev_pad = o->nev_pad;
         so.check_every = o->check_every;
+        so.fixed_sweeps = o->fixed_sweeps;
     }
     return so;
 }
@@ -580,6 +581,7 @@ int ksb_step_defaults(ksb_step_opts* o) {
         o->max_inner = 400;
         o->nev_pad = 4;
         o->check_every = 8;
+        o->fixed_sweeps = 0;
     });
 }
 
@@ -788,6 +790,7 @@ int ksb_inner_scf(ksb_level* l, const ksb_step_opts* o, const double* h_lambda, 
         ip.nev_pad = so.nev_pad;
         ip.hartree = K.sys.hartree_on;
         ip.occ = K.sys.occ;
+        ip.fixed_sweeps = so.fixed_sweeps;
         const auto st = ksb::inner_scf(l->L, K.coarse, K.proj, ip, h_lambda, K.inner, true);
         auto& w = K.inner;
         auto& c = *l->L.ctx;

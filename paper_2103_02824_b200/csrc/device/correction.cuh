@@ -25,7 +25,7 @@ struct System {
 
 struct StepOptions {
     double tol_linear = 1e-9, tol_inner = 1e-8, score_floor = 1e-8;
-    int max_inner = 400, nev_pad = 4, check_every = 8;
+    int max_inner = 400, nev_pad = 4, check_every = 8, fixed_sweeps = 0;
 };
 
 struct StepLog {

@@ -1013,7 +1013,8 @@ InnerStats inner_scf(Level& L, const CoarseOps& co, const ProjOut& P, const Inne
             attr = true;
         }
     }
-    for (int sweep = 1; sweep <= prm.max_iterations; ++sweep) {
+    const int cap = prm.fixed_sweeps > 0 ? prm.fixed_sweeps : prm.max_iterations;
+    for (int sweep = 1; sweep <= cap; ++sweep) {
         const int nx = cur ^ 1;
         // A_H
         if (prm.hartree)
@@ -1071,8 +1072,9 @@ InnerStats inner_scf(Level& L, const CoarseOps& co, const ProjOut& P, const Inne
         st.iterations = sweep;
         cur = nx;
         w.cur = cur;
-        if (delta < prm.tol || !prm.hartree) return st;
+        if (prm.fixed_sweeps <= 0 && (delta < prm.tol || !prm.hartree)) return st;
     }
+    if (prm.fixed_sweeps > 0) return st;
     std::string msg = "inner iteration exceeded " + std::to_string(prm.max_iterations) + " sweeps; recent changes:";
     for (size_t k = st.history.size() > 6 ? st.history.size() - 6 : 0; k < st.history.size(); ++k)
         msg += " " + std::to_string(st.history[k]);

@@ -21,6 +21,7 @@ struct InnerParams {
     int nev_pad = 4;
     bool hartree = true;
     double occ = 2.0;
+    int fixed_sweeps = 0;  // > 0: run exactly this many sweeps, no stopping test (diagnostics)
 };
 
 struct InnerStats {
