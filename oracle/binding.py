@@ -398,9 +398,9 @@ class OBlocks:
         wH = np.empty(nh)
         th1 = C.c_double()
         it = C.c_int()
-        hist = np.zeros(max_it)
+        hist = np.zeros(abs(max_it))
         _chk(lib.orc_inner_scf(self._h, dp(f64(lambdas)), tol, max_it, floor, pad, dp(lam), dp(phi), dp(th2), dp(wH),
-                               C.byref(th1), C.byref(it), dp(hist), max_it))
+                               C.byref(th1), C.byref(it), dp(hist), abs(max_it)))
         return dict(lambda_=lam, phi_H=phi, theta2=th2, w_H=wH, theta1=th1.value, iterations=it.value,
                     history=hist[:it.value])
 

@@ -613,64 +613,82 @@ __global__ void k_arrow_eig(int nh, int N, int nev, const double* __restrict__ d
     if (lane == 0) lam[warp] = 0.5 * (lo + hi);
 }
 
-/// warp per (orbital, k): eigenvector y = [(T - lam)^-1 c ; -1] (rotated basis, unnormalised) and its score
-/// |(L y)_last| / (|y| sqrt(gamma)), (L y)_last = l^T Q y_h + s y_l.
+/// warp per (orbital, k): eigenvector of the arrow-tridiagonal [T c; c^T c22] at the computed eigenvalue by two
+/// steps of inverse iteration with block elimination (robust when the eigenvalue is also an eigenvalue of T,
+/// e.g. a degenerate coarse pair decoupled from the augmentation direction), and its selection score
+/// |(L y)_last| / (|y| sqrt(gamma)), (L y)_last = l^T Q y_h + s y_l (proj/src/eigensolve.cpp:371-396).
 __global__ void k_arrow_vec(int nh, int N, int nev, const double* __restrict__ d, const double* __restrict__ e,
-                            const double* __restrict__ c12, const double* __restrict__ lhat, const double* __restrict__ s,
+                            const double* __restrict__ c12, const double* __restrict__ c22,
+                            const double* __restrict__ lhat, const double* __restrict__ s,
                             const double* __restrict__ orb_scal, const double* __restrict__ lam, double* __restrict__ Y,
-                            double* __restrict__ piv, double* __restrict__ score, double* __restrict__ ynorm) {
+                            double* __restrict__ Z, double* __restrict__ piv, double* __restrict__ score,
+                            double* __restrict__ ylast) {
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (warp >= N * nev) return;
     const int i = warp / nev;
     const double x = lam[warp];
     const double* c = c12 + size_t(i) * nh;
     double* y = Y + size_t(warp) * nh;
+    double* z = Z + size_t(warp) * nh;
     double* pv = piv + size_t(warp) * nh;
     if (lane == 0 && nh > 0) {
-        double q = 1.0, z = 0.0;
+        double tn = 0.0;
+        for (int j = 0; j < nh; ++j) tn = fmax(tn, fabs(d[j]) + (j > 0 ? fabs(e[j - 1]) : 0.0) + (j + 1 < nh ? fabs(e[j]) : 0.0));
+        const double pivmin = DBL_EPSILON * fmax(tn, 1e-300);
+        // LDL^T of T - x
+        double q = 1.0;
         for (int j = 0; j < nh; ++j) {
-            double dj = d[j] - x, zj = c[j];
-            if (j > 0) {
-                const double l = e[j - 1] / q;
-                dj -= l * e[j - 1];
-                zj -= l * z;
-            }
-            if (fabs(dj) < 1e-300) dj = dj < 0 ? -1e-300 : 1e-300;
+            double dj = d[j] - x;
+            if (j > 0) dj -= (e[j - 1] / q) * e[j - 1];
+            if (fabs(dj) < pivmin) dj = dj < 0 ? -pivmin : pivmin;
             pv[j] = dj;
-            y[j] = zj;
             q = dj;
-            z = zj;
         }
-        double nxt = y[nh - 1] / pv[nh - 1];
-        y[nh - 1] = nxt;
-        for (int j = nh - 2; j >= 0; --j) {
-            const double l = e[j] / pv[j];
-            nxt = y[j] / pv[j] - l * nxt;
-            y[j] = nxt;
+        auto solve = [&](double* v) {  // v <- (T - x)^-1 v
+            for (int j = 1; j < nh; ++j) v[j] -= (e[j - 1] / pv[j - 1]) * v[j - 1];
+            v[nh - 1] /= pv[nh - 1];
+            for (int j = nh - 2; j >= 0; --j) v[j] = v[j] / pv[j] - (e[j] / pv[j]) * v[j + 1];
+        };
+        for (int j = 0; j < nh; ++j) z[j] = c[j];
+        solve(z);
+        double cz = 0.0;
+        for (int j = 0; j < nh; ++j) cz += c[j] * z[j];
+        double sch = (c22[i] - x) - cz;
+        if (fabs(sch) < pivmin) sch = sch < 0 ? -pivmin : pivmin;
+        // deterministic start vector, two inverse-iteration steps
+        double yl = 1.0;
+        for (int j = 0; j < nh; ++j) y[j] = 1.0 + 0.5 * double((j * 7919) % 97) / 97.0;
+        for (int rep = 0; rep < 2; ++rep) {
+            const double rl = yl;
+            solve(y);
+            double cu = 0.0;
+            for (int j = 0; j < nh; ++j) cu += c[j] * y[j];
+            yl = (rl - cu) / sch;
+            double nn = yl * yl;
+            for (int j = 0; j < nh; ++j) {
+                y[j] -= z[j] * yl;
+                nn += y[j] * y[j];
+            }
+            const double inv = 1.0 / sqrt(nn);
+            for (int j = 0; j < nh; ++j) y[j] *= inv;
+            yl *= inv;
         }
+        ylast[warp] = yl;
     }
     __syncwarp();
     const double* lh = lhat + size_t(i) * nh;
-    double ov = 0.0, nn = 0.0;
-    for (int j = lane; j < nh; j += 32) {
-        ov += lh[j] * y[j];
-        nn += y[j] * y[j];
-    }
+    double ov = 0.0;
+    for (int j = lane; j < nh; j += 32) ov += lh[j] * y[j];
     ov = warp_sum(ov);
-    nn = warp_sum(nn);
     if (lane == 0) {
-        const double yl = -1.0;
-        ov += s[i] * yl;
-        const double nrm = sqrt(fmax(1e-300, nn + yl * yl));
-        const double g = orb_scal[5 * i + 3];
-        score[warp] = fabs(ov) / (nrm * sqrt(g));
-        ynorm[warp] = nrm;
+        ov += s[i] * ylast[warp];
+        score[warp] = fabs(ov) / sqrt(orb_scal[5 * i + 3]);
     }
 }
 
 /// block per orbital: select (strict >, first wins), back-transform, sign-align against the previous state
 __global__ void k_select(SweepDev S, int nev, const double* __restrict__ lam, const double* __restrict__ Y,
-                         const double* __restrict__ score, const double* __restrict__ ynorm, double floor,
+                         const double* __restrict__ score, const double* __restrict__ ylast, double floor,
                          const double* __restrict__ MH, const double* __restrict__ phi_old,
                          const double* __restrict__ th2_old, double* __restrict__ lam_new, double* __restrict__ phi_new,
                          double* __restrict__ th2_new, int* __restrict__ flag) {
@@ -694,14 +712,14 @@ __global__ void k_select(SweepDev S, int nev, const double* __restrict__ lam, co
     }
     __syncthreads();
     const int w = i * nev + best;
-    const double nrm = ynorm[w];
+    const double nrm = 1.0;  // inverse iteration returns unit vectors
     double* x = sh;  // nh: Q y_h / nrm, then phi_H
     for (int a = threadIdx.x; a < nh; a += blockDim.x) x[a] = Y[size_t(w) * nh + a];
     __syncthreads();
     if (threadIdx.x < 32) apply_q_warp(nh, S.V, x, 0);
     __syncthreads();
     const double si = S.s[i];
-    if (threadIdx.x == 0) th = (-1.0 / nrm) / si;
+    if (threadIdx.x == 0) th = ylast[w] / si;
     __syncthreads();
     const double theta = th;
     for (int a = threadIdx.x; a < nh; a += blockDim.x) x[a] = x[a] / nrm - S.l[size_t(i) * nh + a] * theta;
@@ -876,6 +894,7 @@ void InnerWork::ensure(int nh_, int N_, int nev_, int nct) {
     need(piv, int64_t(std::max(1, N)) * nev * std::max(1, nh));
     need(score, int64_t(std::max(1, N)) * nev);
     need(ynorm, int64_t(std::max(1, N)) * nev);
+    need(Z, int64_t(std::max(1, N)) * nev * std::max(1, nh));
     need(hu, std::max(1, nh));
     need(scal, 16);
     for (int k = 0; k < 2; ++k) {
@@ -1041,8 +1060,9 @@ InnerStats inner_scf(Level& L, const CoarseOps& co, const ProjOut& P, const Inne
         launch(c, "inner:arrow_eig", k_arrow_eig, ceil_div(warps, 4), 128, 0, nh, N, nev, (const double*)w.d.p,
                (const double*)w.e.p, (const double*)w.c12.p, (const double*)w.c22.p, w.lam.p);
         launch(c, "inner:arrow_vec", k_arrow_vec, ceil_div(warps, 4), 128, 0, nh, N, nev, (const double*)w.d.p,
-               (const double*)w.e.p, (const double*)w.c12.p, (const double*)w.lhat.p, (const double*)w.s.p,
-               (const double*)P.orb_scal.p, (const double*)w.lam.p, w.Y.p, w.piv.p, w.score.p, w.ynorm.p);
+               (const double*)w.e.p, (const double*)w.c12.p, (const double*)w.c22.p, (const double*)w.lhat.p,
+               (const double*)w.s.p, (const double*)P.orb_scal.p, (const double*)w.lam.p, w.Y.p, w.Z.p, w.piv.p,
+               w.score.p, w.ynorm.p);
         launch(c, "inner:select", k_select, N, 256, sizeof(double) * 2 * nh, S, nev, (const double*)w.lam.p,
                (const double*)w.Y.p, (const double*)w.score.p, (const double*)w.ynorm.p, prm.score_floor,
                (const double*)co.MH.p, (const double*)w.phi[cur].p, (const double*)w.th2[cur].p, w.lamv[nx].p,
