@@ -142,8 +142,8 @@ __global__ void __launch_bounds__(kThreads) k_init(int ni, Cols cc, const double
 }
 
 // ---------------- K1: Ap = A p, alpha ----------------
-template <int G, int CPL, bool SHIFT, bool SPLIT>
-__global__ void __launch_bounds__(kThreads) k_spmm_dot(int ni, Cols cc, const int32_t* __restrict__ ptr,
+template <int G, int CPL, bool SHIFT, bool SPLIT, bool FULL>
+__global__ void __launch_bounds__(kThreads, 3) k_spmm_dot(int ni, Cols cc, const int32_t* __restrict__ ptr,
                                                        const int32_t* __restrict__ col, const double* __restrict__ A,
                                                        const double* __restrict__ Bv, const double* __restrict__ P,
                                                        double* __restrict__ AP, CgDev s) {
@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(kThreads) k_spmm_dot(int ni, Cols cc, const in
             acc[0] = a;
             accB[0] = b;
         } else {
-            row_product<G, CPL, SHIFT>(rb, re, col, A, Bv, P, ld, c0, N, l, gmask, gbase, acc, accB);
+            row_product<G, CPL, SHIFT, FULL>(r, rb, re, col, A, Bv, P, ld, c0, N, l, gmask, gbase, acc, accB);
         }
         if (!SPLIT || l == 0) {
             if (SHIFT) {
@@ -287,8 +287,8 @@ __global__ void __launch_bounds__(kThreads) k_update_xr(int ni, Cols cc, double*
 }
 
 // ---------------- K3: true residual for flagged columns ----------------
-template <int G, int CPL, bool SHIFT, bool SPLIT>
-__global__ void __launch_bounds__(kThreads) k_trueres(int ni, Cols cc, const int32_t* __restrict__ ptr,
+template <int G, int CPL, bool SHIFT, bool SPLIT, bool FULL>
+__global__ void __launch_bounds__(kThreads, 3) k_trueres(int ni, Cols cc, const int32_t* __restrict__ ptr,
                                                       const int32_t* __restrict__ col, const double* __restrict__ A,
                                                       const double* __restrict__ Bv, const double* __restrict__ Bb,
                                                       const double* __restrict__ X, double* __restrict__ R, CgDev s) {
@@ -324,7 +324,7 @@ __global__ void __launch_bounds__(kThreads) k_trueres(int ni, Cols cc, const int
             acc[0] = a;
             accB[0] = b;
         } else {
-            row_product<G, CPL, SHIFT>(rb, re, col, A, Bv, X, ld, c0, N, l, gmask, gbase, acc, accB);
+            row_product<G, CPL, SHIFT, FULL>(r, rb, re, col, A, Bv, X, ld, c0, N, l, gmask, gbase, acc, accB);
         }
         if ((!SPLIT || l == 0) && c0 < N) {
 #pragma unroll
@@ -414,26 +414,27 @@ struct Plan {
 
 Plan plan_for(int N) {
     if (N == 1) return {8, 1, true};
-    if (N <= 8) return {4, 2, false};
-    if (N <= 16) return {8, 2, false};
-    if (N <= 32) return {16, 2, false};
-    if (N <= 64) return {32, 2, false};
+    if (N <= 4) return {2, 2, false};
+    if (N <= 8) return {2, 4, false};
+    if (N <= 16) return {4, 4, false};
+    if (N <= 32) return {8, 4, false};
+    if (N <= 64) return {16, 4, false};
     return {32, 4, false};
 }
 
-template <int G, int CPL, bool SHIFT, bool SPLIT>
+template <int G, int CPL, bool SHIFT, bool SPLIT, bool FULL>
 void launch_iteration(Ctx& c, const Level& L, const CgWork& w, const Cols& cc, const double* A, const double* Bv,
                       const double* Bb, double* X, int grid_s, int grid_e) {
     const size_t sm_s = sizeof(double) * std::max<size_t>(size_t(kThreads / G) * G * CPL, 2 * size_t(cc.N));
     const size_t sm_e = sizeof(double) * std::max<size_t>(kThreads, 2 * size_t(cc.N));
-    grid_s = std::min(grid_s, resident_grid(c, k_spmm_dot<G, CPL, SHIFT, SPLIT>, kThreads, sm_s));
+    grid_s = std::min(grid_s, resident_grid(c, k_spmm_dot<G, CPL, SHIFT, SPLIT, FULL>, kThreads, sm_s));
     grid_e = std::min(grid_e, resident_grid(c, k_update_xr, kThreads, sm_e));
-    launch(c, "spmm", k_spmm_dot<G, CPL, SHIFT, SPLIT>, grid_s, kThreads, sm_s, L.ni, cc,
+    launch(c, "spmm", k_spmm_dot<G, CPL, SHIFT, SPLIT, FULL>, grid_s, kThreads, sm_s, L.ni, cc,
            (const int32_t*)L.ii_ptr.p, (const int32_t*)L.ii_col.p, A, Bv, (const double*)w.P, w.AP, w.dev);
     launch(c, "cg_update", k_update_xr, grid_e, kThreads, sm_e, L.ni, cc, X, w.R, (const double*)w.P,
            (const double*)w.AP, w.dev);
     if (!cc.fixed)
-        launch(c, "cg_trueres", k_trueres<G, CPL, SHIFT, SPLIT>, grid_s, kThreads, sm_s, L.ni, cc,
+        launch(c, "cg_trueres", k_trueres<G, CPL, SHIFT, SPLIT, FULL>, grid_s, kThreads, sm_s, L.ni, cc,
                (const int32_t*)L.ii_ptr.p, (const int32_t*)L.ii_col.p, A, Bv, Bb, (const double*)X, w.R, w.dev);
     launch(c, "cg_update", k_update_p, grid_e, kThreads, 0, L.ni, cc, (const double*)w.R, w.P, w.dev);
 }
@@ -442,18 +443,23 @@ template <bool SHIFT>
 void iteration(Ctx& c, const Level& L, const CgWork& w, const Cols& cc, const double* A, const double* Bv,
                const double* Bb, double* X, int grid_s, int grid_e) {
     const Plan p = plan_for(cc.N);
+    const bool full = !p.split && cc.N == p.G * p.CPL;
     if (p.split)
-        launch_iteration<8, 1, SHIFT, true>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e);
+        launch_iteration<8, 1, SHIFT, true, false>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e);
+    else if (p.G == 2 && p.CPL == 2)
+        launch_iteration<2, 2, SHIFT, false, false>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e);
+    else if (p.G == 2)
+        launch_iteration<2, 4, SHIFT, false, false>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e);
+    else if (p.G == 4 && full)
+        launch_iteration<4, 4, SHIFT, false, true>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e);
     else if (p.G == 4)
-        launch_iteration<4, 2, SHIFT, false>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e);
+        launch_iteration<4, 4, SHIFT, false, false>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e);
     else if (p.G == 8)
-        launch_iteration<8, 2, SHIFT, false>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e);
+        launch_iteration<8, 4, SHIFT, false, false>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e);
     else if (p.G == 16)
-        launch_iteration<16, 2, SHIFT, false>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e);
-    else if (p.CPL == 2)
-        launch_iteration<32, 2, SHIFT, false>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e);
+        launch_iteration<16, 4, SHIFT, false, false>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e);
     else
-        launch_iteration<32, 4, SHIFT, false>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e);
+        launch_iteration<32, 4, SHIFT, false, false>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e);
 }
 
 } // namespace

@@ -22,7 +22,7 @@ __global__ void __launch_bounds__(256) k_spmm(int ni, const int32_t* __restrict_
         const int c0 = c0t + l * CPL;
         for (int r = warp * rows_per_warp + g; r < ni; r += nwarps * rows_per_warp) {
             double acc[CPL], accB[CPL];
-            row_product<G, CPL, SHIFT>(__ldg(ptr + r), __ldg(ptr + r + 1), col, A, B, X, ldx, c0, N, l, gmask,
+            row_product<G, CPL, SHIFT>(r, __ldg(ptr + r), __ldg(ptr + r + 1), col, A, B, X, ldx, c0, N, l, gmask,
                                        gbase, acc, accB);
             if (SHIFT) {
 #pragma unroll
@@ -83,14 +83,16 @@ void dispatch(Ctx& c, const Level& L, const double* A, const double* B, const do
         const int grid = int(std::min<int64_t>(want, int64_t(c.sm_count) * 8));
         launch(c, "spmm", k_spmv<8, SHIFT>, std::max(grid, 1), 256, 0, L.ni, (const int32_t*)L.ii_ptr.p,
                (const int32_t*)L.ii_col.p, A, B, sigma, X, ldx, Y, ldy);
+    } else if (N <= 4) {
+        run_spmm<2, 2, SHIFT>(c, L, A, B, sigma, X, N, ldx, Y, ldy);
     } else if (N <= 8) {
-        run_spmm<4, 2, SHIFT>(c, L, A, B, sigma, X, N, ldx, Y, ldy);
+        run_spmm<2, 4, SHIFT>(c, L, A, B, sigma, X, N, ldx, Y, ldy);
     } else if (N <= 16) {
-        run_spmm<8, 2, SHIFT>(c, L, A, B, sigma, X, N, ldx, Y, ldy);
+        run_spmm<4, 4, SHIFT>(c, L, A, B, sigma, X, N, ldx, Y, ldy);
     } else if (N <= 32) {
-        run_spmm<16, 2, SHIFT>(c, L, A, B, sigma, X, N, ldx, Y, ldy);
+        run_spmm<8, 4, SHIFT>(c, L, A, B, sigma, X, N, ldx, Y, ldy);
     } else if (N <= 64) {
-        run_spmm<32, 2, SHIFT>(c, L, A, B, sigma, X, N, ldx, Y, ldy);
+        run_spmm<16, 4, SHIFT>(c, L, A, B, sigma, X, N, ldx, Y, ldy);
     } else {
         run_spmm<32, 4, SHIFT>(c, L, A, B, sigma, X, N, ldx, Y, ldy);
     }

@@ -42,6 +42,16 @@ __device__ __forceinline__ void load_cols(const double* __restrict__ p, int c0, 
 }
 
 template <int CPL>
+__device__ __forceinline__ void load_full(const double* __restrict__ p, double (&x)[CPL]) {
+#pragma unroll
+    for (int k = 0; k < CPL; k += 2) {
+        const double2 a = __ldg(reinterpret_cast<const double2*>(p + k));
+        x[k] = a.x;
+        x[k + 1] = a.y;
+    }
+}
+
+template <int CPL>
 __device__ __forceinline__ void store_cols(double* __restrict__ p, int c0, int N, const double (&y)[CPL]) {
     if (c0 + CPL <= N) {
         if constexpr (CPL == 1) {
@@ -60,16 +70,20 @@ __device__ __forceinline__ void store_cols(double* __restrict__ p, int c0, int N
 }
 
 /// Row product for one CSR row: acc = sum_k A_k X[col_k], accB = sum_k B_k X[col_k].
-template <int G, int CPL, bool SHIFT>
-__device__ __forceinline__ void row_product(int rb, int re, const int32_t* __restrict__ col,
+/// FULL: every lane's CPL columns are in range (N == G*CPL), no bounds logic in the gather loop.
+/// Lanes past the row end gather the row's own X row with weight 0, so every chunk issues the
+/// same unpredicated load sequence.
+template <int G, int CPL, bool SHIFT, bool FULL = false>
+__device__ __forceinline__ void row_product(int r, int rb, int re, const int32_t* __restrict__ col,
                                             const double* __restrict__ A, const double* __restrict__ B,
                                             const double* __restrict__ X, int ldx, int c0, int N, int l,
                                             unsigned gmask, int gbase, double (&acc)[CPL], double (&accB)[CPL]) {
 #pragma unroll
     for (int k = 0; k < CPL; ++k) acc[k] = accB[k] = 0.0;
+    constexpr int UB = (G < 16 / CPL) ? G : 16 / CPL;
     for (int k0 = rb; k0 < re; k0 += G) {
         const int k = k0 + l;
-        int mc = 0;
+        int mc = r;
         double ma = 0.0, mb = 0.0;
         if (k < re) {
             mc = __ldg(col + k);
@@ -77,8 +91,6 @@ __device__ __forceinline__ void row_product(int rb, int re, const int32_t* __res
             if (SHIFT) mb = __ldg(B + k);
         }
         const int cnt = min(G, re - k0);
-        // gathers of a sub-batch are all issued before any FMA consumes them (memory-level parallelism)
-        constexpr int UB = (G < 16 / CPL) ? G : 16 / CPL;
 #pragma unroll
         for (int s0 = 0; s0 < G; s0 += UB) {
             if (s0 >= cnt) break;
@@ -86,12 +98,10 @@ __device__ __forceinline__ void row_product(int rb, int re, const int32_t* __res
 #pragma unroll
             for (int u = 0; u < UB; ++u) {
                 const int j = __shfl_sync(gmask, mc, gbase + s0 + u);
-                if (s0 + u < cnt) {
+                if (FULL)
+                    load_full<CPL>(X + size_t(j) * ldx + c0, x[u]);
+                else
                     load_cols<CPL>(X + size_t(j) * ldx + c0, c0, N, x[u]);
-                } else {
-#pragma unroll
-                    for (int q = 0; q < CPL; ++q) x[u][q] = 0.0;
-                }
             }
 #pragma unroll
             for (int u = 0; u < UB; ++u) {
