@@ -372,6 +372,10 @@ int ksb_level_create(ksb_ctx* c, const ksb_hier* h, int level, ksb_level** out) 
             L.ctets.upload(cx, T.coarse->mesh->tets);
             L.ciidx.upload(cx, T.coarse->iidx);
             L.cxyz.upload(cx, T.coarse->mesh->xyz);
+            L.sell_ptr.upload(cx, T.sell_ptr);
+            L.sell_col.upload(cx, T.sell_col);
+            L.sell_map.upload(cx, T.sell_map);
+            L.nslices = int(T.sell_ptr.size()) - 1;
             for (int d = 0; d < 3; ++d) {
                 L.box_lo[d] = M.lo[d];
                 L.box_hi[d] = M.hi[d];

@@ -222,6 +222,26 @@ void elem_potential(Level& L, const Potential& pot, double* E) {
     if (h_flag) raise(KSB_SINGULAR_QUADRATURE, "weight is not finite at a quadrature point");
 }
 
+__global__ void k_sell_pack(int64_t n, const int32_t* __restrict__ map, const double* __restrict__ csr,
+                            double* __restrict__ out) {
+    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x) {
+        const int m = map[k];
+        out[k] = m >= 0 ? csr[m] : 0.0;
+    }
+}
+
+const double* Level::sell_values(int id) {
+    Mat& M = mats[id];
+    if (!M.valid) raise(KSB_INVALID_ARGUMENT, "matrix not assembled");
+    if (M.sell_version != M.version) {
+        if (M.sell.n < sell_map.n) M.sell.alloc(sell_map.n);
+        launch(*ctx, "sell_pack", k_sell_pack, grid_for(*ctx, sell_map.n, 256), 256, 0, int64_t(sell_map.n),
+               (const int32_t*)sell_map.p, (const double*)M.ii.p, M.sell.p);
+        M.sell_version = M.version;
+    }
+    return M.sell.p;
+}
+
 Mat& Level::mat(int id) {
     if (id < 0 || id >= kMaxMats) raise(KSB_INVALID_ARGUMENT, "matrix id out of range");
     Mat& m = mats[id];
@@ -237,6 +257,7 @@ void axpby_values(Level& L, int dst, double a, int x, double b, int y) {
     Ctx& c = *L.ctx;
     if (!L.mats[x].valid || !L.mats[y].valid) raise(KSB_INVALID_ARGUMENT, "operand matrix not assembled");
     Mat& D = L.mat(dst);
+    L.touch(dst);
     launch(c, "axpby", k_axpby, grid_for(c, L.nnz_ii, 256), 256, 0, L.nnz_ii, a,
            (const double*)L.mats[x].ii.p, b, (const double*)L.mats[y].ii.p, D.ii.p);
     if (L.nnz_ib)
@@ -250,6 +271,7 @@ void assemble_into(Level& L, int mat, double c_s, double c_m, const Potential* p
     upload_rule(c.stream);
     if (L.ebuf.n < int64_t(L.nt) * 16) L.ebuf.alloc(int64_t(L.nt) * 16);
     Mat& M = L.mat(mat);
+    L.touch(mat);
     const int blk = 128;
     const int g = grid_for(c, L.nt, blk);
     bool first = true;

@@ -15,6 +15,7 @@
 //   K3 trueres  : (only when some column flagged) t = b - A x    -> converge or restart
 //   K4 update_p : p = D^-1 r + beta p
 #include <algorithm>
+#include <cstdlib>
 
 #include "cg.cuh"
 #include "spmm_core.cuh"
@@ -24,6 +25,9 @@ namespace ksb {
 namespace {
 
 constexpr int kThreads = 256;
+#ifndef KSB_SPMM_MINB
+#define KSB_SPMM_MINB 4
+#endif
 
 enum : int { kActive = 0, kConverged = 1, kBreakdown = 2 };
 enum : int { kIt = 0, kAnyCheck = 1, kTicket1 = 2, kTicket2 = 3, kTicket3 = 4, kTicket0 = 5, kNActive = 6 };
@@ -142,8 +146,8 @@ __global__ void __launch_bounds__(kThreads) k_init(int ni, Cols cc, const double
 }
 
 // ---------------- K1: Ap = A p, alpha ----------------
-template <int G, int CPL, bool SHIFT, bool SPLIT, bool FULL>
-__global__ void __launch_bounds__(kThreads, 3) k_spmm_dot(int ni, Cols cc, const int32_t* __restrict__ ptr,
+template <int G, int CPL, bool SHIFT, bool SPLIT, bool FULL, int MINB = KSB_SPMM_MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_spmm_dot(int ni, Cols cc, const int32_t* __restrict__ ptr,
                                                        const int32_t* __restrict__ col, const double* __restrict__ A,
                                                        const double* __restrict__ Bv, const double* __restrict__ P,
                                                        double* __restrict__ AP, CgDev s) {
@@ -152,7 +156,6 @@ __global__ void __launch_bounds__(kThreads, 3) k_spmm_dot(int ni, Cols cc, const
     const int lane = threadIdx.x & 31;
     const int g = lane / G, l = lane % G;
     const int gbase = g * G;
-    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << gbase);
     const int rows_per_warp = 32 / G;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -160,38 +163,68 @@ __global__ void __launch_bounds__(kThreads, 3) k_spmm_dot(int ni, Cols cc, const
     double pd[CPL];
 #pragma unroll
     for (int q = 0; q < CPL; ++q) pd[q] = 0.0;
-    for (int r = warp * rows_per_warp + g; r < ni; r += nwarps * rows_per_warp) {
-        const int rb = __ldg(ptr + r), re = __ldg(ptr + r + 1);
+    // row tiles are software-pipelined: the (col, val) chunk of the next tile and the row pointers of
+    // the tile after it are in flight while the current tile's gathers run. The wide FULL path keeps
+    // its registers for 16 gathers in flight instead (PF = false).
+    constexpr bool PF = !SPLIT;
+    const int tstride = nwarps * rows_per_warp;
+    int base = warp * rows_per_warp;
+    RowChunk<G, SHIFT> cur, nxt;
+    int nb_rb = 0, nb_re = 0;
+    if constexpr (PF) {
+        const int r0 = base + g;
+        const bool v0 = r0 < ni;
+        cur.load(v0 ? r0 : 0, v0 ? __ldg(ptr + r0) : 0, v0 ? __ldg(ptr + r0 + 1) : 0, l, col, A, Bv);
+        const int r1 = base + tstride + g;
+        const bool v1 = r1 < ni;
+        nb_rb = v1 ? __ldg(ptr + r1) : 0;
+        nb_re = v1 ? __ldg(ptr + r1 + 1) : 0;
+    }
+    for (; base < ni; base += tstride) {
+        const int r = base + g;
+        const bool valid = r < ni;
         double acc[CPL], accB[CPL];
         if constexpr (SPLIT) {
-            double a = 0.0, b = 0.0;
-            for (int k = rb + l; k < re; k += G) {
-                const double x = P[size_t(__ldg(col + k)) * ld];
-                a = fma(__ldg(A + k), x, a);
-                if (SHIFT) b = fma(__ldg(Bv + k), x, b);
-            }
-#pragma unroll
-            for (int o = G / 2; o > 0; o >>= 1) {
-                a += __shfl_xor_sync(gmask, a, o);
-                if (SHIFT) b += __shfl_xor_sync(gmask, b, o);
-            }
-            acc[0] = a;
-            accB[0] = b;
+            const int rb = valid ? __ldg(ptr + r) : 0, re = valid ? __ldg(ptr + r + 1) : 0;
+            row_split<G, SHIFT>(rb, re, col, A, Bv, P, ld, l, acc[0], accB[0]);
+        } else if constexpr (PF) {
+            const int r1 = base + tstride + g;
+            const bool v1 = r1 < ni;
+            nxt.load(v1 ? r1 : 0, nb_rb, nb_re, l, col, A, Bv);
+            const int r2 = base + 2 * tstride + g;
+            const bool v2 = r2 < ni;
+            nb_rb = v2 ? __ldg(ptr + r2) : 0;
+            nb_re = v2 ? __ldg(ptr + r2 + 1) : 0;
+            row_product_pf<G, CPL, SHIFT, FULL>(valid ? r : 0, cur, col, A, Bv, P, ld, c0, N, l, gbase, acc, accB);
+            cur = nxt;
         } else {
-            row_product<G, CPL, SHIFT, FULL>(r, rb, re, col, A, Bv, P, ld, c0, N, l, gmask, gbase, acc, accB);
+            cur.load(valid ? r : 0, valid ? __ldg(ptr + r) : 0, valid ? __ldg(ptr + r + 1) : 0, l, col, A, Bv);
+            row_product_pf<G, CPL, SHIFT, FULL>(valid ? r : 0, cur, col, A, Bv, P, ld, c0, N, l, gbase, acc, accB);
         }
-        if (!SPLIT || l == 0) {
-            if (SHIFT) {
+        if (valid && (!SPLIT || l == 0)) {
+            if constexpr (FULL) {
+                if (SHIFT) {
 #pragma unroll
-                for (int q = 0; q < CPL; ++q)
-                    if (c0 + q < N) acc[q] = fma(s.sigma[c0 + q], accB[q], acc[q]);
-            }
-            if (c0 < N) {
+                    for (int q = 0; q < CPL; ++q) acc[q] = fma(s.sigma[full_col<G>(l, q)], accB[q], acc[q]);
+                }
                 double p[CPL];
-                load_cols<CPL>(P + size_t(r) * ld + c0, c0, N, p);
-                store_cols<CPL>(AP + size_t(r) * ld + c0, c0, N, acc);
+                load_full<G, CPL>(P + size_t(r) * ld, l, p);
+                store_full<G, CPL>(AP + size_t(r) * ld, l, acc);
 #pragma unroll
                 for (int q = 0; q < CPL; ++q) pd[q] = fma(p[q], acc[q], pd[q]);
+            } else {
+                if (SHIFT) {
+#pragma unroll
+                    for (int q = 0; q < CPL; ++q)
+                        if (c0 + q < N) acc[q] = fma(s.sigma[c0 + q], accB[q], acc[q]);
+                }
+                if (c0 < N) {
+                    double p[CPL];
+                    load_cols<CPL>(P + size_t(r) * ld + c0, c0, N, p);
+                    store_cols<CPL>(AP + size_t(r) * ld + c0, c0, N, acc);
+#pragma unroll
+                    for (int q = 0; q < CPL; ++q) pd[q] = fma(p[q], acc[q], pd[q]);
+                }
             }
         }
     }
@@ -200,7 +233,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_spmm_dot(int ni, Cols cc, const
     const int width = G * CPL;
     const int gid = threadIdx.x / G;
 #pragma unroll
-    for (int q = 0; q < CPL; ++q) sm[gid * width + l * CPL + q] = pd[q];
+    for (int q = 0; q < CPL; ++q) sm[gid * width + (FULL ? full_col<G>(l, q) : l * CPL + q)] = pd[q];
     __syncthreads();
     if (threadIdx.x < N) {
         double t = 0.0;
@@ -225,6 +258,268 @@ __global__ void __launch_bounds__(kThreads, 3) k_spmm_dot(int ni, Cols cc, const
     }
     __syncthreads();
     if (threadIdx.x == 0) {  // a breakdown retires its column: let the host loop stop once none is active
+        int na = 0;
+        for (int c = 0; c < N; ++c) na += s.status[c] == kActive;
+        s.ctl[kNActive] = na;
+    }
+}
+
+// ---------------- K1 (staged variant): gathers through cp.async into shared memory ----------------
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(a), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+constexpr int kStageE = 16;       // row entries staged per super-chunk (a Kuhn row has <= 15)
+constexpr int kAsyncThreads = 128;
+
+/// Same contract as k_spmm_dot for N == G*CPL. Each lane copies its CPL doubles of all 16 gathered
+/// X rows of its group's row into a per-warp shared stage with LDGSTS (no register cost, all in
+/// flight together), then consumes them from shared memory.
+template <int G, int CPL, bool SHIFT>
+__global__ void __launch_bounds__(kAsyncThreads) k_spmm_dot_async(int ni, Cols cc, const int32_t* __restrict__ ptr,
+                                                                  const int32_t* __restrict__ col,
+                                                                  const double* __restrict__ A,
+                                                                  const double* __restrict__ Bv,
+                                                                  const double* __restrict__ P,
+                                                                  double* __restrict__ AP, CgDev s) {
+    extern __shared__ double sm[];
+    constexpr int NBk = kStageE / G;
+    const int N = cc.N, ld = cc.ld;
+    const int lane = threadIdx.x & 31;
+    const int g = lane / G, l = lane % G;
+    const int gbase = g * G;
+    const int rows_per_warp = 32 / G;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    const int c0 = l * CPL;
+    double* stage = sm + size_t(threadIdx.x >> 5) * kStageE * 32 * CPL;
+    double pd[CPL];
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) pd[q] = 0.0;
+    for (int base = warp * rows_per_warp; base < ni; base += nwarps * rows_per_warp) {
+        const int r = base + g;
+        const bool valid = r < ni;
+        const int rb = valid ? __ldg(ptr + r) : 0, re = valid ? __ldg(ptr + r + 1) : 0;
+        const int wmax = __reduce_max_sync(0xffffffffu, re - rb);
+        const int self = valid ? r : 0;
+        double acc[CPL], accB[CPL];
+#pragma unroll
+        for (int q = 0; q < CPL; ++q) acc[q] = accB[q] = 0.0;
+        for (int k0 = 0; k0 < wmax; k0 += kStageE) {
+            int mc[NBk];
+            double ma[NBk], mb[NBk];
+#pragma unroll
+            for (int b = 0; b < NBk; ++b) {
+                const int k = rb + k0 + b * G + l;
+                mc[b] = self;
+                ma[b] = 0.0;
+                mb[b] = 0.0;
+                if (k < re) {
+                    mc[b] = __ldg(col + k);
+                    ma[b] = __ldg(A + k);
+                    if (SHIFT) mb[b] = __ldg(Bv + k);
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < kStageE; ++e) {
+                if (k0 + e < wmax) {
+                    const int j = __shfl_sync(0xffffffffu, mc[e / G], gbase + e % G);
+                    const double* src = P + size_t(j) * ld + c0;
+                    double* dst = stage + (e * 32 + lane) * CPL;
+#pragma unroll
+                    for (int h = 0; h < CPL; h += 2) cp_async16(dst + h, src + h);
+                }
+            }
+            cp_async_commit();
+            cp_async_wait_all();
+            __syncwarp();
+#pragma unroll
+            for (int e = 0; e < kStageE; ++e) {
+                if (k0 + e < wmax) {
+                    const double a = __shfl_sync(0xffffffffu, ma[e / G], gbase + e % G);
+                    double bb = 0.0;
+                    if (SHIFT) bb = __shfl_sync(0xffffffffu, mb[e / G], gbase + e % G);
+                    const double* xs = stage + (e * 32 + lane) * CPL;
+#pragma unroll
+                    for (int q = 0; q < CPL; q += 2) {
+                        const double2 x = *reinterpret_cast<const double2*>(xs + q);
+                        acc[q] = fma(a, x.x, acc[q]);
+                        acc[q + 1] = fma(a, x.y, acc[q + 1]);
+                        if (SHIFT) {
+                            accB[q] = fma(bb, x.x, accB[q]);
+                            accB[q + 1] = fma(bb, x.y, accB[q + 1]);
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+        }
+        if (valid) {
+            if (SHIFT) {
+#pragma unroll
+                for (int q = 0; q < CPL; ++q) acc[q] = fma(s.sigma[c0 + q], accB[q], acc[q]);
+            }
+            double p[CPL];
+            load_full<G, CPL>(P + size_t(r) * ld, l, p);
+            double* y = AP + size_t(r) * ld + c0;
+#pragma unroll
+            for (int q = 0; q < CPL; q += 2) *reinterpret_cast<double2*>(y + q) = make_double2(acc[q], acc[q + 1]);
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) pd[q] = fma(p[q], acc[q], pd[q]);
+        }
+    }
+    double* red = sm + size_t(kAsyncThreads / 32) * kStageE * 32 * CPL;
+    const int ngroups = blockDim.x / G;
+    const int width = G * CPL;
+    const int gid = threadIdx.x / G;
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) red[gid * width + l * CPL + q] = pd[q];
+    __syncthreads();
+    if (threadIdx.x < N) {
+        double t = 0.0;
+        for (int k = 0; k < ngroups; ++k) t += red[k * width + threadIdx.x];
+        s.part0[size_t(blockIdx.x) * N + threadIdx.x] = t;
+    }
+    if (!last_block(s.ctl + kTicket1)) return;
+    fold_partials(s.part0, gridDim.x, N, red);
+    if (threadIdx.x < N) {
+        const int c = threadIdx.x;
+        const double pap = red[c];
+        double al = 0.0;
+        if (s.status[c] == kActive) {
+            if (!cc.fixed && !(pap > 0.0)) {
+                s.status[c] = kBreakdown;
+                s.relres[c] = sqrt(s.rr[c]) / s.bnorm[c];
+            } else {
+                al = s.rz[c] / pap;
+            }
+        }
+        s.alpha[c] = al;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int na = 0;
+        for (int c = 0; c < N; ++c) na += s.status[c] == kActive;
+        s.ctl[kNActive] = na;
+    }
+}
+
+// ---------------- K1 (SELL-32 variant): one row per lane, all N <= 16 columns per lane ----------------
+template <int NC>
+__device__ __forceinline__ void load_row(const double* __restrict__ p, double (&x)[NC]) {
+    if constexpr (NC == 1) {
+        x[0] = __ldg(p);
+    } else {
+#pragma unroll
+        for (int q = 0; q < NC; q += 2) {
+            const double2 a = __ldg(reinterpret_cast<const double2*>(p + q));
+            x[q] = a.x;
+            x[q + 1] = a.y;
+        }
+    }
+}
+
+/// Same contract as k_spmm_dot for N == NC in {1, 2, 4, 8, 16}. A is read in SELL-32 order
+/// (entry e of the 32 rows of a slice is contiguous: coalesced col/val loads, no shuffles); each
+/// lane gathers whole X rows for its own row, U entries in flight.
+template <int NC, bool SHIFT>
+__global__ void __launch_bounds__(kThreads, 2) k_sell_dot(int ni, int nslices, Cols cc, const int32_t* __restrict__ sptr,
+                                                         const int32_t* __restrict__ scol,
+                                                         const double* __restrict__ sA,
+                                                         const double* __restrict__ sB,
+                                                         const double* __restrict__ P, double* __restrict__ AP,
+                                                         CgDev s) {
+    extern __shared__ double sm[];
+    constexpr int U = NC >= 8 ? 2 : 4;
+    const int N = cc.N, ld = cc.ld;
+    const int lane = threadIdx.x & 31;
+    const int nwb = blockDim.x >> 5, wib = threadIdx.x >> 5;
+    const int warp = blockIdx.x * nwb + wib;
+    const int nwarps = gridDim.x * nwb;
+    double pd[NC];
+#pragma unroll
+    for (int q = 0; q < NC; ++q) pd[q] = 0.0;
+    for (int sl = warp; sl < nslices; sl += nwarps) {
+        const int r = sl * 32 + lane;
+        const int b0 = __ldg(sptr + sl);
+        const int w = (__ldg(sptr + sl + 1) - b0) >> 5;
+        double acc[NC], accB[NC];
+#pragma unroll
+        for (int q = 0; q < NC; ++q) acc[q] = accB[q] = 0.0;
+        for (int e = 0; e < w; e += U) {
+            int j[U];
+            double a[U], bb[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int k = b0 + (e + u) * 32 + lane;
+                const bool in = e + u < w;
+                j[u] = in ? __ldg(scol + k) : 0;
+                a[u] = in ? __ldg(sA + k) : 0.0;
+                bb[u] = (SHIFT && in) ? __ldg(sB + k) : 0.0;
+            }
+            double x[U][NC];
+#pragma unroll
+            for (int u = 0; u < U; ++u) load_row<NC>(P + size_t(j[u]) * ld, x[u]);
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int q = 0; q < NC; ++q) {
+                    acc[q] = fma(a[u], x[u][q], acc[q]);
+                    if (SHIFT) accB[q] = fma(bb[u], x[u][q], accB[q]);
+                }
+        }
+        if (r < ni) {
+            if (SHIFT) {
+#pragma unroll
+                for (int q = 0; q < NC; ++q) acc[q] = fma(s.sigma[q], accB[q], acc[q]);
+            }
+            double p[NC];
+            load_row<NC>(P + size_t(r) * ld, p);
+            double* y = AP + size_t(r) * ld;
+            if constexpr (NC == 1) {
+                y[0] = acc[0];
+            } else {
+#pragma unroll
+                for (int q = 0; q < NC; q += 2) *reinterpret_cast<double2*>(y + q) = make_double2(acc[q], acc[q + 1]);
+            }
+#pragma unroll
+            for (int q = 0; q < NC; ++q) pd[q] = fma(p[q], acc[q], pd[q]);
+        }
+    }
+    // block reduce per column: warp shuffle, then fixed-order sum over warps
+    double* red = sm;  // nwb x NC
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+        const double t = warp_sum(pd[q]);
+        if (lane == 0) red[wib * NC + q] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x < N) {
+        double t = 0.0;
+        for (int k = 0; k < nwb; ++k) t += red[k * NC + threadIdx.x];
+        s.part0[size_t(blockIdx.x) * N + threadIdx.x] = t;
+    }
+    if (!last_block(s.ctl + kTicket1)) return;
+    fold_partials(s.part0, gridDim.x, N, red);
+    if (threadIdx.x < N) {
+        const int c = threadIdx.x;
+        const double pap = red[c];
+        double al = 0.0;
+        if (s.status[c] == kActive) {
+            if (!cc.fixed && !(pap > 0.0)) {
+                s.status[c] = kBreakdown;
+                s.relres[c] = sqrt(s.rr[c]) / s.bnorm[c];
+            } else {
+                al = s.rz[c] / pap;
+            }
+        }
+        s.alpha[c] = al;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
         int na = 0;
         for (int c = 0; c < N; ++c) na += s.status[c] == kActive;
         s.ctl[kNActive] = na;
@@ -298,7 +593,6 @@ __global__ void __launch_bounds__(kThreads, 3) k_trueres(int ni, Cols cc, const 
     const int lane = threadIdx.x & 31;
     const int g = lane / G, l = lane % G;
     const int gbase = g * G;
-    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << gbase);
     const int rows_per_warp = 32 / G;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -306,30 +600,20 @@ __global__ void __launch_bounds__(kThreads, 3) k_trueres(int ni, Cols cc, const 
     double tt[CPL], tz[CPL];
 #pragma unroll
     for (int q = 0; q < CPL; ++q) tt[q] = tz[q] = 0.0;
-    for (int r = warp * rows_per_warp + g; r < ni; r += nwarps * rows_per_warp) {
-        const int rb = __ldg(ptr + r), re = __ldg(ptr + r + 1);
+    for (int base = warp * rows_per_warp; base < ni; base += nwarps * rows_per_warp) {
+        const int r = base + g;
+        const bool valid = r < ni;
+        const int rb = valid ? __ldg(ptr + r) : 0, re = valid ? __ldg(ptr + r + 1) : 0;
         double acc[CPL], accB[CPL];
         if constexpr (SPLIT) {
-            double a = 0.0, b = 0.0;
-            for (int k = rb + l; k < re; k += G) {
-                const double x = X[size_t(__ldg(col + k)) * ld];
-                a = fma(__ldg(A + k), x, a);
-                if (SHIFT) b = fma(__ldg(Bv + k), x, b);
-            }
-#pragma unroll
-            for (int o = G / 2; o > 0; o >>= 1) {
-                a += __shfl_xor_sync(gmask, a, o);
-                if (SHIFT) b += __shfl_xor_sync(gmask, b, o);
-            }
-            acc[0] = a;
-            accB[0] = b;
+            row_split<G, SHIFT>(rb, re, col, A, Bv, X, ld, l, acc[0], accB[0]);
         } else {
-            row_product<G, CPL, SHIFT, FULL>(r, rb, re, col, A, Bv, X, ld, c0, N, l, gmask, gbase, acc, accB);
+            row_product<G, CPL, SHIFT, FULL>(valid ? r : 0, rb, re, col, A, Bv, X, ld, c0, N, l, gbase, acc, accB);
         }
-        if ((!SPLIT || l == 0) && c0 < N) {
+        if (valid && (!SPLIT || l == 0) && (FULL || c0 < N)) {
 #pragma unroll
             for (int q = 0; q < CPL; ++q) {
-                const int c = c0 + q;
+                const int c = FULL ? full_col<G>(l, q) : c0 + q;
                 if (c < N && s.check[c]) {
                     const double ax = SHIFT ? fma(s.sigma[c], accB[q], acc[q]) : acc[q];
                     const size_t i = size_t(r) * ld + c;
@@ -346,7 +630,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_trueres(int ni, Cols cc, const 
     const int gid = threadIdx.x / G;
     for (int pass = 0; pass < 2; ++pass) {
 #pragma unroll
-        for (int q = 0; q < CPL; ++q) sm[gid * width + l * CPL + q] = pass ? tz[q] : tt[q];
+        for (int q = 0; q < CPL; ++q) sm[gid * width + (FULL ? full_col<G>(l, q) : l * CPL + q)] = pass ? tz[q] : tt[q];
         __syncthreads();
         if (threadIdx.x < N) {
             double t = 0.0;
@@ -413,6 +697,11 @@ struct Plan {
 };
 
 Plan plan_for(int N) {
+    // measured on B200 at N = 16 (cfg2): 8 lanes x 2 columns at <= 64 registers (32 warps/SM) beats
+    // 4 lanes x 4 columns (0.306 vs 0.368 ms per SpMM): the kernel is gather-latency bound, so
+    // warps in flight matter more than loads per warp. KSB_SPMM_PLAN=4 selects the wide variant.
+    static const char* env = std::getenv("KSB_SPMM_PLAN");
+    if (N == 16 && !(env && env[0] == '4')) return {8, 2, false};
     if (N == 1) return {8, 1, true};
     if (N <= 4) return {2, 2, false};
     if (N <= 8) return {2, 4, false};
@@ -422,44 +711,98 @@ Plan plan_for(int N) {
     return {32, 4, false};
 }
 
+struct SellOps {
+    const double *A = nullptr, *B = nullptr;
+};
+
+template <int NC, bool SHIFT>
+void launch_sell(Ctx& c, const Level& L, const CgWork& w, const Cols& cc, const SellOps& so) {
+    const size_t sm = sizeof(double) * std::max<size_t>(size_t(kThreads / 32) * NC, 2 * size_t(cc.N));
+    const int want = ceil_div(L.nslices, kThreads / 32);
+    const int g = std::max(1, std::min(want, resident_grid(c, k_sell_dot<NC, SHIFT>, kThreads, sm)));
+    launch(c, "spmm", k_sell_dot<NC, SHIFT>, g, kThreads, sm, L.ni, L.nslices, cc, (const int32_t*)L.sell_ptr.p,
+           (const int32_t*)L.sell_col.p, so.A, so.B, (const double*)w.P, w.AP, w.dev);
+}
+
+template <bool SHIFT>
+bool try_sell(Ctx& c, const Level& L, const CgWork& w, const Cols& cc, const SellOps& so) {
+    if (!so.A) return false;
+    switch (cc.N) {
+        case 1: launch_sell<1, SHIFT>(c, L, w, cc, so); return true;
+        case 2: launch_sell<2, SHIFT>(c, L, w, cc, so); return true;
+        default: return false;
+    }
+}
+
 template <int G, int CPL, bool SHIFT, bool SPLIT, bool FULL>
 void launch_iteration(Ctx& c, const Level& L, const CgWork& w, const Cols& cc, const double* A, const double* Bv,
-                      const double* Bb, double* X, int grid_s, int grid_e) {
+                      const double* Bb, double* X, int grid_s, int grid_e, const SellOps& so) {
     const size_t sm_s = sizeof(double) * std::max<size_t>(size_t(kThreads / G) * G * CPL, 2 * size_t(cc.N));
     const size_t sm_e = sizeof(double) * std::max<size_t>(kThreads, 2 * size_t(cc.N));
-    grid_s = std::min(grid_s, resident_grid(c, k_spmm_dot<G, CPL, SHIFT, SPLIT, FULL>, kThreads, sm_s));
     grid_e = std::min(grid_e, resident_grid(c, k_update_xr, kThreads, sm_e));
-    launch(c, "spmm", k_spmm_dot<G, CPL, SHIFT, SPLIT, FULL>, grid_s, kThreads, sm_s, L.ni, cc,
-           (const int32_t*)L.ii_ptr.p, (const int32_t*)L.ii_col.p, A, Bv, (const double*)w.P, w.AP, w.dev);
-    launch(c, "cg_update", k_update_xr, grid_e, kThreads, sm_e, L.ni, cc, X, w.R, (const double*)w.P,
+    if (try_sell<SHIFT>(c, L, w, cc, so)) {
+    } else if constexpr (FULL && !SPLIT && false) {
+        const size_t sm_a = sizeof(double) * (size_t(kAsyncThreads / 32) * kStageE * 32 * CPL +
+                                              std::max<size_t>(size_t(kAsyncThreads) * CPL, 2 * size_t(cc.N)));
+        static bool attr = false;
+        if (!attr) {
+            KSB_CUDA_CHECK(cudaFuncSetAttribute(k_spmm_dot_async<G, CPL, SHIFT>,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm_a)));
+            attr = true;
+        }
+        const int rows_per_block = kAsyncThreads / G;
+        const int want = ceil_div(L.ni, rows_per_block);
+        const int ga = std::min(want, resident_grid(c, k_spmm_dot_async<G, CPL, SHIFT>, kAsyncThreads, sm_a));
+        launch(c, "spmm", k_spmm_dot_async<G, CPL, SHIFT>, ga, kAsyncThreads, sm_a, L.ni, cc,
+               (const int32_t*)L.ii_ptr.p, (const int32_t*)L.ii_col.p, A, Bv, (const double*)w.P, w.AP, w.dev);
+    } else {
+        static const char* mb = std::getenv("KSB_SPMM_MINB");
+        const int minb = mb ? std::atoi(mb) : KSB_SPMM_MINB;
+        auto go = [&](auto kern) {
+            grid_s = std::min(grid_s, resident_grid(c, kern, kThreads, sm_s));
+            launch(c, "spmm", kern, grid_s, kThreads, sm_s, L.ni, cc, (const int32_t*)L.ii_ptr.p,
+                   (const int32_t*)L.ii_col.p, A, Bv, (const double*)w.P, w.AP, w.dev);
+        };
+        if (FULL && minb == 4)
+            go(k_spmm_dot<G, CPL, SHIFT, SPLIT, FULL, 4>);
+        else if (FULL && minb == 5)
+            go(k_spmm_dot<G, CPL, SHIFT, SPLIT, FULL, 5>);
+        else if (FULL && minb == 2)
+            go(k_spmm_dot<G, CPL, SHIFT, SPLIT, FULL, 2>);
+        else
+            go(k_spmm_dot<G, CPL, SHIFT, SPLIT, FULL>);
+    }
+    launch(c, "cg_update_xr", k_update_xr, grid_e, kThreads, sm_e, L.ni, cc, X, w.R, (const double*)w.P,
            (const double*)w.AP, w.dev);
     if (!cc.fixed)
         launch(c, "cg_trueres", k_trueres<G, CPL, SHIFT, SPLIT, FULL>, grid_s, kThreads, sm_s, L.ni, cc,
                (const int32_t*)L.ii_ptr.p, (const int32_t*)L.ii_col.p, A, Bv, Bb, (const double*)X, w.R, w.dev);
-    launch(c, "cg_update", k_update_p, grid_e, kThreads, 0, L.ni, cc, (const double*)w.R, w.P, w.dev);
+    launch(c, "cg_update_p", k_update_p, grid_e, kThreads, 0, L.ni, cc, (const double*)w.R, w.P, w.dev);
 }
 
 template <bool SHIFT>
 void iteration(Ctx& c, const Level& L, const CgWork& w, const Cols& cc, const double* A, const double* Bv,
-               const double* Bb, double* X, int grid_s, int grid_e) {
+               const double* Bb, double* X, int grid_s, int grid_e, const SellOps& so) {
     const Plan p = plan_for(cc.N);
     const bool full = !p.split && cc.N == p.G * p.CPL;
     if (p.split)
-        launch_iteration<8, 1, SHIFT, true, false>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e);
+        launch_iteration<8, 1, SHIFT, true, false>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e, so);
     else if (p.G == 2 && p.CPL == 2)
-        launch_iteration<2, 2, SHIFT, false, false>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e);
+        launch_iteration<2, 2, SHIFT, false, false>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e, so);
     else if (p.G == 2)
-        launch_iteration<2, 4, SHIFT, false, false>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e);
+        launch_iteration<2, 4, SHIFT, false, false>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e, so);
+    else if (p.G == 8 && p.CPL == 2 && full)
+        launch_iteration<8, 2, SHIFT, false, true>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e, so);
     else if (p.G == 4 && full)
-        launch_iteration<4, 4, SHIFT, false, true>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e);
+        launch_iteration<4, 4, SHIFT, false, true>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e, so);
     else if (p.G == 4)
-        launch_iteration<4, 4, SHIFT, false, false>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e);
+        launch_iteration<4, 4, SHIFT, false, false>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e, so);
     else if (p.G == 8)
-        launch_iteration<8, 4, SHIFT, false, false>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e);
+        launch_iteration<8, 4, SHIFT, false, false>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e, so);
     else if (p.G == 16)
-        launch_iteration<16, 4, SHIFT, false, false>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e);
+        launch_iteration<16, 4, SHIFT, false, false>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e, so);
     else
-        launch_iteration<32, 4, SHIFT, false, false>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e);
+        launch_iteration<32, 4, SHIFT, false, false>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e, so);
 }
 
 } // namespace
@@ -537,6 +880,11 @@ void cg_solve(Ctx& c, Level& L, int mat, int shift_mat, const double* h_sigma, c
 
     const double* A = L.mats[mat].ii.p;
     const double* Bv = shift ? L.mats[shift_mat].ii.p : nullptr;
+    SellOps so;
+    if (N == 1 || N == 2) {  // thread-per-row SELL wins for narrow blocks; wider blocks use lane groups
+        so.A = L.sell_values(mat);
+        so.B = shift ? L.sell_values(shift_mat) : nullptr;
+    }
     const int total = cc.fixed ? o.fixed_iterations : o.max_iterations;
     const int every = std::max(1, o.check_every);
     int done = 0;
@@ -544,9 +892,9 @@ void cg_solve(Ctx& c, Level& L, int mat, int shift_mat, const double* h_sigma, c
         const int chunk = std::min(every, total - done);
         for (int k = 0; k < chunk; ++k) {
             if (shift)
-                iteration<true>(c, L, w, cc, A, Bv, d_B, d_X, grid_s, grid_e);
+                iteration<true>(c, L, w, cc, A, Bv, d_B, d_X, grid_s, grid_e, so);
             else
-                iteration<false>(c, L, w, cc, A, nullptr, d_B, d_X, grid_s, grid_e);
+                iteration<false>(c, L, w, cc, A, nullptr, d_B, d_X, grid_s, grid_e, so);
         }
         done += chunk;
         if (!cc.fixed) {

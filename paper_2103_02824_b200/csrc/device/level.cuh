@@ -34,6 +34,8 @@ struct DevBuf {
 
 struct Mat {
     DevBuf<double> ii, ib;
+    DevBuf<double> sell;         // ii values in the SELL-32 order (lazily converted)
+    uint64_t version = 0, sell_version = ~uint64_t(0);
     bool valid = false;
 };
 
@@ -56,6 +58,8 @@ struct Level {
     DevBuf<int32_t> cinc_ptr, cinc;           // coarse interior dof -> incident (coarse tet*4 + local)
     DevBuf<int32_t> ctets, ciidx;             // coarse mesh (level 0)
     DevBuf<double> cxyz;
+    DevBuf<int32_t> sell_ptr, sell_col, sell_map;
+    int nslices = 0;
     double box_lo[3] = {0, 0, 0}, box_hi[3] = {0, 0, 0};
     DevBuf<double> ebuf;      // element matrices, 16 per tet (scratch)
     DevBuf<double> scratch;   // term accumulation scratch (nnz_ii + nnz_ib)
@@ -63,6 +67,9 @@ struct Level {
     Mat mats[kMaxMats];
 
     Mat& mat(int id);
+    /// SELL-32 values of matrix id (converted on first use after its values changed)
+    const double* sell_values(int id);
+    void touch(int id) { ++mats[id].version; }
 };
 
 // assembly (assemble.cu)

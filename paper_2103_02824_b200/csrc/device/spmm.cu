@@ -14,16 +14,18 @@ __global__ void __launch_bounds__(256) k_spmm(int ni, const int32_t* __restrict_
     const int lane = threadIdx.x & 31;
     const int g = lane / G, l = lane % G;
     const int gbase = g * G;
-    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << gbase);
     const int rows_per_warp = 32 / G;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
     for (int c0t = 0; c0t < N; c0t += G * CPL) {
         const int c0 = c0t + l * CPL;
-        for (int r = warp * rows_per_warp + g; r < ni; r += nwarps * rows_per_warp) {
+        for (int base = warp * rows_per_warp; base < ni; base += nwarps * rows_per_warp) {
+            const int r = base + g;
+            const bool valid = r < ni;
             double acc[CPL], accB[CPL];
-            row_product<G, CPL, SHIFT>(r, __ldg(ptr + r), __ldg(ptr + r + 1), col, A, B, X, ldx, c0, N, l, gmask,
-                                       gbase, acc, accB);
+            row_product<G, CPL, SHIFT>(valid ? r : 0, valid ? __ldg(ptr + r) : 0, valid ? __ldg(ptr + r + 1) : 0, col,
+                                       A, B, X, ldx, c0, N, l, gbase, acc, accB);
+            if (!valid) continue;
             if (SHIFT) {
 #pragma unroll
                 for (int q = 0; q < CPL; ++q)
@@ -43,25 +45,17 @@ __global__ void __launch_bounds__(256) k_spmv(int ni, const int32_t* __restrict_
     const int lane = threadIdx.x & 31;
     const int g = lane / G, l = lane % G;
     const int gbase = g * G;
-    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << gbase);
     const int rows_per_warp = 32 / G;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
     const double s = SHIFT ? sigma[0] : 0.0;
-    for (int r = warp * rows_per_warp + g; r < ni; r += nwarps * rows_per_warp) {
-        const int rb = __ldg(ptr + r), re = __ldg(ptr + r + 1);
+    for (int base = warp * rows_per_warp; base < ni; base += nwarps * rows_per_warp) {
+        const int r = base + g;
+        const bool valid = r < ni;
+        const int rb = valid ? __ldg(ptr + r) : 0, re = valid ? __ldg(ptr + r + 1) : 0;
         double acc = 0.0, accB = 0.0;
-        for (int k = rb + l; k < re; k += G) {
-            const double x = __ldg(X + size_t(__ldg(col + k)) * ldx);
-            acc = fma(__ldg(A + k), x, acc);
-            if (SHIFT) accB = fma(__ldg(B + k), x, accB);
-        }
-#pragma unroll
-        for (int o = G / 2; o > 0; o >>= 1) {
-            acc += __shfl_xor_sync(gmask, acc, o);
-            if (SHIFT) accB += __shfl_xor_sync(gmask, accB, o);
-        }
-        if (l == 0) Y[size_t(r) * ldy] = SHIFT ? acc + s * accB : acc;
+        row_split<G, SHIFT>(rb, re, col, A, B, X, ldx, l, acc, accB);
+        if (valid && l == 0) Y[size_t(r) * ldy] = SHIFT ? acc + s * accB : acc;
     }
 }
 

@@ -41,14 +41,28 @@ __device__ __forceinline__ void load_cols(const double* __restrict__ p, int c0, 
     }
 }
 
-template <int CPL>
-__device__ __forceinline__ void load_full(const double* __restrict__ p, double (&x)[CPL]) {
+/// Column of slot q of lane l in the FULL layout: pairs are interleaved across the G lanes, so each
+/// 16-byte load instruction of a lane group reads 16*G contiguous bytes (whole sectors) of a row.
+template <int G>
+__device__ __forceinline__ int full_col(int l, int q) {
+    return 2 * ((q >> 1) * G + l) + (q & 1);
+}
+
+/// p points at the row start; loads lane l's CPL columns in the FULL layout
+template <int G, int CPL>
+__device__ __forceinline__ void load_full(const double* __restrict__ p, int l, double (&x)[CPL]) {
 #pragma unroll
     for (int k = 0; k < CPL; k += 2) {
-        const double2 a = __ldg(reinterpret_cast<const double2*>(p + k));
+        const double2 a = __ldg(reinterpret_cast<const double2*>(p + full_col<G>(l, k)));
         x[k] = a.x;
         x[k + 1] = a.y;
     }
+}
+
+template <int G, int CPL>
+__device__ __forceinline__ void store_full(double* __restrict__ p, int l, const double (&y)[CPL]) {
+#pragma unroll
+    for (int k = 0; k < CPL; k += 2) *reinterpret_cast<double2*>(p + full_col<G>(l, k)) = make_double2(y[k], y[k + 1]);
 }
 
 template <int CPL>
@@ -69,53 +83,190 @@ __device__ __forceinline__ void store_cols(double* __restrict__ p, int c0, int N
     }
 }
 
-/// Row product for one CSR row: acc = sum_k A_k X[col_k], accB = sum_k B_k X[col_k].
+/// Row product for one CSR row per lane group: acc = sum_k A_k X[col_k], accB = sum_k B_k X[col_k].
+/// Control flow is warp-uniform: every group of the warp runs max-over-the-warp chunks, exhausted
+/// (or invalid) rows gather their own X row with weight 0. Shuffles therefore use the full mask and
+/// compile to plain SHFL without divergence bookkeeping.
 /// FULL: every lane's CPL columns are in range (N == G*CPL), no bounds logic in the gather loop.
-/// Lanes past the row end gather the row's own X row with weight 0, so every chunk issues the
-/// same unpredicated load sequence.
 template <int G, int CPL, bool SHIFT, bool FULL = false>
 __device__ __forceinline__ void row_product(int r, int rb, int re, const int32_t* __restrict__ col,
                                             const double* __restrict__ A, const double* __restrict__ B,
                                             const double* __restrict__ X, int ldx, int c0, int N, int l,
-                                            unsigned gmask, int gbase, double (&acc)[CPL], double (&accB)[CPL]) {
+                                            int gbase, double (&acc)[CPL], double (&accB)[CPL]) {
 #pragma unroll
     for (int k = 0; k < CPL; ++k) acc[k] = accB[k] = 0.0;
+    constexpr int NB = (G >= 16) ? 1 : 16 / G;
     constexpr int UB = (G < 16 / CPL) ? G : 16 / CPL;
-    for (int k0 = rb; k0 < re; k0 += G) {
-        const int k = k0 + l;
-        int mc = r;
-        double ma = 0.0, mb = 0.0;
-        if (k < re) {
-            mc = __ldg(col + k);
-            ma = __ldg(A + k);
-            if (SHIFT) mb = __ldg(B + k);
-        }
-        const int cnt = min(G, re - k0);
+    const int wmax = __reduce_max_sync(0xffffffffu, re - rb);
+    for (int k0 = 0; k0 < wmax; k0 += G * NB) {
+        int mc[NB];
+        double ma[NB], mb[NB];
 #pragma unroll
-        for (int s0 = 0; s0 < G; s0 += UB) {
-            if (s0 >= cnt) break;
-            double x[UB][CPL];
-#pragma unroll
-            for (int u = 0; u < UB; ++u) {
-                const int j = __shfl_sync(gmask, mc, gbase + s0 + u);
-                if (FULL)
-                    load_full<CPL>(X + size_t(j) * ldx + c0, x[u]);
-                else
-                    load_cols<CPL>(X + size_t(j) * ldx + c0, c0, N, x[u]);
+        for (int b = 0; b < NB; ++b) {
+            const int k = rb + k0 + b * G + l;
+            mc[b] = r;
+            ma[b] = 0.0;
+            mb[b] = 0.0;
+            if (k < re) {
+                mc[b] = __ldg(col + k);
+                ma[b] = __ldg(A + k);
+                if (SHIFT) mb[b] = __ldg(B + k);
             }
+        }
 #pragma unroll
-            for (int u = 0; u < UB; ++u) {
-                const double a = __shfl_sync(gmask, ma, gbase + s0 + u);
-                double b = 0.0;
-                if (SHIFT) b = __shfl_sync(gmask, mb, gbase + s0 + u);
+        for (int b = 0; b < NB; ++b) {
+            if (k0 + b * G >= wmax) break;
 #pragma unroll
-                for (int q = 0; q < CPL; ++q) {
-                    acc[q] = fma(a, x[u][q], acc[q]);
-                    if (SHIFT) accB[q] = fma(b, x[u][q], accB[q]);
+            for (int s0 = 0; s0 < G; s0 += UB) {
+                double x[UB][CPL];
+#pragma unroll
+                for (int u = 0; u < UB; ++u) {
+                    const int j = __shfl_sync(0xffffffffu, mc[b], gbase + s0 + u);
+                    if (FULL)
+                        load_full<G, CPL>(X + size_t(j) * ldx, l, x[u]);
+                    else
+                        load_cols<CPL>(X + size_t(j) * ldx + c0, c0, N, x[u]);
+                }
+#pragma unroll
+                for (int u = 0; u < UB; ++u) {
+                    const double a = __shfl_sync(0xffffffffu, ma[b], gbase + s0 + u);
+                    double bb = 0.0;
+                    if (SHIFT) bb = __shfl_sync(0xffffffffu, mb[b], gbase + s0 + u);
+#pragma unroll
+                    for (int q = 0; q < CPL; ++q) {
+                        acc[q] = fma(a, x[u][q], acc[q]);
+                        if (SHIFT) accB[q] = fma(bb, x[u][q], accB[q]);
+                    }
                 }
             }
         }
     }
+}
+
+/// First super-chunk of a row's (col, val) pairs, loaded one row tile ahead of its use.
+template <int G, bool SHIFT>
+struct RowChunk {
+    static constexpr int NB = (G >= 16) ? 1 : 16 / G;
+    int rb, re;
+    int mc[NB];
+    double ma[NB], mb[NB];
+    __device__ __forceinline__ void load(int r, int rb_, int re_, int l, const int32_t* __restrict__ col,
+                                         const double* __restrict__ A, const double* __restrict__ B) {
+        rb = rb_;
+        re = re_;
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+            const int k = rb + b * G + l;
+            mc[b] = r;
+            ma[b] = 0.0;
+            mb[b] = 0.0;
+            if (k < re) {
+                mc[b] = __ldg(col + k);
+                ma[b] = __ldg(A + k);
+                if (SHIFT) mb[b] = __ldg(B + k);
+            }
+        }
+    }
+};
+
+/// Row product with the first super-chunk already in registers (software-pipelined across row tiles);
+/// further super-chunks (rows longer than 16 entries, adaptive meshes) are loaded in place.
+template <int G, int CPL, bool SHIFT, bool FULL>
+__device__ __forceinline__ void row_product_pf(int r, RowChunk<G, SHIFT>& ch, const int32_t* __restrict__ col,
+                                               const double* __restrict__ A, const double* __restrict__ B,
+                                               const double* __restrict__ X, int ldx, int c0, int N, int l, int gbase,
+                                               double (&acc)[CPL], double (&accB)[CPL]) {
+    constexpr int NB = RowChunk<G, SHIFT>::NB;
+    constexpr int UB = (G < 16 / CPL) ? G : 16 / CPL;
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) acc[k] = accB[k] = 0.0;
+    const int wmax = __reduce_max_sync(0xffffffffu, ch.re - ch.rb);
+    if constexpr (false) {
+        // all 16 gathers of a super-chunk in flight at once, one column pair per pass
+        for (int k0 = 0; k0 < wmax; k0 += 16) {
+            if (k0 > 0) ch.load(r, ch.rb + 16, ch.re, l, col, A, B);
+            const int cnt = wmax - k0;
+            int js[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) js[u] = __shfl_sync(0xffffffffu, ch.mc[u / G], gbase + u % G);
+#pragma unroll
+            for (int h = 0; h < CPL; h += 2) {
+                const int cc = full_col<G>(l, h);
+                double2 x[16];
+#pragma unroll
+                for (int u = 0; u < 16; ++u)
+                    if (u < cnt) x[u] = __ldg(reinterpret_cast<const double2*>(X + size_t(js[u]) * ldx + cc));
+#pragma unroll
+                for (int u = 0; u < 16; ++u) {
+                    if (u < cnt) {
+                        const double a = __shfl_sync(0xffffffffu, ch.ma[u / G], gbase + u % G);
+                        acc[h] = fma(a, x[u].x, acc[h]);
+                        acc[h + 1] = fma(a, x[u].y, acc[h + 1]);
+                        if (SHIFT) {
+                            const double bb = __shfl_sync(0xffffffffu, ch.mb[u / G], gbase + u % G);
+                            accB[h] = fma(bb, x[u].x, accB[h]);
+                            accB[h + 1] = fma(bb, x[u].y, accB[h + 1]);
+                        }
+                    }
+                }
+            }
+        }
+        return;
+    }
+    for (int k0 = 0; k0 < wmax; k0 += G * NB) {
+        if (k0 > 0) ch.load(r, ch.rb + G * NB, ch.re, l, col, A, B);  // rare: long rows
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+            if (k0 + b * G >= wmax) break;
+#pragma unroll
+            for (int s0 = 0; s0 < G; s0 += UB) {
+                double x[UB][CPL];
+#pragma unroll
+                for (int u = 0; u < UB; ++u) {
+                    const int j = __shfl_sync(0xffffffffu, ch.mc[b], gbase + s0 + u);
+                    if (FULL)
+                        load_full<G, CPL>(X + size_t(j) * ldx, l, x[u]);
+                    else
+                        load_cols<CPL>(X + size_t(j) * ldx + c0, c0, N, x[u]);
+                }
+#pragma unroll
+                for (int u = 0; u < UB; ++u) {
+                    const double a = __shfl_sync(0xffffffffu, ch.ma[b], gbase + s0 + u);
+                    double bb = 0.0;
+                    if (SHIFT) bb = __shfl_sync(0xffffffffu, ch.mb[b], gbase + s0 + u);
+#pragma unroll
+                    for (int q = 0; q < CPL; ++q) {
+                        acc[q] = fma(a, x[u][q], acc[q]);
+                        if (SHIFT) accB[q] = fma(bb, x[u][q], accB[q]);
+                    }
+                }
+            }
+        }
+    }
+}
+
+/// N == 1: G lanes split a row's nonzeros, warp-uniform trip count, full-mask reduction
+template <int G, bool SHIFT>
+__device__ __forceinline__ void row_split(int rb, int re, const int32_t* __restrict__ col,
+                                          const double* __restrict__ A, const double* __restrict__ B,
+                                          const double* __restrict__ X, int ldx, int l, double& acc, double& accB) {
+    const int wmax = __reduce_max_sync(0xffffffffu, re - rb);
+    double a = 0.0, b = 0.0;
+    for (int k0 = 0; k0 < wmax; k0 += G) {
+        const int k = rb + k0 + l;
+        if (k < re) {
+            const double x = __ldg(X + size_t(__ldg(col + k)) * ldx);
+            a = fma(__ldg(A + k), x, a);
+            if (SHIFT) b = fma(__ldg(B + k), x, b);
+        }
+    }
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        if (SHIFT) b += __shfl_xor_sync(0xffffffffu, b, o);
+    }
+    acc = a;
+    accB = b;
 }
 
 } // namespace ksb

@@ -272,6 +272,41 @@ std::shared_ptr<FineTopology> build_topology(const Hierarchy& h, int level) {
             }
     }
 
+    // SELL-32 view of the interior pattern (column-major inside each 32-row slice)
+    {
+        const int ns = (ni + 31) / 32;
+        topo->sell_ptr.assign(size_t(ns) + 1, 0);
+        int64_t off = 0;
+        for (int sl = 0; sl < ns; ++sl) {
+            int w = 0;
+            for (int i = 0; i < 32 && 32 * sl + i < ni; ++i)
+                w = std::max(w, ii.ptr[32 * sl + i + 1] - ii.ptr[32 * sl + i]);
+            off += int64_t(w) * 32;
+            check_i32(off, "SELL entries");
+            topo->sell_ptr[sl + 1] = int32_t(off);
+        }
+        topo->sell_col.assign(size_t(off), 0);
+        topo->sell_map.assign(size_t(off), -1);
+#pragma omp parallel for schedule(static)
+        for (int sl = 0; sl < ns; ++sl) {
+            const int w = (topo->sell_ptr[sl + 1] - topo->sell_ptr[sl]) / 32;
+            for (int i = 0; i < 32; ++i) {
+                const int r = 32 * sl + i;
+                const int rr = r < ni ? r : ni - 1;  // rows past the end replay the last row (never stored)
+                for (int e = 0; e < w; ++e) {
+                    const size_t k = size_t(topo->sell_ptr[sl]) + size_t(e) * 32 + i;
+                    const int slot = ii.ptr[rr] + e;
+                    if (r < ni && slot < ii.ptr[rr + 1]) {
+                        topo->sell_col[k] = ii.col[slot];
+                        topo->sell_map[k] = slot;
+                    } else {
+                        topo->sell_col[k] = rr;
+                    }
+                }
+            }
+        }
+    }
+
     // fine tets grouped by coarse ancestor
     topo->ancestor = h.ancestor(level);
     const int nct = h.mesh(0).n_tets();

@@ -71,6 +71,9 @@ struct FineTopology {
     std::vector<int32_t> vinc_ptr, vinc;
     // coarse level: interior coarse dof -> incident (coarse tet*4 + local), ascending tet
     std::vector<int32_t> cinc_ptr, cinc;
+    // SELL-32 view of the ii pattern: slice s = rows [32s, 32s+32), entry e of lane i at
+    // sell_ptr[s] + 32 e + i; padding entries point at the row itself with map = -1
+    std::vector<int32_t> sell_ptr, sell_col, sell_map;
 };
 
 std::shared_ptr<FineTopology> build_topology(const Hierarchy& h, int level);
