@@ -42,6 +42,12 @@ _PROTO = {
     "orc_operator_nnz": (I, [P, I64P]),
     "orc_operator_ii": (I, [P, IP, IP, DP]),
     "orc_operator_ib": (I, [P, IP, IP, DP]),
+    "orc_operator_full": (I, [P, IP, IP, DP]),
+    "orc_operator_solve": (I, [P, DP, DP, D, I, DP, IP, DP]),
+    "orc_keast": (I, [DP, DP]),
+    "orc_prolongation_nnz": (I, [P, I, I, I64P]),
+    "orc_prolongation_csc": (I, [P, I, I, IP, IP, DP]),
+    "orc_load_nodal": (I, [P, I, DP, DP]),
     "orc_operator_min_diag": (I, [P, DP]),
     "orc_operator_spmv": (I, [P, DP, DP]),
     "orc_operator_pcg": (I, [P, DP, DP, I, D, I, I, IP, DP]),
@@ -273,6 +279,22 @@ class Oracle:
         _chk(lib.orc_norms(self._h, level, dp(f64(f)), dp(out)))
         return out
 
+    def prolongation_matrix(self, frm, to):
+        import scipy.sparse as sp
+        nnz = C.c_int64()
+        _chk(lib.orc_prolongation_nnz(self._h, frm, to, C.byref(nnz)))
+        nc = self.n(frm)
+        ptr = np.empty(nc + 1, np.int32)
+        idx = np.empty(nnz.value, np.int32)
+        val = np.empty(nnz.value)
+        _chk(lib.orc_prolongation_csc(self._h, frm, to, ip(ptr), ip(idx), dp(val)))
+        return sp.csc_matrix((val, idx, ptr), shape=(self.n(to), nc))
+
+    def load_nodal(self, level, f):
+        out = np.empty(self.n(level))
+        _chk(lib.orc_load_nodal(self._h, level, dp(f64(f)), dp(out)))
+        return out
+
     def prolong(self, vec, frm, to):
         v = f64(vec)
         if v.ndim == 1:
@@ -326,9 +348,27 @@ class Oracle:
 class OOperator:
     def __init__(self, h):
         self._h = h
-        s = (C.c_int64 * 3)()
+        s = (C.c_int64 * 5)()
         _chk(lib.orc_operator_nnz(self._h, s))
-        self.nnz_ii, self.nnz_ib, self.ni = list(s)
+        self.nnz_ii, self.nnz_ib, self.ni, self.nnz_full, self.n = list(s)
+
+    def full(self):
+        """full n x n matrix as scipy CSC"""
+        import scipy.sparse as sp
+        ptr = np.empty(self.n + 1, np.int32)
+        idx = np.empty(self.nnz_full, np.int32)
+        val = np.empty(self.nnz_full)
+        _chk(lib.orc_operator_full(self._h, ip(ptr), ip(idx), dp(val)))
+        return sp.csc_matrix((val, idx, ptr), shape=(self.n, self.n))
+
+    def solve(self, b, bc=None, tol=1e-9, maxit=20000):
+        x = np.empty(self.n)
+        st = np.empty(3, np.int32)
+        rel = C.c_double()
+        _chk(lib.orc_operator_solve(self._h, dp(f64(b)), dp(f64(bc)) if bc is not None else None, tol, maxit, dp(x),
+                                    ip(st), C.byref(rel)))
+        return x, dict(iterations=int(st[0]), converged=bool(st[1]), breakdown=bool(st[2]),
+                       relative_residual=rel.value)
 
     def __del__(self):
         if getattr(self, "_h", None):
@@ -417,6 +457,13 @@ class OBlocks:
         _chk(lib.orc_blocks_f_g(self._h, dp(f64(phi_H)), dp(f64(theta2)), dp(f64(w_H)), theta1, dp(f), C.byref(g),
                                 dp(A2)))
         return f, g.value, (A2.reshape(self.nh, self.nh, order="F") if want_A2 else None)
+
+
+def keast():
+    b = np.empty((11, 4))
+    w = np.empty(11)
+    _chk(lib.orc_keast(dp(b), dp(w)))
+    return b, w
 
 
 def gen_eig(A, B):

@@ -227,6 +227,39 @@ int orc_operator_nnz(orc_operator* o, int64_t* s) {
         s[0] = o->E->Aii.nnz();
         s[1] = o->E->Aib.nnz();
         s[2] = o->E->Aii.rows;
+        s[3] = o->A.nnz();
+        s[4] = o->A.rows;
+    });
+}
+/// the full n x n matrix (CSC) before Dirichlet reduction
+int orc_operator_full(orc_operator* o, int* ptr, int* idx, double* val) {
+    return guard([&] { put_csc(o->A, ptr, idx, val); });
+}
+/// EllipticSolver::solve (proj/src/solver.cpp:113-131) with full-length b, bc (may be null), x;
+/// stats: iterations, converged, breakdown
+int orc_operator_solve(orc_operator* o, const double* b, const double* bc, double tol, int maxit, double* x,
+                       int* stats, double* relres) {
+    return guard([&] {
+        const int n = o->A.rows;
+        const Space& V = *o->E->V;
+        const auto& bd = V.boundary;
+        Vec xb(bd.size());
+        for (size_t i = 0; i < bd.size(); ++i) xb[i] = bc ? bc[bd[i]] : 0.0;
+        Vec rhs(V.ni());
+        for (int i = 0; i < V.ni(); ++i) rhs[i] = b[V.interior[i]];
+        if (!xb.empty()) {
+            const Vec t = o->E->Aib.mul(xb);
+            for (int i = 0; i < V.ni(); ++i) rhs[i] -= t[i];
+        }
+        SolveStats st;
+        const Vec xi = o->E->pcg(rhs, tol, maxit, &st);
+        for (int i = 0; i < n; ++i) x[i] = 0.0;
+        for (int i = 0; i < V.ni(); ++i) x[V.interior[i]] = xi[i];
+        for (size_t i = 0; i < bd.size(); ++i) x[bd[i]] = xb[i];
+        stats[0] = st.iterations;
+        stats[1] = st.converged;
+        stats[2] = st.breakdown;
+        *relres = st.relres;
     });
 }
 int orc_operator_ii(orc_operator* o, int* ptr, int* idx, double* val) {
@@ -265,6 +298,30 @@ int orc_operator_pcg(orc_operator* o, const double* B, double* X, int N, double 
             if (relres) relres[j] = st.relres;
         }
         pack(xs, X);
+    });
+}
+
+// ---------------- small pieces for the pinning tests ----------------
+int orc_keast(double* bary, double* w) {
+    return guard([&] {
+        const auto& r = keast();
+        for (size_t q = 0; q < r.size(); ++q) {
+            w[q] = r[q].w;
+            for (int k = 0; k < 4; ++k) bary[4 * q + k] = r[q].b[k];
+        }
+    });
+}
+int orc_prolongation_nnz(orc_problem* p, int from, int to, int64_t* nnz) {
+    return guard([&] { *nnz = p->p.hier.prolongation(from, to).nnz(); });
+}
+int orc_prolongation_csc(orc_problem* p, int from, int to, int* ptr, int* idx, double* val) {
+    return guard([&] { put_csc(p->p.hier.prolongation(from, to), ptr, idx, val); });
+}
+int orc_load_nodal(orc_problem* p, int level, const double* f, double* out) {
+    return guard([&] {
+        const Space& V = p->p.space(level);
+        const Vec b = load_nodal(V, Vec(f, f + V.n()));
+        std::memcpy(out, b.data(), sizeof(double) * V.n());
     });
 }
 
