@@ -235,8 +235,8 @@ def run_b200(args, world, rank, local):
     step()
     ctx.set_profiling(False)
     spmm_ms, spmm_n = ctx.kernel_time("spmm")
-    upd_ms, upd_n = ctx.kernel_time("cg_update_xr")
-    updp_ms, updp_n = ctx.kernel_time("cg_update_p")
+    upd_ms, upd_n = ctx.kernel_time("cg_update_r")
+    updp_ms, updp_n = ctx.kernel_time("cg_update_px")
     spmm_avg = spmm_ms / max(1, spmm_n)
     bytes_spmm = 12 * L.nnz_ii + 4 * (ni + 1) + 16 * ni * N_RHS
     achieved = bytes_spmm / (spmm_avg * 1e-3) / 1e9
@@ -282,8 +282,8 @@ def run_b200(args, world, rank, local):
                          "traffic": None, "kernel": "k_spmm_dot", "bytes_per_launch": bytes_spmm,
                          "avg_launch_ms": spmm_avg, "peak_kind": peak_kind},
             "spmm_hbm_frac": achieved / peak,
-            "cg_update_xr_avg_ms": upd_ms / max(1, upd_n),
-            "cg_update_p_avg_ms": updp_ms / max(1, updp_n),
+            "cg_update_r_avg_ms": upd_ms / max(1, upd_n),
+            "cg_update_px_avg_ms": updp_ms / max(1, updp_n),
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": B.nbytes, "d2h_bytes_per_step": B.nbytes,
                     "ms_per_step": e2e_ms},
             "gpu_launches": launches // max(1, args.steps) * args.steps,
@@ -301,7 +301,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--cpu-iters", type=int, default=8, help="CPU oracle sample: iterations per 16-column block")
+    ap.add_argument("--cpu-iters", type=int, default=96, help="CPU oracle sample: iterations per 16-column block")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     world, rank, local = dist_init()

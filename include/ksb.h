@@ -149,10 +149,12 @@ typedef struct {
 } ksb_cg_stats;
 
 int ksb_cg_defaults(ksb_cg_opts* o);
-/* d_B, d_X: interior blocks ni x N (ld). h_sigma: N shifts or NULL. stats: N entries (host). */
+/* d_B, d_X: interior blocks ni x N (ld; ld even when N > 1, 16-byte column pairs).
+ * h_sigma: N shifts or NULL. stats: N entries (host). */
 int ksb_cg_solve(ksb_level* l, int mat, int shift_mat, const double* h_sigma, const double* d_B,
                  double* d_X, int N, int ld, const ksb_cg_opts* o, ksb_cg_stats* h_stats);
-/* same with host buffers (H2D of B and D2H of X inside the call): the e2e entry point */
+/* same with host buffers (H2D of B and D2H of X inside the call): the e2e entry point.
+ * Any ld >= N; only the first N columns of each host row of X are written. */
 int ksb_cg_solve_host(ksb_level* l, int mat, int shift_mat, const double* h_sigma, const double* h_B,
                       double* h_X, int N, int ld, const ksb_cg_opts* o, ksb_cg_stats* h_stats);
 

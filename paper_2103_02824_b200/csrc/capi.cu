@@ -520,16 +520,20 @@ int ksb_cg_solve_host(ksb_level* l, int mat, int shift_mat, const double* h_sigm
                       int N, int ld, const ksb_cg_opts* o, ksb_cg_stats* h_stats) {
     return guard([&] {
         need(l && h_B && h_X, "null argument");
+        need(N >= 1 && ld >= N, "ld must be >= N");
         auto& c = *l->L.ctx;
-        const size_t bytes = sizeof(double) * size_t(l->L.ni) * ld;
+        // device blocks keep an even leading dimension (16-byte column pairs); host rows may be odd
+        const int dld = (N > 1 && (ld & 1)) ? ld + 1 : ld;
         auto& dB = l->owner->io_b;
         auto& dX = l->owner->io_x;
-        const int64_t cnt = int64_t(l->L.ni) * ld;
+        const int64_t cnt = int64_t(l->L.ni) * dld;
         if (dB.n < cnt) dB.alloc(cnt);
         if (dX.n < cnt) dX.alloc(cnt);
-        KSB_CUDA_CHECK(cudaMemcpyAsync(dB.p, h_B, bytes, cudaMemcpyHostToDevice, c.stream));
-        run_cg(l, mat, shift_mat, h_sigma, dB.p, dX.p, N, ld, o, h_stats);
-        KSB_CUDA_CHECK(cudaMemcpyAsync(h_X, dX.p, bytes, cudaMemcpyDeviceToHost, c.stream));
+        const size_t hp = sizeof(double) * size_t(ld), dp = sizeof(double) * size_t(dld);
+        const size_t w = sizeof(double) * size_t(N);
+        KSB_CUDA_CHECK(cudaMemcpy2DAsync(dB.p, dp, h_B, hp, w, size_t(l->L.ni), cudaMemcpyHostToDevice, c.stream));
+        run_cg(l, mat, shift_mat, h_sigma, dB.p, dX.p, N, dld, o, h_stats);
+        KSB_CUDA_CHECK(cudaMemcpy2DAsync(h_X, hp, dX.p, dp, w, size_t(l->L.ni), cudaMemcpyDeviceToHost, c.stream));
         KSB_CUDA_CHECK(cudaStreamSynchronize(c.stream));
     });
 }

@@ -11,9 +11,11 @@
 // Kernel schedule per iteration (all reductions fixed-order; the last block of each
 // producer kernel folds the per-block partials and runs the per-column scalar logic):
 //   K1 spmm_dot : Ap = (A + sigma B) p, partial p.Ap            -> alpha / breakdown
-//   K2 update_xr: x += alpha p, r -= alpha Ap, partial r.r, r.z  -> rel, check flags, beta
-//   K3 trueres  : (only when some column flagged) t = b - A x    -> converge or restart
-//   K4 update_p : p = D^-1 r + beta p
+//   K2 update_r : r -= alpha Ap, partial r.r, r.z               -> rel, check flags, beta
+//   K3 trueres  : (only when some column flagged) t = b - A x - alpha Ap -> converge or restart
+//   K4 update_px: x += alpha p (deferred from K2: K4 reads p anyway), p = D^-1 r + beta p
+// Per iteration this streams 8 column blocks through HBM outside K1 (K2: r, Ap in, r out;
+// K4: x, p, r in, x, p out) instead of 9 with the textbook x/r and p passes.
 #include <algorithm>
 #include <cstdlib>
 
@@ -145,6 +147,34 @@ __global__ void __launch_bounds__(kThreads) k_init(int ni, Cols cc, const double
     }
 }
 
+// ---------------- K1 epilogue ----------------
+/// Last-block alpha / breakdown logic shared by the K1 variants (part0 already holds the block partials);
+/// a breakdown retires its column, so the host loop can stop once none is active.
+__device__ void k1_epilogue(double* sm, int N, const Cols& cc, CgDev& s) {
+    if (!last_block(s.ctl + kTicket1)) return;
+    fold_partials(s.part0, gridDim.x, N, sm);
+    if (threadIdx.x < N) {
+        const int c = threadIdx.x;
+        const double pap = sm[c];
+        double al = 0.0;
+        if (s.status[c] == kActive) {
+            if (!cc.fixed && !(pap > 0.0)) {
+                s.status[c] = kBreakdown;
+                s.relres[c] = sqrt(s.rr[c]) / s.bnorm[c];
+            } else {
+                al = s.rz[c] / pap;
+            }
+        }
+        s.alpha[c] = al;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int na = 0;
+        for (int c = 0; c < N; ++c) na += s.status[c] == kActive;
+        s.ctl[kNActive] = na;
+    }
+}
+
 // ---------------- K1: Ap = A p, alpha ----------------
 template <int G, int CPL, bool SHIFT, bool SPLIT, bool FULL, int MINB = KSB_SPMM_MINB>
 __global__ void __launch_bounds__(kThreads, MINB) k_spmm_dot(int ni, Cols cc, const int32_t* __restrict__ ptr,
@@ -240,171 +270,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_dot(int ni, Cols cc, co
         for (int k = 0; k < ngroups; ++k) t += sm[k * width + threadIdx.x];
         s.part0[size_t(blockIdx.x) * N + threadIdx.x] = t;
     }
-    if (!last_block(s.ctl + kTicket1)) return;
-    fold_partials(s.part0, gridDim.x, N, sm);
-    if (threadIdx.x < N) {
-        const int c = threadIdx.x;
-        const double pap = sm[c];
-        double al = 0.0;
-        if (s.status[c] == kActive) {
-            if (!cc.fixed && !(pap > 0.0)) {
-                s.status[c] = kBreakdown;
-                s.relres[c] = sqrt(s.rr[c]) / s.bnorm[c];
-            } else {
-                al = s.rz[c] / pap;
-            }
-        }
-        s.alpha[c] = al;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {  // a breakdown retires its column: let the host loop stop once none is active
-        int na = 0;
-        for (int c = 0; c < N; ++c) na += s.status[c] == kActive;
-        s.ctl[kNActive] = na;
-    }
-}
-
-// ---------------- K1 (staged variant): gathers through cp.async into shared memory ----------------
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(a), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
-
-constexpr int kStageE = 16;       // row entries staged per super-chunk (a Kuhn row has <= 15)
-constexpr int kAsyncThreads = 128;
-
-/// Same contract as k_spmm_dot for N == G*CPL. Each lane copies its CPL doubles of all 16 gathered
-/// X rows of its group's row into a per-warp shared stage with LDGSTS (no register cost, all in
-/// flight together), then consumes them from shared memory.
-template <int G, int CPL, bool SHIFT>
-__global__ void __launch_bounds__(kAsyncThreads) k_spmm_dot_async(int ni, Cols cc, const int32_t* __restrict__ ptr,
-                                                                  const int32_t* __restrict__ col,
-                                                                  const double* __restrict__ A,
-                                                                  const double* __restrict__ Bv,
-                                                                  const double* __restrict__ P,
-                                                                  double* __restrict__ AP, CgDev s) {
-    extern __shared__ double sm[];
-    constexpr int NBk = kStageE / G;
-    const int N = cc.N, ld = cc.ld;
-    const int lane = threadIdx.x & 31;
-    const int g = lane / G, l = lane % G;
-    const int gbase = g * G;
-    const int rows_per_warp = 32 / G;
-    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int nwarps = (gridDim.x * blockDim.x) >> 5;
-    const int c0 = l * CPL;
-    double* stage = sm + size_t(threadIdx.x >> 5) * kStageE * 32 * CPL;
-    double pd[CPL];
-#pragma unroll
-    for (int q = 0; q < CPL; ++q) pd[q] = 0.0;
-    for (int base = warp * rows_per_warp; base < ni; base += nwarps * rows_per_warp) {
-        const int r = base + g;
-        const bool valid = r < ni;
-        const int rb = valid ? __ldg(ptr + r) : 0, re = valid ? __ldg(ptr + r + 1) : 0;
-        const int wmax = __reduce_max_sync(0xffffffffu, re - rb);
-        const int self = valid ? r : 0;
-        double acc[CPL], accB[CPL];
-#pragma unroll
-        for (int q = 0; q < CPL; ++q) acc[q] = accB[q] = 0.0;
-        for (int k0 = 0; k0 < wmax; k0 += kStageE) {
-            int mc[NBk];
-            double ma[NBk], mb[NBk];
-#pragma unroll
-            for (int b = 0; b < NBk; ++b) {
-                const int k = rb + k0 + b * G + l;
-                mc[b] = self;
-                ma[b] = 0.0;
-                mb[b] = 0.0;
-                if (k < re) {
-                    mc[b] = __ldg(col + k);
-                    ma[b] = __ldg(A + k);
-                    if (SHIFT) mb[b] = __ldg(Bv + k);
-                }
-            }
-#pragma unroll
-            for (int e = 0; e < kStageE; ++e) {
-                if (k0 + e < wmax) {
-                    const int j = __shfl_sync(0xffffffffu, mc[e / G], gbase + e % G);
-                    const double* src = P + size_t(j) * ld + c0;
-                    double* dst = stage + (e * 32 + lane) * CPL;
-#pragma unroll
-                    for (int h = 0; h < CPL; h += 2) cp_async16(dst + h, src + h);
-                }
-            }
-            cp_async_commit();
-            cp_async_wait_all();
-            __syncwarp();
-#pragma unroll
-            for (int e = 0; e < kStageE; ++e) {
-                if (k0 + e < wmax) {
-                    const double a = __shfl_sync(0xffffffffu, ma[e / G], gbase + e % G);
-                    double bb = 0.0;
-                    if (SHIFT) bb = __shfl_sync(0xffffffffu, mb[e / G], gbase + e % G);
-                    const double* xs = stage + (e * 32 + lane) * CPL;
-#pragma unroll
-                    for (int q = 0; q < CPL; q += 2) {
-                        const double2 x = *reinterpret_cast<const double2*>(xs + q);
-                        acc[q] = fma(a, x.x, acc[q]);
-                        acc[q + 1] = fma(a, x.y, acc[q + 1]);
-                        if (SHIFT) {
-                            accB[q] = fma(bb, x.x, accB[q]);
-                            accB[q + 1] = fma(bb, x.y, accB[q + 1]);
-                        }
-                    }
-                }
-            }
-            __syncwarp();
-        }
-        if (valid) {
-            if (SHIFT) {
-#pragma unroll
-                for (int q = 0; q < CPL; ++q) acc[q] = fma(s.sigma[c0 + q], accB[q], acc[q]);
-            }
-            double p[CPL];
-            load_full<G, CPL>(P + size_t(r) * ld, l, p);
-            double* y = AP + size_t(r) * ld + c0;
-#pragma unroll
-            for (int q = 0; q < CPL; q += 2) *reinterpret_cast<double2*>(y + q) = make_double2(acc[q], acc[q + 1]);
-#pragma unroll
-            for (int q = 0; q < CPL; ++q) pd[q] = fma(p[q], acc[q], pd[q]);
-        }
-    }
-    double* red = sm + size_t(kAsyncThreads / 32) * kStageE * 32 * CPL;
-    const int ngroups = blockDim.x / G;
-    const int width = G * CPL;
-    const int gid = threadIdx.x / G;
-#pragma unroll
-    for (int q = 0; q < CPL; ++q) red[gid * width + l * CPL + q] = pd[q];
-    __syncthreads();
-    if (threadIdx.x < N) {
-        double t = 0.0;
-        for (int k = 0; k < ngroups; ++k) t += red[k * width + threadIdx.x];
-        s.part0[size_t(blockIdx.x) * N + threadIdx.x] = t;
-    }
-    if (!last_block(s.ctl + kTicket1)) return;
-    fold_partials(s.part0, gridDim.x, N, red);
-    if (threadIdx.x < N) {
-        const int c = threadIdx.x;
-        const double pap = red[c];
-        double al = 0.0;
-        if (s.status[c] == kActive) {
-            if (!cc.fixed && !(pap > 0.0)) {
-                s.status[c] = kBreakdown;
-                s.relres[c] = sqrt(s.rr[c]) / s.bnorm[c];
-            } else {
-                al = s.rz[c] / pap;
-            }
-        }
-        s.alpha[c] = al;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int na = 0;
-        for (int c = 0; c < N; ++c) na += s.status[c] == kActive;
-        s.ctl[kNActive] = na;
-    }
+    k1_epilogue(sm, N, cc, s);
 }
 
 // ---------------- K1 (SELL-32 variant): one row per lane, all N <= 16 columns per lane ----------------
@@ -502,55 +368,115 @@ __global__ void __launch_bounds__(kThreads, 2) k_sell_dot(int ni, int nslices, C
         for (int k = 0; k < nwb; ++k) t += red[k * NC + threadIdx.x];
         s.part0[size_t(blockIdx.x) * N + threadIdx.x] = t;
     }
-    if (!last_block(s.ctl + kTicket1)) return;
-    fold_partials(s.part0, gridDim.x, N, red);
-    if (threadIdx.x < N) {
-        const int c = threadIdx.x;
-        const double pap = red[c];
-        double al = 0.0;
-        if (s.status[c] == kActive) {
-            if (!cc.fixed && !(pap > 0.0)) {
-                s.status[c] = kBreakdown;
-                s.relres[c] = sqrt(s.rr[c]) / s.bnorm[c];
-            } else {
-                al = s.rz[c] / pap;
-            }
-        }
-        s.alpha[c] = al;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int na = 0;
-        for (int c = 0; c < N; ++c) na += s.status[c] == kActive;
-        s.ctl[kNActive] = na;
-    }
+    k1_epilogue(red, N, cc, s);
 }
 
-// ---------------- K2: x, r update ----------------
-__global__ void __launch_bounds__(kThreads) k_update_xr(int ni, Cols cc, double* __restrict__ X, double* __restrict__ R,
-                                                        const double* __restrict__ P, const double* __restrict__ AP,
-                                                        CgDev s) {
+// ---------------- K2: r update (x is deferred to K4, which reads p anyway) ----------------
+template <int V>
+__device__ __forceinline__ void ldv(const double* __restrict__ p, double (&v)[V]) {
+    if constexpr (V == 2) {
+        const double2 a = *reinterpret_cast<const double2*>(p);
+        v[0] = a.x;
+        v[1] = a.y;
+    } else {
+        v[0] = *p;
+    }
+}
+template <int V>
+__device__ __forceinline__ void stv(double* __restrict__ p, const double (&v)[V]) {
+    if constexpr (V == 2)
+        *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
+    else
+        *p = v[0];
+}
+
+/// Elementwise layout with V adjacent columns per thread (V = 2 needs N and ld even).
+template <int V>
+struct EMap {
+    int c, r0, rstep, valid;
+    __device__ EMap(int N) {
+        const int np = N / V;
+        const int rb = max(1, int(blockDim.x) / np);
+        c = (threadIdx.x % np) * V;
+        const int rl = threadIdx.x / np;
+        valid = rl < rb;
+        r0 = blockIdx.x * rb + rl;
+        rstep = gridDim.x * rb;
+    }
+};
+
+/// block reduction of per-thread column partials (EMap<V> layout) -> part[blockIdx*N + c]
+template <int V>
+__device__ void block_cols_v(const double (&v)[V], int N, double* part, double* smem) {
+    const int np = N / V;
+    const int rb = max(1, int(blockDim.x) / np);
+    if (threadIdx.x < rb * np) {
+#pragma unroll
+        for (int q = 0; q < V; ++q) smem[(threadIdx.x / np) * N + (threadIdx.x % np) * V + q] = v[q];
+    }
+    __syncthreads();
+    if (threadIdx.x < N) {
+        double s = 0.0;
+        for (int k = 0; k < rb; ++k) s += smem[k * N + threadIdx.x];
+        part[size_t(blockIdx.x) * N + threadIdx.x] = s;
+    }
+    __syncthreads();
+}
+
+template <int V>
+__global__ void __launch_bounds__(kThreads, 4) k_update_r(int ni, Cols cc, double* __restrict__ R,
+                                                       const double* __restrict__ AP, CgDev s) {
     extern __shared__ double sm[];
     const int N = cc.N, ld = cc.ld;
-    ElemMap em(N);
-    double rr = 0.0, rz = 0.0;
+    EMap<V> em(N);
+    double rr[V], rz[V];
+#pragma unroll
+    for (int q = 0; q < V; ++q) rr[q] = rz[q] = 0.0;
     if (em.valid) {
-        const double al = s.alpha[em.c];
-        const bool act = s.status[em.c] == kActive;
-        for (int r = em.r0; r < ni; r += em.rstep) {
-            const size_t i = size_t(r) * ld + em.c;
-            double rv = R[i];
-            if (act) {
-                X[i] = fma(al, P[i], X[i]);
-                rv = fma(-al, AP[i], rv);
-                R[i] = rv;
-            }
-            rr = fma(rv, rv, rr);
-            rz = fma(rv, dinv_of(s.diagA, s.diagB, s.sigma, r, em.c) * rv, rz);
+        double al[V], sg[V];
+        bool any = false;
+#pragma unroll
+        for (int q = 0; q < V; ++q) {
+            al[q] = s.status[em.c + q] == kActive ? s.alpha[em.c + q] : 0.0;
+            sg[q] = s.diagB ? s.sigma[em.c + q] : 0.0;
+            any |= s.status[em.c + q] == kActive;
         }
+        // U rows per trip, all loads issued before the first use (bytes in flight per thread)
+        constexpr int U = 2;
+        if (any)
+            for (int r0 = em.r0; r0 < ni; r0 += U * em.rstep) {
+                double rv[U][V], ap[U][V], da[U], db[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int r = r0 + u * em.rstep;
+                    if (r < ni) {
+                        const size_t i = size_t(r) * ld + em.c;
+                        ldv<V>(R + i, rv[u]);
+                        ldv<V>(AP + i, ap[u]);
+                        da[u] = s.diagA[r];
+                        db[u] = s.diagB ? s.diagB[r] : 0.0;
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int r = r0 + u * em.rstep;
+                    if (r < ni) {
+#pragma unroll
+                        for (int q = 0; q < V; ++q) rv[u][q] = fma(-al[q], ap[u][q], rv[u][q]);
+                        stv<V>(R + size_t(r) * ld + em.c, rv[u]);
+#pragma unroll
+                        for (int q = 0; q < V; ++q) {
+                            const double d = fma(sg[q], db[u], da[u]);
+                            const double dinv = d != 0.0 ? 1.0 / d : 1.0;
+                            rr[q] = fma(rv[u][q], rv[u][q], rr[q]);
+                            rz[q] = fma(rv[u][q], dinv * rv[u][q], rz[q]);
+                        }
+                    }
+                }
+            }
     }
-    block_cols(rr, N, s.part0, sm);
-    block_cols(rz, N, s.part1, sm);
+    block_cols_v<V>(rr, N, s.part0, sm);
+    block_cols_v<V>(rz, N, s.part1, sm);
     if (!last_block(s.ctl + kTicket2)) return;
     fold_partials(s.part0, gridDim.x, N, sm);
     fold_partials(s.part1, gridDim.x, N, sm + N);
@@ -586,7 +512,8 @@ template <int G, int CPL, bool SHIFT, bool SPLIT, bool FULL>
 __global__ void __launch_bounds__(kThreads, 3) k_trueres(int ni, Cols cc, const int32_t* __restrict__ ptr,
                                                       const int32_t* __restrict__ col, const double* __restrict__ A,
                                                       const double* __restrict__ Bv, const double* __restrict__ Bb,
-                                                      const double* __restrict__ X, double* __restrict__ R, CgDev s) {
+                                                      const double* __restrict__ X, const double* __restrict__ AP,
+                                                      double* __restrict__ R, CgDev s) {
     extern __shared__ double sm[];
     if (s.ctl[kAnyCheck] == 0) return;  // uniform early exit: nothing flagged this iteration
     const int N = cc.N, ld = cc.ld;
@@ -615,9 +542,10 @@ __global__ void __launch_bounds__(kThreads, 3) k_trueres(int ni, Cols cc, const 
             for (int q = 0; q < CPL; ++q) {
                 const int c = FULL ? full_col<G>(l, q) : c0 + q;
                 if (c < N && s.check[c]) {
+                    // X still holds x_k (K4 applies x += alpha p): A x_{k+1} = A x_k + alpha Ap
                     const double ax = SHIFT ? fma(s.sigma[c], accB[q], acc[q]) : acc[q];
                     const size_t i = size_t(r) * ld + c;
-                    const double t = Bb[i] - ax;
+                    const double t = Bb[i] - fma(s.alpha[c], AP[i], ax);
                     R[i] = t;
                     tt[q] = fma(t, t, tt[q]);
                     tz[q] = fma(t, dinv_of(s.diagA, s.diagB, s.sigma, r, c) * t, tz[q]);
@@ -666,17 +594,64 @@ __global__ void __launch_bounds__(kThreads, 3) k_trueres(int ni, Cols cc, const 
     }
 }
 
-// ---------------- K4: p update ----------------
-__global__ void __launch_bounds__(kThreads) k_update_p(int ni, Cols cc, const double* __restrict__ R,
-                                                       double* __restrict__ P, CgDev s) {
+// ---------------- K4: x += alpha p (deferred from K2), p = D^-1 r + beta p ----------------
+template <int V>
+__global__ void __launch_bounds__(kThreads, 4) k_update_px(int ni, Cols cc, double* __restrict__ X,
+                                                        const double* __restrict__ R, double* __restrict__ P,
+                                                        CgDev s) {
     const int N = cc.N, ld = cc.ld;
-    ElemMap em(N);
+    EMap<V> em(N);
     if (!em.valid) return;
-    if (s.status[em.c] != kActive) return;
-    const double be = s.beta[em.c];
-    for (int r = em.r0; r < ni; r += em.rstep) {
-        const size_t i = size_t(r) * ld + em.c;
-        P[i] = fma(be, P[i], dinv_of(s.diagA, s.diagB, s.sigma, r, em.c) * R[i]);
+    double al[V], be[V], sg[V];
+    bool act[V], anyx = false, anyp = false;
+#pragma unroll
+    for (int q = 0; q < V; ++q) {
+        al[q] = s.alpha[em.c + q];  // 0 for columns not active at K1 of this iteration
+        act[q] = s.status[em.c + q] == kActive;
+        be[q] = s.beta[em.c + q];
+        sg[q] = s.diagB ? s.sigma[em.c + q] : 0.0;
+        anyx |= al[q] != 0.0;
+        anyp |= act[q];
+    }
+    if (!anyx && !anyp) return;
+    constexpr int U = 2;
+    for (int r0 = em.r0; r0 < ni; r0 += U * em.rstep) {
+        double pv[U][V], xv[U][V], rv[U][V], da[U], db[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int r = r0 + u * em.rstep;
+            if (r < ni) {
+                const size_t i = size_t(r) * ld + em.c;
+                ldv<V>(P + i, pv[u]);
+                if (anyx) ldv<V>(X + i, xv[u]);
+                if (anyp) {
+                    ldv<V>(R + i, rv[u]);
+                    da[u] = s.diagA[r];
+                    db[u] = s.diagB ? s.diagB[r] : 0.0;
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int r = r0 + u * em.rstep;
+            if (r < ni) {
+                const size_t i = size_t(r) * ld + em.c;
+                if (anyx) {
+#pragma unroll
+                    for (int q = 0; q < V; ++q) xv[u][q] = fma(al[q], pv[u][q], xv[u][q]);
+                    stv<V>(X + i, xv[u]);
+                }
+                if (anyp) {
+#pragma unroll
+                    for (int q = 0; q < V; ++q) {
+                        const double d = fma(sg[q], db[u], da[u]);
+                        const double z = (d != 0.0 ? 1.0 / d : 1.0) * rv[u][q];
+                        if (act[q]) pv[u][q] = fma(be[q], pv[u][q], z);
+                    }
+                    stv<V>(P + i, pv[u]);
+                }
+            }
+        }
     }
 }
 
@@ -712,7 +687,7 @@ Plan plan_for(int N) {
 }
 
 struct SellOps {
-    const double *A = nullptr, *B = nullptr;
+    const double *A = nullptr, *B = nullptr;  // SELL-32 values (N <= 2)
 };
 
 template <int NC, bool SHIFT>
@@ -738,23 +713,11 @@ template <int G, int CPL, bool SHIFT, bool SPLIT, bool FULL>
 void launch_iteration(Ctx& c, const Level& L, const CgWork& w, const Cols& cc, const double* A, const double* Bv,
                       const double* Bb, double* X, int grid_s, int grid_e, const SellOps& so) {
     const size_t sm_s = sizeof(double) * std::max<size_t>(size_t(kThreads / G) * G * CPL, 2 * size_t(cc.N));
-    const size_t sm_e = sizeof(double) * std::max<size_t>(kThreads, 2 * size_t(cc.N));
-    grid_e = std::min(grid_e, resident_grid(c, k_update_xr, kThreads, sm_e));
+    const size_t sm_e = sizeof(double) * std::max<size_t>(2 * kThreads, 2 * size_t(cc.N));
+    const bool v2 = (cc.N % 2 == 0) && (cc.ld % 2 == 0);
+    grid_e = std::min(grid_e, v2 ? resident_grid(c, k_update_r<2>, kThreads, sm_e)
+                                 : resident_grid(c, k_update_r<1>, kThreads, sm_e));
     if (try_sell<SHIFT>(c, L, w, cc, so)) {
-    } else if constexpr (FULL && !SPLIT && false) {
-        const size_t sm_a = sizeof(double) * (size_t(kAsyncThreads / 32) * kStageE * 32 * CPL +
-                                              std::max<size_t>(size_t(kAsyncThreads) * CPL, 2 * size_t(cc.N)));
-        static bool attr = false;
-        if (!attr) {
-            KSB_CUDA_CHECK(cudaFuncSetAttribute(k_spmm_dot_async<G, CPL, SHIFT>,
-                                                cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm_a)));
-            attr = true;
-        }
-        const int rows_per_block = kAsyncThreads / G;
-        const int want = ceil_div(L.ni, rows_per_block);
-        const int ga = std::min(want, resident_grid(c, k_spmm_dot_async<G, CPL, SHIFT>, kAsyncThreads, sm_a));
-        launch(c, "spmm", k_spmm_dot_async<G, CPL, SHIFT>, ga, kAsyncThreads, sm_a, L.ni, cc,
-               (const int32_t*)L.ii_ptr.p, (const int32_t*)L.ii_col.p, A, Bv, (const double*)w.P, w.AP, w.dev);
     } else {
         static const char* mb = std::getenv("KSB_SPMM_MINB");
         const int minb = mb ? std::atoi(mb) : KSB_SPMM_MINB;
@@ -772,12 +735,18 @@ void launch_iteration(Ctx& c, const Level& L, const CgWork& w, const Cols& cc, c
         else
             go(k_spmm_dot<G, CPL, SHIFT, SPLIT, FULL>);
     }
-    launch(c, "cg_update_xr", k_update_xr, grid_e, kThreads, sm_e, L.ni, cc, X, w.R, (const double*)w.P,
-           (const double*)w.AP, w.dev);
+    if (v2)
+        launch(c, "cg_update_r", k_update_r<2>, grid_e, kThreads, sm_e, L.ni, cc, w.R, (const double*)w.AP, w.dev);
+    else
+        launch(c, "cg_update_r", k_update_r<1>, grid_e, kThreads, sm_e, L.ni, cc, w.R, (const double*)w.AP, w.dev);
     if (!cc.fixed)
         launch(c, "cg_trueres", k_trueres<G, CPL, SHIFT, SPLIT, FULL>, grid_s, kThreads, sm_s, L.ni, cc,
-               (const int32_t*)L.ii_ptr.p, (const int32_t*)L.ii_col.p, A, Bv, Bb, (const double*)X, w.R, w.dev);
-    launch(c, "cg_update_p", k_update_p, grid_e, kThreads, 0, L.ni, cc, (const double*)w.R, w.P, w.dev);
+               (const int32_t*)L.ii_ptr.p, (const int32_t*)L.ii_col.p, A, Bv, Bb, (const double*)X,
+               (const double*)w.AP, w.R, w.dev);
+    if (v2)
+        launch(c, "cg_update_px", k_update_px<2>, grid_e, kThreads, 0, L.ni, cc, X, (const double*)w.R, w.P, w.dev);
+    else
+        launch(c, "cg_update_px", k_update_px<1>, grid_e, kThreads, 0, L.ni, cc, X, (const double*)w.R, w.P, w.dev);
 }
 
 template <bool SHIFT>

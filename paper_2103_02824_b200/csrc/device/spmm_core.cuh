@@ -181,38 +181,6 @@ __device__ __forceinline__ void row_product_pf(int r, RowChunk<G, SHIFT>& ch, co
 #pragma unroll
     for (int k = 0; k < CPL; ++k) acc[k] = accB[k] = 0.0;
     const int wmax = __reduce_max_sync(0xffffffffu, ch.re - ch.rb);
-    if constexpr (false) {
-        // all 16 gathers of a super-chunk in flight at once, one column pair per pass
-        for (int k0 = 0; k0 < wmax; k0 += 16) {
-            if (k0 > 0) ch.load(r, ch.rb + 16, ch.re, l, col, A, B);
-            const int cnt = wmax - k0;
-            int js[16];
-#pragma unroll
-            for (int u = 0; u < 16; ++u) js[u] = __shfl_sync(0xffffffffu, ch.mc[u / G], gbase + u % G);
-#pragma unroll
-            for (int h = 0; h < CPL; h += 2) {
-                const int cc = full_col<G>(l, h);
-                double2 x[16];
-#pragma unroll
-                for (int u = 0; u < 16; ++u)
-                    if (u < cnt) x[u] = __ldg(reinterpret_cast<const double2*>(X + size_t(js[u]) * ldx + cc));
-#pragma unroll
-                for (int u = 0; u < 16; ++u) {
-                    if (u < cnt) {
-                        const double a = __shfl_sync(0xffffffffu, ch.ma[u / G], gbase + u % G);
-                        acc[h] = fma(a, x[u].x, acc[h]);
-                        acc[h + 1] = fma(a, x[u].y, acc[h + 1]);
-                        if (SHIFT) {
-                            const double bb = __shfl_sync(0xffffffffu, ch.mb[u / G], gbase + u % G);
-                            accB[h] = fma(bb, x[u].x, accB[h]);
-                            accB[h + 1] = fma(bb, x[u].y, accB[h + 1]);
-                        }
-                    }
-                }
-            }
-        }
-        return;
-    }
     for (int k0 = 0; k0 < wmax; k0 += G * NB) {
         if (k0 > 0) ch.load(r, ch.rb + G * NB, ch.re, l, col, A, B);  // rare: long rows
 #pragma unroll

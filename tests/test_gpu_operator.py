@@ -81,7 +81,7 @@ def test_spmm_matches_oracle(ctx):
         assert np.abs(Y - ref).max() <= 1e-12 * np.abs(ref).max(), N
 
 
-@pytest.mark.parametrize("N", [1, 4, 16])
+@pytest.mark.parametrize("N", [1, 3, 4, 16, 24])
 def test_cg_matches_oracle_jacobi(ctx, N):
     h, orc = hierarchy(adapt=1)
     lev = h.n_levels - 1
