@@ -56,7 +56,13 @@ def solve_level_corrected(L: api.Level, lambdas: np.ndarray, Phi: api.DeviceArra
     """Outer iterations on one level (proj/src/driver.cpp:106-155); state updated in place."""
     res = LevelResult(level=level, n_dofs=L.n, outer_iterations=0, lambdas=lambdas)
     for outer in range(max_outer):
-        lg = L.correction_step(lambdas, Phi, w, **step_opts)
+        try:
+            lg = L.correction_step(lambdas, Phi, w, **step_opts)
+        except KsbError as e:  # keep the trajectory so far for diagnostics, re-raise unchanged
+            e.partial = res
+            e.step = outer
+            raise
+        lg["lambda"] = np.array(lambdas, copy=True).tolist()
         res.inner_iterations.append(lg["inner_iterations"])
         res.deltas.append(lg["delta"])
         res.logs.append(lg)

@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--max-outer", type=int, default=40)
     ap.add_argument("--json", default="")
     ap.add_argument("--dump", default="")
+    ap.add_argument("--final-npz", default="", help="save each converged level's final orbitals and w here")
     a = ap.parse_args()
     orc = Oracle(ATOMS, n_pairs=1, occ=2.0, xc="lda")
     m = OMesh.box([-10.0] * 3, [10.0] * 3, 8)
@@ -38,6 +39,7 @@ def main():
     lam, orb, w, it = orc.coarse_scf(tol=a.tol, mixing=0.3, tol_eig=1e-9)
     print("coarse", lam.tolist(), it, flush=True)
     out = []
+    finals = {}
     for lev in range(1, a.levels + 1):
         orb = orc.prolong(orb, lev - 1, lev)
         w = orc.prolong(w, lev - 1, lev)[:, 0]
@@ -59,6 +61,10 @@ def main():
             if lg["delta"] < a.tol:
                 break
         out.append({"level": lev, "steps": steps, "energy": orc.energy(lev, orb, w).tolist()})
+        if a.final_npz and steps and "error" not in steps[-1]:
+            finals[f"orb_level{lev}"] = orb
+            finals[f"w_level{lev}"] = w
+            np.savez_compressed(a.final_npz, **finals)
         if steps and "error" in steps[-1]:
             break
     if a.json:

@@ -62,8 +62,12 @@ def run(levels=3, oracle_levels=0, tol_outer=1e-6, verbose=True, dump_dir=""):
         try:
             r = solve_level_corrected(L, lam, Phi, dw, tol_outer=tol_outer, level=lev)
         except kb.KsbError as e:
-            print("gpu level", lev, "failed:", e, flush=True)
-            out["gpu_error"] = str(e)
+            part = getattr(e, "partial", None)
+            rec = {"level": lev, "failed_step": getattr(e, "step", None), "error": str(e),
+                   "deltas": part.deltas if part else [], "inner": part.inner_iterations if part else [],
+                   "lambdas": [lg["lambda"] for lg in part.logs] if part else []}
+            print("gpu level", lev, "failed:", json.dumps(rec), flush=True)
+            out["gpu_error"] = rec
             break
         wall = time.time() - t
         e = L.energy(Phi, dw)
@@ -72,13 +76,15 @@ def run(levels=3, oracle_levels=0, tol_outer=1e-6, verbose=True, dump_dir=""):
                "step_ms": [lg["ms_total"] for lg in r.logs], "bvp_ms": [lg["ms_bvp"] for lg in r.logs],
                "hartree_ms": [lg["ms_hartree"] for lg in r.logs], "project_ms": [lg["ms_project"] for lg in r.logs],
                "inner_ms": [lg["ms_inner"] for lg in r.logs], "cg_iterations": [lg["cg_iterations"] for lg in r.logs],
-               "attempts": [lg["attempts"] for lg in r.logs], "deltas": r.deltas}
+               "attempts": [lg["attempts"] for lg in r.logs], "deltas": r.deltas,
+               "lambdas": [lg["lambda"] for lg in r.logs]}
         out["gpu"].append(rec)
         if verbose:
             print("gpu", json.dumps(rec), flush=True)
         full = np.zeros((L.n, 1))
         full[it] = Phi.download()
         orb, w = full, dw.download()
+        out.setdefault("finals", {})[lev] = {"orb": orb.copy(), "w": w.copy()}
         L.close()
 
     lam = lam0.copy()
