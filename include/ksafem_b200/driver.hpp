@@ -1,0 +1,70 @@
+// The callers of the path (proj/src/driver.cpp:35-47 make_level_ops, :94-163 solve_level_corrected), with the
+// fused device correction step as the B200 form of the outer iteration's body.
+#pragma once
+
+#include "ksafem_b200/correction.hpp"
+
+namespace ksafem::driver {
+
+struct LevelOps {
+    fem::SpacePtr space;
+    SpMat S, M, a_op;  // a_op = 1/2 S + M_{v_ext}
+    std::unique_ptr<fem::EllipticSolver> stiffness;
+    fem::Prolongation P_full;
+};
+
+LevelOps make_level_ops(const fem::SpaceHierarchy& hier, int level, const model::MolecularSystem& sys,
+                        WorkerPool* pool = nullptr);
+
+struct StepOptions {
+    double tol_linear = 1e-9;
+    double tol_inner = 1e-8;
+    double score_floor = 1e-8;
+    int max_inner = 400;
+    int nev_scan_pad = 4;
+    bool hartree = true;
+    bool xc = true;
+};
+
+struct StepLog {
+    int inner_iterations = 0;
+    int hartree_iterations = 0;
+    double delta = 0;  // H1 norm of the density change
+    double ms_bvp = 0, ms_hartree = 0, ms_project = 0, ms_inner = 0, ms_total = 0;
+    std::vector<int> attempts, cg_iterations;
+};
+
+/// One outer iteration of solve_level_corrected (proj/src/driver.cpp:106-150) on device-resident state:
+/// orbitals (interior block, row-major ni x N) and w stay in HBM between steps.
+class CorrectionState {
+public:
+    CorrectionState(const LevelOps& ops, const model::MolecularSystem& sys, const StepOptions& opt,
+                    const VecX& lambdas, const std::vector<fem::FEFunction>& orbitals, const fem::FEFunction& w);
+    StepLog step();
+    VecX lambdas() const { return lambda_; }
+    std::vector<fem::FEFunction> orbitals() const;
+    fem::FEFunction hartree() const;
+
+private:
+    fem::SpacePtr space_;
+    int N_ = 0, ld_ = 0;
+    StepOptions opt_;
+    VecX lambda_;
+    b200::DeviceBuffer phi_, w_;
+};
+
+struct LevelResult {
+    VecX lambdas;
+    std::vector<fem::FEFunction> orbitals;
+    fem::FEFunction hartree;
+    int outer_iterations = 0;
+    std::vector<int> inner_iterations;
+    std::vector<double> deltas;
+};
+
+/// outer loop until the density change drops below tol_outer; "nonconvergence" at max_outer
+LevelResult solve_level_corrected(const LevelOps& ops, const model::MolecularSystem& sys, const StepOptions& opt,
+                                  const VecX& lambdas, const std::vector<fem::FEFunction>& orbitals,
+                                  const fem::FEFunction& w, double tol_outer = 1e-6, int max_outer = 40);
+
+} // namespace ksafem::driver

@@ -159,6 +159,15 @@ int ksb_cg_solve_host(ksb_level* l, int mat, int shift_mat, const double* h_sigm
                       double* h_X, int N, int ld, const ksb_cg_opts* o, ksb_cg_stats* h_stats);
 
 
+/* fem::EllipticSolver::solve / solve_zero_bc (proj/src/solver.cpp:113-135): interior rhs b_I - A_ib bc_B,
+ * PCG (Jacobi) on A_ii, full-length x whose boundary entries are bc (0 when d_bc_full is NULL).
+ * b and bc are full-length (n); interior entries of bc are ignored. */
+int ksb_solve(ksb_level* l, int mat, const double* d_b_full, const double* d_bc_full, const ksb_cg_opts* o,
+              double* d_x_full, ksb_cg_stats* h_stats);
+/* EllipticSolver::min_diagonal (proj/src/solver.cpp:44): min over the interior diagonal of A_ii */
+int ksb_mat_min_diag(ksb_level* l, int mat, double* h_out);
+
+
 /* ---------------- the correction step (one outer iteration, proj/src/driver.cpp:106-150) ----------------
  * Orbitals are interior blocks (ni x ld, row-major): the correction algorithm keeps them in the
  * zero-trace space, so boundary values are structurally zero. Potentials (w, v_xc, rho) are
@@ -203,12 +212,19 @@ int ksb_correction_step_host(ksb_level* l, const ksb_step_opts* o, double* h_lam
 /* pieces of the step, for parity checks against the reference's functions */
 /* model::density + xc_potential_field (proj/src/ks_model.cpp:43-52,101-105); d_vxc may be NULL */
 int ksb_density_xc(ksb_level* l, const double* d_Phi, int N, int ld, double* d_rho, double* d_vxc);
+/* model::density (proj/src/ks_model.cpp:43-52) with an explicit occupancy, full length (boundary entries 0) */
+int ksb_density(ksb_level* l, const double* d_Phi, int N, int ld, double occupancy, double* d_rho_full);
 /* hartree::compute_moments (proj/src/hartree.cpp:15-63): q, centre[3], dipole[3], quadrupole[9] */
 int ksb_moments(ksb_level* l, const double* d_rho, double h_out[16]);
 /* hartree::boundary_values at the boundary vertices, boundary numbering (proj/src/hartree.cpp:76-82) */
 int ksb_boundary_values(ksb_level* l, const double h_moments[16], double* d_bcb);
 /* hartree::squared_density_load restricted to interior rows (proj/src/hartree.cpp:108-129) */
 int ksb_sqload(ksb_level* l, const double* d_Phi, int N, int ld, double* d_out_int);
+/* hartree::squared_density_load, full length n incl. boundary rows (proj/src/hartree.cpp:108-129) */
+int ksb_sqload_full(ksb_level* l, const double* d_Phi, int N, int ld, double occupancy, double* d_out_full);
+/* model::xc_potential_field (proj/src/ks_model.cpp:101-105): v_xc(rho) nodewise, full length */
+int ksb_xc_field(ksb_level* l, int xc_kind, double alpha, double exchange_exponent, const double* d_rho_full,
+                 double* d_vxc_full);
 /* corr::bvp_hartree (proj/src/correction.cpp:67-75): full-length w with boundary data d_bcb */
 int ksb_hartree_solve(ksb_level* l, const double* d_Phi, int N, int ld, const double* d_bcb, double tol,
                       double* d_w_full, int* h_iters);
@@ -216,6 +232,14 @@ int ksb_hartree_solve(ksb_level* l, const double* d_Phi, int N, int ld, const do
 int ksb_outer_solve(ksb_level* l, const ksb_step_opts* o, const double* d_what_full, const double* d_vxc_full,
                     const double* h_lambda, const double* d_Phi, int ld, double* d_PhiT, int* h_attempts,
                     int* h_iters, double* h_min_diag);
+/* OuterOperator constructor (proj/src/correction.cpp:15-24): H = values(aop_mat) + M_{what + vxc} into the level's
+ * H slot (one live OuterOperator per level); h_min_diag = min interior diagonal of H */
+int ksb_outer_build(ksb_level* l, int aop_mat, const double* d_what_full, const double* d_vxc_full,
+                    double* h_min_diag);
+/* OuterOperator::solve_orbital for N orbitals (columns of d_Phi, interior block) against the built H
+ * (proj/src/correction.cpp:26-61): unshifted PCG, then the shift ladder on the columns that failed */
+int ksb_outer_apply(ksb_level* l, const ksb_step_opts* o, const double* h_lambda, const double* d_Phi, int N, int ld,
+                    double* d_PhiT, int* h_attempts, int* h_iters);
 /* corr::prepare_blocks (proj/src/correction.cpp:113-212): w_tilde0 (zero trace) and the lift ell, full length */
 int ksb_prepare_blocks(ksb_level* l, const double* d_PhiT, int ld, const double* d_wt_full, const double* d_ell_full,
                        const double* d_vxc_full);

@@ -90,6 +90,8 @@ PROTOTYPES = {
     "ksb_cg_defaults": (I, [C.POINTER(CgOpts)]),
     "ksb_cg_solve": (I, [P, I, I, DP, P, P, I, I, C.POINTER(CgOpts), C.POINTER(CgStats)]),
     "ksb_cg_solve_host": (I, [P, I, I, DP, P, P, I, I, C.POINTER(CgOpts), C.POINTER(CgStats)]),
+    "ksb_solve": (I, [P, I, P, P, C.POINTER(CgOpts), P, C.POINTER(CgStats)]),
+    "ksb_mat_min_diag": (I, [P, I, DP]),
     "ksb_step_defaults": (I, [SOP]),
     "ksb_system_set": (I, [P, DP, I, I, D, I, D, D, I, I]),
     "ksb_level_ops": (I, [P]),
@@ -101,6 +103,11 @@ PROTOTYPES = {
     "ksb_sqload": (I, [P, P, I, I, P]),
     "ksb_hartree_solve": (I, [P, P, I, I, P, D, P, IP]),
     "ksb_outer_solve": (I, [P, SOP, P, P, DP, P, I, P, IP, IP, DP]),
+    "ksb_sqload_full": (I, [P, P, I, I, D, P]),
+    "ksb_density": (I, [P, P, I, I, D, P]),
+    "ksb_xc_field": (I, [P, I, D, D, P, P]),
+    "ksb_outer_build": (I, [P, I, P, P, DP]),
+    "ksb_outer_apply": (I, [P, SOP, DP, P, I, I, P, IP, IP]),
     "ksb_prepare_blocks": (I, [P, P, I, P, P, P]),
     "ksb_blocks_get": (I, [P, I, DP]),
     "ksb_inner_scf": (I, [P, SOP, DP, DP, DP, DP, DP, DP, IP, DP, I]),

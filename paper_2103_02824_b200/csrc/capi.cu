@@ -23,6 +23,7 @@ struct ksb_level {
     ksb_ctx* owner = nullptr;
     ksb::Level L;
     std::unique_ptr<ksb::Corrector> K;
+    ksb::DevBuf<double> scratch;  // EllipticSolver::solve staging (interior rhs / solution, boundary data)
     ksb::Corrector& corr() {
         if (!K) K = std::make_unique<ksb::Corrector>();
         return *K;
@@ -367,6 +368,8 @@ int ksb_level_create(ksb_ctx* c, const ksb_hier* h, int level, ksb_level** out) 
             L.anc_tets.upload(cx, T.anc_tets);
             L.vinc_ptr.upload(cx, T.vinc_ptr);
             L.vinc.upload(cx, T.vinc);
+            L.bvinc_ptr.upload(cx, T.bvinc_ptr);
+            L.bvinc.upload(cx, T.bvinc);
             L.cinc_ptr.upload(cx, T.cinc_ptr);
             L.cinc.upload(cx, T.cinc);
             L.ctets.upload(cx, T.coarse->mesh->tets);
@@ -539,6 +542,38 @@ int ksb_cg_solve_host(ksb_level* l, int mat, int shift_mat, const double* h_sigm
 }
 
 
+// ---------------- EllipticSolver ----------------
+int ksb_solve(ksb_level* l, int mat, const double* d_b_full, const double* d_bc_full, const ksb_cg_opts* o,
+              double* d_x_full, ksb_cg_stats* st) {
+    return guard([&] {
+        need(l && d_b_full && d_x_full, "null argument");
+        if (mat < 0 || mat >= ksb::kMaxMats) ksb::raise(KSB_INVALID_ARGUMENT, "bad matrix id");
+        ksb::CgOptions co;
+        if (o) {
+            if (o->precond != 0) ksb::raise(KSB_INVALID_ARGUMENT, "only the Jacobi preconditioner is available");
+            co.tol = o->tol;
+            co.max_iterations = o->max_iterations;
+            co.fixed_iterations = o->fixed_iterations;
+            co.check_every = o->check_every;
+        }
+        const auto r = ksb::elliptic_solve(l->L, l->owner->cg, l->scratch, mat, d_b_full, d_bc_full, co, d_x_full);
+        if (st) {
+            st->iterations = r.iterations;
+            st->relative_residual = r.relative_residual;
+            st->converged = r.converged;
+            st->breakdown = r.breakdown;
+        }
+    });
+}
+
+int ksb_mat_min_diag(ksb_level* l, int mat, double* out) {
+    return guard([&] {
+        need(l && out, "null argument");
+        if (mat < 0 || mat >= ksb::kMaxMats) ksb::raise(KSB_INVALID_ARGUMENT, "bad matrix id");
+        *out = ksb::min_diagonal(l->L, mat, l->scratch);
+    });
+}
+
 // ---------------- correction step ----------------
 static ksb::StepOptions step_opts(const ksb_step_opts* o) {
     ksb::StepOptions so;
@@ -666,6 +701,15 @@ int ksb_density_xc(ksb_level* l, const double* d_Phi, int N, int ld, double* d_r
     });
 }
 
+int ksb_density(ksb_level* l, const double* d_Phi, int N, int ld, double occ, double* d_rho) {
+    return guard([&] {
+        need(l && d_Phi && d_rho, "null argument");
+        if (N < 1 || ld < N) ksb::raise(KSB_INVALID_ARGUMENT, "bad block shape");
+        ksb::rho_vxc(l->L, d_Phi, N, ld, occ, ksb::XcParams{0, 0.0, 0.0}, d_rho, nullptr);
+        KSB_CUDA_CHECK(cudaStreamSynchronize(l->L.ctx->stream));
+    });
+}
+
 int ksb_moments(ksb_level* l, const double* d_rho, double out[16]) {
     return guard([&] {
         need(l && d_rho && out, "null argument");
@@ -705,6 +749,24 @@ int ksb_sqload(ksb_level* l, const double* d_Phi, int N, int ld, double* d_out) 
     });
 }
 
+int ksb_sqload_full(ksb_level* l, const double* d_Phi, int N, int ld, double occ, double* d_out_full) {
+    return guard([&] {
+        need(l && d_Phi && d_out_full, "null argument");
+        if (N < 1 || ld < N) ksb::raise(KSB_INVALID_ARGUMENT, "bad block shape");
+        ksb::sqload_full(l->L, d_Phi, N, ld, occ, d_out_full, l->corr().phys);
+        KSB_CUDA_CHECK(cudaStreamSynchronize(l->L.ctx->stream));
+    });
+}
+
+int ksb_xc_field(ksb_level* l, int xc_kind, double alpha, double p_exch, const double* d_rho, double* d_vxc) {
+    return guard([&] {
+        need(l && d_rho && d_vxc, "null argument");
+        if (xc_kind < 0 || xc_kind > 2) ksb::raise(KSB_INVALID_ARGUMENT, "unknown xc kind");
+        ksb::xc_field(l->L, ksb::XcParams{xc_kind, alpha, p_exch}, d_rho, d_vxc);
+        KSB_CUDA_CHECK(cudaStreamSynchronize(l->L.ctx->stream));
+    });
+}
+
 int ksb_hartree_solve(ksb_level* l, const double* d_Phi, int N, int ld, const double* d_bcb, double tol,
                       double* d_w_full, int* iters) {
     return guard([&] {
@@ -726,6 +788,32 @@ int ksb_outer_solve(ksb_level* l, const ksb_step_opts* o, const double* d_what, 
         ksb::StepLog lg;
         ksb::solve_orbitals(l->L, K, l->owner->cg, step_opts(o), h_lambda, d_Phi, ld, d_PhiT, ld, &lg);
         fill_log(lg, nullptr, att, its);
+    });
+}
+
+int ksb_outer_build(ksb_level* l, int aop_mat, const double* d_what, const double* d_vxc, double* h_min_diag) {
+    return guard([&] {
+        auto& K = ready(l);
+        need(d_what && d_vxc, "null argument");
+        if (aop_mat < 0 || aop_mat >= ksb::kMaxMats) ksb::raise(KSB_INVALID_ARGUMENT, "bad matrix id");
+        const double md = ksb::outer_operator(l->L, K, d_what, d_vxc, aop_mat);
+        if (h_min_diag) *h_min_diag = md;
+    });
+}
+
+int ksb_outer_apply(ksb_level* l, const ksb_step_opts* o, const double* h_lambda, const double* d_Phi, int N, int ld,
+                    double* d_PhiT, int* att, int* its) {
+    return guard([&] {
+        auto& K = ready(l);
+        need(h_lambda && d_Phi && d_PhiT, "null argument");
+        if (N < 1 || N > 128 || ld < N || (N > 1 && (ld & 1))) ksb::raise(KSB_INVALID_ARGUMENT, "bad block shape");
+        if (!l->L.mats[ksb::MAT_H].valid) ksb::raise(KSB_INVALID_ARGUMENT, "call ksb_outer_build first");
+        ksb::StepLog lg;
+        ksb::solve_orbitals(l->L, K, l->owner->cg, step_opts(o), h_lambda, d_Phi, ld, d_PhiT, ld, &lg, N);
+        for (int i = 0; i < N; ++i) {
+            if (att) att[i] = lg.attempts[i];
+            if (its) its[i] = lg.iterations[i];
+        }
     });
 }
 

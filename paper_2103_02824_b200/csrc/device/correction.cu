@@ -154,27 +154,68 @@ void level_ops(Level& L, Corrector& K) {
     K.ops_ready = true;
 }
 
-double outer_operator(Level& L, Corrector& K, const double* d_what_full, const double* d_vxc_full) {
+double min_diagonal(Level& L, int mat, DevBuf<double>& scratch) {
     Ctx& c = *L.ctx;
+    if (!L.mats[mat].valid) raise(KSB_INVALID_ARGUMENT, "operator not assembled");
+    need(scratch, 1);
+    launch(c, "elementwise", k_min_diag, 1, 1024, 0, L.ni, (const int32_t*)L.diag_slot.p,
+           (const double*)L.mats[mat].ii.p, scratch.p);
+    double md = 0.0;
+    KSB_CUDA_CHECK(cudaMemcpyAsync(&md, scratch.p, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    KSB_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    return md;
+}
+
+double outer_operator(Level& L, Corrector& K, const double* d_what_full, const double* d_vxc_full, int aop) {
+    Ctx& c = *L.ctx;
+    if (!L.mats[aop].valid) raise(KSB_INVALID_ARGUMENT, "a_op not assembled");
     need(K.pot, L.n);
     launch(c, "elementwise", k_add, grid_of(c, L.n), kT, 0, int64_t(L.n), d_what_full, 1.0, d_vxc_full, 1.0, K.pot.p);
     assemble_into(L, MAT_TMP, 0.0, 0.0, nullptr, 0.0, K.pot.p, 1.0);
-    axpby_values(L, MAT_H, 1.0, 2, 1.0, MAT_TMP);
-    need(K.diff, L.n);
-    launch(c, "elementwise", k_min_diag, 1, 1024, 0, L.ni, (const int32_t*)L.diag_slot.p,
-           (const double*)L.mats[MAT_H].ii.p, K.diff.p);
-    double md = 0.0;
-    KSB_CUDA_CHECK(cudaMemcpyAsync(&md, K.diff.p, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    axpby_values(L, MAT_H, 1.0, aop, 1.0, MAT_TMP);
+    K.min_diag = min_diagonal(L, MAT_H, K.diff);
+    return K.min_diag;
+}
+
+/// gather the interior entries of a full-length vector
+__global__ void k_take_interior(int ni, const int32_t* __restrict__ interior, const double* __restrict__ full,
+                                double* __restrict__ out) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < ni; r += gridDim.x * blockDim.x) out[r] = full[interior[r]];
+}
+__global__ void k_take_boundary(int nb, const int32_t* __restrict__ boundary, const double* __restrict__ full,
+                                double* __restrict__ out) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nb; r += gridDim.x * blockDim.x) out[r] = full[boundary[r]];
+}
+
+// EllipticSolver::solve / solve_zero_bc (proj/src/solver.cpp:113-135)
+CgColumnStats elliptic_solve(Level& L, CgWork& cg, DevBuf<double>& scratch, int mat, const double* d_b_full,
+                             const double* d_bc_full, const CgOptions& o, double* d_x_full) {
+    Ctx& c = *L.ctx;
+    if (!L.mats[mat].valid) raise(KSB_INVALID_ARGUMENT, "operator not assembled");
+    const int ni = L.ni, nb = L.nb;
+    need(scratch, 2 * int64_t(ni) + std::max(1, nb));
+    double* rhs = scratch.p;
+    double* xi = scratch.p + ni;
+    double* bcb = scratch.p + 2 * int64_t(ni);
+    launch(c, "elementwise", k_take_interior, grid_of(c, ni), kT, 0, ni, (const int32_t*)L.interior.p, d_b_full, rhs);
+    if (d_bc_full) {
+        launch(c, "elementwise", k_take_boundary, grid_of(c, std::max(1, nb)), kT, 0, nb, (const int32_t*)L.boundary.p,
+               d_bc_full, bcb);
+        lift(L, mat, bcb, rhs);
+    }
+    CgColumnStats st;
+    cg_solve(c, L, mat, -1, nullptr, rhs, xi, 1, 1, o, &st, cg);
+    launch(c, "elementwise", k_full_from, grid_of(c, L.n), kT, 0, ni, nb, (const int32_t*)L.interior.p,
+           (const int32_t*)L.boundary.p, (const double*)xi, d_bc_full ? (const double*)bcb : nullptr, d_x_full);
     KSB_CUDA_CHECK(cudaStreamSynchronize(c.stream));
-    K.min_diag = md;
-    return md;
+    return st;
 }
 
 // OuterOperator::solve_orbital for all orbitals at once (proj/src/correction.cpp:26-61)
 void solve_orbitals(Level& L, Corrector& K, CgWork& cg, const StepOptions& o, const double* h_lambda,
-                    const double* d_Phi, int ld, double* d_PhiT, int ldT, StepLog* log) {
+                    const double* d_Phi, int ld, double* d_PhiT, int ldT, StepLog* log, int n_cols) {
     Ctx& c = *L.ctx;
-    const int N = K.sys.N, ni = L.ni;
+    const int N = n_cols > 0 ? n_cols : K.sys.N, ni = L.ni;
     need(K.R0, int64_t(ni) * ld);
     need(K.Bblk, int64_t(ni) * ld);
     spmm(c, L, L.mats[1].ii.p, nullptr, nullptr, d_Phi, N, ld, K.R0.p, ld);  // M phi (orbitals vanish on the boundary)
@@ -200,6 +241,7 @@ void solve_orbitals(Level& L, Corrector& K, CgWork& cg, const StepOptions& o, co
         if (!st[i].converged) fail.push_back(i);
     }
     const double base = std::abs(K.min_diag);
+    double last_rel = 0.0;
     for (int k = 0; k < 4 && !fail.empty(); ++k) {
         const double sigma = k == 0 ? base : std::pow(4.0, k) * (base + 1.0);
         const int nf = int(fail.size());
@@ -221,6 +263,7 @@ void solve_orbitals(Level& L, Corrector& K, CgWork& cg, const StepOptions& o, co
         for (int j = 0; j < nf; ++j) {
             iters[fail[j]] += sst[j].iterations;
             take[j] = sst[j].converged;
+            if (j == 0) last_rel = sst[j].relative_residual;
             if (sst[j].converged)
                 attempt[fail[j]] = k;
             else
@@ -232,7 +275,9 @@ void solve_orbitals(Level& L, Corrector& K, CgWork& cg, const StepOptions& o, co
         KSB_CUDA_CHECK(cudaStreamSynchronize(c.stream));
         fail.swap(still);
     }
-    if (!fail.empty()) raise(KSB_NONCONVERGENCE, "orbital correction solve failed even after the level shift");
+    if (!fail.empty())
+        raise(KSB_NONCONVERGENCE, "orbital correction solve failed even after the level shift (residual " +
+                                      std::to_string(last_rel) + ")");
     if (log) {
         log->attempts = attempt;
         log->iterations = iters;
@@ -253,7 +298,8 @@ int hartree_solve(Level& L, Corrector& K, CgWork& cg, const double* d_PhiT, int 
     co.tol = tol;
     CgColumnStats st;
     cg_solve(c, L, 0, -1, nullptr, K.hrhs.p, K.wtil_int.p, 1, 1, co, &st, cg);
-    if (!st.converged) raise(KSB_NONCONVERGENCE, "hartree solve stalled");
+    if (!st.converged)
+        raise(KSB_NONCONVERGENCE, "hartree solve stalled at residual " + std::to_string(st.relative_residual));
     launch(c, "elementwise", k_full_from, grid_of(c, L.n), kT, 0, L.ni, L.nb, (const int32_t*)L.interior.p,
            (const int32_t*)L.boundary.p, (const double*)K.wtil_int.p, d_bcb, d_w_full);
     return st.iterations;

@@ -59,9 +59,14 @@ void correction_step(Level& L, Corrector& K, CgWork& cg, const StepOptions& o, d
                      double* d_w, StepLog* log);
 
 // pieces (also exported through the C-ABI for parity tests)
-double outer_operator(Level& L, Corrector& K, const double* d_what_full, const double* d_vxc_full);
+double outer_operator(Level& L, Corrector& K, const double* d_what_full, const double* d_vxc_full, int aop = 2);
+/// min over the interior diagonal of A_ii (EllipticSolver::min_diagonal, proj/src/solver.cpp:44)
+double min_diagonal(Level& L, int mat, DevBuf<double>& scratch);
+/// EllipticSolver::solve (proj/src/solver.cpp:113-131); d_bc_full NULL = solve_zero_bc
+CgColumnStats elliptic_solve(Level& L, CgWork& cg, DevBuf<double>& scratch, int mat, const double* d_b_full,
+                             const double* d_bc_full, const CgOptions& o, double* d_x_full);
 void solve_orbitals(Level& L, Corrector& K, CgWork& cg, const StepOptions& o, const double* h_lambda,
-                    const double* d_Phi, int ld, double* d_PhiT, int ldT, StepLog* log);
+                    const double* d_Phi, int ld, double* d_PhiT, int ldT, StepLog* log, int n_cols = 0);
 int hartree_solve(Level& L, Corrector& K, CgWork& cg, const double* d_PhiT, int N, int ldT, const double* d_bcb,
                   double tol, double* d_w_full);
 void expand(Level& L, Corrector& K, const double* d_PhiT, int ldT, const double* d_wt_full, const double* d_bcb,

@@ -55,6 +55,7 @@ struct Level {
     DevBuf<double> pint_val;
     DevBuf<int32_t> ancestor, anc_ptr, anc_tets;
     DevBuf<int32_t> vinc_ptr, vinc;           // interior vertex -> incident (tet*4 + local)
+    DevBuf<int32_t> bvinc_ptr, bvinc;         // boundary vertex -> incident (tet*4 + local)
     DevBuf<int32_t> cinc_ptr, cinc;           // coarse interior dof -> incident (coarse tet*4 + local)
     DevBuf<int32_t> ctets, ciidx;             // coarse mesh (level 0)
     DevBuf<double> cxyz;

@@ -155,6 +155,21 @@ __global__ void k_gather_vinc(int ni, const int32_t* __restrict__ ptr, const int
     }
 }
 
+/// out[rows[r]] = scale * sum of the incident element contributions (full-length scatter)
+__global__ void k_gather_vinc_rows(int nr, const int32_t* __restrict__ ptr, const int32_t* __restrict__ inc,
+                                   const double* __restrict__ E4, double scale, const int32_t* __restrict__ rows,
+                                   double* __restrict__ out) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nr; r += gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int k = ptr[r]; k < ptr[r + 1]; ++k) s += E4[inc[k]];
+        out[rows[r]] = scale * s;
+    }
+}
+
+__global__ void k_xc_field(int n, XcParams xc, const double* __restrict__ rho, double* __restrict__ vxc) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) vxc[v] = xc_potential(xc, rho[v]);
+}
+
 /// y[r] -= sum_k A_ib[r,k] xb[k]
 __global__ void k_lift(int ni, const int32_t* __restrict__ ptr, const int32_t* __restrict__ col,
                        const double* __restrict__ val, const double* __restrict__ xb, double* __restrict__ y) {
@@ -309,6 +324,24 @@ void sqload(Level& L, const double* Phi, int N, int ld, double occ, double scale
            (const double*)L.xyz.p, (const int32_t*)L.iidx.p, Phi, N, ld, occ, w.e4.p);
     launch(c, "sqload", k_gather_vinc, grid_of(c, L.ni), kT, 0, L.ni, (const int32_t*)L.vinc_ptr.p,
            (const int32_t*)L.vinc.p, (const double*)w.e4.p, scale, out_int);
+}
+
+void sqload_full(Level& L, const double* Phi, int N, int ld, double occ, double* out_full, PhysWork& w) {
+    Ctx& c = *L.ctx;
+    ensure_rule(c.stream);
+    w.ensure(L);
+    launch(c, "sqload", k_sqload_elem, grid_of(c, L.nt, 128), 128, 0, L.nt, (const int32_t*)L.tets.p,
+           (const double*)L.xyz.p, (const int32_t*)L.iidx.p, Phi, N, ld, occ, w.e4.p);
+    launch(c, "sqload", k_gather_vinc_rows, grid_of(c, L.ni), kT, 0, L.ni, (const int32_t*)L.vinc_ptr.p,
+           (const int32_t*)L.vinc.p, (const double*)w.e4.p, 1.0, (const int32_t*)L.interior.p, out_full);
+    if (L.nb > 0)
+        launch(c, "sqload", k_gather_vinc_rows, grid_of(c, L.nb), kT, 0, L.nb, (const int32_t*)L.bvinc_ptr.p,
+               (const int32_t*)L.bvinc.p, (const double*)w.e4.p, 1.0, (const int32_t*)L.boundary.p, out_full);
+}
+
+void xc_field(Level& L, const XcParams& xc, const double* rho_full, double* vxc_full) {
+    Ctx& c = *L.ctx;
+    launch(c, "rho_vxc", k_xc_field, grid_of(c, L.n), kT, 0, L.n, xc, rho_full, vxc_full);
 }
 
 void lift(Level& L, int mat, const double* bcb, double* y_int) {

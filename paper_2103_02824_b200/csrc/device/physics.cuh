@@ -28,6 +28,10 @@ Moments moments(Level& L, const double* rho_full, PhysWork& w, const double box_
 void boundary_values(Level& L, const Moments& m, double* bcb);
 /// out_int = scale * (occ sum_i phi_i^2, psi_j) on interior rows
 void sqload(Level& L, const double* Phi, int N, int ld, double occ, double scale, double* out_int, PhysWork& w);
+/// hartree::squared_density_load, all n rows (proj/src/hartree.cpp:108-129)
+void sqload_full(Level& L, const double* Phi, int N, int ld, double occ, double* out_full, PhysWork& w);
+/// model::xc_potential_field (proj/src/ks_model.cpp:101-105)
+void xc_field(Level& L, const XcParams& xc, const double* rho_full, double* vxc_full);
 /// y_int -= A_ib(mat) bcb (Dirichlet lift, reference proj/src/solver.cpp:123)
 void lift(Level& L, int mat, const double* bcb, double* y_int);
 /// squared L2 norm and squared H1 seminorm of a full-length nodal function

@@ -252,6 +252,25 @@ std::shared_ptr<FineTopology> build_topology(const Hierarchy& h, int level) {
             topo->vinc[w++] = t * 4 + li;
         }
     }
+    // boundary vertex incidence, same order rule
+    {
+        const int nb = S.nb();
+        topo->bvinc_ptr.assign(size_t(nb) + 1, 0);
+        for (int r = 0; r < nb; ++r)
+            topo->bvinc_ptr[r + 1] = topo->bvinc_ptr[r] + (vptr[S.boundary[r] + 1] - vptr[S.boundary[r]]);
+        topo->bvinc.resize(topo->bvinc_ptr.back());
+#pragma omp parallel for schedule(static)
+        for (int r = 0; r < nb; ++r) {
+            const int v = S.boundary[r];
+            int32_t w = topo->bvinc_ptr[r];
+            for (int p = vptr[v]; p < vptr[v + 1]; ++p) {
+                const int t = vtet[p];
+                int li = 0;
+                while (m.tets[4 * t + li] != v) ++li;
+                topo->bvinc[w++] = t * 4 + li;
+            }
+        }
+    }
     // coarse interior incidence
     {
         const Mesh& cm = *topo->coarse->mesh;

@@ -69,6 +69,8 @@ struct FineTopology {
     std::vector<int32_t> anc_tets;     // fine tets grouped by coarse ancestor, ascending inside a group
     // interior fine vertex -> incident (tet*4 + local), ascending tet (load-vector gather order)
     std::vector<int32_t> vinc_ptr, vinc;
+    // boundary fine vertex -> incident (tet*4 + local), ascending tet (full-length load vectors)
+    std::vector<int32_t> bvinc_ptr, bvinc;
     // coarse level: interior coarse dof -> incident (coarse tet*4 + local), ascending tet
     std::vector<int32_t> cinc_ptr, cinc;
     // SELL-32 view of the ii pattern: slice s = rows [32s, 32s+32), entry e of lane i at
