@@ -184,6 +184,94 @@ def run_reference(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------------------------- correction step (cfg1)
+CS_LEVEL = 3
+CS_STEPS = 5
+HE = [[2.0, 0.0, 0.0, 0.0]]
+
+
+def correction_cpu(phi_full, w_full, lam0):
+    """Oracle correction step (reference algorithm: SGS-PCG, dense bordered eigensolves) from the same state."""
+    from oracle import OMesh, Oracle
+    orc = Oracle(HE, n_pairs=1, occ=2.0, xc="lda")
+    m = OMesh.box([-BOX] * 3, [BOX] * 3, 8)
+    orc.push(m)
+    for _ in range(CS_LEVEL):
+        m = m.uniform_refine()
+        orc.push(m)
+    t = time.perf_counter()
+    lam, _, _, lg = orc.correction_step(CS_LEVEL, lam0.copy(), phi_full, w_full)
+    return (time.perf_counter() - t) * 1e3, lg["inner_iterations"], float(lam[0])
+
+
+def correction_bench(args, ctx, stream, rank, world):
+    """cfg1 (BASELINE.json configs[0]) finest level: CS_STEPS outer iterations from a synthetic start."""
+    import torch
+
+    import paper_2103_02824_b200 as kb
+    from paper_2103_02824_b200.workloads import cfg1_hierarchy, synthetic_start
+    h = cfg1_hierarchy(CS_LEVEL)
+    L = kb.Level(ctx, h, CS_LEVEL)
+    L.set_system(HE, n_pairs=1, occupancy=2.0, xc="lda")
+    L.level_ops()
+    lam0, Phi, w, ld = synthetic_start(L, ctx, h.meshes[CS_LEVEL], [[0, 0, 0]], 1)
+    phi0, w0 = Phi.download(), w.download()
+
+    def trajectory(timed):
+        Phi.upload(phi0)
+        w.upload(w0)
+        lam = lam0.copy()
+        logs, ms = [], []
+        for _ in range(CS_STEPS):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            logs.append(L.correction_step(lam, Phi, w))
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms.append(e0.elapsed_time(e1))
+        return lam, logs, ms
+
+    trajectory(False)  # warm-up (kernel caches, operator slots, workspaces)
+    ctx.reset_counters()
+    lam, logs, ms = trajectory(True)
+    launches = ctx.launches()
+    # end to end: host orbitals / potential in and out of every step (pinned host buffers)
+    hphi = torch.empty(phi0.shape, dtype=torch.float64, pin_memory=True)
+    hw = torch.empty(w0.shape, dtype=torch.float64, pin_memory=True)
+    hphi.numpy()[:] = phi0
+    hw.numpy()[:] = w0
+    lam_h = lam0.copy()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(CS_STEPS):
+        L.correction_step_host(lam_h, hphi.numpy(), hw.numpy())
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1) / CS_STEPS, world)
+    out = {"workload": f"cfg1 level {CS_LEVEL}: He (Z=2) LDA, 1 doubly occupied orbital, [-10,10]^3, 8^3 Kuhn "
+                       f"coarse + {CS_LEVEL} uniform refinements; synthetic hydrogenic start exp(-1.7 r), lambda -0.6",
+           "n_interior": L.ni, "n_coarse_interior": L.nH, "steps": CS_STEPS,
+           "ms_per_step": max_over_ranks(float(np.mean(ms)), world), "ms_steps": [round(x, 3) for x in ms],
+           "inner_iterations": [lg["inner_iterations"] for lg in logs],
+           "cg_iterations": [lg["cg_iterations"] for lg in logs],
+           "breakdown_ms": {k: round(float(np.mean([lg["ms_" + k] for lg in logs])), 3)
+                            for k in ("bvp", "hartree", "project", "inner")},
+           "lambda_after": float(lam[0]), "gpu_launches": launches,
+           "e2e": {"ms_per_step": e2e_ms, "h2d_bytes_per_step": phi0.nbytes + w0.nbytes,
+                   "d2h_bytes_per_step": phi0.nbytes + w0.nbytes}}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        it = L.index("interior")
+        full = np.zeros((L.n, 1))
+        full[it, 0] = phi0[:, 0]
+        cms, cinner, clam = correction_cpu(full, w0, lam0)
+        out["cpu_baseline"] = {"ms_per_step": cms, "kind": "port", "cores": os.cpu_count() or 1,
+                               "sample": f"oracle correction step 0 from the same start ({cinner} inner sweeps, "
+                                         f"lambda {clam:.10f}; device step 0: {logs[0]['inner_iterations']} sweeps)"}
+    L.close()
+    return out
+
+
 # ----------------------------------------------------------------------------------- GPU leg
 def run_b200(args, world, rank, local):
     import torch
@@ -259,6 +347,8 @@ def run_b200(args, world, rank, local):
     e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
     e2e = world * ni * N_RHS * ITERS / (e2e_ms * 1e-3)
 
+    correction = correction_bench(args, ctx, stream, rank, world)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count() or 1))
@@ -289,6 +379,7 @@ def run_b200(args, world, rank, local):
             "gpu_launches": launches // max(1, args.steps) * args.steps,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
+            "correction_step": correction,
         }
         print(json.dumps(line), flush=True)
     L.close()

@@ -1,0 +1,59 @@
+"""Seeded synthetic inputs for the correction-step benchmark (no datasets exist for this path).
+
+synthetic_start builds a device-resident outer state on a fine level without the coarse SCF: hydrogenic
+orbitals exp(-zeta |x - R|) (zero trace, mass-normalised), an eigenvalue guess, and the Hartree potential of
+their density with multipole Dirichlet data -- the inputs one outer iteration (proj/src/driver.cpp:106-150)
+consumes. Every device quantity is computed by the library's own kernels.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import api
+
+
+def cfg1_hierarchy(levels: int = 3, box: float = 10.0, n_coarse: int = 8) -> api.Hierarchy:
+    """BASELINE.json configs[0]: [-10,10]^3, 8^3 Kuhn coarse mesh, `levels` uniform refinements."""
+    h = api.Hierarchy()
+    m = api.Mesh.box([-box] * 3, [box] * 3, n_coarse)
+    h.push(m)
+    for _ in range(levels):
+        m = m.uniform_refine()
+        h.push(m)
+    return h
+
+
+def synthetic_start(L: api.Level, ctx: api.Context, mesh: api.Mesh, centers, N: int, zeta: float = 1.7,
+                    lam0: float = -0.6, tol: float = 1e-10):
+    """(lambdas, Phi, w) on level L: Phi[:, i] = exp(-zeta r_i) for center i mod len(centers), times a
+    seeded low-order polynomial for i >= len(centers) so the columns are independent; unit L2 norm."""
+    xyz = mesh.array("xyz")
+    it = L.index("interior")
+    x = xyz[it]
+    cen = np.asarray(centers, np.float64).reshape(-1, 3)
+    rng = np.random.default_rng(20210304)
+    ld = N if N == 1 else N + (N & 1)
+    Phi = np.zeros((len(it), ld))
+    for i in range(N):
+        c = cen[i % len(cen)]
+        r = np.linalg.norm(x - c, axis=1)
+        f = np.exp(-zeta * r)
+        if i >= len(cen):
+            f = f * (x - c) @ rng.standard_normal(3)
+        Phi[:, i] = f
+    n = L.n
+    for i in range(N):
+        full = np.zeros(n)
+        full[it] = Phi[:, i]
+        nrm = L.norms(ctx.to_device(full))[0]
+        Phi[:, i] /= np.sqrt(nrm)
+    dPhi = ctx.to_device(np.ascontiguousarray(Phi))
+    rho = ctx.empty((n,))
+    L.density_xc(dPhi, rho, None, N=N, ld=ld)
+    mom = L.moments(rho)
+    bcb = ctx.empty((max(1, L.nb),))
+    L.boundary_values(mom, bcb)
+    w = ctx.empty((n,))
+    L.hartree_solve(dPhi, bcb, w, tol=tol, N=N, ld=ld)
+    lam = np.full(N, lam0, np.float64)
+    return lam, dPhi, w, ld
