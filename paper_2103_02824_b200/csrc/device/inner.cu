@@ -86,6 +86,65 @@ __global__ void k_trsv_many(int n, int nrhs, const double* __restrict__ L, int t
     for (int k = lane; k < n; k += 32) X[j * xs + k * xc] = y[k];
 }
 
+/// Y[v*ldy + r] = alpha * sum_c A[r*lda + c] X[v*ldx + c] for r < n, v < nv (warp per (row, vector)).
+/// The explicit inverse factors (L_H^-1, L_H^-T, C_H^-1, built once per level) turn every triangular
+/// solve of the inner sweep into this fully parallel product.
+__global__ void k_gemv_many(int n, int m, int nv, const double* __restrict__ A, int lda, const double* __restrict__ X,
+                            int64_t ldx, double* __restrict__ Y, int64_t ldy, double alpha) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (warp >= n * nv) return;
+    const int r = warp % n, v = warp / n;
+    const double* a = A + size_t(r) * lda;
+    const double* x = X + size_t(v) * ldx;
+    double t = 0.0;
+    for (int c = lane; c < m; c += 32) t += a[c] * x[c];
+    t = warp_sum(t);
+    if (lane == 0) Y[size_t(v) * ldy + r] = alpha * t;
+}
+
+/// block-wide y = A x (A row-major n x n in global, x and y in shared memory), warp per row
+__device__ void block_gemv(int n, const double* __restrict__ A, const double* x, double* y) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int r = warp; r < n; r += nw) {
+        const double* a = A + size_t(r) * n;
+        double t = 0.0;
+        for (int c = lane; c < n; c += 32) t += a[c] * x[c];
+        t = warp_sum(t);
+        if (lane == 0) y[r] = t;
+    }
+}
+
+/// C = A B^T for n x n row-major A, B (32 x 32 output tiles, k in fixed ascending order)
+__global__ void __launch_bounds__(256) k_gemm_nt(int n, const double* __restrict__ A, const double* __restrict__ B,
+                                                 double* __restrict__ C) {
+    __shared__ double As[32][33], Bs[32][33];
+    const int bi = blockIdx.y * 32, bj = blockIdx.x * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int k0 = 0; k0 < n; k0 += 32) {
+        for (int r = ty; r < 32; r += 8) {
+            As[r][tx] = (bi + r < n && k0 + tx < n) ? A[size_t(bi + r) * n + k0 + tx] : 0.0;
+            Bs[r][tx] = (bj + r < n && k0 + tx < n) ? B[size_t(bj + r) * n + k0 + tx] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int k = 0; k < 32; ++k) {
+            const double b = Bs[tx][k];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[q] = fma(As[ty + 8 * q][k], b, acc[q]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        if (bi + ty + 8 * q < n && bj + tx < n) C[size_t(bi + ty + 8 * q) * n + bj + tx] = acc[q];
+}
+
+__global__ void k_identity(int n, double* __restrict__ I) {
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n * n; idx += gridDim.x * blockDim.x)
+        I[idx] = (idx / n == idx % n) ? 1.0 : 0.0;
+}
+
 /// single-CTA Householder tridiagonalisation of symmetric C (row-major, destroyed).
 /// d[n], e[n-1]; V row k holds the unit Householder vector of step k in entries k+1..n-1.
 __global__ void __launch_bounds__(1024) k_tridiag(int n, double* __restrict__ C, double* __restrict__ d,
@@ -175,11 +234,29 @@ __global__ void __launch_bounds__(1024) k_tridiag(int n, double* __restrict__ C,
 
 constexpr int kTriCluster = 8;
 
-/// Cluster-of-8 Householder tridiagonalisation: each CTA keeps a slab of rows of C in shared
-/// memory (343 x 343 doubles = 941 KB spread over 8 SMs); the Householder vector and p = C v
-/// move between CTAs through distributed shared memory, two cluster barriers per step.
-/// Every CTA recomputes the reflector redundantly (same inputs, same order), so all copies agree.
-__global__ void __cluster_dims__(kTriCluster, 1, 1) __launch_bounds__(512)
+/// register slot r / 32 of a lane-distributed vector (element r lives on lane r % 32), unrolled select
+template <int S>
+__device__ __forceinline__ double reg_at(const double (&x)[S], int r) {
+    double t = 0.0;
+    const int j = r >> 5;
+#pragma unroll
+    for (int s = 0; s < S; ++s) t = (s == j) ? x[s] : t;
+    return __shfl_sync(0xffffffffu, t, r & 31);
+}
+
+constexpr int kTriS = 12;  // register slots per lane: n <= 384
+
+/// Cluster-of-8 Householder tridiagonalisation, one cluster barrier per step.
+/// Each CTA keeps a slab of rows of C in shared memory (343 x 343 doubles = 941 KB over 8 SMs); a row
+/// belongs to one warp for the whole run. Every warp carries the current pivot row, the Householder
+/// vector v and w = p - (v.p) v in registers (element c on lane c % 32) and recomputes the scalars
+/// redundantly, so no CTA-level barrier is needed. Per step: each warp forms its rows' p = C v and pushes
+/// them into every CTA's p buffer, the owner of row k+1 pushes that row (distributed shared memory
+/// stores), one cluster barrier, then every warp builds w, the next pivot row and its rows' rank-2
+/// update. p and the pushed row are double-buffered by step parity, which makes the single barrier safe.
+constexpr int kTriThreads = 256;
+
+__global__ void __cluster_dims__(kTriCluster, 1, 1) __launch_bounds__(kTriThreads, 1)
     k_tridiag_cluster(int n, int R, const double* __restrict__ Cin, double* __restrict__ d, double* __restrict__ e,
                       double* __restrict__ V) {
     namespace cg = cooperative_groups;
@@ -187,107 +264,168 @@ __global__ void __cluster_dims__(kTriCluster, 1, 1) __launch_bounds__(512)
     extern __shared__ double sh[];
     const int q = int(cluster.block_rank());
     const int r0 = q * R, r1 = min(n, r0 + R);
-    double* A = sh;               // R x n, rows r0..r1-1
-    double* v = sh + size_t(R) * n;
-    double* p = v + n;            // own segment of p (indices r0..r1-1 valid)
-    double* pf = p + n;           // full p / q
-    __shared__ double red[32];
-    __shared__ double bc[2];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    double* A = sh;                  // R x n, rows r0..r1-1
+    double* pbuf = sh + size_t(R) * n;   // 2 x n
+    double* rbuf = pbuf + 2 * size_t(n); // 2 x n
+    const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5, nw = blockDim.x >> 5;
     for (int idx = tid; idx < (r1 - r0) * n; idx += blockDim.x) A[idx] = Cin[size_t(r0) * n + idx];
+    double cur[kTriS];
+#pragma unroll
+    for (int s = 0; s < kTriS; ++s) {
+        const int c = lane + 32 * s;
+        cur[s] = c < n ? Cin[c] : 0.0;
+    }
     cluster.sync();
     for (int k = 0; k + 2 < n; ++k) {
-        const int m0 = k + 1, m = n - m0;
-        const int owner = k / R;
-        const double* rowk = cluster.map_shared_rank(A, owner) + size_t(k - owner * R) * n;
-        double s = 0.0;
-        for (int i = tid; i < m; i += blockDim.x) {
-            const double x = rowk[m0 + i];
-            v[m0 + i] = x;
-            s += x * x;
+        const int m0 = k + 1;
+        const int par = k & 1;
+        // reflector from the pivot row (every warp, redundantly)
+        double ss = 0.0;
+#pragma unroll
+        for (int s = 0; s < kTriS; ++s) {
+            const int c = lane + 32 * s;
+            if (c >= m0 && c < n) ss = fma(cur[s], cur[s], ss);
         }
-        s = warp_sum(s);
-        if (lane == 0) red[warp] = s;
-        __syncthreads();
-        if (tid == 0) {
-            double t = 0.0;
-            for (int w = 0; w < nw; ++w) t += red[w];
-            const double nx = sqrt(t);
-            const double x0 = v[m0];
-            const double alpha = x0 >= 0.0 ? -nx : nx;
-            const double nv2 = t - x0 * x0 + (x0 - alpha) * (x0 - alpha);
-            bc[0] = alpha;
-            bc[1] = (nx == 0.0 || nv2 <= 0.0) ? 0.0 : 1.0 / sqrt(nv2);
-            v[m0] = x0 - alpha;
-            if (q == 0) {
-                d[k] = rowk[k];
-                e[k] = bc[1] == 0.0 ? v[m0] + alpha : alpha;
+        ss = warp_sum(ss);
+        const double x0 = reg_at(cur, m0);
+        const double nx = sqrt(ss);
+        const double alpha = x0 >= 0.0 ? -nx : nx;
+        const double nv2 = ss - x0 * x0 + (x0 - alpha) * (x0 - alpha);
+        const double inv = (nx == 0.0 || nv2 <= 0.0) ? 0.0 : 1.0 / sqrt(nv2);
+        double v[kTriS];
+#pragma unroll
+        for (int s = 0; s < kTriS; ++s) {
+            const int c = lane + 32 * s;
+            v[s] = (c >= m0 && c < n) ? (c == m0 ? x0 - alpha : cur[s]) * inv : 0.0;
+        }
+        const double dk = reg_at(cur, k);
+        if (q == 0 && wib == 0) {
+            if (lane == 0) {
+                d[k] = dk;
+                e[k] = inv == 0.0 ? x0 : alpha;
+            }
+#pragma unroll
+            for (int s = 0; s < kTriS; ++s) {
+                const int c = lane + 32 * s;
+                if (c >= m0 && c < n) V[size_t(k) * n + c] = v[s];
             }
         }
-        __syncthreads();
-        const double inv = bc[1];
-        if (inv == 0.0) {
-            if (q == 0)
-                for (int i = tid; i < m; i += blockDim.x) V[size_t(k) * n + m0 + i] = 0.0;
-            cluster.sync();  // keep the two-barrier rhythm identical across CTAs
-            cluster.sync();
-            continue;
-        }
-        for (int i = tid; i < m; i += blockDim.x) {
-            v[m0 + i] *= inv;
-            if (q == 0) V[size_t(k) * n + m0 + i] = v[m0 + i];
-        }
-        __syncthreads();
-        const int ra = max(m0, r0);
-        for (int r = ra + warp; r < r1; r += nw) {
+        // p = C v for the own rows, pushed to every CTA; the owner pushes row k+1 as it stands
+        double* pb = pbuf + size_t(par) * n;
+        for (int r = max(m0, r0) + ((wib - (max(m0, r0) - r0) % nw + nw) % nw); r < r1; r += nw) {
             const double* row = A + size_t(r - r0) * n;
             double t = 0.0;
-            for (int c = m0 + lane; c < n; c += 32) t += row[c] * v[c];
+#pragma unroll
+            for (int s = 0; s < kTriS; ++s) {
+                const int c = lane + 32 * s;
+                if (c < n) t = fma(row[c], v[s], t);
+            }
             t = warp_sum(t);
-            if (lane == 0) p[r] = t;
+            if (lane < kTriCluster) cluster.map_shared_rank(pbuf, lane)[size_t(par) * n + r] = t;
         }
-        cluster.sync();  // every CTA's p segment is complete
-        s = 0.0;
-        for (int i = m0 + tid; i < n; i += blockDim.x) {
-            const double pi = cluster.map_shared_rank(p, i / R)[i];
-            pf[i] = pi;
-            s += v[i] * pi;
+        const int k1 = k + 1;
+        if (k1 >= r0 && k1 < r1) {  // the whole owner CTA pushes row k+1 (its warp updated it last step)
+            __syncthreads();
+            const double* row = A + size_t(k1 - r0) * n;
+            for (int idx = tid; idx < kTriCluster * n; idx += blockDim.x) {
+                const int t = idx / n, c = idx - t * n;
+                cluster.map_shared_rank(rbuf, t)[size_t(par) * n + c] = row[c];
+            }
         }
-        s = warp_sum(s);
-        if (lane == 0) red[warp] = s;
-        __syncthreads();
-        if (tid == 0) {
-            double t = 0.0;
-            for (int w = 0; w < nw; ++w) t += red[w];
-            bc[0] = t;
+        cluster.sync();
+        (void)pb;
+        // w = p - (v.p) v
+        const double* pf = pbuf + size_t(par) * n;
+        double kk = 0.0;
+        double w[kTriS];
+#pragma unroll
+        for (int s = 0; s < kTriS; ++s) {
+            const int c = lane + 32 * s;
+            w[s] = (c >= m0 && c < n) ? pf[c] : 0.0;
+            kk = fma(v[s], w[s], kk);
         }
-        __syncthreads();
-        const double K = bc[0];
-        for (int i = m0 + tid; i < n; i += blockDim.x) pf[i] -= K * v[i];
-        __syncthreads();
-        const int nr = r1 - ra;
-        for (int idx = tid; idx < nr * m; idx += blockDim.x) {
-            const int rr = ra + idx / m, c = m0 + idx % m;
-            A[size_t(rr - r0) * n + c] -= 2.0 * (v[rr] * pf[c] + pf[rr] * v[c]);
+        kk = warp_sum(kk);
+#pragma unroll
+        for (int s = 0; s < kTriS; ++s) w[s] = fma(-kk, v[s], w[s]);
+        // next pivot row: row k+1 - 2 (v_{k+1} w + w_{k+1} v)
+        const double vk1 = reg_at(v, k1), wk1 = reg_at(w, k1);
+        const double* rk1 = rbuf + size_t(par) * n;
+#pragma unroll
+        for (int s = 0; s < kTriS; ++s) {
+            const int c = lane + 32 * s;
+            cur[s] = c < n ? rk1[c] - 2.0 * (vk1 * w[s] + wk1 * v[s]) : 0.0;
         }
-        cluster.sync();  // updated rows visible before the next step reads row k+1 remotely
+        // rank-2 update of the own rows
+        for (int r = max(m0, r0) + ((wib - (max(m0, r0) - r0) % nw + nw) % nw); r < r1; r += nw) {
+            double* row = A + size_t(r - r0) * n;
+            const double vr = 2.0 * reg_at(v, r), wr = 2.0 * reg_at(w, r);
+#pragma unroll
+            for (int s = 0; s < kTriS; ++s) {
+                const int c = lane + 32 * s;
+                if (c >= m0 && c < n) row[c] -= vr * w[s] + wr * v[s];
+            }
+        }
     }
-    if (q == 0 && tid == 0) {
-        auto at = [&](int r, int c) { return cluster.map_shared_rank(A, r / R)[size_t(r % R) * n + c]; };
-        if (n >= 2) {
-            d[n - 2] = at(n - 2, n - 2);
-            e[n - 2] = at(n - 1, n - 2);
+    // tail: rows n-2 and n-1 of the final matrix (row n-1 was updated by its own warp)
+    __syncthreads();
+    if (n >= 2 && q == 0 && wib == 0) {
+        const double dn2 = reg_at(cur, n - 2), en2 = reg_at(cur, n - 1);
+        if (lane == 0) {
+            d[n - 2] = dn2;
+            e[n - 2] = en2;
         }
-        if (n >= 1) d[n - 1] = at(n - 1, n - 1);
     }
-    cluster.sync();  // keep remote shared memory alive until rank 0 has read it
+    if (n >= 1 && n - 1 >= r0 && n - 1 < r1 && tid == 0) d[n - 1] = A[size_t(n - 1 - r0) * n + n - 1];
+    if (n == 1 && q == 0 && tid == 0) d[0] = Cin[0];
+    cluster.sync();  // keep remote shared memory alive until every push has landed
 }
 
-/// apply Q^T (forward = 1: H_0 first) or Q (forward = 0: H_{n-3} first) to vectors, warp per vector.
-/// vector j element k at X[j*xs + k].
+/// apply Q^T (forward = 1: H_0 first) or Q (forward = 0: H_{n-3} first) to one vector, one warp.
+/// For n <= 32 kQR the vector lives in registers (element i on lane i % 32, slot i / 32) and the next
+/// reflector's row is prefetched while the current one is applied, so the 341-step chain pays the
+/// shuffle-reduction latency only, not an L2 round trip per step.
+constexpr int kQR = 12;
+
 __device__ void apply_q_warp(int n, const double* __restrict__ V, double* x, int forward) {
     const int lane = threadIdx.x & 31;
     const int steps = n - 2;
+    if (steps <= 0) return;
+    if (n <= 32 * kQR) {
+        double xr[kQR], cur[kQR], nxt[kQR];
+#pragma unroll
+        for (int r = 0; r < kQR; ++r) {
+            const int i = lane + 32 * r;
+            xr[r] = i < n ? x[i] : 0.0;
+        }
+        auto load = [&](int k, double (&dst)[kQR]) {
+            const double* vk = V + size_t(k) * n;
+#pragma unroll
+            for (int r = 0; r < kQR; ++r) {
+                const int i = lane + 32 * r;
+                dst[r] = (i > k && i < n) ? __ldg(vk + i) : 0.0;
+            }
+        };
+        load(forward ? 0 : steps - 1, cur);
+        for (int s = 0; s < steps; ++s) {
+            if (s + 1 < steps) load(forward ? s + 1 : steps - 2 - s, nxt);
+            double t = 0.0;
+#pragma unroll
+            for (int r = 0; r < kQR; ++r) t = fma(cur[r], xr[r], t);
+            t = 2.0 * warp_sum(t);
+#pragma unroll
+            for (int r = 0; r < kQR; ++r) xr[r] = fma(-t, cur[r], xr[r]);
+#pragma unroll
+            for (int r = 0; r < kQR; ++r) cur[r] = nxt[r];
+        }
+        __syncwarp();
+#pragma unroll
+        for (int r = 0; r < kQR; ++r) {
+            const int i = lane + 32 * r;
+            if (i < n) x[i] = xr[r];
+        }
+        __syncwarp();
+        return;
+    }
     for (int s = 0; s < steps; ++s) {
         const int k = forward ? s : steps - 1 - s;
         const double* vk = V + size_t(k) * n;
@@ -479,7 +617,7 @@ __global__ void k_schur(int nh, const double* __restrict__ dHh, const double* __
 // per sweep, per orbital: border, C12, C22, rotated vectors
 
 struct SweepDev {
-    const double *AH, *A3, *A_h4, *orb_vecs, *orb_scal, *LH, *V, *l, *u, *s, *wH, *theta1;
+    const double *AH, *A3, *A_h4, *orb_vecs, *orb_scal, *LHi, *LHiT, *V, *l, *u, *s, *wH, *theta1;
     double *c12, *c22, *lhat, *work;
     int nh, N, hartree;
 };
@@ -523,47 +661,43 @@ __global__ void k_orbital_border(SweepDev S) {
     const double ut = block_dot(u, t, nh);
     const double si = S.s[i];
     if (threadIdx.x == 0) S.c22[i] = (beta - 2.0 * ub + ut) / (si * si);
-    // c12 = L^-1 (b - t) / s (warp 0), l^ = Q^T l (warp 1) after c12
+    // c12 = Q^T L^-1 (b - t) / s, l^ = Q^T l
     double* c12 = S.c12 + size_t(i) * nh;
     double* lh = S.lhat + size_t(i) * nh;
+    double* x = sh + 2 * nh;
+    for (int a = threadIdx.x; a < nh; a += blockDim.x) t[a] = (b[a] - t[a]) / si;
+    __syncthreads();
+    block_gemv(nh, S.LHi, t, x);
+    __syncthreads();
     if (warp == 0) {
-        for (int a = lane; a < nh; a += 32) t[a] = (b[a] - t[a]) / si;
-        __syncwarp();
-        for (int r = 0; r < nh; ++r) {
-            double x = 0.0;
-            for (int k = lane; k < r; k += 32) x += S.LH[size_t(r) * nh + k] * t[k];
-            x = warp_sum(x);
-            if (lane == 0) t[r] = (t[r] - x) / S.LH[size_t(r) * nh + r];
-            __syncwarp();
-        }
-        apply_q_warp(nh, S.V, t, 1);
-        for (int a = lane; a < nh; a += 32) c12[a] = t[a];
-    } else if (warp == 1) {
-        double* x = sh + 2 * nh;  // private scratch: warp 0 still reads b
-        for (int a = lane; a < nh; a += 32) x[a] = S.l[size_t(i) * nh + a];
-        __syncwarp();
         apply_q_warp(nh, S.V, x, 1);
-        for (int a = lane; a < nh; a += 32) lh[a] = x[a];
+        for (int a = lane; a < nh; a += 32) c12[a] = x[a];
+    } else if (warp == 1) {
+        for (int a = lane; a < nh; a += 32) b[a] = S.l[size_t(i) * nh + a];  // b is free now
+        __syncwarp();
+        apply_q_warp(nh, S.V, b, 1);
+        for (int a = lane; a < nh; a += 32) lh[a] = b[a];
     }
 }
 
 /// inertia of [T - x, c; c^T, c22 - x]: number of eigenvalues < x (Sylvester)
 __device__ __forceinline__ int arrow_count(int n, const double* __restrict__ d, const double* __restrict__ e,
                                            const double* __restrict__ c, double c22, double x, double pivmin) {
+    // one reciprocal per step on the dependency chain (it also serves the border term)
     int cnt = 0;
-    double q = 0.0, z = 0.0, acc = 0.0;
+    double rq = 0.0, z = 0.0, acc = 0.0;
     for (int j = 0; j < n; ++j) {
         double dj = d[j] - x;
         double zj = c[j];
         if (j > 0) {
-            const double l = e[j - 1] / q;
+            const double l = e[j - 1] * rq;
             dj -= l * e[j - 1];
             zj -= l * z;
         }
         if (fabs(dj) < pivmin) dj = -pivmin;
         cnt += dj < 0.0;
-        acc += zj * zj / dj;
-        q = dj;
+        rq = 1.0 / dj;
+        acc += zj * zj * rq;
         z = zj;
     }
     const double s = (c22 - x) - acc;
@@ -571,12 +705,25 @@ __device__ __forceinline__ int arrow_count(int n, const double* __restrict__ d, 
 }
 
 /// warp per (orbital, k): k-th smallest eigenvalue by 32-way multisection
-__global__ void k_arrow_eig(int nh, int N, int nev, const double* __restrict__ d, const double* __restrict__ e,
+__global__ void k_arrow_eig(int nh, int N, int nev, const double* __restrict__ dg, const double* __restrict__ eg,
                             const double* __restrict__ c12, const double* __restrict__ c22, double* __restrict__ lam) {
-    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-    if (warp >= N * nev) return;
-    const int i = warp / nev, k = warp % nev;
-    const double* c = c12 + size_t(i) * nh;
+    // T and the border in shared memory: the Sturm recurrence re-reads them on every multisection step
+    extern __shared__ double she[];
+    double* d = she;
+    double* e = she + nh;
+    const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double* c = she + 2 * nh + size_t(wib) * nh;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    for (int j = threadIdx.x; j < nh; j += blockDim.x) {
+        d[j] = dg[j];
+        e[j] = eg[j];
+    }
+    const bool live = warp < N * nev;
+    const int i = live ? warp / nev : 0, k = live ? warp % nev : 0;
+    if (live)
+        for (int j = lane; j < nh; j += 32) c[j] = c12[size_t(i) * nh + j];
+    __syncthreads();
+    if (!live) return;
     const double cc = c22[i];
     // Gershgorin bounds
     double lo = DBL_MAX, hi = -DBL_MAX, csum = 0.0;
@@ -628,14 +775,19 @@ __global__ void k_arrow_vec(int nh, int N, int nev, const double* __restrict__ d
     const int i = warp / nev;
     const double x = lam[warp];
     const double* c = c12 + size_t(i) * nh;
-    double* y = Y + size_t(warp) * nh;
-    double* z = Z + size_t(warp) * nh;
-    double* pv = piv + size_t(warp) * nh;
+    // per-warp scratch in shared memory: the recurrences below read what they just wrote
+    extern __shared__ double shv[];
+    double* mul = shv + size_t(threadIdx.x >> 5) * 4 * nh;
+    double* y = mul + nh;
+    double* z = y + nh;
+    double* pv = z + nh;
+    (void)Z;
+    (void)piv;
     if (lane == 0 && nh > 0) {
         double tn = 0.0;
         for (int j = 0; j < nh; ++j) tn = fmax(tn, fabs(d[j]) + (j > 0 ? fabs(e[j - 1]) : 0.0) + (j + 1 < nh ? fabs(e[j]) : 0.0));
         const double pivmin = DBL_EPSILON * fmax(tn, 1e-300);
-        // LDL^T of T - x
+        // LDL^T of T - x; pv <- 1 / pivot, z scratch <- multipliers e_j / pivot_j (the solves are then FMA chains)
         double q = 1.0;
         for (int j = 0; j < nh; ++j) {
             double dj = d[j] - x;
@@ -644,13 +796,19 @@ __global__ void k_arrow_vec(int nh, int N, int nev, const double* __restrict__ d
             pv[j] = dj;
             q = dj;
         }
-        auto solve = [&](double* v) {  // v <- (T - x)^-1 v
-            for (int j = 1; j < nh; ++j) v[j] -= (e[j - 1] / pv[j - 1]) * v[j - 1];
-            v[nh - 1] /= pv[nh - 1];
-            for (int j = nh - 2; j >= 0; --j) v[j] = v[j] / pv[j] - (e[j] / pv[j]) * v[j + 1];
+        double* lm = mul;
+        for (int j = 0; j < nh; ++j) {
+            const double r = 1.0 / pv[j];
+            lm[j] = j + 1 < nh ? e[j] * r : 0.0;
+            pv[j] = r;
+        }
+        auto solve = [&](double* vv, const double* mlt) {  // vv <- (T - x)^-1 vv
+            for (int j = 1; j < nh; ++j) vv[j] -= mlt[j - 1] * vv[j - 1];
+            vv[nh - 1] *= pv[nh - 1];
+            for (int j = nh - 2; j >= 0; --j) vv[j] = vv[j] * pv[j] - mlt[j] * vv[j + 1];
         };
         for (int j = 0; j < nh; ++j) z[j] = c[j];
-        solve(z);
+        solve(z, mul);
         double cz = 0.0;
         for (int j = 0; j < nh; ++j) cz += c[j] * z[j];
         double sch = (c22[i] - x) - cz;
@@ -660,7 +818,7 @@ __global__ void k_arrow_vec(int nh, int N, int nev, const double* __restrict__ d
         for (int j = 0; j < nh; ++j) y[j] = 1.0 + 0.5 * double((j * 7919) % 97) / 97.0;
         for (int rep = 0; rep < 2; ++rep) {
             const double rl = yl;
-            solve(y);
+            solve(y, mul);
             double cu = 0.0;
             for (int j = 0; j < nh; ++j) cu += c[j] * y[j];
             yl = (rl - cu) / sch;
@@ -675,6 +833,9 @@ __global__ void k_arrow_vec(int nh, int N, int nev, const double* __restrict__ d
         }
         ylast[warp] = yl;
     }
+    __syncwarp();
+    double* yg = Y + size_t(warp) * nh;
+    for (int j = lane; j < nh; j += 32) yg[j] = y[j];
     __syncwarp();
     const double* lh = lhat + size_t(i) * nh;
     double ov = 0.0;
@@ -724,16 +885,10 @@ __global__ void k_select(SweepDev S, int nev, const double* __restrict__ lam, co
     const double theta = th;
     for (int a = threadIdx.x; a < nh; a += blockDim.x) x[a] = x[a] / nrm - S.l[size_t(i) * nh + a] * theta;
     __syncthreads();
-    if (threadIdx.x < 32) {  // phi_H = L_H^-T x
-        const int lane = threadIdx.x;
-        for (int r = nh - 1; r >= 0; --r) {
-            double t = 0.0;
-            for (int k = r + 1 + lane; k < nh; k += 32) t += S.LH[size_t(k) * nh + r] * x[k];
-            t = warp_sum(t);
-            if (lane == 0) x[r] = (x[r] - t) / S.LH[size_t(r) * nh + r];
-            __syncwarp();
-        }
-    }
+    double* y = sh + nh;  // phi_H = L_H^-T x
+    block_gemv(nh, S.LHiT, x, y);
+    __syncthreads();
+    for (int a = threadIdx.x; a < nh; a += blockDim.x) x[a] = y[a];
     __syncthreads();
     // ip = phi_new^T M_H phi_old + th_new c.phi_old + th_old c.phi_new + th_new th_old gamma
     const double* po = phi_old + size_t(i) * nh;
@@ -759,7 +914,7 @@ __global__ void k_select(SweepDev S, int nev, const double* __restrict__ lam, co
 
 /// one block: f_H, g, Hartree bordered solve, theta1, w_H, and the H1 state change delta
 struct HartreeDev {
-    const double *sq, *A_h4, *A3, *orb_vecs, *orb_scal, *shared_vecs, *shared_scal, *LC, *hu, *schur, *CH, *MH;
+    const double *sq, *A_h4, *A3, *orb_vecs, *orb_scal, *shared_vecs, *shared_scal, *CHi, *hu, *schur, *CH, *MH;
     const double *phi_new, *th2_new, *phi_old, *th2_old;
     double *wH_new, *theta1_new, *delta, *f;
     int nh, N, hartree;
@@ -806,23 +961,10 @@ __global__ void k_hartree_delta(HartreeDev H) {
         for (int a = threadIdx.x; a < nh; a += blockDim.x) f[a] = four_pi * (H.occ * f[a]) - H.shared_vecs[nh + a];
         g = four_pi * (H.occ * g) - H.shared_scal[1];
         __syncthreads();
-        // t = C_H^-1 f (L_C L_C^T)
-        if (warp == 0) {
-            for (int r = 0; r < nh; ++r) {
-                double t = 0.0;
-                for (int k = lane; k < r; k += 32) t += H.LC[size_t(r) * nh + k] * f[k];
-                t = warp_sum(t);
-                if (lane == 0) f[r] = (f[r] - t) / H.LC[size_t(r) * nh + r];
-                __syncwarp();
-            }
-            for (int r = nh - 1; r >= 0; --r) {
-                double t = 0.0;
-                for (int k = r + 1 + lane; k < nh; k += 32) t += H.LC[size_t(k) * nh + r] * f[k];
-                t = warp_sum(t);
-                if (lane == 0) f[r] = (f[r] - t) / H.LC[size_t(r) * nh + r];
-                __syncwarp();
-            }
-        }
+        // t = C_H^-1 f
+        block_gemv(nh, H.CHi, f, dp);
+        __syncthreads();
+        for (int a = threadIdx.x; a < nh; a += blockDim.x) f[a] = dp[a];
         __syncthreads();
         const double dt = block_dot(H.shared_vecs, f, nh);
         const double th1 = (g - dt) / H.schur[0];
@@ -974,6 +1116,29 @@ void coarse_level_setup(Level& L, CoarseOps& co) {
         launch(c, "coarse", k_potrf, 1, 1024, 0, nh, co.LC.p, flag.p);
     }
     if (check_flag(c, flag)) raise(KSB_INTERNAL, "coarse mass or stiffness factorization failed");
+    // explicit inverse factors, once per level: columns of L^-1 e_j by triangular solves
+    co.LHi.alloc(nh2);
+    co.LHiT.alloc(nh2);
+    co.CHi.alloc(nh2);
+    if (nh > 0) {
+        DevBuf<double> I, Y;
+        I.alloc(nh2);
+        Y.alloc(nh2);
+        launch(c, "coarse", k_identity, ceil_div(int64_t(nh) * nh, 256), 256, 0, nh, I.p);
+        const size_t sm = sizeof(double) * nh * 4;
+        // L_H^-1 (row-major: x_j = L^-1 e_j is column j) and L_H^-T (row-major: x_j is row j)
+        launch(c, "coarse", k_trsv_many, ceil_div(nh, 4), 128, sm, nh, nh, (const double*)co.LH.p, 0,
+               (const double*)I.p, int64_t(nh), int64_t(1), co.LHi.p, int64_t(1), int64_t(nh), 1.0);
+        launch(c, "coarse", k_trsv_many, ceil_div(nh, 4), 128, sm, nh, nh, (const double*)co.LH.p, 0,
+               (const double*)I.p, int64_t(nh), int64_t(1), co.LHiT.p, int64_t(nh), int64_t(1), 1.0);
+        // C_H^-1 = L_C^-T L_C^-1 (symmetric; column j = row j)
+        launch(c, "coarse", k_trsv_many, ceil_div(nh, 4), 128, sm, nh, nh, (const double*)co.LC.p, 0,
+               (const double*)I.p, int64_t(nh), int64_t(1), Y.p, int64_t(nh), int64_t(1), 1.0);
+        launch(c, "coarse", k_trsv_many, ceil_div(nh, 4), 128, sm, nh, nh, (const double*)co.LC.p, 1,
+               (const double*)Y.p, int64_t(nh), int64_t(1), co.CHi.p, int64_t(nh), int64_t(1), 1.0);
+        launch(c, "coarse", k_symmetrize, ceil_div(int64_t(nh) * nh, 256), 256, 0, nh, co.CHi.p);
+        KSB_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    }
     co.ready = true;
 }
 
@@ -993,18 +1158,17 @@ InnerStats inner_scf(Level& L, const CoarseOps& co, const ProjOut& P, const Inne
     const double* A4 = P.shared_mats.p + 2 * int64_t(nh) * nh;
     // per outer: l_i = L_H^-1 c_i, s_i, u_i = L_H^-T l_i
     const size_t smem_trsv = sizeof(double) * nh * 4;
-    launch(c, "inner:trsv_many", k_trsv_many, ceil_div(N, 4), 128, smem_trsv, nh, N, (const double*)co.LH.p, 0,
-           (const double*)(P.orb_vecs.p + 3 * nh), int64_t(6) * nh, int64_t(1), w.l.p, int64_t(nh), int64_t(1), 1.0);
+    (void)smem_trsv;
+    auto gemv = [&](const double* A, const double* X, int64_t ldx, double* Y, int64_t ldy, int nv) {
+        launch(c, "inner:gemv", k_gemv_many, ceil_div(nh * nv, 8), 256, 0, nh, nh, nv, A, nh, X, ldx, Y, ldy, 1.0);
+    };
+    gemv(co.LHi.p, P.orb_vecs.p + 3 * nh, int64_t(6) * nh, w.l.p, int64_t(nh), N);
     launch(c, "inner:border_scale", k_border_scale, N, 128, 0, nh, N, (const double*)w.l.p, (const double*)P.orb_scal.p, w.s.p,
            w.flag.p);
-    launch(c, "inner:trsv_many", k_trsv_many, ceil_div(N, 4), 128, smem_trsv, nh, N, (const double*)co.LH.p, 1,
-           (const double*)w.l.p, int64_t(nh), int64_t(1), w.u.p, int64_t(nh), int64_t(1), 1.0);
+    gemv(co.LHiT.p, w.l.p, int64_t(nh), w.u.p, int64_t(nh), N);
     if (check_flag(c, w.flag)) raise(KSB_AMBIGUOUS_SELECTION, "bordered mass matrix is not positive definite");
     if (prm.hartree) {
-        launch(c, "inner:trsv_many", k_trsv_many, 1, 32, sizeof(double) * nh, nh, 1, (const double*)co.LC.p, 0,
-               (const double*)P.shared_vecs.p, int64_t(nh), int64_t(1), w.hu.p, int64_t(nh), int64_t(1), 1.0);
-        launch(c, "inner:trsv_many", k_trsv_many, 1, 32, sizeof(double) * nh, nh, 1, (const double*)co.LC.p, 1,
-               (const double*)w.hu.p, int64_t(nh), int64_t(1), w.hu.p, int64_t(nh), int64_t(1), 1.0);
+        gemv(co.CHi.p, P.shared_vecs.p, int64_t(nh), w.hu.p, int64_t(nh), 1);
         launch(c, "inner:schur", k_schur, 1, 128, 0, nh, (const double*)P.shared_vecs.p, (const double*)w.hu.p,
                (const double*)P.shared_scal.p, w.scal.p, w.flag.p);
         if (check_flag(c, w.flag))
@@ -1023,11 +1187,14 @@ InnerStats inner_scf(Level& L, const CoarseOps& co, const ProjOut& P, const Inne
     }
     const size_t tri_smem = sizeof(double) * 2 * nh;
     const int cl_R = (nh + kTriCluster - 1) / kTriCluster;
-    const size_t cl_smem = sizeof(double) * (size_t(cl_R) * nh + 3 * size_t(nh));
-    if (cl_smem <= size_t(200) * 1024) {
+    const size_t cl_smem = sizeof(double) * (size_t(cl_R) * nh + 4 * size_t(nh));
+    const bool use_cluster = cl_smem <= size_t(200) * 1024 && nh <= 32 * kTriS;
+    if (use_cluster) {
         static bool attr = false;
         if (!attr) {
             KSB_CUDA_CHECK(cudaFuncSetAttribute(k_tridiag_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                int(200 * 1024)));
+            KSB_CUDA_CHECK(cudaFuncSetAttribute(k_arrow_vec, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 int(200 * 1024)));
             attr = true;
         }
@@ -1042,24 +1209,25 @@ InnerStats inner_scf(Level& L, const CoarseOps& co, const ProjOut& P, const Inne
         launch(c, "inner:build_", k_build_AH, nh, 128, sizeof(double) * nh, nh, (const int32_t*)L.cinc_ptr.p,
                (const int32_t*)L.cinc.p, (const int32_t*)L.ctets.p, (const int32_t*)L.ciidx.p, A1, A3, A4,
                (const double*)w.E16.p, prm.hartree ? 1 : 0, (const double*)w.th1[cur].p, w.AH.p);
-        // C11 = L^-1 A_H L^-T: W^T = L^-1 A_H (rows of A_H are its columns), then C = L^-1 W
-        launch(c, "inner:trsv_many", k_trsv_many, ceil_div(nh, 4), 128, smem_trsv, nh, nh, (const double*)co.LH.p, 0,
-               (const double*)w.AH.p, int64_t(nh), int64_t(1), w.W.p, int64_t(1), int64_t(nh), 1.0);
-        launch(c, "inner:trsv_many", k_trsv_many, ceil_div(nh, 4), 128, smem_trsv, nh, nh, (const double*)co.LH.p, 0,
-               (const double*)w.W.p, int64_t(nh), int64_t(1), w.C.p, int64_t(1), int64_t(nh), 1.0);
+        // C11 = L^-1 A_H L^-T as two products (A_H symmetric: L^-1 A_H = L^-1 A_H^T)
+        const dim3 gt(ceil_div(nh, 32), ceil_div(nh, 32));
+        launch(c, "inner:gemm", k_gemm_nt, gt, 256, 0, nh, (const double*)co.LHi.p, (const double*)w.AH.p, w.W.p);
+        launch(c, "inner:gemm", k_gemm_nt, gt, 256, 0, nh, (const double*)w.W.p, (const double*)co.LHi.p, w.C.p);
         launch(c, "inner:symmetrize", k_symmetrize, ceil_div(int64_t(nh) * nh, 256), 256, 0, nh, w.C.p);
-        if (cl_smem <= size_t(200) * 1024)
-            launch(c, "inner_tridiag", k_tridiag_cluster, kTriCluster, 512, cl_smem, nh, cl_R, (const double*)w.C.p,
+        if (use_cluster)
+            launch(c, "inner_tridiag", k_tridiag_cluster, kTriCluster, kTriThreads, cl_smem, nh, cl_R, (const double*)w.C.p,
                    w.d.p, w.e.p, w.V.p);
         else
             launch(c, "inner_tridiag", k_tridiag, 1, 1024, tri_smem, nh, w.C.p, w.d.p, w.e.p, w.V.p);
-        SweepDev S{w.AH.p, A3, P.A_h4.p, P.orb_vecs.p, P.orb_scal.p, co.LH.p, w.V.p, w.l.p, w.u.p, w.s.p,
+        SweepDev S{w.AH.p, A3, P.A_h4.p, P.orb_vecs.p, P.orb_scal.p, co.LHi.p, co.LHiT.p, w.V.p, w.l.p, w.u.p, w.s.p,
                    w.wH[cur].p, w.th1[cur].p, w.c12.p, w.c22.p, w.lhat.p, nullptr, nh, N, prm.hartree ? 1 : 0};
         launch(c, "inner:orbital_border", k_orbital_border, N, 256, sizeof(double) * 3 * nh, S);
         const int warps = N * nev;
-        launch(c, "inner:arrow_eig", k_arrow_eig, ceil_div(warps, 4), 128, 0, nh, N, nev, (const double*)w.d.p,
+        launch(c, "inner:arrow_eig", k_arrow_eig, ceil_div(warps, 4), 128, sizeof(double) * 6 * nh, nh, N, nev,
+               (const double*)w.d.p,
                (const double*)w.e.p, (const double*)w.c12.p, (const double*)w.c22.p, w.lam.p);
-        launch(c, "inner:arrow_vec", k_arrow_vec, ceil_div(warps, 4), 128, 0, nh, N, nev, (const double*)w.d.p,
+        launch(c, "inner:arrow_vec", k_arrow_vec, ceil_div(warps, 4), 128, sizeof(double) * 4 * 4 * nh, nh, N, nev,
+               (const double*)w.d.p,
                (const double*)w.e.p, (const double*)w.c12.p, (const double*)w.c22.p, (const double*)w.lhat.p,
                (const double*)w.s.p, (const double*)P.orb_scal.p, (const double*)w.lam.p, w.Y.p, w.Z.p, w.piv.p,
                w.score.p, w.ynorm.p);
@@ -1073,7 +1241,7 @@ InnerStats inner_scf(Level& L, const CoarseOps& co, const ProjOut& P, const Inne
         if (prm.hartree)
             launch(c, "inner:coarse_vec_asm", k_coarse_vec_asm, dim3(ceil_div(nh, 128), N), 128, 0, nh, nct,
                    (const int32_t*)L.cinc_ptr.p, (const int32_t*)L.cinc.p, (const double*)w.E4.p, w.sq.p);
-        HartreeDev H{w.sq.p, P.A_h4.p, A3, P.orb_vecs.p, P.orb_scal.p, P.shared_vecs.p, P.shared_scal.p, co.LC.p,
+        HartreeDev H{w.sq.p, P.A_h4.p, A3, P.orb_vecs.p, P.orb_scal.p, P.shared_vecs.p, P.shared_scal.p, co.CHi.p,
                      w.hu.p, w.scal.p, co.CH.p, co.MH.p, w.phi[nx].p, w.th2[nx].p, w.phi[cur].p, w.th2[cur].p,
                      w.wH[nx].p, w.th1[nx].p, w.scal.p + 1, nullptr, nh, N, prm.hartree ? 1 : 0, prm.occ};
         if (!prm.hartree) {

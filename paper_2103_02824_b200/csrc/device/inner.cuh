@@ -7,9 +7,10 @@
 
 namespace ksb {
 
-/// per-level coarse operators: M_H, C_H (interior blocks, dense row-major) and their Cholesky factors
+/// per-level coarse operators: M_H, C_H (interior blocks, dense row-major), their Cholesky factors and the
+/// explicit inverse factors L_H^-1, L_H^-T (row-major) and C_H^-1 used by the sweep's products
 struct CoarseOps {
-    DevBuf<double> MH, CH, LH, LC;
+    DevBuf<double> MH, CH, LH, LC, LHi, LHiT, CHi;
     bool ready = false;
 };
 void coarse_level_setup(Level& L, CoarseOps& co);

@@ -14,6 +14,7 @@ __global__ void __launch_bounds__(256) k_spmm(int ni, const int32_t* __restrict_
     const int lane = threadIdx.x & 31;
     const int g = lane / G, l = lane % G;
     const int gbase = g * G;
+    (void)gbase;
     const int rows_per_warp = 32 / G;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -45,6 +46,7 @@ __global__ void __launch_bounds__(256) k_spmv(int ni, const int32_t* __restrict_
     const int lane = threadIdx.x & 31;
     const int g = lane / G, l = lane % G;
     const int gbase = g * G;
+    (void)gbase;
     const int rows_per_warp = 32 / G;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;

@@ -31,3 +31,25 @@ for s in range(steps):
                       "cg": lg["cg_iterations"], "att": lg["attempts"]}), flush=True)
     if lg["delta"] < 1e-6:
         break
+
+# per-kernel breakdown of one more step
+NAMES = ["spmm", "cg_update_r", "cg_update_px", "cg_trueres", "cg_setup", "inner_tridiag", "inner:gemm", "inner:gemv",
+         "inner:orbital_border", "inner:arrow_eig", "inner:arrow_vec", "inner:select", "inner:hartree_delta",
+         "inner:coarse_wmass", "inner:build_", "inner:symmetrize", "inner:coarse_sq", "inner:coarse_vec_asm",
+         "inner:border_scale", "inner:schur", "project", "project_asm", "assemble", "axpby", "sqload", "rho_vxc",
+         "moments", "elementwise", "lift", "norm", "reduce", "expand"]
+ctx.reset_counters()
+ctx.set_profiling(True)
+try:
+    lg = L.correction_step(lam, Phi, w)
+    print("profiled step: inner", lg["inner_iterations"], "ms_total", round(lg["ms_total"], 3))
+except kb.KsbError as e:
+    print("profiled step failed", e)
+ctx.set_profiling(False)
+rows = []
+for n in NAMES:
+    ms, cnt = ctx.kernel_time(n)
+    if cnt:
+        rows.append((ms, n, cnt))
+for ms, n, cnt in sorted(rows, reverse=True):
+    print(f"  {n:24s} {ms:9.3f} ms  {cnt:5d} launches  {1e3 * ms / cnt:8.1f} us/launch")
