@@ -247,14 +247,17 @@ __device__ __forceinline__ double reg_at(const double (&x)[S], int r) {
 constexpr int kTriS = 12;  // register slots per lane: n <= 384
 
 /// Cluster-of-8 Householder tridiagonalisation, one cluster barrier per step.
-/// Each CTA keeps a slab of rows of C in shared memory (343 x 343 doubles = 941 KB over 8 SMs); a row
-/// belongs to one warp for the whole run. Every warp carries the current pivot row, the Householder
-/// vector v and w = p - (v.p) v in registers (element c on lane c % 32) and recomputes the scalars
-/// redundantly, so no CTA-level barrier is needed. Per step: each warp forms its rows' p = C v and pushes
-/// them into every CTA's p buffer, the owner of row k+1 pushes that row (distributed shared memory
-/// stores), one cluster barrier, then every warp builds w, the next pivot row and its rows' rank-2
-/// update. p and the pushed row are double-buffered by step parity, which makes the single barrier safe.
+/// Rows are dealt cyclically: CTA q keeps rows q, q+8, q+16, ... of C in shared memory (343 x 343 doubles =
+/// 941 KB over 8 SMs) and slot i of a CTA belongs to warp i % 8, so the active trailing rows stay balanced
+/// over all 64 warps as the reduction proceeds. Every warp carries the pivot row, the Householder vector v
+/// and w = p - (v.p) v in registers (element c on lane c % 32) and recomputes the scalars redundantly.
+/// Per step the only exchange is p = C v: each warp pushes its rows' entries into every CTA's p buffer
+/// (distributed shared memory stores), then one cluster barrier. The pivot rows travel in blocks of
+/// kTriRep: every kTriRep steps their owners push the next block into a replica in every CTA, and each CTA
+/// applies the per-step rank-2 updates to its replica locally, so the next pivot row is always local.
+/// p and the replica are double-buffered, which makes the single barrier safe.
 constexpr int kTriThreads = 256;
+constexpr int kTriRep = kTriThreads / 32;  // one replica row per warp
 
 __global__ void __cluster_dims__(kTriCluster, 1, 1) __launch_bounds__(kTriThreads, 1)
     k_tridiag_cluster(int n, int R, const double* __restrict__ Cin, double* __restrict__ d, double* __restrict__ e,
@@ -262,13 +265,17 @@ __global__ void __cluster_dims__(kTriCluster, 1, 1) __launch_bounds__(kTriThread
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
     extern __shared__ double sh[];
+    constexpr int P = kTriCluster;
     const int q = int(cluster.block_rank());
-    const int r0 = q * R, r1 = min(n, r0 + R);
-    double* A = sh;                  // R x n, rows r0..r1-1
-    double* pbuf = sh + size_t(R) * n;   // 2 x n
-    double* rbuf = pbuf + 2 * size_t(n); // 2 x n
+    const int nslot = (n - q + P - 1) / P;     // rows q + P i < n
+    double* A = sh;                            // R x n, slot i = row q + P i
+    double* pbuf = sh + size_t(R) * n;         // 2 x n
+    double* rep = pbuf + 2 * size_t(n);        // 2 x kTriRep x n
     const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5, nw = blockDim.x >> 5;
-    for (int idx = tid; idx < (r1 - r0) * n; idx += blockDim.x) A[idx] = Cin[size_t(r0) * n + idx];
+    for (int idx = tid; idx < nslot * n; idx += blockDim.x) {
+        const int i = idx / n, c = idx - i * n;
+        A[idx] = Cin[size_t(q + P * i) * n + c];
+    }
     double cur[kTriS];
 #pragma unroll
     for (int s = 0; s < kTriS; ++s) {
@@ -279,12 +286,16 @@ __global__ void __cluster_dims__(kTriCluster, 1, 1) __launch_bounds__(kTriThread
     for (int k = 0; k + 2 < n; ++k) {
         const int m0 = k + 1;
         const int par = k & 1;
+        const int blk = k / kTriRep;
+        const int rb0 = 1 + blk * kTriRep;  // first pivot row of the replica block in use this step
+        double* repb = rep + size_t(blk & 1) * kTriRep * n;
+        const int s0 = m0 >> 5;  // register slots below s0 hold only finished columns
         // reflector from the pivot row (every warp, redundantly)
         double ss = 0.0;
 #pragma unroll
         for (int s = 0; s < kTriS; ++s) {
             const int c = lane + 32 * s;
-            if (c >= m0 && c < n) ss = fma(cur[s], cur[s], ss);
+            if (s >= s0 && c >= m0 && c < n) ss = fma(cur[s], cur[s], ss);
         }
         ss = warp_sum(ss);
         const double x0 = reg_at(cur, m0);
@@ -307,33 +318,38 @@ __global__ void __cluster_dims__(kTriCluster, 1, 1) __launch_bounds__(kTriThread
 #pragma unroll
             for (int s = 0; s < kTriS; ++s) {
                 const int c = lane + 32 * s;
-                if (c >= m0 && c < n) V[size_t(k) * n + c] = v[s];
+                if (s >= s0 && c >= m0 && c < n) V[size_t(k) * n + c] = v[s];
             }
         }
-        // p = C v for the own rows, pushed to every CTA; the owner pushes row k+1 as it stands
-        double* pb = pbuf + size_t(par) * n;
-        for (int r = max(m0, r0) + ((wib - (max(m0, r0) - r0) % nw + nw) % nw); r < r1; r += nw) {
-            const double* row = A + size_t(r - r0) * n;
+        // every kTriRep steps: the owners push the next block of pivot rows (updated through step k-1)
+        if (k % kTriRep == 0) {
+            __syncthreads();  // the rows' own warps finished last step's update
+            const int hi = min(rb0 + kTriRep, n - 1);
+            for (int rr = rb0; rr < hi; ++rr) {
+                if (rr % P != q) continue;
+                const double* src = A + size_t(rr / P) * n;
+                for (int idx = tid; idx < P * n; idx += blockDim.x) {
+                    const int t = idx / n, c = idx - t * n;
+                    cluster.map_shared_rank(repb, t)[size_t(rr - rb0) * n + c] = src[c];
+                }
+            }
+        }
+        // first own slot at or past row m0, then every nw-th slot belongs to this warp
+        const int i0 = m0 > q ? (m0 - q + P - 1) / P : 0;
+        const int ifirst = i0 + ((wib - i0 % nw) % nw + nw) % nw;
+        // p = C v for the own rows, pushed to every CTA
+        for (int i = ifirst; i < nslot; i += nw) {
+            const double* row = A + size_t(i) * n;
             double t = 0.0;
 #pragma unroll
             for (int s = 0; s < kTriS; ++s) {
                 const int c = lane + 32 * s;
-                if (c < n) t = fma(row[c], v[s], t);
+                if (s >= s0 && c < n) t = fma(row[c], v[s], t);
             }
             t = warp_sum(t);
-            if (lane < kTriCluster) cluster.map_shared_rank(pbuf, lane)[size_t(par) * n + r] = t;
-        }
-        const int k1 = k + 1;
-        if (k1 >= r0 && k1 < r1) {  // the whole owner CTA pushes row k+1 (its warp updated it last step)
-            __syncthreads();
-            const double* row = A + size_t(k1 - r0) * n;
-            for (int idx = tid; idx < kTriCluster * n; idx += blockDim.x) {
-                const int t = idx / n, c = idx - t * n;
-                cluster.map_shared_rank(rbuf, t)[size_t(par) * n + c] = row[c];
-            }
+            if (lane < P) cluster.map_shared_rank(pbuf, lane)[size_t(par) * n + q + P * i] = t;
         }
         cluster.sync();
-        (void)pb;
         // w = p - (v.p) v
         const double* pf = pbuf + size_t(par) * n;
         double kk = 0.0;
@@ -341,29 +357,42 @@ __global__ void __cluster_dims__(kTriCluster, 1, 1) __launch_bounds__(kTriThread
 #pragma unroll
         for (int s = 0; s < kTriS; ++s) {
             const int c = lane + 32 * s;
-            w[s] = (c >= m0 && c < n) ? pf[c] : 0.0;
+            w[s] = (s >= s0 && c >= m0 && c < n) ? pf[c] : 0.0;
             kk = fma(v[s], w[s], kk);
         }
         kk = warp_sum(kk);
 #pragma unroll
         for (int s = 0; s < kTriS; ++s) w[s] = fma(-kk, v[s], w[s]);
-        // next pivot row: row k+1 - 2 (v_{k+1} w + w_{k+1} v)
-        const double vk1 = reg_at(v, k1), wk1 = reg_at(w, k1);
-        const double* rk1 = rbuf + size_t(par) * n;
+        // replica rows still ahead take this step's update (warp j owns replica row j)
+        {
+            const int rr = rb0 + wib;
+            const double vr = 2.0 * reg_at(v, rr), wr = 2.0 * reg_at(w, rr);
+            if (rr >= m0 && rr < n - 1) {
+                double* row = repb + size_t(wib) * n;
 #pragma unroll
-        for (int s = 0; s < kTriS; ++s) {
-            const int c = lane + 32 * s;
-            cur[s] = c < n ? rk1[c] - 2.0 * (vk1 * w[s] + wk1 * v[s]) : 0.0;
+                for (int s = 0; s < kTriS; ++s) {
+                    const int c = lane + 32 * s;
+                    if (s >= s0 && c >= m0 && c < n) row[c] -= vr * w[s] + wr * v[s];
+                }
+            }
         }
-        // rank-2 update of the own rows
-        for (int r = max(m0, r0) + ((wib - (max(m0, r0) - r0) % nw + nw) % nw); r < r1; r += nw) {
-            double* row = A + size_t(r - r0) * n;
+        // rank-2 update of the own slab rows
+        for (int i = ifirst; i < nslot; i += nw) {
+            double* row = A + size_t(i) * n;
+            const int r = q + P * i;
             const double vr = 2.0 * reg_at(v, r), wr = 2.0 * reg_at(w, r);
 #pragma unroll
             for (int s = 0; s < kTriS; ++s) {
                 const int c = lane + 32 * s;
-                if (c >= m0 && c < n) row[c] -= vr * w[s] + wr * v[s];
+                if (s >= s0 && c >= m0 && c < n) row[c] -= vr * w[s] + wr * v[s];
             }
+        }
+        __syncthreads();  // replica row k+1 complete
+        const double* nxt = repb + size_t(m0 - rb0) * n;
+#pragma unroll
+        for (int s = 0; s < kTriS; ++s) {
+            const int c = lane + 32 * s;
+            cur[s] = c < n ? nxt[c] : 0.0;
         }
     }
     // tail: rows n-2 and n-1 of the final matrix (row n-1 was updated by its own warp)
@@ -375,7 +404,7 @@ __global__ void __cluster_dims__(kTriCluster, 1, 1) __launch_bounds__(kTriThread
             e[n - 2] = en2;
         }
     }
-    if (n >= 1 && n - 1 >= r0 && n - 1 < r1 && tid == 0) d[n - 1] = A[size_t(n - 1 - r0) * n + n - 1];
+    if (n >= 1 && (n - 1) % P == q && tid == 0) d[n - 1] = A[size_t((n - 1) / P) * n + n - 1];
     if (n == 1 && q == 0 && tid == 0) d[0] = Cin[0];
     cluster.sync();  // keep remote shared memory alive until every push has landed
 }
@@ -1187,7 +1216,7 @@ InnerStats inner_scf(Level& L, const CoarseOps& co, const ProjOut& P, const Inne
     }
     const size_t tri_smem = sizeof(double) * 2 * nh;
     const int cl_R = (nh + kTriCluster - 1) / kTriCluster;
-    const size_t cl_smem = sizeof(double) * (size_t(cl_R) * nh + 4 * size_t(nh));
+    const size_t cl_smem = sizeof(double) * (size_t(cl_R) * nh + (2 + 2 * kTriRep) * size_t(nh));
     const bool use_cluster = cl_smem <= size_t(200) * 1024 && nh <= 32 * kTriS;
     if (use_cluster) {
         static bool attr = false;
