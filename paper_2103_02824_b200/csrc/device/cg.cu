@@ -77,14 +77,39 @@ __device__ bool last_block(int* ticket) {
     return am_last;
 }
 
-/// Deterministic fold of part[b*N + c] over b for every column into out[c] (one warp per column).
+/// Deterministic fold of part[b*N + c] over b for every column into out[c]. Loads are batched (8
+/// independent accumulators per lane) so the fold costs one or two L2 round trips, not nblocks/32; for
+/// N < 8 the columns are split over several warps each. The order is fixed by (nblocks, N, blockDim).
 __device__ void fold_partials(const double* part, int nblocks, int N, double* out_smem) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    for (int c = warp; c < N; c += nw) {
-        double s = 0.0;
-        for (int b = lane; b < nblocks; b += 32) s += __ldcg(part + size_t(b) * N + c);
+    __shared__ double fold_red[32];
+    const int per = N >= nw ? 1 : nw / N;  // warps per column
+    for (int c0 = 0; c0 < N; c0 += nw / per) {
+        const int c = c0 + warp / per, sl = warp % per;
+        double a[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        if (c < N && warp / per < nw / per) {
+            const int stride = per * 32;
+            int b = sl * 32 + lane;
+            for (; b + 7 * stride < nblocks; b += 8 * stride) {
+#pragma unroll
+                for (int u = 0; u < 8; ++u) a[u] += __ldcg(part + size_t(b + u * stride) * N + c);
+            }
+            for (; b < nblocks; b += stride) a[0] += __ldcg(part + size_t(b) * N + c);
+        }
+        double s = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
         s = warp_sum(s);
-        if (lane == 0) out_smem[c] = s;
+        if (per == 1) {
+            if (lane == 0 && c < N) out_smem[c] = s;
+        } else {
+            if (lane == 0) fold_red[warp] = s;
+            __syncthreads();
+            if (threadIdx.x < nw / per && c0 + int(threadIdx.x) < N) {
+                double t = 0.0;
+                for (int k = 0; k < per; ++k) t += fold_red[threadIdx.x * per + k];
+                out_smem[c0 + threadIdx.x] = t;
+            }
+            __syncthreads();
+        }
     }
     __syncthreads();
 }
@@ -102,10 +127,71 @@ struct ElemMap {
     }
 };
 
-/// block reduction of per-thread column partials (ElemMap layout) -> part[blockIdx*N + c]
-__device__ void block_cols(double v, int N, double* part, double* smem) {
-    const int rb = max(1, int(blockDim.x) / N);
-    if (threadIdx.x < rb * N) smem[threadIdx.x] = v;
+template <int V>
+__device__ __forceinline__ void ldv(const double* __restrict__ p, double (&v)[V]) {
+    if constexpr (V == 2) {
+        const double2 a = *reinterpret_cast<const double2*>(p);
+        v[0] = a.x;
+        v[1] = a.y;
+    } else {
+        v[0] = *p;
+    }
+}
+template <int V>
+__device__ __forceinline__ void stv(double* __restrict__ p, const double (&v)[V]) {
+    if constexpr (V == 2)
+        *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
+    else
+        *p = v[0];
+}
+
+/// Elementwise layout with V adjacent columns per thread (V = 2 needs N and ld even).
+template <int V>
+struct EMap {
+    int c, r0, rstep, valid;
+    __device__ EMap(int N) {
+        const int np = N / V;
+        const int rb = max(1, int(blockDim.x) / np);
+        c = (threadIdx.x % np) * V;
+        const int rl = threadIdx.x / np;
+        valid = rl < rb;
+        r0 = blockIdx.x * rb + rl;
+        rstep = gridDim.x * rb;
+    }
+};
+
+/// block reduction of per-thread column partials (EMap<V> layout) -> part[blockIdx*N + c]. When the
+/// number of column groups np divides 32 the lanes of one column are combined by shuffles first (a
+/// fixed xor tree), so the final per-column sum runs over the 8 warps instead of 256 / np rows.
+template <int V>
+__device__ void block_cols_v(const double (&v)[V], int N, double* part, double* smem) {
+    const int np = N / V;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (np <= 32 && (32 % np) == 0 && (int(blockDim.x) % np) == 0) {
+        double x[V];
+#pragma unroll
+        for (int q = 0; q < V; ++q) {
+            x[q] = v[q];
+            for (int o = 16; o >= np; o >>= 1) x[q] += __shfl_xor_sync(0xffffffffu, x[q], o);
+        }
+        if (lane < np) {
+#pragma unroll
+            for (int q = 0; q < V; ++q) smem[warp * N + lane * V + q] = x[q];
+        }
+        __syncthreads();
+        if (threadIdx.x < N) {
+            double s = 0.0;
+            for (int k = 0; k < nw; ++k) s += smem[k * N + threadIdx.x];
+            part[size_t(blockIdx.x) * N + threadIdx.x] = s;
+        }
+        __syncthreads();
+        return;
+    }
+    const int rb = max(1, int(blockDim.x) / np);
+    if (threadIdx.x < rb * np) {
+#pragma unroll
+        for (int q = 0; q < V; ++q) smem[(threadIdx.x / np) * N + (threadIdx.x % np) * V + q] = v[q];
+    }
     __syncthreads();
     if (threadIdx.x < N) {
         double s = 0.0;
@@ -133,8 +219,11 @@ __global__ void __launch_bounds__(kThreads) k_init(int ni, Cols cc, const double
             bb += b * b;
             rz += b * z;
         }
-    block_cols(bb, N, s.part0, sm);
-    block_cols(rz, N, s.part1, sm);
+    {
+        const double b1[1] = {bb}, z1[1] = {rz};
+        block_cols_v<1>(b1, N, s.part0, sm);
+        block_cols_v<1>(z1, N, s.part1, sm);
+    }
     if (!last_block(s.ctl + kTicket0)) return;
     fold_partials(s.part0, gridDim.x, N, sm);
     fold_partials(s.part1, gridDim.x, N, sm + N);
@@ -270,16 +359,21 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_dot(int ni, Cols cc, co
             }
         }
     }
-    // block reduce: groups with equal l hold the same columns
-    const int ngroups = blockDim.x / G;
+    // block reduce: groups with equal l hold the same columns -- xor tree over the groups of a warp,
+    // then a fixed-order sum over the warps
     const int width = G * CPL;
-    const int gid = threadIdx.x / G;
+    const int nwb = blockDim.x >> 5, wib = threadIdx.x >> 5;
 #pragma unroll
-    for (int q = 0; q < CPL; ++q) sm[gid * width + (FULL ? full_col<G>(l, q) : l * CPL + q)] = pd[q];
+    for (int q = 0; q < CPL; ++q)
+        for (int o = 16; o >= G; o >>= 1) pd[q] += __shfl_xor_sync(0xffffffffu, pd[q], o);
+    if (lane < G) {
+#pragma unroll
+        for (int q = 0; q < CPL; ++q) sm[wib * width + (FULL ? full_col<G>(l, q) : l * CPL + q)] = pd[q];
+    }
     __syncthreads();
     if (threadIdx.x < N) {
         double t = 0.0;
-        for (int k = 0; k < ngroups; ++k) t += sm[k * width + threadIdx.x];
+        for (int k = 0; k < nwb; ++k) t += sm[k * width + threadIdx.x];
         s.part0[size_t(blockIdx.x) * N + threadIdx.x] = t;
     }
     k1_epilogue(sm, N, cc, s);
@@ -384,57 +478,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_sell_dot(int ni, int nslices, C
 }
 
 // ---------------- K2: r update (x is deferred to K4, which reads p anyway) ----------------
-template <int V>
-__device__ __forceinline__ void ldv(const double* __restrict__ p, double (&v)[V]) {
-    if constexpr (V == 2) {
-        const double2 a = *reinterpret_cast<const double2*>(p);
-        v[0] = a.x;
-        v[1] = a.y;
-    } else {
-        v[0] = *p;
-    }
-}
-template <int V>
-__device__ __forceinline__ void stv(double* __restrict__ p, const double (&v)[V]) {
-    if constexpr (V == 2)
-        *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
-    else
-        *p = v[0];
-}
-
-/// Elementwise layout with V adjacent columns per thread (V = 2 needs N and ld even).
-template <int V>
-struct EMap {
-    int c, r0, rstep, valid;
-    __device__ EMap(int N) {
-        const int np = N / V;
-        const int rb = max(1, int(blockDim.x) / np);
-        c = (threadIdx.x % np) * V;
-        const int rl = threadIdx.x / np;
-        valid = rl < rb;
-        r0 = blockIdx.x * rb + rl;
-        rstep = gridDim.x * rb;
-    }
-};
-
-/// block reduction of per-thread column partials (EMap<V> layout) -> part[blockIdx*N + c]
-template <int V>
-__device__ void block_cols_v(const double (&v)[V], int N, double* part, double* smem) {
-    const int np = N / V;
-    const int rb = max(1, int(blockDim.x) / np);
-    if (threadIdx.x < rb * np) {
-#pragma unroll
-        for (int q = 0; q < V; ++q) smem[(threadIdx.x / np) * N + (threadIdx.x % np) * V + q] = v[q];
-    }
-    __syncthreads();
-    if (threadIdx.x < N) {
-        double s = 0.0;
-        for (int k = 0; k < rb; ++k) s += smem[k * N + threadIdx.x];
-        part[size_t(blockIdx.x) * N + threadIdx.x] = s;
-    }
-    __syncthreads();
-}
-
 template <int V>
 __global__ void __launch_bounds__(kThreads, 4) k_update_r(int ni, Cols cc, double* __restrict__ R,
                                                        const double* __restrict__ AP, CgDev s) {
