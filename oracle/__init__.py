@@ -10,4 +10,5 @@ CLI11 are absent) and ships no golden vectors, so this
 oracle is pinned by restated versions of the reference's own known-answer and
 identity tests (tests/test_oracle_pins.py) -- not by reference outputs.
 """
-from .binding import OBlocks, OMesh, OOperator, Oracle, OracleError, gen_eig, keast, lib, solve_bordered  # noqa: F401
+from .binding import (OBlocks, OMesh, OOperator, Oracle, OracleError, dorfler_mark, gen_eig, keast, lib,  # noqa: F401
+                      solve_bordered)

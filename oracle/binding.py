@@ -60,6 +60,8 @@ _PROTO = {
     "orc_sqload": (I, [P, I, DP, I, DP]),
     "orc_hartree_exact": (I, [P, I, DP, I, DP, D, DP, IP]),
     "orc_energy": (I, [P, I, DP, I, DP, DP]),
+    "orc_indicators": (I, [P, I, DP, DP, I, DP, DP, DP, DP]),
+    "orc_dorfler": (I, [DP, I64, D, D, IP, C.POINTER(C.c_int64)]),
     "orc_norms": (I, [P, I, DP, DP]),
     "orc_prolong_vec": (I, [P, I, I, DP, I, DP]),
     "orc_coarse_scf": (I, [P, D, I, D, D, DP, DP, DP, IP]),
@@ -274,6 +276,17 @@ class Oracle:
         _chk(lib.orc_energy(self._h, level, dp(orb), orb.shape[1], dp(f64(w)), dp(out)))
         return out
 
+    def indicators(self, level, lambdas, orb, w, vxc):
+        """est::compute_indicators (proj/src/estimator.cpp:11-85): (eta_sq per tet, total)"""
+        orb = f64(orb)
+        if orb.ndim == 1:
+            orb = orb[:, None]
+        eta = np.empty(self.meshes[level].sizes()[1])
+        tot = C.c_double()
+        _chk(lib.orc_indicators(self._h, level, dp(f64(lambdas)), dp(orb), orb.shape[1], dp(f64(w)), dp(f64(vxc)),
+                                dp(eta), C.byref(tot)))
+        return eta, tot.value
+
     def norms(self, level, f):
         out = np.empty(3)
         _chk(lib.orc_norms(self._h, level, dp(f64(f)), dp(out)))
@@ -457,6 +470,15 @@ class OBlocks:
         _chk(lib.orc_blocks_f_g(self._h, dp(f64(phi_H)), dp(f64(theta2)), dp(f64(w_H)), theta1, dp(f), C.byref(g),
                                 dp(A2)))
         return f, g.value, (A2.reshape(self.nh, self.nh, order="F") if want_A2 else None)
+
+
+def dorfler_mark(eta, total, theta):
+    """est::dorfler_mark (proj/src/estimator.cpp:87-104)"""
+    eta = f64(eta)
+    out = np.empty(len(eta), np.int32)
+    n = C.c_int64()
+    _chk(lib.orc_dorfler(dp(eta), len(eta), float(total), float(theta), ip(out), C.byref(n)))
+    return out[:n.value].copy()
 
 
 def keast():

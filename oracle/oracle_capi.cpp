@@ -411,6 +411,22 @@ int orc_energy(orc_problem* p, int level, const double* orb, int N, const double
         out[4] = e.total;
     });
 }
+int orc_indicators(orc_problem* p, int level, const double* lambdas, const double* orb, int N, const double* w,
+                   const double* vxc, double* eta, double* total_sq) {
+    return guard([&] {
+        const Space& V = p->p.space(level);
+        const Vec e = compute_indicators(p->p.sys, V, Vec(lambdas, lambdas + N), unpack(orb, V.n(), N),
+                                         Vec(w, w + V.n()), Vec(vxc, vxc + V.n()), total_sq);
+        std::copy(e.begin(), e.end(), eta);
+    });
+}
+int orc_dorfler(const double* eta, int64_t nt, double total_sq, double theta, int32_t* marked, int64_t* n_marked) {
+    return guard([&] {
+        const auto mk = dorfler_mark(Vec(eta, eta + nt), total_sq, theta);
+        for (size_t i = 0; i < mk.size(); ++i) marked[i] = mk[i];
+        *n_marked = int64_t(mk.size());
+    });
+}
 int orc_norms(orc_problem* p, int level, const double* f, double* out) {
     return guard([&] {
         const Space& V = p->p.space(level);

@@ -898,6 +898,114 @@ Energy total_energy(const System& s, const Space& V, const std::vector<Vec>& orb
     return e;
 }
 
+// =========================================================== estimator (proj/src/estimator.cpp)
+// compute_indicators: estimator.cpp:11-85 (element residual per tet, then face jumps in face order)
+Vec compute_indicators(const System& s, const Space& V, const Vec& lambdas, const std::vector<Vec>& orb,
+                       const Vec& w, const Vec& vxc, double* total_sq) {
+    const Mesh& m = *V.mesh;
+    const int nt = m.nt(), N = int(orb.size());
+    const auto& rule = keast();
+    Vec eta(nt, 0.0);
+#pragma omp parallel for schedule(static)
+    for (int t = 0; t < nt; ++t) {
+        const auto& v = m.tets[t];
+        const double vol = std::abs(m.tet_volume(t));
+        double acc = 0.0;
+        for (const auto& q : rule) {
+            V3 x{{0, 0, 0}};
+            double wq = 0.0, vq = 0.0;
+            for (int k = 0; k < 4; ++k) {
+                for (int d = 0; d < 3; ++d) x[d] += q.b[k] * m.verts[v[k]][d];
+                wq += q.b[k] * w[v[k]];
+                vq += q.b[k] * vxc[v[k]];
+            }
+            const double pot = v_ext(s, x) + wq + vq;
+            double sum_sq = 0.0;
+            for (int i = 0; i < N; ++i) {
+                double phi = 0.0;
+                for (int k = 0; k < 4; ++k) phi += q.b[k] * orb[i][v[k]];
+                const double r = (pot - lambdas[i]) * phi;
+                sum_sq += r * r;
+            }
+            acc += q.w * vol * sum_sq;
+        }
+        double hT = 0.0;
+        for (int i = 0; i < 4; ++i)
+            for (int j = i + 1; j < 4; ++j) {
+                double d2 = 0.0;
+                for (int d = 0; d < 3; ++d) {
+                    const double a = m.verts[v[i]][d] - m.verts[v[j]][d];
+                    d2 += a * a;
+                }
+                hT = std::max(hT, std::sqrt(d2));
+            }
+        eta[t] += hT * hT * acc;
+    }
+    m.quad_cells += (unsigned long long)nt;
+    // face geometry as TetMesh::finalize (mesh.cpp:196-211) and P1 gradients (mesh.cpp:164-173)
+    auto grad = [&](int t, const Vec& f, double g[3]) {
+        const Geo G = tet_geo(m, t);
+        for (int d = 0; d < 3; ++d) g[d] = 0.0;
+        for (int k = 0; k < 4; ++k)
+            for (int d = 0; d < 3; ++d) g[d] += f[m.tets[t][k]] * G.g[k][d];
+    };
+    for (size_t fi = 0; fi < m.ifaces.size(); ++fi) {
+        const auto& key = m.ifaces[fi];
+        const int tp = m.iface_tets[fi][0], tm = m.iface_tets[fi][1];
+        const V3 &a = m.verts[key[0]], &b = m.verts[key[1]], &c = m.verts[key[2]];
+        const V3 ba = sub(b, a), ca = sub(c, a), cb = sub(c, b);
+        V3 nrm = cross(ba, ca);
+        const double len = std::sqrt(dot3(nrm, nrm));
+        const double area = 0.5 * len;
+        for (int d = 0; d < 3; ++d) nrm[d] /= len;
+        const double diam = std::max({std::sqrt(dot3(ba, ba)), std::sqrt(dot3(ca, ca)), std::sqrt(dot3(cb, cb))});
+        V3 cp{{0, 0, 0}};
+        for (int i = 0; i < 4; ++i)
+            for (int d = 0; d < 3; ++d) cp[d] += m.verts[m.tets[tp][i]][d];
+        for (int d = 0; d < 3; ++d) cp[d] /= 4.0;
+        double sgn = 0.0;
+        for (int d = 0; d < 3; ++d) sgn += nrm[d] * ((a[d] + b[d] + c[d]) / 3.0 - cp[d]);
+        if (sgn < 0)
+            for (int d = 0; d < 3; ++d) nrm[d] = -nrm[d];
+        double jump_sq = 0.0;
+        for (int i = 0; i < N; ++i) {
+            double gp[3], gm[3];
+            grad(tp, orb[i], gp);
+            grad(tm, orb[i], gm);
+            double jn = 0.0;
+            for (int d = 0; d < 3; ++d) jn += 0.5 * (gp[d] - gm[d]) * nrm[d];
+            jump_sq += jn * jn;
+        }
+        const double contrib = diam * jump_sq * area;
+        eta[tp] += contrib;
+        eta[tm] += contrib;
+    }
+    double tot = 0.0;
+    for (double x : eta) tot += x;
+    if (total_sq) *total_sq = tot;
+    return eta;
+}
+
+// dorfler_mark: estimator.cpp:87-104 (descending eta, lower index first on ties, stop at theta * total)
+std::vector<int> dorfler_mark(const Vec& eta, double total_sq, double theta) {
+    if (!(theta > 0.0) || theta >= 1.0) fail(E_ARG, "theta must lie in (0,1)");
+    if (total_sq <= 0.0) return {};
+    std::vector<int> order(eta.size());
+    for (size_t i = 0; i < order.size(); ++i) order[i] = int(i);
+    std::sort(order.begin(), order.end(), [&](int a, int b) {
+        if (eta[a] != eta[b]) return eta[a] > eta[b];
+        return a < b;
+    });
+    std::vector<int> marked;
+    double acc = 0.0;
+    for (int t : order) {
+        marked.push_back(t);
+        acc += eta[t];
+        if (acc >= theta * total_sq) break;
+    }
+    return marked;
+}
+
 // =========================================================== hartree (proj/src/hartree.cpp)
 Moments compute_moments(const Space& V, const Vec& rho) {
     const Mesh& m = *V.mesh;

@@ -168,6 +168,13 @@ struct Energy {
     double kinetic = 0, external = 0, hartree = 0, xc = 0, total = 0;
 };
 Energy total_energy(const System& s, const Space& V, const std::vector<Vec>& orb, const Vec& w);
+// ------------------------------------------------------------------ estimator (proj/src/estimator.cpp)
+/// residual indicators eta_T^2: element residual + half-flux jumps (estimator.cpp:11-85)
+Vec compute_indicators(const System& s, const Space& V, const Vec& lambdas, const std::vector<Vec>& orb,
+                       const Vec& w, const Vec& vxc, double* total_sq);
+/// minimal greedy set reaching theta * total (estimator.cpp:87-104)
+std::vector<int> dorfler_mark(const Vec& eta_sq, double total_sq, double theta);
+
 struct Moments {
     double q = 0;
     V3 c{{0, 0, 0}}, dip{{0, 0, 0}};

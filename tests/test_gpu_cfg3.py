@@ -1,0 +1,101 @@
+"""cfg3 geometry (BASELINE.json configs[2]) at reduced size: the multi-orbital correction step on an adaptive
+mesh, device vs oracle.
+
+H2O: Z=8 at the origin, two Z=1 at 1.8 bohr with 104.5 degrees between them, the frame turned by a seeded
+uniform rotation (normalised Gaussian quaternion); N = 5 doubly occupied orbitals, LDA, [-20,20]^3, 8^3 Kuhn
+coarse mesh. The residual estimator is outside this tier, so the adaptive level
+marks the tets whose centroid lies within 6 bohr of a nucleus (a deterministic stand-in for Doerfler
+marking; both mesh pipelines are bit-exact, so both sides refine the same tets). Three outer iterations
+from the oracle's coarse SCF: eigenvalues and energy 1e-8 relative, density and orbitals 1e-6 relative L2.
+"""
+import numpy as np
+import pytest
+
+import paper_2103_02824_b200 as kb
+from oracle import OMesh, Oracle
+
+SEED = 2103
+
+
+def h2o_atoms(seed=SEED):
+    rng = np.random.default_rng(seed)
+    qv = rng.standard_normal(4)
+    a, b, c, d = qv / np.linalg.norm(qv)
+    Rm = np.array([[a * a + b * b - c * c - d * d, 2 * (b * c - a * d), 2 * (b * d + a * c)],
+                   [2 * (b * c + a * d), a * a - b * b + c * c - d * d, 2 * (c * d - a * b)],
+                   [2 * (b * d - a * c), 2 * (c * d + a * b), a * a - b * b - c * c + d * d]])
+    half = np.deg2rad(104.5) / 2
+    h1 = 1.8 * np.array([np.sin(half), np.cos(half), 0.0])
+    h2 = 1.8 * np.array([-np.sin(half), np.cos(half), 0.0])
+    pos = [np.zeros(3), Rm @ h1, Rm @ h2]
+    return [[8.0, *pos[0]], [1.0, *pos[1]], [1.0, *pos[2]]]
+
+
+def near_marks(mesh_xyz, tets, atoms, radius):
+    cen = mesh_xyz[tets].mean(axis=1)
+    d = np.min([np.linalg.norm(cen - np.asarray(a[1:]), axis=1) for a in atoms], axis=0)
+    return np.nonzero(d < radius)[0].astype(np.int32)
+
+
+def test_h2o_geometry():
+    at = h2o_atoms()
+    p0, p1, p2 = (np.asarray(a[1:]) for a in at)
+    assert abs(np.linalg.norm(p1 - p0) - 1.8) < 1e-12 and abs(np.linalg.norm(p2 - p0) - 1.8) < 1e-12
+    cosang = (p1 - p0) @ (p2 - p0) / 1.8 ** 2
+    assert abs(np.degrees(np.arccos(cosang)) - 104.5) < 1e-9
+
+
+@pytest.mark.gpu
+def test_cfg3_adaptive_multi_orbital_step_matches_oracle(ctx):
+    atoms = h2o_atoms()
+    N = 5
+    h = kb.Hierarchy()
+    orc = Oracle(atoms, n_pairs=N, occ=2.0, xc="lda")
+    a, b = kb.Mesh.box([-20.0] * 3, [20.0] * 3, 8), OMesh.box([-20.0] * 3, [20.0] * 3, 8)
+    h.push(a)
+    orc.push(b)
+    a, b = a.uniform_refine(), b.uniform_refine()
+    h.push(a)
+    orc.push(b)
+    marks = near_marks(b.array("xyz"), b.array("tets"), atoms, 6.0)
+    assert len(marks) > 0
+    a, b = a.adapt_refine(marks), b.adapt_refine(marks)
+    assert np.array_equal(a.array("tets"), b.array("tets"))
+    h.push(a)
+    orc.push(b)
+    lev = 2
+    L = kb.Level(ctx, h, lev)
+    L.set_system(atoms, n_pairs=N, occupancy=2.0, xc="lda")
+    L.level_ops()
+    it = L.index("interior")
+    lam0, orb0, w0, _ = orc.coarse_scf(tol=1e-8, mixing=0.3)
+    orb = orc.prolong(orb0, 0, lev)
+    w = orc.prolong(w0, 0, lev)[:, 0]
+    ld = N + (N & 1)
+    blk = np.zeros((L.ni, ld))
+    blk[:, :N] = orb[it]
+    Phi, dw = ctx.to_device(blk), ctx.to_device(w)
+    lam_g, lam_o, orb_o, w_o = lam0.copy(), lam0.copy(), orb.copy(), w.copy()
+    for outer in range(3):
+        lg = L.correction_step(lam_g, Phi, dw, ld=ld)
+        lam_o, orb_o, w_o, lo = orc.correction_step(lev, lam_o, orb_o, w_o)
+        assert lg["attempts"] == lo["attempts"], outer
+        assert abs(lg["inner_iterations"] - lo["inner_iterations"]) <= 1, (lg["inner_iterations"], lo["inner_iterations"])
+        assert np.abs(lam_g - lam_o).max() <= 1e-8 * np.abs(lam_o).max(), (outer, lam_g, lam_o)
+    P = Phi.download()[:, :N]
+    O = orb_o[it]
+    rho_g, rho_o = 2.0 * (P ** 2).sum(1), 2.0 * (O ** 2).sum(1)
+    assert np.linalg.norm(rho_g - rho_o) <= 1e-6 * np.linalg.norm(rho_o)
+    gaps = np.diff(np.sort(lam_o))
+    for i in range(N):  # per orbital where the eigenvalue is separated; else the subspace is compared via rho
+        gap = min([abs(lam_o[i] - lam_o[j]) for j in range(N) if j != i])
+        if gap > 1e-3:
+            s = np.sign(P[:, i] @ O[:, i])
+            assert np.linalg.norm(s * P[:, i] - O[:, i]) <= 1e-6 * np.linalg.norm(O[:, i]), i
+    assert np.linalg.norm(dw.download() - w_o) <= 1e-6 * np.linalg.norm(w_o)
+    full = np.zeros((L.n, N))
+    full[it] = P
+    e_g = L.energy(ctx.to_device(np.ascontiguousarray(P)), dw, N=N)
+    e_o = orc.energy(lev, orb_o, w_o)
+    assert np.abs(np.asarray(e_g) - e_o).max() <= 1e-8 * np.abs(e_o).max()
+    assert gaps.size == N - 1

@@ -646,3 +646,90 @@ def test_inner_iteration_fixed_point_and_expansion():
         ledger = p @ MH @ p + 2 * t * (c[i] @ p) + t * t * gam[i]
         assert abs(fine_sq - ledger) < 1e-9 * max(1.0, fine_sq)
         assert abs(fine_sq - 1.0) < 1e-6
+
+
+# ------------------------------------------------------------------ estimator (test_estimator.cpp:35-175)
+def free_oracle(lo, hi, n, refine=0):
+    return setup(lo, hi, n, refine=refine, atoms=[], n_pairs=1, occ=1.0, xc="none", hartree=False)
+
+
+def test_estimator_zero_state():
+    orc = free_oracle(-1, 1, 2)
+    n = orc.n(0)
+    eta, tot = orc.indicators(0, [0.0], np.zeros((n, 1)), np.zeros(n), np.zeros(n))
+    assert tot == 0.0 and np.all(eta >= 0)
+
+
+def test_estimator_linear_function_has_no_residual():
+    orc = free_oracle(-1, 1, 3)
+    xyz = orc.meshes[0].array("xyz")
+    lin = 0.7 * xyz[:, 0] - 0.1 * xyz[:, 1]
+    n = orc.n(0)
+    _, tot = orc.indicators(0, [0.0], lin[:, None], np.zeros(n), np.zeros(n))
+    assert tot < 1e-24
+
+
+def test_estimator_contracts_by_about_four():
+    lam = 1.5 * math.pi ** 2
+    tots = []
+    for lev_refine in (0, 1):
+        orc = free_oracle(0, 1, 4, refine=lev_refine)
+        lev = lev_refine
+        xyz = orc.meshes[lev].array("xyz")
+        u = np.sin(math.pi * xyz[:, 0]) * np.sin(math.pi * xyz[:, 1]) * np.sin(math.pi * xyz[:, 2])
+        n = orc.n(lev)
+        tots.append(orc.indicators(lev, [lam], u[:, None], np.zeros(n), np.zeros(n))[1])
+    assert 3.0 < tots[0] / tots[1] < 5.0
+
+
+def test_marking_hand_checked():
+    from oracle import dorfler_mark
+    eta = np.array([4.0, 3.0, 2.0, 1.0])
+    assert list(dorfler_mark(eta, 10.0, 0.4)) == [0]
+    assert len(dorfler_mark(eta, 10.0, 0.999)) == 4
+    assert len(dorfler_mark(np.zeros(5), 0.0, 0.4)) == 0
+    with pytest.raises(OracleError):
+        dorfler_mark(eta, 10.0, 1.5)
+
+
+def test_marking_greedy_set_is_minimal():
+    from oracle import dorfler_mark
+    rng = np.random.default_rng(17)
+    for rep in range(20):
+        n = 5 + int(rng.integers(0, 8))
+        eta = rng.uniform(0.01, 1.0, n)
+        tot = float(eta.sum())
+        for theta in (0.15, 0.4, 0.6, 0.85):
+            mk = dorfler_mark(eta, tot, theta)
+            s = eta[mk].sum()
+            assert s >= theta * tot
+            assert s - eta[mk].min() < theta * tot
+            best = n + 1
+            for mask in range(1 << n):
+                sel = [(mask >> i) & 1 for i in range(n)]
+                if eta[np.array(sel, bool)].sum() >= theta * tot:
+                    best = min(best, sum(sel))
+            assert len(mk) == best
+
+
+@pytest.mark.slow
+def test_indicators_concentrate_near_nuclei():
+    atoms = [(3.0, -1.0075, 0, 0), (1.0, 2.0075, 0, 0)]
+    orc = Oracle(list(atoms), n_pairs=2, occ=2.0, xc="x_alpha", hartree=True)
+    orc.push(OMesh.box([-6.0] * 3, [6.0] * 3, 12))
+    lam, orb, w, it = orc.coarse_scf(tol=1e-6, mixing=0.4, tol_eig=1e-9)
+    rho = orc.density(orb)
+    vxc = orc.xc_potential(rho)
+    eta, tot = orc.indicators(0, lam, orb, w, vxc)
+    order = np.argsort(-eta, kind="stable")
+    thr = 0.81 * eta[order[0]]
+    xyz, tets = orc.meshes[0].array("xyz"), orc.meshes[0].array("tets")
+    checked = 0
+    for t in order:
+        if eta[t] < thr:
+            break
+        c = xyz[tets[t]].mean(axis=0)
+        d = min(np.linalg.norm(c - np.asarray(a[1:])) for a in atoms)
+        assert d <= 1.5
+        checked += 1
+    assert checked >= 4
