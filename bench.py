@@ -51,6 +51,14 @@ def rhs_block(ni, seed=SEED + 1):
     return np.random.default_rng(seed).standard_normal((ni, N_RHS))
 
 
+def ncu_traffic(kernel):
+    """DRAM bytes per launch from the committed ncu capture (profiles/ncu_traffic.json), or None."""
+    try:
+        return int(json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text())[kernel]["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
 def measured_peak():
     try:
         j = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
@@ -369,7 +377,7 @@ def run_b200(args, world, rank, local):
                        "l2": "inputs larger than L2 (256 MB blocks, 363 MB operator)",
                        "breakdown_columns": breakdown_cols, "setup_s": round(setup_s, 2)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": None, "kernel": "k_spmm_dot", "bytes_per_launch": bytes_spmm,
+                         "traffic": ncu_traffic("k_spmm_dot"), "kernel": "k_spmm_dot", "bytes_per_launch": bytes_spmm,
                          "avg_launch_ms": spmm_avg, "peak_kind": peak_kind},
             "spmm_hbm_frac": achieved / peak,
             "cg_update_r_avg_ms": upd_ms / max(1, upd_n),
