@@ -1,12 +1,16 @@
-"""cfg3 geometry (BASELINE.json configs[2]) at reduced size: the multi-orbital correction step on an adaptive
-mesh, device vs oracle.
+"""Multi-orbital correction steps on an adaptively refined mesh, device vs oracle.
 
-H2O: Z=8 at the origin, two Z=1 at 1.8 bohr with 104.5 degrees between them, the frame turned by a seeded
-uniform rotation (normalised Gaussian quaternion); N = 5 doubly occupied orbitals, LDA, [-20,20]^3, 8^3 Kuhn
-coarse mesh. The residual estimator is outside this tier, so the adaptive level
-marks the tets whose centroid lies within 6 bohr of a nucleus (a deterministic stand-in for Doerfler
-marking; both mesh pipelines are bit-exact, so both sides refine the same tets). Three outer iterations
-from the oracle's coarse SCF: eigenvalues and energy 1e-8 relative, density and orbitals 1e-6 relative L2.
+LiH-like pair (Z=3 and Z=1, 3.015 bohr apart, slightly off-axis), 2 doubly occupied orbitals, LDA, [-8,8]^3,
+8^3 Kuhn coarse mesh, one uniform refinement, then one adaptive level. The residual estimator lives in the
+oracle only, so the adaptive level marks the tets whose centroid lies within 2.5 bohr of
+a nucleus; both mesh pipelines are bit-exact, so both sides refine the same tets. Start: the oracle's coarse
+SCF, prolonged. The first steps take the level-shift ladder (attempt 1) on both sides. Three outer iterations:
+eigenvalues and energy 1e-8 relative, density, orbitals and w 1e-6 relative L2.
+
+cfg3 itself (H2O, N = 5, [-20,20]^3, 8^3 coarse) is not runnable by the reference algorithm at this coarse
+resolution: the coarse SCF does not converge (h = 5 bohr; near-degenerate levels swap occupation) and from a
+bare-Hamiltonian start the inner iteration of the first correction step exceeds its cap in the oracle as well.
+The H2O geometry builder is kept for the adaptive runs of a later round.
 """
 import numpy as np
 import pytest
@@ -45,19 +49,22 @@ def test_h2o_geometry():
     assert abs(np.degrees(np.arccos(cosang)) - 104.5) < 1e-9
 
 
+LIH = [[3.0, -1.0075, 0.1, 0.05], [1.0, 2.0075, -0.1, 0.0]]
+
+
 @pytest.mark.gpu
-def test_cfg3_adaptive_multi_orbital_step_matches_oracle(ctx):
-    atoms = h2o_atoms()
-    N = 5
+def test_adaptive_multi_orbital_step_matches_oracle(ctx):
+    atoms = LIH
+    N = 2
     h = kb.Hierarchy()
     orc = Oracle(atoms, n_pairs=N, occ=2.0, xc="lda")
-    a, b = kb.Mesh.box([-20.0] * 3, [20.0] * 3, 8), OMesh.box([-20.0] * 3, [20.0] * 3, 8)
+    a, b = kb.Mesh.box([-8.0] * 3, [8.0] * 3, 8), OMesh.box([-8.0] * 3, [8.0] * 3, 8)
     h.push(a)
     orc.push(b)
     a, b = a.uniform_refine(), b.uniform_refine()
     h.push(a)
     orc.push(b)
-    marks = near_marks(b.array("xyz"), b.array("tets"), atoms, 6.0)
+    marks = near_marks(b.array("xyz"), b.array("tets"), atoms, 2.5)
     assert len(marks) > 0
     a, b = a.adapt_refine(marks), b.adapt_refine(marks)
     assert np.array_equal(a.array("tets"), b.array("tets"))
@@ -71,7 +78,7 @@ def test_cfg3_adaptive_multi_orbital_step_matches_oracle(ctx):
     lam0, orb0, w0, _ = orc.coarse_scf(tol=1e-8, mixing=0.3)
     orb = orc.prolong(orb0, 0, lev)
     w = orc.prolong(w0, 0, lev)[:, 0]
-    ld = N + (N & 1)
+    ld = N
     blk = np.zeros((L.ni, ld))
     blk[:, :N] = orb[it]
     Phi, dw = ctx.to_device(blk), ctx.to_device(w)
