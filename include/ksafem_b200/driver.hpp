@@ -3,6 +3,7 @@
 #pragma once
 
 #include "ksafem_b200/correction.hpp"
+#include "ksafem_b200/estimator.hpp"
 
 namespace ksafem::driver {
 

@@ -254,6 +254,15 @@ int ksb_inner_scf(ksb_level* l, const ksb_step_opts* o, const double* h_lambda, 
 /* corr::expand of the last inner state (proj/src/correction.cpp:370-381) */
 int ksb_expand(ksb_level* l, const double* d_PhiT, int ld, const double* d_wt_full, const double* d_bcb,
                double* d_Phi, double* d_w_full);
+/* est::compute_indicators (proj/src/estimator.cpp:11-85): element residual of (V_ext + w + v_xc - lambda_i) phi_i
+ * plus half-flux jumps across interior faces; d_eta gets eta_T^2 for every tet (n_tets), h_total_sq their sum.
+ * Orbitals: interior block (N = the system's n_pairs columns); w, v_xc full length. */
+int ksb_indicators(ksb_level* l, const double* h_lambda, const double* d_Phi, int ld, const double* d_w_full,
+                   const double* d_vxc_full, double* d_eta, double* h_total_sq);
+/* est::dorfler_mark (proj/src/estimator.cpp:87-104), host: descending eta, lower index first on ties, minimal
+ * prefix reaching theta * total. h_marked needs room for n_tets entries. No device needed. */
+int ksb_dorfler_mark(const double* h_eta, int64_t n_tets, double total_sq, double theta, int32_t* h_marked,
+                     int64_t* h_n_marked);
 /* l2_norm^2, h1_seminorm^2, h1_norm of a full-length nodal function (proj/src/assembly.cpp:251-287) */
 int ksb_norms(ksb_level* l, const double* d_f_full, double h_out[3]);
 /* model::total_energy (proj/src/ks_model.cpp:107-143): kinetic, external, hartree, xc, total */

@@ -421,6 +421,15 @@ class Level:
     def expand(self, PhiT: DeviceArray, wt: DeviceArray, bcb: DeviceArray, Phi: DeviceArray, w: DeviceArray):
         check(lib.ksb_expand(self._h, PhiT.ptr, int(PhiT.shape[1]), wt.ptr, bcb.ptr, Phi.ptr, w.ptr))
 
+    def indicators(self, lambdas, Phi: DeviceArray, w: DeviceArray, vxc: DeviceArray, ld: int | None = None):
+        """est::compute_indicators (proj/src/estimator.cpp:11-85) on the device: (eta_sq per tet, total)."""
+        lam = np.ascontiguousarray(lambdas, np.float64)
+        eta = self.ctx.empty((self.nt,))
+        tot = C.c_double()
+        check(lib.ksb_indicators(self._h, _dp(lam), Phi.ptr, int(ld or Phi.shape[1]), w.ptr, vxc.ptr, eta.ptr,
+                                 C.byref(tot)))
+        return eta.download(), tot.value
+
     def norms(self, f: DeviceArray) -> np.ndarray:
         out = np.empty(3)
         check(lib.ksb_norms(self._h, f.ptr, _dp(out)))
@@ -430,6 +439,15 @@ class Level:
         out = np.empty(5)
         check(lib.ksb_energy(self._h, Phi.ptr, int(N or self.N), int(ld or Phi.shape[1]), w.ptr, _dp(out)))
         return out
+
+
+def dorfler_mark(eta, total_sq: float, theta: float) -> np.ndarray:
+    """est::dorfler_mark (proj/src/estimator.cpp:87-104), host side of the C-ABI."""
+    e = np.ascontiguousarray(eta, np.float64)
+    out = np.empty(len(e), np.int32)
+    n = C.c_int64()
+    check(lib.ksb_dorfler_mark(_dp(e), len(e), float(total_sq), float(theta), _ip(out), C.byref(n)))
+    return out[:n.value].copy()
 
 
 def N_cols(n: int) -> int:

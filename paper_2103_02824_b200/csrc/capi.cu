@@ -1,4 +1,5 @@
 // C-ABI implementation (include/ksb.h). No exceptions cross this boundary.
+#include <algorithm>
 #include <cstring>
 #include <exception>
 #include <new>
@@ -910,6 +911,41 @@ int ksb_expand(ksb_level* l, const double* d_PhiT, int ld, const double* d_wt, c
         need(d_PhiT && d_wt && d_bcb && d_Phi && d_w, "null argument");
         ksb::expand(l->L, K, d_PhiT, ld, d_wt, d_bcb, d_Phi, ld, d_w);
         KSB_CUDA_CHECK(cudaStreamSynchronize(l->L.ctx->stream));
+    });
+}
+
+int ksb_indicators(ksb_level* l, const double* h_lambda, const double* d_Phi, int ld, const double* d_w,
+                   const double* d_vxc, double* d_eta, double* h_total_sq) {
+    return guard([&] {
+        auto& K = ready(l);
+        need(h_lambda && d_Phi && d_w && d_vxc && d_eta, "null argument");
+        const int N = K.sys.N;
+        if (ld < N) ksb::raise(KSB_INVALID_ARGUMENT, "ld must be >= N");
+        const double tot = ksb::indicators(l->L, K.est, K.sys.atoms, h_lambda, N, d_Phi, ld, d_w, d_vxc, d_eta);
+        if (h_total_sq) *h_total_sq = tot;
+    });
+}
+
+int ksb_dorfler_mark(const double* eta, int64_t nt, double total_sq, double theta, int32_t* marked, int64_t* n_marked) {
+    return guard([&] {
+        need(eta && marked && n_marked, "null argument");
+        if (!(theta > 0.0) || theta >= 1.0) ksb::raise(KSB_INVALID_ARGUMENT, "theta must lie in (0,1)");
+        *n_marked = 0;
+        if (total_sq <= 0.0) return;
+        std::vector<int32_t> order(static_cast<size_t>(nt));
+        for (int64_t i = 0; i < nt; ++i) order[size_t(i)] = int32_t(i);
+        std::sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
+            if (eta[a] != eta[b]) return eta[a] > eta[b];
+            return a < b;
+        });
+        double acc = 0.0;
+        int64_t k = 0;
+        for (int32_t t : order) {
+            marked[k++] = t;
+            acc += eta[t];
+            if (acc >= theta * total_sq) break;
+        }
+        *n_marked = k;
     });
 }
 

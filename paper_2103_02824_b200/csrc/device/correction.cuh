@@ -52,6 +52,7 @@ struct Corrector {
     DevBuf<double> R0, Bblk, Xblk, Bc, Xc, PhiT;
     DevBuf<int> idx;
     int ldT = 0;
+    EstimatorData est;
 };
 
 void level_ops(Level& L, Corrector& K);

@@ -32,6 +32,16 @@ void sqload(Level& L, const double* Phi, int N, int ld, double occ, double scale
 void sqload_full(Level& L, const double* Phi, int N, int ld, double occ, double* out_full, PhysWork& w);
 /// model::xc_potential_field (proj/src/ks_model.cpp:101-105)
 void xc_field(Level& L, const XcParams& xc, const double* rho_full, double* vxc_full);
+/// residual-indicator device data (face lists, per-tet face gather), uploaded on first use
+struct EstimatorData {
+    DevBuf<int32_t> ftets, tptr, tface;
+    DevBuf<double> fgeom, contrib, part, scal, lam, atoms;
+    bool ready = false;
+    void ensure(Level& L);
+};
+/// est::compute_indicators (proj/src/estimator.cpp:11-85): eta_T^2 per tet into d_eta (nt); returns the total
+double indicators(Level& L, EstimatorData& E, const std::vector<double>& atoms, const double* h_lambda, int N,
+                  const double* d_Phi, int ld, const double* d_w, const double* d_vxc, double* d_eta);
 /// y_int -= A_ib(mat) bcb (Dirichlet lift, reference proj/src/solver.cpp:123)
 void lift(Level& L, int mat, const double* bcb, double* y_int);
 /// squared L2 norm and squared H1 seminorm of a full-length nodal function

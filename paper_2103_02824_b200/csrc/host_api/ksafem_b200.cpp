@@ -906,6 +906,39 @@ Expanded expand(const AugmentedState& s, const AugmentedBlocks& blocks) {
 
 } // namespace corr
 
+// ------------------------------------------------------------------ estimator
+namespace est {
+
+Indicators compute_indicators(const fem::FESpace& V, const model::MolecularSystem& sys, const VecX& lambdas,
+                              const std::vector<fem::FEFunction>& orbitals, const fem::FEFunction& hartree_fn,
+                              const fem::FEFunction& vxc_fn, WorkerPool*) {
+    if (orbitals.empty()) fail("invalid-argument", "empty orbital set");
+    if (lambdas.size() != orbitals.size()) fail("invalid-argument", "one eigenvalue per orbital");
+    fem::same_space(hartree_fn, V, "hartree potential on a different space");
+    fem::same_space(vxc_fn, V, "v_xc on a different space");
+    model::MolecularSystem s2 = sys;
+    s2.n_pairs = int(orbitals.size());
+    model::set_system(V, s2, true, sys.xc.kind != model::XcKind::none);
+    int ld = 0;
+    auto blk = fem::orbital_block(V, orbitals, ld);
+    b200::DeviceBuffer dw(V.device(), hartree_fn.coeffs), dv(V.device(), vxc_fn.coeffs);
+    b200::DeviceBuffer deta(V.device(), int64_t(V.mesh().n_tets()));
+    Indicators ind;
+    b200::check(ksb_indicators(V.device_level(), lambdas.data(), blk.data(), ld, dw.data(), dv.data(), deta.data(),
+                               &ind.total_sq));
+    ind.eta_sq = deta.to_host();
+    return ind;
+}
+
+std::vector<int> dorfler_mark(const Indicators& ind, double theta) {
+    std::vector<int32_t> mk(ind.eta_sq.size());
+    int64_t n = 0;
+    b200::check(ksb_dorfler_mark(ind.eta_sq.data(), int64_t(ind.eta_sq.size()), ind.total_sq, theta, mk.data(), &n));
+    return std::vector<int>(mk.begin(), mk.begin() + n);
+}
+
+} // namespace est
+
 // ------------------------------------------------------------------ driver
 namespace driver {
 

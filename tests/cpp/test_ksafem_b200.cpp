@@ -356,6 +356,43 @@ TEST_CASE("ledger symmetry, zero inputs, inner iteration and expansion", t_block
     CHECK_THROWS_CODE(corr::expand(init, B), "invalid-argument");
 }
 
+// ---------------------------------------------------------------- estimator (test_estimator.cpp:35-100)
+TEST_CASE("indicators: zero state, linear function, marking", t_estimator) {
+    fem::SpaceHierarchy hier;
+    model::MolecularSystem sys;
+    sys.n_pairs = 1;
+    sys.occupancy = 1.0;
+    sys.domain = cube(-1, 1);
+    sys.xc.kind = model::XcKind::none;
+    sys.atoms.push_back({1.0, Vec3(0.3, 0.1, -0.2)});
+    auto m = mesh::build_box_mesh(sys.domain, 3);
+    hier.push(m);
+    const auto ops = driver::make_level_ops(hier, 0, sys);
+    const auto& V = ops.space;
+    const fem::FEFunction z(V);
+    const auto ind0 = est::compute_indicators(*V, sys, VecX{0.0}, {fem::FEFunction(V, fem::Role::wavefunction)}, z, z);
+    CHECK(ind0.total_sq == 0.0 && int(ind0.eta_sq.size()) == V->mesh().n_tets());
+    CHECK(est::dorfler_mark(ind0, 0.4).empty());
+    fem::FEFunction phi(V, fem::Role::wavefunction);
+    const auto xyz = V->mesh().vertices();
+    for (int i : V->interior_dofs()) {
+        const auto& x = xyz[size_t(i)];
+        phi.coeffs[size_t(i)] = std::exp(-2.0 * (x[0] * x[0] + x[1] * x[1] + x[2] * x[2]));
+    }
+    const auto ind = est::compute_indicators(*V, sys, VecX{-0.5}, {phi}, z, z);
+    double sum = 0;
+    for (double e : ind.eta_sq) sum += e;
+    CHECK(ind.total_sq > 0 && std::fabs(sum - ind.total_sq) <= 1e-12 * ind.total_sq);
+    const auto mk = est::dorfler_mark(ind, 0.4);
+    double got = 0, mn = 1e300;
+    for (int t : mk) {
+        got += ind.eta_sq[size_t(t)];
+        mn = std::min(mn, ind.eta_sq[size_t(t)]);
+    }
+    CHECK(got >= 0.4 * ind.total_sq && got - mn < 0.4 * ind.total_sq);
+    CHECK_THROWS_CODE(est::dorfler_mark(ind, 1.5), "invalid-argument");
+}
+
 // ---------------------------------------------------------------- driver: a small level loop end to end
 TEST_CASE("solve_level_corrected converges from a hydrogenic start", t_driver) {
     fem::SpaceHierarchy hier;

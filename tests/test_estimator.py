@@ -1,0 +1,76 @@
+"""Residual estimator: device indicators and host Doerfler marking vs the oracle.
+
+Indicators: est::compute_indicators (proj/src/estimator.cpp:11-85) on converged-ish states (oracle coarse SCF
+prolonged, one correction step) -- per tet within 1e-11 relative to the largest, total within 1e-12, and the
+Doerfler set (theta = 0.4, proj/include/ksafem/runconfig.hpp:17) identical. Marking: est::dorfler_mark
+(estimator.cpp:87-104) through the C-ABI's host entry, against the oracle, on random data with ties.
+"""
+import numpy as np
+import pytest
+
+import paper_2103_02824_b200 as kb
+from oracle import OMesh, Oracle, dorfler_mark as o_mark
+
+
+def test_dorfler_mark_host_entry_matches_oracle():
+    rng = np.random.default_rng(5)
+    for rep in range(50):
+        n = int(rng.integers(1, 400))
+        eta = rng.uniform(0.0, 1.0, n)
+        if rep % 3 == 0:  # ties: index order decides
+            eta = np.round(eta * 7) / 7
+        tot = float(eta.sum())
+        for theta in (0.1, 0.4, 0.75, 0.99):
+            assert np.array_equal(kb.dorfler_mark(eta, tot, theta), o_mark(eta, tot, theta))
+    assert len(kb.dorfler_mark(np.zeros(4), 0.0, 0.4)) == 0
+    with pytest.raises(kb.KsbError):
+        kb.dorfler_mark(np.ones(3), 3.0, 1.5)
+
+
+def _case(ctx, atoms, N, occ, xc, box, n_coarse, adapt_radius=None):
+    h = kb.Hierarchy()
+    orc = Oracle(atoms, n_pairs=N, occ=occ, xc=xc)
+    a, b = kb.Mesh.box([-box] * 3, [box] * 3, n_coarse), OMesh.box([-box] * 3, [box] * 3, n_coarse)
+    h.push(a)
+    orc.push(b)
+    a, b = a.uniform_refine(), b.uniform_refine()
+    h.push(a)
+    orc.push(b)
+    if adapt_radius:
+        xyz, tets = b.array("xyz"), b.array("tets")
+        cen = xyz[tets].mean(axis=1)
+        d = np.min([np.linalg.norm(cen - np.asarray(at[1:]), axis=1) for at in atoms], axis=0)
+        mk = np.nonzero(d < adapt_radius)[0].astype(np.int32)
+        a, b = a.adapt_refine(mk), b.adapt_refine(mk)
+        h.push(a)
+        orc.push(b)
+    lev = h.n_levels - 1
+    L = kb.Level(ctx, h, lev)
+    L.set_system(atoms, n_pairs=N, occupancy=occ, xc=xc)
+    L.level_ops()
+    lam, orb0, w0, _ = orc.coarse_scf(tol=1e-8, mixing=0.3)
+    orb = orc.prolong(orb0, 0, lev)
+    w = orc.prolong(w0, 0, lev)[:, 0]
+    lam, orb, w, _ = orc.correction_step(lev, lam, orb, w)
+    return L, orc, lev, lam, orb, w
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("which", ["he", "lih_adaptive"])
+def test_indicators_match_oracle(ctx, which):
+    if which == "he":
+        L, orc, lev, lam, orb, w = _case(ctx, [[2.0, 0.3, -0.2, 0.1]], 1, 2.0, "lda", 6.0, 4)
+    else:
+        L, orc, lev, lam, orb, w = _case(ctx, [[3.0, -1.0075, 0.1, 0.05], [1.0, 2.0075, -0.1, 0.0]], 2, 2.0, "lda",
+                                         8.0, 8, adapt_radius=2.5)
+    it = L.index("interior")
+    rho = orc.density(orb)
+    vxc = orc.xc_potential(rho)
+    eta_o, tot_o = orc.indicators(lev, lam, orb, w, vxc)
+    N = orb.shape[1]
+    eta_g, tot_g = L.indicators(lam, ctx.to_device(np.ascontiguousarray(orb[it])), ctx.to_device(w),
+                                ctx.to_device(vxc), ld=N)
+    assert eta_g.shape == eta_o.shape
+    assert np.abs(eta_g - eta_o).max() <= 1e-11 * eta_o.max()
+    assert abs(tot_g - tot_o) <= 1e-12 * tot_o
+    assert np.array_equal(kb.dorfler_mark(eta_g, tot_g, 0.4), o_mark(eta_o, tot_o, 0.4))
