@@ -18,6 +18,7 @@
 // K4: x, p, r in, x, p out) instead of 9 with the textbook x/r and p passes.
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 #include "cg.cuh"
 #include "spmm_core.cuh"
@@ -831,6 +832,11 @@ void iteration(Ctx& c, const Level& L, const CgWork& w, const Cols& cc, const do
 
 } // namespace
 
+CgWork::~CgWork() {
+    for (auto& g : graphs)
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+}
+
 void CgWork::ensure(int ni, int N, int ld, int max_blocks) {
     const int64_t vec = int64_t(ni) * ld;
     if (vec > cap_vec) {
@@ -911,14 +917,64 @@ void cg_solve(Ctx& c, Level& L, int mat, int shift_mat, const double* h_sigma, c
     }
     const int total = cc.fixed ? o.fixed_iterations : o.max_iterations;
     const int every = std::max(1, o.check_every);
-    int done = 0;
-    while (done < total) {
-        const int chunk = std::min(every, total - done);
+    auto run_chunk = [&](int chunk) {
         for (int k = 0; k < chunk; ++k) {
             if (shift)
                 iteration<true>(c, L, w, cc, A, Bv, d_B, d_X, grid_s, grid_e, so);
             else
                 iteration<false>(c, L, w, cc, A, nullptr, d_B, d_X, grid_s, grid_e, so);
+        }
+    };
+    // After the first chunk (which also warms the occupancy caches), chunks replay as CUDA graphs: one launch
+    // per check_every iterations instead of 3-4 per iteration. Off while profiling (per-kernel events) or with
+    // KSB_CG_GRAPHS=0.
+    static const char* genv = std::getenv("KSB_CG_GRAPHS");
+    const bool graphs_on = !c.profiling && !(genv && genv[0] == '0');
+    auto graph_for = [&](int chunk) -> CgGraph& {
+        CgGraphKey key;
+        std::memset(&key, 0, sizeof key);
+        const void* ptrs[16] = {&L, A, Bv, d_B, d_X, so.A, so.B, w.R, w.P, w.AP, w.scal.p, w.parts.p, w.ints.p,
+                                d.diagA, d.diagB, L.ii_col.p};
+        std::memcpy(key.ptrs, ptrs, sizeof ptrs);
+        const int ints[8] = {mat, shift_mat, N, ld, chunk, grid_s, grid_e, cc.fixed};
+        std::memcpy(key.ints, ints, sizeof ints);
+        key.tol = cc.tol;
+        for (auto& g : w.graphs)
+            if (std::memcmp(&g.key, &key, sizeof key) == 0) return g;
+        if (w.graphs.size() >= 8) {
+            cudaGraphExecDestroy(w.graphs.front().exec);
+            w.graphs.erase(w.graphs.begin());
+        }
+        CgGraph g;
+        g.key = key;
+        const int64_t l0 = c.launches;
+        KSB_CUDA_CHECK(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeRelaxed));
+        try {
+            run_chunk(chunk);
+        } catch (...) {
+            cudaGraph_t bad = nullptr;
+            cudaStreamEndCapture(c.stream, &bad);
+            if (bad) cudaGraphDestroy(bad);
+            throw;
+        }
+        cudaGraph_t graph = nullptr;
+        KSB_CUDA_CHECK(cudaStreamEndCapture(c.stream, &graph));
+        g.kernels = c.launches - l0;
+        c.launches = l0;
+        KSB_CUDA_CHECK(cudaGraphInstantiate(&g.exec, graph, 0));
+        cudaGraphDestroy(graph);
+        w.graphs.push_back(g);
+        return w.graphs.back();
+    };
+    int done = 0;
+    while (done < total) {
+        const int chunk = std::min(every, total - done);
+        if (graphs_on && done > 0) {
+            CgGraph& g = graph_for(chunk);
+            KSB_CUDA_CHECK(cudaGraphLaunch(g.exec, c.stream));
+            c.launches += g.kernels;
+        } else {
+            run_chunk(chunk);
         }
         done += chunk;
         if (!cc.fixed) {

@@ -27,6 +27,19 @@ struct CgDev {
     double *part0, *part1;
 };
 
+/// identity of a captured chunk of CG iterations: every kernel argument that can differ between solves
+struct CgGraphKey {
+    const void* ptrs[16];
+    int ints[8];
+    double tol;
+};
+
+struct CgGraph {
+    CgGraphKey key;
+    cudaGraphExec_t exec = nullptr;
+    int64_t kernels = 0;
+};
+
 struct CgWork {
     DevBuf<double> rbuf, pbuf, apbuf, scal, parts, diagA, diagB;
     DevBuf<int> ints;
@@ -34,7 +47,9 @@ struct CgWork {
     int64_t cap_vec = 0;
     int cap_cols = 0, cap_blocks = 0;
     CgDev dev{};
+    std::vector<CgGraph> graphs;  // chunks of iterations captured as CUDA graphs (small FIFO cache)
     void ensure(int ni, int N, int ld, int max_blocks);
+    ~CgWork();
 };
 
 void cg_solve(Ctx& c, Level& L, int mat, int shift_mat, const double* h_sigma, const double* d_B, double* d_X, int N,
