@@ -209,6 +209,21 @@ int ksb_correction_step(ksb_level* l, const ksb_step_opts* o, double* h_lambda, 
 int ksb_correction_step_host(ksb_level* l, const ksb_step_opts* o, double* h_lambda, double* h_Phi, int ld,
                              double* h_w, ksb_step_log* log, int* h_attempts, int* h_iters);
 
+/* scf::self_consistent_solve on the coarsest space (proj/src/scf.cpp:22-90), level 0 of the hierarchy:
+ * dense lowest eigenpairs of the current Hamiltonian, linear density mixing, Hartree potential of the mixed
+ * density. Outputs: lambdas (N, host), orbitals (interior block, device), mixed density and Hartree potential
+ * (full length, device); history = density change per iteration. */
+typedef struct {
+    double tol;          /* density-change stop (RunConfig::tol_outer, 1e-6) */
+    int max_iterations;  /* RunConfig::max_scf (200) */
+    double mixing;       /* RunConfig::mixing (0.3) */
+    int hartree_on, xc_on;
+    double tol_eig;      /* Hartree solve tolerance (RunConfig::tol_eig, 1e-9) */
+} ksb_scf_opts;
+int ksb_scf_defaults(ksb_scf_opts* o);
+int ksb_coarse_scf(ksb_level* l, const ksb_scf_opts* o, double* h_lambda, double* d_Phi, int ld, double* d_rho_full,
+                   double* d_w_full, int* h_iterations, double* h_history, int hist_cap);
+
 /* pieces of the step, for parity checks against the reference's functions */
 /* model::density + xc_potential_field (proj/src/ks_model.cpp:43-52,101-105); d_vxc may be NULL */
 int ksb_density_xc(ksb_level* l, const double* d_Phi, int N, int ld, double* d_rho, double* d_vxc);

@@ -43,6 +43,11 @@ class StepOpts(C.Structure):
                 ("check_every", I), ("fixed_sweeps", I)]
 
 
+class ScfOpts(C.Structure):
+    _fields_ = [("tol", C.c_double), ("max_iterations", C.c_int), ("mixing", C.c_double), ("hartree_on", C.c_int),
+                ("xc_on", C.c_int), ("tol_eig", C.c_double)]
+
+
 class StepLog(C.Structure):
     _fields_ = [("inner_iterations", I), ("hartree_iterations", I), ("delta", D), ("ms_bvp", D), ("ms_hartree", D),
                 ("ms_project", D), ("ms_inner", D), ("ms_total", D), ("cg_iterations", I64)]
@@ -93,6 +98,8 @@ PROTOTYPES = {
     "ksb_solve": (I, [P, I, P, P, C.POINTER(CgOpts), P, C.POINTER(CgStats)]),
     "ksb_mat_min_diag": (I, [P, I, DP]),
     "ksb_step_defaults": (I, [SOP]),
+    "ksb_scf_defaults": (I, [C.POINTER(ScfOpts)]),
+    "ksb_coarse_scf": (I, [P, C.POINTER(ScfOpts), DP, P, I, P, P, IP, DP, I]),
     "ksb_system_set": (I, [P, DP, I, I, D, I, D, D, I, I]),
     "ksb_level_ops": (I, [P]),
     "ksb_correction_step": (I, [P, SOP, DP, P, I, P, SLP, IP, IP]),

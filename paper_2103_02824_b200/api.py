@@ -333,6 +333,23 @@ class Level:
                 "ms_inner": lg.ms_inner, "ms_total": lg.ms_total, "cg_iterations": int(lg.cg_iterations),
                 "attempts": att.tolist(), "iterations": its.tolist()}
 
+    def coarse_scf(self, tol=1e-6, max_iterations=200, mixing=0.3, hartree=True, xc=True, tol_eig=1e-9):
+        """scf::self_consistent_solve on level 0 (proj/src/scf.cpp:22-90): (lambdas, Phi, rho, w, iterations, history)."""
+        o = _N.ScfOpts()
+        check(lib.ksb_scf_defaults(C.byref(o)))
+        o.tol, o.max_iterations, o.mixing = float(tol), int(max_iterations), float(mixing)
+        o.hartree_on, o.xc_on, o.tol_eig = int(hartree), int(xc), float(tol_eig)
+        N = self.N
+        ld = N if N == 1 else N + (N & 1)
+        lam = np.empty(N)
+        Phi = self.ctx.empty((self.ni, ld))
+        rho, w = self.ctx.empty((self.n,)), self.ctx.empty((self.n,))
+        it = C.c_int()
+        hist = np.zeros(max(1, int(max_iterations)))
+        check(lib.ksb_coarse_scf(self._h, C.byref(o), _dp(lam), Phi.ptr, ld, rho.ptr, w.ptr, C.byref(it), _dp(hist),
+                                 len(hist)))
+        return lam, Phi, rho, w, it.value, hist[:it.value]
+
     def correction_step(self, lambdas: np.ndarray, Phi: DeviceArray, w: DeviceArray, ld: int | None = None, **opts):
         """One outer iteration (proj/src/driver.cpp:106-150) on device-resident state; lambdas updated in place."""
         o = self.step_options(**opts)

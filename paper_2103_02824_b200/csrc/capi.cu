@@ -659,6 +659,45 @@ int ksb_level_ops(ksb_level* l) {
     });
 }
 
+int ksb_scf_defaults(ksb_scf_opts* o) {
+    return guard([&] {
+        need(o, "null argument");
+        o->tol = 1e-6;
+        o->max_iterations = 200;
+        o->mixing = 0.3;
+        o->hartree_on = 1;
+        o->xc_on = 1;
+        o->tol_eig = 1e-9;
+    });
+}
+
+int ksb_coarse_scf(ksb_level* l, const ksb_scf_opts* o, double* h_lambda, double* d_Phi, int ld, double* d_rho,
+                   double* d_w, int* iters, double* hist, int cap) {
+    return guard([&] {
+        auto& K = ready(l);
+        need(o && h_lambda && d_Phi && d_rho && d_w, "null argument");
+        if (ld < K.sys.N || (K.sys.N > 1 && (ld & 1))) ksb::raise(KSB_INVALID_ARGUMENT, "bad block shape");
+        ksb::ScfParams p;
+        p.tol = o->tol;
+        p.max_iterations = o->max_iterations;
+        p.mixing = o->mixing;
+        p.hartree_on = o->hartree_on != 0;
+        p.xc_on = o->xc_on != 0;
+        p.tol_eig = o->tol_eig;
+        ksb::ScfStats st;
+        std::exception_ptr err;
+        try {
+            st = ksb::coarse_scf(l->L, K, l->owner->cg, p, h_lambda, d_Phi, ld, d_rho, d_w);
+        } catch (...) {
+            err = std::current_exception();
+        }
+        if (iters) *iters = st.iterations;
+        if (err) std::rethrow_exception(err);
+        if (hist)
+            for (int k = 0; k < std::min<int>(cap, int(st.history.size())); ++k) hist[k] = st.history[k];
+    });
+}
+
 int ksb_correction_step(ksb_level* l, const ksb_step_opts* o, double* h_lambda, double* d_Phi, int ld, double* d_w,
                         ksb_step_log* log, int* att, int* its) {
     return guard([&] {

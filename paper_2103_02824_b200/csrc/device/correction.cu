@@ -396,4 +396,77 @@ void correction_step(Level& L, Corrector& K, CgWork& cg, const StepOptions& o, d
     if (log) *log = lg;
 }
 
+ScfStats coarse_scf(Level& L, Corrector& K, CgWork& cg, const ScfParams& p, double* h_lambda, double* d_Phi, int ld,
+                    double* d_rho, double* d_w) {
+    Ctx& c = *L.ctx;
+    if (!K.ops_ready) level_ops(L, K);
+    const int n = L.n, ni = L.ni, N = K.sys.N;
+    if (ni != L.nH) raise(KSB_INVALID_ARGUMENT, "the coarse self-consistent solve runs on level 0");
+    need(K.rho_t, n);
+    need(K.vxc, n);
+    need(K.what_full, n);
+    need(K.diff, n);
+    need(K.bcb, std::max(1, L.nb));
+    need(K.hrhs, ni);
+    need(K.wtil_int, ni);
+    need(K.pot, ni);
+    KSB_CUDA_CHECK(cudaMemsetAsync(d_rho, 0, sizeof(double) * n, c.stream));
+    KSB_CUDA_CHECK(cudaMemsetAsync(d_w, 0, sizeof(double) * n, c.stream));
+    const double ctr[3] = {0.5 * (L.box_lo[0] + L.box_hi[0]), 0.5 * (L.box_lo[1] + L.box_hi[1]),
+                           0.5 * (L.box_lo[2] + L.box_hi[2])};
+    ScfStats st;
+    for (int iter = 1; iter <= p.max_iterations; ++iter) {
+        // potential carried by one nodal field (hartree + v_xc(rho)), proj/src/scf.cpp:42-50
+        if (p.hartree_on)
+            KSB_CUDA_CHECK(cudaMemcpyAsync(K.what_full.p, d_w, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream));
+        else
+            KSB_CUDA_CHECK(cudaMemsetAsync(K.what_full.p, 0, sizeof(double) * n, c.stream));
+        if (p.xc_on)
+            xc_field(L, K.sys.xc, d_rho, K.vxc.p);
+        else
+            KSB_CUDA_CHECK(cudaMemsetAsync(K.vxc.p, 0, sizeof(double) * n, c.stream));
+        outer_operator(L, K, K.what_full.p, K.vxc.p);
+        dense_lowest_eigs(L, K.coarse, K.inner, MAT_H, N, h_lambda, d_Phi, ld);
+        // density of the new orbitals and its H1 change (scf.cpp:67-70)
+        rho_vxc(L, d_Phi, N, ld, K.sys.occ, K.sys.xc, K.rho_t.p, nullptr);
+        launch(c, "elementwise", k_add, grid_of(c, n), kT, 0, int64_t(n), (const double*)K.rho_t.p, 1.0,
+               (const double*)d_rho, -1.0, K.diff.p);
+        const auto nn = norms_sq(L, K.diff.p, K.phys);
+        const double delta = std::sqrt(std::max(0.0, nn[0]) + std::max(0.0, nn[1]));
+        st.history.push_back(delta);
+        st.iterations = iter;
+        const double mix = (p.hartree_on || p.xc_on) ? p.mixing : 1.0;
+        launch(c, "elementwise", k_add, grid_of(c, n), kT, 0, int64_t(n), (const double*)d_rho, 1.0 - mix,
+               (const double*)K.rho_t.p, mix, d_rho);
+        if (p.hartree_on) {  // hartree::solve_hartree of the mixed density (hartree.cpp:86-106), tol = tol_eig
+            const Moments m = moments(L, d_rho, K.phys, ctr);
+            boundary_values(L, m, K.bcb.p);
+            launch(c, "elementwise", k_take_interior, grid_of(c, ni), kT, 0, ni, (const int32_t*)L.interior.p,
+                   (const double*)d_rho, K.pot.p);
+            spmm(c, L, L.mats[1].ii.p, nullptr, nullptr, K.pot.p, 1, 1, K.hrhs.p, 1);
+            launch(c, "elementwise", k_add, grid_of(c, ni), kT, 0, int64_t(ni), (const double*)K.hrhs.p, kFourPi,
+                   (const double*)K.hrhs.p, 0.0, K.hrhs.p);
+            lift(L, 0, K.bcb.p, K.hrhs.p);
+            CgOptions co;
+            co.tol = p.tol_eig;
+            CgColumnStats cs;
+            cg_solve(c, L, 0, -1, nullptr, K.hrhs.p, K.wtil_int.p, 1, 1, co, &cs, cg);
+            if (!cs.converged)
+                raise(KSB_NONCONVERGENCE, "hartree solve stalled at residual " + std::to_string(cs.relative_residual));
+            launch(c, "elementwise", k_full_from, grid_of(c, n), kT, 0, ni, L.nb, (const int32_t*)L.interior.p,
+                   (const int32_t*)L.boundary.p, (const double*)K.wtil_int.p, (const double*)K.bcb.p, d_w);
+        }
+        KSB_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+        if (delta < p.tol && iter >= 2) return st;
+    }
+    std::string msg = "self-consistent iteration exceeded " + std::to_string(p.max_iterations) +
+                      " steps; density changes:";
+    for (size_t k = st.history.size() > 6 ? st.history.size() - 6 : 0; k < st.history.size(); ++k) {
+        char b[32];
+        std::snprintf(b, sizeof b, " %g", st.history[k]);
+        msg += b;
+    }
+    raise(KSB_NONCONVERGENCE, msg);
+}
+
 }  // namespace ksb

@@ -56,6 +56,22 @@ struct Corrector {
 };
 
 void level_ops(Level& L, Corrector& K);
+
+/// scf::self_consistent_solve on level 0 (proj/src/scf.cpp:22-90): dense lowest eigenpairs of the current
+/// Hamiltonian, linear density mixing, Poisson solve for the Hartree potential of the mixed density
+struct ScfParams {
+    double tol = 1e-6;
+    int max_iterations = 200;
+    double mixing = 0.3;
+    bool hartree_on = true, xc_on = true;
+    double tol_eig = 1e-9;
+};
+struct ScfStats {
+    int iterations = 0;
+    std::vector<double> history;
+};
+ScfStats coarse_scf(Level& L, Corrector& K, CgWork& cg, const ScfParams& p, double* h_lambda, double* d_Phi, int ld,
+                    double* d_rho_full, double* d_w_full);
 void correction_step(Level& L, Corrector& K, CgWork& cg, const StepOptions& o, double* h_lambda, double* d_Phi, int ld,
                      double* d_w, StepLog* log);
 

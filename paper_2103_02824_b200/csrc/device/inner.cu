@@ -1031,6 +1031,189 @@ __global__ void k_hartree_delta(HartreeDev H) {
     if (threadIdx.x == 0) H.delta[0] = tot;
 }
 
+// ------------------------------------------------------------------------------------------
+// dense generalized eigensolve for the coarse SCF (eig::solve_smallest dense path,
+// proj/src/eigensolve.cpp:306-367): C = L^-1 A L^-T, Householder tridiagonalisation, Sturm multisection
+// for the lowest nev eigenvalues, inverse iteration + Gram-Schmidt, back-transform, normalize_sign.
+
+__device__ __forceinline__ int tri_count(int n, const double* d, const double* e, double x, double pivmin) {
+    int cnt = 0;
+    double q = 1.0;
+    for (int j = 0; j < n; ++j) {
+        double dj = d[j] - x;
+        if (j > 0) dj -= e[j - 1] * e[j - 1] / q;
+        if (fabs(dj) < pivmin) dj = -pivmin;
+        cnt += dj < 0.0;
+        q = dj;
+    }
+    return cnt;
+}
+
+/// warp k: k-th smallest eigenvalue of the symmetric tridiagonal (d, e) by 33-way multisection
+__global__ void k_tri_eig(int n, int nev, const double* __restrict__ dg, const double* __restrict__ eg,
+                          double* __restrict__ lam) {
+    extern __shared__ double she2[];
+    double* d = she2;
+    double* e = she2 + n;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        d[j] = dg[j];
+        e[j] = j + 1 < n ? eg[j] : 0.0;
+    }
+    __syncthreads();
+    const int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (k >= nev) return;
+    double lo = DBL_MAX, hi = -DBL_MAX;
+    for (int j = lane; j < n; j += 32) {
+        const double r = (j > 0 ? fabs(e[j - 1]) : 0.0) + (j + 1 < n ? fabs(e[j]) : 0.0);
+        lo = fmin(lo, d[j] - r);
+        hi = fmax(hi, d[j] + r);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    const double span = fmax(fabs(lo), fabs(hi));
+    lo -= 1e-12 * span + DBL_MIN;
+    hi += 1e-12 * span + DBL_MIN;
+    const double pivmin = DBL_MIN / DBL_EPSILON * fmax(1.0, span * span);
+    for (int it = 0; it < 60; ++it) {
+        const double w = hi - lo;
+        if (w <= 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + DBL_MIN) break;
+        const double x = lo + w * double(lane + 1) / 33.0;
+        const int cnt = tri_count(n, d, e, x, pivmin);
+        const unsigned above = __ballot_sync(0xffffffffu, cnt > k);
+        const int f = above ? __ffs(above) - 1 : 32;
+        const double nlo = f == 0 ? lo : lo + w * double(f) / 33.0;
+        const double nhi = f == 32 ? hi : lo + w * double(f + 1) / 33.0;
+        lo = nlo;
+        hi = nhi;
+    }
+    if (lane == 0) lam[k] = 0.5 * (lo + hi);
+}
+
+/// warp k: eigenvector of T at lam[k] by three inverse-iteration steps (unit norm), into Y[k*n ..]
+__global__ void k_tri_vec(int n, int nev, const double* __restrict__ d, const double* __restrict__ e,
+                          const double* __restrict__ lam, double* __restrict__ Y) {
+    extern __shared__ double shv2[];
+    const int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (k >= nev) return;
+    double* mul = shv2 + size_t(threadIdx.x >> 5) * 3 * n;
+    double* rp = mul + n;
+    double* y = rp + n;
+    if (lane == 0) {
+        const double x = lam[k];
+        double tn = 0.0;
+        for (int j = 0; j < n; ++j) tn = fmax(tn, fabs(d[j]) + (j > 0 ? fabs(e[j - 1]) : 0.0) + (j + 1 < n ? fabs(e[j]) : 0.0));
+        const double pivmin = DBL_EPSILON * fmax(tn, 1e-300);
+        double q = 1.0;
+        for (int j = 0; j < n; ++j) {
+            double dj = d[j] - x;
+            if (j > 0) dj -= (e[j - 1] / q) * e[j - 1];
+            if (fabs(dj) < pivmin) dj = dj < 0 ? -pivmin : pivmin;
+            rp[j] = dj;
+            q = dj;
+        }
+        for (int j = 0; j < n; ++j) {
+            const double r = 1.0 / rp[j];
+            mul[j] = j + 1 < n ? e[j] * r : 0.0;
+            rp[j] = r;
+        }
+        for (int j = 0; j < n; ++j) y[j] = 1.0 + 0.5 * double((j * 7919 + 31 * k) % 97) / 97.0;
+        for (int rep = 0; rep < 3; ++rep) {
+            for (int j = 1; j < n; ++j) y[j] -= mul[j - 1] * y[j - 1];
+            y[n - 1] *= rp[n - 1];
+            for (int j = n - 2; j >= 0; --j) y[j] = y[j] * rp[j] - mul[j] * y[j + 1];
+            double nn = 0.0;
+            for (int j = 0; j < n; ++j) nn += y[j] * y[j];
+            const double inv = 1.0 / sqrt(nn);
+            for (int j = 0; j < n; ++j) y[j] *= inv;
+        }
+    }
+    __syncwarp();
+    for (int j = lane; j < n; j += 32) Y[size_t(k) * n + j] = y[j];
+}
+
+/// one block: modified Gram-Schmidt over the nev vectors in ascending eigenvalue order (separates the
+/// inverse-iteration vectors of a degenerate cluster; vectors of distinct eigenvalues are already orthogonal)
+__global__ void k_mgs(int n, int nev, double* __restrict__ Y) {
+    for (int k = 0; k < nev; ++k) {
+        double* yk = Y + size_t(k) * n;
+        for (int j = 0; j < k; ++j) {
+            const double ip = block_dot(Y + size_t(j) * n, yk, n);
+            for (int a = threadIdx.x; a < n; a += blockDim.x) yk[a] -= ip * Y[size_t(j) * n + a];
+            __syncthreads();
+        }
+        const double nn = block_dot(yk, yk, n);
+        const double inv = 1.0 / sqrt(nn);
+        for (int a = threadIdx.x; a < n; a += blockDim.x) yk[a] *= inv;
+        __syncthreads();
+    }
+}
+
+/// block per vector k: x = Q y (Householder back-transform), v = L^-T x, then normalize_sign: the entry of
+/// largest magnitude (lowest index on ties) made positive (proj/src/eigensolve.cpp:306-319); v into column k
+/// of the interior block Phi (ld)
+__global__ void k_back_sign(int n, const double* __restrict__ V, const double* __restrict__ LiT,
+                            const double* __restrict__ Y, double* __restrict__ Phi, int ld) {
+    extern __shared__ double shb[];
+    double* x = shb;
+    double* v = shb + n;
+    const int k = blockIdx.x;
+    for (int a = threadIdx.x; a < n; a += blockDim.x) x[a] = Y[size_t(k) * n + a];
+    __syncthreads();
+    if (threadIdx.x < 32) apply_q_warp(n, V, x, 0);
+    __syncthreads();
+    block_gemv(n, LiT, x, v);
+    __syncthreads();
+    __shared__ double bv[32];
+    __shared__ int bi[32];
+    double best = -1.0;
+    int bidx = 0x7fffffff;
+    for (int a = threadIdx.x; a < n; a += blockDim.x) {
+        const double m = fabs(v[a]);
+        if (m > best || (m == best && a < bidx)) {
+            best = m;
+            bidx = a;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+        if (ob > best || (ob == best && oi < bidx)) {
+            best = ob;
+            bidx = oi;
+        }
+    }
+    if ((threadIdx.x & 31) == 0) {
+        bv[threadIdx.x >> 5] = best;
+        bi[threadIdx.x >> 5] = bidx;
+    }
+    __syncthreads();
+    __shared__ double sg;
+    if (threadIdx.x == 0) {
+        double b = -1.0;
+        int i = 0x7fffffff;
+        for (int w = 0; w < int(blockDim.x >> 5); ++w)
+            if (bv[w] > b || (bv[w] == b && bi[w] < i)) {
+                b = bv[w];
+                i = bi[w];
+            }
+        sg = v[i] < 0.0 ? -1.0 : 1.0;
+    }
+    __syncthreads();
+    for (int a = threadIdx.x; a < n; a += blockDim.x) Phi[size_t(a) * ld + k] = sg * v[a];
+}
+
+/// dense row-major copy of an interior CSR block
+__global__ void k_csr_dense(int n, const int32_t* __restrict__ ptr, const int32_t* __restrict__ col,
+                            const double* __restrict__ val, double* __restrict__ D) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+        double* row = D + size_t(r) * n;
+        for (int c = 0; c < n; ++c) row[c] = 0.0;
+        for (int k = ptr[r]; k < ptr[r + 1]; ++k) row[col[k]] = val[k];
+    }
+}
+
 }  // namespace
 
 // ==========================================================================================
@@ -1169,6 +1352,54 @@ void coarse_level_setup(Level& L, CoarseOps& co) {
         KSB_CUDA_CHECK(cudaStreamSynchronize(c.stream));
     }
     co.ready = true;
+}
+
+void dense_lowest_eigs(Level& L, const CoarseOps& co, InnerWork& w, int mat, int nev, double* h_lambda, double* d_Phi,
+                       int ld) {
+    Ctx& c = *L.ctx;
+    const int n = L.ni;
+    if (n != L.nH) raise(KSB_INVALID_ARGUMENT, "the dense coarse eigensolve runs on level 0");
+    if (nev < 1 || nev > n) raise(KSB_INVALID_ARGUMENT, "nev out of range");
+    const int64_t n2 = std::max<int64_t>(1, int64_t(n) * n);
+    auto need = [](DevBuf<double>& b, int64_t m) {
+        if (b.n < m) b.alloc(m);
+    };
+    need(w.AH, n2);
+    need(w.W, n2);
+    need(w.C, n2);
+    need(w.V, n2);
+    need(w.d, n + 1);
+    need(w.e, n + 1);
+    need(w.lam, nev);
+    need(w.Y, int64_t(nev) * n);
+    launch(c, "scf:dense", k_csr_dense, ceil_div(n, 128), 128, 0, n, (const int32_t*)L.ii_ptr.p,
+           (const int32_t*)L.ii_col.p, (const double*)L.mats[mat].ii.p, w.AH.p);
+    const dim3 gt(ceil_div(n, 32), ceil_div(n, 32));
+    launch(c, "scf:gemm", k_gemm_nt, gt, 256, 0, n, (const double*)co.LHi.p, (const double*)w.AH.p, w.W.p);
+    launch(c, "scf:gemm", k_gemm_nt, gt, 256, 0, n, (const double*)w.W.p, (const double*)co.LHi.p, w.C.p);
+    launch(c, "scf:symmetrize", k_symmetrize, ceil_div(int64_t(n) * n, 256), 256, 0, n, w.C.p);
+    const int cl_R = (n + kTriCluster - 1) / kTriCluster;
+    const size_t cl_smem = sizeof(double) * (size_t(cl_R) * n + (2 + 2 * kTriRep) * size_t(n));
+    if (cl_smem <= size_t(200) * 1024 && n <= 32 * kTriS) {
+        KSB_CUDA_CHECK(cudaFuncSetAttribute(k_tridiag_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            int(200 * 1024)));
+        launch(c, "scf:tridiag", k_tridiag_cluster, kTriCluster, kTriThreads, cl_smem, n, cl_R, (const double*)w.C.p,
+               w.d.p, w.e.p, w.V.p);
+    } else {
+        launch(c, "scf:tridiag", k_tridiag, 1, 1024, sizeof(double) * 2 * n, n, w.C.p, w.d.p, w.e.p, w.V.p);
+    }
+    launch(c, "scf:eig", k_tri_eig, ceil_div(nev, 4), 128, sizeof(double) * 2 * n, n, nev, (const double*)w.d.p,
+           (const double*)w.e.p, w.lam.p);
+    const size_t vsm = sizeof(double) * 4 * 3 * size_t(n);
+    if (vsm > 48 * 1024)
+        KSB_CUDA_CHECK(cudaFuncSetAttribute(k_tri_vec, cudaFuncAttributeMaxDynamicSharedMemorySize, int(vsm)));
+    launch(c, "scf:vec", k_tri_vec, ceil_div(nev, 4), 128, vsm, n, nev, (const double*)w.d.p, (const double*)w.e.p,
+           (const double*)w.lam.p, w.Y.p);
+    launch(c, "scf:mgs", k_mgs, 1, 256, 0, n, nev, w.Y.p);
+    launch(c, "scf:back", k_back_sign, nev, 256, sizeof(double) * 2 * n, n, (const double*)w.V.p,
+           (const double*)co.LHiT.p, (const double*)w.Y.p, d_Phi, ld);
+    KSB_CUDA_CHECK(cudaMemcpyAsync(h_lambda, w.lam.p, sizeof(double) * nev, cudaMemcpyDeviceToHost, c.stream));
+    KSB_CUDA_CHECK(cudaStreamSynchronize(c.stream));
 }
 
 InnerStats inner_scf(Level& L, const CoarseOps& co, const ProjOut& P, const InnerParams& prm, const double* h_lambda,

@@ -39,6 +39,12 @@ struct InnerWork {
     void ensure(int nh, int N, int nev, int nct);
 };
 
+/// lowest nev eigenpairs of (A_ii(mat), M_H) on level 0 (dense path of eig::solve_smallest,
+/// proj/src/eigensolve.cpp:321-367): ascending values to h_lambda, M-orthonormal sign-normalised vectors into
+/// the interior block d_Phi (ld)
+void dense_lowest_eigs(Level& L, const CoarseOps& co, InnerWork& w, int mat, int nev, double* h_lambda, double* d_Phi,
+                       int ld);
+
 /// runs sweeps from the pure augmentation state (phi_H = 0, theta2 = 1, w_H = 0, theta1 = hartree)
 InnerStats inner_scf(Level& L, const CoarseOps& co, const ProjOut& P, const InnerParams& prm, const double* h_lambda,
                      InnerWork& w, bool start_pure = true);
