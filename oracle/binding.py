@@ -61,6 +61,7 @@ _PROTO = {
     "orc_hartree_exact": (I, [P, I, DP, I, DP, D, DP, IP]),
     "orc_energy": (I, [P, I, DP, I, DP, DP]),
     "orc_indicators": (I, [P, I, DP, DP, I, DP, DP, DP, DP]),
+    "orc_last_scf_rho": (I, [P, DP]),
     "orc_dorfler": (I, [DP, I64, D, D, IP, C.POINTER(C.c_int64)]),
     "orc_norms": (I, [P, I, DP, DP]),
     "orc_prolong_vec": (I, [P, I, I, DP, I, DP]),
@@ -324,6 +325,12 @@ class Oracle:
         it = C.c_int()
         _chk(lib.orc_coarse_scf(self._h, tol, max_it, mixing, tol_eig, dp(lam), dp(orb), dp(w), C.byref(it)))
         return lam, orb, w, it.value
+
+    def last_scf_rho(self):
+        """mixed density of the last coarse_scf (ScfResult::rho, proj/src/scf.cpp:73)"""
+        out = np.empty(self.n(0))
+        _chk(lib.orc_last_scf_rho(self._h, dp(out)))
+        return out
 
     def correction_step(self, level, lambdas, orb, w, tol_linear=1e-9, tol_inner=1e-8, score_floor=1e-8,
                         max_inner=400, nev_pad=4, precond=0):

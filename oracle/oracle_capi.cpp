@@ -62,6 +62,7 @@ struct orc_mesh {
 };
 struct orc_problem {
     Problem p;
+    Vec last_scf_rho;
 };
 struct orc_operator {
     std::unique_ptr<Elliptic> E;
@@ -454,7 +455,12 @@ int orc_coarse_scf(orc_problem* p, double tol, int max_it, double mixing, double
         pack(r.orbitals, orb);
         std::memcpy(hartree, r.hartree.data(), sizeof(double) * r.hartree.size());
         if (iters) *iters = r.iterations;
+        p->last_scf_rho = r.rho;
     });
+}
+/// mixed density of the last orc_coarse_scf (ScfResult::rho, proj/src/scf.cpp:73)
+int orc_last_scf_rho(orc_problem* p, double* rho) {
+    return guard([&] { std::memcpy(rho, p->last_scf_rho.data(), sizeof(double) * p->last_scf_rho.size()); });
 }
 
 /// cfg_d: tol_linear, tol_inner, score_floor; cfg_i: max_inner, nev_pad, precond

@@ -313,6 +313,8 @@ class Level:
         check(lib.ksb_system_set(self._h, _dp(a.reshape(-1)), a.shape[0], int(n_pairs), float(occupancy),
                                  self.XC[xc], float(alpha), float(exchange_exponent), int(hartree), int(xc_on)))
         self.N = int(n_pairs)
+        self.occ = float(occupancy)
+        self.xc = (self.XC[xc] if xc_on else 0, float(alpha), float(exchange_exponent))
 
     def level_ops(self):
         """make_level_ops (proj/src/driver.cpp:35-47)."""
@@ -373,6 +375,14 @@ class Level:
     def density_xc(self, Phi: DeviceArray, rho: DeviceArray, vxc: DeviceArray | None = None, N=None, ld=None):
         check(lib.ksb_density_xc(self._h, Phi.ptr, int(N or self.N), int(ld or Phi.shape[1]), rho.ptr,
                                  vxc.ptr if vxc is not None else None))
+
+    def xc_field(self, rho: DeviceArray, vxc: DeviceArray):
+        """model::xc_potential_field (proj/src/ks_model.cpp:101-105) with the level's functional."""
+        kind, alpha, p = self.xc
+        check(lib.ksb_xc_field(self._h, kind, alpha, p, rho.ptr, vxc.ptr))
+
+    def density(self, Phi: DeviceArray, rho: DeviceArray, N=None, ld=None):
+        check(lib.ksb_density(self._h, Phi.ptr, int(N or self.N), int(ld or Phi.shape[1]), self.occ, rho.ptr))
 
     def moments(self, rho: DeviceArray) -> np.ndarray:
         out = np.empty(16)

@@ -1,4 +1,4 @@
-"""Level driver around the device correction step.
+"""Level driver around the device correction step, and the accelerated adaptive run.
 
 solve_level_corrected mirrors the reference's outer loop (proj/src/driver.cpp:94-163): one
 correction step per outer iteration until the H1 norm of the density change drops below
@@ -70,3 +70,103 @@ def solve_level_corrected(L: api.Level, lambdas: np.ndarray, Phi: api.DeviceArra
         if lg["delta"] < tol_outer:
             return res
     raise KsbError(1, f"nonconvergence: outer iteration cap reached on level {level}")
+
+
+@dataclass
+class LevelRecord:
+    """driver::LevelRecord (proj/include/ksafem/driver.hpp:12-23)"""
+    level: int
+    n_tets: int
+    n_dofs: int
+    lambdas: list
+    energy: list  # kinetic, external, hartree, xc, total
+    eta_sq_total: float
+    outer_iterations: int
+    inner_iterations: list
+    t_refine: float
+    t_solve: float
+    t_estimate: float
+    t_total: float
+
+
+@dataclass
+class RunLog:
+    records: list = field(default_factory=list)
+    aborted: bool = False
+    abort_reason: str = ""
+    wall_seconds: float = 0.0
+
+
+def run(ctx: api.Context, atoms, n_pairs: int, occupancy: float, xc: str, box: float, n_coarse: int, max_levels: int,
+        refine: str = "adaptive", theta: float = 0.4, tol_outer: float = 1e-6, mixing: float = 0.3, max_scf: int = 200,
+        tol_eig: float = 1e-9, max_outer: int = 40, **step_opts) -> RunLog:
+    """driver::run in accelerated mode (proj/src/driver.cpp:306-435), all solves on the device: coarse SCF on
+    level 0, then per level Doerfler marks of the residual indicators (or uniform refinement, as BASELINE's
+    cfg1 prescribes), nested warm start, solve_level_corrected, indicators. Errors abort the run like the
+    reference (RunLog.aborted, abort_reason)."""
+    import time
+
+    t_start = time.perf_counter()
+    log = RunLog()
+    h = api.Hierarchy()
+    mesh = api.Mesh.box([-box] * 3, [box] * 3, n_coarse)
+    h.push(mesh)
+    lam = orb_full = w_full = None
+    eta = tot = None
+    L = None
+    try:
+        for level in range(max_levels):
+            t_level = time.perf_counter()
+            t0 = time.perf_counter()
+            if level > 0:
+                if refine == "uniform":
+                    mesh = mesh.uniform_refine()
+                else:
+                    mesh = mesh.adapt_refine(api.dorfler_mark(eta, tot, theta))
+                h.push(mesh)
+            if L is not None:
+                L.close()
+            L = api.Level(ctx, h, level)
+            L.set_system(atoms, n_pairs=n_pairs, occupancy=occupancy, xc=xc)
+            L.level_ops()
+            it = L.index("interior")
+            t_refine = time.perf_counter() - t0
+            t1 = time.perf_counter()
+            if level == 0:
+                lam, Phi, rho, w, scf_it, _ = L.coarse_scf(tol=tol_outer, max_iterations=max_scf, mixing=mixing,
+                                                           tol_eig=tol_eig)
+                outer, inner = scf_it, []
+            else:
+                orb_full = prolong(mesh, orb_full)
+                w_full = prolong(mesh, w_full)
+                ld = n_pairs if n_pairs == 1 else n_pairs + (n_pairs & 1)
+                blk = np.zeros((L.ni, ld))
+                blk[:, :n_pairs] = orb_full[it]
+                Phi, w = ctx.to_device(blk), ctx.to_device(w_full)
+                res = solve_level_corrected(L, lam, Phi, w, tol_outer=tol_outer, max_outer=max_outer, level=level,
+                                            **step_opts)
+                outer, inner = res.outer_iterations, res.inner_iterations
+                rho = ctx.empty((L.n,))
+                L.density(Phi, rho)
+            t_solve = time.perf_counter() - t1
+            t2 = time.perf_counter()
+            vxc = ctx.empty((L.n,))
+            L.xc_field(rho, vxc)
+            eta, tot = L.indicators(lam, Phi, w, vxc)
+            t_estimate = time.perf_counter() - t2
+            energy = L.energy(Phi, w)
+            P = Phi.download()
+            orb_full = np.zeros((L.n, n_pairs))
+            orb_full[it] = P[:, :n_pairs]
+            w_full = w.download()
+            log.records.append(LevelRecord(level, L.nt, L.n, np.asarray(lam).tolist(), np.asarray(energy).tolist(),
+                                           float(tot), outer, inner, t_refine, t_solve, t_estimate,
+                                           time.perf_counter() - t_level))
+    except KsbError as e:
+        log.aborted = True
+        log.abort_reason = str(e)
+    finally:
+        if L is not None:
+            L.close()
+    log.wall_seconds = time.perf_counter() - t_start
+    return log
