@@ -4,6 +4,7 @@
 
 #include "ksafem_b200/correction.hpp"
 #include "ksafem_b200/estimator.hpp"
+#include "ksafem_b200/scf.hpp"
 
 namespace ksafem::driver {
 
@@ -67,5 +68,46 @@ struct LevelResult {
 LevelResult solve_level_corrected(const LevelOps& ops, const model::MolecularSystem& sys, const StepOptions& opt,
                                   const VecX& lambdas, const std::vector<fem::FEFunction>& orbitals,
                                   const fem::FEFunction& w, double tol_outer = 1e-6, int max_outer = 40);
+
+/// the adaptive run in accelerated mode (proj/src/driver.cpp:306-435); refinement by Doerfler marks of the
+/// residual indicators, or uniform (BASELINE's cfg1) when `uniform` is set
+struct RunConfig {
+    model::MolecularSystem system;
+    int n_coarse = 16;
+    int max_levels = 8;
+    double theta = 0.4;
+    double tol_outer = 1e-6;
+    double tol_inner = 1e-8;
+    double tol_linear = 1e-9;
+    double tol_eig = 1e-9;
+    double mixing = 0.3;
+    int max_outer = 40;
+    int max_inner = 400;
+    int max_scf = 200;
+    double score_floor = 1e-8;
+    int nev_scan_pad = 4;
+    bool uniform = false;
+};
+
+struct LevelRecord {
+    int level = 0;
+    int n_tets = 0;
+    int n_dofs = 0;
+    VecX lambdas;
+    model::EnergyBreakdown energy;
+    double eta_sq_total = 0;
+    int outer_iterations = 0;
+    std::vector<int> inner_iterations;
+    double t_solve = 0, t_estimate = 0, t_refine = 0, t_total = 0;
+};
+
+struct RunLog {
+    std::vector<LevelRecord> records;
+    bool aborted = false;
+    std::string abort_reason;
+    double wall_seconds = 0;
+};
+
+RunLog run(const RunConfig& cfg);
 
 } // namespace ksafem::driver

@@ -14,6 +14,7 @@
 //   expand                                                 include/ksafem/correction.hpp:21-172
 //   driver make_level_ops / solve_level_corrected          src/driver.cpp:35-47, 94-163
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -906,6 +907,51 @@ Expanded expand(const AugmentedState& s, const AugmentedBlocks& blocks) {
 
 } // namespace corr
 
+// ------------------------------------------------------------------ scf
+namespace scf {
+
+ScfResult self_consistent_solve(const model::MolecularSystem& sys, fem::SpacePtr space, const ScfOptions& opt,
+                                WorkerPool*) {
+    sys.validate();
+    if (!space || space->state()->level != 0 || space->n_interior() != space->state()->nH)
+        fail("invalid-argument", "the device coarse solve runs on level 0 of a hierarchy");
+    if (opt.norm_l1) fail("invalid-argument", "only the H1 density-change norm is available on the device");
+    const auto& V = *space;
+    model::set_system(V, sys, opt.hartree_on, opt.xc_on && sys.xc.kind != model::XcKind::none);
+    ksb_scf_opts o;
+    b200::check(ksb_scf_defaults(&o));
+    o.tol = opt.tol;
+    o.max_iterations = opt.max_iterations;
+    o.mixing = opt.mixing;
+    o.hartree_on = opt.hartree_on ? 1 : 0;
+    o.xc_on = opt.xc_on ? 1 : 0;
+    o.tol_eig = opt.tol_eig;
+    const int N = sys.n_pairs, ld = N == 1 ? 1 : N + (N & 1);
+    auto& dev = V.device();
+    b200::DeviceBuffer phi(dev, int64_t(V.n_interior()) * ld), rho(dev, int64_t(V.n_dofs())),
+        w(dev, int64_t(V.n_dofs()));
+    ScfResult r;
+    r.lambdas.assign(size_t(N), 0.0);
+    VecX hist(size_t(std::max(1, opt.max_iterations)), 0.0);
+    int it = 0;
+    b200::check(ksb_coarse_scf(V.device_level(), &o, r.lambdas.data(), phi.data(), ld, rho.data(), w.data(), &it,
+                               hist.data(), int(hist.size())));
+    r.iterations = it;
+    r.history.assign(hist.begin(), hist.begin() + it);
+    r.orbitals = fem::from_block(space, phi.to_host(), N, ld, fem::Role::wavefunction);
+    r.rho = fem::FEFunction(space, rho.to_host(), fem::Role::density);
+    r.hartree = fem::FEFunction(space, w.to_host(), fem::Role::hartree);
+    return r;
+}
+
+ScfResult initial_coarse_solve(const model::MolecularSystem& sys, fem::SpacePtr space, double scf_tol, ScfOptions opt,
+                               WorkerPool* pool) {
+    opt.tol = scf_tol;
+    return self_consistent_solve(sys, std::move(space), opt, pool);
+}
+
+} // namespace scf
+
 // ------------------------------------------------------------------ estimator
 namespace est {
 
@@ -992,6 +1038,84 @@ std::vector<fem::FEFunction> CorrectionState::orbitals() const {
     return fem::from_block(space_, phi_.to_host(), N_, ld_, fem::Role::wavefunction);
 }
 fem::FEFunction CorrectionState::hartree() const { return fem::FEFunction(space_, w_.to_host(), fem::Role::hartree); }
+
+RunLog run(const RunConfig& cfg) {
+    using Clock = std::chrono::steady_clock;
+    auto secs = [](Clock::time_point t) { return std::chrono::duration<double>(Clock::now() - t).count(); };
+    const auto t_start = Clock::now();
+    RunLog log;
+    const auto& sys = cfg.system;
+    fem::SpaceHierarchy hier;
+    mesh::MeshPtr m = mesh::build_box_mesh(sys.domain, cfg.n_coarse);
+    hier.push(m);
+    VecX lam;
+    std::vector<fem::FEFunction> orbs;
+    fem::FEFunction w, rho;
+    est::Indicators ind;
+    StepOptions so;
+    so.tol_linear = cfg.tol_linear;
+    so.tol_inner = cfg.tol_inner;
+    so.score_floor = cfg.score_floor;
+    so.max_inner = cfg.max_inner;
+    so.nev_scan_pad = cfg.nev_scan_pad;
+    try {
+        for (int level = 0; level < cfg.max_levels; ++level) {
+            LevelRecord rec;
+            rec.level = level;
+            const auto t_level = Clock::now();
+            auto t0 = Clock::now();
+            if (level > 0) {
+                m = cfg.uniform ? mesh::uniform_refine(*m) : mesh::adapt_refine(*m, est::dorfler_mark(ind, cfg.theta));
+                hier.push(m);
+            }
+            const LevelOps ops = make_level_ops(hier, level, sys);
+            rec.t_refine = secs(t0);
+            t0 = Clock::now();
+            if (level == 0) {
+                scf::ScfOptions opt;
+                opt.tol = cfg.tol_outer;
+                opt.max_iterations = cfg.max_scf;
+                opt.mixing = cfg.mixing;
+                opt.tol_eig = cfg.tol_eig;
+                const auto r = scf::initial_coarse_solve(sys, hier.space(0), cfg.tol_outer, opt);
+                rec.outer_iterations = r.iterations;
+                lam = r.lambdas;
+                orbs = r.orbitals;
+                w = r.hartree;
+                rho = r.rho;
+            } else {
+                std::vector<fem::FEFunction> warm;
+                for (const auto& o : orbs) warm.push_back(hier.prolong(o, level));
+                const auto res = solve_level_corrected(ops, sys, so, lam, warm, hier.prolong(w, level),
+                                                       cfg.tol_outer, cfg.max_outer);
+                lam = res.lambdas;
+                orbs = res.orbitals;
+                w = res.hartree;
+                rho = model::density(orbs, sys.occupancy);
+                rec.outer_iterations = res.outer_iterations;
+                rec.inner_iterations = res.inner_iterations;
+            }
+            rec.t_solve = secs(t0);
+            t0 = Clock::now();
+            const auto vxc = sys.xc.kind == model::XcKind::none ? fem::FEFunction(ops.space)
+                                                                : model::xc_potential_field(sys.xc, rho);
+            ind = est::compute_indicators(*ops.space, sys, lam, orbs, w, vxc);
+            rec.t_estimate = secs(t0);
+            rec.n_tets = m->n_tets();
+            rec.n_dofs = ops.space->n_dofs();
+            rec.lambdas = lam;
+            rec.energy = model::total_energy(sys, orbs, w);
+            rec.eta_sq_total = ind.total_sq;
+            rec.t_total = secs(t_level);
+            log.records.push_back(rec);
+        }
+    } catch (const Error& e) {
+        log.aborted = true;
+        log.abort_reason = e.what();
+    }
+    log.wall_seconds = secs(t_start);
+    return log;
+}
 
 LevelResult solve_level_corrected(const LevelOps& ops, const model::MolecularSystem& sys, const StepOptions& opt,
                                   const VecX& lambdas, const std::vector<fem::FEFunction>& orbitals,

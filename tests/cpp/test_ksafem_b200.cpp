@@ -427,6 +427,37 @@ TEST_CASE("solve_level_corrected converges from a hydrogenic start", t_driver) {
     std::printf("  level-1 He: lambda %.10f, E %.10f, %d outer steps\n", res.lambdas[0], e.total, res.outer_iterations);
 }
 
+// ---------------------------------------------------------------- scf + run (scf.cpp, driver.cpp:306-435)
+TEST_CASE("coarse SCF of cfg1 and the adaptive run", t_run) {
+    model::MolecularSystem sys;
+    sys.atoms.push_back({2.0, Vec3()});
+    sys.n_pairs = 1;
+    sys.occupancy = 2.0;
+    sys.domain = cube(-10, 10);
+    sys.xc.kind = model::XcKind::lda_pz81;
+    fem::SpaceHierarchy hier;
+    hier.push(mesh::build_box_mesh(sys.domain, 8));
+    const auto r = scf::initial_coarse_solve(sys, hier.space(0), 1e-6);
+    // the oracle's coarse SCF of cfg1 (tests/golden/cfg1_oracle_trajectory.json via tests/cfg1_oracle.py)
+    CHECK(r.iterations == 37);
+    CHECK(std::fabs(r.lambdas[0] - (-0.00526096437936834)) < 1e-8 * 0.0053 + 1e-14);
+    std::printf("  cfg1 coarse SCF: %d iterations, lambda %.14f\n", r.iterations, r.lambdas[0]);
+
+    driver::RunConfig cfg;
+    cfg.system = sys;
+    cfg.system.domain = cube(-6, 6);
+    cfg.system.atoms[0].position = Vec3(0.3, -0.2, 0.1);
+    cfg.n_coarse = 4;
+    cfg.max_levels = 4;
+    const auto log = driver::run(cfg);
+    CHECK(!log.aborted);
+    CHECK(log.records.size() == 4);
+    for (size_t k = 1; k < log.records.size(); ++k) CHECK(log.records[k].n_dofs >= log.records[k - 1].n_dofs);
+    for (const auto& rec : log.records)
+        std::printf("  level %d: %d dofs, lambda %.10f, E %.10f, eta^2 %.6e\n", rec.level, rec.n_dofs, rec.lambdas[0],
+                    rec.energy.total, rec.eta_sq_total);
+}
+
 int main(int argc, char** argv) {
     const char* filter = argc > 1 ? argv[1] : nullptr;
     if (filter && std::strcmp(filter, "--list") == 0) {
