@@ -280,6 +280,49 @@ def correction_bench(args, ctx, stream, rank, world):
     return out
 
 
+# ----------------------------------------------------------------------------------- cfg1 run (levels 0-2)
+RUN_LEVELS = 3  # coarse SCF + levels 1 and 2; on level 3 the reference algorithm itself stalls
+
+
+def cfg1_run_cpu():
+    """The same run composed from the oracle's pieces (reference algorithm) on the host cores."""
+    from oracle import OMesh, Oracle
+    t = time.perf_counter()
+    orc = Oracle(HE, n_pairs=1, occ=2.0, xc="lda")
+    m = OMesh.box([-BOX] * 3, [BOX] * 3, 8)
+    orc.push(m)
+    lam, orb, w, _ = orc.coarse_scf(tol=1e-6, mixing=0.3, tol_eig=1e-9)
+    for level in range(1, RUN_LEVELS):
+        m = m.uniform_refine()
+        orc.push(m)
+        orb = orc.prolong(orb, level - 1, level)
+        w = orc.prolong(w, level - 1, level)[:, 0]
+        for _ in range(40):
+            lam, orb, w, lg = orc.correction_step(level, lam, orb, w)
+            if lg["delta"] < 1e-6:
+                break
+    return time.perf_counter() - t, float(lam[0])
+
+
+def cfg1_run_bench(args, ctx, rank, world):
+    from paper_2103_02824_b200.driver import run
+    run(ctx, HE, 1, 2.0, "lda", BOX, 8, 2, refine="uniform")  # warm-up: kernel caches, first-use allocations
+    t = time.perf_counter()
+    log = run(ctx, HE, 1, 2.0, "lda", BOX, 8, RUN_LEVELS, refine="uniform")
+    wall = time.perf_counter() - t
+    out = {"workload": "cfg1 (configs[0]) run from scratch on the device: coarse SCF on 8^3, uniform levels 1-2, "
+                       "corrected level solves to tol_outer 1e-6, indicators per level",
+           "wall_s": max_over_ranks(wall, world), "aborted": log.aborted,
+           "levels": [{"level": r.level, "n_dofs": r.n_dofs, "lambda": r.lambdas[0], "energy": r.energy[4],
+                       "outer": r.outer_iterations, "t_total_s": round(r.t_total, 4)} for r in log.records]}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cw, clam = cfg1_run_cpu()
+        out["cpu_baseline"] = {"wall_s": cw, "kind": "port", "cores": os.cpu_count() or 1,
+                               "sample": f"the same run from the oracle's pieces (SGS-PCG, dense eigensolves); "
+                                         f"final lambda {clam:.12f}"}
+    return out
+
+
 # ----------------------------------------------------------------------------------- GPU leg
 def run_b200(args, world, rank, local):
     import torch
@@ -356,6 +399,7 @@ def run_b200(args, world, rank, local):
     e2e = world * ni * N_RHS * ITERS / (e2e_ms * 1e-3)
 
     correction = correction_bench(args, ctx, stream, rank, world)
+    cfg1_run = cfg1_run_bench(args, ctx, rank, world)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -388,6 +432,7 @@ def run_b200(args, world, rank, local):
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
             "correction_step": correction,
+            "cfg1_run": cfg1_run,
         }
         print(json.dumps(line), flush=True)
     L.close()
