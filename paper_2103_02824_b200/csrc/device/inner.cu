@@ -257,6 +257,7 @@ constexpr int kTriS = 12;  // register slots per lane: n <= 384
 /// applies the per-step rank-2 updates to its replica locally, so the next pivot row is always local.
 /// p and the replica are double-buffered, which makes the single barrier safe.
 constexpr int kTriThreads = 256;
+constexpr int kMaxDynSmem = 227 * 1024;  // sm_100 per-block opt-in shared memory
 constexpr int kTriRep = kTriThreads / 32;  // one replica row per warp
 
 __global__ void __cluster_dims__(kTriCluster, 1, 1) __launch_bounds__(kTriThreads, 1)
@@ -709,84 +710,111 @@ __global__ void k_orbital_border(SweepDev S) {
     }
 }
 
-/// inertia of [T - x, c; c^T, c22 - x]: number of eigenvalues < x (Sylvester)
-__device__ __forceinline__ int arrow_count(int n, const double* __restrict__ d, const double* __restrict__ e,
-                                           const double* __restrict__ c, double c22, double x, double pivmin) {
-    // one reciprocal per step on the dependency chain (it also serves the border term)
-    int cnt = 0;
-    double rq = 0.0, z = 0.0, acc = 0.0;
-    for (int j = 0; j < n; ++j) {
-        double dj = d[j] - x;
-        double zj = c[j];
-        if (j > 0) {
-            const double l = e[j - 1] * rq;
-            dj -= l * e[j - 1];
-            zj -= l * z;
-        }
-        if (fabs(dj) < pivmin) dj = -pivmin;
-        cnt += dj < 0.0;
-        rq = 1.0 / dj;
-        acc += zj * zj * rq;
-        z = zj;
-    }
-    const double s = (c22 - x) - acc;
-    return cnt + (s < 0.0 ? 1 : 0);
-}
+/// inertia of [T - x, c; c^T, c22 - x]: number of eigenvalues < x (Sylvester), one LDL^T pass with one
+/// reciprocal per step on the dependency chain -- evaluated inline, two points per lane, in k_arrow_eig.
+/// block per (orbital, k): k-th smallest eigenvalue by 513-way multisection -- 8 warps x 32 lanes x 2 points
+/// per lane (two independent Sturm recurrences interleaved per lane), so an iteration gains 9 bits and the
+/// eigenvalue needs ~7 iterations of the 343-step dependency chain instead of ~12 with one warp.
+constexpr int kEigWarps = 8;
 
-/// warp per (orbital, k): k-th smallest eigenvalue by 32-way multisection
-__global__ void k_arrow_eig(int nh, int N, int nev, const double* __restrict__ dg, const double* __restrict__ eg,
-                            const double* __restrict__ c12, const double* __restrict__ c22, double* __restrict__ lam) {
-    // T and the border in shared memory: the Sturm recurrence re-reads them on every multisection step
+__global__ void __launch_bounds__(kEigWarps * 32) k_arrow_eig(int nh, int N, int nev, const double* __restrict__ dg,
+                                                              const double* __restrict__ eg,
+                                                              const double* __restrict__ c12,
+                                                              const double* __restrict__ c22,
+                                                              double* __restrict__ lam) {
     extern __shared__ double she[];
     double* d = she;
     double* e = she + nh;
+    double* c = she + 2 * nh;
+    __shared__ int first_above[kEigWarps];
+    __shared__ double bounds[2];
     const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    double* c = she + 2 * nh + size_t(wib) * nh;
-    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int item = blockIdx.x;  // (orbital, k)
+    const int i = item / nev, k = item % nev;
     for (int j = threadIdx.x; j < nh; j += blockDim.x) {
         d[j] = dg[j];
         e[j] = eg[j];
+        c[j] = c12[size_t(i) * nh + j];
     }
-    const bool live = warp < N * nev;
-    const int i = live ? warp / nev : 0, k = live ? warp % nev : 0;
-    if (live)
-        for (int j = lane; j < nh; j += 32) c[j] = c12[size_t(i) * nh + j];
     __syncthreads();
-    if (!live) return;
     const double cc = c22[i];
-    // Gershgorin bounds
-    double lo = DBL_MAX, hi = -DBL_MAX, csum = 0.0;
-    for (int j = lane; j < nh; j += 32) {
-        const double r = (j > 0 ? fabs(e[j - 1]) : 0.0) + (j + 1 < nh ? fabs(e[j]) : 0.0) + fabs(c[j]);
-        lo = fmin(lo, d[j] - r);
-        hi = fmax(hi, d[j] + r);
-        csum += fabs(c[j]);
+    if (threadIdx.x < 32) {  // Gershgorin bounds
+        double lo = DBL_MAX, hi = -DBL_MAX, csum = 0.0;
+        for (int j = lane; j < nh; j += 32) {
+            const double r = (j > 0 ? fabs(e[j - 1]) : 0.0) + (j + 1 < nh ? fabs(e[j]) : 0.0) + fabs(c[j]);
+            lo = fmin(lo, d[j] - r);
+            hi = fmax(hi, d[j] + r);
+            csum += fabs(c[j]);
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        }
+        csum = warp_sum(csum);
+        lo = fmin(lo, cc - csum);
+        hi = fmax(hi, cc + csum);
+        const double span = fmax(fabs(lo), fabs(hi));
+        if (lane == 0) {
+            bounds[0] = lo - (1e-12 * span + DBL_MIN);
+            bounds[1] = hi + (1e-12 * span + DBL_MIN);
+        }
     }
-    for (int o = 16; o > 0; o >>= 1) {
-        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-    }
-    csum = warp_sum(csum);
-    lo = fmin(lo, cc - csum);
-    hi = fmax(hi, cc + csum);
+    __syncthreads();
+    double lo = bounds[0], hi = bounds[1];
     const double span = fmax(fabs(lo), fabs(hi));
-    lo -= 1e-12 * span + DBL_MIN;
-    hi += 1e-12 * span + DBL_MIN;
     const double pivmin = DBL_MIN / DBL_EPSILON * fmax(1.0, span * span);
+    constexpr int P = kEigWarps * 64;  // evaluation points; point index p = 2 * (32 wib + lane) + h
     for (int it = 0; it < 40; ++it) {
         const double w = hi - lo;
         if (w <= 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + DBL_MIN) break;
-        const double x = lo + w * double(lane + 1) / 33.0;
-        const int cnt = arrow_count(nh, d, e, c, cc, x, pivmin);
-        // first lane whose count exceeds k bounds the eigenvalue from above
-        const unsigned above = __ballot_sync(0xffffffffu, cnt > k);
-        const int f = above ? __ffs(above) - 1 : 32;  // lanes 0..f-1 have count <= k
-        const double nlo = f == 0 ? lo : lo + w * double(f) / 33.0;
-        const double nhi = f == 32 ? hi : lo + w * double(f + 1) / 33.0;
+        const int p0 = 2 * (32 * wib + lane);
+        const double x0 = lo + w * double(p0 + 1) / double(P + 1);
+        const double x1 = lo + w * double(p0 + 2) / double(P + 1);
+        // two interleaved Sturm recurrences (arrow_count at x0 and x1)
+        int cnt0 = 0, cnt1 = 0;
+        double rq0 = 0.0, rq1 = 0.0, z0 = 0.0, z1 = 0.0, acc0 = 0.0, acc1 = 0.0;
+        for (int j = 0; j < nh; ++j) {
+            const double dj = d[j], cj = c[j];
+            double a0 = dj - x0, a1 = dj - x1, b0 = cj, b1 = cj;
+            if (j > 0) {
+                const double ej = e[j - 1];
+                const double l0 = ej * rq0, l1 = ej * rq1;
+                a0 -= l0 * ej;
+                a1 -= l1 * ej;
+                b0 -= l0 * z0;
+                b1 -= l1 * z1;
+            }
+            if (fabs(a0) < pivmin) a0 = -pivmin;
+            if (fabs(a1) < pivmin) a1 = -pivmin;
+            cnt0 += a0 < 0.0;
+            cnt1 += a1 < 0.0;
+            rq0 = 1.0 / a0;
+            rq1 = 1.0 / a1;
+            acc0 += b0 * b0 * rq0;
+            acc1 += b1 * b1 * rq1;
+            z0 = b0;
+            z1 = b1;
+        }
+        cnt0 += ((cc - x0) - acc0) < 0.0 ? 1 : 0;
+        cnt1 += ((cc - x1) - acc1) < 0.0 ? 1 : 0;
+        // first point whose count exceeds k: counts are monotone in x
+        const unsigned a0m = __ballot_sync(0xffffffffu, cnt0 > k), a1m = __ballot_sync(0xffffffffu, cnt1 > k);
+        int f = P;  // first point index above, this warp
+        if (a0m || a1m) {
+            const int l0 = a0m ? __ffs(a0m) - 1 : 32, l1 = a1m ? __ffs(a1m) - 1 : 32;
+            f = min(l0 < 32 ? 2 * (32 * wib + l0) : P, l1 < 32 ? 2 * (32 * wib + l1) + 1 : P);
+        }
+        if (lane == 0) first_above[wib] = f;
+        __syncthreads();
+        int fa = P;
+        for (int q = 0; q < kEigWarps; ++q) fa = min(fa, first_above[q]);
+        __syncthreads();
+        const double nlo = fa == 0 ? lo : lo + w * double(fa) / double(P + 1);
+        const double nhi = fa == P ? hi : lo + w * double(fa + 1) / double(P + 1);
         lo = nlo;
         hi = nhi;
     }
-    if (lane == 0) lam[warp] = 0.5 * (lo + hi);
+    if (threadIdx.x == 0) lam[item] = 0.5 * (lo + hi);
 }
 
 /// warp per (orbital, k): eigenvector of the arrow-tridiagonal [T c; c^T c22] at the computed eigenvalue by two
@@ -1380,9 +1408,9 @@ void dense_lowest_eigs(Level& L, const CoarseOps& co, InnerWork& w, int mat, int
     launch(c, "scf:symmetrize", k_symmetrize, ceil_div(int64_t(n) * n, 256), 256, 0, n, w.C.p);
     const int cl_R = (n + kTriCluster - 1) / kTriCluster;
     const size_t cl_smem = sizeof(double) * (size_t(cl_R) * n + (2 + 2 * kTriRep) * size_t(n));
-    if (cl_smem <= size_t(200) * 1024 && n <= 32 * kTriS) {
+    if (cl_smem <= size_t(kMaxDynSmem) && n <= 32 * kTriS) {
         KSB_CUDA_CHECK(cudaFuncSetAttribute(k_tridiag_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            int(200 * 1024)));
+                                            int(kMaxDynSmem)));
         launch(c, "scf:tridiag", k_tridiag_cluster, kTriCluster, kTriThreads, cl_smem, n, cl_R, (const double*)w.C.p,
                w.d.p, w.e.p, w.V.p);
     } else {
@@ -1448,14 +1476,14 @@ InnerStats inner_scf(Level& L, const CoarseOps& co, const ProjOut& P, const Inne
     const size_t tri_smem = sizeof(double) * 2 * nh;
     const int cl_R = (nh + kTriCluster - 1) / kTriCluster;
     const size_t cl_smem = sizeof(double) * (size_t(cl_R) * nh + (2 + 2 * kTriRep) * size_t(nh));
-    const bool use_cluster = cl_smem <= size_t(200) * 1024 && nh <= 32 * kTriS;
+    const bool use_cluster = cl_smem <= size_t(kMaxDynSmem) && nh <= 32 * kTriS;
     if (use_cluster) {
         static bool attr = false;
         if (!attr) {
             KSB_CUDA_CHECK(cudaFuncSetAttribute(k_tridiag_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                int(200 * 1024)));
+                                                int(kMaxDynSmem)));
             KSB_CUDA_CHECK(cudaFuncSetAttribute(k_arrow_vec, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                int(200 * 1024)));
+                                                int(kMaxDynSmem)));
             attr = true;
         }
     }
@@ -1483,7 +1511,7 @@ InnerStats inner_scf(Level& L, const CoarseOps& co, const ProjOut& P, const Inne
                    w.wH[cur].p, w.th1[cur].p, w.c12.p, w.c22.p, w.lhat.p, nullptr, nh, N, prm.hartree ? 1 : 0};
         launch(c, "inner:orbital_border", k_orbital_border, N, 256, sizeof(double) * 3 * nh, S);
         const int warps = N * nev;
-        launch(c, "inner:arrow_eig", k_arrow_eig, ceil_div(warps, 4), 128, sizeof(double) * 6 * nh, nh, N, nev,
+        launch(c, "inner:arrow_eig", k_arrow_eig, warps, kEigWarps * 32, sizeof(double) * 3 * nh, nh, N, nev,
                (const double*)w.d.p,
                (const double*)w.e.p, (const double*)w.c12.p, (const double*)w.c22.p, w.lam.p);
         launch(c, "inner:arrow_vec", k_arrow_vec, ceil_div(warps, 4), 128, sizeof(double) * 4 * 4 * nh, nh, N, nev,
