@@ -229,6 +229,9 @@ int ksb_ctx_create(int device, ksb_ctx** out) {
         KSB_CUDA_CHECK(cudaGetDeviceProperties(&prop, device));
         c->c.sm_count = prop.multiProcessorCount;
         KSB_CUDA_CHECK(cudaStreamCreateWithFlags(&c->c.stream, cudaStreamNonBlocking));
+        KSB_CUDA_CHECK(cudaStreamCreateWithFlags(&c->c.aux, cudaStreamNonBlocking));
+        KSB_CUDA_CHECK(cudaEventCreateWithFlags(&c->c.fork, cudaEventDisableTiming));
+        KSB_CUDA_CHECK(cudaEventCreateWithFlags(&c->c.join, cudaEventDisableTiming));
         *out = c;
     });
 }
@@ -242,6 +245,10 @@ void ksb_ctx_destroy(ksb_ctx* c) {
         cudaEventDestroy(p.second.second);
     }
     for (auto e : c->c.event_pool) cudaEventDestroy(e);
+    cudaStreamSynchronize(c->c.aux);
+    cudaEventDestroy(c->c.fork);
+    cudaEventDestroy(c->c.join);
+    cudaStreamDestroy(c->c.aux);
     cudaStreamDestroy(c->c.stream);
     delete c;
 }

@@ -26,6 +26,8 @@ struct Ctx {
     int device = 0;
     int sm_count = kSMs;
     cudaStream_t stream = nullptr;
+    cudaStream_t aux = nullptr;              // side stream for work independent of the critical path
+    cudaEvent_t fork = nullptr, join = nullptr;
     bool profiling = false;
     int64_t launches = 0;
     struct Timer {
@@ -51,6 +53,29 @@ inline void launch(Ctx& c, const char* name, Kernel k, dim3 grid, dim3 block, si
     ++c.launches;
     KSB_CUDA_CHECK(cudaGetLastError());
     if (c.profiling) c.end(name, e0);
+}
+
+/// same as launch() on an explicit stream (the context's side stream)
+template <typename Kernel, typename... Args>
+inline void launch_on(Ctx& c, cudaStream_t st, const char* name, Kernel k, dim3 grid, dim3 block, size_t smem,
+                      Args... args) {
+    cudaStream_t keep = c.stream;
+    c.stream = st;  // profiling events go to the launching stream
+    cudaEvent_t e0 = nullptr;
+    if (c.profiling) c.begin(name, &e0);
+    k<<<grid, block, smem, st>>>(args...);
+    ++c.launches;
+    const cudaError_t err = cudaGetLastError();
+    if (c.profiling) c.end(name, e0);
+    c.stream = keep;
+    if (err != cudaSuccess) ::ksb::raise(KSB_CUDA, std::string("launch: ") + cudaGetErrorString(err));
+}
+
+/// make `to` wait for everything issued so far on `from`
+inline void stream_wait(Ctx& c, cudaStream_t from, cudaStream_t to, cudaEvent_t ev) {
+    KSB_CUDA_CHECK(cudaEventRecord(ev, from));
+    KSB_CUDA_CHECK(cudaStreamWaitEvent(to, ev, 0));
+    (void)c;
 }
 
 inline int ceil_div(int64_t a, int64_t b) { return int((a + b - 1) / b); }

@@ -652,8 +652,9 @@ struct SweepDev {
     int nh, N, hartree;
 };
 
-/// block per orbital: b, beta, t = A_H u, c12 = L^-1 (b - t)/s, c22, then c^ = Q^T c12, l^ = Q^T l
-__global__ void k_orbital_border(SweepDev S) {
+/// block per orbital, independent of the tridiagonalisation (runs on the side stream while it does):
+/// b, beta, t = A_H u, c22, and x = L^-1 (b - t) / s into c12 (rotated by k_border_q)
+__global__ void k_border_pre(SweepDev S) {
     extern __shared__ double sh[];
     const int i = blockIdx.x, nh = S.nh;
     double* b = sh;            // nh
@@ -691,23 +692,26 @@ __global__ void k_orbital_border(SweepDev S) {
     const double ut = block_dot(u, t, nh);
     const double si = S.s[i];
     if (threadIdx.x == 0) S.c22[i] = (beta - 2.0 * ub + ut) / (si * si);
-    // c12 = Q^T L^-1 (b - t) / s, l^ = Q^T l
-    double* c12 = S.c12 + size_t(i) * nh;
-    double* lh = S.lhat + size_t(i) * nh;
-    double* x = sh + 2 * nh;
     for (int a = threadIdx.x; a < nh; a += blockDim.x) t[a] = (b[a] - t[a]) / si;
     __syncthreads();
+    double* x = sh + 2 * nh;
     block_gemv(nh, S.LHi, t, x);
     __syncthreads();
-    if (warp == 0) {
-        apply_q_warp(nh, S.V, x, 1);
-        for (int a = lane; a < nh; a += 32) c12[a] = x[a];
-    } else if (warp == 1) {
-        for (int a = lane; a < nh; a += 32) b[a] = S.l[size_t(i) * nh + a];  // b is free now
-        __syncwarp();
-        apply_q_warp(nh, S.V, b, 1);
-        for (int a = lane; a < nh; a += 32) lh[a] = b[a];
-    }
+    for (int a = threadIdx.x; a < nh; a += blockDim.x) S.c12[size_t(i) * nh + a] = x[a];
+}
+
+/// block per orbital (2 warps): c12 <- Q^T c12 (warp 0), l^ = Q^T l (warp 1)
+__global__ void k_border_q(SweepDev S) {
+    extern __shared__ double sh[];
+    const int i = blockIdx.x, nh = S.nh;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double* vec = sh + size_t(warp) * nh;
+    const double* src = warp == 0 ? S.c12 + size_t(i) * nh : S.l + size_t(i) * nh;
+    double* dst = warp == 0 ? S.c12 + size_t(i) * nh : S.lhat + size_t(i) * nh;
+    for (int a = lane; a < nh; a += 32) vec[a] = src[a];
+    __syncwarp();
+    apply_q_warp(nh, S.V, vec, 1);
+    for (int a = lane; a < nh; a += 32) dst[a] = vec[a];
 }
 
 /// inertia of [T - x, c; c^T, c22 - x]: number of eigenvalues < x (Sylvester), one LDL^T pass with one
@@ -1477,6 +1481,7 @@ InnerStats inner_scf(Level& L, const CoarseOps& co, const ProjOut& P, const Inne
     const int cl_R = (nh + kTriCluster - 1) / kTriCluster;
     const size_t cl_smem = sizeof(double) * (size_t(cl_R) * nh + (2 + 2 * kTriRep) * size_t(nh));
     const bool use_cluster = cl_smem <= size_t(kMaxDynSmem) && nh <= 32 * kTriS;
+
     if (use_cluster) {
         static bool attr = false;
         if (!attr) {
@@ -1497,6 +1502,11 @@ InnerStats inner_scf(Level& L, const CoarseOps& co, const ProjOut& P, const Inne
         launch(c, "inner:build_", k_build_AH, nh, 128, sizeof(double) * nh, nh, (const int32_t*)L.cinc_ptr.p,
                (const int32_t*)L.cinc.p, (const int32_t*)L.ctets.p, (const int32_t*)L.ciidx.p, A1, A3, A4,
                (const double*)w.E16.p, prm.hartree ? 1 : 0, (const double*)w.th1[cur].p, w.AH.p);
+        // the orbital borders depend on A_H but not on the tridiagonalisation: side stream, joined below
+        SweepDev S{w.AH.p, A3, P.A_h4.p, P.orb_vecs.p, P.orb_scal.p, co.LHi.p, co.LHiT.p, w.V.p, w.l.p, w.u.p, w.s.p,
+                   w.wH[cur].p, w.th1[cur].p, w.c12.p, w.c22.p, w.lhat.p, nullptr, nh, N, prm.hartree ? 1 : 0};
+        stream_wait(c, c.stream, c.aux, c.fork);
+        launch_on(c, c.aux, "inner:border_pre", k_border_pre, N, 256, sizeof(double) * 3 * nh, S);
         // C11 = L^-1 A_H L^-T as two products (A_H symmetric: L^-1 A_H = L^-1 A_H^T)
         const dim3 gt(ceil_div(nh, 32), ceil_div(nh, 32));
         launch(c, "inner:gemm", k_gemm_nt, gt, 256, 0, nh, (const double*)co.LHi.p, (const double*)w.AH.p, w.W.p);
@@ -1507,9 +1517,8 @@ InnerStats inner_scf(Level& L, const CoarseOps& co, const ProjOut& P, const Inne
                    w.d.p, w.e.p, w.V.p);
         else
             launch(c, "inner_tridiag", k_tridiag, 1, 1024, tri_smem, nh, w.C.p, w.d.p, w.e.p, w.V.p);
-        SweepDev S{w.AH.p, A3, P.A_h4.p, P.orb_vecs.p, P.orb_scal.p, co.LHi.p, co.LHiT.p, w.V.p, w.l.p, w.u.p, w.s.p,
-                   w.wH[cur].p, w.th1[cur].p, w.c12.p, w.c22.p, w.lhat.p, nullptr, nh, N, prm.hartree ? 1 : 0};
-        launch(c, "inner:orbital_border", k_orbital_border, N, 256, sizeof(double) * 3 * nh, S);
+        stream_wait(c, c.aux, c.stream, c.join);
+        launch(c, "inner:border_q", k_border_q, N, 64, sizeof(double) * 2 * nh, S);
         const int warps = N * nev;
         launch(c, "inner:arrow_eig", k_arrow_eig, warps, kEigWarps * 32, sizeof(double) * 3 * nh, nh, N, nev,
                (const double*)w.d.p,
