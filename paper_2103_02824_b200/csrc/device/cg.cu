@@ -719,7 +719,10 @@ __global__ void k_diag(int ni, const int32_t* __restrict__ dslot, const double* 
 int elem_grid(const Ctx& c, int ni, int N) {
     const int rb = std::max(1, kThreads / N);
     const int64_t want = (int64_t(ni) + rb - 1) / rb;
-    return int(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(c.sm_count) * 8)));
+    // narrow blocks (N <= 2) move few bytes per row: two blocks per SM are enough to saturate HBM and keep the
+    // per-block partials (and their fences) few
+    const int64_t cap = int64_t(c.sm_count) * (N <= 2 ? 2 : 8);
+    return int(std::max<int64_t>(1, std::min<int64_t>(want, cap)));
 }
 
 struct Plan {
@@ -796,7 +799,9 @@ void launch_iteration(Ctx& c, const Level& L, const CgWork& w, const Cols& cc, c
     else
         launch(c, "cg_update_r", k_update_r<1>, grid_e, kThreads, sm_e, L.ni, cc, w.R, (const double*)w.AP, w.dev);
     if (!cc.fixed)
-        launch(c, "cg_trueres", k_trueres<G, CPL, SHIFT, SPLIT, FULL>, grid_s, kThreads, sm_s, L.ni, cc,
+        // runs every iteration but only works when a column was flagged (rare): one block per SM keeps the
+        // common early exit cheap
+        launch(c, "cg_trueres", k_trueres<G, CPL, SHIFT, SPLIT, FULL>, std::min(grid_s, c.sm_count), kThreads, sm_s, L.ni, cc,
                (const int32_t*)L.ii_ptr.p, (const int32_t*)L.ii_col.p, A, Bv, Bb, (const double*)X,
                (const double*)w.AP, w.R, w.dev);
     if (v2)
