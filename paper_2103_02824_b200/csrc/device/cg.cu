@@ -20,6 +20,8 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <cooperative_groups.h>
+
 #include "cg.cuh"
 #include "spmm_core.cuh"
 
@@ -476,6 +478,281 @@ __global__ void __launch_bounds__(kThreads, 2) k_sell_dot(int ni, int nslices, C
         s.part0[size_t(blockIdx.x) * N + threadIdx.x] = t;
     }
     k1_epilogue(red, N, cc, s);
+}
+
+// ---------------- persistent cooperative CG for N <= 2 ----------------
+// Small solves (the orbital BVP at N = 1-2 and every Hartree solve) are latency bound as four kernels per
+// iteration. This kernel runs a chunk of iterations in one cooperative launch: the same four phases
+// (K1 SpMV + p.Ap, K2 r update + r.r/r.z, K3 true residual when flagged, K4 x/p update) separated by grid
+// barriers. Every block folds the per-block partials in the same fixed order and advances an identical copy
+// of the per-column scalar state in shared memory, so no block waits on another for alpha / beta; block 0
+// writes the state back at the end of the chunk. Rows follow the SELL-32 slices (warp per slice, lane per
+// row) in every phase, so each thread only touches its own rows between barriers.
+struct CoopState {
+    double alpha[2], beta[2], rz[2], rr[2], bnorm[2], relres[2];
+    int status[2], check[2], iters[2];
+    int it, nactive, anycheck;
+};
+
+template <int NC>
+__device__ void coop_load(CoopState& st, const CgDev& s) {
+    if (threadIdx.x == 0) {
+        for (int c = 0; c < NC; ++c) {
+            st.alpha[c] = s.alpha[c];
+            st.beta[c] = s.beta[c];
+            st.rz[c] = s.rz[c];
+            st.rr[c] = s.rr[c];
+            st.bnorm[c] = s.bnorm[c];
+            st.relres[c] = s.relres[c];
+            st.status[c] = s.status[c];
+            st.check[c] = s.check[c];
+            st.iters[c] = s.iters[c];
+        }
+        st.it = s.ctl[kIt];
+        st.nactive = s.ctl[kNActive];
+        st.anycheck = s.ctl[kAnyCheck];
+    }
+    __syncthreads();
+}
+
+template <int NC>
+__device__ void coop_store(const CoopState& st, CgDev& s) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        for (int c = 0; c < NC; ++c) {
+            s.alpha[c] = st.alpha[c];
+            s.beta[c] = st.beta[c];
+            s.rz[c] = st.rz[c];
+            s.rr[c] = st.rr[c];
+            s.relres[c] = st.relres[c];
+            s.status[c] = st.status[c];
+            s.check[c] = st.check[c];
+            s.iters[c] = st.iters[c];
+        }
+        s.ctl[kIt] = st.it;
+        s.ctl[kNActive] = st.nactive;
+        s.ctl[kAnyCheck] = st.anycheck;
+    }
+}
+
+/// per-block sum of K partial vectors (thread values v[k]) -> part[blockIdx * K + k], fixed order
+template <int K>
+__device__ void coop_block_sum(const double (&v)[K], double* part, double* red) {
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const double t = warp_sum(v[k]);
+        if (lane == 0) red[wib * K + k] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x < K) {
+        double t = 0.0;
+        for (int w = 0; w < nw; ++w) t += red[w * K + threadIdx.x];
+        part[size_t(blockIdx.x) * K + threadIdx.x] = t;
+    }
+    __syncthreads();
+}
+
+template <int NC, bool SHIFT>
+__global__ void __launch_bounds__(kThreads) k_cg_coop(int ni, int nsl, Cols cc, const int32_t* __restrict__ sptr,
+                                                      const int32_t* __restrict__ scol, const double* __restrict__ sA,
+                                                      const double* __restrict__ sB, const double* __restrict__ Bb,
+                                                      double* __restrict__ X, double* __restrict__ R,
+                                                      double* __restrict__ P, double* __restrict__ AP, CgDev s,
+                                                      int n_iters) {
+    namespace cgx = cooperative_groups;
+    cgx::grid_group grid = cgx::this_grid();
+    __shared__ CoopState st;
+    __shared__ double red[32 * 2 * NC];
+    __shared__ double fold[4 * NC];
+    const int ld = cc.ld;
+    const int lane = threadIdx.x & 31;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    coop_load<NC>(st, s);
+    double sig[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) sig[c] = SHIFT ? s.sigma[c] : 0.0;
+    auto dinv = [&](int r, int c) {
+        double d = s.diagA[r];
+        if (s.diagB) d += s.sigma[c] * s.diagB[r];
+        return d != 0.0 ? 1.0 / d : 1.0;
+    };
+    // SpMV of the own rows: y = (A + sigma B) v for every slice of this warp
+    auto spmv_rows = [&](const double* __restrict__ V, auto&& per_row) {
+        for (int sl = warp; sl < nsl; sl += nwarps) {
+            const int r = sl * 32 + lane;
+            const int b0 = __ldg(sptr + sl);
+            const int w = (__ldg(sptr + sl + 1) - b0) >> 5;
+            double acc[NC], accB[NC];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) acc[c] = accB[c] = 0.0;
+            constexpr int U = 4;  // entries in flight per lane: index loads, then gathers, then FMAs
+            for (int e0 = 0; e0 < w; e0 += U) {
+                int j[U];
+                double a[U], bb[U], x[U][NC];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int k = b0 + (e0 + u) * 32 + lane;
+                    const bool in = e0 + u < w;
+                    j[u] = in ? __ldg(scol + k) : 0;
+                    a[u] = in ? __ldg(sA + k) : 0.0;
+                    bb[u] = (SHIFT && in) ? __ldg(sB + k) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+#pragma unroll
+                    for (int c = 0; c < NC; ++c) x[u][c] = V[size_t(j[u]) * ld + c];
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+#pragma unroll
+                    for (int c = 0; c < NC; ++c) {
+                        acc[c] = fma(a[u], x[u][c], acc[c]);
+                        if (SHIFT) accB[c] = fma(bb[u], x[u][c], accB[c]);
+                    }
+            }
+            if (r < ni) {
+#pragma unroll
+                for (int c = 0; c < NC; ++c)
+                    if (SHIFT) acc[c] = fma(sig[c], accB[c], acc[c]);
+                per_row(r, acc);
+            }
+        }
+    };
+    for (int k = 0; k < n_iters; ++k) {
+        if (!cc.fixed && st.nactive == 0) break;
+        // ---- K1: Ap = A p, p.Ap
+        {
+            double pd[NC];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) pd[c] = 0.0;
+            spmv_rows(P, [&](int r, const double (&acc)[NC]) {
+#pragma unroll
+                for (int c = 0; c < NC; ++c) {
+                    AP[size_t(r) * ld + c] = acc[c];
+                    pd[c] = fma(P[size_t(r) * ld + c], acc[c], pd[c]);
+                }
+            });
+            coop_block_sum<NC>(pd, s.part0, red);
+        }
+        grid.sync();
+        fold_partials(s.part0, gridDim.x, NC, fold);
+        if (threadIdx.x == 0) {
+            for (int c = 0; c < NC; ++c) {
+                const double pap = fold[c];
+                double al = 0.0;
+                if (st.status[c] == kActive) {
+                    if (!cc.fixed && !(pap > 0.0)) {
+                        st.status[c] = kBreakdown;
+                        st.relres[c] = sqrt(st.rr[c]) / st.bnorm[c];
+                    } else {
+                        al = st.rz[c] / pap;
+                    }
+                }
+                st.alpha[c] = al;
+            }
+            int na = 0;
+            for (int c = 0; c < NC; ++c) na += st.status[c] == kActive;
+            st.nactive = na;
+        }
+        __syncthreads();
+        // ---- K2: r -= alpha Ap (active columns), r.r and r.z
+        {
+            double part[2 * NC];
+#pragma unroll
+            for (int c = 0; c < 2 * NC; ++c) part[c] = 0.0;
+            for (int sl = warp; sl < nsl; sl += nwarps) {
+                const int r = sl * 32 + lane;
+                if (r >= ni) continue;
+#pragma unroll
+                for (int c = 0; c < NC; ++c) {
+                    if (st.status[c] != kActive) continue;
+                    const size_t i = size_t(r) * ld + c;
+                    const double rv = fma(-st.alpha[c], AP[i], R[i]);
+                    R[i] = rv;
+                    part[c] = fma(rv, rv, part[c]);
+                    part[NC + c] = fma(rv, dinv(r, c) * rv, part[NC + c]);
+                }
+            }
+            coop_block_sum<2 * NC>(part, s.part1, red);
+        }
+        grid.sync();
+        fold_partials(s.part1, gridDim.x, 2 * NC, fold);
+        if (threadIdx.x == 0) {
+            int any = 0;
+            for (int c = 0; c < NC; ++c) {
+                if (st.status[c] != kActive) continue;
+                const double rr = fold[c], rz = fold[NC + c];
+                const double rel = sqrt(rr) / st.bnorm[c];
+                st.rr[c] = rr;
+                st.iters[c] = st.it + 1;
+                st.relres[c] = rel;
+                if (!cc.fixed && rel <= cc.tol) {
+                    st.check[c] = 1;
+                    any = 1;
+                } else {
+                    st.beta[c] = rz / st.rz[c];
+                    st.rz[c] = rz;
+                }
+            }
+            st.it += 1;
+            st.anycheck = any;
+        }
+        __syncthreads();
+        // ---- K3: true residual t = b - A x - alpha Ap for flagged columns (x still x_k)
+        if (!cc.fixed && st.anycheck) {
+            double part[2 * NC];
+#pragma unroll
+            for (int c = 0; c < 2 * NC; ++c) part[c] = 0.0;
+            spmv_rows(X, [&](int r, const double (&acc)[NC]) {
+#pragma unroll
+                for (int c = 0; c < NC; ++c) {
+                    if (!st.check[c]) continue;
+                    const size_t i = size_t(r) * ld + c;
+                    const double t = Bb[i] - fma(st.alpha[c], AP[i], acc[c]);
+                    R[i] = t;
+                    part[c] = fma(t, t, part[c]);
+                    part[NC + c] = fma(t, dinv(r, c) * t, part[NC + c]);
+                }
+            });
+            coop_block_sum<2 * NC>(part, s.part0, red);
+            grid.sync();
+            fold_partials(s.part0, gridDim.x, 2 * NC, fold);
+            if (threadIdx.x == 0) {
+                for (int c = 0; c < NC; ++c) {
+                    if (!st.check[c]) continue;
+                    const double rel = sqrt(fold[c]) / st.bnorm[c];
+                    st.relres[c] = rel;
+                    st.rr[c] = fold[c];
+                    if (rel <= cc.tol) {
+                        st.status[c] = kConverged;
+                    } else {
+                        st.rz[c] = fold[NC + c];
+                        st.beta[c] = 0.0;
+                    }
+                    st.check[c] = 0;
+                }
+                st.anycheck = 0;
+                int na = 0;
+                for (int c = 0; c < NC; ++c) na += st.status[c] == kActive;
+                st.nactive = na;
+            }
+            __syncthreads();
+        }
+        // ---- K4: x += alpha p, p = z + beta p
+        for (int sl = warp; sl < nsl; sl += nwarps) {
+            const int r = sl * 32 + lane;
+            if (r >= ni) continue;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                const size_t i = size_t(r) * ld + c;
+                const double pv = P[i];
+                if (st.alpha[c] != 0.0) X[i] = fma(st.alpha[c], pv, X[i]);
+                if (st.status[c] == kActive) P[i] = fma(st.beta[c], pv, dinv(r, c) * R[i]);
+            }
+        }
+        grid.sync();
+    }
+    coop_store<NC>(st, s);
 }
 
 // ---------------- K2: r update (x is deferred to K4, which reads p anyway) ----------------
@@ -971,7 +1248,50 @@ void cg_solve(Ctx& c, Level& L, int mat, int shift_mat, const double* h_sigma, c
         w.graphs.push_back(g);
         return w.graphs.back();
     };
-    int done = 0;
+    // N <= 2: the whole solve is one cooperative launch (the kernel stops itself once no column is active)
+    static const char* cenv = std::getenv("KSB_CG_COOP");
+    if (so.A && N <= 2 && !(cenv && cenv[0] == '0')) {
+        auto coop = [&](auto kern) {
+            const int block = kThreads;
+            // resident blocks per SM for the cooperative grid: KSB_COOP_BLOCKS_PER_SM (default 2; fewer blocks make
+            // the grid barriers cheaper but leave the SpMV phase latency bound)
+            static const char* bpe = std::getenv("KSB_COOP_BLOCKS_PER_SM");
+            const int bps = bpe ? std::max(1, std::atoi(bpe)) : 2;
+            const int want = std::max(1, ceil_div(L.nslices, 2 * (block / 32)));
+            const int grid =
+                std::max(1, std::min({want, resident_grid(c, kern, block, 0), c.sm_count * bps}));
+            int ni = L.ni, nsl = L.nslices, iters = total;
+            const int32_t* sptr = L.sell_ptr.p;
+            const int32_t* scol = L.sell_col.p;
+            const double* sA = so.A;
+            const double* sB = so.B;
+            const double* Bb = d_B;
+            double* Xp = d_X;
+            double* Rp = w.R;
+            double* Pp = w.P;
+            double* APp = w.AP;
+            CgDev dv = d;
+            void* args[] = {&ni, &nsl, &cc, &sptr, &scol, &sA, &sB, &Bb, &Xp, &Rp, &Pp, &APp, &dv, &iters};
+            cudaEvent_t e0 = nullptr;
+            if (c.profiling) c.begin("cg_coop", &e0);
+            KSB_CUDA_CHECK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(grid), dim3(block),
+                                                       args, 0, c.stream));
+            ++c.launches;
+            if (c.profiling) c.end("cg_coop", e0);
+        };
+        if (N == 1) {
+            if (shift)
+                coop(k_cg_coop<1, true>);
+            else
+                coop(k_cg_coop<1, false>);
+        } else {
+            if (shift)
+                coop(k_cg_coop<2, true>);
+            else
+                coop(k_cg_coop<2, false>);
+        }
+    }
+    int done = (so.A && N <= 2 && !(cenv && cenv[0] == '0')) ? total : 0;
     while (done < total) {
         const int chunk = std::min(every, total - done);
         if (graphs_on && done > 0) {

@@ -33,7 +33,7 @@ for s in range(steps):
         break
 
 # per-kernel breakdown of one more step
-NAMES = ["spmm", "cg_update_r", "cg_update_px", "cg_trueres", "cg_setup", "inner_tridiag", "inner:gemm", "inner:gemv",
+NAMES = ["cg_coop", "spmm", "cg_update_r", "cg_update_px", "cg_trueres", "cg_setup", "inner_tridiag", "inner:gemm", "inner:gemv",
          "inner:orbital_border", "inner:border_pre", "inner:border_q", "inner:arrow_eig", "inner:arrow_vec", "inner:select", "inner:hartree_delta",
          "inner:coarse_wmass", "inner:build_", "inner:symmetrize", "inner:coarse_sq", "inner:coarse_vec_asm",
          "inner:border_scale", "inner:schur", "project", "project_asm", "assemble", "axpby", "sqload", "rho_vxc",
