@@ -373,6 +373,7 @@ void correction_step(Level& L, Corrector& K, CgWork& cg, const StepOptions& o, d
     ip.nev_pad = o.nev_pad;
     ip.hartree = K.sys.hartree_on;
     ip.occ = K.sys.occ;
+    ip.fixed_sweeps = o.fixed_sweeps;
     const InnerStats ist = inner_scf(L, K.coarse, K.proj, ip, h_lambda, K.inner, true);
     lg.inner_iterations = ist.iterations;
     lg.inner_history = ist.history;

@@ -39,7 +39,7 @@ def synthetic_start(L: api.Level, ctx: api.Context, mesh: api.Mesh, centers, N: 
         r = np.linalg.norm(x - c, axis=1)
         f = np.exp(-zeta * r)
         if i >= len(cen):
-            f = f * (x - c) @ rng.standard_normal(3)
+            f = f * ((x - c) @ rng.standard_normal(3))
         Phi[:, i] = f
     n = L.n
     for i in range(N):

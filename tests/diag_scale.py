@@ -1,0 +1,74 @@
+"""GPU diagnostic: correction steps at cfg4/cfg5 orbital counts (N = 21, 120) on uniform Kuhn meshes, synthetic
+start (one Gaussian-like orbital per center, columns beyond the centers get seeded polynomial factors),
+fixed inner sweeps so the timing is defined whatever the inner dynamics do."""
+import json
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import paper_2103_02824_b200 as kb  # noqa: E402
+from paper_2103_02824_b200.workloads import synthetic_start  # noqa: E402
+
+
+def ring_atoms():
+    """cfg4-like: 6 Z=6 on r = 2.64, 6 Z=1 on r = 4.68 (coplanar), seeded angle offset and jitter"""
+    rng = np.random.default_rng(21)
+    off = rng.uniform(0, np.pi / 3)
+    at = []
+    for k in range(6):
+        t = off + k * np.pi / 3
+        at.append([6.0, 2.64 * np.cos(t), 2.64 * np.sin(t), 0.0])
+        at.append([1.0, 4.68 * np.cos(t), 4.68 * np.sin(t), 0.0])
+    a = np.array(at)
+    a[:, 1:] += rng.uniform(-0.05, 0.05, (12, 3))
+    return a.tolist()
+
+
+def sphere_atoms(n=60, r=6.7, dmin=2.5, seed=60):
+    rng = np.random.default_rng(seed)
+    pts = []
+    while len(pts) < n:
+        v = rng.standard_normal(3)
+        v *= r / np.linalg.norm(v)
+        if all(np.linalg.norm(v - p) >= dmin for p in pts):
+            pts.append(v)
+    return [[6.0, *p] for p in pts]
+
+
+def run(name, atoms, N, box, refine, sweeps, steps=2):
+    h = kb.Hierarchy()
+    m = kb.Mesh.box([-box] * 3, [box] * 3, 8)
+    h.push(m)
+    for _ in range(refine):
+        m = m.uniform_refine()
+        h.push(m)
+    ctx = kb.Context(0)
+    L = kb.Level(ctx, h, refine)
+    L.set_system(atoms, n_pairs=N, occupancy=2.0, xc="lda")
+    t = time.time()
+    L.level_ops()
+    t_ops = time.time() - t
+    cen = [a[1:] for a in atoms]
+    lam, Phi, w, ld = synthetic_start(L, ctx, h.meshes[refine], cen, N, zeta=1.0, lam0=-0.5)
+    lam = np.linspace(-1.5, -0.3, N)
+    out = {"name": name, "N": N, "n_interior": L.ni, "ops_s": round(t_ops, 3), "steps": []}
+    for s in range(steps):
+        try:
+            lg = L.correction_step(lam, Phi, w, ld=ld, fixed_sweeps=sweeps)
+        except kb.KsbError as e:
+            out["steps"].append({"error": str(e)[:200]})
+            break
+        out["steps"].append({k: round(lg[k], 3) for k in ("ms_bvp", "ms_hartree", "ms_project", "ms_inner", "ms_total")}
+                            | {"cg": lg["cg_iterations"], "attempts": sorted(set(lg["attempts"]))})
+    print(json.dumps(out), flush=True)
+    L.close()
+    ctx.close()
+
+
+if __name__ == "__main__":
+    run("cfg4-like N=21, 250k dofs", ring_atoms(), 21, 25.0, 3, 10)
+    run("cfg5-like N=120, 250k dofs", sphere_atoms(), 120, 30.0, 3, 10)
+    run("cfg5-like N=120, 2.1M dofs", sphere_atoms(), 120, 30.0, 4, 10)
