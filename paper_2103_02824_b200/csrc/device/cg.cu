@@ -282,7 +282,7 @@ __device__ void k1_epilogue(double* sm, int N, const Cols& cc, CgDev& s) {
 }
 
 // ---------------- K1: Ap = A p, alpha ----------------
-template <int G, int CPL, bool SHIFT, bool SPLIT, bool FULL, int MINB = KSB_SPMM_MINB>
+template <int G, int CPL, bool SHIFT, bool SPLIT, int FULL, int MINB = KSB_SPMM_MINB>
 __global__ void __launch_bounds__(kThreads, MINB) k_spmm_dot(int ni, Cols cc, const int32_t* __restrict__ ptr,
                                                        const int32_t* __restrict__ col, const double* __restrict__ A,
                                                        const double* __restrict__ Bv, const double* __restrict__ P,
@@ -339,11 +339,12 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_dot(int ni, Cols cc, co
             if constexpr (FULL) {
                 if (SHIFT) {
 #pragma unroll
-                    for (int q = 0; q < CPL; ++q) acc[q] = fma(s.sigma[full_col<G>(l, q)], accB[q], acc[q]);
+                    for (int q = 0; q < CPL; ++q)
+                        if (FULL == 1 || full_col<G>(l, q) < N) acc[q] = fma(s.sigma[full_col<G>(l, q)], accB[q], acc[q]);
                 }
                 double p[CPL];
-                load_full<G, CPL>(P + size_t(r) * ld, l, p);
-                store_full<G, CPL>(AP + size_t(r) * ld, l, acc);
+                load_full<G, CPL, FULL>(P + size_t(r) * ld, l, N, p);
+                store_full<G, CPL, FULL>(AP + size_t(r) * ld, l, N, acc);
 #pragma unroll
                 for (int q = 0; q < CPL; ++q) pd[q] = fma(p[q], acc[q], pd[q]);
             } else {
@@ -841,7 +842,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_update_r(int ni, Cols cc, doubl
 }
 
 // ---------------- K3: true residual for flagged columns ----------------
-template <int G, int CPL, bool SHIFT, bool SPLIT, bool FULL>
+template <int G, int CPL, bool SHIFT, bool SPLIT, int FULL>
 __global__ void __launch_bounds__(kThreads, 3) k_trueres(int ni, Cols cc, const int32_t* __restrict__ ptr,
                                                       const int32_t* __restrict__ col, const double* __restrict__ A,
                                                       const double* __restrict__ Bv, const double* __restrict__ Bb,
@@ -1045,7 +1046,7 @@ bool try_sell(Ctx& c, const Level& L, const CgWork& w, const Cols& cc, const Sel
     }
 }
 
-template <int G, int CPL, bool SHIFT, bool SPLIT, bool FULL>
+template <int G, int CPL, bool SHIFT, bool SPLIT, int FULL>
 void launch_iteration(Ctx& c, const Level& L, const CgWork& w, const Cols& cc, const double* A, const double* Bv,
                       const double* Bb, double* X, int grid_s, int grid_e, const SellOps& so) {
     const size_t sm_s = sizeof(double) * std::max<size_t>(size_t(kThreads / G) * G * CPL, 2 * size_t(cc.N));
@@ -1092,24 +1093,41 @@ void iteration(Ctx& c, const Level& L, const CgWork& w, const Cols& cc, const do
                const double* Bb, double* X, int grid_s, int grid_e, const SellOps& so) {
     const Plan p = plan_for(cc.N);
     const bool full = !p.split && cc.N == p.G * p.CPL;
+    // partial blocks (N < G*CPL) keep the interleaved layout with a pair tail mask when the leading dimension
+    // is even (the pair straddling an odd N then ends inside the row)
+    const bool tail = !p.split && !full && p.CPL == 4 && p.G >= 4 && cc.ld % 2 == 0;
     if (p.split)
-        launch_iteration<8, 1, SHIFT, true, false>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e, so);
+        launch_iteration<8, 1, SHIFT, true, 0>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e, so);
     else if (p.G == 2 && p.CPL == 2)
-        launch_iteration<2, 2, SHIFT, false, false>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e, so);
+        launch_iteration<2, 2, SHIFT, false, 0>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e, so);
     else if (p.G == 2)
-        launch_iteration<2, 4, SHIFT, false, false>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e, so);
+        launch_iteration<2, 4, SHIFT, false, 0>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e, so);
     else if (p.G == 8 && p.CPL == 2 && full)
-        launch_iteration<8, 2, SHIFT, false, true>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e, so);
+        launch_iteration<8, 2, SHIFT, false, 1>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e, so);
     else if (p.G == 4 && full)
-        launch_iteration<4, 4, SHIFT, false, true>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e, so);
+        launch_iteration<4, 4, SHIFT, false, 1>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e, so);
+    else if (p.G == 4 && tail)
+        launch_iteration<4, 4, SHIFT, false, 2>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e, so);
     else if (p.G == 4)
-        launch_iteration<4, 4, SHIFT, false, false>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e, so);
+        launch_iteration<4, 4, SHIFT, false, 0>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e, so);
+    else if (p.G == 8 && full)
+        launch_iteration<8, 4, SHIFT, false, 1>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e, so);
+    else if (p.G == 8 && tail)
+        launch_iteration<8, 4, SHIFT, false, 2>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e, so);
     else if (p.G == 8)
-        launch_iteration<8, 4, SHIFT, false, false>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e, so);
+        launch_iteration<8, 4, SHIFT, false, 0>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e, so);
+    else if (p.G == 16 && full)
+        launch_iteration<16, 4, SHIFT, false, 1>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e, so);
+    else if (p.G == 16 && tail)
+        launch_iteration<16, 4, SHIFT, false, 2>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e, so);
     else if (p.G == 16)
-        launch_iteration<16, 4, SHIFT, false, false>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e, so);
+        launch_iteration<16, 4, SHIFT, false, 0>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e, so);
+    else if (full)
+        launch_iteration<32, 4, SHIFT, false, 1>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e, so);
+    else if (tail)
+        launch_iteration<32, 4, SHIFT, false, 2>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e, so);
     else
-        launch_iteration<32, 4, SHIFT, false, false>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e, so);
+        launch_iteration<32, 4, SHIFT, false, 0>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e, so);
 }
 
 } // namespace

@@ -719,9 +719,10 @@ __global__ void k_border_q(SweepDev S) {
 /// block per (orbital, k): k-th smallest eigenvalue by 513-way multisection -- 8 warps x 32 lanes x 2 points
 /// per lane (two independent Sturm recurrences interleaved per lane), so an iteration gains 9 bits and the
 /// eigenvalue needs ~7 iterations of the 343-step dependency chain instead of ~12 with one warp.
-constexpr int kEigWarps = 8;
-
-__global__ void __launch_bounds__(kEigWarps * 32) k_arrow_eig(int nh, int N, int nev, const double* __restrict__ dg,
+/// W warps per item: 8 when few items (latency: fewer multisection rounds), 1 when the items fill the GPU
+/// (throughput: less total work per eigenvalue).
+template <int W>
+__global__ void __launch_bounds__(W * 32) k_arrow_eig(int nh, int N, int nev, const double* __restrict__ dg,
                                                               const double* __restrict__ eg,
                                                               const double* __restrict__ c12,
                                                               const double* __restrict__ c22,
@@ -730,7 +731,7 @@ __global__ void __launch_bounds__(kEigWarps * 32) k_arrow_eig(int nh, int N, int
     double* d = she;
     double* e = she + nh;
     double* c = she + 2 * nh;
-    __shared__ int first_above[kEigWarps];
+    __shared__ int first_above[W];
     __shared__ double bounds[2];
     const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int item = blockIdx.x;  // (orbital, k)
@@ -767,7 +768,7 @@ __global__ void __launch_bounds__(kEigWarps * 32) k_arrow_eig(int nh, int N, int
     double lo = bounds[0], hi = bounds[1];
     const double span = fmax(fabs(lo), fabs(hi));
     const double pivmin = DBL_MIN / DBL_EPSILON * fmax(1.0, span * span);
-    constexpr int P = kEigWarps * 64;  // evaluation points; point index p = 2 * (32 wib + lane) + h
+    constexpr int P = W * 64;  // evaluation points; point index p = 2 * (32 wib + lane) + h
     for (int it = 0; it < 40; ++it) {
         const double w = hi - lo;
         if (w <= 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + DBL_MIN) break;
@@ -811,7 +812,7 @@ __global__ void __launch_bounds__(kEigWarps * 32) k_arrow_eig(int nh, int N, int
         if (lane == 0) first_above[wib] = f;
         __syncthreads();
         int fa = P;
-        for (int q = 0; q < kEigWarps; ++q) fa = min(fa, first_above[q]);
+        for (int q = 0; q < W; ++q) fa = min(fa, first_above[q]);
         __syncthreads();
         const double nlo = fa == 0 ? lo : lo + w * double(fa) / double(P + 1);
         const double nhi = fa == P ? hi : lo + w * double(fa + 1) / double(P + 1);
@@ -973,94 +974,105 @@ __global__ void k_select(SweepDev S, int nev, const double* __restrict__ lam, co
     if (threadIdx.x == 0) th2_new[i] = sg * theta;
 }
 
-/// one block: f_H, g, Hartree bordered solve, theta1, w_H, and the H1 state change delta
+/// f_H, g, Hartree bordered solve, theta1, w_H, and the H1 state change delta. Two kernels: one block per orbital
+/// forms that orbital's load contribution, energy term and delta term (the nh x nh products dominate, so orbitals
+/// run in parallel); one block sums them in orbital order and does the bordered solve.
 struct HartreeDev {
     const double *sq, *A_h4, *A3, *orb_vecs, *orb_scal, *shared_vecs, *shared_scal, *CHi, *hu, *schur, *CH, *MH;
     const double *phi_new, *th2_new, *phi_old, *th2_old;
-    double *wH_new, *theta1_new, *delta, *f;
+    double *wH_new, *theta1_new, *delta, *part;  // part: N*nh load contributions, then N energy, N delta terms
     int nh, N, hartree;
     double occ;
 };
 
-__global__ void k_hartree_delta(HartreeDev H) {
+__global__ void __launch_bounds__(512) k_hartree_parts(HartreeDev H) {
     extern __shared__ double sh[];
-    const int nh = H.nh;
-    double* f = sh;           // nh
-    double* tmp = sh + nh;    // nh
-    double* dp = sh + 2 * nh; // nh
+    const int nh = H.nh, i = blockIdx.x;
+    double* tmp = sh;       // nh
+    double* dp = sh + nh;   // nh
+    double* tmq = sh + 2 * nh;  // nh
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    constexpr double four_pi = 4.0 * 3.14159265358979323846;
+    const double* ov = H.orb_vecs + size_t(i) * 6 * nh;
+    const double* sc = H.orb_scal + size_t(i) * 5;
     if (H.hartree) {
-        double g = 0.0;
-        for (int a = threadIdx.x; a < nh; a += blockDim.x) f[a] = 0.0;
-        __syncthreads();
-        for (int i = 0; i < H.N; ++i) {
-            const double* ph = H.phi_new + size_t(i) * nh;
-            const double t2 = H.th2_new[i];
-            const double* Ah4 = H.A_h4 + size_t(i) * nh * nh;
-            for (int a = warp; a < nh; a += nw) {
-                double t = 0.0, u = 0.0;
-                for (int c = lane; c < nh; c += 32) {
-                    t += Ah4[size_t(a) * nh + c] * ph[c];
-                    u += H.A3[size_t(a) * nh + c] * ph[c];
-                }
-                t = warp_sum(t);
-                u = warp_sum(u);
-                if (lane == 0) {
-                    const double* ov = H.orb_vecs + size_t(i) * 6 * nh;
-                    f[a] += H.sq[size_t(i) * nh + a];
-                    f[a] += 2.0 * t2 * t;
-                    f[a] += t2 * t2 * ov[5 * nh + a];
-                    tmp[a] = u;
-                }
+        const double* ph = H.phi_new + size_t(i) * nh;
+        const double t2 = H.th2_new[i];
+        const double* Ah4 = H.A_h4 + size_t(i) * nh * nh;
+        double* F = H.part + size_t(i) * nh;
+        for (int a = warp; a < nh; a += nw) {
+            double t = 0.0, u = 0.0;
+            for (int c = lane; c < nh; c += 32) {
+                t += Ah4[size_t(a) * nh + c] * ph[c];
+                u += H.A3[size_t(a) * nh + c] * ph[c];
             }
-            __syncthreads();
-            g += block_dot(ph, tmp, nh);
-            g += 2.0 * t2 * block_dot(H.orb_vecs + size_t(i) * 6 * nh + nh, ph, nh);
-            g += t2 * t2 * H.orb_scal[5 * i + 1];
+            t = warp_sum(t);
+            u = warp_sum(u);
+            if (lane == 0) {
+                F[a] = H.sq[size_t(i) * nh + a] + 2.0 * t2 * t + t2 * t2 * ov[5 * nh + a];
+                tmp[a] = u;
+            }
         }
-        for (int a = threadIdx.x; a < nh; a += blockDim.x) f[a] = four_pi * (H.occ * f[a]) - H.shared_vecs[nh + a];
+        __syncthreads();
+        double g = block_dot(ph, tmp, nh);
+        g += 2.0 * t2 * block_dot(ov + nh, ph, nh);
+        g += t2 * t2 * sc[1];
+        if (threadIdx.x == 0) H.part[size_t(H.N) * nh + i] = g;
+        __syncthreads();
+    }
+    // delta_i^2 = dphi^T (C_H + M_H) dphi + 2 dth (d_phi + c_Hh).dphi + dth^2 (zeta_phi + gamma)
+    for (int a = threadIdx.x; a < nh; a += blockDim.x)
+        dp[a] = H.phi_new[size_t(i) * nh + a] - H.phi_old[size_t(i) * nh + a];
+    __syncthreads();
+    const double dth = H.th2_new[i] - H.th2_old[i];
+    for (int a = warp; a < nh; a += nw) {
+        double t = 0.0, u = 0.0;
+        for (int c = lane; c < nh; c += 32) {
+            t += H.CH[size_t(a) * nh + c] * dp[c];
+            u += H.MH[size_t(a) * nh + c] * dp[c];
+        }
+        t = warp_sum(t);
+        u = warp_sum(u);
+        if (lane == 0) {
+            tmp[a] = t;
+            tmq[a] = u;
+        }
+    }
+    __syncthreads();
+    const double semi = block_dot(dp, tmp, nh) + 2.0 * dth * block_dot(ov + 4 * nh, dp, nh) + dth * dth * sc[4];
+    const double l2 = block_dot(dp, tmq, nh) + 2.0 * dth * block_dot(ov + 3 * nh, dp, nh) + dth * dth * sc[3];
+    if (threadIdx.x == 0) H.part[size_t(H.N) * nh + H.N + i] = semi + l2;
+}
+
+__global__ void __launch_bounds__(512) k_hartree_final(HartreeDev H) {
+    extern __shared__ double sh[];
+    const int nh = H.nh, N = H.N;
+    double* f = sh;           // nh
+    double* dp = sh + nh;     // nh
+    constexpr double four_pi = 4.0 * 3.14159265358979323846;
+    const double* gpart = H.part + size_t(N) * nh;
+    if (H.hartree) {
+        for (int a = threadIdx.x; a < nh; a += blockDim.x) {
+            double s = 0.0;
+            for (int i = 0; i < N; ++i) s += H.part[size_t(i) * nh + a];
+            f[a] = four_pi * (H.occ * s) - H.shared_vecs[nh + a];
+        }
+        double g = 0.0;
+        for (int i = 0; i < N; ++i) g += gpart[i];
         g = four_pi * (H.occ * g) - H.shared_scal[1];
         __syncthreads();
         // t = C_H^-1 f
         block_gemv(nh, H.CHi, f, dp);
         __syncthreads();
-        for (int a = threadIdx.x; a < nh; a += blockDim.x) f[a] = dp[a];
-        __syncthreads();
-        const double dt = block_dot(H.shared_vecs, f, nh);
+        const double dt = block_dot(H.shared_vecs, dp, nh);
         const double th1 = (g - dt) / H.schur[0];
-        for (int a = threadIdx.x; a < nh; a += blockDim.x) H.wH_new[a] = f[a] - th1 * H.hu[a];
+        for (int a = threadIdx.x; a < nh; a += blockDim.x) H.wH_new[a] = dp[a] - th1 * H.hu[a];
         if (threadIdx.x == 0) H.theta1_new[0] = th1;
     }
-    __syncthreads();
-    // delta^2 = sum_i dphi^T (C_H + M_H) dphi + 2 dth (d_phi + c_Hh).dphi + dth^2 (zeta_phi + gamma)
-    double tot = 0.0;
-    for (int i = 0; i < H.N; ++i) {
-        for (int a = threadIdx.x; a < nh; a += blockDim.x)
-            dp[a] = H.phi_new[size_t(i) * nh + a] - H.phi_old[size_t(i) * nh + a];
-        __syncthreads();
-        const double dth = H.th2_new[i] - H.th2_old[i];
-        for (int a = warp; a < nh; a += nw) {
-            double t = 0.0, u = 0.0;
-            for (int c = lane; c < nh; c += 32) {
-                t += H.CH[size_t(a) * nh + c] * dp[c];
-                u += H.MH[size_t(a) * nh + c] * dp[c];
-            }
-            t = warp_sum(t);
-            u = warp_sum(u);
-            if (lane == 0) {
-                tmp[a] = t;
-                f[a] = u;
-            }
-        }
-        __syncthreads();
-        const double* ov = H.orb_vecs + size_t(i) * 6 * nh;
-        const double* sc = H.orb_scal + size_t(i) * 5;
-        const double semi = block_dot(dp, tmp, nh) + 2.0 * dth * block_dot(ov + 4 * nh, dp, nh) + dth * dth * sc[4];
-        const double l2 = block_dot(dp, f, nh) + 2.0 * dth * block_dot(ov + 3 * nh, dp, nh) + dth * dth * sc[3];
-        tot += semi + l2;
+    if (threadIdx.x == 0) {
+        double tot = 0.0;
+        for (int i = 0; i < N; ++i) tot += gpart[N + i];
+        H.delta[0] = tot;
     }
-    if (threadIdx.x == 0) H.delta[0] = tot;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1282,6 +1294,7 @@ void InnerWork::ensure(int nh_, int N_, int nev_, int nct) {
     need(ynorm, int64_t(std::max(1, N)) * nev);
     need(Z, int64_t(std::max(1, N)) * nev * std::max(1, nh));
     need(hu, std::max(1, nh));
+    need(hpart, v + 2 * int64_t(std::max(1, N)));
     need(scal, 16);
     for (int k = 0; k < 2; ++k) {
         need(phi[k], v);
@@ -1520,7 +1533,12 @@ InnerStats inner_scf(Level& L, const CoarseOps& co, const ProjOut& P, const Inne
         stream_wait(c, c.aux, c.stream, c.join);
         launch(c, "inner:border_q", k_border_q, N, 64, sizeof(double) * 2 * nh, S);
         const int warps = N * nev;
-        launch(c, "inner:arrow_eig", k_arrow_eig, warps, kEigWarps * 32, sizeof(double) * 3 * nh, nh, N, nev,
+        if (warps >= 4 * c.sm_count)
+            launch(c, "inner:arrow_eig", k_arrow_eig<1>, warps, 32, sizeof(double) * 3 * nh, nh, N, nev,
+                   (const double*)w.d.p, (const double*)w.e.p, (const double*)w.c12.p, (const double*)w.c22.p,
+                   w.lam.p);
+        else
+            launch(c, "inner:arrow_eig", k_arrow_eig<8>, warps, 8 * 32, sizeof(double) * 3 * nh, nh, N, nev,
                (const double*)w.d.p,
                (const double*)w.e.p, (const double*)w.c12.p, (const double*)w.c22.p, w.lam.p);
         launch(c, "inner:arrow_vec", k_arrow_vec, ceil_div(warps, 4), 128, sizeof(double) * 4 * 4 * nh, nh, N, nev,
@@ -1540,12 +1558,13 @@ InnerStats inner_scf(Level& L, const CoarseOps& co, const ProjOut& P, const Inne
                    (const int32_t*)L.cinc_ptr.p, (const int32_t*)L.cinc.p, (const double*)w.E4.p, w.sq.p);
         HartreeDev H{w.sq.p, P.A_h4.p, A3, P.orb_vecs.p, P.orb_scal.p, P.shared_vecs.p, P.shared_scal.p, co.CHi.p,
                      w.hu.p, w.scal.p, co.CH.p, co.MH.p, w.phi[nx].p, w.th2[nx].p, w.phi[cur].p, w.th2[cur].p,
-                     w.wH[nx].p, w.th1[nx].p, w.scal.p + 1, nullptr, nh, N, prm.hartree ? 1 : 0, prm.occ};
+                     w.wH[nx].p, w.th1[nx].p, w.scal.p + 1, w.hpart.p, nh, N, prm.hartree ? 1 : 0, prm.occ};
         if (!prm.hartree) {
             KSB_CUDA_CHECK(cudaMemcpyAsync(w.wH[nx].p, w.wH[cur].p, sizeof(double) * nh, cudaMemcpyDeviceToDevice, c.stream));
             KSB_CUDA_CHECK(cudaMemcpyAsync(w.th1[nx].p, w.th1[cur].p, sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
         }
-        launch(c, "inner:hartree_delta", k_hartree_delta, 1, 512, sizeof(double) * 3 * nh, H);
+        launch(c, "inner:hartree_delta", k_hartree_parts, N, 512, sizeof(double) * 3 * nh, H);
+        launch(c, "inner:hartree_delta", k_hartree_final, 1, 512, sizeof(double) * 2 * nh, H);
         double dsq = 0.0;
         int fl[4];
         KSB_CUDA_CHECK(cudaMemcpyAsync(&dsq, w.scal.p + 1, sizeof(double), cudaMemcpyDeviceToHost, c.stream));

@@ -33,7 +33,7 @@ struct InnerStats {
 /// double-buffered augmented state + scratch; the result lives in buffers [cur]
 struct InnerWork {
     int nh = 0, N = 0, nev = 0, cur = 0;
-    DevBuf<double> AH, W, C, V, d, e, E16, E4, sq, l, u, s, c12, c22, lhat, lam, Y, Z, piv, score, ynorm, hu, scal;
+    DevBuf<double> AH, W, C, V, d, e, E16, E4, sq, l, u, s, c12, c22, lhat, lam, Y, Z, piv, score, ynorm, hu, scal, hpart;
     DevBuf<double> phi[2], th2[2], lamv[2], wH[2], th1[2];
     DevBuf<int> flag;
     void ensure(int nh, int N, int nev, int nct);

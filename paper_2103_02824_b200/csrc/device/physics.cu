@@ -118,7 +118,26 @@ __global__ void k_bc(int nb, const int32_t* __restrict__ boundary, const double*
     }
 }
 
-/// per-tet contributions of occ * sum_i phi_i^2 tested against the four hat functions (Keast rule)
+/// per-tet contributions of occ * sum_i phi_i^2 tested against the four hat functions (Keast rule).
+/// The density at a quadrature point is the quadratic form b_q^T Gm b_q of the vertex Gram matrix
+/// Gm_kl = sum_i phi_i(v_k) phi_i(v_l) (10 unique entries), so the orbitals are read once per tet, not per point.
+__device__ __forceinline__ int gram_idx(int k, int l) { return k <= l ? k * 4 - k * (k - 1) / 2 + (l - k) : l * 4 - l * (l - 1) / 2 + (k - l); }
+
+__device__ __forceinline__ double4 sq_quad(double vol, double occ, const double (&gm)[10]) {
+    double out[4] = {0, 0, 0, 0};
+    for (int q = 0; q < 11; ++q) {
+        double dens = 0.0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int l = 0; l < 4; ++l) dens += g_qb[q][k] * g_qb[q][l] * gm[gram_idx(k, l)];
+        const double s = g_qw[q] * vol * occ * dens;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) out[k] += s * g_qb[q][k];
+    }
+    return make_double4(out[0], out[1], out[2], out[3]);
+}
+
 __global__ void k_sqload_elem(int nt, const int32_t* __restrict__ tets, const double* __restrict__ xyz,
                               const int32_t* __restrict__ iidx, const double* __restrict__ Phi, int N, int ld,
                               double occ, double* __restrict__ E4) {
@@ -127,22 +146,60 @@ __global__ void k_sqload_elem(int nt, const int32_t* __restrict__ tets, const do
         TetG G;
         tet_geometry(xyz, v, G);
         const int rr[4] = {iidx[v.x], iidx[v.y], iidx[v.z], iidx[v.w]};
-        double out[4] = {0, 0, 0, 0};
-        for (int q = 0; q < 11; ++q) {
-            double dens = 0.0;
-            for (int i = 0; i < N; ++i) {
-                double val = 0.0;
+        double gm[10];
 #pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    if (rr[k] >= 0) val += g_qb[q][k] * Phi[size_t(rr[k]) * ld + i];
-                dens += val * val;
-            }
-            const double s = g_qw[q] * G.vol * occ * dens;
+        for (int k = 0; k < 10; ++k) gm[k] = 0.0;
+        for (int i = 0; i < N; ++i) {
+            double f[4];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) out[k] += s * g_qb[q][k];
+            for (int k = 0; k < 4; ++k) f[k] = rr[k] >= 0 ? Phi[size_t(rr[k]) * ld + i] : 0.0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+#pragma unroll
+                for (int l = k; l < 4; ++l) gm[gram_idx(k, l)] += f[k] * f[l];
         }
-        reinterpret_cast<double4*>(E4)[t] = make_double4(out[0], out[1], out[2], out[3]);
+        reinterpret_cast<double4*>(E4)[t] = sq_quad(G.vol, occ, gm);
     }
+}
+
+/// many orbitals: one warp per tet, lanes stride the orbitals of the four vertex rows (coalesced row reads)
+__global__ void k_sqload_elem_warp(int nt, const int32_t* __restrict__ tets, const double* __restrict__ xyz,
+                                   const int32_t* __restrict__ iidx, const double* __restrict__ Phi, int N, int ld,
+                                   double occ, double* __restrict__ E4) {
+    const int lane = threadIdx.x & 31;
+    const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    for (int t = w0; t < nt; t += nw) {
+        const int4 v = reinterpret_cast<const int4*>(tets)[t];
+        const int rr[4] = {iidx[v.x], iidx[v.y], iidx[v.z], iidx[v.w]};
+        double gm[10];
+#pragma unroll
+        for (int k = 0; k < 10; ++k) gm[k] = 0.0;
+        for (int i = lane; i < N; i += 32) {
+            double f[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) f[k] = rr[k] >= 0 ? Phi[size_t(rr[k]) * ld + i] : 0.0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+#pragma unroll
+                for (int l = k; l < 4; ++l) gm[gram_idx(k, l)] += f[k] * f[l];
+        }
+#pragma unroll
+        for (int k = 0; k < 10; ++k) gm[k] = warp_sum(gm[k]);
+        if (lane == 0) {
+            TetG G;
+            tet_geometry(xyz, v, G);
+            reinterpret_cast<double4*>(E4)[t] = sq_quad(G.vol, occ, gm);
+        }
+    }
+}
+
+void launch_sqload_elem(Ctx& c, Level& L, const double* Phi, int N, int ld, double occ, double* e4) {
+    if (N >= 32)
+        launch(c, "sqload", k_sqload_elem_warp, grid_of(c, int64_t(L.nt) * 32, 256), 256, 0, L.nt,
+               (const int32_t*)L.tets.p, (const double*)L.xyz.p, (const int32_t*)L.iidx.p, Phi, N, ld, occ, e4);
+    else
+        launch(c, "sqload", k_sqload_elem, grid_of(c, L.nt, 128), 128, 0, L.nt, (const int32_t*)L.tets.p,
+               (const double*)L.xyz.p, (const int32_t*)L.iidx.p, Phi, N, ld, occ, e4);
 }
 
 /// out[r] = scale * sum over incident (t, l) of E4[t*4 + l], ascending t
@@ -320,8 +377,7 @@ void sqload(Level& L, const double* Phi, int N, int ld, double occ, double scale
     Ctx& c = *L.ctx;
     ensure_rule(c.stream);
     w.ensure(L);
-    launch(c, "sqload", k_sqload_elem, grid_of(c, L.nt, 128), 128, 0, L.nt, (const int32_t*)L.tets.p,
-           (const double*)L.xyz.p, (const int32_t*)L.iidx.p, Phi, N, ld, occ, w.e4.p);
+    launch_sqload_elem(c, L, Phi, N, ld, occ, w.e4.p);
     launch(c, "sqload", k_gather_vinc, grid_of(c, L.ni), kT, 0, L.ni, (const int32_t*)L.vinc_ptr.p,
            (const int32_t*)L.vinc.p, (const double*)w.e4.p, scale, out_int);
 }
@@ -330,8 +386,7 @@ void sqload_full(Level& L, const double* Phi, int N, int ld, double occ, double*
     Ctx& c = *L.ctx;
     ensure_rule(c.stream);
     w.ensure(L);
-    launch(c, "sqload", k_sqload_elem, grid_of(c, L.nt, 128), 128, 0, L.nt, (const int32_t*)L.tets.p,
-           (const double*)L.xyz.p, (const int32_t*)L.iidx.p, Phi, N, ld, occ, w.e4.p);
+    launch_sqload_elem(c, L, Phi, N, ld, occ, w.e4.p);
     launch(c, "sqload", k_gather_vinc_rows, grid_of(c, L.ni), kT, 0, L.ni, (const int32_t*)L.vinc_ptr.p,
            (const int32_t*)L.vinc.p, (const double*)w.e4.p, 1.0, (const int32_t*)L.interior.p, out_full);
     if (L.nb > 0)

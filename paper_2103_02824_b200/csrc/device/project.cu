@@ -17,6 +17,7 @@ namespace ksb {
 namespace {
 
 constexpr int kProjThreads = 128;
+constexpr int kProjWideMin = 8;  // orbital count from which the staged (orbital-parallel) kernel is used
 
 struct ProjIn {
     const int32_t *tets, *iidx, *anc_ptr, *anc_tets, *ctets, *ciidx, *pint_col;
@@ -194,6 +195,117 @@ __global__ void __launch_bounds__(kProjThreads) k_proj_orbital(ProjIn in, double
     block_reduce_store<kOrbK>(acc, part + (size_t(1 + i) * in.nct + C) * kStride);
 }
 
+// Wide variant for many orbitals: the orbital-independent per-tet data (mu, the element matrices of the
+// a_eff, w~, v_xc, unit and stiffness operators) is staged in shared memory once per chunk of fine tets, and the
+// block's threads then run (orbital, tet slot) pairs over it. Orbital values of a fine vertex are read by
+// consecutive threads from one row of Phi (coalesced). Each thread owns the 49 accumulators of its orbital;
+// tet slots are folded in fixed order at the end.
+constexpr int kWideTets = 64;   // fine tets per staged chunk
+constexpr int kWideRec = 104;   // doubles per staged tet: mu 16, E1 E3 E4 Eone S (5 x 16), vol, 4 rows (as int), pad
+
+__global__ void __launch_bounds__(kProjThreads) k_proj_orbital_wide(ProjIn in, double* __restrict__ part) {
+    extern __shared__ double st[];  // kWideTets * kWideRec, reused for the final fold
+    const int C = blockIdx.x;
+    const int N = in.N;
+    const int i0 = blockIdx.y * kProjThreads;
+    const int NI = min(N - i0, kProjThreads);
+    const int TS = kProjThreads / NI;  // tet slots per orbital
+    const int oi = threadIdx.x % NI, slot = threadIdx.x / NI;
+    const bool act = slot < TS;
+    const int i = i0 + oi;
+    double acc[kOrbK];
+#pragma unroll
+    for (int k = 0; k < kOrbK; ++k) acc[k] = 0.0;
+    const int4 cv = reinterpret_cast<const int4*>(in.ctets)[C];
+    const int ci[4] = {in.ciidx[cv.x], in.ciidx[cv.y], in.ciidx[cv.z], in.ciidx[cv.w]};
+    const int pb = in.anc_ptr[C], pe = in.anc_ptr[C + 1];
+    for (int c0 = pb; c0 < pe; c0 += kWideTets) {
+        const int nc = min(kWideTets, pe - c0);
+        __syncthreads();
+        if (threadIdx.x < nc) {
+            double* R = st + threadIdx.x * kWideRec;
+            const int t = in.anc_tets[c0 + threadIdx.x];
+            const int4 v = reinterpret_cast<const int4*>(in.tets)[t];
+            TetG G;
+            tet_geometry(in.xyz, v, G);
+            double mu[4][4];
+            load_mu(in, v, ci, mu);
+            const double wt[4] = {in.wt[v.x], in.wt[v.y], in.wt[v.z], in.wt[v.w]};
+            const double el[4] = {in.ell[v.x], in.ell[v.y], in.ell[v.z], in.ell[v.w]};
+            const double xc[4] = {in.vxc[v.x], in.vxc[v.y], in.vxc[v.z], in.vxc[v.w]};
+            const double one[4] = {1.0, 1.0, 1.0, 1.0};
+            double S[4][4], E[4][4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    S[a][b] = G.vol * (G.g[a][0] * G.g[b][0] + G.g[a][1] * G.g[b][1] + G.g[a][2] * G.g[b][2]);
+                    R[4 * a + b] = mu[a][b];
+                    R[80 + 4 * a + b] = S[a][b];
+                }
+            mass_elem(G.vol, el, E);
+            const double* ex = in.eext + size_t(t) * 16;
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) R[16 + 4 * a + b] = E[a][b] + 0.5 * S[a][b] + ex[4 * a + b];
+            mass_elem(G.vol, wt, E);
+#pragma unroll
+            for (int k = 0; k < 16; ++k) R[32 + k] = E[k / 4][k % 4];
+            mass_elem(G.vol, xc, E);
+#pragma unroll
+            for (int k = 0; k < 16; ++k) R[48 + k] = E[k / 4][k % 4];
+            mass_elem(G.vol, one, E);
+#pragma unroll
+            for (int k = 0; k < 16; ++k) R[64 + k] = E[k / 4][k % 4];
+            R[96] = G.vol;
+            int* ri = reinterpret_cast<int*>(R + 97);
+            ri[0] = in.iidx[v.x];
+            ri[1] = in.iidx[v.y];
+            ri[2] = in.iidx[v.z];
+            ri[3] = in.iidx[v.w];
+        }
+        __syncthreads();
+        if (act)
+            for (int q = slot; q < nc; q += TS) {
+                const double* R = st + q * kWideRec;
+                const int* ri = reinterpret_cast<const int*>(R + 97);
+                double ph[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) ph[k] = ri[k] >= 0 ? in.Phi[size_t(ri[k]) * in.ld + i] : 0.0;
+                double mu[4][4], E[4][4];
+#pragma unroll
+                for (int k = 0; k < 16; ++k) mu[k / 4][k % 4] = R[k];
+                mass_elem(R[96], ph, E);  // M_phi
+                acc_proj(mu, E, acc + 0);
+                acc_vec(mu, E, ph, acc + 40);  // rhs = P^T (M_phi phi)
+#pragma unroll
+                for (int m = 0; m < 5; ++m) {
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) E[k / 4][k % 4] = R[16 + 16 * m + k];
+                    // b_H1/beta1, b_H3/beta3, b_H4/beta4, c_Hh/gamma, d_phi/zeta_phi
+                    acc[44 + m] += acc_vec(mu, E, ph, acc + 16 + 4 * m);
+                }
+            }
+    }
+    // fold the tet slots of each orbital in slot order
+    __syncthreads();
+    if (TS > 1) {
+        if (act)
+            for (int k = 0; k < kOrbK; ++k) st[(size_t(slot) * NI + oi) * kOrbK + k] = acc[k];
+        __syncthreads();
+        for (int e = threadIdx.x; e < NI * kOrbK; e += blockDim.x) {
+            const int o = e / kOrbK, k = e % kOrbK;
+            double s2 = 0.0;
+            for (int sl = 0; sl < TS; ++sl) s2 += st[(size_t(sl) * NI + o) * kOrbK + k];
+            part[(size_t(1 + i0 + o) * in.nct + C) * kStride + k] = s2;
+        }
+    } else if (act) {
+        double* dst = part + (size_t(1 + i) * in.nct + C) * kStride;
+        for (int k = 0; k < kOrbK; ++k) dst[k] = acc[k];
+    }
+}
+
 /// dense coarse assembly: out[m][a][b] = sum over (C, la) of a, lb with ci[lb] >= 0 of part[m][C][off + 4 la + lb]
 __global__ void k_coarse_mat(int nh, int nmats, const int32_t* __restrict__ cinc_ptr, const int32_t* __restrict__ cinc,
                              const int32_t* __restrict__ ctets, const int32_t* __restrict__ ciidx,
@@ -260,7 +372,18 @@ void project_blocks(Level& L, const double* Phi, int N, int ld, const double* wt
               (const int32_t*)L.pint_col.p, (const double*)L.xyz.p, (const double*)L.pint_val.p, eext, Phi, wt_full,
               ell_full, vxc_full, N, ld, nct};
     launch(c, "project", k_proj_shared, nct, kProjThreads, 0, in, o.part.p);
-    if (N > 0) launch(c, "project", k_proj_orbital, dim3(nct, N), kProjThreads, 0, in, o.part.p);
+    if (N >= kProjWideMin) {
+        const size_t smem = sizeof(double) * std::max(kWideTets * kWideRec, kProjThreads * kOrbK);
+        static bool attr = false;
+        if (!attr) {
+            KSB_CUDA_CHECK(cudaFuncSetAttribute(k_proj_orbital_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            attr = true;
+        }
+        launch(c, "project", k_proj_orbital_wide, dim3(nct, ceil_div(N, kProjThreads)), kProjThreads, smem, in,
+               o.part.p);
+    } else if (N > 0) {
+        launch(c, "project", k_proj_orbital, dim3(nct, N), kProjThreads, 0, in, o.part.p);
+    }
 
     const int64_t fstride = int64_t(nct) * kStride;  // stride between functions in part
     const int64_t nh2 = int64_t(nh) * nh;

@@ -48,21 +48,29 @@ __device__ __forceinline__ int full_col(int l, int q) {
     return 2 * ((q >> 1) * G + l) + (q & 1);
 }
 
+/// FULL layout modes: 1 = every slot in range (N == G*CPL); 2 = tail mask (N < G*CPL): a column pair is
+/// skipped when it starts at or beyond N. A pair straddling N (odd N) touches column N, which lies inside the
+/// even leading dimension and is never consumed.
+__device__ __forceinline__ bool pair_ok(int FULLMODE, int c, int N) { return FULLMODE != 2 || c < N; }
+
 /// p points at the row start; loads lane l's CPL columns in the FULL layout
-template <int G, int CPL>
-__device__ __forceinline__ void load_full(const double* __restrict__ p, int l, double (&x)[CPL]) {
+template <int G, int CPL, int FM = 1>
+__device__ __forceinline__ void load_full(const double* __restrict__ p, int l, int N, double (&x)[CPL]) {
 #pragma unroll
     for (int k = 0; k < CPL; k += 2) {
-        const double2 a = __ldg(reinterpret_cast<const double2*>(p + full_col<G>(l, k)));
+        double2 a = make_double2(0.0, 0.0);
+        if (pair_ok(FM, full_col<G>(l, k), N)) a = __ldg(reinterpret_cast<const double2*>(p + full_col<G>(l, k)));
         x[k] = a.x;
         x[k + 1] = a.y;
     }
 }
 
-template <int G, int CPL>
-__device__ __forceinline__ void store_full(double* __restrict__ p, int l, const double (&y)[CPL]) {
+template <int G, int CPL, int FM = 1>
+__device__ __forceinline__ void store_full(double* __restrict__ p, int l, int N, const double (&y)[CPL]) {
 #pragma unroll
-    for (int k = 0; k < CPL; k += 2) *reinterpret_cast<double2*>(p + full_col<G>(l, k)) = make_double2(y[k], y[k + 1]);
+    for (int k = 0; k < CPL; k += 2)
+        if (pair_ok(FM, full_col<G>(l, k), N))
+            *reinterpret_cast<double2*>(p + full_col<G>(l, k)) = make_double2(y[k], y[k + 1]);
 }
 
 template <int CPL>
@@ -87,8 +95,11 @@ __device__ __forceinline__ void store_cols(double* __restrict__ p, int c0, int N
 /// Control flow is warp-uniform: every group of the warp runs max-over-the-warp chunks, exhausted
 /// (or invalid) rows gather their own X row with weight 0. Shuffles therefore use the full mask and
 /// compile to plain SHFL without divergence bookkeeping.
-/// FULL: every lane's CPL columns are in range (N == G*CPL), no bounds logic in the gather loop.
-template <int G, int CPL, bool SHIFT, bool FULL = false>
+/// FULL (nonzero): interleaved pair layout; 1 = every lane's CPL columns in range (N == G*CPL), no bounds logic
+/// in the gather loop; 2 = with the pair tail mask.
+/// Slot blocks beyond the warp's longest row are skipped (warp-uniform), so wide groups (G = 32) on short rows
+/// do not gather padding slots.
+template <int G, int CPL, bool SHIFT, int FULL = 0>
 __device__ __forceinline__ void row_product(int r, int rb, int re, const int32_t* __restrict__ col,
                                             const double* __restrict__ A, const double* __restrict__ B,
                                             const double* __restrict__ X, int ldx, int c0, int N, int l,
@@ -118,12 +129,13 @@ __device__ __forceinline__ void row_product(int r, int rb, int re, const int32_t
             if (k0 + b * G >= wmax) break;
 #pragma unroll
             for (int s0 = 0; s0 < G; s0 += UB) {
+                if (s0 > 0 && k0 + b * G + s0 >= wmax) break;
                 double x[UB][CPL];
 #pragma unroll
                 for (int u = 0; u < UB; ++u) {
                     const int j = __shfl_sync(0xffffffffu, mc[b], gbase + s0 + u);
                     if (FULL)
-                        load_full<G, CPL>(X + size_t(j) * ldx, l, x[u]);
+                        load_full<G, CPL, FULL>(X + size_t(j) * ldx, l, N, x[u]);
                     else
                         load_cols<CPL>(X + size_t(j) * ldx + c0, c0, N, x[u]);
                 }
@@ -171,7 +183,7 @@ struct RowChunk {
 
 /// Row product with the first super-chunk already in registers (software-pipelined across row tiles);
 /// further super-chunks (rows longer than 16 entries, adaptive meshes) are loaded in place.
-template <int G, int CPL, bool SHIFT, bool FULL>
+template <int G, int CPL, bool SHIFT, int FULL>
 __device__ __forceinline__ void row_product_pf(int r, RowChunk<G, SHIFT>& ch, const int32_t* __restrict__ col,
                                                const double* __restrict__ A, const double* __restrict__ B,
                                                const double* __restrict__ X, int ldx, int c0, int N, int l, int gbase,
@@ -188,12 +200,13 @@ __device__ __forceinline__ void row_product_pf(int r, RowChunk<G, SHIFT>& ch, co
             if (k0 + b * G >= wmax) break;
 #pragma unroll
             for (int s0 = 0; s0 < G; s0 += UB) {
+                if (s0 > 0 && k0 + b * G + s0 >= wmax) break;
                 double x[UB][CPL];
 #pragma unroll
                 for (int u = 0; u < UB; ++u) {
                     const int j = __shfl_sync(0xffffffffu, ch.mc[b], gbase + s0 + u);
                     if (FULL)
-                        load_full<G, CPL>(X + size_t(j) * ldx, l, x[u]);
+                        load_full<G, CPL, FULL>(X + size_t(j) * ldx, l, N, x[u]);
                     else
                         load_cols<CPL>(X + size_t(j) * ldx + c0, c0, N, x[u]);
                 }

@@ -38,7 +38,7 @@ def sphere_atoms(n=60, r=6.7, dmin=2.5, seed=60):
     return [[6.0, *p] for p in pts]
 
 
-def run(name, atoms, N, box, refine, sweeps, steps=2):
+def run(name, atoms, N, box, refine, sweeps, steps=2, profile=True):
     h = kb.Hierarchy()
     m = kb.Mesh.box([-box] * 3, [box] * 3, 8)
     h.push(m)
@@ -64,6 +64,23 @@ def run(name, atoms, N, box, refine, sweeps, steps=2):
         out["steps"].append({k: round(lg[k], 3) for k in ("ms_bvp", "ms_hartree", "ms_project", "ms_inner", "ms_total")}
                             | {"cg": lg["cg_iterations"], "attempts": sorted(set(lg["attempts"]))})
     print(json.dumps(out), flush=True)
+    if profile:
+        ctx.reset_counters()
+        ctx.set_profiling(True)
+        try:
+            L.correction_step(lam, Phi, w, ld=ld, fixed_sweeps=sweeps)
+        except kb.KsbError:
+            pass
+        ctx.set_profiling(False)
+        names = ["cg_coop", "spmm", "cg_update_r", "cg_update_px", "cg_trueres", "inner_tridiag", "inner:gemm",
+                 "inner:gemv", "inner:border_pre", "inner:border_q", "inner:arrow_eig", "inner:arrow_vec",
+                 "inner:select", "inner:hartree_delta", "inner:coarse_wmass", "inner:build_", "inner:coarse_sq",
+                 "inner:coarse_vec_asm", "project", "project_asm", "assemble", "axpby", "sqload", "rho_vxc",
+                 "elementwise", "norm", "expand", "moments"]
+        rows = sorted(((ctx.kernel_time(n)[0], n, ctx.kernel_time(n)[1]) for n in names), reverse=True)
+        for ms, n, cnt in rows[:14]:
+            if cnt:
+                print(f"  {n:24s} {ms:9.3f} ms {cnt:6d} launches", flush=True)
     L.close()
     ctx.close()
 
