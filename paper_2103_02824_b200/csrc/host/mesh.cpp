@@ -84,6 +84,7 @@ struct Bisector {
     };
     std::vector<Elem> work;
     EdgeTable split;
+    std::vector<uint8_t> vsplit;  // vertex is an endpoint of a split edge: cheap pre-filter for the closure scan
 
     explicit Bisector(const Mesh& m) : in(m), xyz(m.xyz), vpar(m.vparent) {
         const int nt = m.n_tets();
@@ -107,6 +108,8 @@ struct Bisector {
         vpar.push_back(std::min(a, b));
         vpar.push_back(std::max(a, b));
         split.insert(key, v);
+        if (vsplit.size() < size_t(v) + 1) vsplit.resize(std::max(size_t(v) + 1, vsplit.size() * 2), 0);
+        vsplit[size_t(a)] = vsplit[size_t(b)] = 1;
         return v;
     }
 
@@ -128,6 +131,10 @@ struct Bisector {
     }
 
     bool touches_split_edge(const Elem& e) const {
+        // an element can only contain a split edge if two of its vertices are split-edge endpoints
+        int flagged = 0;
+        for (int i = 0; i < 4; ++i) flagged += size_t(e.t[i]) < vsplit.size() && vsplit[size_t(e.t[i])];
+        if (flagged < 2) return false;
         for (int i = 0; i < 4; ++i)
             for (int j = i + 1; j < 4; ++j)
                 if (split.find(edge_id(e.t[i], e.t[j])) >= 0) return true;
@@ -184,28 +191,26 @@ void Mesh::finalize() {
     const int nv = n_vertices();
     const int nt = n_tets();
     on_boundary.assign(nv, 0);
-    bface.clear();
-    iface.clear();
-    iface_tets.clear();
-    iface_geom.clear();
 
     // Face records bucketed by their smallest vertex (counting sort), then each
     // bucket sorted by (b, c, tet): identical to ordered-map key order with
-    // owners in ascending tet order.
+    // owners in ascending tet order. Buckets are independent, so they are sorted
+    // and classified in parallel; a count pass and a prefix sum place every
+    // bucket's faces at their sequential (ascending key) position.
     struct Rec {
         int32_t b, c, t;
     };
     static const int local[4][3] = {{1, 2, 3}, {0, 2, 3}, {0, 1, 3}, {0, 1, 2}};
-    std::vector<int64_t> start(size_t(nv) + 1, 0);
     std::vector<std::array<int32_t, 3>> keys(size_t(nt) * 4);
+#pragma omp parallel for schedule(static)
     for (int t = 0; t < nt; ++t)
         for (int f = 0; f < 4; ++f) {
-            std::array<int32_t, 3> k{tets[4 * t + local[f][0]], tets[4 * t + local[f][1]],
-                                     tets[4 * t + local[f][2]]};
+            std::array<int32_t, 3> k{tets[4 * t + local[f][0]], tets[4 * t + local[f][1]], tets[4 * t + local[f][2]]};
             std::sort(k.begin(), k.end());
             keys[size_t(t) * 4 + f] = k;
-            ++start[k[0] + 1];
         }
+    std::vector<int64_t> start(size_t(nv) + 1, 0);
+    for (size_t i = 0; i < keys.size(); ++i) ++start[keys[i][0] + 1];
     for (int v = 0; v < nv; ++v) start[v + 1] += start[v];
     std::vector<Rec> rec(size_t(nt) * 4);
     {
@@ -218,6 +223,10 @@ void Mesh::finalize() {
     }
     keys.clear();
     keys.shrink_to_fit();
+    // pass 1: sort each bucket, count its boundary and interior faces
+    std::vector<int64_t> nb(size_t(nv) + 1, 0), ni(size_t(nv) + 1, 0);
+    int bad = 0;
+#pragma omp parallel for schedule(dynamic, 4096) reduction(| : bad)
     for (int a = 0; a < nv; ++a) {
         auto* lo_ = rec.data() + start[a];
         auto* hi_ = rec.data() + start[a + 1];
@@ -226,23 +235,54 @@ void Mesh::finalize() {
             if (x.c != y.c) return x.c < y.c;
             return x.t < y.t;
         });
+        int64_t cb = 0, ci = 0;
         for (auto* p = lo_; p < hi_;) {
             auto* q = p + 1;
             while (q < hi_ && q->b == p->b && q->c == p->c) ++q;
             const int64_t cnt = q - p;
+            if (cnt == 1)
+                ++cb;
+            else if (cnt == 2)
+                ++ci;
+            else
+                bad = 1;
+            p = q;
+        }
+        nb[size_t(a) + 1] = cb;
+        ni[size_t(a) + 1] = ci;
+    }
+    if (bad) raise(KSB_INTERNAL, "face shared by more than two tets");
+    for (int a = 0; a < nv; ++a) {
+        nb[size_t(a) + 1] += nb[size_t(a)];
+        ni[size_t(a) + 1] += ni[size_t(a)];
+    }
+    bface.assign(size_t(nb[nv]) * 3, 0);
+    iface.assign(size_t(ni[nv]) * 3, 0);
+    iface_tets.assign(size_t(ni[nv]) * 2, 0);
+    iface_geom.assign(size_t(ni[nv]) * 5, 0.0);
+    // pass 2: write the faces at their offsets
+#pragma omp parallel for schedule(dynamic, 4096)
+    for (int a = 0; a < nv; ++a) {
+        const auto* lo_ = rec.data() + start[a];
+        const auto* hi_ = rec.data() + start[a + 1];
+        int64_t jb = nb[a], ji = ni[a];
+        for (auto* p = lo_; p < hi_;) {
+            auto* q = p + 1;
+            while (q < hi_ && q->b == p->b && q->c == p->c) ++q;
             const int32_t fa = a, fb = p->b, fc = p->c;
-            if (cnt == 1) {
-                bface.push_back(fa);
-                bface.push_back(fb);
-                bface.push_back(fc);
-                on_boundary[fa] = on_boundary[fb] = on_boundary[fc] = 1;
-            } else if (cnt == 2) {
+            if (q - p == 1) {
+                int32_t* o = &bface[size_t(jb++) * 3];
+                o[0] = fa;
+                o[1] = fb;
+                o[2] = fc;
+            } else {
                 const int32_t tp = std::min(p[0].t, p[1].t), tm = std::max(p[0].t, p[1].t);
-                iface.push_back(fa);
-                iface.push_back(fb);
-                iface.push_back(fc);
-                iface_tets.push_back(tp);
-                iface_tets.push_back(tm);
+                int32_t* o = &iface[size_t(ji) * 3];
+                o[0] = fa;
+                o[1] = fb;
+                o[2] = fc;
+                iface_tets[size_t(ji) * 2] = tp;
+                iface_tets[size_t(ji) * 2 + 1] = tm;
                 const double* A = &xyz[3 * fa];
                 const double* B = &xyz[3 * fb];
                 const double* C = &xyz[3 * fc];
@@ -270,13 +310,18 @@ void Mesh::finalize() {
                 for (int d = 0; d < 3; ++d) s += nrm[d] * ((A[d] + B[d] + C[d]) / 3.0 - cp[d] / 4.0);
                 if (s < 0)
                     for (double& x : nrm) x = -x;
-                iface_geom.insert(iface_geom.end(), {nrm[0], nrm[1], nrm[2], area, diam});
-            } else {
-                raise(KSB_INTERNAL, "face shared by more than two tets");
+                double* g = &iface_geom[size_t(ji) * 5];
+                g[0] = nrm[0];
+                g[1] = nrm[1];
+                g[2] = nrm[2];
+                g[3] = area;
+                g[4] = diam;
+                ++ji;
             }
             p = q;
         }
     }
+    for (size_t i = 0; i < bface.size(); ++i) on_boundary[size_t(bface[i])] = 1;
 }
 
 MeshPtr build_box_mesh(const double lo[3], const double hi[3], int n) {
