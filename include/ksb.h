@@ -269,6 +269,13 @@ int ksb_inner_scf(ksb_level* l, const ksb_step_opts* o, const double* h_lambda, 
 /* corr::expand of the last inner state (proj/src/correction.cpp:370-381) */
 int ksb_expand(ksb_level* l, const double* d_PhiT, int ld, const double* d_wt_full, const double* d_bcb,
                double* d_Phi, double* d_w_full);
+/* fem::SpaceHierarchy::prolong one level up (proj/src/fespace.cpp:76-84, rows of prolongation_matrix :35-56), the
+ * nested warm start of driver::run (proj/src/driver.cpp:367-371): out = P_step in, per column, summed in ascending
+ * previous-vertex order without fused multiply-add (bit-exact with the reference's sparse product).
+ * in: previous level, full vertex layout (in_interior = 0, n_prev rows) or interior block (1, zero boundary);
+ * out: this level, full (out_interior = 0, n rows) or interior block (1, ni rows). Row-major, leading dims given. */
+int ksb_prolong(ksb_level* l, const double* d_in, int in_interior, int ld_in, int ncols, double* d_out,
+                int out_interior, int ld_out);
 /* est::compute_indicators (proj/src/estimator.cpp:11-85): element residual of (V_ext + w + v_xc - lambda_i) phi_i
  * plus half-flux jumps across interior faces; d_eta gets eta_T^2 for every tet (n_tets), h_total_sq their sum.
  * Orbitals: interior block (N = the system's n_pairs columns); w, v_xc full length. */

@@ -114,6 +114,7 @@ PROTOTYPES = {
     "ksb_density": (I, [P, P, I, I, D, P]),
     "ksb_xc_field": (I, [P, I, D, D, P, P]),
     "ksb_indicators": (I, [P, DP, P, I, P, P, P, DP]),
+    "ksb_prolong": (I, [P, P, I, I, I, P, I, I]),
     "ksb_dorfler_mark": (I, [DP, C.c_int64, D, D, IP, C.POINTER(C.c_int64)]),
     "ksb_outer_build": (I, [P, I, P, P, DP]),
     "ksb_outer_apply": (I, [P, SOP, DP, P, I, I, P, IP, IP]),

@@ -393,6 +393,14 @@ class Level:
         m = np.ascontiguousarray(moments, np.float64)
         check(lib.ksb_boundary_values(self._h, _dp(m), bcb.ptr))
 
+    def prolong(self, src: DeviceArray, dst: DeviceArray, src_interior: bool, dst_interior: bool, ncols=None):
+        """fem::SpaceHierarchy::prolong from the previous level (proj/src/fespace.cpp:76-84), bit-exact:
+        src on level-1 (full vertex rows or interior block), dst on this level (full or interior block)."""
+        sc = src.shape[1] if len(src.shape) > 1 else 1
+        dc = dst.shape[1] if len(dst.shape) > 1 else 1
+        check(lib.ksb_prolong(self._h, src.ptr, int(src_interior), sc, int(ncols or min(sc, dc)), dst.ptr,
+                              int(dst_interior), dc))
+
     def sqload(self, Phi: DeviceArray, out: DeviceArray, N=None, ld=None):
         check(lib.ksb_sqload(self._h, Phi.ptr, int(N or self.N), int(ld or Phi.shape[1]), out.ptr))
 

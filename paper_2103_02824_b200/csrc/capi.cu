@@ -387,6 +387,12 @@ int ksb_level_create(ksb_ctx* c, const ksb_hier* h, int level, ksb_level** out) 
             L.sell_col.upload(cx, T.sell_col);
             L.sell_map.upload(cx, T.sell_map);
             L.nslices = int(T.sell_ptr.size()) - 1;
+            L.n_prev = T.n_prev;
+            if (T.n_prev > 0) {
+                L.pstep_col.upload(cx, T.pstep_col);
+                L.pstep_val.upload(cx, T.pstep_val);
+                L.prev_iidx.upload(cx, T.prev_iidx);
+            }
             for (int d = 0; d < 3; ++d) {
                 L.box_lo[d] = M.lo[d];
                 L.box_hi[d] = M.hi[d];
@@ -957,6 +963,18 @@ int ksb_expand(ksb_level* l, const double* d_PhiT, int ld, const double* d_wt, c
         need(d_PhiT && d_wt && d_bcb && d_Phi && d_w, "null argument");
         ksb::expand(l->L, K, d_PhiT, ld, d_wt, d_bcb, d_Phi, ld, d_w);
         KSB_CUDA_CHECK(cudaStreamSynchronize(l->L.ctx->stream));
+    });
+}
+
+int ksb_prolong(ksb_level* l, const double* d_in, int in_interior, int ld_in, int ncols, double* d_out,
+                int out_interior, int ld_out) {
+    return guard([&] {
+        need(l && d_in && d_out, "null argument");
+        auto& L = l->L;
+        if (L.n_prev == 0) ksb::raise(KSB_HIERARCHY, "level 0 has no previous level");
+        if (ncols < 1 || ld_in < ncols || ld_out < ncols) ksb::raise(KSB_INVALID_ARGUMENT, "need 1 <= ncols <= ld");
+        ksb::prolong(L, d_in, in_interior != 0, ld_in, ncols, d_out, out_interior != 0, ld_out);
+        KSB_CUDA_CHECK(cudaStreamSynchronize(L.ctx->stream));
     });
 }
 

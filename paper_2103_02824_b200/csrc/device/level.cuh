@@ -61,6 +61,9 @@ struct Level {
     DevBuf<double> cxyz;
     DevBuf<int32_t> sell_ptr, sell_col, sell_map;
     int nslices = 0;
+    DevBuf<int32_t> pstep_col, prev_iidx;   // one-step prolongation from level-1 (empty on level 0)
+    DevBuf<double> pstep_val;
+    int n_prev = 0;
     double box_lo[3] = {0, 0, 0}, box_hi[3] = {0, 0, 0};
     DevBuf<double> ebuf;      // element matrices, 16 per tet (scratch)
     DevBuf<double> scratch;   // term accumulation scratch (nnz_ii + nnz_ib)

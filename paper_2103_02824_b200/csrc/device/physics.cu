@@ -436,4 +436,42 @@ std::array<double, 5> energy(Level& L, const double* Phi, int N, int ld, const d
     return e;
 }
 
+namespace {
+/// out row = sum over the step row's (u, w) of w * in(u), ascending u, mul and add rounded separately
+/// (the reference's col-major sparse product compiled without contraction)
+__global__ void k_prolong(int rows, int ncols, const int32_t* __restrict__ out_vertex, const int32_t* __restrict__ pcol,
+                          const double* __restrict__ pval, const int32_t* __restrict__ prev_iidx,
+                          const double* __restrict__ in, int ld_in, double* __restrict__ out, int ld_out) {
+    const int64_t total = int64_t(rows) * ncols;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+        const int r = int(e / ncols), c = int(e % ncols);
+        const int v = out_vertex ? out_vertex[r] : r;
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int u = pcol[4 * size_t(v) + k];
+            if (u < 0) break;
+            double x;
+            if (prev_iidx) {
+                const int q = prev_iidx[u];
+                x = q >= 0 ? in[size_t(q) * ld_in + c] : 0.0;
+            } else {
+                x = in[size_t(u) * ld_in + c];
+            }
+            acc = __dadd_rn(acc, __dmul_rn(pval[4 * size_t(v) + k], x));
+        }
+        out[size_t(r) * ld_out + c] = acc;
+    }
+}
+}  // namespace
+
+void prolong(Level& L, const double* in, bool in_interior, int ld_in, int ncols, double* out, bool out_interior,
+             int ld_out) {
+    Ctx& c = *L.ctx;
+    const int rows = out_interior ? L.ni : L.n;
+    launch(c, "prolong", k_prolong, grid_of(c, int64_t(rows) * ncols), kT, 0, rows, ncols,
+           out_interior ? (const int32_t*)L.interior.p : nullptr, (const int32_t*)L.pstep_col.p,
+           (const double*)L.pstep_val.p, in_interior ? (const int32_t*)L.prev_iidx.p : nullptr, in, ld_in, out, ld_out);
+}
+
 } // namespace ksb

@@ -50,4 +50,8 @@ std::array<double, 2> norms_sq(Level& L, const double* f_full, PhysWork& w);
 std::array<double, 5> energy(Level& L, const double* Phi, int N, int ld, const double* rho_full, const double* w_full,
                              const std::vector<double>& atoms, double occ, const XcParams& xc, PhysWork& w);
 
+/// one-level prolongation of nodal columns (see ksb_prolong)
+void prolong(Level& L, const double* in, bool in_interior, int ld_in, int ncols, double* out, bool out_interior,
+             int ld_out);
+
 } // namespace ksb

@@ -337,6 +337,54 @@ std::shared_ptr<FineTopology> build_topology(const Hierarchy& h, int level) {
         std::vector<int32_t> fill(topo->anc_ptr.begin(), topo->anc_ptr.end() - 1);
         for (int t = 0; t < nt; ++t) topo->anc_tets[fill[topo->ancestor[t]]++] = t;
     }
+    if (level > 0) {
+        // rows in creation order (parents precede children), accumulated like the reference's per-row map:
+        // 0 + 0.5 w over the first parent's entries, then the second's; stored in ascending column order
+        const Mesh& pm = h.mesh(level - 1);
+        topo->n_prev = pm.n_vertices();
+        topo->prev_iidx = Space(h.mesh_ptr(level - 1)).iidx;
+        const int npv = m.n_parent_vertices;
+        if (npv != topo->n_prev) raise(KSB_HIERARCHY, "levels are not nested");
+        topo->pstep_col.assign(size_t(nv) * 4, -1);
+        topo->pstep_val.assign(size_t(nv) * 4, 0.0);
+        for (int v = 0; v < nv; ++v) {
+            int32_t* pc = &topo->pstep_col[size_t(v) * 4];
+            double* pv = &topo->pstep_val[size_t(v) * 4];
+            if (v < npv) {
+                pc[0] = v;
+                pv[0] = 1.0;
+                continue;
+            }
+            int32_t cc[8];
+            double cv[8];
+            int w = 0;
+            for (int side = 0; side < 2; ++side) {
+                const int32_t par = m.vparent[2 * size_t(v) + side];
+                if (par >= v) raise(KSB_INTERNAL, "vertex parent created after its child");
+                const int32_t* qc = &topo->pstep_col[size_t(par) * 4];
+                const double* qv = &topo->pstep_val[size_t(par) * 4];
+                for (int k = 0; k < 4 && qc[k] >= 0; ++k) {
+                    int j = 0;
+                    while (j < w && cc[j] != qc[k]) ++j;
+                    if (j == w) {
+                        cc[w] = qc[k];
+                        cv[w++] = 0.0;
+                    }
+                    cv[j] += 0.5 * qv[k];
+                }
+            }
+            if (w > 4) raise(KSB_INTERNAL, "prolongation row wider than 4");
+            for (int i = 1; i < w; ++i)  // insertion sort by column
+                for (int j = i; j > 0 && cc[j - 1] > cc[j]; --j) {
+                    std::swap(cc[j - 1], cc[j]);
+                    std::swap(cv[j - 1], cv[j]);
+                }
+            for (int k = 0; k < w; ++k) {
+                pc[k] = cc[k];
+                pv[k] = cv[k];
+            }
+        }
+    }
     return topo;
 }
 

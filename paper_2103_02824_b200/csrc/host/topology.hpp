@@ -76,6 +76,12 @@ struct FineTopology {
     // SELL-32 view of the ii pattern: slice s = rows [32s, 32s+32), entry e of lane i at
     // sell_ptr[s] + 32 e + i; padding entries point at the row itself with map = -1
     std::vector<int32_t> sell_ptr, sell_col, sell_map;
+    // one-step prolongation from level-1 (fem::prolongation_matrix, proj/src/fespace.cpp:35-56): per vertex <= 4
+    // (previous-level vertex, weight), ascending vertex, -1 padded; empty on level 0. prev_iidx: the previous
+    // level's vertex -> interior index (interior-block inputs).
+    int n_prev = 0;
+    std::vector<int32_t> pstep_col, prev_iidx;
+    std::vector<double> pstep_val;
 };
 
 std::shared_ptr<FineTopology> build_topology(const Hierarchy& h, int level);

@@ -111,9 +111,9 @@ def run(ctx: api.Context, atoms, n_pairs: int, occupancy: float, xc: str, box: f
     h = api.Hierarchy()
     mesh = api.Mesh.box([-box] * 3, [box] * 3, n_coarse)
     h.push(mesh)
-    lam = orb_full = w_full = None
+    lam = Phi = w = None
     eta = tot = None
-    L = None
+    L = prev = None
     try:
         for level in range(max_levels):
             t_level = time.perf_counter()
@@ -124,12 +124,10 @@ def run(ctx: api.Context, atoms, n_pairs: int, occupancy: float, xc: str, box: f
                 else:
                     mesh = mesh.adapt_refine(api.dorfler_mark(eta, tot, theta))
                 h.push(mesh)
-            if L is not None:
-                L.close()
+            prev = L
             L = api.Level(ctx, h, level)
             L.set_system(atoms, n_pairs=n_pairs, occupancy=occupancy, xc=xc)
             L.level_ops()
-            it = L.index("interior")
             t_refine = time.perf_counter() - t0
             t1 = time.perf_counter()
             if level == 0:
@@ -137,12 +135,13 @@ def run(ctx: api.Context, atoms, n_pairs: int, occupancy: float, xc: str, box: f
                                                            tol_eig=tol_eig)
                 outer, inner = scf_it, []
             else:
-                orb_full = prolong(mesh, orb_full)
-                w_full = prolong(mesh, w_full)
+                # nested warm start on the device (proj/src/driver.cpp:367-371): orbitals as interior blocks
+                # (zero trace), the Hartree potential with its boundary values
                 ld = n_pairs if n_pairs == 1 else n_pairs + (n_pairs & 1)
-                blk = np.zeros((L.ni, ld))
-                blk[:, :n_pairs] = orb_full[it]
-                Phi, w = ctx.to_device(blk), ctx.to_device(w_full)
+                Phi_new, w_new = ctx.to_device(np.zeros((L.ni, ld))), ctx.empty((L.n,))
+                L.prolong(Phi, Phi_new, True, True, ncols=n_pairs)
+                L.prolong(w, w_new, False, False)
+                Phi, w = Phi_new, w_new
                 res = solve_level_corrected(L, lam, Phi, w, tol_outer=tol_outer, max_outer=max_outer, level=level,
                                             **step_opts)
                 outer, inner = res.outer_iterations, res.inner_iterations
@@ -155,10 +154,8 @@ def run(ctx: api.Context, atoms, n_pairs: int, occupancy: float, xc: str, box: f
             eta, tot = L.indicators(lam, Phi, w, vxc)
             t_estimate = time.perf_counter() - t2
             energy = L.energy(Phi, w)
-            P = Phi.download()
-            orb_full = np.zeros((L.n, n_pairs))
-            orb_full[it] = P[:, :n_pairs]
-            w_full = w.download()
+            if prev is not None:
+                prev.close()
             log.records.append(LevelRecord(level, L.nt, L.n, np.asarray(lam).tolist(), np.asarray(energy).tolist(),
                                            float(tot), outer, inner, t_refine, t_solve, t_estimate,
                                            time.perf_counter() - t_level))
@@ -166,7 +163,8 @@ def run(ctx: api.Context, atoms, n_pairs: int, occupancy: float, xc: str, box: f
         log.aborted = True
         log.abort_reason = str(e)
     finally:
-        if L is not None:
-            L.close()
+        for lv in (prev, L):
+            if lv is not None:
+                lv.close()
     log.wall_seconds = time.perf_counter() - t_start
     return log
