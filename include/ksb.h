@@ -209,6 +209,21 @@ int ksb_correction_step(ksb_level* l, const ksb_step_opts* o, double* h_lambda, 
 int ksb_correction_step_host(ksb_level* l, const ksb_step_opts* o, double* h_lambda, double* h_Phi, int ld,
                              double* h_w, ksb_step_log* log, int* h_attempts, int* h_iters);
 
+/* Standard multilevel correction, the reference's comparison method (driver::solve_level_mlc,
+ * proj/src/driver.cpp:200-302), split at its sweep loop so the host keeps the loop, the stopping test and the
+ * iteration-cap error:
+ *   ksb_mlc_begin: orbital BVPs with the warm start's potentials (h_lambda, d_Phi, d_w unchanged), Hartree
+ *     boundary data from the phi_tilde density; the correction-space state starts pure (phi_H = 0, theta = 1).
+ *   ksb_mlc_sweep: Hartree potential of the current density, pot = w + v_xc, one bordered solve per orbital with
+ *     A_H1 + P^T M_pot P (sign-aligned with the previous sweep), expansion into d_Phi, lambdas into h_lambda,
+ *     h_delta = H1 norm of the density change.
+ *   ksb_mlc_finish: Hartree potential of the final density (zero when Hartree is off) and, if d_rho is not NULL,
+ *     the density itself (full length). */
+int ksb_mlc_begin(ksb_level* l, const ksb_step_opts* o, const double* h_lambda, const double* d_Phi, int ld,
+                  const double* d_w, ksb_step_log* log, int* h_attempts, int* h_iters);
+int ksb_mlc_sweep(ksb_level* l, const ksb_step_opts* o, double* h_lambda, double* d_Phi, int ld, double* h_delta);
+int ksb_mlc_finish(ksb_level* l, const ksb_step_opts* o, double* d_w_full, double* d_rho_full);
+
 /* scf::self_consistent_solve on the coarsest space (proj/src/scf.cpp:22-90), level 0 of the hierarchy:
  * dense lowest eigenpairs of the current Hamiltonian, linear density mixing, Hartree potential of the mixed
  * density. Outputs: lambdas (N, host), orbitals (interior block, device), mixed density and Hartree potential

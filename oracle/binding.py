@@ -67,6 +67,7 @@ _PROTO = {
     "orc_prolong_vec": (I, [P, I, I, DP, I, DP]),
     "orc_coarse_scf": (I, [P, D, I, D, D, DP, DP, DP, IP]),
     "orc_correction_step": (I, [P, I, DP, IP, DP, DP, DP, IP, DP]),
+    "orc_solve_level_mlc": (I, [P, I, DP, IP, D, I, DP, DP, DP, DP, IP, DP, I]),
     "orc_outer_solve": (I, [P, I, DP, DP, DP, DP, D, I, DP, IP, IP, DP]),
     "orc_prepare_blocks": (I, [P, I, DP, DP, DP, DP, I, PP]),
     "orc_blocks_free": (None, [P]),
@@ -347,6 +348,21 @@ class Oracle:
                "delta": ld[0], "t_bvp": ld[1], "t_hartree": ld[2], "t_blocks": ld[3], "t_inner": ld[4],
                "t_total": ld[5]}
         return lam, orb, w, log
+
+    def solve_level_mlc(self, level, lambdas, orb, w, tol_outer=1e-6, max_scf=200, tol_linear=1e-9, tol_inner=1e-8,
+                        score_floor=1e-8, max_inner=400, nev_pad=4, precond=0):
+        """driver::solve_level_mlc (proj/src/driver.cpp:200-302): (lambdas, orbitals, w, rho, deltas)"""
+        lam = f64(lambdas).copy()
+        orb = f64(orb).copy()
+        w = f64(w).copy()
+        rho = np.empty(self.n(level))
+        cd = np.array([tol_linear, tol_inner, score_floor])
+        ci = np.array([max_inner, nev_pad, precond], np.int32)
+        sw = C.c_int()
+        ds = np.zeros(max(1, max_scf))
+        _chk(lib.orc_solve_level_mlc(self._h, level, dp(cd), ip(ci), float(tol_outer), int(max_scf), dp(lam), dp(orb),
+                                     dp(w), dp(rho), C.byref(sw), dp(ds), len(ds)))
+        return lam, orb, w, rho, ds[:sw.value]
 
     def outer_solve(self, level, w_hat, vxc, lambdas, orb, tol=1e-9, precond=0):
         n = self.n(level)

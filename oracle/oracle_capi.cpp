@@ -505,6 +505,33 @@ int orc_correction_step(orc_problem* p, int level, const double* cfg_d, const in
     });
 }
 
+int orc_solve_level_mlc(orc_problem* p, int level, const double* cfg_d, const int* cfg_i, double tol_outer,
+                        int max_scf, double* lambdas, double* orb, double* w, double* rho, int* sweeps,
+                        double* deltas, int deltas_cap) {
+    return guard([&] {
+        auto& o = p->p.level(level);
+        const int N = p->p.sys.n_pairs;
+        const int n = o.V->n();
+        StepConfig c;
+        c.tol_linear = cfg_d[0];
+        c.tol_inner = cfg_d[1];
+        c.score_floor = cfg_d[2];
+        c.max_inner = cfg_i[0];
+        c.nev_pad = cfg_i[1];
+        c.precond = cfg_i[2];
+        Vec lam(lambdas, lambdas + N);
+        auto orbs = unpack(orb, n, N);
+        Vec wv(w, w + n), r;
+        std::vector<double> ds;
+        solve_level_mlc(p->p.sys, p->p.hier, o, c, tol_outer, max_scf, lam, orbs, wv, r, sweeps, &ds);
+        std::memcpy(lambdas, lam.data(), sizeof(double) * N);
+        pack(orbs, orb);
+        std::memcpy(w, wv.data(), sizeof(double) * n);
+        std::memcpy(rho, r.data(), sizeof(double) * n);
+        for (int k = 0; k < int(ds.size()) && k < deltas_cap; ++k) deltas[k] = ds[k];
+    });
+}
+
 /// bvp_orbital for every orbital: phi_tilde (row-major n x N), attempts[N], iters[N]
 int orc_outer_solve(orc_problem* p, int level, const double* w_hat, const double* vxc, const double* lambdas,
                     const double* orb, double tol, int precond, double* phi_tilde, int* attempts, int* iters,

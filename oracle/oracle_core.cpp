@@ -1843,4 +1843,65 @@ void correction_step(const System& s, const Hier& h, const LevelOps& ops, const 
     }
 }
 
+// proj/src/driver.cpp:200-302. The reference builds A_H = A_H1 + P^T M_pot P, b = b_H1 + P^T M_pot phi_tilde and
+// beta = beta1 + phi_tilde^T M_pot phi_tilde each sweep and solves the bordered problems directly; here the same
+// terms come from prepare_blocks with pot in the v_xc slot (A_H4 = P^T M_pot P, b_H4, beta4 are exactly those
+// products) and one Hartree-off inner sweep (A_H1 + A_H4, b_H1 + b_H4, beta1 + beta4), sign-aligned with the
+// previous sweep's state as the reference does.
+void solve_level_mlc(const System& s, const Hier& h, const LevelOps& ops, const StepConfig& cfg, double tol_outer,
+                     int max_scf, Vec& lambdas, std::vector<Vec>& orbitals, Vec& w, Vec& rho, int* sweeps,
+                     std::vector<double>* deltas) {
+    const int N = s.n_pairs;
+    const Space& V = *ops.V;
+    const Vec zero(V.n(), 0.0);
+    const Vec rho_prev = density(orbitals, s.occ);
+    const Vec vxc_prev = s.xc_on ? xc_field(s, rho_prev) : zero;
+    Outer op(ops.V, ops.a_op, &ops.M, s.hartree_on ? w : zero, vxc_prev, cfg.tol_linear, cfg.precond);
+    std::vector<Vec> phi_t(N);
+    for (int i = 0; i < N; ++i) phi_t[i] = op.solve_orbital(lambdas[i], orbitals[i], nullptr, nullptr);
+    Vec bc(V.n(), 0.0);
+    if (s.hartree_on) bc = boundary_values(compute_moments(V, density(phi_t, s.occ)), V);
+    auto hartree_of = [&](const Vec& r) {  // hartree::solve_hartree_cached (proj/src/hartree.cpp:95-106)
+        Vec load = ops.M.mul(r);
+        for (double& x : load) x *= 4.0 * kPi;
+        SolveStats st;
+        Vec out = ops.stiff->solve(load, bc, cfg.tol_linear, &st);
+        if (!st.converged) fail(E_NONCONV, "hartree solve stalled");
+        return out;
+    };
+    const Blocks B0 = prepare_blocks(h.spaces[0], ops.V, ops.P_full, ops.S, ops.M, ops.a_op, phi_t, zero, zero, s.occ,
+                                     false, Vec());
+    AState state = pure_state(B0, lambdas);
+    std::vector<Vec> orb;
+    Vec wscr;
+    expand(state, B0, orb, wscr);
+    Vec rho_cur = density(orb, s.occ);
+    Vec w_cur(V.n(), 0.0);
+    int done = 0;
+    for (int sw = 1; sw <= max_scf; ++sw) {
+        const Vec vxc = s.xc_on ? xc_field(s, rho_cur) : zero;
+        if (s.hartree_on) w_cur = hartree_of(rho_cur);
+        Vec pot(V.n());
+        for (int i = 0; i < V.n(); ++i) pot[i] = w_cur[i] + vxc[i];
+        const Blocks B = prepare_blocks(h.spaces[0], ops.V, ops.P_full, ops.S, ops.M, ops.a_op, phi_t, zero, pot, s.occ,
+                                        false, Vec());
+        state = inner_scf(B, state, cfg.tol_inner, 1, cfg.score_floor, cfg.nev_pad).state;
+        expand(state, B, orb, wscr);
+        const Vec rho_next = density(orb, s.occ);
+        Vec d(V.n());
+        for (int i = 0; i < V.n(); ++i) d[i] = rho_next[i] - rho_cur[i];
+        const double delta = h1_norm(V, d);
+        if (deltas) deltas->push_back(delta);
+        rho_cur = rho_next;
+        done = sw;
+        if (delta < tol_outer) break;
+        if (sw == max_scf) fail(E_NONCONV, "correction-space iteration cap reached");
+    }
+    if (sweeps) *sweeps = done;
+    lambdas = state.lambda;
+    orbitals = orb;
+    w = s.hartree_on ? hartree_of(rho_cur) : zero;
+    rho = rho_cur;
+}
+
 }  // namespace orc

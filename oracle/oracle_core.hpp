@@ -303,5 +303,11 @@ struct StepLog {
 /// one outer iteration of solve_level_corrected (proj/src/driver.cpp:106-150)
 void correction_step(const System& s, const Hier& h, const LevelOps& ops, const StepConfig& cfg, Vec& lambdas,
                      std::vector<Vec>& orbitals, Vec& w, StepLog* log);
+/// solve_level_mlc (proj/src/driver.cpp:200-302): the standard multilevel correction on one level. In: warm
+/// lambdas / orbitals / Hartree potential; out: lambdas, expanded orbitals, Hartree potential of the final
+/// density, that density; sweeps run and the density change of each.
+void solve_level_mlc(const System& s, const Hier& h, const LevelOps& ops, const StepConfig& cfg, double tol_outer,
+                     int max_scf, Vec& lambdas, std::vector<Vec>& orbitals, Vec& w, Vec& rho, int* sweeps,
+                     std::vector<double>* deltas);
 
 } // namespace orc

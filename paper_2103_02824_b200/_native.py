@@ -103,6 +103,9 @@ PROTOTYPES = {
     "ksb_system_set": (I, [P, DP, I, I, D, I, D, D, I, I]),
     "ksb_level_ops": (I, [P]),
     "ksb_correction_step": (I, [P, SOP, DP, P, I, P, SLP, IP, IP]),
+    "ksb_mlc_begin": (I, [P, SOP, DP, P, I, P, SLP, IP, IP]),
+    "ksb_mlc_sweep": (I, [P, SOP, DP, P, I, DP]),
+    "ksb_mlc_finish": (I, [P, SOP, P, P]),
     "ksb_correction_step_host": (I, [P, SOP, DP, P, I, P, SLP, IP, IP]),
     "ksb_density_xc": (I, [P, P, I, I, P, P]),
     "ksb_moments": (I, [P, P, DP]),

@@ -362,6 +362,27 @@ class Level:
                                       C.byref(lg), _ip(att), _ip(its)))
         return self._log(lg, att, its)
 
+    def mlc_begin(self, lambdas: np.ndarray, Phi: DeviceArray, w: DeviceArray, **opts):
+        """standard MLC setup (proj/src/driver.cpp:206-243): orbital BVPs with the warm potentials, Hartree bc"""
+        o = self.step_options(**opts)
+        lg = _N.StepLog()
+        att = np.zeros(self.N, np.int32)
+        its = np.zeros(self.N, np.int32)
+        check(lib.ksb_mlc_begin(self._h, C.byref(o), _dp(np.ascontiguousarray(lambdas, np.float64)), Phi.ptr,
+                                int(Phi.shape[1]), w.ptr, C.byref(lg), _ip(att), _ip(its)))
+        return self._log(lg, att, its)
+
+    def mlc_sweep(self, lambdas: np.ndarray, Phi: DeviceArray, **opts) -> float:
+        """one correction-space sweep (proj/src/driver.cpp:244-300); lambdas and Phi updated, returns the H1 change"""
+        o = self.step_options(**opts)
+        d = C.c_double()
+        check(lib.ksb_mlc_sweep(self._h, C.byref(o), _dp(lambdas), Phi.ptr, int(Phi.shape[1]), C.byref(d)))
+        return d.value
+
+    def mlc_finish(self, w: DeviceArray, rho: DeviceArray | None = None, **opts):
+        o = self.step_options(**opts)
+        check(lib.ksb_mlc_finish(self._h, C.byref(o), w.ptr, rho.ptr if rho is not None else None))
+
     def correction_step_host(self, lambdas: np.ndarray, Phi: np.ndarray, w: np.ndarray, **opts):
         o = self.step_options(**opts)
         lg = _N.StepLog()

@@ -745,6 +745,35 @@ int ksb_correction_step_host(ksb_level* l, const ksb_step_opts* o, double* h_lam
     });
 }
 
+int ksb_mlc_begin(ksb_level* l, const ksb_step_opts* o, const double* h_lambda, const double* d_Phi, int ld,
+                  const double* d_w, ksb_step_log* log, int* att, int* its) {
+    return guard([&] {
+        auto& K = ready(l);
+        need(h_lambda && d_Phi && d_w, "null argument");
+        if (ld < K.sys.N || (K.sys.N > 1 && (ld & 1))) ksb::raise(KSB_INVALID_ARGUMENT, "bad ld");
+        ksb::StepLog lg;
+        ksb::mlc_begin(l->L, K, l->owner->cg, step_opts(o), h_lambda, d_Phi, ld, d_w, &lg);
+        fill_log(lg, log, att, its);
+    });
+}
+
+int ksb_mlc_sweep(ksb_level* l, const ksb_step_opts* o, double* h_lambda, double* d_Phi, int ld, double* h_delta) {
+    return guard([&] {
+        auto& K = ready(l);
+        need(h_lambda && d_Phi, "null argument");
+        const double d = ksb::mlc_sweep(l->L, K, l->owner->cg, step_opts(o), h_lambda, d_Phi, ld);
+        if (h_delta) *h_delta = d;
+    });
+}
+
+int ksb_mlc_finish(ksb_level* l, const ksb_step_opts* o, double* d_w, double* d_rho) {
+    return guard([&] {
+        auto& K = ready(l);
+        need(d_w, "null argument");
+        ksb::mlc_finish(l->L, K, l->owner->cg, step_opts(o), d_w, d_rho);
+    });
+}
+
 int ksb_density_xc(ksb_level* l, const double* d_Phi, int N, int ld, double* d_rho, double* d_vxc) {
     return guard([&] {
         need(l && d_Phi && d_rho, "null argument");

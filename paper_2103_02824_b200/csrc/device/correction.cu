@@ -397,6 +397,127 @@ void correction_step(Level& L, Corrector& K, CgWork& cg, const StepOptions& o, d
     if (log) *log = lg;
 }
 
+namespace {
+/// hartree::solve_hartree_cached (proj/src/hartree.cpp:95-106): S w = 4 pi M rho with Dirichlet data bcb. rho is a
+/// density of zero-trace orbitals, so M rho restricted to interior rows is M_ii rho_int.
+void hartree_of_density(Level& L, Corrector& K, CgWork& cg, const double* d_rho, const double* d_bcb, double tol,
+                        double* d_w_full) {
+    Ctx& c = *L.ctx;
+    const int ni = L.ni;
+    need(K.hrhs, ni);
+    need(K.wtil_int, ni);
+    need(K.pot, ni);
+    launch(c, "elementwise", k_take_interior, grid_of(c, ni), kT, 0, ni, (const int32_t*)L.interior.p, d_rho, K.pot.p);
+    spmm(c, L, L.mats[1].ii.p, nullptr, nullptr, K.pot.p, 1, 1, K.hrhs.p, 1);
+    launch(c, "elementwise", k_add, grid_of(c, ni), kT, 0, int64_t(ni), (const double*)K.hrhs.p, kFourPi,
+           (const double*)K.hrhs.p, 0.0, K.hrhs.p);
+    lift(L, 0, d_bcb, K.hrhs.p);
+    CgOptions co;
+    co.tol = tol;
+    CgColumnStats cs;
+    cg_solve(c, L, 0, -1, nullptr, K.hrhs.p, K.wtil_int.p, 1, 1, co, &cs, cg);
+    if (!cs.converged)
+        raise(KSB_NONCONVERGENCE, "hartree solve stalled at residual " + std::to_string(cs.relative_residual));
+    launch(c, "elementwise", k_full_from, grid_of(c, L.n), kT, 0, ni, L.nb, (const int32_t*)L.interior.p,
+           (const int32_t*)L.boundary.p, (const double*)K.wtil_int.p, d_bcb, d_w_full);
+}
+}  // namespace
+
+void mlc_begin(Level& L, Corrector& K, CgWork& cg, const StepOptions& o, const double* h_lambda, const double* d_Phi,
+               int ld, const double* d_w, StepLog* log) {
+    Ctx& c = *L.ctx;
+    if (!K.ops_ready) level_ops(L, K);
+    const int N = K.sys.N, n = L.n, ni = L.ni;
+    for (auto* b : {&K.rho, &K.vxc, &K.what_full, &K.wt_full, &K.ell_full, &K.rho_t, &K.diff, &K.potf, &K.wscr})
+        need(*b, n);
+    need(K.bcb, std::max(1, L.nb));
+    need(K.PhiT, int64_t(ni) * ld);
+    // OuterOperator with the warm start's Hartree potential and v_xc(rho_prev) (driver.cpp:208-213)
+    rho_vxc(L, d_Phi, N, ld, K.sys.occ, K.sys.xc, K.rho.p, K.sys.xc_on ? K.vxc.p : nullptr);
+    if (!K.sys.xc_on) KSB_CUDA_CHECK(cudaMemsetAsync(K.vxc.p, 0, sizeof(double) * n, c.stream));
+    if (K.sys.hartree_on)
+        KSB_CUDA_CHECK(cudaMemcpyAsync(K.what_full.p, d_w, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream));
+    else
+        KSB_CUDA_CHECK(cudaMemsetAsync(K.what_full.p, 0, sizeof(double) * n, c.stream));
+    outer_operator(L, K, K.what_full.p, K.vxc.p);
+    StepLog lg;
+    solve_orbitals(L, K, cg, o, h_lambda, d_Phi, ld, K.PhiT.p, ld, &lg);
+    // Hartree boundary data from the moments of the phi_tilde density (driver.cpp:219-223)
+    KSB_CUDA_CHECK(cudaMemsetAsync(K.bcb.p, 0, sizeof(double) * std::max(1, L.nb), c.stream));
+    rho_vxc(L, K.PhiT.p, N, ld, K.sys.occ, K.sys.xc, K.rho_t.p, nullptr);
+    if (K.sys.hartree_on) {
+        const double ctr[3] = {0.5 * (L.box_lo[0] + L.box_hi[0]), 0.5 * (L.box_lo[1] + L.box_hi[1]),
+                               0.5 * (L.box_lo[2] + L.box_hi[2])};
+        boundary_values(L, moments(L, K.rho_t.p, K.phys, ctr), K.bcb.p);
+    }
+    // base blocks carry no static potential split (w_tilde = 0, lift = 0); rho_cur = density of the expansion of
+    // the pure state (phi_H = 0, theta = 1), i.e. of phi_tilde (driver.cpp:225-243)
+    KSB_CUDA_CHECK(cudaMemsetAsync(K.wt_full.p, 0, sizeof(double) * n, c.stream));
+    KSB_CUDA_CHECK(cudaMemsetAsync(K.ell_full.p, 0, sizeof(double) * n, c.stream));
+    KSB_CUDA_CHECK(cudaMemcpyAsync(K.rho.p, K.rho_t.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream));
+    KSB_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    K.mlc_ld = ld;
+    K.mlc_sweeps = 0;
+    if (log) *log = lg;
+}
+
+double mlc_sweep(Level& L, Corrector& K, CgWork& cg, const StepOptions& o, double* h_lambda, double* d_Phi, int ld) {
+    Ctx& c = *L.ctx;
+    if (K.mlc_ld == 0) raise(KSB_INVALID_ARGUMENT, "mlc_sweep before mlc_begin");
+    if (ld != K.mlc_ld) raise(KSB_INVALID_ARGUMENT, "mlc_sweep: ld differs from mlc_begin's");
+    const int N = K.sys.N, n = L.n;
+    // pot = w(rho_cur) + v_xc(rho_cur) (driver.cpp:244-248)
+    if (K.sys.xc_on)
+        xc_field(L, K.sys.xc, K.rho.p, K.vxc.p);
+    else
+        KSB_CUDA_CHECK(cudaMemsetAsync(K.vxc.p, 0, sizeof(double) * n, c.stream));
+    if (K.sys.hartree_on)
+        hartree_of_density(L, K, cg, K.rho.p, K.bcb.p, o.tol_linear, K.what_full.p);
+    else
+        KSB_CUDA_CHECK(cudaMemsetAsync(K.what_full.p, 0, sizeof(double) * n, c.stream));
+    launch(c, "elementwise", k_add, grid_of(c, n), kT, 0, int64_t(n), (const double*)K.what_full.p, 1.0,
+           (const double*)K.vxc.p, 1.0, K.potf.p);
+    // A_H = A_H1 + P^T M_pot P, b_i = b_H1 + P^T M_pot phi_tilde_i, beta_i = beta1 + phi_tilde_i^T M_pot phi_tilde_i
+    // (driver.cpp:250-265): the pot-weighted terms ride in the v_xc slots of the ledger (A_H4, b_H4, beta4),
+    // which a Hartree-off inner sweep adds to the a_op terms
+    project_blocks(L, K.PhiT.p, N, ld, K.wt_full.p, K.ell_full.p, K.potf.p, K.eext.p, K.proj);
+    InnerParams ip;
+    ip.tol = o.tol_inner;
+    ip.max_iterations = 1;
+    ip.score_floor = o.score_floor;
+    ip.nev_pad = o.nev_pad;
+    ip.hartree = false;
+    ip.occ = K.sys.occ;
+    // sign alignment against the previous sweep's state (driver.cpp:277-283): the inner state persists
+    inner_scf(L, K.coarse, K.proj, ip, h_lambda, K.inner, K.mlc_sweeps == 0);
+    expand(L, K, K.PhiT.p, ld, K.wt_full.p, K.bcb.p, d_Phi, ld, K.wscr.p);
+    // density change (driver.cpp:289-291)
+    rho_vxc(L, d_Phi, N, ld, K.sys.occ, K.sys.xc, K.rho_t.p, nullptr);
+    launch(c, "elementwise", k_add, grid_of(c, n), kT, 0, int64_t(n), (const double*)K.rho_t.p, 1.0,
+           (const double*)K.rho.p, -1.0, K.diff.p);
+    const auto nn = norms_sq(L, K.diff.p, K.phys);
+    KSB_CUDA_CHECK(cudaMemcpyAsync(K.rho.p, K.rho_t.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream));
+    KSB_CUDA_CHECK(cudaMemcpyAsync(h_lambda, K.inner.lamv[K.inner.cur].p, sizeof(double) * N, cudaMemcpyDeviceToHost,
+                                   c.stream));
+    KSB_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    ++K.mlc_sweeps;
+    const double l2 = std::sqrt(std::max(0.0, nn[0])), semi = std::sqrt(std::max(0.0, nn[1]));
+    return std::sqrt(l2 * l2 + semi * semi);
+}
+
+void mlc_finish(Level& L, Corrector& K, CgWork& cg, const StepOptions& o, double* d_w, double* d_rho) {
+    Ctx& c = *L.ctx;
+    if (K.mlc_ld == 0) raise(KSB_INVALID_ARGUMENT, "mlc_finish before mlc_begin");
+    const int n = L.n;
+    if (K.sys.hartree_on)
+        hartree_of_density(L, K, cg, K.rho.p, K.bcb.p, o.tol_linear, d_w);
+    else
+        KSB_CUDA_CHECK(cudaMemsetAsync(d_w, 0, sizeof(double) * n, c.stream));
+    if (d_rho) KSB_CUDA_CHECK(cudaMemcpyAsync(d_rho, K.rho.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream));
+    KSB_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    K.mlc_ld = 0;
+}
+
 ScfStats coarse_scf(Level& L, Corrector& K, CgWork& cg, const ScfParams& p, double* h_lambda, double* d_Phi, int ld,
                     double* d_rho, double* d_w) {
     Ctx& c = *L.ctx;

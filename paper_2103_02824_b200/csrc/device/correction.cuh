@@ -50,8 +50,10 @@ struct Corrector {
     // work vectors (full = n, int = ni, blocks = ni x ld)
     DevBuf<double> rho, vxc, pot, rho_t, bcb, wt_full, ell_full, what_full, diff, wtil_int, hrhs;
     DevBuf<double> R0, Bblk, Xblk, Bc, Xc, PhiT;
+    DevBuf<double> potf, wscr;  // standard MLC: w + v_xc (full), scratch w of expand
     DevBuf<int> idx;
     int ldT = 0;
+    int mlc_ld = 0, mlc_sweeps = 0;  // standard MLC state: ld of PhiT, sweeps run
     EstimatorData est;
 };
 
@@ -74,6 +76,15 @@ ScfStats coarse_scf(Level& L, Corrector& K, CgWork& cg, const ScfParams& p, doub
                     double* d_rho_full, double* d_w_full);
 void correction_step(Level& L, Corrector& K, CgWork& cg, const StepOptions& o, double* h_lambda, double* d_Phi, int ld,
                      double* d_w, StepLog* log);
+
+/// standard multilevel correction (driver::solve_level_mlc, proj/src/driver.cpp:200-302), split at its loop:
+/// begin = orbital BVPs with the warm potentials + Hartree boundary data; sweep = one correction-space
+/// iteration (Hartree of the current density, pot = w + v_xc, bordered solves, expand, density change);
+/// finish = Hartree potential of the final density.
+void mlc_begin(Level& L, Corrector& K, CgWork& cg, const StepOptions& o, const double* h_lambda, const double* d_Phi,
+               int ld, const double* d_w, StepLog* log);
+double mlc_sweep(Level& L, Corrector& K, CgWork& cg, const StepOptions& o, double* h_lambda, double* d_Phi, int ld);
+void mlc_finish(Level& L, Corrector& K, CgWork& cg, const StepOptions& o, double* d_w, double* d_rho);
 
 // pieces (also exported through the C-ABI for parity tests)
 double outer_operator(Level& L, Corrector& K, const double* d_what_full, const double* d_vxc_full, int aop = 2);

@@ -72,6 +72,33 @@ def solve_level_corrected(L: api.Level, lambdas: np.ndarray, Phi: api.DeviceArra
     raise KsbError(1, f"nonconvergence: outer iteration cap reached on level {level}")
 
 
+def solve_level_mlc(L: api.Level, lambdas: np.ndarray, Phi: api.DeviceArray, w: api.DeviceArray,
+                    tol_outer: float = 1e-6, max_scf: int = 200, level: int = 0, rho: api.DeviceArray | None = None,
+                    **step_opts) -> LevelResult:
+    """The reference's standard multilevel correction on one level (driver::solve_level_mlc,
+    proj/src/driver.cpp:200-302): one set of orbital BVPs with the warm potentials, then correction-space sweeps
+    that rebuild the potential-weighted coarse blocks from the current density until its H1 change drops below
+    tol_outer. lambdas / Phi / w are updated in place (Phi = the expanded orbitals, w = the Hartree potential of
+    the final density); rho, when given, receives that density."""
+    res = LevelResult(level=level, n_dofs=L.n, outer_iterations=0, lambdas=lambdas)
+    res.logs.append(L.mlc_begin(lambdas, Phi, w, **step_opts))
+    for s in range(1, max_scf + 1):
+        try:
+            delta = L.mlc_sweep(lambdas, Phi, **step_opts)
+        except KsbError as e:
+            e.partial = res
+            e.step = s
+            raise
+        res.deltas.append(delta)
+        res.outer_iterations = s
+        if delta < tol_outer:
+            break
+        if s == max_scf:
+            raise KsbError(1, f"correction-space iteration cap reached on level {level}")
+    L.mlc_finish(w, rho, **step_opts)
+    return res
+
+
 @dataclass
 class LevelRecord:
     """driver::LevelRecord (proj/include/ksafem/driver.hpp:12-23)"""
@@ -99,13 +126,20 @@ class RunLog:
 
 def run(ctx: api.Context, atoms, n_pairs: int, occupancy: float, xc: str, box: float, n_coarse: int, max_levels: int,
         refine: str = "adaptive", theta: float = 0.4, tol_outer: float = 1e-6, mixing: float = 0.3, max_scf: int = 200,
-        tol_eig: float = 1e-9, max_outer: int = 40, **step_opts) -> RunLog:
-    """driver::run in accelerated mode (proj/src/driver.cpp:306-435), all solves on the device: coarse SCF on
+        tol_eig: float = 1e-9, max_outer: int = 40, mode: str = "accelerated", **step_opts) -> RunLog:
+    """driver::run (proj/src/driver.cpp:306-435), all solves on the device; mode "accelerated" (the paper's
+    corrected method, solve_level_corrected) or "standard_mlc" (solve_level_mlc, the comparison method): coarse SCF on
     level 0, then per level Doerfler marks of the residual indicators (or uniform refinement, as BASELINE's
     cfg1 prescribes), nested warm start, solve_level_corrected, indicators. Errors abort the run like the
     reference (RunLog.aborted, abort_reason)."""
     import time
 
+    if mode not in ("accelerated", "linear", "standard_mlc"):
+        raise ValueError(f"mode {mode!r}: the device path runs accelerated, linear and standard_mlc "
+                         "(standard_afem / xc_only / hartree_only re-solve the full fine eigenproblem)")
+    # RunConfig::hartree_enabled / xc_enabled (proj/include/ksafem/runconfig.hpp:39-45)
+    hart = mode != "linear"
+    xc_on = mode != "linear" and xc != "none"
     t_start = time.perf_counter()
     log = RunLog()
     h = api.Hierarchy()
@@ -126,13 +160,13 @@ def run(ctx: api.Context, atoms, n_pairs: int, occupancy: float, xc: str, box: f
                 h.push(mesh)
             prev = L
             L = api.Level(ctx, h, level)
-            L.set_system(atoms, n_pairs=n_pairs, occupancy=occupancy, xc=xc)
+            L.set_system(atoms, n_pairs=n_pairs, occupancy=occupancy, xc=xc, hartree=hart, xc_on=xc_on)
             L.level_ops()
             t_refine = time.perf_counter() - t0
             t1 = time.perf_counter()
             if level == 0:
                 lam, Phi, rho, w, scf_it, _ = L.coarse_scf(tol=tol_outer, max_iterations=max_scf, mixing=mixing,
-                                                           tol_eig=tol_eig)
+                                                           hartree=hart, xc=xc_on, tol_eig=tol_eig)
                 outer, inner = scf_it, []
             else:
                 # nested warm start on the device (proj/src/driver.cpp:367-371): orbitals as interior blocks
@@ -142,8 +176,12 @@ def run(ctx: api.Context, atoms, n_pairs: int, occupancy: float, xc: str, box: f
                 L.prolong(Phi, Phi_new, True, True, ncols=n_pairs)
                 L.prolong(w, w_new, False, False)
                 Phi, w = Phi_new, w_new
-                res = solve_level_corrected(L, lam, Phi, w, tol_outer=tol_outer, max_outer=max_outer, level=level,
-                                            **step_opts)
+                if mode == "standard_mlc":
+                    res = solve_level_mlc(L, lam, Phi, w, tol_outer=tol_outer, max_scf=max_scf, level=level,
+                                          **step_opts)
+                else:
+                    res = solve_level_corrected(L, lam, Phi, w, tol_outer=tol_outer, max_outer=max_outer,
+                                                level=level, **step_opts)
                 outer, inner = res.outer_iterations, res.inner_iterations
                 rho = ctx.empty((L.n,))
                 L.density(Phi, rho)
