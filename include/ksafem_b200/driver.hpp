@@ -69,8 +69,19 @@ LevelResult solve_level_corrected(const LevelOps& ops, const model::MolecularSys
                                   const VecX& lambdas, const std::vector<fem::FEFunction>& orbitals,
                                   const fem::FEFunction& w, double tol_outer = 1e-6, int max_outer = 40);
 
-/// the adaptive run in accelerated mode (proj/src/driver.cpp:306-435); refinement by Doerfler marks of the
-/// residual indicators, or uniform (BASELINE's cfg1) when `uniform` is set
+/// The standard multilevel correction on one level (driver::solve_level_mlc, proj/src/driver.cpp:200-302):
+/// orbital BVPs with the warm potentials, then correction-space sweeps rebuilding the potential-weighted coarse
+/// blocks from the current density until its H1 change drops below tol_outer ("nonconvergence" after max_scf).
+LevelResult solve_level_mlc(const LevelOps& ops, const model::MolecularSystem& sys, const StepOptions& opt,
+                            const VecX& lambdas, const std::vector<fem::FEFunction>& orbitals,
+                            const fem::FEFunction& w, double tol_outer = 1e-6, int max_scf = 200);
+
+/// RunConfig::Mode subset the device path runs (proj/include/ksafem/runconfig.hpp:9): the corrected method with
+/// (accelerated) or without (linear) the nonlinear terms, and the standard MLC comparison method
+enum class Mode { accelerated, linear, standard_mlc };
+
+/// the adaptive run (proj/src/driver.cpp:306-435); refinement by Doerfler marks of the residual indicators, or
+/// uniform (BASELINE's cfg1) when `uniform` is set
 struct RunConfig {
     model::MolecularSystem system;
     int n_coarse = 16;
@@ -87,6 +98,7 @@ struct RunConfig {
     double score_floor = 1e-8;
     int nev_scan_pad = 4;
     bool uniform = false;
+    Mode mode = Mode::accelerated;
 };
 
 struct LevelRecord {

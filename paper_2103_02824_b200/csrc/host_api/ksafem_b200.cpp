@@ -1058,6 +1058,9 @@ RunLog run(const RunConfig& cfg) {
     so.score_floor = cfg.score_floor;
     so.max_inner = cfg.max_inner;
     so.nev_scan_pad = cfg.nev_scan_pad;
+    // RunConfig::hartree_enabled / xc_enabled (proj/include/ksafem/runconfig.hpp:39-45)
+    so.hartree = cfg.mode != Mode::linear;
+    so.xc = cfg.mode != Mode::linear;
     try {
         for (int level = 0; level < cfg.max_levels; ++level) {
             LevelRecord rec;
@@ -1077,6 +1080,8 @@ RunLog run(const RunConfig& cfg) {
                 opt.max_iterations = cfg.max_scf;
                 opt.mixing = cfg.mixing;
                 opt.tol_eig = cfg.tol_eig;
+                opt.hartree_on = so.hartree;
+                opt.xc_on = so.xc;
                 const auto r = scf::initial_coarse_solve(sys, hier.space(0), cfg.tol_outer, opt);
                 rec.outer_iterations = r.iterations;
                 lam = r.lambdas;
@@ -1086,8 +1091,11 @@ RunLog run(const RunConfig& cfg) {
             } else {
                 std::vector<fem::FEFunction> warm;
                 for (const auto& o : orbs) warm.push_back(hier.prolong(o, level));
-                const auto res = solve_level_corrected(ops, sys, so, lam, warm, hier.prolong(w, level),
-                                                       cfg.tol_outer, cfg.max_outer);
+                const auto res = cfg.mode == Mode::standard_mlc
+                                     ? solve_level_mlc(ops, sys, so, lam, warm, hier.prolong(w, level), cfg.tol_outer,
+                                                       cfg.max_scf)
+                                     : solve_level_corrected(ops, sys, so, lam, warm, hier.prolong(w, level),
+                                                             cfg.tol_outer, cfg.max_outer);
                 lam = res.lambdas;
                 orbs = res.orbitals;
                 w = res.hartree;
@@ -1135,6 +1143,39 @@ LevelResult solve_level_corrected(const LevelOps& ops, const model::MolecularSys
         }
     }
     fail("nonconvergence", "outer iteration cap reached");
+}
+
+LevelResult solve_level_mlc(const LevelOps& ops, const model::MolecularSystem& sys, const StepOptions& opt,
+                            const VecX& lambdas, const std::vector<fem::FEFunction>& orbitals,
+                            const fem::FEFunction& w, double tol_outer, int max_scf) {
+    const int N = int(orbitals.size());
+    if (N != sys.n_pairs || int(lambdas.size()) != N) fail("invalid-argument", "one orbital and eigenvalue per pair");
+    const auto& space = ops.space;
+    model::set_system(*space, sys, opt.hartree, opt.xc && sys.xc.kind != model::XcKind::none);
+    int ld = 0;
+    b200::DeviceBuffer phi = fem::orbital_block(*space, orbitals, ld);
+    fem::same_space(w, *space, "w lives on a different space");
+    b200::DeviceBuffer wd(space->device(), w.coeffs);
+    const auto o = corr::step_opts(opt.tol_linear, opt.tol_inner, opt.max_inner, opt.score_floor, opt.nev_scan_pad);
+    VecX lam = lambdas;
+    ksb_step_log lg{};
+    std::vector<int> att(static_cast<size_t>(N)), its(static_cast<size_t>(N));
+    b200::check(ksb_mlc_begin(space->device_level(), &o, lam.data(), phi.data(), ld, wd.data(), &lg, att.data(),
+                              its.data()));
+    LevelResult r;
+    for (int s = 1; s <= max_scf; ++s) {
+        double delta = 0.0;
+        b200::check(ksb_mlc_sweep(space->device_level(), &o, lam.data(), phi.data(), ld, &delta));
+        r.deltas.push_back(delta);
+        r.outer_iterations = s;
+        if (delta < tol_outer) break;
+        if (s == max_scf) fail("nonconvergence", "correction-space iteration cap reached");
+    }
+    b200::check(ksb_mlc_finish(space->device_level(), &o, wd.data(), nullptr));
+    r.lambdas = lam;
+    r.orbitals = fem::from_block(space, phi.to_host(), N, ld, fem::Role::wavefunction);
+    r.hartree = fem::FEFunction(space, wd.to_host(), fem::Role::hartree);
+    return r;
 }
 
 } // namespace driver

@@ -427,6 +427,47 @@ TEST_CASE("solve_level_corrected converges from a hydrogenic start", t_driver) {
     std::printf("  level-1 He: lambda %.10f, E %.10f, %d outer steps\n", res.lambdas[0], e.total, res.outer_iterations);
 }
 
+TEST_CASE("solve_level_mlc and the standard_mlc run", t_mlc) {
+    fem::SpaceHierarchy hier;
+    model::MolecularSystem sys;
+    sys.atoms.push_back({2.0, Vec3()});
+    sys.n_pairs = 1;
+    sys.occupancy = 2.0;
+    sys.domain = cube(-6, 6);
+    sys.xc.kind = model::XcKind::lda_pz81;
+    auto m = mesh::build_box_mesh(sys.domain, 6);
+    hier.push(m);
+    hier.push(mesh::uniform_refine(*m));
+    const auto ops = driver::make_level_ops(hier, 1, sys);
+    const auto& V = ops.space;
+    fem::FEFunction phi(V, fem::Role::wavefunction);
+    const auto xyz = V->mesh().vertices();
+    for (int i : V->interior_dofs()) {
+        const auto& x = xyz[size_t(i)];
+        phi.coeffs[size_t(i)] = std::exp(-1.7 * std::sqrt(x[0] * x[0] + x[1] * x[1] + x[2] * x[2]));
+    }
+    const double n0 = fem::l2_norm(phi);
+    for (auto& c : phi.coeffs) c /= n0;
+    const auto rho = model::density({phi}, 2.0);
+    const VecX bc = hartree::boundary_values(hartree::compute_moments(rho), *V);
+    const auto w = hartree::solve_hartree_exact(*ops.stiffness, *V, {phi}, 2.0, bc, 1e-10);
+    driver::StepOptions so;
+    const auto res = driver::solve_level_mlc(ops, sys, so, VecX{-0.6}, {phi}, w, 1e-6, 200);
+    CHECK(res.deltas.back() < 1e-6);
+    CHECK(res.lambdas[0] < -0.2 && res.lambdas[0] > -1.2);
+    std::printf("  level-1 He (standard MLC): lambda %.10f, %d sweeps\n", res.lambdas[0], res.outer_iterations);
+
+    driver::RunConfig cfg;
+    cfg.system = sys;
+    cfg.n_coarse = 4;
+    cfg.max_levels = 3;
+    cfg.uniform = true;
+    cfg.mode = driver::Mode::standard_mlc;
+    const auto log = driver::run(cfg);
+    CHECK(!log.aborted);
+    CHECK(log.records.size() == 3);
+}
+
 // ---------------------------------------------------------------- scf + run (scf.cpp, driver.cpp:306-435)
 TEST_CASE("coarse SCF of cfg1 and the adaptive run", t_run) {
     model::MolecularSystem sys;
