@@ -71,6 +71,24 @@ int ksb_hier_levels(const ksb_hier* h);
  * replaces SpaceHierarchy::prolongation (proj/src/fespace.cpp:64-74) */
 int ksb_hier_prolongation(const ksb_hier* h, int level, int32_t* h_col, double* h_val);
 
+/* level `level` of a hierarchy as a mesh handle (shared, free with ksb_mesh_free) */
+int ksb_hier_mesh(const ksb_hier* h, int level, ksb_mesh** out);
+
+/* ---------------- binary dumps (the reference has none: its CSV/VTK outputs, proj/src/driver.cpp:509-543,
+ * proj/src/mesh.cpp:259-279, stay text). Versioned little-endian files with an FNV-1a 64 checksum; meshes keep
+ * their defining arrays (coordinates, tets, bisection tuples and tags, parents), faces are recomputed on load.
+ * Errors: KSB_IO (open/short/corrupt/checksum), KSB_HIERARCHY (stored levels not nested). */
+int ksb_hier_save(const ksb_hier* h, const char* path);
+int ksb_hier_load(const char* path, ksb_hier** out);
+int ksb_mesh_save(const ksb_mesh* m, const char* path);
+int ksb_mesh_load(const char* path, ksb_mesh** out);
+/* solver state of one level: lambdas (N), orbitals (interior block ni x N, read with leading dim ld),
+ * Hartree potential (n, full) */
+int ksb_state_save(const char* path, int level, int N, int64_t ni, int64_t n, const double* h_lambda,
+                   const double* h_Phi, int ld, const double* h_w);
+int ksb_state_sizes(const char* path, int64_t sizes[4]); /* level, N, ni, n */
+int ksb_state_load(const char* path, double* h_lambda, double* h_Phi, int ld, double* h_w);
+
 /* ---------------- device context ---------------- */
 int ksb_ctx_create(int device, ksb_ctx** out);
 void ksb_ctx_destroy(ksb_ctx* c);

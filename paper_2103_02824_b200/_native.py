@@ -69,6 +69,14 @@ PROTOTYPES = {
     "ksb_mesh_get": (I, [P, I, P]),
     "ksb_hier_create": (I, [PP]),
     "ksb_hier_push": (I, [P, P]),
+    "ksb_hier_mesh": (I, [P, I, PP]),
+    "ksb_hier_save": (I, [P, C.c_char_p]),
+    "ksb_hier_load": (I, [C.c_char_p, PP]),
+    "ksb_mesh_save": (I, [P, C.c_char_p]),
+    "ksb_mesh_load": (I, [C.c_char_p, PP]),
+    "ksb_state_save": (I, [C.c_char_p, I, I, C.c_int64, C.c_int64, DP, DP, I, DP]),
+    "ksb_state_sizes": (I, [C.c_char_p, P]),
+    "ksb_state_load": (I, [C.c_char_p, DP, DP, I, DP]),
     "ksb_hier_free": (None, [P]),
     "ksb_hier_levels": (I, [P]),
     "ksb_hier_prolongation": (I, [P, I, IP, DP]),

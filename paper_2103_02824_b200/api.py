@@ -69,6 +69,16 @@ class Mesh:
         check(lib.ksb_mesh_adapt_refine(self._h, _ip(m), len(m), C.byref(h)))
         return Mesh(h)
 
+    def save(self, path) -> None:
+        """binary dump (include/ksb.h ksb_mesh_save): defining arrays, faces recomputed on load"""
+        check(lib.ksb_mesh_save(self._h, str(path).encode()))
+
+    @staticmethod
+    def load(path) -> "Mesh":
+        h = C.c_void_p()
+        check(lib.ksb_mesh_load(str(path).encode(), C.byref(h)))
+        return Mesh(h)
+
     def sizes(self):
         s = (C.c_int64 * 8)()
         check(lib.ksb_mesh_sizes(self._h, s))
@@ -116,12 +126,49 @@ class Hierarchy:
     def n_levels(self):
         return lib.ksb_hier_levels(self._h)
 
+    def save(self, path) -> None:
+        """binary dump of every level (include/ksb.h ksb_hier_save)"""
+        check(lib.ksb_hier_save(self._h, str(path).encode()))
+
+    @staticmethod
+    def load(path) -> "Hierarchy":
+        h = C.c_void_p()
+        check(lib.ksb_hier_load(str(path).encode(), C.byref(h)))
+        out = Hierarchy.__new__(Hierarchy)
+        out._h = h
+        out.meshes = []
+        for k in range(lib.ksb_hier_levels(h)):
+            m = C.c_void_p()
+            check(lib.ksb_hier_mesh(h, k, C.byref(m)))
+            out.meshes.append(Mesh(m))
+        return out
+
     def prolongation(self, level: int):
         n = self.meshes[level].n_vertices
         col = np.empty((n, 4), np.int32)
         val = np.empty((n, 4), np.float64)
         check(lib.ksb_hier_prolongation(self._h, level, _ip(col), _dp(val)))
         return col, val
+
+
+def save_state(path, level: int, lambdas, Phi: np.ndarray, w: np.ndarray, N: int | None = None) -> None:
+    """binary solver state of one level (include/ksb.h ksb_state_save): lambdas, interior orbital block, w"""
+    lam = np.ascontiguousarray(lambdas, np.float64)
+    P = np.ascontiguousarray(Phi, np.float64)
+    P2 = P.reshape(P.shape[0], -1)
+    wv = np.ascontiguousarray(w, np.float64)
+    N = int(N or len(lam))
+    check(lib.ksb_state_save(str(path).encode(), int(level), N, P2.shape[0], wv.shape[0], _dp(lam), _dp(P2),
+                             P2.shape[1], _dp(wv)))
+
+
+def load_state(path) -> dict:
+    s = (C.c_int64 * 4)()
+    check(lib.ksb_state_sizes(str(path).encode(), s))
+    level, N, ni, n = (int(x) for x in s)
+    lam, Phi, w = np.empty(N), np.empty((ni, N)), np.empty(n)
+    check(lib.ksb_state_load(str(path).encode(), _dp(lam), _dp(Phi), N, _dp(w)))
+    return {"level": level, "lambdas": lam, "Phi": Phi, "w": w}
 
 
 # ----------------------------------------------------------------------------- device

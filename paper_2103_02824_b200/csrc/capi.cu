@@ -1,4 +1,5 @@
 // C-ABI implementation (include/ksb.h). No exceptions cross this boundary.
+#include "host/dump.hpp"
 #include <algorithm>
 #include <cstring>
 #include <exception>
@@ -203,6 +204,100 @@ int ksb_hier_push(ksb_hier* h, const ksb_mesh* m) {
 void ksb_hier_free(ksb_hier* h) { delete h; }
 
 int ksb_hier_levels(const ksb_hier* h) { return h ? h->h.n_levels() : 0; }
+
+int ksb_hier_mesh(const ksb_hier* h, int level, ksb_mesh** out) {
+    return guard([&] {
+        need(h && out, "null argument");
+        if (level < 0 || level >= h->h.n_levels()) ksb::raise(KSB_HIERARCHY, "level out of range");
+        *out = new ksb_mesh{h->h.mesh_ptr(level)};
+    });
+}
+
+int ksb_hier_save(const ksb_hier* h, const char* path) {
+    return guard([&] {
+        need(h && path, "null argument");
+        std::vector<ksb::MeshPtr> ms;
+        for (int k = 0; k < h->h.n_levels(); ++k) ms.push_back(h->h.mesh_ptr(k));
+        ksb::save_meshes(path, ms);
+    });
+}
+
+int ksb_hier_load(const char* path, ksb_hier** out) {
+    return guard([&] {
+        need(path && out, "null argument");
+        auto ms = ksb::load_meshes(path);
+        auto* h = new ksb_hier;
+        try {
+            for (size_t k = 0; k < ms.size(); ++k) {
+                if (k > 0 && ms[k]->n_parent_vertices != ms[k - 1]->n_vertices())
+                    ksb::raise(KSB_HIERARCHY, "stored levels are not nested");
+                h->h.push(ms[k]);
+            }
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+int ksb_mesh_save(const ksb_mesh* m, const char* path) {
+    return guard([&] {
+        need(m && path, "null argument");
+        ksb::save_meshes(path, {m->m});
+    });
+}
+
+int ksb_mesh_load(const char* path, ksb_mesh** out) {
+    return guard([&] {
+        need(path && out, "null argument");
+        auto ms = ksb::load_meshes(path);
+        if (ms.size() != 1) ksb::raise(KSB_IO, std::string(path) + ": holds " + std::to_string(ms.size()) + " meshes");
+        *out = new ksb_mesh{ms[0]};
+    });
+}
+
+int ksb_state_save(const char* path, int level, int N, int64_t ni, int64_t n, const double* h_lambda,
+                   const double* h_Phi, int ld, const double* h_w) {
+    return guard([&] {
+        need(path && h_lambda && h_Phi && h_w, "null argument");
+        if (N < 1 || ld < N || ni < 0 || n < ni) ksb::raise(KSB_INVALID_ARGUMENT, "bad state sizes");
+        ksb::State s;
+        s.level = level;
+        s.N = N;
+        s.ni = ni;
+        s.n = n;
+        s.lambdas.assign(h_lambda, h_lambda + N);
+        s.phi.resize(size_t(ni) * N);
+        for (int64_t r = 0; r < ni; ++r)
+            for (int c = 0; c < N; ++c) s.phi[size_t(r) * N + c] = h_Phi[size_t(r) * ld + c];
+        s.w.assign(h_w, h_w + n);
+        ksb::save_state(path, s);
+    });
+}
+
+int ksb_state_sizes(const char* path, int64_t sizes[4]) {
+    return guard([&] {
+        need(path && sizes, "null argument");
+        const auto s = ksb::load_state(path);
+        sizes[0] = s.level;
+        sizes[1] = s.N;
+        sizes[2] = s.ni;
+        sizes[3] = s.n;
+    });
+}
+
+int ksb_state_load(const char* path, double* h_lambda, double* h_Phi, int ld, double* h_w) {
+    return guard([&] {
+        need(path && h_lambda && h_Phi && h_w, "null argument");
+        const auto s = ksb::load_state(path);
+        if (ld < s.N) ksb::raise(KSB_INVALID_ARGUMENT, "ld < N");
+        std::memcpy(h_lambda, s.lambdas.data(), sizeof(double) * size_t(s.N));
+        for (int64_t r = 0; r < s.ni; ++r)
+            for (int c = 0; c < s.N; ++c) h_Phi[size_t(r) * ld + c] = s.phi[size_t(r) * s.N + c];
+        std::memcpy(h_w, s.w.data(), sizeof(double) * size_t(s.n));
+    });
+}
 
 int ksb_hier_prolongation(const ksb_hier* h, int level, int32_t* col, double* val) {
     return guard([&] {
