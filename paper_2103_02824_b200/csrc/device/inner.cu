@@ -272,6 +272,7 @@ __global__ void __cluster_dims__(kTriCluster, 1, 1) __launch_bounds__(kTriThread
     double* A = sh;                            // R x n, slot i = row q + P i
     double* pbuf = sh + size_t(R) * n;         // 2 x n
     double* rep = pbuf + 2 * size_t(n);        // 2 x kTriRep x n
+    double* vsh = rep + 2 * size_t(kTriRep) * n;  // n: this step's v (row scalars of the rank-2 update)
     const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5, nw = blockDim.x >> 5;
     for (int idx = tid; idx < nslot * n; idx += blockDim.x) {
         const int i = idx / n, c = idx - i * n;
@@ -311,6 +312,13 @@ __global__ void __cluster_dims__(kTriCluster, 1, 1) __launch_bounds__(kTriThread
             v[s] = (c >= m0 && c < n) ? (c == m0 ? x0 - alpha : cur[s]) * inv : 0.0;
         }
         const double dk = reg_at(cur, k);
+        if (wib == 0) {  // v for the row scalars; read after the cluster barrier below
+#pragma unroll
+            for (int s = 0; s < kTriS; ++s) {
+                const int c = lane + 32 * s;
+                if (s >= s0 && c < n) vsh[c] = v[s];
+            }
+        }
         if (q == 0 && wib == 0) {
             if (lane == 0) {
                 d[k] = dk;
@@ -367,8 +375,8 @@ __global__ void __cluster_dims__(kTriCluster, 1, 1) __launch_bounds__(kTriThread
         // replica rows still ahead take this step's update (warp j owns replica row j)
         {
             const int rr = rb0 + wib;
-            const double vr = 2.0 * reg_at(v, rr), wr = 2.0 * reg_at(w, rr);
             if (rr >= m0 && rr < n - 1) {
+                const double vr = 2.0 * vsh[rr], wr = 2.0 * fma(-kk, vsh[rr], pf[rr]);
                 double* row = repb + size_t(wib) * n;
 #pragma unroll
                 for (int s = 0; s < kTriS; ++s) {
@@ -381,7 +389,7 @@ __global__ void __cluster_dims__(kTriCluster, 1, 1) __launch_bounds__(kTriThread
         for (int i = ifirst; i < nslot; i += nw) {
             double* row = A + size_t(i) * n;
             const int r = q + P * i;
-            const double vr = 2.0 * reg_at(v, r), wr = 2.0 * reg_at(w, r);
+            const double vr = 2.0 * vsh[r], wr = 2.0 * fma(-kk, vsh[r], pf[r]);
 #pragma unroll
             for (int s = 0; s < kTriS; ++s) {
                 const int c = lane + 32 * s;
@@ -1424,7 +1432,7 @@ void dense_lowest_eigs(Level& L, const CoarseOps& co, InnerWork& w, int mat, int
     launch(c, "scf:gemm", k_gemm_nt, gt, 256, 0, n, (const double*)w.W.p, (const double*)co.LHi.p, w.C.p);
     launch(c, "scf:symmetrize", k_symmetrize, ceil_div(int64_t(n) * n, 256), 256, 0, n, w.C.p);
     const int cl_R = (n + kTriCluster - 1) / kTriCluster;
-    const size_t cl_smem = sizeof(double) * (size_t(cl_R) * n + (2 + 2 * kTriRep) * size_t(n));
+    const size_t cl_smem = sizeof(double) * (size_t(cl_R) * n + (3 + 2 * kTriRep) * size_t(n));
     if (cl_smem <= size_t(kMaxDynSmem) && n <= 32 * kTriS) {
         KSB_CUDA_CHECK(cudaFuncSetAttribute(k_tridiag_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             int(kMaxDynSmem)));
@@ -1492,7 +1500,7 @@ InnerStats inner_scf(Level& L, const CoarseOps& co, const ProjOut& P, const Inne
     }
     const size_t tri_smem = sizeof(double) * 2 * nh;
     const int cl_R = (nh + kTriCluster - 1) / kTriCluster;
-    const size_t cl_smem = sizeof(double) * (size_t(cl_R) * nh + (2 + 2 * kTriRep) * size_t(nh));
+    const size_t cl_smem = sizeof(double) * (size_t(cl_R) * nh + (3 + 2 * kTriRep) * size_t(nh));
     const bool use_cluster = cl_smem <= size_t(kMaxDynSmem) && nh <= 32 * kTriS;
 
     if (use_cluster) {
