@@ -86,6 +86,21 @@ __global__ void k_trsv_many(int n, int nrhs, const double* __restrict__ L, int t
     for (int k = lane; k < n; k += 32) X[j * xs + k * xc] = y[k];
 }
 
+/// lane-strided dot of a row with a vector, four independent accumulators: four row loads in flight per lane
+/// (a single accumulator chain stalls the warp on every load -- these dense coarse kernels are latency-bound)
+__device__ __forceinline__ double lane_dot(const double* __restrict__ a, const double* x, int n, int lane) {
+    double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
+    int c = lane;
+    for (; c + 96 < n; c += 128) {
+        t0 = fma(a[c], x[c], t0);
+        t1 = fma(a[c + 32], x[c + 32], t1);
+        t2 = fma(a[c + 64], x[c + 64], t2);
+        t3 = fma(a[c + 96], x[c + 96], t3);
+    }
+    for (; c < n; c += 32) t0 = fma(a[c], x[c], t0);
+    return (t0 + t1) + (t2 + t3);
+}
+
 /// Y[v*ldy + r] = alpha * sum_c A[r*lda + c] X[v*ldx + c] for r < n, v < nv (warp per (row, vector)).
 /// The explicit inverse factors (L_H^-1, L_H^-T, C_H^-1, built once per level) turn every triangular
 /// solve of the inner sweep into this fully parallel product.
@@ -96,8 +111,7 @@ __global__ void k_gemv_many(int n, int m, int nv, const double* __restrict__ A, 
     const int r = warp % n, v = warp / n;
     const double* a = A + size_t(r) * lda;
     const double* x = X + size_t(v) * ldx;
-    double t = 0.0;
-    for (int c = lane; c < m; c += 32) t += a[c] * x[c];
+    double t = lane_dot(a, x, m, lane);
     t = warp_sum(t);
     if (lane == 0) Y[size_t(v) * ldy + r] = alpha * t;
 }
@@ -106,9 +120,7 @@ __global__ void k_gemv_many(int n, int m, int nv, const double* __restrict__ A, 
 __device__ void block_gemv(int n, const double* __restrict__ A, const double* x, double* y) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     for (int r = warp; r < n; r += nw) {
-        const double* a = A + size_t(r) * n;
-        double t = 0.0;
-        for (int c = lane; c < n; c += 32) t += a[c] * x[c];
+        double t = lane_dot(A + size_t(r) * n, x, n, lane);
         t = warp_sum(t);
         if (lane == 0) y[r] = t;
     }
@@ -675,8 +687,7 @@ __global__ void k_border_pre(SweepDev S) {
     // border b = b_H1 + b_H4 [+ (A_h4 w_H + theta1 b_H3)]
     for (int a = warp; a < nh; a += nw) {
         double x = 0.0;
-        if (S.hartree)
-            for (int c = lane; c < nh; c += 32) x += Ah4[size_t(a) * nh + c] * S.wH[c];
+        if (S.hartree) x = lane_dot(Ah4 + size_t(a) * nh, S.wH, nh, lane);
         x = warp_sum(x);
         if (lane == 0) {
             double bb = ov[a] + ov[2 * nh + a];
@@ -690,8 +701,7 @@ __global__ void k_border_pre(SweepDev S) {
     // t = A_H u
     const double* u = S.u + size_t(i) * nh;
     for (int a = warp; a < nh; a += nw) {
-        double x = 0.0;
-        for (int c = lane; c < nh; c += 32) x += S.AH[size_t(a) * nh + c] * u[c];
+        double x = lane_dot(S.AH + size_t(a) * nh, u, nh, lane);
         x = warp_sum(x);
         if (lane == 0) t[a] = x;
     }
@@ -966,8 +976,7 @@ __global__ void k_select(SweepDev S, int nev, const double* __restrict__ lam, co
     double* tmp = sh + nh;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     for (int a = warp; a < nh; a += nw) {
-        double t = 0.0;
-        for (int c = lane; c < nh; c += 32) t += MH[size_t(a) * nh + c] * po[c];
+        double t = lane_dot(MH + size_t(a) * nh, po, nh, lane);
         t = warp_sum(t);
         if (lane == 0) tmp[a] = t;
     }
@@ -1008,11 +1017,8 @@ __global__ void __launch_bounds__(512) k_hartree_parts(HartreeDev H) {
         const double* Ah4 = H.A_h4 + size_t(i) * nh * nh;
         double* F = H.part + size_t(i) * nh;
         for (int a = warp; a < nh; a += nw) {
-            double t = 0.0, u = 0.0;
-            for (int c = lane; c < nh; c += 32) {
-                t += Ah4[size_t(a) * nh + c] * ph[c];
-                u += H.A3[size_t(a) * nh + c] * ph[c];
-            }
+            double t = lane_dot(Ah4 + size_t(a) * nh, ph, nh, lane);
+            double u = lane_dot(H.A3 + size_t(a) * nh, ph, nh, lane);
             t = warp_sum(t);
             u = warp_sum(u);
             if (lane == 0) {
@@ -1033,11 +1039,8 @@ __global__ void __launch_bounds__(512) k_hartree_parts(HartreeDev H) {
     __syncthreads();
     const double dth = H.th2_new[i] - H.th2_old[i];
     for (int a = warp; a < nh; a += nw) {
-        double t = 0.0, u = 0.0;
-        for (int c = lane; c < nh; c += 32) {
-            t += H.CH[size_t(a) * nh + c] * dp[c];
-            u += H.MH[size_t(a) * nh + c] * dp[c];
-        }
+        double t = lane_dot(H.CH + size_t(a) * nh, dp, nh, lane);
+        double u = lane_dot(H.MH + size_t(a) * nh, dp, nh, lane);
         t = warp_sum(t);
         u = warp_sum(u);
         if (lane == 0) {
