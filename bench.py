@@ -280,6 +280,66 @@ def correction_bench(args, ctx, stream, rank, world):
     return out
 
 
+# ----------------------------------------------------------------------------------- cfg4 / cfg5 orbital counts
+SCALE_CASES = [  # (name, generator, N, box, uniform refinements of the 8^3 coarse mesh)
+    ("cfg4-like", "ring_atoms", 21, 25.0, 3),
+    ("cfg5-like", "sphere_atoms", 120, 30.0, 4),
+]
+SCALE_SWEEPS = 10
+
+
+def scale_bench(args, ctx, stream, world):
+    """Correction steps at BASELINE configs[3]/[4]'s orbital counts (N = 21, 120) on uniform Kuhn levels
+    (250,047 and 2,048,383 interior DOFs) from a seeded synthetic start, with a fixed number of inner sweeps so
+    the step's work is defined whatever the inner dynamics do. The configs' own adaptive runs cannot start: the
+    reference algorithm's coarse SCF does not converge for these molecules on an 8^3 coarse mesh."""
+    import torch
+
+    import paper_2103_02824_b200 as kb
+    from paper_2103_02824_b200 import workloads
+    out = []
+    for name, gen, N, box, refine in SCALE_CASES:
+        atoms = getattr(workloads, gen)()
+        h = kb.Hierarchy()
+        m = kb.Mesh.box([-box] * 3, [box] * 3, 8)
+        h.push(m)
+        for _ in range(refine):
+            m = m.uniform_refine()
+            h.push(m)
+        L = kb.Level(ctx, h, refine)
+        L.set_system(atoms, n_pairs=N, occupancy=2.0, xc="lda")
+        L.level_ops()
+        lam0, Phi, w, ld = workloads.synthetic_start(L, ctx, h.meshes[refine], [a[1:] for a in atoms], N, zeta=1.0,
+                                                     lam0=-0.5)
+        lam0 = np.linspace(-1.5, -0.3, N)
+        phi0, w0 = Phi.download(), w.download()
+        rec = {"workload": f"{name}: {len(atoms)} nuclei, N = {N}, LDA, [-{box:g},{box:g}]^3, 8^3 Kuhn coarse + "
+                           f"{refine} uniform refinements, synthetic start, {SCALE_SWEEPS} inner sweeps per step",
+               "n_interior": L.ni, "N": N, "steps": []}
+        try:
+            lam = lam0.copy()
+            L.correction_step(lam, Phi, w, ld=ld, fixed_sweeps=SCALE_SWEEPS)  # warm-up
+            Phi.upload(phi0)
+            w.upload(w0)
+            lam = lam0.copy()
+            ms = []
+            for _ in range(2):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                lg = L.correction_step(lam, Phi, w, ld=ld, fixed_sweeps=SCALE_SWEEPS)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                ms.append(e0.elapsed_time(e1))
+                rec["steps"].append({k: round(lg["ms_" + k], 3) for k in ("bvp", "hartree", "project", "inner")}
+                                    | {"cg_iterations": lg["cg_iterations"]})
+            rec["ms_per_step"] = max_over_ranks(float(np.mean(ms)), world)
+        except kb.KsbError as e:
+            rec["error"] = str(e)[:200]
+        out.append(rec)
+        L.close()
+    return out
+
+
 # ----------------------------------------------------------------------------------- cfg1 run (levels 0-2)
 RUN_LEVELS = 3  # coarse SCF + levels 1 and 2; on level 3 the reference algorithm itself stalls (DESIGN.md section 1)
 
@@ -400,6 +460,7 @@ def run_b200(args, world, rank, local):
 
     correction = correction_bench(args, ctx, stream, rank, world)
     cfg1_run = cfg1_run_bench(args, ctx, rank, world)
+    scale = None if args.no_scale else scale_bench(args, ctx, stream, world)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -433,6 +494,7 @@ def run_b200(args, world, rank, local):
             "cpu_baseline": cpu,
             "correction_step": correction,
             "cfg1_run": cfg1_run,
+            "scale": scale,
         }
         print(json.dumps(line), flush=True)
     L.close()
@@ -447,6 +509,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-iters", type=int, default=96, help="CPU oracle sample: iterations per 16-column block")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-scale", action="store_true", help="skip the N = 21 / 120 correction-step section")
     args = ap.parse_args()
     world, rank, local = dist_init()
     if args.impl == "reference":

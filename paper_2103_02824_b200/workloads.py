@@ -57,3 +57,32 @@ def synthetic_start(L: api.Level, ctx: api.Context, mesh: api.Mesh, centers, N: 
     L.hartree_solve(dPhi, bcb, w, tol=tol, N=N, ld=ld)
     lam = np.full(N, lam0, np.float64)
     return lam, dPhi, w, ld
+
+
+def ring_atoms(seed: int = 21):
+    """BASELINE configs[3] (cfg4-like): six Z=6 on a planar ring r = 2.64 bohr and six Z=1 on the coplanar ring
+    r = 4.68, a seeded angle offset, and seeded per-coordinate jitter U(-0.05, 0.05)."""
+    rng = np.random.default_rng(seed)
+    off = rng.uniform(0, np.pi / 3)
+    at = []
+    for k in range(6):
+        t = off + k * np.pi / 3
+        at.append([6.0, 2.64 * np.cos(t), 2.64 * np.sin(t), 0.0])
+        at.append([1.0, 4.68 * np.cos(t), 4.68 * np.sin(t), 0.0])
+    a = np.array(at)
+    a[:, 1:] += rng.uniform(-0.05, 0.05, (12, 3))
+    return a.tolist()
+
+
+def sphere_atoms(n: int = 60, r: float = 6.7, dmin: float = 2.5, seed: int = 60):
+    """BASELINE configs[4] (cfg5-like): n Z=6 nuclei at seeded quasi-uniform points on a sphere of radius r, minimum
+    pairwise separation dmin by rejection sampling."""
+    rng = np.random.default_rng(seed)
+    pts = []
+    while len(pts) < n:
+        v = rng.standard_normal(3)
+        v *= r / np.linalg.norm(v)
+        if all(np.linalg.norm(v - p) >= dmin for p in pts):
+            pts.append(v)
+    return [[6.0, *p] for p in pts]
+

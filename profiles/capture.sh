@@ -10,11 +10,11 @@ python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $O/smoke
 python bench.py > $O/bench_$R.log 2>&1
 echo "bench rc=$?" >> $O/bench_$R.log
 # cfg2 CG step: launch list (serialised, cold per launch) and one full capture of the three CG kernels
-python bench.py --steps 1 --warmup 3 --no-cpu > $O/bench_short_$R.log 2>&1 || exit 1
+python bench.py --steps 1 --warmup 3 --no-cpu --no-scale > $O/bench_short_$R.log 2>&1 || exit 1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_$R.csv \
-    python bench.py --steps 1 --warmup 3 --no-cpu > $O/ncu_launch_$R.log 2>&1
+    python bench.py --steps 1 --warmup 3 --no-cpu --no-scale > $O/ncu_launch_$R.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"k_spmm_dot|k_update_r|k_update_px" -c 3 \
-    -o $O/full_$R -f python bench.py --steps 1 --warmup 3 --no-cpu > $O/ncu_full_$R.log 2>&1
+    -o $O/full_$R -f python bench.py --steps 1 --warmup 3 --no-cpu --no-scale > $O/ncu_full_$R.log 2>&1
 echo "ncu rc=$?" >> $O/ncu_full_$R.log
 # cfg1 level-3 correction step: launch list and the inner-sweep kernels
 python tests/diag_step3.py 3 2 > $O/diag_step3_$R.log 2>&1 || exit 1

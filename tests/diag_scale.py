@@ -10,32 +10,7 @@ import numpy as np
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import paper_2103_02824_b200 as kb  # noqa: E402
-from paper_2103_02824_b200.workloads import synthetic_start  # noqa: E402
-
-
-def ring_atoms():
-    """cfg4-like: 6 Z=6 on r = 2.64, 6 Z=1 on r = 4.68 (coplanar), seeded angle offset and jitter"""
-    rng = np.random.default_rng(21)
-    off = rng.uniform(0, np.pi / 3)
-    at = []
-    for k in range(6):
-        t = off + k * np.pi / 3
-        at.append([6.0, 2.64 * np.cos(t), 2.64 * np.sin(t), 0.0])
-        at.append([1.0, 4.68 * np.cos(t), 4.68 * np.sin(t), 0.0])
-    a = np.array(at)
-    a[:, 1:] += rng.uniform(-0.05, 0.05, (12, 3))
-    return a.tolist()
-
-
-def sphere_atoms(n=60, r=6.7, dmin=2.5, seed=60):
-    rng = np.random.default_rng(seed)
-    pts = []
-    while len(pts) < n:
-        v = rng.standard_normal(3)
-        v *= r / np.linalg.norm(v)
-        if all(np.linalg.norm(v - p) >= dmin for p in pts):
-            pts.append(v)
-    return [[6.0, *p] for p in pts]
+from paper_2103_02824_b200.workloads import ring_atoms, sphere_atoms, synthetic_start  # noqa: E402
 
 
 def run(name, atoms, N, box, refine, sweeps, steps=2, profile=True):
