@@ -323,6 +323,7 @@ void correction_step(Level& L, Corrector& K, CgWork& cg, const StepOptions& o, d
                      double* d_w, StepLog* log) {
     Ctx& c = *L.ctx;
     if (!K.ops_ready) level_ops(L, K);
+    K.mlc_ld = 0;  // the step reuses the standard-MLC work buffers: a pending MLC level must be restarted
     const int N = K.sys.N, n = L.n, ni = L.ni;
     Timer tm(c.stream);
     tm.mark();

@@ -138,6 +138,12 @@ std::vector<MeshPtr> load_meshes(const std::string& path) {
         m->vparent = r.vec<int32_t>(2 * nv);
         for (int32_t v : m->tets)
             if (v < 0 || v >= nv) raise(KSB_IO, path + ": tet vertex out of range");
+        for (int32_t v : m->tuple)
+            if (v < 0 || v >= nv) raise(KSB_IO, path + ": bisection tuple vertex out of range");
+        for (int32_t v : m->vparent)
+            if (v < 0 || v >= nv) raise(KSB_IO, path + ": vertex parent out of range");
+        for (int8_t t : m->tag)
+            if (t < 1 || t > 3) raise(KSB_IO, path + ": bisection tag out of range");
         m->finalize();
         out.push_back(std::move(m));
     }

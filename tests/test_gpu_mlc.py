@@ -43,6 +43,12 @@ def test_mlc_sweep_needs_begin(ctx):
     Phi = c.dev(c.phi_block(c.orb))
     with pytest.raises(kb.KsbError, match="before mlc_begin"):
         c.L.mlc_sweep(c.lam.copy(), Phi)
+    # a correction step in between invalidates a begun MLC level (it reuses the work buffers)
+    w = c.dev(c.w)
+    c.L.mlc_begin(c.lam.copy(), Phi, w, tol_linear=1e-12)
+    c.L.correction_step(c.lam.copy(), c.dev(c.phi_block(c.orb)), c.dev(c.w), tol_linear=1e-12)
+    with pytest.raises(kb.KsbError, match="before mlc_begin"):
+        c.L.mlc_sweep(c.lam.copy(), Phi)
 
 
 def test_run_standard_mlc_mode(ctx):
