@@ -8,6 +8,7 @@
 //   expand                         proj/src/correction.cpp:370-381
 //   density_change (H1)            proj/src/driver.cpp:56-60
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 
 #include "correction.cuh"
@@ -286,6 +287,24 @@ void solve_orbitals(Level& L, Corrector& K, CgWork& cg, const StepOptions& o, co
     }
 }
 
+/// S x = rhs on the interior (single column): multigrid-preconditioned CG on levels above the coarse mesh,
+/// Jacobi CG otherwise or when KSB_STIFF_MG=0; a multigrid solve that breaks down or stalls is redone with
+/// Jacobi CG. Same PCG contract either way (proj/src/solver.cpp:57-111).
+CgColumnStats stiffness_solve(Level& L, Corrector& K, CgWork& cg, const double* rhs, double* x, double tol) {
+    static const char* env = std::getenv("KSB_STIFF_MG");
+    const bool use_mg = L.meshes.size() >= 2 && !(env && env[0] == '0') && K.coarse.CHi.n > 0;
+    if (use_mg) {
+        if (!K.mg.ready) mg_setup(L, K.mg, K.coarse.CHi.p);
+        const CgColumnStats st = mg_pcg(L, K.mg, rhs, x, tol, 20000);
+        if (st.converged) return st;
+    }
+    CgOptions co;
+    co.tol = tol;
+    CgColumnStats st;
+    cg_solve(*L.ctx, L, 0, -1, nullptr, rhs, x, 1, 1, co, &st, cg);
+    return st;
+}
+
 // bvp_hartree -> solve_hartree_exact (proj/src/hartree.cpp:131-144): w with Dirichlet data bcb
 int hartree_solve(Level& L, Corrector& K, CgWork& cg, const double* d_PhiT, int N, int ldT, const double* d_bcb,
                   double tol, double* d_w_full) {
@@ -294,10 +313,7 @@ int hartree_solve(Level& L, Corrector& K, CgWork& cg, const double* d_PhiT, int 
     need(K.wtil_int, L.ni);
     sqload(L, d_PhiT, N, ldT, K.sys.occ, kFourPi, K.hrhs.p, K.phys);
     lift(L, 0, d_bcb, K.hrhs.p);
-    CgOptions co;
-    co.tol = tol;
-    CgColumnStats st;
-    cg_solve(c, L, 0, -1, nullptr, K.hrhs.p, K.wtil_int.p, 1, 1, co, &st, cg);
+    const CgColumnStats st = stiffness_solve(L, K, cg, K.hrhs.p, K.wtil_int.p, tol);
     if (!st.converged)
         raise(KSB_NONCONVERGENCE, "hartree solve stalled at residual " + std::to_string(st.relative_residual));
     launch(c, "elementwise", k_full_from, grid_of(c, L.n), kT, 0, L.ni, L.nb, (const int32_t*)L.interior.p,
@@ -413,10 +429,7 @@ void hartree_of_density(Level& L, Corrector& K, CgWork& cg, const double* d_rho,
     launch(c, "elementwise", k_add, grid_of(c, ni), kT, 0, int64_t(ni), (const double*)K.hrhs.p, kFourPi,
            (const double*)K.hrhs.p, 0.0, K.hrhs.p);
     lift(L, 0, d_bcb, K.hrhs.p);
-    CgOptions co;
-    co.tol = tol;
-    CgColumnStats cs;
-    cg_solve(c, L, 0, -1, nullptr, K.hrhs.p, K.wtil_int.p, 1, 1, co, &cs, cg);
+    const CgColumnStats cs = stiffness_solve(L, K, cg, K.hrhs.p, K.wtil_int.p, tol);
     if (!cs.converged)
         raise(KSB_NONCONVERGENCE, "hartree solve stalled at residual " + std::to_string(cs.relative_residual));
     launch(c, "elementwise", k_full_from, grid_of(c, L.n), kT, 0, ni, L.nb, (const int32_t*)L.interior.p,

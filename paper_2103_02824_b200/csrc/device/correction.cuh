@@ -1,6 +1,7 @@
 // One outer iteration of the corrected level solve on the device (see correction.cu).
 #pragma once
 
+#include "mg.cuh"
 #include <array>
 #include <vector>
 
@@ -55,6 +56,7 @@ struct Corrector {
     int ldT = 0;
     int mlc_ld = 0, mlc_sweeps = 0;  // standard MLC state: ld of PhiT, sweeps run
     EstimatorData est;
+    Multigrid mg;  // V-cycle preconditioner of the stiffness solves (built on first use)
 };
 
 void level_ops(Level& L, Corrector& K);

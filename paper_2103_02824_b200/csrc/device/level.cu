@@ -1,0 +1,65 @@
+// Upload of one level's host index data (host/topology.hpp) into a device Level.
+#include "level.cuh"
+
+namespace ksb {
+
+void upload_level(Ctx& cx, std::shared_ptr<FineTopology> topo, Level& L) {
+    L.ctx = &cx;
+    L.topo = std::move(topo);
+    const auto& T = *L.topo;
+    const auto& S = *T.space;
+    const auto& M = *S.mesh;
+    L.n = S.n();
+    L.ni = S.ni();
+    L.nb = S.nb();
+    L.nt = M.n_tets();
+    L.nnz_ii = T.ii.nnz();
+    L.nnz_ib = T.ib.nnz();
+    L.nH = T.coarse->ni();
+    L.nct = T.coarse->mesh->n_tets();
+    L.ncv = T.coarse->n();
+    L.xyz.upload(cx, M.xyz);
+    L.tets.upload(cx, M.tets);
+    L.interior.upload(cx, S.interior);
+    L.boundary.upload(cx, S.boundary);
+    L.iidx.upload(cx, S.iidx);
+    L.ii_ptr.upload(cx, T.ii.ptr);
+    L.ii_col.upload(cx, T.ii.col);
+    L.ib_ptr.upload(cx, T.ib.ptr);
+    L.ib_col.upload(cx, T.ib.col);
+    L.diag_slot.upload(cx, T.diag_slot);
+    L.ii_gptr.upload(cx, T.ii_gptr);
+    L.ii_gent.upload(cx, T.ii_gent);
+    L.ib_gptr.upload(cx, T.ib_gptr);
+    L.ib_gent.upload(cx, T.ib_gent);
+    L.pint_col.upload(cx, T.pint_col);
+    L.pint_val.upload(cx, T.pint_val);
+    L.ancestor.upload(cx, T.ancestor);
+    L.anc_ptr.upload(cx, T.anc_ptr);
+    L.anc_tets.upload(cx, T.anc_tets);
+    L.vinc_ptr.upload(cx, T.vinc_ptr);
+    L.vinc.upload(cx, T.vinc);
+    L.bvinc_ptr.upload(cx, T.bvinc_ptr);
+    L.bvinc.upload(cx, T.bvinc);
+    L.cinc_ptr.upload(cx, T.cinc_ptr);
+    L.cinc.upload(cx, T.cinc);
+    L.ctets.upload(cx, T.coarse->mesh->tets);
+    L.ciidx.upload(cx, T.coarse->iidx);
+    L.cxyz.upload(cx, T.coarse->mesh->xyz);
+    L.sell_ptr.upload(cx, T.sell_ptr);
+    L.sell_col.upload(cx, T.sell_col);
+    L.sell_map.upload(cx, T.sell_map);
+    L.nslices = int(T.sell_ptr.size()) - 1;
+    L.n_prev = T.n_prev;
+    if (T.n_prev > 0) {
+        L.pstep_col.upload(cx, T.pstep_col);
+        L.pstep_val.upload(cx, T.pstep_val);
+        L.prev_iidx.upload(cx, T.prev_iidx);
+    }
+    for (int d = 0; d < 3; ++d) {
+        L.box_lo[d] = M.lo[d];
+        L.box_hi[d] = M.hi[d];
+    }
+}
+
+} // namespace ksb

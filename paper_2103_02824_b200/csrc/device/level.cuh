@@ -69,12 +69,16 @@ struct Level {
     DevBuf<double> scratch;   // term accumulation scratch (nnz_ii + nnz_ib)
     DevBuf<int> flag;         // device error flag (singular quadrature)
     Mat mats[kMaxMats];
+    std::vector<MeshPtr> meshes;  // the hierarchy's meshes 0..level (coarser levels for the multigrid)
 
     Mat& mat(int id);
     /// SELL-32 values of matrix id (converted on first use after its values changed)
     const double* sell_values(int id);
     void touch(int id) { ++mats[id].version; }
 };
+
+/// host index data -> device arrays (level.cu); L.ctx and L.topo set, operator values not assembled
+void upload_level(Ctx& cx, std::shared_ptr<FineTopology> topo, Level& L);
 
 // assembly (assemble.cu)
 struct Potential {

@@ -1,0 +1,398 @@
+// Multigrid-preconditioned CG for single-column stiffness solves (see mg.cuh).
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+
+#include "mg.cuh"
+
+namespace ksb {
+
+namespace {
+
+constexpr int kT = 256;
+
+int grid_rows(const Ctx& c, int64_t rows) {
+    return int(std::max<int64_t>(1, std::min<int64_t>((rows + kT - 1) / kT, int64_t(c.sm_count) * 4)));
+}
+
+/// (A x)_row on the SELL-32 layout: entries in ascending CSR slot order, padding has value 0
+__device__ __forceinline__ double sell_row(int row, const int32_t* __restrict__ sptr, const int32_t* __restrict__ scol,
+                                           const double* __restrict__ sval, const double* __restrict__ x) {
+    const int sl = row >> 5, i = row & 31;
+    const int base = sptr[sl], w = (sptr[sl + 1] - base) >> 5;
+    double acc = 0.0;
+    for (int e = 0; e < w; ++e) {
+        const int k = base + 32 * e + i;
+        acc = fma(sval[k], x[scol[k]], acc);
+    }
+    return acc;
+}
+
+__device__ __forceinline__ void block_partial(double v, double* part) {
+    __shared__ double red[kT / 32];
+    v = warp_sum(v);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < int(blockDim.x >> 5); ++w) s += red[w];
+        part[blockIdx.x] = s;
+    }
+}
+
+/// mode 0: out = x_in + omega D^-1 (b - A x_in)   (x_in == nullptr: out = omega D^-1 b)
+/// mode 1: out = b - A x_in
+__global__ void k_mg_smooth(int ni, const int32_t* __restrict__ sptr, const int32_t* __restrict__ scol,
+                            const double* __restrict__ sval, const double* __restrict__ dinv,
+                            const double* __restrict__ b, const double* __restrict__ xin, double* __restrict__ out,
+                            double omega, int mode) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < ni; r += gridDim.x * blockDim.x) {
+        const double ax = xin ? sell_row(r, sptr, scol, sval, xin) : 0.0;
+        const double res = b[r] - ax;
+        out[r] = mode == 1 ? res : (xin ? xin[r] : 0.0) + omega * dinv[r] * res;
+    }
+}
+
+__global__ void k_mg_restrict(int nc, const int32_t* __restrict__ rptr, const int32_t* __restrict__ ridx,
+                              const double* __restrict__ rval, const double* __restrict__ rf, double* __restrict__ bc) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nc; i += gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int k = rptr[i]; k < rptr[i + 1]; ++k) s = fma(rval[k], rf[ridx[k]], s);
+        bc[i] = s;
+    }
+}
+
+__global__ void k_mg_prolong_add(int ni, const int32_t* __restrict__ pcol, const double* __restrict__ pval,
+                                 const double* __restrict__ xc, double* __restrict__ x) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < ni; r += gridDim.x * blockDim.x) {
+        double s = x[r];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int q = pcol[4 * size_t(r) + k];
+            if (q >= 0) s = fma(pval[4 * size_t(r) + k], xc[q], s);
+        }
+        x[r] = s;
+    }
+}
+
+/// x = A b for a dense row-major n x n A: warp per row, four independent load chains per lane
+__global__ void k_mg_dense(int n, const double* __restrict__ A, const double* __restrict__ b, double* __restrict__ x) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (warp >= n) return;
+    const double* a = A + size_t(warp) * n;
+    double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
+    int c = lane;
+    for (; c + 96 < n; c += 128) {
+        t0 = fma(a[c], b[c], t0);
+        t1 = fma(a[c + 32], b[c + 32], t1);
+        t2 = fma(a[c + 64], b[c + 64], t2);
+        t3 = fma(a[c + 96], b[c + 96], t3);
+    }
+    for (; c < n; c += 32) t0 = fma(a[c], b[c], t0);
+    const double t = warp_sum((t0 + t1) + (t2 + t3));
+    if (lane == 0) x[warp] = t;
+}
+
+__global__ void k_mg_dinv(int ni, const int32_t* __restrict__ diag_slot, const double* __restrict__ vals,
+                          double* __restrict__ dinv) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < ni; r += gridDim.x * blockDim.x) {
+        const double d = vals[diag_slot[r]];
+        dinv[r] = d != 0.0 ? 1.0 / d : 1.0;
+    }
+}
+
+// ---- PCG pieces; scalars live in scal[], fixed-order reductions (block partials, then one fold)
+enum { kRZ0 = 0, kRZ1 = 1, kPAP = 2, kRR = 3, kBB = 4 };
+
+__global__ void __launch_bounds__(kT) k_pcg_spmv_dot(int ni, const int32_t* __restrict__ sptr,
+                                                     const int32_t* __restrict__ scol, const double* __restrict__ sval,
+                                                     const double* __restrict__ p, double* __restrict__ q,
+                                                     double* __restrict__ part) {
+    double acc = 0.0;
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < ni; r += gridDim.x * blockDim.x) {
+        const double v = sell_row(r, sptr, scol, sval, p);
+        q[r] = v;
+        acc = fma(p[r], v, acc);
+    }
+    block_partial(acc, part);
+}
+
+__global__ void __launch_bounds__(kT) k_pcg_axpy(int ni, double* __restrict__ x, double* __restrict__ r,
+                                                 const double* __restrict__ p, const double* __restrict__ q,
+                                                 const double* __restrict__ scal, int irz, double* __restrict__ part) {
+    const double pap = scal[kPAP];
+    const double alpha = pap > 0.0 ? scal[irz] / pap : 0.0;
+    double acc = 0.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ni; i += gridDim.x * blockDim.x) {
+        x[i] = fma(alpha, p[i], x[i]);
+        const double v = fma(-alpha, q[i], r[i]);
+        r[i] = v;
+        acc = fma(v, v, acc);
+    }
+    block_partial(acc, part);
+}
+
+__global__ void __launch_bounds__(kT) k_pcg_dot(int ni, const double* __restrict__ a, const double* __restrict__ b,
+                                                double* __restrict__ part) {
+    double acc = 0.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ni; i += gridDim.x * blockDim.x) acc = fma(a[i], b[i], acc);
+    block_partial(acc, part);
+}
+
+/// r = b - A x, partial r.r
+__global__ void __launch_bounds__(kT) k_pcg_resid(int ni, const int32_t* __restrict__ sptr,
+                                                  const int32_t* __restrict__ scol, const double* __restrict__ sval,
+                                                  const double* __restrict__ b, const double* __restrict__ x,
+                                                  double* __restrict__ r, double* __restrict__ part) {
+    double acc = 0.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ni; i += gridDim.x * blockDim.x) {
+        const double v = b[i] - sell_row(i, sptr, scol, sval, x);
+        r[i] = v;
+        acc = fma(v, v, acc);
+    }
+    block_partial(acc, part);
+}
+
+__global__ void k_fold(int nb, const double* __restrict__ part, double* __restrict__ scal, int idx) {
+    double s = 0.0;
+    for (int i = threadIdx.x; i < nb; i += 32) s += part[i];
+    s = warp_sum(s);
+    if (threadIdx.x == 0) scal[idx] = s;
+}
+
+/// p = z + (rz_new / rz_old) p
+__global__ void k_pcg_p(int ni, const double* __restrict__ z, double* __restrict__ p, const double* __restrict__ scal,
+                        int inew, int iold) {
+    const double beta = scal[inew] / scal[iold];
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ni; i += gridDim.x * blockDim.x) p[i] = fma(beta, p[i], z[i]);
+}
+
+void vcycle(Multigrid& mg, int l, const double* b, double* x) {
+    Ctx& c = *mg.lv[size_t(mg.top)]->L->ctx;
+    if (l == 0) {
+        launch(c, "mg", k_mg_dense, ceil_div(mg.nH * 32, kT), kT, 0, mg.nH, mg.CHi, b, x);
+        return;
+    }
+    MgLevel& m = *mg.lv[size_t(l)];
+    Level& L = *m.L;
+    const double* A = L.sell_values(0);
+    const int g = grid_rows(c, m.ni);
+    auto smooth = [&](const double* xin, double* out, int mode) {
+        launch(c, "mg", k_mg_smooth, g, kT, 0, m.ni, (const int32_t*)L.sell_ptr.p, (const int32_t*)L.sell_col.p, A,
+               (const double*)m.dinv.p, b, xin, out, mg.omega, mode);
+    };
+    // pre-smoothing from x = 0; the sweeps alternate between x and y
+    smooth(nullptr, x, 0);
+    double* cur = x;
+    double* oth = m.y.p;
+    for (int s = 1; s < mg.nu; ++s) {
+        smooth(cur, oth, 0);
+        std::swap(cur, oth);
+    }
+    smooth(cur, m.r.p, 1);
+    double* bc = l == 1 ? mg.b0.p : mg.lv[size_t(l) - 1]->b.p;
+    double* xc = l == 1 ? mg.x0.p : mg.lv[size_t(l) - 1]->x.p;
+    launch(c, "mg", k_mg_restrict, grid_rows(c, m.nc), kT, 0, m.nc, (const int32_t*)m.rptr.p,
+           (const int32_t*)m.ridx.p, (const double*)m.rval.p, (const double*)m.r.p, bc);
+    vcycle(mg, l - 1, bc, xc);
+    launch(c, "mg", k_mg_prolong_add, g, kT, 0, m.ni, (const int32_t*)m.pcol.p, (const double*)m.pval.p,
+           (const double*)xc, cur);
+    for (int s = 0; s < mg.nu; ++s) {
+        smooth(cur, oth, 0);
+        std::swap(cur, oth);
+    }
+    if (cur != x) KSB_CUDA_CHECK(cudaMemcpyAsync(x, cur, sizeof(double) * m.ni, cudaMemcpyDeviceToDevice, c.stream));
+}
+
+}  // namespace
+
+Multigrid::~Multigrid() {
+    for (auto& e : iter_exec)
+        if (e) cudaGraphExecDestroy(e);
+}
+
+void mg_setup(Level& L, Multigrid& mg, const double* d_CHi) {
+    Ctx& c = *L.ctx;
+    const int top = int(L.meshes.size()) - 1;
+    if (top < 1) raise(KSB_INVALID_ARGUMENT, "multigrid needs a level above the coarse mesh");
+    if (!L.mats[0].valid) raise(KSB_INVALID_ARGUMENT, "multigrid: stiffness not assembled");
+    mg.lv.clear();
+    for (int l = 0; l <= top; ++l) mg.lv.push_back(std::make_unique<MgLevel>());
+    mg.top = top;
+    mg.CHi = d_CHi;
+    mg.nH = L.nH;
+    for (int l = 1; l <= top; ++l) {
+        MgLevel& m = *mg.lv[size_t(l)];
+        if (l == top) {
+            m.L = &L;
+        } else {
+            Hierarchy h;
+            for (int k = 0; k <= l; ++k) h.push(L.meshes[size_t(k)]);
+            m.own = std::make_unique<Level>();
+            upload_level(c, build_topology(h, l), *m.own);
+            m.own->flag.alloc(4);
+            assemble_into(*m.own, 0, 1.0, 0.0, nullptr, 0.0, nullptr, 0.0);  // S
+            m.L = m.own.get();
+        }
+        const FineTopology& T = *m.L->topo;
+        const Space& S = *T.space;
+        m.ni = S.ni();
+        m.nc = l == 1 ? L.nH : mg.lv[size_t(l) - 1]->ni;
+        // interior-restricted one-step prolongation and its transpose
+        std::vector<int32_t> pc(size_t(m.ni) * 4, -1), cnt(size_t(m.nc) + 1, 0);
+        std::vector<double> pv(size_t(m.ni) * 4, 0.0);
+        for (int r = 0; r < m.ni; ++r) {
+            const int v = S.interior[size_t(r)];
+            int w = 0;
+            for (int k = 0; k < 4; ++k) {
+                const int u = T.pstep_col[4 * size_t(v) + k];
+                if (u < 0) break;
+                const int q = T.prev_iidx[size_t(u)];
+                if (q < 0) continue;
+                pc[4 * size_t(r) + w] = q;
+                pv[4 * size_t(r) + w] = T.pstep_val[4 * size_t(v) + k];
+                ++cnt[size_t(q) + 1];
+                ++w;
+            }
+        }
+        for (int i = 0; i < m.nc; ++i) cnt[size_t(i) + 1] += cnt[size_t(i)];
+        const size_t nr = static_cast<size_t>(cnt[size_t(m.nc)]);
+        std::vector<int32_t> ri(nr), fill(cnt.begin(), cnt.end() - 1);
+        std::vector<double> rv(ri.size());
+        for (int r = 0; r < m.ni; ++r)  // ascending fine row inside every coarse row
+            for (int k = 0; k < 4; ++k) {
+                const int q = pc[4 * size_t(r) + k];
+                if (q < 0) break;
+                ri[size_t(fill[size_t(q)])] = r;
+                rv[size_t(fill[size_t(q)]++)] = pv[4 * size_t(r) + k];
+            }
+        m.pcol.upload(c, pc);
+        m.pval.upload(c, pv);
+        m.rptr.upload(c, cnt);
+        m.ridx.upload(c, ri);
+        m.rval.upload(c, rv);
+        for (auto* b : {&m.dinv, &m.b, &m.x, &m.y, &m.r}) b->alloc(std::max(1, m.ni));
+        launch(c, "mg", k_mg_dinv, grid_rows(c, m.ni), kT, 0, m.ni, (const int32_t*)m.L->diag_slot.p,
+               (const double*)m.L->mats[0].ii.p, m.dinv.p);
+        KSB_CUDA_CHECK(cudaStreamSynchronize(c.stream));  // host staging vectors go out of scope
+    }
+    mg.b0.alloc(std::max(1, mg.nH));
+    mg.x0.alloc(std::max(1, mg.nH));
+    mg.part.alloc(int64_t(c.sm_count) * 4);
+    mg.scal.alloc(8);
+    for (auto* b : {&mg.p, &mg.q, &mg.z, &mg.r, &mg.t}) b->alloc(std::max(1, L.ni));
+    mg.ready = true;
+}
+
+CgColumnStats mg_pcg(Level& L, Multigrid& mg, const double* d_b, double* d_x, double tol, int max_iterations) {
+    Ctx& c = *L.ctx;
+    const int ni = L.ni, top = mg.top;
+    const double* A = L.sell_values(0);
+    const int32_t* sp = (const int32_t*)L.sell_ptr.p;
+    const int32_t* sc = (const int32_t*)L.sell_col.p;
+    const int g = grid_rows(c, ni);
+    auto fold = [&](int idx) { launch(c, "mg", k_fold, 1, 32, 0, g, (const double*)mg.part.p, mg.scal.p, idx); };
+    auto read = [&](int i0, int n, double* h) {
+        KSB_CUDA_CHECK(cudaMemcpyAsync(h, mg.scal.p + i0, sizeof(double) * n, cudaMemcpyDeviceToHost, c.stream));
+        KSB_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    };
+    CgColumnStats st;
+    launch(c, "mg", k_pcg_dot, g, kT, 0, ni, d_b, d_b, mg.part.p);
+    fold(kBB);
+    double bb;
+    read(kBB, 1, &bb);
+    const double bnorm = std::sqrt(bb);
+    KSB_CUDA_CHECK(cudaMemsetAsync(d_x, 0, sizeof(double) * ni, c.stream));
+    if (bnorm == 0.0) {  // zero-rhs exit (proj/src/solver.cpp:62-66)
+        st.converged = 1;
+        KSB_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+        return st;
+    }
+    KSB_CUDA_CHECK(cudaMemcpyAsync(mg.r.p, d_b, sizeof(double) * ni, cudaMemcpyDeviceToDevice, c.stream));
+    int irz = kRZ0;
+    auto precondition = [&]() {  // z = V(r); p = z; rz = r.z into slot irz
+        vcycle(mg, top, mg.r.p, mg.z.p);
+        KSB_CUDA_CHECK(cudaMemcpyAsync(mg.p.p, mg.z.p, sizeof(double) * ni, cudaMemcpyDeviceToDevice, c.stream));
+        launch(c, "mg", k_pcg_dot, g, kT, 0, ni, (const double*)mg.r.p, (const double*)mg.z.p, mg.part.p);
+        fold(irz);
+    };
+    // A p, pAp, x += alpha p, r -= alpha q, r.r with alpha from slot irz
+    auto step = [&](int iz) {
+        launch(c, "mg", k_pcg_spmv_dot, g, kT, 0, ni, sp, sc, A, (const double*)mg.p.p, mg.q.p, mg.part.p);
+        fold(kPAP);
+        launch(c, "mg", k_pcg_axpy, g, kT, 0, ni, d_x, mg.r.p, (const double*)mg.p.p, (const double*)mg.q.p,
+               (const double*)mg.scal.p, iz, mg.part.p);
+        fold(kRR);
+    };
+    // z = V(r), r.z into the other slot, p = z + beta p, then the next step: one graph per slot parity
+    auto next = [&](int iz) {
+        const int inew = iz ^ 1;
+        vcycle(mg, top, mg.r.p, mg.z.p);
+        launch(c, "mg", k_pcg_dot, g, kT, 0, ni, (const double*)mg.r.p, (const double*)mg.z.p, mg.part.p);
+        fold(inew);
+        launch(c, "mg", k_pcg_p, g, kT, 0, ni, (const double*)mg.z.p, mg.p.p, (const double*)mg.scal.p, inew, iz);
+        step(inew);
+    };
+    static const char* genv = std::getenv("KSB_MG_GRAPHS");
+    const bool graphs = !c.profiling && !(genv && genv[0] == '0');
+    if (graphs && mg.iter_x != d_x) {
+        for (auto& e : mg.iter_exec)
+            if (e) {
+                cudaGraphExecDestroy(e);
+                e = nullptr;
+            }
+        mg.iter_x = d_x;
+    }
+    auto run_next = [&](int iz) {
+        if (!graphs) {
+            next(iz);
+            return;
+        }
+        if (!mg.iter_exec[iz]) {
+            cudaGraph_t graph;
+            KSB_CUDA_CHECK(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeRelaxed));
+            next(iz);
+            KSB_CUDA_CHECK(cudaStreamEndCapture(c.stream, &graph));
+            KSB_CUDA_CHECK(cudaGraphInstantiate(&mg.iter_exec[iz], graph, 0));
+            KSB_CUDA_CHECK(cudaGraphDestroy(graph));
+        }
+        KSB_CUDA_CHECK(cudaGraphLaunch(mg.iter_exec[iz], c.stream));
+    };
+    precondition();
+    step(irz);
+    for (int it = 0; it < max_iterations; ++it) {
+        double h[2];
+        read(kPAP, 2, h);
+        if (!(h[0] > 0.0)) {  // breakdown (solver.cpp:74-79): alpha = 0 left x and r unchanged, h[1] = r.r
+            st.breakdown = 1;
+            st.iterations = it;
+            st.relative_residual = std::sqrt(h[1]) / bnorm;
+            return st;
+        }
+        double rel = std::sqrt(h[1]) / bnorm;
+        st.iterations = it + 1;
+        st.relative_residual = rel;
+        if (rel <= tol) {  // accept on the true residual, else restart from it (solver.cpp:84-101)
+            launch(c, "mg", k_pcg_resid, g, kT, 0, ni, sp, sc, A, d_b, (const double*)d_x, mg.r.p, mg.part.p);
+            fold(kRR);
+            double rr;
+            read(kRR, 1, &rr);
+            rel = std::sqrt(rr) / bnorm;
+            st.relative_residual = rel;
+            if (rel <= tol) {
+                st.converged = 1;
+                return st;
+            }
+            precondition();
+            step(irz);
+            continue;
+        }
+        if (it + 1 == max_iterations) break;
+        run_next(irz);
+        irz ^= 1;
+    }
+    KSB_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    return st;
+}
+
+} // namespace ksb
