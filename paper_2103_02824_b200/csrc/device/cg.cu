@@ -861,6 +861,19 @@ __global__ void __launch_bounds__(kThreads, 3) k_trueres(int ni, Cols cc, const 
     double tt[CPL], tz[CPL];
 #pragma unroll
     for (int q = 0; q < CPL; ++q) tt[q] = tz[q] = 0.0;
+    // gather only the column pairs (FULL) / lane columns that have a flagged column: usually a few of N
+    unsigned need = 0;
+    if constexpr (FULL != 0) {
+#pragma unroll
+        for (int q = 0; q < CPL; q += 2) {
+            const int c = full_col<G>(l, q);
+            if ((c < N && s.check[c]) || (c + 1 < N && s.check[c + 1])) need |= 1u << (q >> 1);
+        }
+    } else if constexpr (!SPLIT) {
+#pragma unroll
+        for (int q = 0; q < CPL; ++q)
+            if (c0 + q < N && s.check[c0 + q]) need = 1u;
+    }
     for (int base = warp * rows_per_warp; base < ni; base += nwarps * rows_per_warp) {
         const int r = base + g;
         const bool valid = r < ni;
@@ -869,7 +882,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_trueres(int ni, Cols cc, const 
         if constexpr (SPLIT) {
             row_split<G, SHIFT>(rb, re, col, A, Bv, X, ld, l, acc[0], accB[0]);
         } else {
-            row_product<G, CPL, SHIFT, FULL>(valid ? r : 0, rb, re, col, A, Bv, X, ld, c0, N, l, gbase, acc, accB);
+            row_product<G, CPL, SHIFT, FULL>(valid ? r : 0, rb, re, col, A, Bv, X, ld, c0, N, l, gbase, acc, accB,
+                                             need);
         }
         if (valid && (!SPLIT || l == 0) && (FULL || c0 < N)) {
 #pragma unroll
@@ -1077,9 +1091,9 @@ void launch_iteration(Ctx& c, const Level& L, const CgWork& w, const Cols& cc, c
     else
         launch(c, "cg_update_r", k_update_r<1>, grid_e, kThreads, sm_e, L.ni, cc, w.R, (const double*)w.AP, w.dev);
     if (!cc.fixed)
-        // runs every iteration but only works when a column was flagged (rare): one block per SM keeps the
-        // common early exit cheap
-        launch(c, "cg_trueres", k_trueres<G, CPL, SHIFT, SPLIT, FULL>, std::min(grid_s, c.sm_count), kThreads, sm_s, L.ni, cc,
+        // runs every iteration but only works when a column was flagged; with many columns that is most
+        // iterations (N = 120: 40 of 41), so it gets the SpMM's full resident grid (the early exit stays ~2 us)
+        launch(c, "cg_trueres", k_trueres<G, CPL, SHIFT, SPLIT, FULL>, grid_s, kThreads, sm_s, L.ni, cc,
                (const int32_t*)L.ii_ptr.p, (const int32_t*)L.ii_col.p, A, Bv, Bb, (const double*)X,
                (const double*)w.AP, w.R, w.dev);
     if (v2)

@@ -103,7 +103,8 @@ template <int G, int CPL, bool SHIFT, int FULL = 0>
 __device__ __forceinline__ void row_product(int r, int rb, int re, const int32_t* __restrict__ col,
                                             const double* __restrict__ A, const double* __restrict__ B,
                                             const double* __restrict__ X, int ldx, int c0, int N, int l,
-                                            int gbase, double (&acc)[CPL], double (&accB)[CPL]) {
+                                            int gbase, double (&acc)[CPL], double (&accB)[CPL],
+                                            unsigned need = ~0u) {
 #pragma unroll
     for (int k = 0; k < CPL; ++k) acc[k] = accB[k] = 0.0;
     constexpr int NB = (G >= 16) ? 1 : 16 / G;
@@ -134,10 +135,22 @@ __device__ __forceinline__ void row_product(int r, int rb, int re, const int32_t
 #pragma unroll
                 for (int u = 0; u < UB; ++u) {
                     const int j = __shfl_sync(0xffffffffu, mc[b], gbase + s0 + u);
-                    if (FULL)
-                        load_full<G, CPL, FULL>(X + size_t(j) * ldx, l, N, x[u]);
-                    else
+                    if (FULL) {
+                        // need: bit k of a FULL lane = its column pair k is wanted (skipped pairs read nothing)
+#pragma unroll
+                        for (int k = 0; k < CPL; k += 2) {
+                            double2 a = make_double2(0.0, 0.0);
+                            if (((need >> (k >> 1)) & 1u) && pair_ok(FULL, full_col<G>(l, k), N))
+                                a = __ldg(reinterpret_cast<const double2*>(X + size_t(j) * ldx + full_col<G>(l, k)));
+                            x[u][k] = a.x;
+                            x[u][k + 1] = a.y;
+                        }
+                    } else if (need & 1u) {
                         load_cols<CPL>(X + size_t(j) * ldx + c0, c0, N, x[u]);
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < CPL; ++k) x[u][k] = 0.0;
+                    }
                 }
 #pragma unroll
                 for (int u = 0; u < UB; ++u) {
