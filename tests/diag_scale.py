@@ -61,6 +61,9 @@ def run(name, atoms, N, box, refine, sweeps, steps=2, profile=True):
 
 
 if __name__ == "__main__":
-    run("cfg4-like N=21, 250k dofs", ring_atoms(), 21, 25.0, 3, 10)
-    run("cfg5-like N=120, 250k dofs", sphere_atoms(), 120, 30.0, 3, 10)
-    run("cfg5-like N=120, 2.1M dofs", sphere_atoms(), 120, 30.0, 4, 10)
+    cases = [("cfg4-like N=21, 250k dofs", ring_atoms(), 21, 25.0, 3, 10),
+             ("cfg5-like N=120, 250k dofs", sphere_atoms(), 120, 30.0, 3, 10),
+             ("cfg5-like N=120, 2.1M dofs", sphere_atoms(), 120, 30.0, 4, 10)]
+    pick = [int(a) for a in sys.argv[1:]] or range(len(cases))
+    for k in pick:
+        run(*cases[k], steps=1 if len(sys.argv) > 1 else 2, profile=len(sys.argv) == 1)
