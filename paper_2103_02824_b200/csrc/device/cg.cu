@@ -286,7 +286,9 @@ template <int G, int CPL, bool SHIFT, bool SPLIT, int FULL, int MINB = KSB_SPMM_
 __global__ void __launch_bounds__(kThreads, MINB) k_spmm_dot(int ni, Cols cc, const int32_t* __restrict__ ptr,
                                                        const int32_t* __restrict__ col, const double* __restrict__ A,
                                                        const double* __restrict__ Bv, const double* __restrict__ P,
-                                                       double* __restrict__ AP, CgDev s) {
+                                                       double* __restrict__ AP, CgDev s, int sync_every) {
+    // sync_every > 0 (cooperative launch only): a grid barrier every sync_every tile steps keeps the blocks in
+    // one band of rows, so the band's stencil window of wide X rows stays in L2 instead of being re-read
     extern __shared__ double sm[];
     const int N = cc.N, ld = cc.ld;
     const int lane = threadIdx.x & 31;
@@ -314,7 +316,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_dot(int ni, Cols cc, co
         nb_rb = v1 ? __ldg(ptr + r1) : 0;
         nb_re = v1 ? __ldg(ptr + r1 + 1) : 0;
     }
-    for (; t < tw.tend; t += tw.step) {
+    const int ksteps = (tw.tend + tw.step - 1) / tw.step;  // the same count for every warp of the grid
+    for (int ks = 0; ks < ksteps; ++ks, t += tw.step) {
+        if (sync_every > 0 && ks > 0 && ks % sync_every == 0) cooperative_groups::this_grid().sync();
         const int r = t * rows_per_warp + g;
         const bool valid = r < ni;
         double acc[CPL], accB[CPL];
@@ -1072,10 +1076,30 @@ void launch_iteration(Ctx& c, const Level& L, const CgWork& w, const Cols& cc, c
     } else {
         static const char* mb = std::getenv("KSB_SPMM_MINB");
         const int minb = mb ? std::atoi(mb) : KSB_SPMM_MINB;
+        static const char* senv = std::getenv("KSB_SPMM_SYNC");
+        const int sync_every = G >= 16 ? (senv ? std::atoi(senv) : 8) : 0;
         auto go = [&](auto kern) {
             grid_s = std::min(grid_s, resident_grid(c, kern, kThreads, sm_s));
-            launch(c, "spmm", kern, grid_s, kThreads, sm_s, L.ni, cc, (const int32_t*)L.ii_ptr.p,
-                   (const int32_t*)L.ii_col.p, A, Bv, (const double*)w.P, w.AP, w.dev);
+            if (sync_every > 0) {
+                int ni = L.ni;
+                Cols ccv = cc;
+                const int32_t* ptr = L.ii_ptr.p;
+                const int32_t* col = L.ii_col.p;
+                const double* Pp = w.P;
+                double* APp = w.AP;
+                CgDev dv = w.dev;
+                int se = sync_every;
+                void* args[] = {&ni, &ccv, &ptr, &col, &A, &Bv, &Pp, &APp, &dv, &se};
+                cudaEvent_t e0 = nullptr;
+                if (c.profiling) c.begin("spmm", &e0);
+                KSB_CUDA_CHECK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(grid_s),
+                                                           dim3(kThreads), args, sm_s, c.stream));
+                ++c.launches;
+                if (c.profiling) c.end("spmm", e0);
+            } else {
+                launch(c, "spmm", kern, grid_s, kThreads, sm_s, L.ni, cc, (const int32_t*)L.ii_ptr.p,
+                       (const int32_t*)L.ii_col.p, A, Bv, (const double*)w.P, w.AP, w.dev, 0);
+            }
         };
         if (FULL && minb == 4)
             go(k_spmm_dot<G, CPL, SHIFT, SPLIT, FULL, 4>);
