@@ -242,6 +242,19 @@ const double* Level::sell_values(int id) {
     return M.sell.p;
 }
 
+const double* Level::t8_values(int id) {
+    Mat& M = mats[id];
+    if (!M.valid) raise(KSB_INVALID_ARGUMENT, "matrix not assembled");
+    if (t8_map.n == 0) return nullptr;
+    if (M.t8_version != M.version) {
+        if (M.t8.n < t8_map.n) M.t8.alloc(t8_map.n);
+        launch(*ctx, "t8_pack", k_sell_pack, grid_for(*ctx, t8_map.n, 256), 256, 0, int64_t(t8_map.n),
+               (const int32_t*)t8_map.p, (const double*)M.ii.p, M.t8.p);
+        M.t8_version = M.version;
+    }
+    return M.t8.p;
+}
+
 Mat& Level::mat(int id) {
     if (id < 0 || id >= kMaxMats) raise(KSB_INVALID_ARGUMENT, "matrix id out of range");
     Mat& m = mats[id];

@@ -344,7 +344,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_dot(int ni, Cols cc, co
                 if (SHIFT) {
 #pragma unroll
                     for (int q = 0; q < CPL; ++q)
-                        if (FULL == 1 || full_col<G>(l, q) < N) acc[q] = fma(s.sigma[full_col<G>(l, q)], accB[q], acc[q]);
+                        if (FULL != 2 || lay_col<G, FULL>(l, q) < N) acc[q] = fma(s.sigma[lay_col<G, FULL>(l, q)], accB[q], acc[q]);
                 }
                 double p[CPL];
                 load_full<G, CPL, FULL>(P + size_t(r) * ld, l, N, p);
@@ -376,13 +376,200 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_dot(int ni, Cols cc, co
         for (int o = 16; o >= G; o >>= 1) pd[q] += __shfl_xor_sync(0xffffffffu, pd[q], o);
     if (lane < G) {
 #pragma unroll
-        for (int q = 0; q < CPL; ++q) sm[wib * width + (FULL ? full_col<G>(l, q) : l * CPL + q)] = pd[q];
+        for (int q = 0; q < CPL; ++q) sm[wib * width + (FULL ? lay_col<G, FULL>(l, q) : l * CPL + q)] = pd[q];
     }
     __syncthreads();
     if (threadIdx.x < N) {
         double t = 0.0;
         for (int k = 0; k < nwb; ++k) t += sm[k * width + threadIdx.x];
         s.part0[size_t(blockIdx.x) * N + threadIdx.x] = t;
+    }
+    k1_epilogue(sm, N, cc, s);
+}
+
+// ---------------- K1 (streamed quad variant): a continuous gather pipeline across row tiles ----------------
+/// Quad layout, CPL = 4, no shift. The tile's SL = NB*G slots are consumed in order from a ring of D gather
+/// buffers; every consumed slot immediately refills its buffer with the gather D slots ahead -- in the current
+/// tile, and past its end in the NEXT tile (whose (col, val) chunk is already in registers). So every lane keeps
+/// D gathers in flight through the tile boundaries and the row epilogue, instead of draining its batch before
+/// each new one (k_spmm_dot). Used when no row of the pattern is longer than SL (the host checks
+/// Level::max_row_ii); same accumulation order per row as k_spmm_dot.
+template <int G, int D, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_spmm_stream(int ni, Cols cc, const int32_t* __restrict__ ptr,
+                                                              const int32_t* __restrict__ col,
+                                                              const double* __restrict__ A, const double* __restrict__ P,
+                                                              double* __restrict__ AP, CgDev s) {
+    constexpr int CPL = 4;
+    using Ch = RowChunk<G, false>;
+    constexpr int SL = Ch::NB * G;
+    static_assert(SL % D == 0, "slots per tile must be a multiple of the pipeline depth");
+    extern __shared__ double sm[];
+    const int N = cc.N, ld = cc.ld;
+    const int lane = threadIdx.x & 31;
+    const int g = lane / G, l = lane % G;
+    const int gbase = g * G;
+    constexpr int RPW = 32 / G;
+    const int xoff = lay_col<G, 3>(l, 0);
+    double pd[CPL] = {0.0, 0.0, 0.0, 0.0};
+    const TileWalk tw((ni + RPW - 1) / RPW);
+    const int ksteps = (tw.tend + tw.step - 1) / tw.step;
+    auto chunk_of = [&](int t, Ch& ch) {
+        const int r = t * RPW + g;
+        const bool v = t < tw.tend && r < ni;
+        ch.load(v ? r : 0, v ? __ldg(ptr + r) : 0, v ? __ldg(ptr + r + 1) : 0, l, col, A, nullptr);
+        return __reduce_max_sync(0xffffffffu, ch.re - ch.rb);
+    };
+    // gather of slot q of chunk ch into x (predicated off past the warp's longest row)
+    auto gather = [&](const Ch& ch, int w, int q, double (&x)[CPL]) {
+        const int j = __shfl_sync(0xffffffffu, ch.mc[q / G], gbase + q % G);
+        if (q < w)
+            ldg4(P + size_t(j) * ld + xoff, x[0], x[1], x[2], x[3]);
+        else
+            x[0] = x[1] = x[2] = x[3] = 0.0;
+    };
+    int t = tw.t0;
+    Ch cur, nxt;
+    int wc = chunk_of(t, cur);
+    int wn = chunk_of(t + tw.step, nxt);
+    double x[D][CPL];
+#pragma unroll
+    for (int q = 0; q < D; ++q) gather(cur, wc, q, x[q]);
+    for (int ks = 0; ks < ksteps; ++ks, t += tw.step) {
+        const int r = t * RPW + g;
+        const bool valid = r < ni && t < tw.tend;
+        double acc[CPL] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int q = 0; q < SL; ++q) {
+            const int b = q % D;
+            const double a = __shfl_sync(0xffffffffu, cur.ma[q / G], gbase + q % G);
+#pragma unroll
+            for (int k = 0; k < CPL; ++k) acc[k] = fma(a, x[b][k], acc[k]);
+            if (q + D < SL)
+                gather(cur, wc, q + D, x[b]);
+            else
+                gather(nxt, wn, q + D - SL, x[b]);
+        }
+        if (valid) {
+            double p[CPL];
+            load_full<G, CPL, 3>(P + size_t(r) * ld, l, N, p);
+            store_full<G, CPL, 3>(AP + size_t(r) * ld, l, N, acc);
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) pd[q] = fma(p[q], acc[q], pd[q]);
+        }
+        cur = nxt;
+        wc = wn;
+        wn = chunk_of(t + 2 * tw.step, nxt);
+    }
+    const int width = G * CPL;
+    const int nwb = blockDim.x >> 5, wib = threadIdx.x >> 5;
+#pragma unroll
+    for (int q = 0; q < CPL; ++q)
+        for (int o = 16; o >= G; o >>= 1) pd[q] += __shfl_xor_sync(0xffffffffu, pd[q], o);
+    if (lane < G) {
+#pragma unroll
+        for (int q = 0; q < CPL; ++q) sm[wib * width + lay_col<G, 3>(l, q)] = pd[q];
+    }
+    __syncthreads();
+    if (threadIdx.x < N) {
+        double tt = 0.0;
+        for (int k = 0; k < nwb; ++k) tt += sm[k * width + threadIdx.x];
+        s.part0[size_t(blockIdx.x) * N + threadIdx.x] = tt;
+    }
+    k1_epilogue(sm, N, cc, s);
+}
+
+// ---------------- K1 (T8 variant, N = 16): ELL-16 rows, one load per tile, continuous gather pipeline ----------------
+/// The T8 view is ELL with 16 slots per row (row-major), so a warp tile of 8 rows is one contiguous 512-byte
+/// column run and one 1-KB value run: lane l of row group g loads slots 4l..4l+3 of its row with one 16-byte
+/// and one 32-byte load (12 L1 wavefronts per tile instead of ~60 for the scattered CSR chunk loads of
+/// k_spmm_stream), one tile ahead. Slot q's (col, val) is then broadcast from lane 4g + q/4, register q%4.
+/// The slot stream runs across tile boundaries as in k_spmm_stream: consume slot s, issue the gather of slot
+/// s + D. Lane l owns the column quad 4l..4l+3 of the N = 16 block. Padding slots (col = -1) gather nothing.
+/// Same accumulation order per row as the CSR kernels.
+struct EllChunk {
+    int c[4];
+    double v[4];
+};
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 2) k_spmm_t8(int ni, Cols cc, const int32_t* __restrict__ tcol,
+                                                       const double* __restrict__ tval, const double* __restrict__ P,
+                                                       double* __restrict__ AP, CgDev s) {
+    constexpr int G = 4, CPL = 4, RPW = 8, SL = 16;
+    static_assert(SL % D == 0, "pipeline depth");
+    extern __shared__ double sm[];
+    const int N = cc.N, ld = cc.ld;
+    const int lane = threadIdx.x & 31;
+    const int g = lane / G, l = lane % G;
+    const int gbase = g * G;
+    const int xoff = CPL * l;
+    double pd[CPL] = {0.0, 0.0, 0.0, 0.0};
+    const TileWalk tw((ni + RPW - 1) / RPW);
+    const int ksteps = (tw.tend + tw.step - 1) / tw.step;
+    auto chunk_of = [&](int k, EllChunk& ch) {
+        const int t = tw.t0 + k * tw.step;
+        const int r = t * RPW + g;
+        if (t < tw.tend && r < ni) {
+            const int4 c4 = __ldg(reinterpret_cast<const int4*>(tcol + size_t(r) * SL) + l);
+            ch.c[0] = c4.x, ch.c[1] = c4.y, ch.c[2] = c4.z, ch.c[3] = c4.w;
+            ldg4(tval + size_t(r) * SL + 4 * l, ch.v[0], ch.v[1], ch.v[2], ch.v[3]);
+        } else {
+            ch.c[0] = ch.c[1] = ch.c[2] = ch.c[3] = -1;
+            ch.v[0] = ch.v[1] = ch.v[2] = ch.v[3] = 0.0;
+        }
+    };
+    auto gather = [&](const EllChunk& ch, int q, double (&x)[CPL]) {
+        const int j = __shfl_sync(0xffffffffu, ch.c[q % 4], gbase + q / 4);
+        if (j >= 0)
+            ldg4(P + size_t(j) * ld + xoff, x[0], x[1], x[2], x[3]);
+        else
+            x[0] = x[1] = x[2] = x[3] = 0.0;
+    };
+    EllChunk cur, nxt;
+    chunk_of(0, cur);
+    chunk_of(1, nxt);
+    double x[D][CPL];
+#pragma unroll
+    for (int q = 0; q < D; ++q) gather(cur, q, x[q]);
+    for (int k = 0; k < ksteps; ++k) {
+        double acc[CPL] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int q = 0; q < SL; ++q) {
+            const int b = q % D;
+            const double a = __shfl_sync(0xffffffffu, cur.v[q % 4], gbase + q / 4);
+#pragma unroll
+            for (int e = 0; e < CPL; ++e) acc[e] = fma(a, x[b][e], acc[e]);
+            if (q + D < SL)
+                gather(cur, q + D, x[b]);
+            else
+                gather(nxt, q + D - SL, x[b]);
+        }
+        const int t = tw.t0 + k * tw.step;
+        const int r = t * RPW + g;
+        if (t < tw.tend && r < ni) {
+            double p[CPL];
+            load_full<G, CPL, 3>(P + size_t(r) * ld, l, N, p);
+            store_full<G, CPL, 3>(AP + size_t(r) * ld, l, N, acc);
+#pragma unroll
+            for (int e = 0; e < CPL; ++e) pd[e] = fma(p[e], acc[e], pd[e]);
+        }
+        cur = nxt;
+        chunk_of(k + 2, nxt);
+    }
+    const int width = G * CPL;
+    const int nwb = blockDim.x >> 5, wib = threadIdx.x >> 5;
+#pragma unroll
+    for (int e = 0; e < CPL; ++e)
+        for (int o = 16; o >= G; o >>= 1) pd[e] += __shfl_xor_sync(0xffffffffu, pd[e], o);
+    if (lane < G) {
+#pragma unroll
+        for (int e = 0; e < CPL; ++e) sm[wib * width + xoff + e] = pd[e];
+    }
+    __syncthreads();
+    if (threadIdx.x < N) {
+        double tt = 0.0;
+        for (int k = 0; k < nwb; ++k) tt += sm[k * width + threadIdx.x];
+        s.part0[size_t(blockIdx.x) * N + threadIdx.x] = tt;
     }
     k1_epilogue(sm, N, cc, s);
 }
@@ -867,7 +1054,11 @@ __global__ void __launch_bounds__(kThreads, 3) k_trueres(int ni, Cols cc, const 
     for (int q = 0; q < CPL; ++q) tt[q] = tz[q] = 0.0;
     // gather only the column pairs (FULL) / lane columns that have a flagged column: usually a few of N
     unsigned need = 0;
-    if constexpr (FULL != 0) {
+    if constexpr (FULL == 3) {
+#pragma unroll
+        for (int q = 0; q < CPL; ++q)
+            if (s.check[lay_col<G, 3>(l, q)]) need |= 1u << (q >> 2);
+    } else if constexpr (FULL != 0) {
 #pragma unroll
         for (int q = 0; q < CPL; q += 2) {
             const int c = full_col<G>(l, q);
@@ -892,7 +1083,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_trueres(int ni, Cols cc, const 
         if (valid && (!SPLIT || l == 0) && (FULL || c0 < N)) {
 #pragma unroll
             for (int q = 0; q < CPL; ++q) {
-                const int c = FULL ? full_col<G>(l, q) : c0 + q;
+                const int c = FULL ? lay_col<G, FULL>(l, q) : c0 + q;
                 if (c < N && s.check[c]) {
                     // X still holds x_k (K4 applies x += alpha p): A x_{k+1} = A x_k + alpha Ap
                     const double ax = SHIFT ? fma(s.sigma[c], accB[q], acc[q]) : acc[q];
@@ -910,7 +1101,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_trueres(int ni, Cols cc, const 
     const int gid = threadIdx.x / G;
     for (int pass = 0; pass < 2; ++pass) {
 #pragma unroll
-        for (int q = 0; q < CPL; ++q) sm[gid * width + (FULL ? full_col<G>(l, q) : l * CPL + q)] = pass ? tz[q] : tt[q];
+        for (int q = 0; q < CPL; ++q) sm[gid * width + (FULL ? lay_col<G, FULL>(l, q) : l * CPL + q)] = pass ? tz[q] : tt[q];
         __syncthreads();
         if (threadIdx.x < N) {
             double t = 0.0;
@@ -1030,8 +1221,11 @@ Plan plan_for(int N) {
     // measured on B200 at N = 16 (cfg2): 8 lanes x 2 columns at <= 64 registers (32 warps/SM) beats
     // 4 lanes x 4 columns (0.306 vs 0.368 ms per SpMM): the kernel is gather-latency bound, so
     // warps in flight matter more than loads per warp. KSB_SPMM_PLAN=4 selects the wide variant.
+    // Later measurement: 4 lanes x 4 columns in the quad layout (one 256-bit load per gathered row per lane, a
+    // warp covers 8 rows per gather and the (col, val) shuffles feed 8 rows instead of 4) -- see iteration().
+    // KSB_SPMM_PLAN=8 selects 8 lanes x 2 columns, =4 the pair-layout 4 x 4.
     static const char* env = std::getenv("KSB_SPMM_PLAN");
-    if (N == 16 && !(env && env[0] == '4')) return {8, 2, false};
+    if (N == 16 && env && env[0] == '8') return {8, 2, false};
     if (N == 1) return {8, 1, true};
     if (N <= 4) return {2, 2, false};
     if (N <= 8) return {2, 4, false};
@@ -1043,6 +1237,7 @@ Plan plan_for(int N) {
 
 struct SellOps {
     const double *A = nullptr, *B = nullptr;  // SELL-32 values (N <= 2)
+    const double* T8 = nullptr;               // T8 values (N = 16, no shift, rows of <= 16 entries)
 };
 
 template <int NC, bool SHIFT>
@@ -1101,10 +1296,35 @@ void launch_iteration(Ctx& c, const Level& L, const CgWork& w, const Cols& cc, c
                        (const int32_t*)L.ii_col.p, A, Bv, (const double*)w.P, w.AP, w.dev, 0);
             }
         };
-        if (FULL && minb == 4)
+        // streamed gather pipeline (quad layout, N = 4G); KSB_SPMM_STREAM=0 selects k_spmm_dot
+        static const char* st = std::getenv("KSB_SPMM_STREAM");
+        bool streamed = false;
+        static const char* t8e = std::getenv("KSB_SPMM_T8");
+        if constexpr (FULL == 3 && !SHIFT && CPL == 4 && G == 4) {
+            if (so.T8 && cc.N == 16 && !(t8e && t8e[0] == '0')) {
+                auto kern = k_spmm_t8<8>;
+                grid_s = std::min(grid_s, resident_grid(c, kern, kThreads, sm_s));
+                launch(c, "spmm", kern, grid_s, kThreads, sm_s, L.ni, cc, (const int32_t*)L.t8_col.p, so.T8,
+                       (const double*)w.P, w.AP, w.dev);
+                streamed = true;
+            }
+        }
+        if constexpr (FULL == 3 && !SHIFT && CPL == 4 && G <= 8) {
+            if (!streamed && !(st && st[0] == '0') && L.max_row_ii <= RowChunk<G, false>::NB * G) {
+                auto kern = (G == 4 && minb != 3) ? k_spmm_stream<G, 8, 2> : k_spmm_stream<G, 4, 3>;
+                grid_s = std::min(grid_s, resident_grid(c, kern, kThreads, sm_s));
+                launch(c, "spmm", kern, grid_s, kThreads, sm_s, L.ni, cc, (const int32_t*)L.ii_ptr.p,
+                       (const int32_t*)L.ii_col.p, A, (const double*)w.P, w.AP, w.dev);
+                streamed = true;
+            }
+        }
+        if (streamed) {
+        } else if (FULL && minb == 4)
             go(k_spmm_dot<G, CPL, SHIFT, SPLIT, FULL, 4>);
         else if (FULL && minb == 5)
             go(k_spmm_dot<G, CPL, SHIFT, SPLIT, FULL, 5>);
+        else if (FULL == 3 && minb == 3)
+            go(k_spmm_dot<G, CPL, SHIFT, SPLIT, FULL, 3>);
         else if (FULL && minb == 2)
             go(k_spmm_dot<G, CPL, SHIFT, SPLIT, FULL, 2>);
         else
@@ -1134,6 +1354,11 @@ void iteration(Ctx& c, const Level& L, const CgWork& w, const Cols& cc, const do
     // partial blocks (N < G*CPL) keep the interleaved layout with a pair tail mask when the leading dimension
     // is even (the pair straddling an odd N then ends inside the row)
     const bool tail = !p.split && !full && p.CPL == 4 && p.G >= 4 && cc.ld % 2 == 0;
+    // quad layout (256-bit gathers): every slot in range, rows 32-byte aligned (all internal blocks are; X is the
+    // caller's block, read by the true-residual pass)
+    static const char* env = std::getenv("KSB_SPMM_PLAN");
+    const bool quad = full && p.CPL == 4 && cc.ld % 4 == 0 && (reinterpret_cast<uintptr_t>(X) & 31) == 0 &&
+                      !(env && (env[0] == '4' || env[0] == '8'));
     if (p.split)
         launch_iteration<8, 1, SHIFT, true, 0>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e, so);
     else if (p.G == 2 && p.CPL == 2)
@@ -1142,6 +1367,14 @@ void iteration(Ctx& c, const Level& L, const CgWork& w, const Cols& cc, const do
         launch_iteration<2, 4, SHIFT, false, 0>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e, so);
     else if (p.G == 8 && p.CPL == 2 && full)
         launch_iteration<8, 2, SHIFT, false, 1>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e, so);
+    else if (p.G == 4 && quad)
+        launch_iteration<4, 4, SHIFT, false, 3>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e, so);
+    else if (p.G == 8 && quad)
+        launch_iteration<8, 4, SHIFT, false, 3>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e, so);
+    else if (p.G == 16 && quad)
+        launch_iteration<16, 4, SHIFT, false, 3>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e, so);
+    else if (p.G == 32 && quad)
+        launch_iteration<32, 4, SHIFT, false, 3>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e, so);
     else if (p.G == 4 && full)
         launch_iteration<4, 4, SHIFT, false, 1>(c, L, w, cc, A, Bv, Bb, X, grid_s, grid_e, so);
     else if (p.G == 4 && tail)
@@ -1253,6 +1486,7 @@ void cg_solve(Ctx& c, Level& L, int mat, int shift_mat, const double* h_sigma, c
         so.A = L.sell_values(mat);
         so.B = shift ? L.sell_values(shift_mat) : nullptr;
     }
+    if (N == 16 && !shift) so.T8 = L.t8_values(mat);
     const int total = cc.fixed ? o.fixed_iterations : o.max_iterations;
     const int every = std::max(1, o.check_every);
     auto run_chunk = [&](int chunk) {
@@ -1271,8 +1505,8 @@ void cg_solve(Ctx& c, Level& L, int mat, int shift_mat, const double* h_sigma, c
     auto graph_for = [&](int chunk) -> CgGraph& {
         CgGraphKey key;
         std::memset(&key, 0, sizeof key);
-        const void* ptrs[16] = {&L, A, Bv, d_B, d_X, so.A, so.B, w.R, w.P, w.AP, w.scal.p, w.parts.p, w.ints.p,
-                                d.diagA, d.diagB, L.ii_col.p};
+        const void* ptrs[17] = {&L, A, Bv, d_B, d_X, so.A, so.B, w.R, w.P, w.AP, w.scal.p, w.parts.p, w.ints.p,
+                                d.diagA, d.diagB, L.ii_col.p, so.T8};
         std::memcpy(key.ptrs, ptrs, sizeof ptrs);
         const int ints[8] = {mat, shift_mat, N, ld, chunk, grid_s, grid_e, cc.fixed};
         std::memcpy(key.ints, ints, sizeof ints);

@@ -29,7 +29,7 @@ struct CgDev {
 
 /// identity of a captured chunk of CG iterations: every kernel argument that can differ between solves
 struct CgGraphKey {
-    const void* ptrs[16];
+    const void* ptrs[17];
     int ints[8];
     double tol;
 };

@@ -1,4 +1,6 @@
 // Upload of one level's host index data (host/topology.hpp) into a device Level.
+#include <algorithm>
+
 #include "level.cuh"
 
 namespace ksb {
@@ -49,7 +51,11 @@ void upload_level(Ctx& cx, std::shared_ptr<FineTopology> topo, Level& L) {
     L.sell_ptr.upload(cx, T.sell_ptr);
     L.sell_col.upload(cx, T.sell_col);
     L.sell_map.upload(cx, T.sell_map);
+    L.t8_col.upload(cx, T.t8_col);
+    L.t8_map.upload(cx, T.t8_map);
     L.nslices = int(T.sell_ptr.size()) - 1;
+    L.max_row_ii = 0;
+    for (size_t i = 0; i + 1 < T.ii.ptr.size(); ++i) L.max_row_ii = std::max(L.max_row_ii, int(T.ii.ptr[i + 1] - T.ii.ptr[i]));
     L.n_prev = T.n_prev;
     if (T.n_prev > 0) {
         L.pstep_col.upload(cx, T.pstep_col);

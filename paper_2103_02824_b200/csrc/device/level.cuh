@@ -35,7 +35,8 @@ struct DevBuf {
 struct Mat {
     DevBuf<double> ii, ib;
     DevBuf<double> sell;         // ii values in the SELL-32 order (lazily converted)
-    uint64_t version = 0, sell_version = ~uint64_t(0);
+    DevBuf<double> t8;           // ii values in the T8 order (lazily converted)
+    uint64_t version = 0, sell_version = ~uint64_t(0), t8_version = ~uint64_t(0);
     bool valid = false;
 };
 
@@ -60,7 +61,9 @@ struct Level {
     DevBuf<int32_t> ctets, ciidx;             // coarse mesh (level 0)
     DevBuf<double> cxyz;
     DevBuf<int32_t> sell_ptr, sell_col, sell_map;
+    DevBuf<int32_t> t8_col, t8_map;  // T8 view (empty when a row is longer than 16)
     int nslices = 0;
+    int max_row_ii = 0;  // longest row of the interior pattern (selects the streamed SpMM when <= 16)
     DevBuf<int32_t> pstep_col, prev_iidx;   // one-step prolongation from level-1 (empty on level 0)
     DevBuf<double> pstep_val;
     int n_prev = 0;
@@ -74,6 +77,8 @@ struct Level {
     Mat& mat(int id);
     /// SELL-32 values of matrix id (converted on first use after its values changed)
     const double* sell_values(int id);
+    /// T8 values of matrix id (converted on first use after its values changed); null without a T8 view
+    const double* t8_values(int id);
     void touch(int id) { ++mats[id].version; }
 };
 

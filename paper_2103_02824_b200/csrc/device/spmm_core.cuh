@@ -50,27 +50,61 @@ __device__ __forceinline__ int full_col(int l, int q) {
 
 /// FULL layout modes: 1 = every slot in range (N == G*CPL); 2 = tail mask (N < G*CPL): a column pair is
 /// skipped when it starts at or beyond N. A pair straddling N (odd N) touches column N, which lies inside the
-/// even leading dimension and is never consumed.
+/// even leading dimension and is never consumed. 3 = quad layout, every slot in range: lane l owns the
+/// 32-byte column quads l, l+G, ... and reads each with one 256-bit load (sm_100 LDG.256), so a group of
+/// G = 4 lanes reads a 128-byte row in one instruction and a warp covers 8 rows per gather.
 __device__ __forceinline__ bool pair_ok(int FULLMODE, int c, int N) { return FULLMODE != 2 || c < N; }
+
+/// Column of slot q of lane l for FULL mode FM (see full_col / the quad layout above)
+template <int G, int FM>
+__device__ __forceinline__ int lay_col(int l, int q) {
+    if constexpr (FM == 3)
+        return 4 * ((q >> 2) * G + l) + (q & 3);
+    else
+        return full_col<G>(l, q);
+}
+
+/// 256-bit read-only load of 4 doubles (p 32-byte aligned)
+__device__ __forceinline__ void ldg4(const double* p, double& a, double& b, double& c, double& d) {
+    asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(a), "=d"(b), "=d"(c), "=d"(d)
+                 : "l"(p));
+}
+
+/// 256-bit store of 4 doubles (p 32-byte aligned)
+__device__ __forceinline__ void stg4(double* p, double a, double b, double c, double d) {
+    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
 
 /// p points at the row start; loads lane l's CPL columns in the FULL layout
 template <int G, int CPL, int FM = 1>
 __device__ __forceinline__ void load_full(const double* __restrict__ p, int l, int N, double (&x)[CPL]) {
+    if constexpr (FM == 3) {
+        static_assert(CPL % 4 == 0, "quad layout needs CPL % 4 == 0");
 #pragma unroll
-    for (int k = 0; k < CPL; k += 2) {
-        double2 a = make_double2(0.0, 0.0);
-        if (pair_ok(FM, full_col<G>(l, k), N)) a = __ldg(reinterpret_cast<const double2*>(p + full_col<G>(l, k)));
-        x[k] = a.x;
-        x[k + 1] = a.y;
+        for (int k = 0; k < CPL; k += 4) ldg4(p + lay_col<G, 3>(l, k), x[k], x[k + 1], x[k + 2], x[k + 3]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < CPL; k += 2) {
+            double2 a = make_double2(0.0, 0.0);
+            if (pair_ok(FM, full_col<G>(l, k), N)) a = __ldg(reinterpret_cast<const double2*>(p + full_col<G>(l, k)));
+            x[k] = a.x;
+            x[k + 1] = a.y;
+        }
     }
 }
 
 template <int G, int CPL, int FM = 1>
 __device__ __forceinline__ void store_full(double* __restrict__ p, int l, int N, const double (&y)[CPL]) {
+    if constexpr (FM == 3) {
 #pragma unroll
-    for (int k = 0; k < CPL; k += 2)
-        if (pair_ok(FM, full_col<G>(l, k), N))
-            *reinterpret_cast<double2*>(p + full_col<G>(l, k)) = make_double2(y[k], y[k + 1]);
+        for (int k = 0; k < CPL; k += 4) stg4(p + lay_col<G, 3>(l, k), y[k], y[k + 1], y[k + 2], y[k + 3]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < CPL; k += 2)
+            if (pair_ok(FM, full_col<G>(l, k), N))
+                *reinterpret_cast<double2*>(p + full_col<G>(l, k)) = make_double2(y[k], y[k + 1]);
+    }
 }
 
 template <int CPL>
@@ -135,7 +169,16 @@ __device__ __forceinline__ void row_product(int r, int rb, int re, const int32_t
 #pragma unroll
                 for (int u = 0; u < UB; ++u) {
                     const int j = __shfl_sync(0xffffffffu, mc[b], gbase + s0 + u);
-                    if (FULL) {
+                    if (FULL == 3) {
+                        // need: bit k = quad k is wanted
+#pragma unroll
+                        for (int k = 0; k < CPL; k += 4) {
+                            x[u][k] = x[u][k + 1] = x[u][k + 2] = x[u][k + 3] = 0.0;
+                            if ((need >> (k >> 2)) & 1u)
+                                ldg4(X + size_t(j) * ldx + lay_col<G, 3>(l, k), x[u][k], x[u][k + 1], x[u][k + 2],
+                                     x[u][k + 3]);
+                        }
+                    } else if (FULL) {
                         // need: bit k of a FULL lane = its column pair k is wanted (skipped pairs read nothing)
 #pragma unroll
                         for (int k = 0; k < CPL; k += 2) {
@@ -195,44 +238,44 @@ struct RowChunk {
 };
 
 /// Row product with the first super-chunk already in registers (software-pipelined across row tiles);
-/// further super-chunks (rows longer than 16 entries, adaptive meshes) are loaded in place.
+/// further super-chunks (rows longer than NB*G entries, adaptive meshes) are loaded in place.
+/// The super-chunk's NB*G slots are walked as one flat sequence in batches of UB gathers in flight per lane
+/// (quad layout: 8 x 32 bytes; otherwise 16 doubles' worth).
 template <int G, int CPL, bool SHIFT, int FULL>
 __device__ __forceinline__ void row_product_pf(int r, RowChunk<G, SHIFT>& ch, const int32_t* __restrict__ col,
                                                const double* __restrict__ A, const double* __restrict__ B,
                                                const double* __restrict__ X, int ldx, int c0, int N, int l, int gbase,
                                                double (&acc)[CPL], double (&accB)[CPL]) {
     constexpr int NB = RowChunk<G, SHIFT>::NB;
-    constexpr int UB = (G < 16 / CPL) ? G : 16 / CPL;
+    constexpr int SL = NB * G;
+    constexpr int UB0 = (G < 16 / CPL) ? G : 16 / CPL;
+    constexpr int UB = (FULL == 3) ? (SL < 8 ? SL : 8) : UB0;
 #pragma unroll
     for (int k = 0; k < CPL; ++k) acc[k] = accB[k] = 0.0;
     const int wmax = __reduce_max_sync(0xffffffffu, ch.re - ch.rb);
-    for (int k0 = 0; k0 < wmax; k0 += G * NB) {
-        if (k0 > 0) ch.load(r, ch.rb + G * NB, ch.re, l, col, A, B);  // rare: long rows
+    for (int k0 = 0; k0 < wmax; k0 += SL) {
+        if (k0 > 0) ch.load(r, ch.rb + SL, ch.re, l, col, A, B);  // rare: long rows
 #pragma unroll
-        for (int b = 0; b < NB; ++b) {
-            if (k0 + b * G >= wmax) break;
+        for (int s0 = 0; s0 < SL; s0 += UB) {
+            if (s0 > 0 && k0 + s0 >= wmax) break;
+            double x[UB][CPL];
 #pragma unroll
-            for (int s0 = 0; s0 < G; s0 += UB) {
-                if (s0 > 0 && k0 + b * G + s0 >= wmax) break;
-                double x[UB][CPL];
+            for (int u = 0; u < UB; ++u) {
+                const int j = __shfl_sync(0xffffffffu, ch.mc[(s0 + u) / G], gbase + (s0 + u) % G);
+                if (FULL)
+                    load_full<G, CPL, FULL>(X + size_t(j) * ldx, l, N, x[u]);
+                else
+                    load_cols<CPL>(X + size_t(j) * ldx + c0, c0, N, x[u]);
+            }
 #pragma unroll
-                for (int u = 0; u < UB; ++u) {
-                    const int j = __shfl_sync(0xffffffffu, ch.mc[b], gbase + s0 + u);
-                    if (FULL)
-                        load_full<G, CPL, FULL>(X + size_t(j) * ldx, l, N, x[u]);
-                    else
-                        load_cols<CPL>(X + size_t(j) * ldx + c0, c0, N, x[u]);
-                }
+            for (int u = 0; u < UB; ++u) {
+                const double a = __shfl_sync(0xffffffffu, ch.ma[(s0 + u) / G], gbase + (s0 + u) % G);
+                double bb = 0.0;
+                if (SHIFT) bb = __shfl_sync(0xffffffffu, ch.mb[(s0 + u) / G], gbase + (s0 + u) % G);
 #pragma unroll
-                for (int u = 0; u < UB; ++u) {
-                    const double a = __shfl_sync(0xffffffffu, ch.ma[b], gbase + s0 + u);
-                    double bb = 0.0;
-                    if (SHIFT) bb = __shfl_sync(0xffffffffu, ch.mb[b], gbase + s0 + u);
-#pragma unroll
-                    for (int q = 0; q < CPL; ++q) {
-                        acc[q] = fma(a, x[u][q], acc[q]);
-                        if (SHIFT) accB[q] = fma(bb, x[u][q], accB[q]);
-                    }
+                for (int q = 0; q < CPL; ++q) {
+                    acc[q] = fma(a, x[u][q], acc[q]);
+                    if (SHIFT) accB[q] = fma(bb, x[u][q], accB[q]);
                 }
             }
         }

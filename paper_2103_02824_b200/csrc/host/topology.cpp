@@ -326,6 +326,24 @@ std::shared_ptr<FineTopology> build_topology(const Hierarchy& h, int level) {
         }
     }
 
+    // T8 view of the interior pattern (streamed N = 16 SpMM): built when every row fits 16 slots
+    {
+        int wmax = 0;
+        for (int r = 0; r < ni; ++r) wmax = std::max(wmax, ii.ptr[r + 1] - ii.ptr[r]);
+        if (wmax <= 16 && ni > 0) {
+            check_i32(int64_t(ni) * 16, "T8 entries");
+            topo->t8_col.assign(size_t(ni) * 16, -1);
+            topo->t8_map.assign(size_t(ni) * 16, -1);
+#pragma omp parallel for schedule(static)
+            for (int r = 0; r < ni; ++r) {
+                for (int q = 0; q < ii.ptr[r + 1] - ii.ptr[r]; ++q) {
+                    topo->t8_col[size_t(r) * 16 + q] = ii.col[ii.ptr[r] + q];
+                    topo->t8_map[size_t(r) * 16 + q] = ii.ptr[r] + q;
+                }
+            }
+        }
+    }
+
     // fine tets grouped by coarse ancestor
     topo->ancestor = h.ancestor(level);
     const int nct = h.mesh(0).n_tets();

@@ -76,6 +76,9 @@ struct FineTopology {
     // SELL-32 view of the ii pattern: slice s = rows [32s, 32s+32), entry e of lane i at
     // sell_ptr[s] + 32 e + i; padding entries point at the row itself with map = -1
     std::vector<int32_t> sell_ptr, sell_col, sell_map;
+    // T8 view (only when no interior row is longer than 16): ELL with 16 slots per row, row-major:
+    // t8_col[16 r + q] = column of slot q of row r, t8_map[16 r + q] = its CSR position; padding -1 / -1
+    std::vector<int32_t> t8_col, t8_map;
     // one-step prolongation from level-1 (fem::prolongation_matrix, proj/src/fespace.cpp:35-56): per vertex <= 4
     // (previous-level vertex, weight), ascending vertex, -1 padded; empty on level 0. prev_iidx: the previous
     // level's vertex -> interior index (interior-block inputs).

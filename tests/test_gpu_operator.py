@@ -102,6 +102,25 @@ def test_cg_matches_oracle_jacobi(ctx, N):
         assert st[1].iterations == 0 and st[1].converged and np.all(X[:, 1] == 0.0)
 
 
+@pytest.mark.parametrize("N", [16, 32])
+def test_cg_streamed_spmm_uniform(ctx, N):
+    """Uniform Kuhn levels (rows of <= 15 entries) take the streamed quad-layout SpMM (k_spmm_stream) at
+    N = 16 / 32; same iterations and solution as the oracle's Jacobi PCG, and a plain SpMM against the oracle."""
+    h, orc = hierarchy(n=4, levels=2)
+    lev = h.n_levels - 1
+    L = kb.Level(ctx, h, lev)
+    L.assemble(kb.MAT_USER0, c_s=0.5, c_m=0.5, potential=(kb.POT_GAUSSIAN, GAUSS))
+    op = orc.operator(lev, c_s=0.5, c_m=0.5, potential=(1, GAUSS), precond=1)
+    rng = np.random.default_rng(9)
+    B = rng.standard_normal((L.ni, N))
+    X, st = L.cg_solve_host(kb.MAT_USER0, B, N, opts=L.cg_options(tol=1e-10))
+    Xo, sto = op.pcg(B, tol=1e-10)
+    for j in range(N):
+        assert st[j].converged == sto[j]["converged"]
+        assert abs(st[j].iterations - sto[j]["iterations"]) <= 1
+    assert np.linalg.norm(X - Xo) <= 1e-9 * np.linalg.norm(Xo)
+
+
 def test_cg_breakdown_on_indefinite_operator(ctx):
     """a_op alone is indefinite (bound states): CG stops with breakdown like the reference."""
     h, orc = hierarchy(levels=1)
