@@ -482,7 +482,7 @@ def run_b200(args, world, rank, local):
                        "l2": "inputs larger than L2 (256 MB blocks, 363 MB operator)",
                        "breakdown_columns": breakdown_cols, "setup_s": round(setup_s, 2)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": ncu_traffic("k_spmm_dot"), "kernel": "k_spmm_dot", "bytes_per_launch": bytes_spmm,
+                         "traffic": ncu_traffic("k_spmm_t8"), "kernel": "k_spmm_t8", "bytes_per_launch": bytes_spmm,
                          "avg_launch_ms": spmm_avg, "peak_kind": peak_kind},
             "spmm_hbm_frac": achieved / peak,
             "cg_update_r_avg_ms": upd_ms / max(1, upd_n),

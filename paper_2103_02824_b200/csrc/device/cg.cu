@@ -525,13 +525,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_spmm_t8(int ni, Cols cc, const 
         else
             x[0] = x[1] = x[2] = x[3] = 0.0;
     };
-    EllChunk cur, nxt;
-    chunk_of(0, cur);
-    chunk_of(1, nxt);
+    // two chunk buffers in ping-pong (tile loop unrolled by two), so no chunk is copied between tiles
+    EllChunk ca, cb;
+    chunk_of(0, ca);
+    chunk_of(1, cb);
     double x[D][CPL];
 #pragma unroll
-    for (int q = 0; q < D; ++q) gather(cur, q, x[q]);
-    for (int k = 0; k < ksteps; ++k) {
+    for (int q = 0; q < D; ++q) gather(ca, q, x[q]);
+    auto tile = [&](int k, EllChunk& cur, const EllChunk& nxt) {
         double acc[CPL] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
         for (int q = 0; q < SL; ++q) {
@@ -544,6 +545,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_spmm_t8(int ni, Cols cc, const 
             else
                 gather(nxt, q + D - SL, x[b]);
         }
+        chunk_of(k + 2, cur);
         const int t = tw.t0 + k * tw.step;
         const int r = t * RPW + g;
         if (t < tw.tend && r < ni) {
@@ -553,8 +555,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_spmm_t8(int ni, Cols cc, const 
 #pragma unroll
             for (int e = 0; e < CPL; ++e) pd[e] = fma(p[e], acc[e], pd[e]);
         }
-        cur = nxt;
-        chunk_of(k + 2, nxt);
+    };
+    for (int k = 0; k < ksteps; k += 2) {
+        tile(k, ca, cb);
+        if (k + 1 < ksteps) tile(k + 1, cb, ca);
     }
     const int width = G * CPL;
     const int nwb = blockDim.x >> 5, wib = threadIdx.x >> 5;
