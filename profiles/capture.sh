@@ -13,7 +13,7 @@ echo "bench rc=$?" >> $O/bench_$R.log
 python bench.py --steps 1 --warmup 3 --no-cpu --no-scale > $O/bench_short_$R.log 2>&1 || exit 1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_$R.csv \
     python bench.py --steps 1 --warmup 3 --no-cpu --no-scale > $O/ncu_launch_$R.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:"k_spmm_dot|k_update_r|k_update_px" -c 3 \
+ncu --set full --clock-control none --import-source on -k regex:"k_spmm_t8|k_update_r|k_update_px" -c 3 \
     -o $O/full_$R -f python bench.py --steps 1 --warmup 3 --no-cpu --no-scale > $O/ncu_full_$R.log 2>&1
 echo "ncu rc=$?" >> $O/ncu_full_$R.log
 # cfg1 level-3 correction step: launch list and the inner-sweep kernels
