@@ -116,7 +116,9 @@ void ksb_level_destroy(ksb_level* l);
  * n_coarse_tets, n_coarse_vertices, 0 */
 int ksb_level_sizes(const ksb_level* l, int64_t sizes[10]);
 /* host copies of index data for bit-exactness checks: what 0 ii.ptr 1 ii.col 2 ib.ptr
- * 3 ib.col 4 interior vertex ids 5 P_int cols (ni*4) 6 P_int vals (double ni*4) */
+ * 3 ib.col 4 interior vertex ids 5 P_int cols (ni*4) 6 P_int vals (double ni*4)
+ * 7 T8 view columns (ni*16, ELL with 16 slots per row, padding -1; KSB_INVALID_ARGUMENT when a row of
+ * the interior pattern is longer than 16 and the level has no T8 view) */
 int ksb_level_index(const ksb_level* l, int what, void* h_dst);
 
 /* ---------------- operators (interior blocks stored on the shared pattern) ----------------

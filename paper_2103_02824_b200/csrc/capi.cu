@@ -485,6 +485,10 @@ int ksb_level_index(const ksb_level* l, int what, void* dst) {
             case 4: put(T.space->interior); break;
             case 5: put(T.pint_col); break;
             case 6: put(T.pint_val); break;
+            case 7:
+                if (T.t8_col.empty()) ksb::raise(KSB_INVALID_ARGUMENT, "level has no T8 view (a row is longer than 16)");
+                put(T.t8_col);
+                break;
             default: ksb::raise(KSB_INVALID_ARGUMENT, "unknown index array");
         }
     });

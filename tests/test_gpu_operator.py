@@ -102,12 +102,31 @@ def test_cg_matches_oracle_jacobi(ctx, N):
         assert st[1].iterations == 0 and st[1].converged and np.all(X[:, 1] == 0.0)
 
 
+def test_t8_view_matches_csr(ctx):
+    """The ELL-16 (T8) view of a Kuhn box mesh (<= 15 entries per row) holds every CSR row in order, padded
+    with -1; refined levels with rows longer than 16 have none (and N = 16 solves take the CSR kernels)."""
+    h, _ = hierarchy(n=12, levels=0)
+    L = kb.Level(ctx, h, 0)
+    ptr, col, t8 = L.index("ii_ptr"), L.index("ii_col"), L.index("t8_col").reshape(L.ni, 16)
+    lens = np.diff(ptr)
+    assert lens.max() <= 16
+    for r in range(L.ni):
+        assert np.array_equal(t8[r, :lens[r]], col[ptr[r]:ptr[r + 1]])
+        assert np.all(t8[r, lens[r]:] == -1)
+    ha, _ = hierarchy(adapt=2)
+    La = kb.Level(ctx, ha, ha.n_levels - 1)
+    if np.diff(La.index("ii_ptr")).max() > 16:
+        with pytest.raises(RuntimeError):
+            La.index("t8_col")
+
+
 @pytest.mark.parametrize("N", [16, 32])
 def test_cg_streamed_spmm_uniform(ctx, N):
-    """Uniform Kuhn levels (rows of <= 15 entries) take the streamed quad-layout SpMM (k_spmm_stream) at
-    N = 16 / 32; same iterations and solution as the oracle's Jacobi PCG, and a plain SpMM against the oracle."""
-    h, orc = hierarchy(n=4, levels=2)
-    lev = h.n_levels - 1
+    """Kuhn box meshes (rows of <= 15 entries, like cfg2) take the T8 SpMM (k_spmm_t8) at N = 16 and the
+    streamed quad-layout SpMM (k_spmm_stream) at N = 32; same iterations and solution as the oracle's Jacobi
+    PCG."""
+    h, orc = hierarchy(n=14, levels=0)
+    lev = 0
     L = kb.Level(ctx, h, lev)
     L.assemble(kb.MAT_USER0, c_s=0.5, c_m=0.5, potential=(kb.POT_GAUSSIAN, GAUSS))
     op = orc.operator(lev, c_s=0.5, c_m=0.5, potential=(1, GAUSS), precond=1)
