@@ -1276,7 +1276,7 @@ void launch_iteration(Ctx& c, const Level& L, const CgWork& w, const Cols& cc, c
         static const char* mb = std::getenv("KSB_SPMM_MINB");
         const int minb = mb ? std::atoi(mb) : KSB_SPMM_MINB;
         static const char* senv = std::getenv("KSB_SPMM_SYNC");
-        const int sync_every = G >= 16 ? (senv ? std::atoi(senv) : 8) : 0;
+        const int sync_every = G >= 16 ? (senv ? std::atoi(senv) : 16) : 0;
         auto go = [&](auto kern) {
             grid_s = std::min(grid_s, resident_grid(c, kern, kThreads, sm_s));
             if (sync_every > 0) {

@@ -24,7 +24,7 @@ def cfg1_hierarchy(levels: int = 3, box: float = 10.0, n_coarse: int = 8) -> api
 
 
 def synthetic_start(L: api.Level, ctx: api.Context, mesh: api.Mesh, centers, N: int, zeta: float = 1.7,
-                    lam0: float = -0.6, tol: float = 1e-10):
+                    lam0: float = -0.6, tol: float = 1e-10, ld: int | None = None):
     """(lambdas, Phi, w) on level L: Phi[:, i] = exp(-zeta r_i) for center i mod len(centers), times a
     seeded low-order polynomial for i >= len(centers) so the columns are independent; unit L2 norm."""
     xyz = mesh.array("xyz")
@@ -32,7 +32,8 @@ def synthetic_start(L: api.Level, ctx: api.Context, mesh: api.Mesh, centers, N: 
     x = xyz[it]
     cen = np.asarray(centers, np.float64).reshape(-1, 3)
     rng = np.random.default_rng(20210304)
-    ld = N if N == 1 else N + (N & 1)
+    if ld is None:
+        ld = N if N == 1 else N + (N & 1)
     Phi = np.zeros((len(it), ld))
     for i in range(N):
         c = cen[i % len(cen)]

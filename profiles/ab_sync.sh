@@ -1,0 +1,12 @@
+#!/bin/bash
+# A/B of the wide (N = 120) SpMM on the cfg5-like scale step (GPU box): "SYNC LD" pairs, e.g. "8 120" "8 128".
+for v in "$@"; do
+  set -- $v
+  echo "SYNC=$1 LD=$2"
+  KSB_SPMM_SYNC=$1 python -c "
+import sys; sys.argv=['x']; sys.path.insert(0,'tests')
+import diag_scale as d
+from paper_2103_02824_b200.workloads import sphere_atoms
+d.run('cfg5-like N=120, 2.1M dofs', sphere_atoms(), 120, 30.0, 4, 10, steps=1, profile=True, ld=$2)
+" 2>&1 | grep -E "spmm|cg_update|ms_total|name" | cut -c1-300
+done

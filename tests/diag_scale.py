@@ -13,7 +13,7 @@ import paper_2103_02824_b200 as kb  # noqa: E402
 from paper_2103_02824_b200.workloads import ring_atoms, sphere_atoms, synthetic_start  # noqa: E402
 
 
-def run(name, atoms, N, box, refine, sweeps, steps=2, profile=True):
+def run(name, atoms, N, box, refine, sweeps, steps=2, profile=True, ld=None):
     h = kb.Hierarchy()
     m = kb.Mesh.box([-box] * 3, [box] * 3, 8)
     h.push(m)
@@ -27,7 +27,7 @@ def run(name, atoms, N, box, refine, sweeps, steps=2, profile=True):
     L.level_ops()
     t_ops = time.time() - t
     cen = [a[1:] for a in atoms]
-    lam, Phi, w, ld = synthetic_start(L, ctx, h.meshes[refine], cen, N, zeta=1.0, lam0=-0.5)
+    lam, Phi, w, ld = synthetic_start(L, ctx, h.meshes[refine], cen, N, zeta=1.0, lam0=-0.5, ld=ld)
     lam = np.linspace(-1.5, -0.3, N)
     out = {"name": name, "N": N, "n_interior": L.ni, "ops_s": round(t_ops, 3), "steps": []}
     for s in range(steps):
