@@ -118,7 +118,9 @@ int ksb_level_sizes(const ksb_level* l, int64_t sizes[10]);
 /* host copies of index data for bit-exactness checks: what 0 ii.ptr 1 ii.col 2 ib.ptr
  * 3 ib.col 4 interior vertex ids 5 P_int cols (ni*4) 6 P_int vals (double ni*4)
  * 7 T8 view columns (ni*16, ELL with 16 slots per row, padding -1; KSB_INVALID_ARGUMENT when a row of
- * the interior pattern is longer than 16 and the level has no T8 view) */
+ * the interior pattern is longer than 16 and the level has no T8 view)
+ * 8 locality order perm (ni: natural row of ordered row i) 9 its pattern ptr (ni+1) 10 its columns (nnz_ii);
+ * KSB_INVALID_ARGUMENT on levels without a locality order (those with a T8 view) */
 int ksb_level_index(const ksb_level* l, int what, void* h_dst);
 
 /* ---------------- operators (interior blocks stored on the shared pattern) ----------------

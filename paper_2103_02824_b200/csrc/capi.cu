@@ -489,6 +489,12 @@ int ksb_level_index(const ksb_level* l, int what, void* dst) {
                 if (T.t8_col.empty()) ksb::raise(KSB_INVALID_ARGUMENT, "level has no T8 view (a row is longer than 16)");
                 put(T.t8_col);
                 break;
+            case 8:
+            case 9:
+            case 10:
+                if (T.lo_perm.empty()) ksb::raise(KSB_INVALID_ARGUMENT, "level has no locality order");
+                put(what == 8 ? T.lo_perm : what == 9 ? T.lo_ptr : T.lo_col);
+                break;
             default: ksb::raise(KSB_INVALID_ARGUMENT, "unknown index array");
         }
     });

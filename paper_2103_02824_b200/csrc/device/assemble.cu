@@ -255,6 +255,19 @@ const double* Level::t8_values(int id) {
     return M.t8.p;
 }
 
+const double* Level::lo_values(int id) {
+    Mat& M = mats[id];
+    if (!M.valid) raise(KSB_INVALID_ARGUMENT, "matrix not assembled");
+    if (lo_map.n == 0) return nullptr;
+    if (M.lo_version != M.version) {
+        if (M.lo.n < lo_map.n) M.lo.alloc(lo_map.n);
+        launch(*ctx, "lo_pack", k_sell_pack, grid_for(*ctx, lo_map.n, 256), 256, 0, int64_t(lo_map.n),
+               (const int32_t*)lo_map.p, (const double*)M.ii.p, M.lo.p);
+        M.lo_version = M.version;
+    }
+    return M.lo.p;
+}
+
 Mat& Level::mat(int id) {
     if (id < 0 || id >= kMaxMats) raise(KSB_INVALID_ARGUMENT, "matrix id out of range");
     Mat& m = mats[id];

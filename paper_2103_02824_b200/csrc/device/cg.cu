@@ -258,6 +258,7 @@ __global__ void __launch_bounds__(kThreads) k_init(int ni, Cols cc, const double
 /// a breakdown retires its column, so the host loop can stop once none is active.
 __device__ void k1_epilogue(double* sm, int N, const Cols& cc, CgDev& s) {
     if (!last_block(s.ctl + kTicket1)) return;
+    if (threadIdx.x < 2) s.ctl[8 + threadIdx.x] = 0;  // die-split tickets of the wide SpMM
     fold_partials(s.part0, gridDim.x, N, sm);
     if (threadIdx.x < N) {
         const int c = threadIdx.x;
@@ -303,7 +304,35 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_dot(int ni, Cols cc, co
     // the tile after it are in flight while the current tile's gathers run. The wide FULL path keeps
     // its registers for 16 gathers in flight instead (PF = false).
     constexpr bool PF = !SPLIT;
-    const TileWalk tw((ni + rows_per_warp - 1) / rows_per_warp);
+    TileWalk tw((ni + rows_per_warp - 1) / rows_per_warp);
+    // sync_every bits 16+: die split (cooperative launch). Blocks on the two halves of the SM id range sweep the
+    // two halves of the rows as separate bands (rank within the half from an atomic ticket), so each die's L2
+    // holds one band's stencil window. 1: halves by smid < nsmid / 2, 2: by smid parity.
+    const int die_split = sync_every >> 16;
+    sync_every &= 0xffff;
+    int ksteps = (tw.tend + tw.step - 1) / tw.step;  // the same count for every warp of the grid
+    if (die_split > 0 && sync_every > 0) {
+        __shared__ int s_half, s_rank;
+        if (threadIdx.x == 0) {
+            unsigned smid, nsm;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            asm volatile("mov.u32 %0, %%nsmid;" : "=r"(nsm));
+            const int h = die_split == 1 ? int(smid >= nsm / 2) : int(smid & 1);
+            s_half = h;
+            s_rank = atomicAdd(s.ctl + 8 + h, 1);
+        }
+        cooperative_groups::this_grid().sync();
+        const int cnt0 = *(volatile int*)(s.ctl + 8), cnt1 = *(volatile int*)(s.ctl + 9);
+        const int h = s_half, rank = s_rank;
+        const int nt = tw.tend, wpb = blockDim.x >> 5;
+        const int t_mid = cnt1 == 0 ? nt : cnt0 == 0 ? 0 : int((int64_t(nt) * cnt0) / (cnt0 + cnt1));
+        const int k0 = cnt0 > 0 ? (t_mid + cnt0 * wpb - 1) / (cnt0 * wpb) : 0;
+        const int k1 = cnt1 > 0 ? (nt - t_mid + cnt1 * wpb - 1) / (cnt1 * wpb) : 0;
+        ksteps = max(k0, k1);
+        tw.t0 = (h ? t_mid : 0) + rank * wpb + int(threadIdx.x >> 5);
+        tw.step = (h ? cnt1 : cnt0) * wpb;
+        tw.tend = h ? nt : t_mid;
+    }
     int t = tw.t0;
     RowChunk<G, SHIFT> cur, nxt;
     int nb_rb = 0, nb_re = 0;
@@ -316,11 +345,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_dot(int ni, Cols cc, co
         nb_rb = v1 ? __ldg(ptr + r1) : 0;
         nb_re = v1 ? __ldg(ptr + r1 + 1) : 0;
     }
-    const int ksteps = (tw.tend + tw.step - 1) / tw.step;  // the same count for every warp of the grid
     for (int ks = 0; ks < ksteps; ++ks, t += tw.step) {
         if (sync_every > 0 && ks > 0 && ks % sync_every == 0) cooperative_groups::this_grid().sync();
         const int r = t * rows_per_warp + g;
-        const bool valid = r < ni;
+        const bool valid = r < ni && t < tw.tend;
         double acc[CPL], accB[CPL];
         if constexpr (SPLIT) {
             const int rb = valid ? __ldg(ptr + r) : 0, re = valid ? __ldg(ptr + r + 1) : 0;
@@ -1242,7 +1270,24 @@ Plan plan_for(int N) {
 struct SellOps {
     const double *A = nullptr, *B = nullptr;  // SELL-32 values (N <= 2)
     const double* T8 = nullptr;               // T8 values (N = 16, no shift, rows of <= 16 entries)
+    // CSR pattern the row kernels walk: the level's natural interior pattern, or its locality-ordered copy
+    const int32_t *ptr = nullptr, *col = nullptr;
+    int max_row = 0;
 };
+
+/// dst row i = src row perm[i] (scatter = 0) or dst row perm[i] = src row i (scatter = 1), N columns, stride ld
+__global__ void k_permute_rows(int ni, int N, int ld, const int32_t* __restrict__ perm, const double* __restrict__ src,
+                               double* __restrict__ dst, int scatter) {
+    const int64_t total = int64_t(ni) * N;
+    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < total; k += int64_t(gridDim.x) * blockDim.x) {
+        const int i = int(k / N), c = int(k % N);
+        const int j = perm[i];
+        if (scatter)
+            dst[size_t(j) * ld + c] = src[size_t(i) * ld + c];
+        else
+            dst[size_t(i) * ld + c] = src[size_t(j) * ld + c];
+    }
+}
 
 template <int NC, bool SHIFT>
 void launch_sell(Ctx& c, const Level& L, const CgWork& w, const Cols& cc, const SellOps& so) {
@@ -1276,14 +1321,16 @@ void launch_iteration(Ctx& c, const Level& L, const CgWork& w, const Cols& cc, c
         static const char* mb = std::getenv("KSB_SPMM_MINB");
         const int minb = mb ? std::atoi(mb) : KSB_SPMM_MINB;
         static const char* senv = std::getenv("KSB_SPMM_SYNC");
-        const int sync_every = G >= 16 ? (senv ? std::atoi(senv) : 16) : 0;
+        static const char* denv = std::getenv("KSB_SPMM_DIE");
+        const int die = denv ? std::atoi(denv) : 0;
+        const int sync_every = G >= 16 ? ((senv ? std::atoi(senv) : 16) | (die << 16)) : 0;
         auto go = [&](auto kern) {
             grid_s = std::min(grid_s, resident_grid(c, kern, kThreads, sm_s));
             if (sync_every > 0) {
                 int ni = L.ni;
                 Cols ccv = cc;
-                const int32_t* ptr = L.ii_ptr.p;
-                const int32_t* col = L.ii_col.p;
+                const int32_t* ptr = so.ptr;
+                const int32_t* col = so.col;
                 const double* Pp = w.P;
                 double* APp = w.AP;
                 CgDev dv = w.dev;
@@ -1296,8 +1343,8 @@ void launch_iteration(Ctx& c, const Level& L, const CgWork& w, const Cols& cc, c
                 ++c.launches;
                 if (c.profiling) c.end("spmm", e0);
             } else {
-                launch(c, "spmm", kern, grid_s, kThreads, sm_s, L.ni, cc, (const int32_t*)L.ii_ptr.p,
-                       (const int32_t*)L.ii_col.p, A, Bv, (const double*)w.P, w.AP, w.dev, 0);
+                launch(c, "spmm", kern, grid_s, kThreads, sm_s, L.ni, cc, so.ptr, so.col, A, Bv, (const double*)w.P,
+                       w.AP, w.dev, 0);
             }
         };
         // streamed gather pipeline (quad layout, N = 4G); KSB_SPMM_STREAM=0 selects k_spmm_dot
@@ -1314,11 +1361,11 @@ void launch_iteration(Ctx& c, const Level& L, const CgWork& w, const Cols& cc, c
             }
         }
         if constexpr (FULL == 3 && !SHIFT && CPL == 4 && G <= 8) {
-            if (!streamed && !(st && st[0] == '0') && L.max_row_ii <= RowChunk<G, false>::NB * G) {
+            if (!streamed && !(st && st[0] == '0') && so.max_row <= RowChunk<G, false>::NB * G) {
                 auto kern = (G == 4 && minb != 3) ? k_spmm_stream<G, 8, 2> : k_spmm_stream<G, 4, 3>;
                 grid_s = std::min(grid_s, resident_grid(c, kern, kThreads, sm_s));
-                launch(c, "spmm", kern, grid_s, kThreads, sm_s, L.ni, cc, (const int32_t*)L.ii_ptr.p,
-                       (const int32_t*)L.ii_col.p, A, (const double*)w.P, w.AP, w.dev);
+                launch(c, "spmm", kern, grid_s, kThreads, sm_s, L.ni, cc, so.ptr, so.col, A, (const double*)w.P,
+                       w.AP, w.dev);
                 streamed = true;
             }
         }
@@ -1341,8 +1388,8 @@ void launch_iteration(Ctx& c, const Level& L, const CgWork& w, const Cols& cc, c
     if (!cc.fixed)
         // runs every iteration but only works when a column was flagged; with many columns that is most
         // iterations (N = 120: 40 of 41), so it gets the SpMM's full resident grid (the early exit stays ~2 us)
-        launch(c, "cg_trueres", k_trueres<G, CPL, SHIFT, SPLIT, FULL>, grid_s, kThreads, sm_s, L.ni, cc,
-               (const int32_t*)L.ii_ptr.p, (const int32_t*)L.ii_col.p, A, Bv, Bb, (const double*)X,
+        launch(c, "cg_trueres", k_trueres<G, CPL, SHIFT, SPLIT, FULL>, grid_s, kThreads, sm_s, L.ni, cc, so.ptr,
+               so.col, A, Bv, Bb, (const double*)X,
                (const double*)w.AP, w.R, w.dev);
     if (v2)
         launch(c, "cg_update_px", k_update_px<2>, grid_e, kThreads, 0, L.ni, cc, X, (const double*)w.R, w.P, w.dev);
@@ -1463,16 +1510,36 @@ void cg_solve(Ctx& c, Level& L, int mat, int shift_mat, const double* h_sigma, c
     d.ctl = w.ints.p + 4 * cap;
     d.part0 = w.parts.p;
     d.part1 = w.parts.p + int64_t(w.cap_blocks) * cap;
+    // Multi-column solves on levels with a locality order (refined / adaptive numbering) run on the reordered
+    // pattern: B and X are permuted in and X out once per solve, so the SpMM's gathered rows come from a band of
+    // the block instead of the whole block (N = 120 at 2 M DOFs: the block is ~2 GB and otherwise re-read ~6x
+    // from DRAM per SpMM). KSB_CG_REORDER=0 disables it.
+    static const char* roenv = std::getenv("KSB_CG_REORDER");
+    const bool lo = N >= 4 && L.lo_perm.n == L.ni && L.ni > 0 && !(roenv && roenv[0] == '0');
+    const int32_t* dslot = lo ? L.lo_dslot.p : L.diag_slot.p;
+    const double* A = lo ? L.lo_values(mat) : L.mats[mat].ii.p;
+    const double* Bv = shift ? (lo ? L.lo_values(shift_mat) : L.mats[shift_mat].ii.p) : nullptr;
+    double* X_user = d_X;
+    if (lo) {
+        const int64_t vec = int64_t(L.ni) * ld;
+        if (w.lo_b.n < vec) w.lo_b.alloc(vec);
+        if (w.lo_x.n < vec) w.lo_x.alloc(vec);
+        const int gp = elem_grid(c, L.ni, N);
+        launch(c, "cg_setup", k_permute_rows, gp, kThreads, 0, L.ni, N, ld, (const int32_t*)L.lo_perm.p, d_B,
+               w.lo_b.p, 0);
+        launch(c, "cg_setup", k_permute_rows, gp, kThreads, 0, L.ni, N, ld, (const int32_t*)L.lo_perm.p,
+               (const double*)d_X, w.lo_x.p, 0);
+        d_B = w.lo_b.p;
+        d_X = w.lo_x.p;
+    }
     if (w.diagA.n < L.ni) w.diagA.alloc(L.ni);
     if (w.diagB.n < L.ni) w.diagB.alloc(L.ni);
-    launch(c, "cg_setup", k_diag, elem_grid(c, L.ni, 1), kThreads, 0, L.ni, (const int32_t*)L.diag_slot.p,
-           (const double*)L.mats[mat].ii.p, w.diagA.p);
+    launch(c, "cg_setup", k_diag, elem_grid(c, L.ni, 1), kThreads, 0, L.ni, dslot, A, w.diagA.p);
     d.diagA = w.diagA.p;
     d.diagB = nullptr;
     std::vector<double> sig(N, 0.0);
     if (shift) {
-        launch(c, "cg_setup", k_diag, elem_grid(c, L.ni, 1), kThreads, 0, L.ni, (const int32_t*)L.diag_slot.p,
-               (const double*)L.mats[shift_mat].ii.p, w.diagB.p);
+        launch(c, "cg_setup", k_diag, elem_grid(c, L.ni, 1), kThreads, 0, L.ni, dslot, Bv, w.diagB.p);
         d.diagB = w.diagB.p;
         if (h_sigma) std::copy(h_sigma, h_sigma + N, sig.begin());
     }
@@ -1483,9 +1550,10 @@ void cg_solve(Ctx& c, Level& L, int mat, int shift_mat, const double* h_sigma, c
     const size_t sm_e = sizeof(double) * std::max<size_t>(kThreads, 2 * size_t(N));
     launch(c, "cg_setup", k_init, grid_e, kThreads, sm_e, L.ni, cc, d_B, d_X, w.R, w.P, d);
 
-    const double* A = L.mats[mat].ii.p;
-    const double* Bv = shift ? L.mats[shift_mat].ii.p : nullptr;
     SellOps so;
+    so.ptr = lo ? L.lo_ptr.p : L.ii_ptr.p;
+    so.col = lo ? L.lo_col.p : L.ii_col.p;
+    so.max_row = lo ? L.lo_max_row : L.max_row_ii;
     if (N == 1 || N == 2) {  // thread-per-row SELL wins for narrow blocks; wider blocks use lane groups
         so.A = L.sell_values(mat);
         so.B = shift ? L.sell_values(shift_mat) : nullptr;
@@ -1510,7 +1578,7 @@ void cg_solve(Ctx& c, Level& L, int mat, int shift_mat, const double* h_sigma, c
         CgGraphKey key;
         std::memset(&key, 0, sizeof key);
         const void* ptrs[17] = {&L, A, Bv, d_B, d_X, so.A, so.B, w.R, w.P, w.AP, w.scal.p, w.parts.p, w.ints.p,
-                                d.diagA, d.diagB, L.ii_col.p, so.T8};
+                                d.diagA, d.diagB, so.col, so.T8};
         std::memcpy(key.ptrs, ptrs, sizeof ptrs);
         const int ints[8] = {mat, shift_mat, N, ld, chunk, grid_s, grid_e, cc.fixed};
         std::memcpy(key.ints, ints, sizeof ints);
@@ -1603,6 +1671,9 @@ void cg_solve(Ctx& c, Level& L, int mat, int shift_mat, const double* h_sigma, c
             if (ctl[kNActive] == 0) break;
         }
     }
+    if (lo)
+        launch(c, "cg_setup", k_permute_rows, elem_grid(c, L.ni, N), kThreads, 0, L.ni, N, ld,
+               (const int32_t*)L.lo_perm.p, (const double*)d_X, X_user, 1);
     if (stats) {
         std::vector<int> st(N), it(N);
         std::vector<double> rel(N);

@@ -42,6 +42,7 @@ struct CgGraph {
 
 struct CgWork {
     DevBuf<double> rbuf, pbuf, apbuf, scal, parts, diagA, diagB;
+    DevBuf<double> lo_b, lo_x;  // B and X in the level's locality order (reordered solves)
     DevBuf<int> ints;
     double *R = nullptr, *P = nullptr, *AP = nullptr;
     int64_t cap_vec = 0;

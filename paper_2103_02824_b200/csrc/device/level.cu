@@ -53,6 +53,12 @@ void upload_level(Ctx& cx, std::shared_ptr<FineTopology> topo, Level& L) {
     L.sell_map.upload(cx, T.sell_map);
     L.t8_col.upload(cx, T.t8_col);
     L.t8_map.upload(cx, T.t8_map);
+    L.lo_perm.upload(cx, T.lo_perm);
+    L.lo_ptr.upload(cx, T.lo_ptr);
+    L.lo_col.upload(cx, T.lo_col);
+    L.lo_map.upload(cx, T.lo_map);
+    L.lo_dslot.upload(cx, T.lo_dslot);
+    L.lo_max_row = T.lo_max_row;
     L.nslices = int(T.sell_ptr.size()) - 1;
     L.max_row_ii = 0;
     for (size_t i = 0; i + 1 < T.ii.ptr.size(); ++i) L.max_row_ii = std::max(L.max_row_ii, int(T.ii.ptr[i + 1] - T.ii.ptr[i]));

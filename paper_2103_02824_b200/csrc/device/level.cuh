@@ -36,7 +36,8 @@ struct Mat {
     DevBuf<double> ii, ib;
     DevBuf<double> sell;         // ii values in the SELL-32 order (lazily converted)
     DevBuf<double> t8;           // ii values in the T8 order (lazily converted)
-    uint64_t version = 0, sell_version = ~uint64_t(0), t8_version = ~uint64_t(0);
+    DevBuf<double> lo;           // ii values on the locality-ordered pattern (lazily converted)
+    uint64_t version = 0, sell_version = ~uint64_t(0), t8_version = ~uint64_t(0), lo_version = ~uint64_t(0);
     bool valid = false;
 };
 
@@ -62,6 +63,8 @@ struct Level {
     DevBuf<double> cxyz;
     DevBuf<int32_t> sell_ptr, sell_col, sell_map;
     DevBuf<int32_t> t8_col, t8_map;  // T8 view (empty when a row is longer than 16)
+    DevBuf<int32_t> lo_perm, lo_ptr, lo_col, lo_map, lo_dslot;  // locality-ordered pattern (topology.hpp)
+    int lo_max_row = 0;
     int nslices = 0;
     int max_row_ii = 0;  // longest row of the interior pattern (selects the streamed SpMM when <= 16)
     DevBuf<int32_t> pstep_col, prev_iidx;   // one-step prolongation from level-1 (empty on level 0)
@@ -79,6 +82,9 @@ struct Level {
     const double* sell_values(int id);
     /// T8 values of matrix id (converted on first use after its values changed); null without a T8 view
     const double* t8_values(int id);
+    /// values of matrix id on the locality-ordered pattern (converted on first use after a change); null
+    /// without a locality order
+    const double* lo_values(int id);
     void touch(int id) { ++mats[id].version; }
 };
 

@@ -76,6 +76,37 @@ __device__ __forceinline__ void stg4(double* p, double a, double b, double c, do
     asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
 }
 
+/// L2 eviction-priority policies (wide SpMM: gathered rows evict-last, streamed matrix / output evict-first)
+__device__ __forceinline__ uint64_t l2_policy_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ double2 ldg2_hint(const double* p, uint64_t pol) {
+    double2 a;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;" : "=d"(a.x), "=d"(a.y) : "l"(p), "l"(pol));
+    return a;
+}
+template <typename T>
+__device__ __forceinline__ T ldg_first(const T* p, uint64_t pol);
+template <>
+__device__ __forceinline__ double ldg_first<double>(const double* p, uint64_t pol) {
+    double a;
+    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(a) : "l"(p), "l"(pol));
+    return a;
+}
+template <>
+__device__ __forceinline__ int32_t ldg_first<int32_t>(const int32_t* p, uint64_t pol) {
+    int32_t a;
+    asm volatile("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(a) : "l"(p), "l"(pol));
+    return a;
+}
+
 /// p points at the row start; loads lane l's CPL columns in the FULL layout
 template <int G, int CPL, int FM = 1>
 __device__ __forceinline__ void load_full(const double* __restrict__ p, int l, int N, double (&x)[CPL]) {
@@ -87,7 +118,12 @@ __device__ __forceinline__ void load_full(const double* __restrict__ p, int l, i
 #pragma unroll
         for (int k = 0; k < CPL; k += 2) {
             double2 a = make_double2(0.0, 0.0);
-            if (pair_ok(FM, full_col<G>(l, k), N)) a = __ldg(reinterpret_cast<const double2*>(p + full_col<G>(l, k)));
+            if (pair_ok(FM, full_col<G>(l, k), N)) {
+                if constexpr (G >= 16)
+                    a = ldg2_hint(p + full_col<G>(l, k), l2_policy_last());
+                else
+                    a = __ldg(reinterpret_cast<const double2*>(p + full_col<G>(l, k)));
+            }
             x[k] = a.x;
             x[k + 1] = a.y;
         }
@@ -102,8 +138,12 @@ __device__ __forceinline__ void store_full(double* __restrict__ p, int l, int N,
     } else {
 #pragma unroll
         for (int k = 0; k < CPL; k += 2)
-            if (pair_ok(FM, full_col<G>(l, k), N))
-                *reinterpret_cast<double2*>(p + full_col<G>(l, k)) = make_double2(y[k], y[k + 1]);
+            if (pair_ok(FM, full_col<G>(l, k), N)) {
+                if constexpr (G >= 16)
+                    __stcs(reinterpret_cast<double2*>(p + full_col<G>(l, k)), make_double2(y[k], y[k + 1]));
+                else
+                    *reinterpret_cast<double2*>(p + full_col<G>(l, k)) = make_double2(y[k], y[k + 1]);
+            }
     }
 }
 
@@ -229,9 +269,16 @@ struct RowChunk {
             ma[b] = 0.0;
             mb[b] = 0.0;
             if (k < re) {
-                mc[b] = __ldg(col + k);
-                ma[b] = __ldg(A + k);
-                if (SHIFT) mb[b] = __ldg(B + k);
+                if constexpr (G >= 16) {
+                    const uint64_t pf = l2_policy_first();
+                    mc[b] = ldg_first(col + k, pf);
+                    ma[b] = ldg_first(A + k, pf);
+                    if (SHIFT) mb[b] = ldg_first(B + k, pf);
+                } else {
+                    mc[b] = __ldg(col + k);
+                    ma[b] = __ldg(A + k);
+                    if (SHIFT) mb[b] = __ldg(B + k);
+                }
             }
         }
     }

@@ -344,6 +344,43 @@ std::shared_ptr<FineTopology> build_topology(const Hierarchy& h, int level) {
         }
     }
 
+    // locality order for the multi-column CG (refined / adaptive levels, see topology.hpp)
+    if (topo->t8_col.empty() && ni > 0) {
+        auto& perm = topo->lo_perm;
+        perm.resize(ni);
+        for (int r = 0; r < ni; ++r) perm[r] = r;
+        const double* X = m.xyz.data();
+        std::stable_sort(perm.begin(), perm.end(), [&](int a, int b) {
+            const double* pa = X + 3 * size_t(S.interior[a]);
+            const double* pb = X + 3 * size_t(S.interior[b]);
+            if (pa[2] != pb[2]) return pa[2] < pb[2];
+            if (pa[1] != pb[1]) return pa[1] < pb[1];
+            return pa[0] < pb[0];
+        });
+        std::vector<int32_t> iperm(ni);
+        for (int i = 0; i < ni; ++i) iperm[perm[i]] = i;
+        topo->lo_ptr.assign(size_t(ni) + 1, 0);
+        for (int i = 0; i < ni; ++i) topo->lo_ptr[i + 1] = topo->lo_ptr[i] + (ii.ptr[perm[i] + 1] - ii.ptr[perm[i]]);
+        topo->lo_col.resize(ii.col.size());
+        topo->lo_map.resize(ii.col.size());
+        topo->lo_dslot.assign(ni, -1);
+        int wmax = 0;
+#pragma omp parallel for schedule(static) reduction(max : wmax)
+        for (int i = 0; i < ni; ++i) {
+            const int r = perm[i], b = ii.ptr[r], len = ii.ptr[r + 1] - b;
+            wmax = std::max(wmax, len);
+            std::vector<std::pair<int32_t, int32_t>> e(len);
+            for (int q = 0; q < len; ++q) e[q] = {iperm[ii.col[b + q]], b + q};
+            std::sort(e.begin(), e.end());
+            for (int q = 0; q < len; ++q) {
+                topo->lo_col[topo->lo_ptr[i] + q] = e[q].first;
+                topo->lo_map[topo->lo_ptr[i] + q] = e[q].second;
+                if (e[q].first == i) topo->lo_dslot[i] = topo->lo_ptr[i] + q;
+            }
+        }
+        topo->lo_max_row = wmax;
+    }
+
     // fine tets grouped by coarse ancestor
     topo->ancestor = h.ancestor(level);
     const int nct = h.mesh(0).n_tets();

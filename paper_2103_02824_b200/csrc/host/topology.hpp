@@ -79,6 +79,13 @@ struct FineTopology {
     // T8 view (only when no interior row is longer than 16): ELL with 16 slots per row, row-major:
     // t8_col[16 r + q] = column of slot q of row r, t8_map[16 r + q] = its CSR position; padding -1 / -1
     std::vector<int32_t> t8_col, t8_map;
+    // Locality order for the multi-column CG (only when the T8 view is absent, i.e. refined / adaptive levels,
+    // whose vertex numbering scatters a row's neighbours over the whole index range): interior rows sorted by
+    // vertex (z, y, x). perm[i] = natural row of ordered row i; the ordered pattern (lo_ptr, lo_col, rows and
+    // columns renumbered, columns ascending), lo_map = natural CSR slot of each ordered slot, lo_dslot = diagonal
+    // slot. Empty when not built.
+    std::vector<int32_t> lo_perm, lo_ptr, lo_col, lo_map, lo_dslot;
+    int lo_max_row = 0;
     // one-step prolongation from level-1 (fem::prolongation_matrix, proj/src/fespace.cpp:35-56): per vertex <= 4
     // (previous-level vertex, weight), ascending vertex, -1 padded; empty on level 0. prev_iidx: the previous
     // level's vertex -> interior index (interior-block inputs).

@@ -120,6 +120,36 @@ def test_t8_view_matches_csr(ctx):
             La.index("t8_col")
 
 
+def test_locality_order(ctx):
+    """Refined levels carry a locality order (interior rows by vertex z, y, x) that the multi-column CG runs on:
+    a permutation whose pattern is the natural one renumbered and much narrower than the natural numbering; the
+    reordered solve (N = 8: B, X permuted in and out) matches the oracle's Jacobi PCG."""
+    h, orc = hierarchy(n=4, levels=2, adapt=1)
+    lev = h.n_levels - 1
+    L = kb.Level(ctx, h, lev)
+    perm, lp, lc = L.index("lo_perm"), L.index("lo_ptr"), L.index("lo_col")
+    ptr, col = L.index("ii_ptr"), L.index("ii_col")
+    assert np.array_equal(np.sort(perm), np.arange(L.ni))
+    iperm = np.empty_like(perm)
+    iperm[perm] = np.arange(L.ni)
+    bw_nat, bw_lo = 0, 0
+    for i in range(L.ni):
+        r = perm[i]
+        assert np.array_equal(lc[lp[i]:lp[i + 1]], np.sort(iperm[col[ptr[r]:ptr[r + 1]]]))
+        bw_lo += np.abs(lc[lp[i]:lp[i + 1]] - i).sum()
+        bw_nat += np.abs(col[ptr[r]:ptr[r + 1]] - r).sum()
+    assert bw_lo < 0.5 * bw_nat
+    L.assemble(kb.MAT_USER0, c_s=0.5, c_m=0.5, potential=(kb.POT_GAUSSIAN, GAUSS))
+    op = orc.operator(lev, c_s=0.5, c_m=0.5, potential=(1, GAUSS), precond=1)
+    B = np.random.default_rng(11).standard_normal((L.ni, 8))
+    X, st = L.cg_solve_host(kb.MAT_USER0, B, 8, opts=L.cg_options(tol=1e-10))
+    Xo, sto = op.pcg(B, tol=1e-10)
+    for j in range(8):
+        assert st[j].converged == sto[j]["converged"]
+        assert abs(st[j].iterations - sto[j]["iterations"]) <= 1
+    assert np.linalg.norm(X - Xo) <= 1e-9 * np.linalg.norm(Xo)
+
+
 @pytest.mark.parametrize("N", [16, 32])
 def test_cg_streamed_spmm_uniform(ctx, N):
     """Kuhn box meshes (rows of <= 15 entries, like cfg2) take the T8 SpMM (k_spmm_t8) at N = 16 and the
