@@ -1391,10 +1391,13 @@ void launch_iteration(Ctx& c, const Level& L, const CgWork& w, const Cols& cc, c
         launch(c, "cg_trueres", k_trueres<G, CPL, SHIFT, SPLIT, FULL>, grid_s, kThreads, sm_s, L.ni, cc, so.ptr,
                so.col, A, Bv, Bb, (const double*)X,
                (const double*)w.AP, w.R, w.dev);
+    // the x / p pass streams 5 blocks per row with no reduction: two blocks per SM beat the residual pass's grid
+    // (cfg2: 0.205 vs 0.214 ms; 3 per SM 0.207), whose dot products want more blocks in flight
+    const int grid_px = std::min(grid_e, 2 * c.sm_count);
     if (v2)
-        launch(c, "cg_update_px", k_update_px<2>, grid_e, kThreads, 0, L.ni, cc, X, (const double*)w.R, w.P, w.dev);
+        launch(c, "cg_update_px", k_update_px<2>, grid_px, kThreads, 0, L.ni, cc, X, (const double*)w.R, w.P, w.dev);
     else
-        launch(c, "cg_update_px", k_update_px<1>, grid_e, kThreads, 0, L.ni, cc, X, (const double*)w.R, w.P, w.dev);
+        launch(c, "cg_update_px", k_update_px<1>, grid_px, kThreads, 0, L.ni, cc, X, (const double*)w.R, w.P, w.dev);
 }
 
 template <bool SHIFT>
