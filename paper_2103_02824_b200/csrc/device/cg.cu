@@ -1517,8 +1517,10 @@ void cg_solve(Ctx& c, Level& L, int mat, int shift_mat, const double* h_sigma, c
     // pattern: B and X are permuted in and X out once per solve, so the SpMM's gathered rows come from a band of
     // the block instead of the whole block (N = 120 at 2 M DOFs: the block is ~2 GB and otherwise re-read ~6x
     // from DRAM per SpMM). KSB_CG_REORDER=0 disables it.
-    static const char* roenv = std::getenv("KSB_CG_REORDER");
-    const bool lo = N >= 4 && L.lo_perm.n == L.ni && L.ni > 0 && !(roenv && roenv[0] == '0');
+    // Blocks that fit in L2 anyway (< 48 MB: N = 21 at 250 k DOFs) keep the natural order and skip the permutes.
+    const char* roenv = std::getenv("KSB_CG_REORDER");  // read per solve (tests switch it)
+    const bool lo = N >= 4 && L.lo_perm.n == L.ni && L.ni > 0 && !(roenv && roenv[0] == '0') &&
+                    ((roenv && roenv[0] == '2') || int64_t(L.ni) * ld * 8 > (int64_t(48) << 20));
     const int32_t* dslot = lo ? L.lo_dslot.p : L.diag_slot.p;
     const double* A = lo ? L.lo_values(mat) : L.mats[mat].ii.p;
     const double* Bv = shift ? (lo ? L.lo_values(shift_mat) : L.mats[shift_mat].ii.p) : nullptr;

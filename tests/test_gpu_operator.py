@@ -1,4 +1,6 @@
 """K-ASM / K-SpMM / multi-RHS CG through the C-ABI vs the CPU oracle."""
+import os
+
 import numpy as np
 import pytest
 import scipy.sparse as sp
@@ -142,7 +144,12 @@ def test_locality_order(ctx):
     L.assemble(kb.MAT_USER0, c_s=0.5, c_m=0.5, potential=(kb.POT_GAUSSIAN, GAUSS))
     op = orc.operator(lev, c_s=0.5, c_m=0.5, potential=(1, GAUSS), precond=1)
     B = np.random.default_rng(11).standard_normal((L.ni, 8))
-    X, st = L.cg_solve_host(kb.MAT_USER0, B, 8, opts=L.cg_options(tol=1e-10))
+    # the order is used for blocks above 48 MB; KSB_CG_REORDER=2 forces it on this small one
+    os.environ["KSB_CG_REORDER"] = "2"
+    try:
+        X, st = L.cg_solve_host(kb.MAT_USER0, B, 8, opts=L.cg_options(tol=1e-10))
+    finally:
+        del os.environ["KSB_CG_REORDER"]
     Xo, sto = op.pcg(B, tol=1e-10)
     for j in range(8):
         assert st[j].converged == sto[j]["converged"]
