@@ -113,15 +113,20 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
-def dist_init():
+def dist_init(backend: str | None = None):
+    """One process per GPU (torchrun env). NCCL on GPU boxes; gloo where CUDA is absent (the CPU tests of the
+    replica plumbing, tests/test_replicas.py)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        if backend is None:
+            backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend)
     return world, rank, local
 
 
@@ -136,9 +141,16 @@ def max_over_ranks(x, world):
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def replica_value(units_per_rank: float, ms_local: float, world: int) -> tuple[float, float]:
+    """Whole-job throughput of `world` replicas: all ranks' units over the slowest rank's time (max over ranks)."""
+    ms = max_over_ranks(ms_local, world)
+    return world * units_per_rank / (ms * 1e-3), ms
 
 
 # ----------------------------------------------------------------------------------- CPU legs
@@ -424,8 +436,7 @@ def run_b200(args, world, rank, local):
     barrier(world)
     launches = ctx.launches() - launches0
     ms = ev0.elapsed_time(ev1) / args.steps
-    ms = max_over_ranks(ms, world)
-    value = world * ni * N_RHS * ITERS / (ms * 1e-3)
+    value, ms = replica_value(ni * N_RHS * ITERS, ms, world)
     breakdown_cols = sum(1 for s in stats if s.breakdown)
 
     # dominant kernel: the fused SpMM (Ap = A p + p.Ap partials), timed per launch with events on its stream
