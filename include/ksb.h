@@ -167,7 +167,9 @@ typedef struct {
     int iterations;
     double relative_residual;
     int converged;
-    int breakdown;
+    int breakdown; /* 1 = stopped on !(pAp > 0); fixed-iteration mode (no stopping test): the number of
+                      iterations that saw !(pAp > 0) -- the column keeps iterating, alpha = 0 when pAp is
+                      0 or non-finite */
 } ksb_cg_stats;
 
 int ksb_cg_defaults(ksb_cg_opts* o);

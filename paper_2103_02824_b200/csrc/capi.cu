@@ -16,9 +16,12 @@ struct ksb_mesh {
 struct ksb_hier {
     ksb::Hierarchy h;
 };
+struct ksb_level;
 struct ksb_ctx {
     ksb::Ctx c;
     ksb::CgWork cg;
+    std::vector<ksb_level*> levels;  // live levels created on this context (their owner pointers are cleared
+                                     // when the context goes first)
     ksb::DevBuf<double> io_b, io_x;  // staging for the host-buffer entry points
 };
 struct ksb_level {
@@ -335,6 +338,7 @@ void ksb_ctx_destroy(ksb_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->c.device);
     cudaStreamSynchronize(c->c.stream);
+    for (auto* l : c->levels) l->owner = nullptr;
     for (auto& p : c->c.pending) {
         cudaEventDestroy(p.second.first);
         cudaEventDestroy(p.second.second);
@@ -445,13 +449,18 @@ int ksb_level_create(ksb_ctx* c, const ksb_hier* h, int level, ksb_level** out) 
             delete lv;
             throw;
         }
+        c->levels.push_back(lv);
         *out = lv;
     });
 }
 
 void ksb_level_destroy(ksb_level* l) {
     if (!l) return;
-    cudaDeviceSynchronize();  // the owning context may already be gone; never touch it here
+    cudaDeviceSynchronize();
+    if (ksb_ctx* c = l->owner) {  // null when the context was destroyed first
+        c->cg.forget_level(l->L.uid);  // its captured CG graphs reference this level's arrays
+        c->levels.erase(std::remove(c->levels.begin(), c->levels.end(), l), c->levels.end());
+    }
     delete l;
 }
 

@@ -240,6 +240,7 @@ __global__ void __launch_bounds__(kThreads) k_init(int ni, Cols cc, const double
         s.beta[c] = 0.0;
         s.iters[c] = 0;
         s.check[c] = 0;
+        s.nonpos[c] = 0;
         s.relres[c] = 0.0;
         s.status[c] = (bn == 0.0) ? kConverged : kActive;
     }
@@ -265,9 +266,16 @@ __device__ void k1_epilogue(double* sm, int N, const Cols& cc, CgDev& s) {
         const double pap = sm[c];
         double al = 0.0;
         if (s.status[c] == kActive) {
-            if (!cc.fixed && !(pap > 0.0)) {
-                s.status[c] = kBreakdown;
-                s.relres[c] = sqrt(s.rr[c]) / s.bnorm[c];
+            if (!(pap > 0.0)) {
+                if (!cc.fixed) {
+                    s.status[c] = kBreakdown;
+                    s.relres[c] = sqrt(s.rr[c]) / s.bnorm[c];
+                } else {
+                    // benchmark mode keeps iterating on an indefinite operator: record the event, and never
+                    // let a zero / non-finite curvature poison the column with inf / NaN
+                    s.nonpos[c] += 1;
+                    if (pap != 0.0 && isfinite(pap)) al = s.rz[c] / pap;
+                }
             } else {
                 al = s.rz[c] / pap;
             }
@@ -714,7 +722,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_sell_dot(int ni, int nslices, C
 // row) in every phase, so each thread only touches its own rows between barriers.
 struct CoopState {
     double alpha[2], beta[2], rz[2], rr[2], bnorm[2], relres[2];
-    int status[2], check[2], iters[2];
+    int status[2], check[2], iters[2], nonpos[2];
     int it, nactive, anycheck;
 };
 
@@ -731,6 +739,7 @@ __device__ void coop_load(CoopState& st, const CgDev& s) {
             st.status[c] = s.status[c];
             st.check[c] = s.check[c];
             st.iters[c] = s.iters[c];
+            st.nonpos[c] = s.nonpos[c];
         }
         st.it = s.ctl[kIt];
         st.nactive = s.ctl[kNActive];
@@ -751,6 +760,7 @@ __device__ void coop_store(const CoopState& st, CgDev& s) {
             s.status[c] = st.status[c];
             s.check[c] = st.check[c];
             s.iters[c] = st.iters[c];
+            s.nonpos[c] = st.nonpos[c];
         }
         s.ctl[kIt] = st.it;
         s.ctl[kNActive] = st.nactive;
@@ -865,9 +875,14 @@ __global__ void __launch_bounds__(kThreads) k_cg_coop(int ni, int nsl, Cols cc, 
                 const double pap = fold[c];
                 double al = 0.0;
                 if (st.status[c] == kActive) {
-                    if (!cc.fixed && !(pap > 0.0)) {
-                        st.status[c] = kBreakdown;
-                        st.relres[c] = sqrt(st.rr[c]) / st.bnorm[c];
+                    if (!(pap > 0.0)) {
+                        if (!cc.fixed) {
+                            st.status[c] = kBreakdown;
+                            st.relres[c] = sqrt(st.rr[c]) / st.bnorm[c];
+                        } else {
+                            st.nonpos[c] += 1;
+                            if (pap != 0.0 && isfinite(pap)) al = st.rz[c] / pap;
+                        }
                     } else {
                         al = st.rz[c] / pap;
                     }
@@ -1462,6 +1477,17 @@ CgWork::~CgWork() {
         if (g.exec) cudaGraphExecDestroy(g.exec);
 }
 
+void CgWork::forget_level(uint64_t uid) {
+    for (size_t k = 0; k < graphs.size();) {
+        if (graphs[k].key.level_uid == uid) {
+            if (graphs[k].exec) cudaGraphExecDestroy(graphs[k].exec);
+            graphs.erase(graphs.begin() + k);
+        } else {
+            ++k;
+        }
+    }
+}
+
 void CgWork::ensure(int ni, int N, int ld, int max_blocks) {
     const int64_t vec = int64_t(ni) * ld;
     if (vec > cap_vec) {
@@ -1510,6 +1536,7 @@ void cg_solve(Ctx& c, Level& L, int mat, int shift_mat, const double* h_sigma, c
     d.status = w.ints.p;
     d.check = w.ints.p + cap;
     d.iters = w.ints.p + 2 * cap;
+    d.nonpos = w.ints.p + 3 * cap;
     d.ctl = w.ints.p + 4 * cap;
     d.part0 = w.parts.p;
     d.part1 = w.parts.p + int64_t(w.cap_blocks) * cap;
@@ -1532,8 +1559,7 @@ void cg_solve(Ctx& c, Level& L, int mat, int shift_mat, const double* h_sigma, c
         const int gp = elem_grid(c, L.ni, N);
         launch(c, "cg_setup", k_permute_rows, gp, kThreads, 0, L.ni, N, ld, (const int32_t*)L.lo_perm.p, d_B,
                w.lo_b.p, 0);
-        launch(c, "cg_setup", k_permute_rows, gp, kThreads, 0, L.ni, N, ld, (const int32_t*)L.lo_perm.p,
-               (const double*)d_X, w.lo_x.p, 0);
+        // X is not permuted in: k_init starts every column from x0 = 0 (proj/src/solver.cpp:59)
         d_B = w.lo_b.p;
         d_X = w.lo_x.p;
     }
@@ -1582,10 +1608,13 @@ void cg_solve(Ctx& c, Level& L, int mat, int shift_mat, const double* h_sigma, c
     auto graph_for = [&](int chunk) -> CgGraph& {
         CgGraphKey key;
         std::memset(&key, 0, sizeof key);
-        const void* ptrs[17] = {&L, A, Bv, d_B, d_X, so.A, so.B, w.R, w.P, w.AP, w.scal.p, w.parts.p, w.ints.p,
-                                d.diagA, d.diagB, so.col, so.T8};
+        key.level_uid = L.uid;
+        // every pointer a captured kernel dereferences
+        const void* ptrs[24] = {A, Bv, d_B, d_X, so.A, so.B, w.R, w.P, w.AP, w.scal.p, w.parts.p, w.ints.p,
+                                d.diagA, d.diagB, so.ptr, so.col, so.T8, L.t8_col.p, L.sell_ptr.p, L.sell_col.p,
+                                L.ii_ptr.p, L.ii_col.p, L.lo_ptr.p, L.lo_col.p};
         std::memcpy(key.ptrs, ptrs, sizeof ptrs);
-        const int ints[8] = {mat, shift_mat, N, ld, chunk, grid_s, grid_e, cc.fixed};
+        const int ints[10] = {mat, shift_mat, N, ld, chunk, grid_s, grid_e, cc.fixed, L.ni, L.nslices};
         std::memcpy(key.ints, ints, sizeof ints);
         key.tol = cc.tol;
         for (auto& g : w.graphs)
@@ -1680,9 +1709,10 @@ void cg_solve(Ctx& c, Level& L, int mat, int shift_mat, const double* h_sigma, c
         launch(c, "cg_setup", k_permute_rows, elem_grid(c, L.ni, N), kThreads, 0, L.ni, N, ld,
                (const int32_t*)L.lo_perm.p, (const double*)d_X, X_user, 1);
     if (stats) {
-        std::vector<int> st(N), it(N);
+        std::vector<int> st(N), it(N), np(N);
         std::vector<double> rel(N);
         KSB_CUDA_CHECK(cudaMemcpyAsync(st.data(), d.status, sizeof(int) * N, cudaMemcpyDeviceToHost, c.stream));
+        KSB_CUDA_CHECK(cudaMemcpyAsync(np.data(), d.nonpos, sizeof(int) * N, cudaMemcpyDeviceToHost, c.stream));
         KSB_CUDA_CHECK(cudaMemcpyAsync(it.data(), d.iters, sizeof(int) * N, cudaMemcpyDeviceToHost, c.stream));
         KSB_CUDA_CHECK(cudaMemcpyAsync(rel.data(), d.relres, sizeof(double) * N, cudaMemcpyDeviceToHost, c.stream));
         KSB_CUDA_CHECK(cudaStreamSynchronize(c.stream));
@@ -1690,7 +1720,8 @@ void cg_solve(Ctx& c, Level& L, int mat, int shift_mat, const double* h_sigma, c
             stats[j].iterations = it[j];
             stats[j].relative_residual = rel[j];
             stats[j].converged = st[j] == kConverged;
-            stats[j].breakdown = st[j] == kBreakdown;
+            // fixed-iteration mode: the number of iterations that saw !(p.Ap > 0) (the column kept iterating)
+            stats[j].breakdown = cc.fixed ? np[j] : int(st[j] == kBreakdown);
         }
     }
 }

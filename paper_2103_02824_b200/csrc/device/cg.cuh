@@ -24,13 +24,15 @@ struct CgDev {
     double *bnorm, *rz, *rr, *alpha, *beta, *relres, *sigma;
     const double *diagA, *diagB;
     int *status, *check, *iters, *ctl;
+    int* nonpos;  // fixed-iteration mode: iterations with !(p.Ap > 0) per column (recorded, column not retired)
     double *part0, *part1;
 };
 
 /// identity of a captured chunk of CG iterations: every kernel argument that can differ between solves
 struct CgGraphKey {
-    const void* ptrs[17];
-    int ints[8];
+    uint64_t level_uid;  // Level::uid: never reused, so a graph of a destroyed level can never match
+    const void* ptrs[24];
+    int ints[10];
     double tol;
 };
 
@@ -50,6 +52,8 @@ struct CgWork {
     CgDev dev{};
     std::vector<CgGraph> graphs;  // chunks of iterations captured as CUDA graphs (small FIFO cache)
     void ensure(int ni, int N, int ld, int max_blocks);
+    /// drop the captured graphs of one level (ksb_level_destroy)
+    void forget_level(uint64_t uid);
     ~CgWork();
 };
 

@@ -33,18 +33,38 @@ __global__ void k_add(int64_t n, const double* __restrict__ a, double sa, const 
         y[i] = sa * a[i] + sb * b[i];
 }
 
+/// grid-wide min over the interior diagonal: per-block minima into part[1 + b], the last block to finish folds
+/// them into out[0] (min is exact, so the result does not depend on the order)
 __global__ void k_min_diag(int ni, const int32_t* __restrict__ dslot, const double* __restrict__ vals,
-                           double* __restrict__ out) {
+                           double* __restrict__ part, int* __restrict__ ticket, double* __restrict__ out) {
     __shared__ double red[32];
+    __shared__ bool last;
     double m = INFINITY;
-    for (int r = threadIdx.x; r < ni; r += blockDim.x) m = fmin(m, vals[dslot[r]]);
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < ni; r += gridDim.x * blockDim.x)
+        m = fmin(m, __ldg(vals + __ldg(dslot + r)));
     for (int o = 16; o > 0; o >>= 1) m = fmin(m, __shfl_xor_sync(0xffffffffu, m, o));
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
     __syncthreads();
     if (threadIdx.x == 0) {
         double t = INFINITY;
         for (int w = 0; w < int(blockDim.x >> 5); ++w) t = fmin(t, red[w]);
-        out[0] = ni > 0 ? t : 0.0;
+        part[blockIdx.x] = t;
+        __threadfence();
+        last = atomicAdd(ticket, 1) == int(gridDim.x) - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    double t = INFINITY;
+    for (int b = threadIdx.x; b < int(gridDim.x); b += blockDim.x) t = fmin(t, __ldcg(part + b));
+    for (int o = 16; o > 0; o >>= 1) t = fmin(t, __shfl_xor_sync(0xffffffffu, t, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double u = INFINITY;
+        for (int w = 0; w < int(blockDim.x >> 5); ++w) u = fmin(u, red[w]);
+        out[0] = ni > 0 ? u : 0.0;
+        *ticket = 0;
     }
 }
 
@@ -158,9 +178,13 @@ void level_ops(Level& L, Corrector& K) {
 double min_diagonal(Level& L, int mat, DevBuf<double>& scratch) {
     Ctx& c = *L.ctx;
     if (!L.mats[mat].valid) raise(KSB_INVALID_ARGUMENT, "operator not assembled");
-    need(scratch, 1);
-    launch(c, "elementwise", k_min_diag, 1, 1024, 0, L.ni, (const int32_t*)L.diag_slot.p,
-           (const double*)L.mats[mat].ii.p, scratch.p);
+    const int g = std::max(1, std::min(ceil_div(L.ni, 256), 2 * c.sm_count));
+    need(scratch, 2 + g);
+    // the ticket lives in the scratch block's last slot (zeroed here, reset by the folding block)
+    int* ticket = reinterpret_cast<int*>(scratch.p + 1 + g);
+    KSB_CUDA_CHECK(cudaMemsetAsync(ticket, 0, sizeof(int), c.stream));
+    launch(c, "elementwise", k_min_diag, g, 256, 0, L.ni, (const int32_t*)L.diag_slot.p,
+           (const double*)L.mats[mat].ii.p, scratch.p + 1, ticket, scratch.p);
     double md = 0.0;
     KSB_CUDA_CHECK(cudaMemcpyAsync(&md, scratch.p, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
     KSB_CUDA_CHECK(cudaStreamSynchronize(c.stream));
@@ -221,14 +245,14 @@ void solve_orbitals(Level& L, Corrector& K, CgWork& cg, const StepOptions& o, co
     need(K.Bblk, int64_t(ni) * ld);
     spmm(c, L, L.mats[1].ii.p, nullptr, nullptr, d_Phi, N, ld, K.R0.p, ld);  // M phi (orbitals vanish on the boundary)
     if (K.idx.n < 4 * N + 8) K.idx.alloc(4 * N + 8);
-    DevBuf<double> sc;
-    sc.alloc(N);
+    need(K.colscale, N);
+    double* sc = K.colscale.p;
     std::vector<int> cols(N);
     for (int i = 0; i < N; ++i) cols[i] = i;
     KSB_CUDA_CHECK(cudaMemcpyAsync(K.idx.p, cols.data(), sizeof(int) * N, cudaMemcpyHostToDevice, c.stream));
-    KSB_CUDA_CHECK(cudaMemcpyAsync(sc.p, h_lambda, sizeof(double) * N, cudaMemcpyHostToDevice, c.stream));
+    KSB_CUDA_CHECK(cudaMemcpyAsync(sc, h_lambda, sizeof(double) * N, cudaMemcpyHostToDevice, c.stream));
     launch(c, "elementwise", k_gather_cols, grid_of(c, int64_t(ni) * N), kT, 0, ni, N, (const int*)K.idx.p,
-           (const double*)sc.p, (const double*)K.R0.p, ld, K.Bblk.p, ld);
+           (const double*)sc, (const double*)K.R0.p, ld, K.Bblk.p, ld);
     CgOptions co;
     co.tol = o.tol_linear;
     co.check_every = o.check_every;
@@ -251,13 +275,12 @@ void solve_orbitals(Level& L, Corrector& K, CgWork& cg, const StepOptions& o, co
         need(K.Xc, int64_t(ni) * ldc);
         std::vector<double> scale(nf), sig(nf, sigma);
         for (int j = 0; j < nf; ++j) scale[j] = h_lambda[fail[j]] + sigma;
-        DevBuf<double> dsc;
-        dsc.alloc(nf);
+        double* dsc = K.colscale.p;  // the unshifted solve's scales are consumed (stream order)
         KSB_CUDA_CHECK(cudaMemcpyAsync(K.idx.p, fail.data(), sizeof(int) * nf, cudaMemcpyHostToDevice, c.stream));
-        KSB_CUDA_CHECK(cudaMemcpyAsync(dsc.p, scale.data(), sizeof(double) * nf, cudaMemcpyHostToDevice, c.stream));
+        KSB_CUDA_CHECK(cudaMemcpyAsync(dsc, scale.data(), sizeof(double) * nf, cudaMemcpyHostToDevice, c.stream));
         if (ldc > nf) KSB_CUDA_CHECK(cudaMemsetAsync(K.Bc.p, 0, sizeof(double) * ni * ldc, c.stream));
         launch(c, "elementwise", k_gather_cols, grid_of(c, int64_t(ni) * nf), kT, 0, ni, nf, (const int*)K.idx.p,
-               (const double*)dsc.p, (const double*)K.R0.p, ld, K.Bc.p, ldc);
+               (const double*)dsc, (const double*)K.R0.p, ld, K.Bc.p, ldc);
         std::vector<CgColumnStats> sst(nf);
         cg_solve(c, L, MAT_H, 1, sig.data(), K.Bc.p, K.Xc.p, nf, ldc, co, sst.data(), cg);
         std::vector<int> take(nf), still;

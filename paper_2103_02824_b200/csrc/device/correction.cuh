@@ -51,6 +51,7 @@ struct Corrector {
     // work vectors (full = n, int = ni, blocks = ni x ld)
     DevBuf<double> rho, vxc, pot, rho_t, bcb, wt_full, ell_full, what_full, diff, wtil_int, hrhs;
     DevBuf<double> R0, Bblk, Xblk, Bc, Xc, PhiT;
+    DevBuf<double> colscale;    // per-column right-hand-side scales of the orbital solves
     DevBuf<double> potf, wscr;  // standard MLC: w + v_xc (full), scratch w of expand
     DevBuf<int> idx;
     int ldT = 0;

@@ -1,12 +1,15 @@
 // Upload of one level's host index data (host/topology.hpp) into a device Level.
 #include <algorithm>
+#include <atomic>
 
 #include "level.cuh"
 
 namespace ksb {
 
 void upload_level(Ctx& cx, std::shared_ptr<FineTopology> topo, Level& L) {
+    static std::atomic<uint64_t> next_uid{1};
     L.ctx = &cx;
+    L.uid = next_uid.fetch_add(1);
     L.topo = std::move(topo);
     const auto& T = *L.topo;
     const auto& S = *T.space;

@@ -43,6 +43,7 @@ struct Mat {
 
 struct Level {
     Ctx* ctx = nullptr;
+    uint64_t uid = 0;  // process-unique id (never reused): keys the CG graph cache (cg.cu)
     std::shared_ptr<FineTopology> topo;
     int n = 0, ni = 0, nb = 0, nt = 0;
     int64_t nnz_ii = 0, nnz_ib = 0;

@@ -142,6 +142,17 @@ std::vector<MeshPtr> load_meshes(const std::string& path) {
             if (v < 0 || v >= nv) raise(KSB_IO, path + ": bisection tuple vertex out of range");
         for (int32_t v : m->vparent)
             if (v < 0 || v >= nv) raise(KSB_IO, path + ": vertex parent out of range");
+        for (int32_t v = m->n_parent_vertices; v < int32_t(nv); ++v)
+            if (m->vparent[2 * size_t(v)] >= v || m->vparent[2 * size_t(v) + 1] >= v)
+                raise(KSB_IO, path + ": vertex parent created after its child");
+        if (k == 0) {
+            for (int32_t p : m->parent)
+                if (p < 0 || p >= nt) raise(KSB_IO, path + ": tet parent out of range");
+        } else {
+            const int64_t npt = out.back()->n_tets();
+            for (int32_t p : m->parent)
+                if (p < 0 || p >= npt) raise(KSB_IO, path + ": tet parent out of range of the previous level");
+        }
         for (int8_t t : m->tag)
             if (t < 1 || t > 3) raise(KSB_IO, path + ": bisection tag out of range");
         m->finalize();

@@ -44,6 +44,8 @@ void Hierarchy::push(MeshPtr m) {
         // every row is a convex combination of <= 4 coarse vertices (dyadic, exact)
         for (int v = np; v < nv; ++v) {
             const int a = m->vparent[2 * v], b = m->vparent[2 * v + 1];
+            // parents precede children (also guards loaded dumps against out-of-range or cyclic parents)
+            if (a < 0 || b < 0 || a >= v || b >= v) raise(KSB_HIERARCHY, "vertex parent not created before its child");
             int32_t c[8];
             double w[8];
             int cnt = 0;
@@ -77,7 +79,12 @@ void Hierarchy::push(MeshPtr m) {
             }
         }
         const auto& pa = anc_.back();
-        for (int t = 0; t < m->n_tets(); ++t) anc[t] = pa[m->parent[t]];
+        const int64_t npt = int64_t(pa.size());
+        for (int t = 0; t < m->n_tets(); ++t) {
+            const int32_t p = m->parent[t];
+            if (p < 0 || p >= npt) raise(KSB_HIERARCHY, "tet parent out of range of the previous level");
+            anc[t] = pa[p];
+        }
     }
     meshes_.push_back(std::move(m));
     pcol_.push_back(std::move(col));
