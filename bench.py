@@ -154,20 +154,54 @@ def replica_value(units_per_rank: float, ms_local: float, world: int) -> tuple[f
 
 
 # ----------------------------------------------------------------------------------- CPU legs
-def cpu_leg(iters_sample: int):
-    """Oracle SGS-PCG (reference algorithm) on the same operator; a bounded sample: 16 columns x iters_sample."""
+_CFG2_ORACLE = {}
+
+
+def cfg2_oracle_operator(precond):
+    """The cfg2 operator in the CPU oracle (built once per process; precond 0 = SGS, the reference's
+    proj/src/solver.cpp:50-55, 1 = Jacobi, the device's)"""
     from oracle import OMesh, Oracle
-    t0 = time.time()
-    m = OMesh.box([-BOX] * 3, [BOX] * 3, GRID)
-    orc = Oracle([[1.0, 0, 0, 0]])
-    orc.push(m)
-    op = orc.operator(0, c_s=0.5, c_m=0.5, potential=(1, gaussians()), precond=0)
+    if "orc" not in _CFG2_ORACLE:
+        t0 = time.time()
+        m = OMesh.box([-BOX] * 3, [BOX] * 3, GRID)
+        orc = Oracle([[1.0, 0, 0, 0]])
+        orc.push(m)
+        _CFG2_ORACLE.update(orc=orc, mesh=m, setup_s=time.time() - t0)
+    key = f"op{precond}"
+    if key not in _CFG2_ORACLE:
+        _CFG2_ORACLE[key] = _CFG2_ORACLE["orc"].operator(0, c_s=0.5, c_m=0.5, potential=(1, gaussians()),
+                                                         precond=precond)
+    return _CFG2_ORACLE[key]
+
+
+def cpu_leg(iters_sample: int, precond: int = 0):
+    """Oracle PCG on the same operator; a bounded sample: 16 columns x iters_sample iterations. precond 0 = SGS (the
+    reference's algorithm), 1 = Jacobi (like for like with the device iteration)."""
+    op = cfg2_oracle_operator(precond)
     B = rhs_block(op.ni)
-    setup = time.time() - t0
     t1 = time.perf_counter()
     op.pcg(B, fixed=iters_sample)
     dt = time.perf_counter() - t1
-    return op.ni, dt, setup
+    return op.ni, dt, _CFG2_ORACLE["setup_s"]
+
+
+def parity_gate(X_dev, stats_dev, iters):
+    """The timed cfg2 result against the oracle: the same fixed-count Jacobi PCG (iters iterations, 16 columns) on
+    the host; relative L2 difference of the whole block and of the reported residuals."""
+    op = cfg2_oracle_operator(1)
+    B = rhs_block(op.ni)
+    t = time.perf_counter()
+    Xo, so = op.pcg(B, fixed=iters)
+    dt = time.perf_counter() - t
+    err = float(np.linalg.norm(X_dev - Xo) / np.linalg.norm(Xo))
+    rr = max(abs(s.relative_residual - o["relative_residual"]) / max(o["relative_residual"], 1e-300)
+             for s, o in zip(stats_dev, so))
+    return {"checked": "timed cfg2 block X (200 Jacobi-PCG iterations, 16 columns) vs the oracle's Jacobi PCG",
+            "x_rel_l2": err, "relres_max_rel_diff": float(rr), "tol": PARITY_TOL, "ok": bool(err <= PARITY_TOL),
+            "oracle_s": round(dt, 1)}
+
+
+PARITY_TOL = 1e-6
 
 
 def run_reference(args, world, rank):
@@ -176,11 +210,7 @@ def run_reference(args, world, rank):
     cores = os.cpu_count() or 1
     os.environ.setdefault("OMP_NUM_THREADS", str(cores))
     sample = args.cpu_iters
-    from oracle import OMesh, Oracle
-    m = OMesh.box([-BOX] * 3, [BOX] * 3, GRID)
-    orc = Oracle([[1.0, 0, 0, 0]])
-    orc.push(m)
-    op = orc.operator(0, c_s=0.5, c_m=0.5, potential=(1, gaussians()), precond=0)
+    op = cfg2_oracle_operator(0)
     B = rhs_block(op.ni)
     for _ in range(max(0, args.warmup)):
         op.pcg(B, fixed=1)
@@ -192,14 +222,21 @@ def run_reference(args, world, rank):
     dt = float(np.mean(times))
     value = op.ni * N_RHS * sample / dt
     used = min(cores, N_RHS)
+    # like-for-like: the device's Jacobi iteration in the same oracle (one sample, reported beside the value)
+    _, djac, _ = cpu_leg(sample, precond=1)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 * ITERS / sample,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "cfg2 operator micro-benchmark: 128^3 Kuhn P1, A=1/2K+M_V+0.5M, N=16, 200 CG its",
-                       "n_interior": op.ni, "n_rhs": N_RHS, "iterations": ITERS, "l2": "inputs larger than L2"},
+                       "n_interior": op.ni, "n_rhs": N_RHS, "iterations": ITERS, "l2": "inputs larger than L2",
+                       "step": f"one step = one measured sample of {sample} SGS-PCG iterations on all 16 columns "
+                               f"(ms_per_step is that sample's time; value is per iteration, so it compares with "
+                               f"the device's 200-iteration steps)"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": used, "kind": "port",
                              "sample": f"oracle SGS-PCG (reference algorithm), 16 columns x {sample} iterations per "
                                        f"step, OpenMP over columns"},
+            "cpu_jacobi": {"value": op.ni * N_RHS * sample / djac, "unit": UNIT, "cores": used,
+                           "sample": f"the same oracle with the device's Jacobi preconditioner, 16 x {sample} its"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -437,7 +474,9 @@ def run_b200(args, world, rank, local):
     launches = ctx.launches() - launches0
     ms = ev0.elapsed_time(ev1) / args.steps
     value, ms = replica_value(ni * N_RHS * ITERS, ms, world)
-    breakdown_cols = sum(1 for s in stats if s.breakdown)
+    # fixed-count mode reports, per column, the iterations that saw p.Ap <= 0 (A is indefinite: wells below -0.5)
+    curvature_events = [int(s.breakdown) for s in stats]
+    X_timed = dX.download() if (rank == 0 and not args.no_parity) else None
 
     # dominant kernel: the fused SpMM (Ap = A p + p.Ap partials), timed per launch with events on its stream
     ctx.reset_counters()
@@ -473,7 +512,11 @@ def run_b200(args, world, rank, local):
     cfg1_run = cfg1_run_bench(args, ctx, rank, world)
     scale = None if args.no_scale else scale_bench(args, ctx, stream, world)
 
-    cpu = None
+    parity = None
+    if rank == 0 and not args.no_parity:
+        os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count() or 1))
+        parity = parity_gate(X_timed, stats, ITERS)
+    cpu = cpu_jac = None
     if rank == 0 and world == 1 and not args.no_cpu:
         os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count() or 1))
         cni, cdt, _ = cpu_leg(args.cpu_iters)
@@ -481,6 +524,11 @@ def run_b200(args, world, rank, local):
                "cores": min(os.cpu_count() or 1, N_RHS), "kind": "port",
                "sample": f"oracle SGS-PCG (reference algorithm) on the same operator: 16 columns x {args.cpu_iters} "
                          f"iterations ({cdt:.1f} s), OpenMP over columns"}
+        _, jdt, _ = cpu_leg(args.cpu_iters, precond=1)
+        cpu_jac = {"value": cni * N_RHS * args.cpu_iters / jdt, "unit": UNIT,
+                   "cores": min(os.cpu_count() or 1, N_RHS), "kind": "port",
+                   "sample": f"like for like: the oracle with the device's Jacobi preconditioner, 16 columns x "
+                             f"{args.cpu_iters} iterations ({jdt:.1f} s)"}
 
     if rank == 0:
         line = {
@@ -491,7 +539,7 @@ def run_b200(args, world, rank, local):
                        "n_interior": ni, "nnz_interior": L.nnz_ii, "n_rhs": N_RHS, "iterations": ITERS,
                        "preconditioner": "jacobi", "parallelism": f"replicas{world}",
                        "l2": "inputs larger than L2 (256 MB blocks, 363 MB operator)",
-                       "breakdown_columns": breakdown_cols, "setup_s": round(setup_s, 2)},
+                       "nonpositive_curvature_iterations": curvature_events, "setup_s": round(setup_s, 2)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": ncu_traffic("k_spmm_t8"), "kernel": "k_spmm_t8", "bytes_per_launch": bytes_spmm,
                          "avg_launch_ms": spmm_avg, "peak_kind": peak_kind},
@@ -503,6 +551,12 @@ def run_b200(args, world, rank, local):
             "gpu_launches": launches // max(1, args.steps) * args.steps,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
+            "cpu_baseline_jacobi": cpu_jac,
+            "ratio_basis": "value / cpu_baseline compares a Jacobi-PCG iteration (device) with an SGS-PCG iteration "
+                           "(the reference's algorithm); cpu_baseline_jacobi is the like-for-like iteration; the "
+                           "time-to-solution comparison is correction_step (one outer iteration to tolerance, "
+                           "device Jacobi/MG vs oracle SGS)",
+            "parity": parity,
             "correction_step": correction,
             "cfg1_run": cfg1_run,
             "scale": scale,
@@ -510,6 +564,9 @@ def run_b200(args, world, rank, local):
         print(json.dumps(line), flush=True)
     L.close()
     ctx.close()
+    if parity is not None and not parity["ok"]:
+        print(f"parity gate failed: {parity}", file=sys.stderr)
+        sys.exit(3)
 
 
 def main():
@@ -521,6 +578,7 @@ def main():
     ap.add_argument("--cpu-iters", type=int, default=96, help="CPU oracle sample: iterations per 16-column block")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-scale", action="store_true", help="skip the N = 21 / 120 correction-step section")
+    ap.add_argument("--no-parity", action="store_true", help="skip the oracle check of the timed cfg2 result")
     args = ap.parse_args()
     world, rank, local = dist_init()
     if args.impl == "reference":

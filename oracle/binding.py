@@ -62,6 +62,7 @@ _PROTO = {
     "orc_energy": (I, [P, I, DP, I, DP, DP]),
     "orc_indicators": (I, [P, I, DP, DP, I, DP, DP, DP, DP]),
     "orc_last_scf_rho": (I, [P, DP]),
+    "orc_last_scf_history": (I, [P, DP, IP]),
     "orc_dorfler": (I, [DP, I64, D, D, IP, C.POINTER(C.c_int64)]),
     "orc_norms": (I, [P, I, DP, DP]),
     "orc_prolong_vec": (I, [P, I, I, DP, I, DP]),
@@ -326,6 +327,13 @@ class Oracle:
         it = C.c_int()
         _chk(lib.orc_coarse_scf(self._h, tol, max_it, mixing, tol_eig, dp(lam), dp(orb), dp(w), C.byref(it)))
         return lam, orb, w, it.value
+
+    def last_scf_history(self):
+        """H1 density change per coarse-SCF iteration of the last coarse_scf call, also after it failed"""
+        cap = C.c_int(100000)
+        buf = np.empty(cap.value)
+        _chk(lib.orc_last_scf_history(self._h, dp(buf), C.byref(cap)))
+        return buf[:cap.value].copy()
 
     def last_scf_rho(self):
         """mixed density of the last coarse_scf (ScfResult::rho, proj/src/scf.cpp:73)"""

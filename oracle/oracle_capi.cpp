@@ -63,6 +63,7 @@ struct orc_mesh {
 struct orc_problem {
     Problem p;
     Vec last_scf_rho;
+    std::vector<double> last_scf_hist;
 };
 struct orc_operator {
     std::unique_ptr<Elliptic> E;
@@ -450,12 +451,22 @@ int orc_prolong_vec(orc_problem* p, int from, int to, const double* in, int N, d
 int orc_coarse_scf(orc_problem* p, double tol, int max_it, double mixing, double tol_eig, double* lambdas, double* orb,
                    double* hartree, int* iters) {
     return guard([&] {
-        const auto r = self_consistent_solve(p->p.sys, p->p.hier.spaces.at(0), tol, max_it, mixing, tol_eig);
+        p->last_scf_hist.clear();
+        const auto r = self_consistent_solve(p->p.sys, p->p.hier.spaces.at(0), tol, max_it, mixing, tol_eig,
+                                             &p->last_scf_hist);
         std::memcpy(lambdas, r.lambdas.data(), sizeof(double) * r.lambdas.size());
         pack(r.orbitals, orb);
         std::memcpy(hartree, r.hartree.data(), sizeof(double) * r.hartree.size());
         if (iters) *iters = r.iterations;
         p->last_scf_rho = r.rho;
+    });
+}
+/// H1 density changes of the last orc_coarse_scf, also after it failed (n_out: capacity in, count out)
+int orc_last_scf_history(orc_problem* p, double* hist, int* n_out) {
+    return guard([&] {
+        const int n = std::min<int>(*n_out, int(p->last_scf_hist.size()));
+        std::memcpy(hist, p->last_scf_hist.data(), sizeof(double) * n);
+        *n_out = int(p->last_scf_hist.size());
     });
 }
 /// mixed density of the last orc_coarse_scf (ScfResult::rho, proj/src/scf.cpp:73)

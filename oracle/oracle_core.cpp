@@ -1697,7 +1697,8 @@ LevelOps make_level_ops(const Hier& h, int level, const System& s) {
 }
 
 // proj/src/scf.cpp:22-90 with the dense branch of solve_smallest (proj/src/eigensolve.cpp:321-367)
-ScfResult self_consistent_solve(const System& s, SpaceP V, double tol, int max_it, double mixing, double tol_eig) {
+ScfResult self_consistent_solve(const System& s, SpaceP V, double tol, int max_it, double mixing, double tol_eig,
+                                std::vector<double>* hist_out) {
     const Csc S = assemble_stiffness(*V), M = assemble_mass(*V);
     Potential p;
     p.kind = 0;
@@ -1763,6 +1764,7 @@ ScfResult self_consistent_solve(const System& s, SpaceP V, double tol, int max_i
         for (int i = 0; i < V->n(); ++i) d[i] = rn[i] - res.rho[i];
         const double delta = h1_norm(*V, d);
         res.iterations = it;
+        if (hist_out) hist_out->push_back(delta);
         const double mix = (s.hartree_on || s.xc_on) ? mixing : 1.0;
         for (int i = 0; i < V->n(); ++i) res.rho[i] = (1.0 - mix) * res.rho[i] + mix * rn[i];
         if (s.hartree_on) {

@@ -285,7 +285,9 @@ struct ScfResult {
     Vec hartree, rho;
     int iterations = 0;
 };
-ScfResult self_consistent_solve(const System& s, SpaceP V, double tol, int max_it, double mixing, double tol_eig);
+/// hist_out (optional): the H1 density change of every iteration, also when the cap is hit (proj/src/scf.cpp:70-71)
+ScfResult self_consistent_solve(const System& s, SpaceP V, double tol, int max_it, double mixing, double tol_eig,
+                                std::vector<double>* hist_out = nullptr);
 
 struct StepConfig {
     double tol_linear = 1e-9, tol_inner = 1e-8, score_floor = 1e-8;

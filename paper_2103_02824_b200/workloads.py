@@ -87,3 +87,19 @@ def sphere_atoms(n: int = 60, r: float = 6.7, dmin: float = 2.5, seed: int = 60)
             pts.append(v)
     return [[6.0, *p] for p in pts]
 
+
+
+def h2o_atoms(seed: int = 2103):
+    """BASELINE configs[2] (cfg3): Z=8 at the origin, two Z=1 at 1.8 bohr with 104.5 degrees between them, the frame
+    rotated by a seeded uniform rotation (normalised Gaussian quaternion)."""
+    rng = np.random.default_rng(seed)
+    qv = rng.standard_normal(4)
+    a, b, c, d = qv / np.linalg.norm(qv)
+    rot = np.array([[a * a + b * b - c * c - d * d, 2 * (b * c - a * d), 2 * (b * d + a * c)],
+                    [2 * (b * c + a * d), a * a - b * b + c * c - d * d, 2 * (c * d - a * b)],
+                    [2 * (b * d - a * c), 2 * (c * d + a * b), a * a - b * b - c * c + d * d]])
+    half = np.deg2rad(104.5) / 2
+    h1 = 1.8 * np.array([np.sin(half), np.cos(half), 0.0])
+    h2 = 1.8 * np.array([-np.sin(half), np.cos(half), 0.0])
+    pos = [np.zeros(3), rot @ h1, rot @ h2]
+    return [[8.0, *pos[0]], [1.0, *pos[1]], [1.0, *pos[2]]]
