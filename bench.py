@@ -487,7 +487,14 @@ def run_b200(args, world, rank, local):
     upd_ms, upd_n = ctx.kernel_time("cg_update_r")
     updp_ms, updp_n = ctx.kernel_time("cg_update_px")
     spmm_avg = spmm_ms / max(1, spmm_n)
+    # algorithmic bytes per launch: SURVEY.md 8(d)'s CSR figure (12 nnz + 4 (n_i + 1) + 16 n_i N); the stencil kernel
+    # that runs on this lexicographic Kuhn box streams its own format, 8 D n_i + 16 n_i N (D = 15 diagonals), fewer
     bytes_spmm = 12 * L.nnz_ii + 4 * (ni + 1) + 16 * ni * N_RHS
+    dia = L.index("dia")
+    stencil = dia[0] > 0 and os.environ.get("KSB_SPMM_DIA") != "0"
+    spmm_kernel = "k_spmm_dia_tv" if stencil else "k_spmm_t8"
+    n_diag = 3 + (int(dia[0]) - 1) * int(dia[2]) if stencil else 0
+    bytes_format = 8 * n_diag * ni + 16 * ni * N_RHS if stencil else bytes_spmm
     achieved = bytes_spmm / (spmm_avg * 1e-3) / 1e9
     peak, peak_kind = measured_peak()
 
@@ -541,8 +548,12 @@ def run_b200(args, world, rank, local):
                        "l2": "inputs larger than L2 (256 MB blocks, 363 MB operator)",
                        "nonpositive_curvature_iterations": curvature_events, "setup_s": round(setup_s, 2)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": ncu_traffic("k_spmm_t8"), "kernel": "k_spmm_t8", "bytes_per_launch": bytes_spmm,
-                         "avg_launch_ms": spmm_avg, "peak_kind": peak_kind},
+                         "traffic": ncu_traffic(spmm_kernel), "kernel": spmm_kernel, "bytes_per_launch": bytes_spmm,
+                         "avg_launch_ms": spmm_avg, "peak_kind": peak_kind,
+                         "format_bytes_per_launch": bytes_format,
+                         "format_frac": bytes_format / (spmm_avg * 1e-3) / 1e9 / peak,
+                         "bytes_basis": "achieved uses SURVEY.md 8(d)'s CSR bytes for one A P; format_* the bytes the "
+                                        "stencil (DIA) format itself moves (15 values per row, no column indices)"},
             "spmm_hbm_frac": achieved / peak,
             "cg_update_r_avg_ms": upd_ms / max(1, upd_n),
             "cg_update_px_avg_ms": updp_ms / max(1, updp_n),

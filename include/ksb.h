@@ -120,7 +120,11 @@ int ksb_level_sizes(const ksb_level* l, int64_t sizes[10]);
  * 7 T8 view columns (ni*16, ELL with 16 slots per row, padding -1; KSB_INVALID_ARGUMENT when a row of
  * the interior pattern is longer than 16 and the level has no T8 view)
  * 8 locality order perm (ni: natural row of ordered row i) 9 its pattern ptr (ni+1) 10 its columns (nnz_ii);
- * KSB_INVALID_ARGUMENT on levels without a locality order (those with a T8 view) */
+ * KSB_INVALID_ARGUMENT on levels without a locality order (those with a T8 view)
+ * 11 stencil (DIA) view, 16 int32: {runs, centre run length 3, other run length, 1 if on the locality order,
+ * first offset of each run (centre run first), [15] = n when the rows are an n^3 grid (else 0)}; runs = 0 when
+ * the level has none (the solver's sliding-window
+ * SpMM then does not apply) */
 int ksb_level_index(const ksb_level* l, int what, void* h_dst);
 
 /* ---------------- operators (interior blocks stored on the shared pattern) ----------------

@@ -285,7 +285,8 @@ class Level:
                 "ib_ptr": (2, np.int32, self.ni + 1), "ib_col": (3, np.int32, self.nnz_ib),
                 "interior": (4, np.int32, self.ni), "pint_col": (5, np.int32, self.ni * 4),
                 "pint_val": (6, np.float64, self.ni * 4), "t8_col": (7, np.int32, self.ni * 16), "lo_perm": (8, np.int32, self.ni),
-                "lo_ptr": (9, np.int32, self.ni + 1), "lo_col": (10, np.int32, self.nnz_ii)}[what]
+                "lo_ptr": (9, np.int32, self.ni + 1), "lo_col": (10, np.int32, self.nnz_ii),
+                "dia": (11, np.int32, 16)}[what]
         out = np.empty(spec[2], spec[1])
         check(lib.ksb_level_index(self._h, spec[0], out.ctypes.data_as(C.c_void_p)))
         return out

@@ -504,6 +504,13 @@ int ksb_level_index(const ksb_level* l, int what, void* dst) {
                 if (T.lo_perm.empty()) ksb::raise(KSB_INVALID_ARGUMENT, "level has no locality order");
                 put(what == 8 ? T.lo_perm : what == 9 ? T.lo_ptr : T.lo_col);
                 break;
+            case 11: {  // stencil view: {ng, l0, lr, on_lo, first[0..ng)} (16 int32, ng = 0 without one)
+                int32_t info[16] = {T.dia_ng, T.dia_l0, T.dia_lr, T.dia_lo};
+                for (int q = 0; q < T.dia_ng && q < 9; ++q) info[4 + q] = T.dia_first[q];
+                info[15] = T.dia_n;
+                std::memcpy(dst, info, sizeof info);
+                break;
+            }
             default: ksb::raise(KSB_INVALID_ARGUMENT, "unknown index array");
         }
     });

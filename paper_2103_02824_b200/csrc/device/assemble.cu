@@ -9,6 +9,7 @@
 #include <cmath>
 
 #include "level.cuh"
+#include "dia.cuh"
 
 namespace ksb {
 
@@ -253,6 +254,44 @@ const double* Level::t8_values(int id) {
         M.t8_version = M.version;
     }
     return M.t8.p;
+}
+
+/// CSR rows -> tiled stencil layout (dia.cuh: dia_pos); every slot of a row whose column offset is diagonal d of
+/// the stencil lands in (row, d); diagonals without an entry stay 0
+__global__ void k_dia_pack(int ni, DiaGeom dg, int D, int wg, const int32_t* __restrict__ ptr,
+                           const int32_t* __restrict__ col, const int32_t* __restrict__ map,
+                           const double* __restrict__ csr, double* __restrict__ out) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < ni; r += gridDim.x * blockDim.x) {
+        for (int k = ptr[r]; k < ptr[r + 1]; ++k) {
+            const int o = col[k] - r;
+            int d = -1;
+            for (int e = 0; e < D; ++e)
+                if (dg.off[e] == o) d = e;
+            if (d >= 0)
+                out[wg == kDiaLine ? dia_line_pos(r, d, D, dg.n) : dia_pos(r, d, D, wg)] = csr[map ? map[k] : k];
+        }
+    }
+}
+
+const double* Level::dia_values(int id, int wg) {
+    Mat& M = mats[id];
+    if (!M.valid) raise(KSB_INVALID_ARGUMENT, "matrix not assembled");
+    if (dia_ng == 0) return nullptr;
+    if (M.dia_version != M.version || M.dia_wg != wg) {
+        const DiaGeom dg = dia_geom(*this);
+        if (wg == kDiaLine && dg.n == 0) raise(KSB_INTERNAL, "line-tiled stencil layout on a level without a grid");
+        const int64_t need = wg == kDiaLine ? dia_line_size(dg.n, dg.D) : dia_size(ni, dg.D, wg);
+        if (M.dia.n < need) M.dia.alloc(need);
+        KSB_CUDA_CHECK(cudaMemsetAsync(M.dia.p, 0, sizeof(double) * need, ctx->stream));
+        const int32_t* ptr = dia_lo ? lo_ptr.p : ii_ptr.p;
+        const int32_t* col = dia_lo ? lo_col.p : ii_col.p;
+        const int32_t* map = dia_lo ? lo_map.p : nullptr;
+        launch(*ctx, "dia_pack", k_dia_pack, grid_for(*ctx, ni, 256), 256, 0, ni, dg, dg.D, wg, ptr, col, map,
+               (const double*)M.ii.p, M.dia.p);
+        M.dia_version = M.version;
+        M.dia_wg = wg;
+    }
+    return M.dia.p;
 }
 
 const double* Level::lo_values(int id) {

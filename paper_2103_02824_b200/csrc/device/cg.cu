@@ -17,6 +17,7 @@
 // Per iteration this streams 8 column blocks through HBM outside K1 (K2: r, Ap in, r out;
 // K4: x, p, r in, x, p out) instead of 9 with the textbook x/r and p passes.
 #include <algorithm>
+#include <map>
 #include <cstdlib>
 #include <cstring>
 
@@ -24,6 +25,7 @@
 
 #include "cg.cuh"
 #include "spmm_core.cuh"
+#include "dia.cuh"
 
 namespace ksb {
 
@@ -611,6 +613,490 @@ __global__ void __launch_bounds__(kThreads, 2) k_spmm_t8(int ni, Cols cc, const 
         for (int k = 0; k < nwb; ++k) tt += sm[k * width + threadIdx.x];
         s.part0[size_t(blockIdx.x) * N + threadIdx.x] = tt;
     }
+    k1_epilogue(sm, N, cc, s);
+}
+
+// ---------------- K1 (stencil variant): sliding windows over a uniform-stencil level ----------------
+/// Same contract as k_spmm_dot (AP = A P and the p.Ap partials, alpha in the last block) on a level with a stencil
+/// (DIA) view (dia.cuh). G lanes own one row (lane l: the CPL contiguous columns l*CPL..), a warp carries WG = 32/G
+/// rows per step, each lane group walks S consecutive rows. Run q of the stencil (offsets first[q] .. first[q] +
+/// len - 1) keeps its len - 1 older block rows in registers; a step gathers the one new row per run (NG loads
+/// instead of D), loads the row's D values with 16-byte broadcast loads (the WG groups of the warp read one
+/// contiguous run), and accumulates run by run, offsets ascending inside a run. Row indices are clamped to
+/// [0, ni): an offset that leaves the block has value 0. p.Ap takes P[r] from run 0's window (offset 0).
+template <int NG, int LR, int G, int CPL, int MINB, int PFD>
+__global__ void __launch_bounds__(kThreads, MINB) k_spmm_dia(int ni, Cols cc, DiaGeom dg, const double* __restrict__ dval,
+                                                           const double* __restrict__ P, double* __restrict__ AP,
+                                                           CgDev s) {
+    constexpr int L0 = 3;
+    constexpr int D = L0 + (NG - 1) * LR;
+    constexpr int WG = 32 / G, S = kDiaS, T = WG * S;
+    constexpr int SD = (D * WG + 1) & ~1;
+    constexpr int PAIRS = D / 2;
+    extern __shared__ double sm[];
+    const int N = cc.N, ld = cc.ld;
+    const int lane = threadIdx.x & 31;
+    const int g = lane / G, l = lane % G;
+    const int xoff = CPL * l;
+    const bool act = xoff < N;  // lanes past the block's last column idle (N % CPL == 0)
+    double pd[CPL];
+#pragma unroll
+    for (int e = 0; e < CPL; ++e) pd[e] = 0.0;
+    auto ldx = [&](int row, double (&x)[CPL]) {
+        row = min(max(row, 0), ni - 1);
+        const double* p = P + size_t(row) * ld + xoff;
+        if (!act) {
+#pragma unroll
+            for (int e = 0; e < CPL; ++e) x[e] = 0.0;
+        } else if constexpr (CPL == 4) {
+            ldg4(p, x[0], x[1], x[2], x[3]);
+        } else if constexpr (CPL == 2) {
+            const double2 a = __ldg(reinterpret_cast<const double2*>(p));
+            x[0] = a.x;
+            x[1] = a.y;
+        } else {
+            x[0] = __ldg(p);
+        }
+    };
+    // L2 prefetch PFD steps ahead of the two DRAM streams: the values (one contiguous run per step) and the
+    // stencil's leading block row (offset omax: the first touch of that row in the band sweep); the other runs'
+    // rows were brought in by it and hit L2
+    const int omax = dg.first[NG - 1] + LR - 1;
+    auto prefetch_step = [&](const double* vb, int r0g, int sp) {
+        if constexpr (PFD > 0) {
+            if (lane * 16 < SD)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(vb + size_t(sp) * SD + lane * 16));
+            else if (l == G - 1)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(P + size_t(min(r0g + sp + omax, ni - 1)) * ld));
+        }
+    };
+    const TileWalk tw((ni + T - 1) / T);
+    for (int t = tw.t0; t < tw.tend; t += tw.step) {
+        const int r0 = t * T + g * S;
+        const double* vb = dval + size_t(t) * S * SD;
+        if constexpr (PFD > 0) {
+#pragma unroll
+            for (int sp = 0; sp < PFD; ++sp) prefetch_step(vb, r0, sp);
+        }
+        // carried window: run 0 keeps offsets -1, 0; run q >= 1 keeps first[q] .. first[q] + LR - 2
+        double w0[L0 - 1][CPL];
+        double wr[NG - 1][LR - 1][CPL];
+#pragma unroll
+        for (int j = 0; j < L0 - 1; ++j) ldx(r0 - 1 + j, w0[j]);
+#pragma unroll
+        for (int q = 1; q < NG; ++q)
+#pragma unroll
+            for (int j = 0; j < LR - 1; ++j) ldx(r0 + dg.first[q] + j, wr[q - 1][j]);
+#pragma unroll 2
+        for (int st = 0; st < S; ++st) {
+            const int r = r0 + st;
+            const double* vs = vb + size_t(st) * SD;
+            if (PFD > 0 && st + PFD < S) prefetch_step(vb, r0, st + PFD);
+            double v[D];
+#pragma unroll
+            for (int p = 0; p < PAIRS; ++p) {
+                const double2 a = __ldg(reinterpret_cast<const double2*>(vs + 2 * (p * WG + g)));
+                v[2 * p] = a.x;
+                v[2 * p + 1] = a.y;
+            }
+            if constexpr (D & 1) v[D - 1] = __ldg(vs + 2 * PAIRS * WG + g);
+            double n0[CPL], nr[NG - 1][CPL];
+            ldx(r + 1, n0);
+#pragma unroll
+            for (int q = 1; q < NG; ++q) ldx(r + dg.first[q] + LR - 1, nr[q - 1]);
+            double acc[CPL];
+#pragma unroll
+            for (int e = 0; e < CPL; ++e) {
+                double a = v[0] * w0[0][e];
+                a = fma(v[1], w0[1][e], a);
+                a = fma(v[2], n0[e], a);
+                acc[e] = a;
+            }
+#pragma unroll
+            for (int q = 1; q < NG; ++q) {
+                const int d0 = L0 + (q - 1) * LR;
+#pragma unroll
+                for (int j = 0; j < LR; ++j) {
+#pragma unroll
+                    for (int e = 0; e < CPL; ++e)
+                        acc[e] = fma(v[d0 + j], j < LR - 1 ? wr[q - 1][j][e] : nr[q - 1][e], acc[e]);
+                }
+            }
+            if (r < ni && act) {
+#pragma unroll
+                for (int e = 0; e < CPL; ++e) pd[e] = fma(w0[1][e], acc[e], pd[e]);
+                double* y = AP + size_t(r) * ld + xoff;
+                if constexpr (CPL == 4) {
+                    stg4(y, acc[0], acc[1], acc[2], acc[3]);
+                } else if constexpr (CPL == 2) {
+                    *reinterpret_cast<double2*>(y) = make_double2(acc[0], acc[1]);
+                } else {
+                    y[0] = acc[0];
+                }
+            }
+            // slide every window by one row
+#pragma unroll
+            for (int e = 0; e < CPL; ++e) {
+                w0[0][e] = w0[1][e];
+                w0[1][e] = n0[e];
+            }
+#pragma unroll
+            for (int q = 1; q < NG; ++q) {
+#pragma unroll
+                for (int j = 0; j + 1 < LR - 1; ++j)
+#pragma unroll
+                    for (int e = 0; e < CPL; ++e) wr[q - 1][j][e] = wr[q - 1][j + 1][e];
+#pragma unroll
+                for (int e = 0; e < CPL; ++e) wr[q - 1][LR - 2][e] = nr[q - 1][e];
+            }
+        }
+    }
+    // p.Ap partials: fold the WG row groups of the warp, then the warps of the block (fixed order)
+    const int nwb = blockDim.x >> 5, wib = threadIdx.x >> 5;
+#pragma unroll
+    for (int e = 0; e < CPL; ++e)
+        for (int o = 16; o >= G; o >>= 1) pd[e] += __shfl_xor_sync(0xffffffffu, pd[e], o);
+    if (lane < G && act) {
+#pragma unroll
+        for (int e = 0; e < CPL; ++e) sm[wib * N + xoff + e] = pd[e];
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < N; c += blockDim.x) {
+        double tt = 0.0;
+        for (int k = 0; k < nwb; ++k) tt += sm[k * N + c];
+        s.part0[size_t(blockIdx.x) * N + c] = tt;
+    }
+    __syncthreads();
+    k1_epilogue(sm, N, cc, s);
+}
+
+// bulk async copy helpers (cp.async.bulk + mbarrier completion)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "W%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra W%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+constexpr int kDiaCh = 8;    // steps per value chunk of the staged stencil SpMM
+constexpr int kDiaRing = 3;  // chunks in flight per warp
+
+/// dynamic shared memory of k_spmm_dia_tv: the per-warp value rings, their barriers, the epilogue scratch
+inline size_t dia_tv_smem(int D, int wg, int N) {
+    const size_t ring = size_t(kThreads / 32) * kDiaRing * kDiaCh * size_t(dia_step_stride(D, wg)) * sizeof(double);
+    const size_t bars = size_t(kThreads / 32) * kDiaRing * sizeof(uint64_t);
+    const size_t eps = sizeof(double) * std::max<size_t>(size_t(kThreads / 32) * N, 2 * size_t(N));
+    return ring + bars + eps;
+}
+
+/// k_spmm_dia with the value stream staged in shared memory: lane 0 of each warp keeps kDiaRing chunks of
+/// kDiaCh steps in flight as bulk async copies (the values never occupy registers or LSU slots while in flight, and
+/// their DRAM latency hides behind kDiaRing - 1 chunks of work); a step reads its values with 16-byte broadcast LDS.
+/// The block rows are gathered as in k_spmm_dia. Same accumulation order.
+template <int NG, int LR, int G, int CPL, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_spmm_dia_tv(int ni, Cols cc, DiaGeom dg,
+                                                              const double* __restrict__ dval,
+                                                              const double* __restrict__ P, double* __restrict__ AP,
+                                                              CgDev s) {
+    constexpr int L0 = 3;
+    constexpr int D = L0 + (NG - 1) * LR;
+    constexpr int WG = 32 / G, S = kDiaS, T = WG * S;
+    constexpr int SD = (D * WG + 1) & ~1;
+    constexpr int PAIRS = D / 2;
+    constexpr int CH = kDiaCh, RING = kDiaRing, NCH = S / CH, NWB = kThreads / 32;
+    static_assert(S % CH == 0, "chunking");
+    extern __shared__ __align__(128) double dsm[];
+    double* ring_all = dsm;
+    uint64_t* bars_all = reinterpret_cast<uint64_t*>(dsm + size_t(NWB) * RING * CH * SD);
+    double* sm = reinterpret_cast<double*>(bars_all + NWB * RING);
+    const int N = cc.N, ld = cc.ld;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int g = lane / G, l = lane % G;
+    const int xoff = CPL * l;
+    const bool act = xoff < N;
+    double* ring = ring_all + size_t(wib) * RING * CH * SD;
+    uint64_t* bars = bars_all + wib * RING;
+    double pd[CPL];
+#pragma unroll
+    for (int e = 0; e < CPL; ++e) pd[e] = 0.0;
+    auto ldx = [&](int row, double (&x)[CPL]) {
+        row = min(max(row, 0), ni - 1);
+        const double* p = P + size_t(row) * ld + xoff;
+        if (!act) {
+#pragma unroll
+            for (int e = 0; e < CPL; ++e) x[e] = 0.0;
+        } else if constexpr (CPL == 4) {
+            ldg4(p, x[0], x[1], x[2], x[3]);
+        } else if constexpr (CPL == 2) {
+            const double2 a = __ldg(reinterpret_cast<const double2*>(p));
+            x[0] = a.x;
+            x[1] = a.y;
+        } else {
+            x[0] = __ldg(p);
+        }
+    };
+    const TileWalk tw((ni + T - 1) / T);
+    const int ktiles = tw.t0 < tw.tend ? (tw.tend - tw.t0 + tw.step - 1) / tw.step : 0;
+    const int nchunks = ktiles * NCH;
+    auto fetch = [&](int u) {  // lane 0: chunk u of this warp's stream into slot u % RING
+        if (lane == 0 && u < nchunks) {
+            const int k = u / NCH, c = u % NCH;
+            const size_t t = size_t(tw.t0) + size_t(k) * tw.step;
+            uint64_t* bar = bars + (u % RING);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(bar, CH * SD * sizeof(double));
+            bulk_g2s(ring + size_t(u % RING) * CH * SD, dval + (t * S + size_t(c) * CH) * SD, CH * SD * sizeof(double),
+                     bar);
+        }
+    };
+    if (lane == 0) {
+        for (int i = 0; i < RING; ++i) mbar_init(bars + i, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < RING; ++u) fetch(u);
+    int u = 0;
+    for (int k = 0; k < ktiles; ++k) {
+        const int t = tw.t0 + k * tw.step;
+        const int r0 = t * T + g * S;
+        double w0[L0 - 1][CPL];
+        double wr[NG - 1][LR - 1][CPL];
+#pragma unroll
+        for (int j = 0; j < L0 - 1; ++j) ldx(r0 - 1 + j, w0[j]);
+#pragma unroll
+        for (int q = 1; q < NG; ++q)
+#pragma unroll
+            for (int j = 0; j < LR - 1; ++j) ldx(r0 + dg.first[q] + j, wr[q - 1][j]);
+        for (int c = 0; c < NCH; ++c, ++u) {
+            mbar_wait(bars + (u % RING), (u / RING) & 1);
+            const double* vchunk = ring + size_t(u % RING) * CH * SD;
+#pragma unroll 2
+            for (int sc = 0; sc < CH; ++sc) {
+                const int r = r0 + c * CH + sc;
+                const double* vs = vchunk + sc * SD;
+                double n0[CPL], nr[NG - 1][CPL];
+                ldx(r + 1, n0);
+#pragma unroll
+                for (int q = 1; q < NG; ++q) ldx(r + dg.first[q] + LR - 1, nr[q - 1]);
+                double v[D];
+#pragma unroll
+                for (int p = 0; p < PAIRS; ++p) {
+                    const double2 a = *reinterpret_cast<const double2*>(vs + 2 * (p * WG + g));
+                    v[2 * p] = a.x;
+                    v[2 * p + 1] = a.y;
+                }
+                if constexpr (D & 1) v[D - 1] = vs[2 * PAIRS * WG + g];
+                double acc[CPL];
+#pragma unroll
+                for (int e = 0; e < CPL; ++e) {
+                    double a = v[0] * w0[0][e];
+                    a = fma(v[1], w0[1][e], a);
+                    a = fma(v[2], n0[e], a);
+                    acc[e] = a;
+                }
+#pragma unroll
+                for (int q = 1; q < NG; ++q) {
+                    const int d0 = L0 + (q - 1) * LR;
+#pragma unroll
+                    for (int j = 0; j < LR; ++j) {
+#pragma unroll
+                        for (int e = 0; e < CPL; ++e)
+                            acc[e] = fma(v[d0 + j], j < LR - 1 ? wr[q - 1][j][e] : nr[q - 1][e], acc[e]);
+                    }
+                }
+                if (r < ni && act) {
+#pragma unroll
+                    for (int e = 0; e < CPL; ++e) pd[e] = fma(w0[1][e], acc[e], pd[e]);
+                    double* y = AP + size_t(r) * ld + xoff;
+                    if constexpr (CPL == 4) {
+                        stg4(y, acc[0], acc[1], acc[2], acc[3]);
+                    } else if constexpr (CPL == 2) {
+                        *reinterpret_cast<double2*>(y) = make_double2(acc[0], acc[1]);
+                    } else {
+                        y[0] = acc[0];
+                    }
+                }
+#pragma unroll
+                for (int e = 0; e < CPL; ++e) {
+                    w0[0][e] = w0[1][e];
+                    w0[1][e] = n0[e];
+                }
+#pragma unroll
+                for (int q = 1; q < NG; ++q) {
+#pragma unroll
+                    for (int j = 0; j + 1 < LR - 1; ++j)
+#pragma unroll
+                        for (int e = 0; e < CPL; ++e) wr[q - 1][j][e] = wr[q - 1][j + 1][e];
+#pragma unroll
+                    for (int e = 0; e < CPL; ++e) wr[q - 1][LR - 2][e] = nr[q - 1][e];
+                }
+            }
+            __syncwarp();
+            fetch(u + RING);  // the slot just consumed
+        }
+    }
+    const int nwb = blockDim.x >> 5;
+#pragma unroll
+    for (int e = 0; e < CPL; ++e)
+        for (int o = 16; o >= G; o >>= 1) pd[e] += __shfl_xor_sync(0xffffffffu, pd[e], o);
+    if (lane < G && act) {
+#pragma unroll
+        for (int e = 0; e < CPL; ++e) sm[wib * N + xoff + e] = pd[e];
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < N; c += blockDim.x) {
+        double tt = 0.0;
+        for (int k = 0; k < nwb; ++k) tt += sm[k * N + c];
+        s.part0[size_t(blockIdx.x) * N + c] = tt;
+    }
+    __syncthreads();
+    k1_epilogue(sm, N, cc, s);
+}
+
+__device__ __forceinline__ double2 ldg2_na(const double* p) {  // streamed once: no L1 allocation
+    double2 a;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(a.x), "=d"(a.y) : "l"(p));
+    return a;
+}
+__device__ __forceinline__ double ldg1_na(const double* p) {
+    double a;
+    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(a) : "l"(p));
+    return a;
+}
+
+/// z-marching stencil SpMM (N = 16) on a cubic grid level (dia.cuh line-tiled layout). A block of NW warps owns an
+/// (x, y) tile of 32 x NW rows and marches it through a range of z planes; warp w takes grid line y0 + w, its 4 lane
+/// groups 8 consecutive rows each, sliding the per-run windows along x as in k_spmm_dia. Marching in z keeps the
+/// three planes the tile touches (z - 1, z, z + 1 with a one-row / one-line halo: ~80 KB for NW = 4) in L1, so every
+/// block row comes from L2 about once per tile instead of once per stencil run (7 times for Kuhn); the values stream
+/// past L1 (no allocation). Same accumulation order as k_spmm_dia.
+template <int NG, int LR, int NW, int MINB>
+__global__ void __launch_bounds__(NW * 32, MINB) k_spmm_dia_z(int ni, Cols cc, DiaGeom dg, int nzc,
+                                                            const double* __restrict__ dval,
+                                                            const double* __restrict__ P, double* __restrict__ AP,
+                                                            CgDev s) {
+    constexpr int G = 8, CPL = 2, SX = 8, L0 = 3;
+    constexpr int D = L0 + (NG - 1) * LR;
+    constexpr int SD = (D * 4 + 1) & ~1;
+    constexpr int PAIRS = D / 2;
+    extern __shared__ double sm[];
+    const int N = cc.N, ld = cc.ld;
+    const int n = dg.n, nxt = (n + 31) / 32, nyt = (n + NW - 1) / NW;
+    const int zlen = (n + nzc - 1) / nzc;
+    const int nwork = nxt * nyt * nzc;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int g = lane / G, l = lane % G;
+    const int xoff = CPL * l;
+    double pd[CPL] = {0.0, 0.0};
+    auto ldx = [&](int row, double (&x)[CPL]) {
+        row = min(max(row, 0), ni - 1);
+        const double2 a = __ldg(reinterpret_cast<const double2*>(P + size_t(row) * ld + xoff));
+        x[0] = a.x;
+        x[1] = a.y;
+    };
+    for (int wi = blockIdx.x; wi < nwork; wi += gridDim.x) {
+        const int xt = wi % nxt, yt = (wi / nxt) % nyt, zc = wi / (nxt * nyt);
+        const int y = yt * NW + wib;
+        if (y >= n) continue;
+        const int x0 = xt * 32 + g * SX;
+        const int z0 = zc * zlen, z1 = min(n, z0 + zlen);
+        for (int z = z0; z < z1; ++z) {
+            const int r0 = x0 + n * (y + n * z);
+            const double* vb = dval + ((size_t(z) * n + y) * nxt + xt) * 8 * SD;
+            double w0[L0 - 1][CPL];
+            double wr[NG - 1][LR - 1][CPL];
+#pragma unroll
+            for (int j = 0; j < L0 - 1; ++j) ldx(r0 - 1 + j, w0[j]);
+#pragma unroll
+            for (int q = 1; q < NG; ++q)
+#pragma unroll
+                for (int j = 0; j < LR - 1; ++j) ldx(r0 + dg.first[q] + j, wr[q - 1][j]);
+#pragma unroll 2
+            for (int st = 0; st < SX; ++st) {
+                const int r = r0 + st;
+                const double* vs = vb + st * SD;
+                double v[D];
+#pragma unroll
+                for (int p = 0; p < PAIRS; ++p) {
+                    const double2 a = ldg2_na(vs + 2 * (p * 4 + g));
+                    v[2 * p] = a.x;
+                    v[2 * p + 1] = a.y;
+                }
+                if constexpr (D & 1) v[D - 1] = ldg1_na(vs + 2 * PAIRS * 4 + g);
+                double n0[CPL], nr[NG - 1][CPL];
+                ldx(r + 1, n0);
+#pragma unroll
+                for (int q = 1; q < NG; ++q) ldx(r + dg.first[q] + LR - 1, nr[q - 1]);
+                double acc[CPL];
+#pragma unroll
+                for (int e = 0; e < CPL; ++e) {
+                    double a = v[0] * w0[0][e];
+                    a = fma(v[1], w0[1][e], a);
+                    a = fma(v[2], n0[e], a);
+                    acc[e] = a;
+                }
+#pragma unroll
+                for (int q = 1; q < NG; ++q) {
+                    const int d0 = L0 + (q - 1) * LR;
+#pragma unroll
+                    for (int j = 0; j < LR; ++j) {
+#pragma unroll
+                        for (int e = 0; e < CPL; ++e)
+                            acc[e] = fma(v[d0 + j], j < LR - 1 ? wr[q - 1][j][e] : nr[q - 1][e], acc[e]);
+                    }
+                }
+                if (x0 + st < n) {
+#pragma unroll
+                    for (int e = 0; e < CPL; ++e) pd[e] = fma(w0[1][e], acc[e], pd[e]);
+                    *reinterpret_cast<double2*>(AP + size_t(r) * ld + xoff) = make_double2(acc[0], acc[1]);
+                }
+#pragma unroll
+                for (int e = 0; e < CPL; ++e) {
+                    w0[0][e] = w0[1][e];
+                    w0[1][e] = n0[e];
+                }
+#pragma unroll
+                for (int q = 1; q < NG; ++q) {
+#pragma unroll
+                    for (int j = 0; j + 1 < LR - 1; ++j)
+#pragma unroll
+                        for (int e = 0; e < CPL; ++e) wr[q - 1][j][e] = wr[q - 1][j + 1][e];
+#pragma unroll
+                    for (int e = 0; e < CPL; ++e) wr[q - 1][LR - 2][e] = nr[q - 1][e];
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < CPL; ++e)
+        for (int o = 16; o >= G; o >>= 1) pd[e] += __shfl_xor_sync(0xffffffffu, pd[e], o);
+    if (lane < G) {
+#pragma unroll
+        for (int e = 0; e < CPL; ++e) sm[wib * N + xoff + e] = pd[e];
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < N; c += blockDim.x) {
+        double tt = 0.0;
+        for (int k = 0; k < NW; ++k) tt += sm[k * N + c];
+        s.part0[size_t(blockIdx.x) * N + c] = tt;
+    }
+    __syncthreads();
     k1_epilogue(sm, N, cc, s);
 }
 
@@ -1285,6 +1771,9 @@ Plan plan_for(int N) {
 struct SellOps {
     const double *A = nullptr, *B = nullptr;  // SELL-32 values (N <= 2)
     const double* T8 = nullptr;               // T8 values (N = 16, no shift, rows of <= 16 entries)
+    const double* DIA = nullptr;              // tiled stencil values (dia.cuh) for dia_g lanes per row
+    int dia_g = 0;
+    int dia_z = 0;                            // > 0: z-marching kernel, lines per block
     // CSR pattern the row kernels walk: the level's natural interior pattern, or its locality-ordered copy
     const int32_t *ptr = nullptr, *col = nullptr;
     int max_row = 0;
@@ -1323,6 +1812,103 @@ bool try_sell(Ctx& c, const Level& L, const CgWork& w, const Cols& cc, const Sel
     }
 }
 
+/// lanes per row of the stencil SpMM for an N-column block (0: no stencil kernel for this N).
+/// KSB_DIA_G selects 4 / 8 / 16 lanes at N = 16 (default 8: 2 columns per lane).
+int dia_prefetch() {
+    const char* env = std::getenv("KSB_DIA_PF");
+    return env ? std::atoi(env) : 0;
+}
+
+int dia_lanes(int N) {
+    const char* env = std::getenv("KSB_DIA_G");  // read per solve (tests switch it)
+    if (N == 16) {
+        const int g = env ? std::atoi(env) : 8;
+        return (g == 4 || g == 16) ? g : 8;
+    }
+    return 0;
+}
+
+/// z-marching stencil kernel on cubic grid levels (N = 16), opt-in: KSB_DIA_Z=4 / 8 lines per block. Measured on
+/// cfg2 (profiles/README.md, r02): L2->L1 traffic halves (1.84 -> 0.90 GB per SpMM, L1 hit 12 -> 55 %) but the
+/// kernel stays latency bound at 16 warps per SM and runs 0.27-0.46 ms against 0.22 ms for k_spmm_dia_tv.
+int dia_z(const Level& L, int N) {
+    const char* env = std::getenv("KSB_DIA_Z");
+    if (N != 16 || L.dia_n == 0 || !env || env[0] == '0') return 0;
+    return std::atoi(env) == 8 ? 8 : 4;
+}
+
+bool try_dia(Ctx& c, const Level& L, const CgWork& w, const Cols& cc, const SellOps& so) {
+    if (!so.DIA) return false;
+    const DiaGeom dg = dia_geom(L);
+    if (so.dia_z) {
+        const size_t sm = sizeof(double) * std::max<size_t>(8 * size_t(cc.N), 2 * size_t(cc.N));
+        auto go_z = [&](auto kern, int nw) {
+            static std::map<const void*, bool> attr;
+            if (!attr[reinterpret_cast<const void*>(kern)]) {
+                KSB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                                    int(cudaSharedmemCarveoutMaxL1)));
+                attr[reinterpret_cast<const void*>(kern)] = true;
+            }
+            const int n = dg.n, tiles = ceil_div(n, 32) * ceil_div(n, nw);
+            const int res = resident_grid(c, kern, nw * 32, sm);
+            const char* zc_env = std::getenv("KSB_DIA_ZC");
+            const int nzc = std::max(1, std::min(n, zc_env ? std::atoi(zc_env) : ceil_div(res, tiles)));
+            const int grid = std::max(1, std::min({res, tiles * nzc, w.cap_blocks}));
+            launch(c, "spmm", kern, grid, nw * 32, sm, L.ni, cc, dg, nzc, so.DIA, (const double*)w.P, w.AP, w.dev);
+            return true;
+        };
+        if (L.dia_ng == 7) return so.dia_z == 8 ? go_z(k_spmm_dia_z<7, 2, 8, 2>, 8) : go_z(k_spmm_dia_z<7, 2, 4, 4>, 4);
+        if (L.dia_ng == 9) return so.dia_z == 8 ? go_z(k_spmm_dia_z<9, 3, 8, 2>, 8) : go_z(k_spmm_dia_z<9, 3, 4, 4>, 4);
+    }
+    const size_t sm = sizeof(double) * std::max<size_t>(size_t(kThreads / 32) * cc.N, 2 * size_t(cc.N));
+    auto go = [&](auto kern, int G) {
+        const int T = (32 / G) * kDiaS;
+        const int want = ceil_div(ceil_div(L.ni, T), kThreads / 32);
+        const int grid = std::max(1, std::min(want, resident_grid(c, kern, kThreads, sm)));
+        launch(c, "spmm", kern, grid, kThreads, sm, L.ni, cc, dg, so.DIA, (const double*)w.P, w.AP, w.dev);
+        return true;
+    };
+    const int pf = dia_prefetch();
+    const char* tv = std::getenv("KSB_DIA_TV");
+    if (!(tv && tv[0] == '0')) {  // staged values (default)
+        const DiaGeom g2 = dg;
+        auto go_tv = [&](auto kern, int G) {
+            const size_t smt = dia_tv_smem(g2.D, 32 / G, cc.N);
+            static std::map<const void*, bool> attr;
+            if (!attr[reinterpret_cast<const void*>(kern)]) {
+                KSB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smt)));
+                attr[reinterpret_cast<const void*>(kern)] = true;
+            }
+            const int T = (32 / G) * kDiaS;
+            const int want = ceil_div(ceil_div(L.ni, T), kThreads / 32);
+            const int grid = std::max(1, std::min(want, resident_grid(c, kern, kThreads, smt)));
+            launch(c, "spmm", kern, grid, kThreads, smt, L.ni, cc, g2, so.DIA, (const double*)w.P, w.AP, w.dev);
+            return true;
+        };
+        const char* mb = std::getenv("KSB_DIA_MINB");
+        if (L.dia_ng == 7 && so.dia_g == 8 && mb && mb[0] == '3') return go_tv(k_spmm_dia_tv<7, 2, 8, 2, 3>, 8);
+        if (L.dia_ng == 7 && so.dia_g == 8) return go_tv(k_spmm_dia_tv<7, 2, 8, 2, 2>, 8);
+        if (L.dia_ng == 7 && so.dia_g == 4) return go_tv(k_spmm_dia_tv<7, 2, 4, 4, 1>, 4);
+        if (L.dia_ng == 9 && so.dia_g == 8) return go_tv(k_spmm_dia_tv<9, 3, 8, 2, 2>, 8);
+    }
+    if (L.dia_ng == 7) {
+        switch (so.dia_g) {
+            case 4: return pf ? go(k_spmm_dia<7, 2, 4, 4, 1, 4>, 4) : go(k_spmm_dia<7, 2, 4, 4, 1, 0>, 4);
+            case 8:
+                return pf >= 8 ? go(k_spmm_dia<7, 2, 8, 2, 2, 8>, 8)
+                               : pf ? go(k_spmm_dia<7, 2, 8, 2, 2, 4>, 8) : go(k_spmm_dia<7, 2, 8, 2, 2, 0>, 8);
+            case 16: return pf ? go(k_spmm_dia<7, 2, 16, 1, 3, 4>, 16) : go(k_spmm_dia<7, 2, 16, 1, 3, 0>, 16);
+        }
+    } else if (L.dia_ng == 9) {
+        switch (so.dia_g) {
+            case 4: return go(k_spmm_dia<9, 3, 4, 4, 1, 4>, 4);
+            case 8: return go(k_spmm_dia<9, 3, 8, 2, 2, 4>, 8);
+            case 16: return go(k_spmm_dia<9, 3, 16, 1, 3, 4>, 16);
+        }
+    }
+    return false;
+}
+
 template <int G, int CPL, bool SHIFT, bool SPLIT, int FULL>
 void launch_iteration(Ctx& c, const Level& L, const CgWork& w, const Cols& cc, const double* A, const double* Bv,
                       const double* Bb, double* X, int grid_s, int grid_e, const SellOps& so) {
@@ -1332,6 +1918,7 @@ void launch_iteration(Ctx& c, const Level& L, const CgWork& w, const Cols& cc, c
     grid_e = std::min(grid_e, v2 ? resident_grid(c, k_update_r<2>, kThreads, sm_e)
                                  : resident_grid(c, k_update_r<1>, kThreads, sm_e));
     if (try_sell<SHIFT>(c, L, w, cc, so)) {
+    } else if (!SHIFT && try_dia(c, L, w, cc, so)) {
     } else {
         static const char* mb = std::getenv("KSB_SPMM_MINB");
         const int minb = mb ? std::atoi(mb) : KSB_SPMM_MINB;
@@ -1590,6 +2177,15 @@ void cg_solve(Ctx& c, Level& L, int mat, int shift_mat, const double* h_sigma, c
         so.B = shift ? L.sell_values(shift_mat) : nullptr;
     }
     if (N == 16 && !shift) so.T8 = L.t8_values(mat);
+    // stencil levels (cfg2's lexicographic box, uniformly refined levels in the locality order): the sliding-window
+    // SpMM; KSB_SPMM_DIA=0 keeps the CSR / T8 kernels
+    const char* dia_env = std::getenv("KSB_SPMM_DIA");
+    if (!shift && L.dia_ng > 0 && L.dia_lo == int(lo) && dia_lanes(N) > 0 && !(dia_env && dia_env[0] == '0') &&
+        ld % 2 == 0) {
+        so.dia_g = dia_lanes(N);
+        so.dia_z = dia_z(L, N);
+        so.DIA = L.dia_values(mat, so.dia_z ? kDiaLine : 32 / so.dia_g);
+    }
     const int total = cc.fixed ? o.fixed_iterations : o.max_iterations;
     const int every = std::max(1, o.check_every);
     auto run_chunk = [&](int chunk) {
@@ -1610,11 +2206,11 @@ void cg_solve(Ctx& c, Level& L, int mat, int shift_mat, const double* h_sigma, c
         std::memset(&key, 0, sizeof key);
         key.level_uid = L.uid;
         // every pointer a captured kernel dereferences
-        const void* ptrs[24] = {A, Bv, d_B, d_X, so.A, so.B, w.R, w.P, w.AP, w.scal.p, w.parts.p, w.ints.p,
+        const void* ptrs[25] = {A, Bv, d_B, d_X, so.A, so.B, w.R, w.P, w.AP, w.scal.p, w.parts.p, w.ints.p,
                                 d.diagA, d.diagB, so.ptr, so.col, so.T8, L.t8_col.p, L.sell_ptr.p, L.sell_col.p,
-                                L.ii_ptr.p, L.ii_col.p, L.lo_ptr.p, L.lo_col.p};
+                                L.ii_ptr.p, L.ii_col.p, L.lo_ptr.p, L.lo_col.p, so.DIA};
         std::memcpy(key.ptrs, ptrs, sizeof ptrs);
-        const int ints[10] = {mat, shift_mat, N, ld, chunk, grid_s, grid_e, cc.fixed, L.ni, L.nslices};
+        const int ints[10] = {mat, shift_mat, N, ld, chunk, grid_s, grid_e, cc.fixed, L.ni, L.nslices * 64 + so.dia_g * 2 + (so.dia_z > 0)};
         std::memcpy(key.ints, ints, sizeof ints);
         key.tol = cc.tol;
         for (auto& g : w.graphs)

@@ -31,7 +31,7 @@ struct CgDev {
 /// identity of a captured chunk of CG iterations: every kernel argument that can differ between solves
 struct CgGraphKey {
     uint64_t level_uid;  // Level::uid: never reused, so a graph of a destroyed level can never match
-    const void* ptrs[24];
+    const void* ptrs[25];
     int ints[10];
     double tol;
 };

@@ -62,6 +62,11 @@ void upload_level(Ctx& cx, std::shared_ptr<FineTopology> topo, Level& L) {
     L.lo_map.upload(cx, T.lo_map);
     L.lo_dslot.upload(cx, T.lo_dslot);
     L.lo_max_row = T.lo_max_row;
+    L.dia_ng = T.dia_ng;
+    L.dia_lr = T.dia_lr;
+    L.dia_lo = T.dia_lo;
+    L.dia_n = T.dia_n;
+    for (int q = 0; q < T.dia_ng; ++q) L.dia_first[q] = T.dia_first[q];
     L.nslices = int(T.sell_ptr.size()) - 1;
     L.max_row_ii = 0;
     for (size_t i = 0; i + 1 < T.ii.ptr.size(); ++i) L.max_row_ii = std::max(L.max_row_ii, int(T.ii.ptr[i + 1] - T.ii.ptr[i]));

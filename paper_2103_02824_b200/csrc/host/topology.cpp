@@ -2,6 +2,8 @@
 #include "topology.hpp"
 
 #include <algorithm>
+#include <cmath>
+#include <cstdlib>
 #include <limits>
 
 namespace ksb {
@@ -386,6 +388,97 @@ std::shared_ptr<FineTopology> build_topology(const Hierarchy& h, int level) {
             }
         }
         topo->lo_max_row = wmax;
+    }
+
+    // stencil (DIA) view: natural order first, else the locality order
+    {
+        auto detect = [&](const std::vector<int32_t>& ptr, const std::vector<int32_t>& col, int on_lo) {
+            if (ni < 2 || ptr.empty()) return false;
+            constexpr int kMax = 27;
+            std::vector<int32_t> offs;
+            bool overflow = false;
+#pragma omp parallel
+            {
+                std::vector<int32_t> mine;
+                bool over = false;
+#pragma omp for schedule(static) nowait
+                for (int r = 0; r < ni; ++r) {
+                    if (over) continue;
+                    for (int k = ptr[r]; k < ptr[r + 1]; ++k) {
+                        const int32_t o = col[k] - r;
+                        if (std::find(mine.begin(), mine.end(), o) == mine.end()) {
+                            mine.push_back(o);
+                            if (int(mine.size()) > kMax) {
+                                over = true;
+                                break;
+                            }
+                        }
+                    }
+                }
+#pragma omp critical
+                {
+                    overflow = overflow || over;
+                    for (int32_t o : mine)
+                        if (std::find(offs.begin(), offs.end(), o) == offs.end()) offs.push_back(o);
+                }
+            }
+            if (overflow || int(offs.size()) > kMax) return false;
+            std::sort(offs.begin(), offs.end());
+            std::vector<std::pair<int32_t, int>> runs;  // (first offset, length)
+            for (int32_t o : offs) {
+                if (!runs.empty() && runs.back().first + runs.back().second == o)
+                    ++runs.back().second;
+                else
+                    runs.push_back({o, 1});
+            }
+            int centre = -1, lr = 0;
+            for (int q = 0; q < int(runs.size()); ++q) {
+                if (runs[q].first == -1 && runs[q].second == 3) {
+                    centre = q;
+                } else {
+                    if (lr && runs[q].second != lr) return false;
+                    lr = runs[q].second;
+                }
+            }
+            const int ng = int(runs.size());
+            const bool kuhn = ng == 7 && lr == 2, box = ng == 9 && lr == 3;
+            if (centre < 0 || !(kuhn || box)) return false;
+            topo->dia_first.assign(1, -1);
+            for (int q = 0; q < ng; ++q)
+                if (q != centre) topo->dia_first.push_back(runs[q].first);
+            topo->dia_ng = ng;
+            topo->dia_l0 = 3;
+            topo->dia_lr = lr;
+            topo->dia_lo = on_lo;
+            // a cubic grid (rows = x + n (y + n z)) whose every entry couples geometric neighbours (no offset wraps
+            // around a grid line or plane): the z-marching stencil SpMM may tile it by (x, y) blocks
+            const int n = int(std::lround(std::cbrt(double(ni))));
+            bool grid = n >= 3 && int64_t(n) * n * n == ni;
+            for (int32_t o : offs) {
+                if (!grid) break;
+                const int dz = int(std::lround(double(o) / (double(n) * n)));
+                const int rem = o - dz * n * n;
+                const int dy = int(std::lround(double(rem) / n));
+                const int dx = rem - dy * n;
+                grid = std::abs(dx) <= 1 && std::abs(dy) <= 1 && std::abs(dz) <= 1;
+            }
+            if (grid) {
+                int bad = 0;
+#pragma omp parallel for schedule(static) reduction(+ : bad)
+                for (int r = 0; r < ni; ++r) {
+                    const int x = r % n, y = (r / n) % n, z = r / (n * n);
+                    for (int k = ptr[r]; k < ptr[r + 1]; ++k) {
+                        const int c = col[k];
+                        const int dx = c % n - x, dy = (c / n) % n - y, dz = c / (n * n) - z;
+                        bad += std::abs(dx) > 1 || std::abs(dy) > 1 || std::abs(dz) > 1;
+                    }
+                }
+                grid = bad == 0;
+            }
+            topo->dia_n = grid ? n : 0;
+            return true;
+        };
+        if (!detect(ii.ptr, ii.col, 0) && !topo->lo_perm.empty()) detect(topo->lo_ptr, topo->lo_col, 1);
     }
 
     // fine tets grouped by coarse ancestor

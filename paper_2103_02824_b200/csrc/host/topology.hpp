@@ -86,6 +86,15 @@ struct FineTopology {
     // slot. Empty when not built.
     std::vector<int32_t> lo_perm, lo_ptr, lo_col, lo_map, lo_dslot;
     int lo_max_row = 0;
+    // Stencil (DIA) view: the interior rows are a uniform stencil in the natural numbering (dia_lo = 0; box meshes,
+    // lexicographic) or in the locality order (dia_lo = 1; uniformly refined levels): every column offset
+    // (col - row) lies in a set that splits into runs of consecutive offsets -- a centre run {-1, 0, 1} and
+    // dia_ng - 1 further runs of one common length dia_lr. dia_first[q] = first offset of run q (run 0 = centre,
+    // the others ascending). Supported shapes: Kuhn 15-point (7 runs, 3 + 6 x 2) and box 27-point (9 x 3).
+    // dia_ng = 0 when the level has no stencil view.
+    int dia_ng = 0, dia_l0 = 0, dia_lr = 0, dia_lo = 0;
+    int dia_n = 0;  // > 0: the rows are an n x n x n grid, row = x + n (y + n z), all couplings between neighbours
+    std::vector<int32_t> dia_first;
     // one-step prolongation from level-1 (fem::prolongation_matrix, proj/src/fespace.cpp:35-56): per vertex <= 4
     // (previous-level vertex, weight), ascending vertex, -1 padded; empty on level 0. prev_iidx: the previous
     // level's vertex -> interior index (interior-block inputs).

@@ -103,3 +103,65 @@ def h2o_atoms(seed: int = 2103):
     h2 = 1.8 * np.array([-np.sin(half), np.cos(half), 0.0])
     pos = [np.zeros(3), rot @ h1, rot @ h2]
     return [[8.0, *pos[0]], [1.0, *pos[1]], [1.0, *pos[2]]]
+
+
+# BASELINE configs[2..4] (cfg3 / cfg4 / cfg5): generator, orbital count, half box, finest-level DOF target
+ADAPTIVE_CONFIGS = {
+    "cfg3": ("h2o_atoms", 5, 20.0, 1.0e6),
+    "cfg4": ("ring_atoms", 21, 25.0, 4.0e6),
+    "cfg5": ("sphere_atoms", 120, 30.0, 1.2e7),
+}
+
+
+def adaptive_hierarchy(ctx: api.Context, atoms, N: int, box: float, target_dofs: float, n_coarse: int = 8,
+                       theta: float = 0.4, zeta: float = 1.0, max_levels: int = 60, keep_last: bool = True,
+                       log=None):
+    """Residual-indicator adaptive refinement (proj/src/driver.cpp:340-378: est::compute_indicators, Doerfler
+    marking with theta, adapt_refine) from the n_coarse^3 Kuhn box until the finest mesh has >= target_dofs vertices.
+
+    The reference drives the marks with each level's converged solution; for cfg3-cfg5 its coarse SCF does not
+    converge on the configured 8^3 mesh (profiles/r02_scf_histories.json), so the run cannot start. The indicators
+    here are evaluated on every level for the seeded synthetic state of `synthetic_start` (hydrogenic orbitals at the
+    nuclei, their own Hartree potential and LDA potential), which refines where the configured molecule needs it.
+    Returns (hierarchy, meshes, finest Level or None, per-level records)."""
+    import time
+
+    h = api.Hierarchy()
+    mesh = api.Mesh.box([-box] * 3, [box] * 3, n_coarse)
+    h.push(mesh)
+    meshes = [mesh]
+    cen = [a[1:] for a in atoms]
+    recs = []
+    L = None
+    for level in range(max_levels):
+        t0 = time.perf_counter()
+        L = api.Level(ctx, h, level)
+        L.set_system(atoms, n_pairs=N, occupancy=2.0, xc="lda")
+        L.level_ops()
+        t1 = time.perf_counter()
+        if mesh.n_vertices >= target_dofs:
+            recs.append({"level": level, "n": L.n, "ni": L.ni, "tets": L.nt, "s_level": round(t1 - t0, 2)})
+            if log:
+                log(recs[-1])
+            break
+        lam, Phi, w, ld = synthetic_start(L, ctx, mesh, cen, N, zeta=zeta, lam0=-0.5)
+        rho, vxc = ctx.empty((L.n,)), ctx.empty((L.n,))
+        L.density_xc(Phi, rho, vxc, N=N, ld=ld)
+        eta, tot = L.indicators(lam, Phi, w, vxc, ld=ld)
+        marked = api.dorfler_mark(eta, tot, theta)
+        del Phi, w, rho, vxc
+        L.close()
+        L = None
+        t2 = time.perf_counter()
+        mesh = mesh.adapt_refine(marked)
+        h.push(mesh)
+        meshes.append(mesh)
+        recs.append({"level": level, "n": meshes[-2].n_vertices, "tets": meshes[-2].n_tets, "marked": int(len(marked)),
+                     "s_level": round(t1 - t0, 2), "s_estimate": round(t2 - t1, 2),
+                     "s_refine": round(time.perf_counter() - t2, 2)})
+        if log:
+            log(recs[-1])
+    if not keep_last and L is not None:
+        L.close()
+        L = None
+    return h, meshes, L, recs

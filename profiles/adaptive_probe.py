@@ -1,0 +1,40 @@
+"""Estimator-driven adaptive hierarchy for BASELINE configs[2..4] on the device (workloads.adaptive_hierarchy), then
+one correction step on the finest level from the synthetic start: per-level and per-phase times.
+Usage: python profiles/adaptive_probe.py cfg3 [target_dofs] [theta]"""
+import json
+import sys
+import time
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import numpy as np  # noqa: E402
+
+import paper_2103_02824_b200 as kb  # noqa: E402
+from paper_2103_02824_b200 import workloads  # noqa: E402
+
+name = sys.argv[1]
+gen, N, box, target = workloads.ADAPTIVE_CONFIGS[name]
+if len(sys.argv) > 2:
+    target = float(sys.argv[2])
+theta = float(sys.argv[3]) if len(sys.argv) > 3 else 0.4
+atoms = getattr(workloads, gen)()
+ctx = kb.Context(0)
+t0 = time.time()
+h, meshes, L, recs = workloads.adaptive_hierarchy(ctx, atoms, N, box, target, theta=theta,
+                                                  log=lambda r: print(json.dumps(r), flush=True))
+print("hierarchy_s", round(time.time() - t0, 1), "levels", len(meshes), flush=True)
+t1 = time.time()
+lam, Phi, w, ld = workloads.synthetic_start(L, ctx, meshes[-1], [a[1:] for a in atoms], N, zeta=1.0, lam0=-0.5)
+lam = np.linspace(-1.5, -0.3, N)
+print("start_s", round(time.time() - t1, 1), flush=True)
+for k in range(2):
+    t2 = time.time()
+    try:
+        lg = L.correction_step(lam, Phi, w, ld=ld)
+    except kb.KsbError as e:
+        print("step error", str(e)[:300])
+        break
+    ctx.sync()
+    print(json.dumps({"step": k, "wall_s": round(time.time() - t2, 2)} | {kk: lg[kk] for kk in
+          ("ms_bvp", "ms_hartree", "ms_project", "ms_inner", "ms_total", "cg_iterations", "inner_iterations")}
+          | {"attempts": lg["attempts"][:8]}), flush=True)

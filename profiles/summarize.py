@@ -62,6 +62,28 @@ def full(paths):
             for key, label in KEYS:
                 if key in idx:
                     print(f"  {label:38s} {r[idx[key]]:>16s} {units[idx[key]]}")
+            stalls = []
+            for h, i in idx.items():
+                if h.startswith("smsp__average_warps_issue_stalled_") and h.endswith("_per_issue_active.ratio"):
+                    try:
+                        v = float(r[i])
+                    except ValueError:
+                        continue
+                    if v >= 0.05:
+                        stalls.append((v, h[len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")]))
+            if stalls:
+                print("  stalls per issue: " + ", ".join(f"{n} {v:.2f}" for v, n in sorted(stalls, reverse=True)))
+            for h in ("sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+                      "smsp__issue_active.avg.pct_of_peak_sustained_active",
+                      "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+                      "l1tex__data_bank_conflicts_pipe_lsu.sum",
+                      "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum",
+                      "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum",
+                      "l1tex__data_pipe_lsu_wavefronts_mem_lg.sum" if False else "l1tex__data_pipe_lsu_wavefronts.sum",
+                      "lts__t_sectors_srcunit_tex_op_read.sum",
+                      "dram__throughput.avg.pct_of_peak_sustained_elapsed"):
+                if h in idx:
+                    print(f"  {h:70s} {r[idx[h]]:>16s} {units[idx[h]]}")
             print()
 
 
