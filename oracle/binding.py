@@ -342,12 +342,12 @@ class Oracle:
         return out
 
     def correction_step(self, level, lambdas, orb, w, tol_linear=1e-9, tol_inner=1e-8, score_floor=1e-8,
-                        max_inner=400, nev_pad=4, precond=0):
+                        max_inner=400, nev_pad=4, precond=0, fixed_sweeps=0):
         lam = f64(lambdas).copy()
         orb = f64(orb).copy()
         w = f64(w).copy()
         cd = np.array([tol_linear, tol_inner, score_floor])
-        ci = np.array([max_inner, nev_pad, precond], np.int32)
+        ci = np.array([max_inner, nev_pad, precond, fixed_sweeps], np.int32)
         li = np.zeros(2 + 2 * self.N, np.int32)
         ld = np.zeros(6)
         _chk(lib.orc_correction_step(self._h, level, dp(cd), ip(ci), dp(lam), dp(orb), dp(w), ip(li), dp(ld)))

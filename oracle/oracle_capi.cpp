@@ -474,7 +474,7 @@ int orc_last_scf_rho(orc_problem* p, double* rho) {
     return guard([&] { std::memcpy(rho, p->last_scf_rho.data(), sizeof(double) * p->last_scf_rho.size()); });
 }
 
-/// cfg_d: tol_linear, tol_inner, score_floor; cfg_i: max_inner, nev_pad, precond
+/// cfg_d: tol_linear, tol_inner, score_floor; cfg_i: max_inner, nev_pad, precond, fixed_sweeps
 /// log_i: inner_iterations, hartree_iterations, attempts[N], cg_iters[N]; log_d: delta, t_bvp, t_hartree, t_blocks, t_inner, t_total
 int orc_correction_step(orc_problem* p, int level, const double* cfg_d, const int* cfg_i, double* lambdas, double* orb,
                         double* w, int* log_i, double* log_d) {
@@ -489,6 +489,7 @@ int orc_correction_step(orc_problem* p, int level, const double* cfg_d, const in
         c.max_inner = cfg_i[0];
         c.nev_pad = cfg_i[1];
         c.precond = cfg_i[2];
+        c.fixed_sweeps = cfg_i[3];
         Vec lam(lambdas, lambdas + N);
         auto orbs = unpack(orb, n, N);
         Vec wv(w, w + n);

@@ -1822,7 +1822,9 @@ void correction_step(const System& s, const Hier& h, const LevelOps& ops, const 
     const Blocks B =
         prepare_blocks(h.spaces[0], ops.V, ops.P_full, ops.S, ops.M, ops.a_op, phi_t, w_tilde, vxc, s.occ, s.hartree_on, bc);
     const double t3 = now();
-    const InnerResult inner = inner_scf(B, pure_state(B, lambdas), cfg.tol_inner, cfg.max_inner, cfg.score_floor, cfg.nev_pad);
+    const bool fixed = cfg.fixed_sweeps > 0;
+    const InnerResult inner = inner_scf(B, pure_state(B, lambdas), cfg.tol_inner, fixed ? cfg.fixed_sweeps : cfg.max_inner,
+                                        cfg.score_floor, cfg.nev_pad, fixed);
     const double t4 = now();
     std::vector<Vec> orb;
     Vec wn;

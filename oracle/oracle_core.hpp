@@ -293,6 +293,7 @@ struct StepConfig {
     double tol_linear = 1e-9, tol_inner = 1e-8, score_floor = 1e-8;
     int max_inner = 400, nev_pad = 4;
     int precond = 0;  // linear-solve preconditioner used by the oracle (0 SGS = reference)
+    int fixed_sweeps = 0;  // > 0: the inner loop runs exactly this many sweeps (benchmark harness; mirrors the device)
 };
 struct StepLog {
     ShiftLog shifts;

@@ -224,7 +224,21 @@ class Context:
 
 
 class DeviceArray:
+    @classmethod
+    def wrap(cls, ctx: Context, ptr: int, shape, dtype=np.float64, keep=None) -> "DeviceArray":
+        """non-owning view of device memory allocated elsewhere (e.g. a torch tensor, kept alive by `keep`)"""
+        d = cls.__new__(cls)
+        d.ctx = ctx
+        d.shape = tuple(int(s) for s in (shape if isinstance(shape, (tuple, list)) else (shape,)))
+        d.dtype = np.dtype(dtype)
+        d.nbytes = int(np.prod(d.shape)) * d.dtype.itemsize
+        d.ptr = C.c_void_p(int(ptr))
+        d._owned = False
+        d._keep = keep
+        return d
+
     def __init__(self, ctx: Context, shape, dtype=np.float64):
+        self._owned = True
         self.ctx = ctx
         self.shape = tuple(int(s) for s in (shape if isinstance(shape, (tuple, list)) else (shape,)))
         self.dtype = np.dtype(dtype)
@@ -234,9 +248,9 @@ class DeviceArray:
         self.ptr = p
 
     def __del__(self):
-        if getattr(self, "ptr", None) and getattr(self.ctx, "_h", None):
+        if getattr(self, "_owned", True) and getattr(self, "ptr", None) and getattr(self.ctx, "_h", None):
             lib.ksb_free(self.ctx._h, self.ptr)
-            self.ptr = None
+        self.ptr = None
 
     def upload(self, a: np.ndarray):
         a = np.ascontiguousarray(a, self.dtype)

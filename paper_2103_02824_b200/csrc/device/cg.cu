@@ -2142,13 +2142,12 @@ void cg_solve(Ctx& c, Level& L, int mat, int shift_mat, const double* h_sigma, c
     if (lo) {
         const int64_t vec = int64_t(L.ni) * ld;
         if (w.lo_b.n < vec) w.lo_b.alloc(vec);
-        if (w.lo_x.n < vec) w.lo_x.alloc(vec);
         const int gp = elem_grid(c, L.ni, N);
         launch(c, "cg_setup", k_permute_rows, gp, kThreads, 0, L.ni, N, ld, (const int32_t*)L.lo_perm.p, d_B,
                w.lo_b.p, 0);
-        // X is not permuted in: k_init starts every column from x0 = 0 (proj/src/solver.cpp:59)
+        // X is not permuted in: k_init starts every column from x0 = 0 (proj/src/solver.cpp:59). The caller's X
+        // holds the ordered iterate during the solve and is put back in place at the end (through the free R block)
         d_B = w.lo_b.p;
-        d_X = w.lo_x.p;
     }
     if (w.diagA.n < L.ni) w.diagA.alloc(L.ni);
     if (w.diagB.n < L.ni) w.diagB.alloc(L.ni);
@@ -2301,9 +2300,11 @@ void cg_solve(Ctx& c, Level& L, int mat, int shift_mat, const double* h_sigma, c
             if (ctl[kNActive] == 0) break;
         }
     }
-    if (lo)
+    if (lo) {
+        KSB_CUDA_CHECK(cudaMemcpyAsync(w.R, d_X, sizeof(double) * size_t(L.ni) * ld, cudaMemcpyDeviceToDevice, c.stream));
         launch(c, "cg_setup", k_permute_rows, elem_grid(c, L.ni, N), kThreads, 0, L.ni, N, ld,
-               (const int32_t*)L.lo_perm.p, (const double*)d_X, X_user, 1);
+               (const int32_t*)L.lo_perm.p, (const double*)w.R, X_user, 1);
+    }
     if (stats) {
         std::vector<int> st(N), it(N), np(N);
         std::vector<double> rel(N);

@@ -74,7 +74,16 @@ __global__ void k_gather_cols(int ni, int nc, const int* __restrict__ cols, cons
     for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < int64_t(ni) * nc;
          e += int64_t(gridDim.x) * blockDim.x) {
         const int r = int(e / nc), j = int(e % nc);
-        B[size_t(r) * ldb + j] = scale[j] * R[size_t(r) * ldr + cols[j]];
+        B[size_t(r) * ldb + j] = (scale ? scale[j] : 1.0) * R[size_t(r) * ldr + cols[j]];
+    }
+}
+
+/// B[r, j] *= scale[j], j < nc
+__global__ void k_scale_cols(int ni, int nc, const double* __restrict__ scale, double* __restrict__ B, int ldb) {
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < int64_t(ni) * nc;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        const int r = int(e / nc), j = int(e % nc);
+        B[size_t(r) * ldb + j] *= scale[j];
     }
 }
 
@@ -241,9 +250,10 @@ void solve_orbitals(Level& L, Corrector& K, CgWork& cg, const StepOptions& o, co
                     const double* d_Phi, int ld, double* d_PhiT, int ldT, StepLog* log, int n_cols) {
     Ctx& c = *L.ctx;
     const int N = n_cols > 0 ? n_cols : K.sys.N, ni = L.ni;
+    // one block-sized buffer: R0 = M phi (orbitals vanish on the boundary), scaled in place by lambda into the
+    // right-hand sides; the level-shift attempts recompute M phi for their (few) columns
     need(K.R0, int64_t(ni) * ld);
-    need(K.Bblk, int64_t(ni) * ld);
-    spmm(c, L, L.mats[1].ii.p, nullptr, nullptr, d_Phi, N, ld, K.R0.p, ld);  // M phi (orbitals vanish on the boundary)
+    spmm(c, L, L.mats[1].ii.p, nullptr, nullptr, d_Phi, N, ld, K.R0.p, ld);
     if (K.idx.n < 4 * N + 8) K.idx.alloc(4 * N + 8);
     need(K.colscale, N);
     double* sc = K.colscale.p;
@@ -251,13 +261,12 @@ void solve_orbitals(Level& L, Corrector& K, CgWork& cg, const StepOptions& o, co
     for (int i = 0; i < N; ++i) cols[i] = i;
     KSB_CUDA_CHECK(cudaMemcpyAsync(K.idx.p, cols.data(), sizeof(int) * N, cudaMemcpyHostToDevice, c.stream));
     KSB_CUDA_CHECK(cudaMemcpyAsync(sc, h_lambda, sizeof(double) * N, cudaMemcpyHostToDevice, c.stream));
-    launch(c, "elementwise", k_gather_cols, grid_of(c, int64_t(ni) * N), kT, 0, ni, N, (const int*)K.idx.p,
-           (const double*)sc, (const double*)K.R0.p, ld, K.Bblk.p, ld);
+    launch(c, "elementwise", k_scale_cols, grid_of(c, int64_t(ni) * N), kT, 0, ni, N, (const double*)sc, K.R0.p, ld);
     CgOptions co;
     co.tol = o.tol_linear;
     co.check_every = o.check_every;
     std::vector<CgColumnStats> st(N);
-    cg_solve(c, L, MAT_H, -1, nullptr, K.Bblk.p, d_PhiT, N, ld, co, st.data(), cg);
+    cg_solve(c, L, MAT_H, -1, nullptr, K.R0.p, d_PhiT, N, ld, co, st.data(), cg);
     if (ldT != ld) raise(KSB_INVALID_ARGUMENT, "solve_orbitals: ld mismatch");
     std::vector<int> attempt(N, -1), iters(N);
     std::vector<int> fail;
@@ -280,7 +289,10 @@ void solve_orbitals(Level& L, Corrector& K, CgWork& cg, const StepOptions& o, co
         KSB_CUDA_CHECK(cudaMemcpyAsync(dsc, scale.data(), sizeof(double) * nf, cudaMemcpyHostToDevice, c.stream));
         if (ldc > nf) KSB_CUDA_CHECK(cudaMemsetAsync(K.Bc.p, 0, sizeof(double) * ni * ldc, c.stream));
         launch(c, "elementwise", k_gather_cols, grid_of(c, int64_t(ni) * nf), kT, 0, ni, nf, (const int*)K.idx.p,
-               (const double*)dsc, (const double*)K.R0.p, ld, K.Bc.p, ldc);
+               (const double*)nullptr, d_Phi, ld, K.Xc.p, ldc);
+        spmm(c, L, L.mats[1].ii.p, nullptr, nullptr, K.Xc.p, nf, ldc, K.Bc.p, ldc);  // (lambda + sigma) M phi
+        launch(c, "elementwise", k_scale_cols, grid_of(c, int64_t(ni) * nf), kT, 0, ni, nf, (const double*)dsc, K.Bc.p,
+               ldc);
         std::vector<CgColumnStats> sst(nf);
         cg_solve(c, L, MAT_H, 1, sig.data(), K.Bc.p, K.Xc.p, nf, ldc, co, sst.data(), cg);
         std::vector<int> take(nf), still;

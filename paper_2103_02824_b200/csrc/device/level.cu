@@ -42,6 +42,29 @@ void upload_level(Ctx& cx, std::shared_ptr<FineTopology> topo, Level& L) {
     L.ancestor.upload(cx, T.ancestor);
     L.anc_ptr.upload(cx, T.anc_ptr);
     L.anc_tets.upload(cx, T.anc_tets);
+    {
+        // K-PROJ chunks: at most `cap` fine tets each, so that a coarse tet holding most of an adaptive level's
+        // tets (near a nucleus) is spread over many blocks; uniform levels (nt / nct <= cap) keep one per coarse tet
+        const int nct = std::max(0, int(T.anc_ptr.size()) - 1);
+        const int64_t cap = std::max<int64_t>(1024, (int64_t(T.anc_tets.size()) + 2047) / 2048);
+        std::vector<int32_t> cc, cb, ce, cp(size_t(nct) + 1, 0);
+        for (int C = 0; C < nct; ++C) {
+            cp[size_t(C)] = int32_t(cc.size());
+            const int32_t b = T.anc_ptr[size_t(C)], e = T.anc_ptr[size_t(C) + 1];
+            const int64_t pieces = std::max<int64_t>(1, (int64_t(e - b) + cap - 1) / cap);
+            for (int64_t q = 0; q < pieces; ++q) {
+                cc.push_back(C);
+                cb.push_back(int32_t(b + (int64_t(e - b) * q) / pieces));
+                ce.push_back(int32_t(b + (int64_t(e - b) * (q + 1)) / pieces));
+            }
+        }
+        if (!T.anc_ptr.empty()) cp[size_t(nct)] = int32_t(cc.size());
+        L.pj_n = int(cc.size());
+        L.pj_c.upload(cx, cc);
+        L.pj_b.upload(cx, cb);
+        L.pj_e.upload(cx, ce);
+        L.pj_ptr.upload(cx, cp);
+    }
     L.vinc_ptr.upload(cx, T.vinc_ptr);
     L.vinc.upload(cx, T.vinc);
     L.bvinc_ptr.upload(cx, T.bvinc_ptr);

@@ -15,7 +15,19 @@ struct DevBuf {
     void alloc(int64_t count) {
         release();
         n = count;
-        if (count > 0) KSB_CUDA_CHECK(cudaMalloc(&p, sizeof(T) * size_t(count)));
+        if (count > 0) {
+            const cudaError_t e = cudaMalloc(&p, sizeof(T) * size_t(count));
+            if (e != cudaSuccess) {
+                size_t fr = 0, tot = 0;
+                cudaGetLastError();
+                cudaMemGetInfo(&fr, &tot);
+                p = nullptr;
+                n = 0;
+                raise(KSB_CUDA, "cudaMalloc of " + std::to_string(sizeof(T) * size_t(count) >> 20) + " MiB failed (" +
+                                    cudaGetErrorString(e) + "; " + std::to_string(fr >> 20) + " of " +
+                                    std::to_string(tot >> 20) + " MiB free)");
+            }
+        }
     }
     void upload(Ctx& c, const std::vector<T>& h) {
         alloc(int64_t(h.size()));
@@ -60,6 +72,10 @@ struct Level {
     DevBuf<int32_t> pint_col;
     DevBuf<double> pint_val;
     DevBuf<int32_t> ancestor, anc_ptr, anc_tets;
+    // K-PROJ work chunks over anc_tets (project.cu): chunk k = [pj_b[k], pj_e[k]) of coarse tet pj_c[k]; pj_ptr[C] =
+    // first chunk of coarse tet C; pj_n = number of chunks (== nct when no coarse tet is split)
+    DevBuf<int32_t> pj_c, pj_b, pj_e, pj_ptr;
+    int pj_n = 0;
     DevBuf<int32_t> vinc_ptr, vinc;           // interior vertex -> incident (tet*4 + local)
     DevBuf<int32_t> bvinc_ptr, bvinc;         // boundary vertex -> incident (tet*4 + local)
     DevBuf<int32_t> cinc_ptr, cinc;           // coarse interior dof -> incident (coarse tet*4 + local)

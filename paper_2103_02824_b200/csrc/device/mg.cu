@@ -221,15 +221,15 @@ void mg_setup(Level& L, Multigrid& mg, const double* d_CHi) {
     mg.top = top;
     mg.CHi = d_CHi;
     mg.nH = L.nH;
+    Hierarchy h;  // levels 0 .. top-1, pushed once (each push chains the composite transfer data)
+    for (int k = 0; k < top; ++k) h.push(L.meshes[size_t(k)]);
     for (int l = 1; l <= top; ++l) {
         MgLevel& m = *mg.lv[size_t(l)];
         if (l == top) {
             m.L = &L;
         } else {
-            Hierarchy h;
-            for (int k = 0; k <= l; ++k) h.push(L.meshes[size_t(k)]);
             m.own = std::make_unique<Level>();
-            upload_level(c, build_topology(h, l), *m.own);
+            upload_level(c, build_topology(h, l, true), *m.own);
             m.own->flag.alloc(4);
             assemble_into(*m.own, 0, 1.0, 0.0, nullptr, 0.0, nullptr, 0.0);  // S
             m.L = m.own.get();
@@ -274,6 +274,21 @@ void mg_setup(Level& L, Multigrid& mg, const double* d_CHi) {
         for (auto* b : {&m.dinv, &m.b, &m.x, &m.y, &m.r}) b->alloc(std::max(1, m.ni));
         launch(c, "mg", k_mg_dinv, grid_rows(c, m.ni), kT, 0, m.ni, (const int32_t*)m.L->diag_slot.p,
                (const double*)m.L->mats[0].ii.p, m.dinv.p);
+        if (m.own) {
+            // the smoother reads S in the SELL-32 order only: convert once, then drop the assembly scratch (element
+            // matrices, gather lists) and the CSR copies, which would otherwise hold ~4x the top level's index data
+            // over an adaptive hierarchy of dozens of levels
+            Level& o = *m.own;
+            o.sell_values(0);
+            KSB_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+            for (auto* b : {&o.ii_gptr, &o.ii_gent, &o.ib_gptr, &o.ib_gent, &o.sell_map, &o.ii_col, &o.ib_col,
+                            &o.tets, &o.vinc, &o.bvinc})
+                b->release();
+            o.ebuf.release();
+            o.scratch.release();
+            o.mats[0].ii.release();
+            o.mats[0].ib.release();
+        }
         KSB_CUDA_CHECK(cudaStreamSynchronize(c.stream));  // host staging vectors go out of scope
     }
     mg.b0.alloc(std::max(1, mg.nH));

@@ -23,6 +23,10 @@ struct ProjIn {
     const int32_t *tets, *iidx, *anc_ptr, *anc_tets, *ctets, *ciidx, *pint_col;
     const double *xyz, *pint_val, *eext, *Phi, *wt, *ell, *vxc;
     int N, ld, nct;
+    // work chunks: chunk k covers anc_tets[ch_b[k], ch_e[k]) of coarse tet ch_c[k] (a coarse tet with more fine
+    // descendants than the chunk size is split, so adaptive levels keep every SM busy); partials per chunk
+    const int32_t *ch_c, *ch_b, *ch_e;
+    int nch;
 };
 
 __device__ __forceinline__ void load_mu(const ProjIn& in, int4 v, const int (&ci)[4], double (&mu)[4][4]) {
@@ -96,13 +100,14 @@ __device__ void block_reduce_store(double (&acc)[K], double* __restrict__ dst) {
 
 // shared part (function y == N): A_H1 (16) A_H3 (16) A_H4 (16) d_Hh (4) lift_load (4) zeta lift0
 __global__ void __launch_bounds__(kProjThreads) k_proj_shared(ProjIn in, double* __restrict__ part) {
-    const int C = blockIdx.x;
+    const int ch = blockIdx.x;
+    const int C = in.ch_c[ch];
     double acc[kSharedK];
 #pragma unroll
     for (int k = 0; k < kSharedK; ++k) acc[k] = 0.0;
     const int4 cv = reinterpret_cast<const int4*>(in.ctets)[C];
     const int ci[4] = {in.ciidx[cv.x], in.ciidx[cv.y], in.ciidx[cv.z], in.ciidx[cv.w]};
-    for (int p = in.anc_ptr[C] + threadIdx.x; p < in.anc_ptr[C + 1]; p += blockDim.x) {
+    for (int p = in.ch_b[ch] + threadIdx.x; p < in.ch_e[ch]; p += blockDim.x) {
         const int t = in.anc_tets[p];
         const int4 v = reinterpret_cast<const int4*>(in.tets)[t];
         TetG G;
@@ -138,19 +143,20 @@ __global__ void __launch_bounds__(kProjThreads) k_proj_shared(ProjIn in, double*
         for (int a = 0; a < 4; ++a) acc[53 + a] += mu[0][a] * y[0] + mu[1][a] * y[1] + mu[2][a] * y[2] + mu[3][a] * y[3];
         acc[57] += wt[0] * y[0] + wt[1] * y[1] + wt[2] * y[2] + wt[3] * y[3];
     }
-    block_reduce_store<kSharedK>(acc, part + size_t(C) * kStride);
+    block_reduce_store<kSharedK>(acc, part + size_t(ch) * kStride);
 }
 
 // per orbital (function y = i): A_h4 (16) b_H1 b_H3 b_H4 c_Hh d_phi rhs (6 x 4) beta1 beta3 beta4 gamma zeta_phi (5)
 __global__ void __launch_bounds__(kProjThreads) k_proj_orbital(ProjIn in, double* __restrict__ part) {
-    const int C = blockIdx.x;
+    const int ch = blockIdx.x;
+    const int C = in.ch_c[ch];
     const int i = blockIdx.y;
     double acc[kOrbK];
 #pragma unroll
     for (int k = 0; k < kOrbK; ++k) acc[k] = 0.0;
     const int4 cv = reinterpret_cast<const int4*>(in.ctets)[C];
     const int ci[4] = {in.ciidx[cv.x], in.ciidx[cv.y], in.ciidx[cv.z], in.ciidx[cv.w]};
-    for (int p = in.anc_ptr[C] + threadIdx.x; p < in.anc_ptr[C + 1]; p += blockDim.x) {
+    for (int p = in.ch_b[ch] + threadIdx.x; p < in.ch_e[ch]; p += blockDim.x) {
         const int t = in.anc_tets[p];
         const int4 v = reinterpret_cast<const int4*>(in.tets)[t];
         TetG G;
@@ -192,7 +198,7 @@ __global__ void __launch_bounds__(kProjThreads) k_proj_orbital(ProjIn in, double
         acc[47] += acc_vec(mu, E, ph, acc + 28);  // c_Hh, gamma
         acc[48] += acc_vec(mu, S, ph, acc + 32);  // d_phi, zeta_phi
     }
-    block_reduce_store<kOrbK>(acc, part + (size_t(1 + i) * in.nct + C) * kStride);
+    block_reduce_store<kOrbK>(acc, part + (size_t(1 + i) * in.nch + ch) * kStride);
 }
 
 // Wide variant for many orbitals: the orbital-independent per-tet data (mu, the element matrices of the
@@ -205,7 +211,8 @@ constexpr int kWideRec = 104;   // doubles per staged tet: mu 16, E1 E3 E4 Eone 
 
 __global__ void __launch_bounds__(kProjThreads) k_proj_orbital_wide(ProjIn in, double* __restrict__ part) {
     extern __shared__ double st[];  // kWideTets * kWideRec, reused for the final fold
-    const int C = blockIdx.x;
+    const int ch = blockIdx.x;
+    const int C = in.ch_c[ch];
     const int N = in.N;
     const int i0 = blockIdx.y * kProjThreads;
     const int NI = min(N - i0, kProjThreads);
@@ -218,7 +225,7 @@ __global__ void __launch_bounds__(kProjThreads) k_proj_orbital_wide(ProjIn in, d
     for (int k = 0; k < kOrbK; ++k) acc[k] = 0.0;
     const int4 cv = reinterpret_cast<const int4*>(in.ctets)[C];
     const int ci[4] = {in.ciidx[cv.x], in.ciidx[cv.y], in.ciidx[cv.z], in.ciidx[cv.w]};
-    const int pb = in.anc_ptr[C], pe = in.anc_ptr[C + 1];
+    const int pb = in.ch_b[ch], pe = in.ch_e[ch];
     for (int c0 = pb; c0 < pe; c0 += kWideTets) {
         const int nc = min(kWideTets, pe - c0);
         __syncthreads();
@@ -298,10 +305,10 @@ __global__ void __launch_bounds__(kProjThreads) k_proj_orbital_wide(ProjIn in, d
             const int o = e / kOrbK, k = e % kOrbK;
             double s2 = 0.0;
             for (int sl = 0; sl < TS; ++sl) s2 += st[(size_t(sl) * NI + o) * kOrbK + k];
-            part[(size_t(1 + i0 + o) * in.nct + C) * kStride + k] = s2;
+            part[(size_t(1 + i0 + o) * in.nch + ch) * kStride + k] = s2;
         }
     } else if (act) {
-        double* dst = part + (size_t(1 + i) * in.nct + C) * kStride;
+        double* dst = part + (size_t(1 + i) * in.nch + ch) * kStride;
         for (int k = 0; k < kOrbK; ++k) dst[k] = acc[k];
     }
 }
@@ -360,6 +367,20 @@ __global__ void k_coarse_scalar(int nct, int nvals, const double* __restrict__ p
     if (lane == 0) out[v] = s;
 }
 
+/// per-coarse-tet partials from the chunk partials, chunks in ascending order (deterministic)
+__global__ void k_proj_fold(int nct, int nfun, int nch, const int32_t* __restrict__ cptr,
+                            const double* __restrict__ pch, double* __restrict__ part) {
+    const int64_t total = int64_t(nfun) * nct * kStride;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+        const int k = int(e % kStride);
+        const int64_t fc = e / kStride;
+        const int C = int(fc % nct), f = int(fc / nct);
+        double s = 0.0;
+        for (int q = cptr[C]; q < cptr[C + 1]; ++q) s += pch[(size_t(f) * nch + q) * kStride + k];
+        part[e] = s;
+    }
+}
+
 }  // namespace
 
 void project_blocks(Level& L, const double* Phi, int N, int ld, const double* wt_full, const double* ell_full,
@@ -367,11 +388,16 @@ void project_blocks(Level& L, const double* Phi, int N, int ld, const double* wt
     Ctx& c = *L.ctx;
     const int nh = L.nH, nct = L.nct;
     o.ensure(nh, N, nct);
+    const int nch = L.pj_n;
+    const bool split = nch != nct;
+    if (split && o.pchunk.n < int64_t(nch) * kStride * (N + 1)) o.pchunk.alloc(int64_t(nch) * kStride * (N + 1));
+    double* dst = split ? o.pchunk.p : o.part.p;
     ProjIn in{(const int32_t*)L.tets.p, (const int32_t*)L.iidx.p, (const int32_t*)L.anc_ptr.p,
               (const int32_t*)L.anc_tets.p, (const int32_t*)L.ctets.p, (const int32_t*)L.ciidx.p,
               (const int32_t*)L.pint_col.p, (const double*)L.xyz.p, (const double*)L.pint_val.p, eext, Phi, wt_full,
-              ell_full, vxc_full, N, ld, nct};
-    launch(c, "project", k_proj_shared, nct, kProjThreads, 0, in, o.part.p);
+              ell_full, vxc_full, N, ld, nct, (const int32_t*)L.pj_c.p, (const int32_t*)L.pj_b.p,
+              (const int32_t*)L.pj_e.p, nch};
+    launch(c, "project", k_proj_shared, nch, kProjThreads, 0, in, dst);
     if (N >= kProjWideMin) {
         const size_t smem = sizeof(double) * std::max(kWideTets * kWideRec, kProjThreads * kOrbK);
         static bool attr = false;
@@ -379,11 +405,13 @@ void project_blocks(Level& L, const double* Phi, int N, int ld, const double* wt
             KSB_CUDA_CHECK(cudaFuncSetAttribute(k_proj_orbital_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
             attr = true;
         }
-        launch(c, "project", k_proj_orbital_wide, dim3(nct, ceil_div(N, kProjThreads)), kProjThreads, smem, in,
-               o.part.p);
+        launch(c, "project", k_proj_orbital_wide, dim3(nch, ceil_div(N, kProjThreads)), kProjThreads, smem, in, dst);
     } else if (N > 0) {
-        launch(c, "project", k_proj_orbital, dim3(nct, N), kProjThreads, 0, in, o.part.p);
+        launch(c, "project", k_proj_orbital, dim3(nch, N), kProjThreads, 0, in, dst);
     }
+    if (split)
+        launch(c, "project", k_proj_fold, c.sm_count * 8, 256, 0, nct, N + 1, nch, (const int32_t*)L.pj_ptr.p,
+               (const double*)o.pchunk.p, o.part.p);
 
     const int64_t fstride = int64_t(nct) * kStride;  // stride between functions in part
     const int64_t nh2 = int64_t(nh) * nh;

@@ -13,6 +13,7 @@ constexpr int kStride = 64;   // per (function, coarse tet) record in the partia
 struct ProjOut {
     int nh = 0, N = 0;
     DevBuf<double> part;
+    DevBuf<double> pchunk;       // per-chunk partials on levels whose coarse tets are split into several chunks
     DevBuf<double> shared_mats;  // A_H1, A_H3, A_H4
     DevBuf<double> A_h4;         // N x nh x nh
     DevBuf<double> shared_vecs;  // d_Hh, lift_load

@@ -103,7 +103,7 @@ void check_i32(int64_t x, const char* what) {
 
 } // namespace
 
-std::shared_ptr<FineTopology> build_topology(const Hierarchy& h, int level) {
+std::shared_ptr<FineTopology> build_topology(const Hierarchy& h, int level, bool lite) {
     auto topo = std::make_shared<FineTopology>();
     const Mesh& m = h.mesh(level);
     topo->space = std::make_shared<Space>(h.mesh_ptr(level));
@@ -221,6 +221,7 @@ std::shared_ptr<FineTopology> build_topology(const Hierarchy& h, int level) {
         }
     }
 
+    if (!lite) {
     // composite prolongation restricted to interior coarse columns (P_int), interior fine rows
     const Space& C = *topo->coarse;
     const auto& pc = h.pcol(level);
@@ -300,6 +301,8 @@ std::shared_ptr<FineTopology> build_topology(const Hierarchy& h, int level) {
             }
     }
 
+    }  // !lite
+
     // SELL-32 view of the interior pattern (column-major inside each 32-row slice)
     {
         const int ns = (ni + 31) / 32;
@@ -335,6 +338,7 @@ std::shared_ptr<FineTopology> build_topology(const Hierarchy& h, int level) {
         }
     }
 
+    if (!lite) {
     // T8 view of the interior pattern (streamed N = 16 SpMM): built when every row fits 16 slots
     {
         int wmax = 0;
@@ -492,6 +496,7 @@ std::shared_ptr<FineTopology> build_topology(const Hierarchy& h, int level) {
         std::vector<int32_t> fill(topo->anc_ptr.begin(), topo->anc_ptr.end() - 1);
         for (int t = 0; t < nt; ++t) topo->anc_tets[fill[topo->ancestor[t]]++] = t;
     }
+    }  // !lite
     if (level > 0) {
         // rows in creation order (parents precede children), accumulated like the reference's per-row map:
         // 0 + 0.5 w over the first parent's entries, then the second's; stored in ascending column order

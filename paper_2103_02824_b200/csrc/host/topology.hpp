@@ -103,6 +103,8 @@ struct FineTopology {
     std::vector<double> pstep_val;
 };
 
-std::shared_ptr<FineTopology> build_topology(const Hierarchy& h, int level);
+/// lite: only what a multigrid level needs (interior / boundary patterns, assembly gathers, diagonal, SELL-32 view,
+/// one-step prolongation); P_int, incidences, T8 / locality / stencil views and the ancestor grouping stay empty
+std::shared_ptr<FineTopology> build_topology(const Hierarchy& h, int level, bool lite = false);
 
 } // namespace ksb

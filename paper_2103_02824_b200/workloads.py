@@ -60,6 +60,64 @@ def synthetic_start(L: api.Level, ctx: api.Context, mesh: api.Mesh, centers, N: 
     return lam, dPhi, w, ld
 
 
+def orbitals_device(L: api.Level, ctx: api.Context, mesh: api.Mesh, centers, N: int, zeta: float = 1.0,
+                    ld: int | None = None):
+    """The orbital block of synthetic_start generated on the device (torch; the library's stream order is kept by
+    synchronising around it) and mass-normalised through the level's own M_ii SpMM: the same state family at any
+    size without a host-side block (cfg5: 1.2e7 x 120 doubles). Returns (Phi, ld)."""
+    import torch
+
+    it = L.index("interior")
+    cen = np.asarray(centers, np.float64).reshape(-1, 3)
+    rng = np.random.default_rng(20210304)
+    if ld is None:
+        ld = N if N == 1 else N + (N & 1)
+    ctx.sync()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    x = torch.from_numpy(np.ascontiguousarray(mesh.array("xyz")[it])).to(dev)
+    Phi = torch.zeros((len(it), ld), dtype=torch.float64, device=dev)
+    for i in range(N):
+        d = x - torch.from_numpy(cen[i % len(cen)]).to(dev)
+        f = torch.exp(-zeta * torch.linalg.vector_norm(d, dim=1))
+        if i >= len(cen):
+            f = f * (d @ torch.from_numpy(rng.standard_normal(3)).to(dev))
+        Phi[:, i] = f
+    del x
+    Y = torch.empty_like(Phi)
+    torch.cuda.synchronize()
+    dPhi = api.DeviceArray.wrap(ctx, Phi.data_ptr(), tuple(Phi.shape), keep=Phi)
+    dY = api.DeviceArray.wrap(ctx, Y.data_ptr(), tuple(Y.shape), keep=Y)
+    L.spmm(api.MAT_M, dPhi, dY, N, ld, ld)  # zero trace: |phi|_M^2 = phi_I^T M_II phi_I
+    ctx.sync()
+    nrm = (Phi[:, :N] * Y[:, :N]).sum(0)
+    Phi[:, :N] /= torch.sqrt(nrm)
+    del Y, dY
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()  # the library allocates with cudaMalloc: hand torch's cached blocks back
+    return dPhi, ld
+
+
+def hartree_of(L: api.Level, ctx: api.Context, Phi: api.DeviceArray, N: int, ld: int, tol: float = 1e-10):
+    """w for the density of Phi: multipole Dirichlet data and the exact Hartree solve (proj/src/hartree.cpp:15-144)"""
+    n = L.n
+    rho = ctx.empty((n,))
+    L.density_xc(Phi, rho, None, N=N, ld=ld)
+    mom = L.moments(rho)
+    bcb = ctx.empty((max(1, L.nb),))
+    L.boundary_values(mom, bcb)
+    w = ctx.empty((n,))
+    L.hartree_solve(Phi, bcb, w, tol=tol, N=N, ld=ld)
+    return w
+
+
+def synthetic_start_device(L: api.Level, ctx: api.Context, mesh: api.Mesh, centers, N: int, zeta: float = 1.0,
+                           lam0: float = -0.5, tol: float = 1e-10, ld: int | None = None):
+    """synthetic_start with the block generated on the device (orbitals_device) and its own Hartree potential"""
+    Phi, ld = orbitals_device(L, ctx, mesh, centers, N, zeta, ld)
+    w = hartree_of(L, ctx, Phi, N, ld, tol)
+    return np.full(N, lam0, np.float64), Phi, w, ld
+
+
 def ring_atoms(seed: int = 21):
     """BASELINE configs[3] (cfg4-like): six Z=6 on a planar ring r = 2.64 bohr and six Z=1 on the coplanar ring
     r = 4.68, a seeded angle offset, and seeded per-coordinate jitter U(-0.05, 0.05)."""
@@ -122,8 +180,10 @@ def adaptive_hierarchy(ctx: api.Context, atoms, N: int, box: float, target_dofs:
     The reference drives the marks with each level's converged solution; for cfg3-cfg5 its coarse SCF does not
     converge on the configured 8^3 mesh (profiles/r02_scf_histories.json), so the run cannot start. The indicators
     here are evaluated on every level for the seeded synthetic state of `synthetic_start` (hydrogenic orbitals at the
-    nuclei, their own Hartree potential and LDA potential), which refines where the configured molecule needs it.
-    Returns (hierarchy, meshes, finest Level or None, per-level records)."""
+    nuclei, their Hartree potential -- solved on the coarse mesh, then carried by the nested prolongation -- and LDA
+    potential), which refines where the configured molecule needs it. The finest level is the one whose vertex count
+    is nearest target_dofs (ratio-wise).
+    Returns (hierarchy, meshes, finest Level or None, per-level records, the marks of every refinement step)."""
     import time
 
     h = api.Hierarchy()
@@ -132,36 +192,61 @@ def adaptive_hierarchy(ctx: api.Context, atoms, N: int, box: float, target_dofs:
     meshes = [mesh]
     cen = [a[1:] for a in atoms]
     recs = []
+    marks = []
     L = None
+    w = None
+    level = 0
+    t0 = time.perf_counter()
+    L = api.Level(ctx, h, level)
+    L.set_system(atoms, n_pairs=N, occupancy=2.0, xc="lda")
+    L.level_ops()
+    t1 = time.perf_counter()
     for level in range(max_levels):
-        t0 = time.perf_counter()
-        L = api.Level(ctx, h, level)
-        L.set_system(atoms, n_pairs=N, occupancy=2.0, xc="lda")
-        L.level_ops()
-        t1 = time.perf_counter()
         if mesh.n_vertices >= target_dofs:
-            recs.append({"level": level, "n": L.n, "ni": L.ni, "tets": L.nt, "s_level": round(t1 - t0, 2)})
-            if log:
-                log(recs[-1])
             break
-        lam, Phi, w, ld = synthetic_start(L, ctx, mesh, cen, N, zeta=zeta, lam0=-0.5)
+        # the orbitals are regenerated on every level; the Hartree potential is solved once on the coarse mesh and
+        # carried by the nested prolongation (proj/src/driver.cpp:367-371), which keeps every level O(n)
+        Phi, ld = orbitals_device(L, ctx, mesh, cen, N, zeta)
+        lam = np.full(N, -0.5)
+        w_new = hartree_of(L, ctx, Phi, N, ld) if level == 0 else ctx.empty((L.n,))
+        if level > 0:
+            L.prolong(w, w_new, False, False)
+        w = w_new
+        ts = time.perf_counter()
         rho, vxc = ctx.empty((L.n,)), ctx.empty((L.n,))
         L.density_xc(Phi, rho, vxc, N=N, ld=ld)
         eta, tot = L.indicators(lam, Phi, w, vxc, ld=ld)
+        ti = time.perf_counter()
         marked = api.dorfler_mark(eta, tot, theta)
-        del Phi, w, rho, vxc
-        L.close()
-        L = None
+        del Phi, rho, vxc
+        import torch
+        torch.cuda.empty_cache()
         t2 = time.perf_counter()
-        mesh = mesh.adapt_refine(marked)
+        cand = mesh.adapt_refine(marked)
+        rec = {"level": level, "n": mesh.n_vertices, "tets": mesh.n_tets, "marked": int(len(marked)),
+               "s_level": round(t1 - t0, 2), "s_start": round(ts - t1, 2), "s_indicators": round(ti - ts, 2),
+               "s_mark": round(t2 - ti, 2), "s_refine": round(time.perf_counter() - t2, 2)}
+        recs.append(rec)
+        if log:
+            log(rec)
+        # stop on the level whose DOF count is nearest the target (ratio-wise)
+        if cand.n_vertices >= target_dofs and cand.n_vertices / target_dofs > target_dofs / mesh.n_vertices:
+            break
+        marks.append(marked)
+        mesh = cand
         h.push(mesh)
         meshes.append(mesh)
-        recs.append({"level": level, "n": meshes[-2].n_vertices, "tets": meshes[-2].n_tets, "marked": int(len(marked)),
-                     "s_level": round(t1 - t0, 2), "s_estimate": round(t2 - t1, 2),
-                     "s_refine": round(time.perf_counter() - t2, 2)})
-        if log:
-            log(recs[-1])
+        L.close()
+        t0 = time.perf_counter()
+        L = api.Level(ctx, h, level + 1)
+        L.set_system(atoms, n_pairs=N, occupancy=2.0, xc="lda")
+        L.level_ops()
+        t1 = time.perf_counter()
+    recs.append({"level": len(meshes) - 1, "n": L.n, "ni": L.ni, "tets": L.nt, "s_level": round(t1 - t0, 2),
+                 "final": True})
+    if log:
+        log(recs[-1])
     if not keep_last and L is not None:
         L.close()
         L = None
-    return h, meshes, L, recs
+    return h, meshes, L, recs, marks

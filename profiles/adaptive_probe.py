@@ -9,6 +9,8 @@ from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import numpy as np  # noqa: E402
 
+import torch  # noqa: E402,F401
+
 import paper_2103_02824_b200 as kb  # noqa: E402
 from paper_2103_02824_b200 import workloads  # noqa: E402
 
@@ -20,17 +22,18 @@ theta = float(sys.argv[3]) if len(sys.argv) > 3 else 0.4
 atoms = getattr(workloads, gen)()
 ctx = kb.Context(0)
 t0 = time.time()
-h, meshes, L, recs = workloads.adaptive_hierarchy(ctx, atoms, N, box, target, theta=theta,
+h, meshes, L, recs, marks = workloads.adaptive_hierarchy(ctx, atoms, N, box, target, theta=theta,
                                                   log=lambda r: print(json.dumps(r), flush=True))
 print("hierarchy_s", round(time.time() - t0, 1), "levels", len(meshes), flush=True)
 t1 = time.time()
-lam, Phi, w, ld = workloads.synthetic_start(L, ctx, meshes[-1], [a[1:] for a in atoms], N, zeta=1.0, lam0=-0.5)
+lam, Phi, w, ld = workloads.synthetic_start_device(L, ctx, meshes[-1], [a[1:] for a in atoms], N, zeta=1.0, lam0=-0.5)
 lam = np.linspace(-1.5, -0.3, N)
 print("start_s", round(time.time() - t1, 1), flush=True)
+print("mem free/total GB", [round(x / 2**30, 1) for x in torch.cuda.mem_get_info()], flush=True)
 for k in range(2):
     t2 = time.time()
     try:
-        lg = L.correction_step(lam, Phi, w, ld=ld)
+        lg = L.correction_step(lam, Phi, w, ld=ld, fixed_sweeps=10)
     except kb.KsbError as e:
         print("step error", str(e)[:300])
         break
