@@ -329,63 +329,179 @@ def correction_bench(args, ctx, stream, rank, world):
     return out
 
 
-# ----------------------------------------------------------------------------------- cfg4 / cfg5 orbital counts
-SCALE_CASES = [  # (name, generator, N, box, uniform refinements of the 8^3 coarse mesh)
-    ("cfg4-like", "ring_atoms", 21, 25.0, 3),
-    ("cfg5-like", "sphere_atoms", 120, 30.0, 4),
-]
-SCALE_SWEEPS = 10
+# ----------------------------------------------------------------------------------- configs[2..4] at their sizes
+ADAPTIVE_SWEEPS = 10  # inner sweeps per timed step: the work is defined whatever the inner dynamics do
+# parity / CPU-sample level: the finest level of the same hierarchy with at most this many vertices
+ADAPTIVE_SAMPLE_N = {"cfg3": 60000, "cfg4": 40000, "cfg5": 12000}
+ADAPTIVE_SAMPLE_SWEEPS = 3  # inner sweeps of the sample step (the oracle's dense bordered eigensolves dominate it)
+PROJ_FLOP_PER_TET_ORB = 720  # k_proj_orbital_wide: M_phi element, P^T E P (256), six E x / mu^T y / x.y (432)
 
 
-def scale_bench(args, ctx, stream, world):
-    """Correction steps at BASELINE configs[3]/[4]'s orbital counts (N = 21, 120) on uniform Kuhn levels
-    (250,047 and 2,048,383 interior DOFs) from a seeded synthetic start, with a fixed number of inner sweeps so
-    the step's work is defined whatever the inner dynamics do. The configs' own adaptive runs cannot start: the
-    reference algorithm's coarse SCF does not converge for these molecules on an 8^3 coarse mesh."""
+def fp64_peak():
+    try:
+        d = json.loads((ROOT / "profiles" / "r01_fp64_peak.json").read_text())
+        return float(d["dfma_tflops"]), "measured DFMA (profiles/micro/fp64_peak.cu)"
+    except (OSError, ValueError, KeyError):
+        return 40.0, "vendor FP64"
+
+
+def adaptive_case(name, args, ctx, stream, world, rank):
+    """One correction step (proj/src/driver.cpp:106-150) on the finest level of an estimator-driven adaptive
+    hierarchy of BASELINE configs[2..4] (workloads.adaptive_hierarchy), at the configured DOF count, from the seeded
+    device synthetic start, ADAPTIVE_SWEEPS inner sweeps. Per-phase roofline; parity and the CPU oracle's step on
+    the hierarchy's sample level; the oracle's full-size step extrapolated per phase from it."""
     import torch
 
     import paper_2103_02824_b200 as kb
+    from oracle import OMesh, Oracle
     from paper_2103_02824_b200 import workloads
-    out = []
-    for name, gen, N, box, refine in SCALE_CASES:
-        atoms = getattr(workloads, gen)()
-        h = kb.Hierarchy()
-        m = kb.Mesh.box([-box] * 3, [box] * 3, 8)
-        h.push(m)
-        for _ in range(refine):
-            m = m.uniform_refine()
-            h.push(m)
-        L = kb.Level(ctx, h, refine)
-        L.set_system(atoms, n_pairs=N, occupancy=2.0, xc="lda")
-        L.level_ops()
-        lam0, Phi, w, ld = workloads.synthetic_start(L, ctx, h.meshes[refine], [a[1:] for a in atoms], N, zeta=1.0,
-                                                     lam0=-0.5)
-        lam0 = np.linspace(-1.5, -0.3, N)
-        phi0, w0 = Phi.download(), w.download()
-        rec = {"workload": f"{name}: {len(atoms)} nuclei, N = {N}, LDA, [-{box:g},{box:g}]^3, 8^3 Kuhn coarse + "
-                           f"{refine} uniform refinements, synthetic start, {SCALE_SWEEPS} inner sweeps per step",
-               "n_interior": L.ni, "N": N, "steps": []}
-        try:
-            lam = lam0.copy()
-            L.correction_step(lam, Phi, w, ld=ld, fixed_sweeps=SCALE_SWEEPS)  # warm-up
-            Phi.upload(phi0)
-            w.upload(w0)
-            lam = lam0.copy()
-            ms = []
-            for _ in range(2):
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                lg = L.correction_step(lam, Phi, w, ld=ld, fixed_sweeps=SCALE_SWEEPS)
-                e1.record(stream)
-                torch.cuda.synchronize()
-                ms.append(e0.elapsed_time(e1))
-                rec["steps"].append({k: round(lg["ms_" + k], 3) for k in ("bvp", "hartree", "project", "inner")}
-                                    | {"cg_iterations": lg["cg_iterations"]})
-            rec["ms_per_step"] = max_over_ranks(float(np.mean(ms)), world)
-        except kb.KsbError as e:
-            rec["error"] = str(e)[:200]
-        out.append(rec)
+    gen, N, box, target = workloads.ADAPTIVE_CONFIGS[name]
+    atoms = getattr(workloads, gen)()
+    cen = [a[1:] for a in atoms]
+    t0 = time.time()
+    h, meshes, L, recs, marks = workloads.adaptive_hierarchy(ctx, atoms, N, box, target)
+    hier_s = time.time() - t0
+    rec = {"workload": f"{name} (BASELINE configs[{int(name[-1]) - 1}]): {len(atoms)} nuclei, N = {N}, LDA, "
+                       f"[-{box:g},{box:g}]^3, 8^3 Kuhn coarse, residual-indicator Doerfler (theta 0.4) adaptive "
+                       f"refinement to ~{target:.1e} DOFs (marks from the seeded synthetic state; the reference's "
+                       f"coarse SCF diverges on this mesh, profiles/r02_scf_histories.json), synthetic start, "
+                       f"{ADAPTIVE_SWEEPS} inner sweeps per step",
+           "n_dofs": L.n, "n_interior": L.ni, "n_tets": L.nt, "nnz_interior": L.nnz_ii, "N": N,
+           "levels": len(meshes), "hierarchy_s": round(hier_s, 1)}
+    lam0 = np.linspace(-1.5, -0.3, N)
+    _, Phi, w, ld = workloads.synthetic_start_device(L, ctx, meshes[-1], cen, N, zeta=1.0)
+    phi0, w0 = Phi.download(), w.download()
+    try:
+        lam = lam0.copy()
+        L.correction_step(lam, Phi, w, ld=ld, fixed_sweeps=ADAPTIVE_SWEEPS)  # warm-up (multigrid setup, caches)
+        Phi.upload(phi0)
+        w.upload(w0)
+        lam = lam0.copy()
+        ctx.reset_counters()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        lg = L.correction_step(lam, Phi, w, ld=ld, fixed_sweeps=ADAPTIVE_SWEEPS)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = max_over_ranks(e0.elapsed_time(e1), world)
+        launches = ctx.launches()
+    except kb.KsbError as e:
+        rec["error"] = str(e)[:300]
         L.close()
+        return rec
+    its = np.asarray(lg["iterations"])
+    block_its = int(its.max())
+    # per-phase roofline. BVPs (HBM): per block iteration the matrix (12 nnz + 4 (n_i + 1) + 16 n_i) plus 88 n_i per
+    # active column (SURVEY.md 8(d)'s CG-iteration bytes), summed over the columns' own iteration counts
+    bvp_bytes = block_its * (12 * L.nnz_ii + 4 * (L.ni + 1) + 16 * L.ni) + 88 * L.ni * int(its.sum())
+    peak, peak_kind = measured_peak()
+    fpk, fp_kind = fp64_peak()
+    proj_flop = PROJ_FLOP_PER_TET_ORB * N * L.nt
+    rec.update({
+        "ms_per_step": ms, "gpu_launches": launches,
+        "phases_ms": {k: round(lg["ms_" + k], 3) for k in ("bvp", "hartree", "project", "inner")},
+        "cg_iterations": lg["cg_iterations"], "block_iterations": block_its,
+        "shift_attempts": {str(a): int((np.asarray(lg["attempts"]) == a).sum()) for a in (-1, 0, 1, 2, 3)},
+        "hartree_iterations": lg["hartree_iterations"], "inner_sweeps": lg["inner_iterations"],
+        "roofline": {"bound": "hbm", "phase": "bvp (multi-column CG, CSR SpMM)",
+                     "achieved": bvp_bytes / (lg["ms_bvp"] * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                     "frac": bvp_bytes / (lg["ms_bvp"] * 1e-3) / 1e9 / peak, "traffic": None,
+                     "bytes": bvp_bytes, "peak_kind": peak_kind},
+        "roofline_project": {"bound": "fp64", "achieved": proj_flop / (lg["ms_project"] * 1e-3) / 1e12,
+                             "peak": fpk, "unit": "TFLOP/s",
+                             "frac": proj_flop / (lg["ms_project"] * 1e-3) / 1e12 / fpk, "peak_kind": fp_kind,
+                             "flop": proj_flop},
+        "lambda_after": [float(x) for x in lam[:4]],
+    })
+    # end to end: host orbitals / potential in and out of the step (pinned host buffers)
+    del Phi
+    torch.cuda.empty_cache()
+    hphi = torch.empty(phi0.shape, dtype=torch.float64, pin_memory=True)
+    hw = torch.empty(w0.shape, dtype=torch.float64, pin_memory=True)
+    hphi.numpy()[:] = phi0
+    hw.numpy()[:] = w0
+    lam_h = lam0.copy()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    try:
+        L.correction_step_host(lam_h, hphi.numpy(), hw.numpy(), fixed_sweeps=ADAPTIVE_SWEEPS)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        rec["e2e"] = {"ms_per_step": max_over_ranks(e0.elapsed_time(e1), world),
+                      "h2d_bytes_per_step": phi0.nbytes + w0.nbytes, "d2h_bytes_per_step": phi0.nbytes + w0.nbytes}
+    except kb.KsbError as e:
+        rec["e2e"] = {"error": str(e)[:200]}
+    del hphi, hw
+    L.close()
+
+    # parity and the CPU sample: the same hierarchy's level kp, device step vs oracle step from the same state
+    kp = max(k for k, m in enumerate(meshes) if m.n_vertices <= ADAPTIVE_SAMPLE_N[name])
+    Lk = kb.Level(ctx, h, kp)
+    Lk.set_system(atoms, n_pairs=N, occupancy=2.0, xc="lda")
+    Lk.level_ops()
+    _, Pk, wk, ldk = workloads.synthetic_start_device(Lk, ctx, meshes[kp], cen, N, zeta=1.0)
+    it = Lk.index("interior")
+    orb = np.zeros((Lk.n, N))
+    orb[it] = Pk.download()[:, :N]
+    wk0 = wk.download()
+    lam_d = lam0.copy()
+    lgk = Lk.correction_step(lam_d, Pk, wk, ld=ldk, fixed_sweeps=ADAPTIVE_SAMPLE_SWEEPS)
+    par = {"level": kp, "n_dofs": Lk.n, "N": N, "inner_sweeps": ADAPTIVE_SAMPLE_SWEEPS}
+    if rank == 0 and not args.no_cpu:
+        os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count() or 1))
+        orc = Oracle(atoms, n_pairs=N, occ=2.0, xc="lda")
+        om = OMesh.box([-box] * 3, [box] * 3, 8)
+        orc.push(om)
+        for j in range(kp):
+            om = om.adapt_refine(marks[j])
+            orc.push(om)
+        t1 = time.time()
+        lam_o, orb_o, w_o, lo = orc.correction_step(kp, lam0.copy(), orb, wk0, fixed_sweeps=ADAPTIVE_SAMPLE_SWEEPS)
+        cpu_s = time.time() - t1
+        P = Pk.download()[:, :N]
+        O = orb_o[it]
+        rho_g, rho_o = 2.0 * (P ** 2).sum(1), 2.0 * (O ** 2).sum(1)
+        gaps = [min(abs(lam_o[i] - lam_o[j]) for j in range(N) if j != i) for i in range(N)]
+        orb_err = max((np.linalg.norm(np.sign(P[:, i] @ O[:, i]) * P[:, i] - O[:, i]) / np.linalg.norm(O[:, i])
+                       for i in range(N) if gaps[i] > 1e-3), default=0.0)
+        par.update({
+            "mesh_bitexact": bool(np.array_equal(om.array("tets"), meshes[kp].array("tets"))),
+            "lambda_max_rel": float(np.abs(lam_d - lam_o).max() / np.abs(lam_o).max()),
+            "rho_rel": float(np.linalg.norm(rho_g - rho_o) / np.linalg.norm(rho_o)),
+            "w_rel": float(np.linalg.norm(wk.download() - w_o) / np.linalg.norm(w_o)),
+            "orbital_max_rel": float(orb_err), "attempts_equal": lgk["attempts"] == lo["attempts"],
+            "tol": {"lambda": 1e-8, "rho_w_orbitals": 1e-6}})
+        par["ok"] = bool(par["mesh_bitexact"] and par["lambda_max_rel"] <= 1e-8 and par["rho_rel"] <= 1e-6
+                         and par["w_rel"] <= 1e-6 and par["orbital_max_rel"] <= 1e-6)
+        # oracle's full-size step, extrapolated per phase from the sample level: vector phases by the tet / DOF
+        # ratio (the BVPs also by the device's block-CG iteration ratio), the coarse inner loop as measured
+        r_n, r_t = rec["n_dofs"] / Lk.n, rec["n_tets"] / Lk.nt
+        r_it = block_its / max(1, int(np.asarray(lgk["iterations"]).max()))
+        ext = {"bvp": lo["t_bvp"] * r_n * r_it, "hartree": lo["t_hartree"] * r_n, "project": lo["t_blocks"] * r_t,
+               "inner": lo["t_inner"] * ADAPTIVE_SWEEPS / ADAPTIVE_SAMPLE_SWEEPS}
+        rec["cpu_baseline"] = {
+            "ms_per_step": 1e3 * sum(ext.values()), "kind": "port", "cores": os.cpu_count() or 1,
+            "extrapolated": True, "phases_ms": {k: round(1e3 * v, 1) for k, v in ext.items()},
+            "sample": f"oracle correction step on level {kp} of the same hierarchy ({Lk.n} DOFs, {cpu_s:.1f} s, "
+                      f"SGS-PCG, {ADAPTIVE_SAMPLE_SWEEPS} inner sweeps), phases scaled to {rec['n_dofs']} DOFs: BVPs "
+                      f"x DOF ratio {r_n:.0f} x device block-CG iteration ratio {r_it:.2f}, Hartree x DOF ratio "
+                      f"(iteration growth ignored: a lower bound), projection x tet ratio, inner loop x "
+                      f"{ADAPTIVE_SWEEPS}/{ADAPTIVE_SAMPLE_SWEEPS} sweeps (its size does not depend on the level)"}
+    rec["parity_sample"] = par
+    Lk.close()
+    return rec
+
+
+def adaptive_bench(args, ctx, stream, world, rank):
+    out = {}
+    for name in ("cfg3", "cfg4", "cfg5"):
+        try:
+            out[name] = adaptive_case(name, args, ctx, stream, world, rank)
+        except Exception as e:  # noqa: BLE001 -- a failed section is reported, the bench line still prints
+            out[name] = {"error": f"{type(e).__name__}: {str(e)[:300]}"}
+        import torch
+        torch.cuda.empty_cache()
     return out
 
 
@@ -517,7 +633,7 @@ def run_b200(args, world, rank, local):
 
     correction = correction_bench(args, ctx, stream, rank, world)
     cfg1_run = cfg1_run_bench(args, ctx, rank, world)
-    scale = None if args.no_scale else scale_bench(args, ctx, stream, world)
+    adaptive = None if args.no_adaptive else adaptive_bench(args, ctx, stream, world, rank)
 
     parity = None
     if rank == 0 and not args.no_parity:
@@ -570,7 +686,7 @@ def run_b200(args, world, rank, local):
             "parity": parity,
             "correction_step": correction,
             "cfg1_run": cfg1_run,
-            "scale": scale,
+            "adaptive": adaptive,
         }
         print(json.dumps(line), flush=True)
     L.close()
@@ -588,7 +704,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-iters", type=int, default=96, help="CPU oracle sample: iterations per 16-column block")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-scale", action="store_true", help="skip the N = 21 / 120 correction-step section")
+    ap.add_argument("--no-adaptive", "--no-scale", dest="no_adaptive", action="store_true",
+                    help="skip the configs[2..4] section (adaptive hierarchies to 1e6 / 4e6 / 1.2e7 DOFs)")
     ap.add_argument("--no-parity", action="store_true", help="skip the oracle check of the timed cfg2 result")
     args = ap.parse_args()
     world, rank, local = dist_init()

@@ -411,8 +411,10 @@ class Level:
         rho, w = self.ctx.empty((self.n,)), self.ctx.empty((self.n,))
         it = C.c_int()
         hist = np.zeros(max(1, int(max_iterations)))
-        check(lib.ksb_coarse_scf(self._h, C.byref(o), _dp(lam), Phi.ptr, ld, rho.ptr, w.ptr, C.byref(it), _dp(hist),
-                                 len(hist)))
+        st = lib.ksb_coarse_scf(self._h, C.byref(o), _dp(lam), Phi.ptr, ld, rho.ptr, w.ptr, C.byref(it), _dp(hist),
+                                len(hist))
+        self.last_scf_history = hist[:it.value].copy()  # kept when the iteration fails (the error is raised below)
+        check(st)
         return lam, Phi, rho, w, it.value, hist[:it.value]
 
     def correction_step(self, lambdas: np.ndarray, Phi: DeviceArray, w: DeviceArray, ld: int | None = None, **opts):

@@ -772,10 +772,10 @@ int ksb_coarse_scf(ksb_level* l, const ksb_scf_opts* o, double* h_lambda, double
         } catch (...) {
             err = std::current_exception();
         }
-        if (iters) *iters = st.iterations;
+        if (iters) *iters = err ? int(K.scf_history.size()) : st.iterations;
+        if (hist)  // also when the cap was hit: the history says whether the iteration oscillates or creeps
+            for (int k = 0; k < std::min<int>(cap, int(K.scf_history.size())); ++k) hist[k] = K.scf_history[k];
         if (err) std::rethrow_exception(err);
-        if (hist)
-            for (int k = 0; k < std::min<int>(cap, int(st.history.size())); ++k) hist[k] = st.history[k];
     });
 }
 
@@ -1093,20 +1093,7 @@ int ksb_dorfler_mark(const double* eta, int64_t nt, double total_sq, double thet
         if (!(theta > 0.0) || theta >= 1.0) ksb::raise(KSB_INVALID_ARGUMENT, "theta must lie in (0,1)");
         *n_marked = 0;
         if (total_sq <= 0.0) return;
-        std::vector<int32_t> order(static_cast<size_t>(nt));
-        for (int64_t i = 0; i < nt; ++i) order[size_t(i)] = int32_t(i);
-        std::sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
-            if (eta[a] != eta[b]) return eta[a] > eta[b];
-            return a < b;
-        });
-        double acc = 0.0;
-        int64_t k = 0;
-        for (int32_t t : order) {
-            marked[k++] = t;
-            acc += eta[t];
-            if (acc >= theta * total_sq) break;
-        }
-        *n_marked = k;
+        *n_marked = ksb::dorfler_mark(eta, nt, total_sq, theta, marked);
     });
 }
 

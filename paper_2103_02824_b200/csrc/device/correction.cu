@@ -573,6 +573,7 @@ ScfStats coarse_scf(Level& L, Corrector& K, CgWork& cg, const ScfParams& p, doub
     if (!K.ops_ready) level_ops(L, K);
     const int n = L.n, ni = L.ni, N = K.sys.N;
     if (ni != L.nH) raise(KSB_INVALID_ARGUMENT, "the coarse self-consistent solve runs on level 0");
+    K.scf_history.clear();
     need(K.rho_t, n);
     need(K.vxc, n);
     need(K.what_full, n);
@@ -628,6 +629,7 @@ ScfStats coarse_scf(Level& L, Corrector& K, CgWork& cg, const ScfParams& p, doub
                    (const int32_t*)L.boundary.p, (const double*)K.wtil_int.p, (const double*)K.bcb.p, d_w);
         }
         KSB_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+        K.scf_history = st.history;
         if (delta < p.tol && iter >= 2) return st;
     }
     std::string msg = "self-consistent iteration exceeded " + std::to_string(p.max_iterations) +

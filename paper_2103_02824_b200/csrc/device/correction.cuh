@@ -54,6 +54,7 @@ struct Corrector {
     DevBuf<double> colscale;    // per-column right-hand-side scales of the orbital solves
     DevBuf<double> potf, wscr;  // standard MLC: w + v_xc (full), scratch w of expand
     DevBuf<int> idx;
+    std::vector<double> scf_history;  // density changes of the last coarse_scf, kept when it fails (diagnostics)
     int ldT = 0;
     int mlc_ld = 0, mlc_sweeps = 0;  // standard MLC state: ld of PhiT, sweeps run
     EstimatorData est;

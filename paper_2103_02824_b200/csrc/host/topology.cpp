@@ -2,6 +2,7 @@
 #include "topology.hpp"
 
 #include <algorithm>
+#include <parallel/algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <limits>
@@ -546,6 +547,24 @@ std::shared_ptr<FineTopology> build_topology(const Hierarchy& h, int level, bool
         }
     }
     return topo;
+}
+
+int64_t dorfler_mark(const double* eta, int64_t nt, double total_sq, double theta, int32_t* marked) {
+    std::vector<int32_t> order(static_cast<size_t>(nt));
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < nt; ++i) order[size_t(i)] = int32_t(i);
+    __gnu_parallel::sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
+        if (eta[a] != eta[b]) return eta[a] > eta[b];
+        return a < b;
+    });
+    double acc = 0.0;
+    int64_t k = 0;
+    for (int32_t t : order) {
+        marked[k++] = t;
+        acc += eta[t];
+        if (acc >= theta * total_sq) break;
+    }
+    return k;
 }
 
 } // namespace ksb

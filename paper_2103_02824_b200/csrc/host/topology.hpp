@@ -107,4 +107,9 @@ struct FineTopology {
 /// one-step prolongation); P_int, incidences, T8 / locality / stencil views and the ancestor grouping stay empty
 std::shared_ptr<FineTopology> build_topology(const Hierarchy& h, int level, bool lite = false);
 
+/// est::dorfler_mark (proj/src/estimator.cpp:87-104): tets by descending eta, ties by lower index, up to the first
+/// cumulative sum >= theta * total; writes them to `marked` in that order and returns their count. The order is a
+/// strict total order, so the parallel sort gives the reference's sequence exactly.
+int64_t dorfler_mark(const double* eta, int64_t nt, double total_sq, double theta, int32_t* marked);
+
 } // namespace ksb

@@ -74,3 +74,22 @@ def test_indicators_match_oracle(ctx, which):
     assert np.abs(eta_g - eta_o).max() <= 1e-11 * eta_o.max()
     assert abs(tot_g - tot_o) <= 1e-12 * tot_o
     assert np.array_equal(kb.dorfler_mark(eta_g, tot_g, 0.4), o_mark(eta_o, tot_o, 0.4))
+
+
+def test_dorfler_mark_large_with_ties_matches_sequential_rule():
+    """the parallel sort inside ksb_dorfler_mark keeps the reference's sequence (proj/src/estimator.cpp:92-102):
+    descending eta, ties by lower index, up to the first cumulative sum >= theta * total"""
+    import paper_2103_02824_b200 as kb
+    rng = np.random.default_rng(11)
+    eta = np.round(rng.exponential(1.0, 300_000), 2)  # many exact ties
+    tot = float(eta.sum())
+    for theta in (0.1, 0.4, 0.9):
+        got = kb.dorfler_mark(eta, tot, theta)
+        order = np.lexsort((np.arange(len(eta)), -eta))
+        acc, k = 0.0, 0
+        for t in order:
+            k += 1
+            acc += eta[t]
+            if acc >= theta * tot:
+                break
+        assert np.array_equal(got, order[:k].astype(np.int32))
