@@ -608,7 +608,9 @@ def run_b200(args, world, rank, local):
     bytes_spmm = 12 * L.nnz_ii + 4 * (ni + 1) + 16 * ni * N_RHS
     dia = L.index("dia")
     stencil = dia[0] > 0 and os.environ.get("KSB_SPMM_DIA") != "0"
-    spmm_kernel = "k_spmm_dia_tv" if stencil else "k_spmm_t8"
+    grid_lvl = stencil and dia[15] > 0 and os.environ.get("KSB_DIA_ZT") != "0"
+    spmm_kernel = ("k_spmm_dia_zw" if os.environ.get("KSB_DIA_ZW") != "0" else "k_spmm_dia_zt") if grid_lvl else \
+        "k_spmm_dia_tv" if stencil else "k_spmm_t8"
     n_diag = 3 + (int(dia[0]) - 1) * int(dia[2]) if stencil else 0
     bytes_format = 8 * n_diag * ni + 16 * ni * N_RHS if stencil else bytes_spmm
     achieved = bytes_spmm / (spmm_avg * 1e-3) / 1e9

@@ -26,12 +26,13 @@ struct StepOptions {
     int nev_scan_pad = 4;
     bool hartree = true;
     bool xc = true;
+    bool norm_l1 = false;  // density change in L1 instead of H1 (RunConfig::outer_norm_l1)
 };
 
 struct StepLog {
     int inner_iterations = 0;
     int hartree_iterations = 0;
-    double delta = 0;  // H1 norm of the density change
+    double delta = 0;  // H1 (L1 with norm_l1) norm of the density change
     double ms_bvp = 0, ms_hartree = 0, ms_project = 0, ms_inner = 0, ms_total = 0;
     std::vector<int> attempts, cg_iterations;
 };
@@ -98,6 +99,7 @@ struct RunConfig {
     double score_floor = 1e-8;
     int nev_scan_pad = 4;
     bool uniform = false;
+    bool outer_norm_l1 = false;  // density-change norm: H1 unless set (proj/include/ksafem/runconfig.hpp:32)
     Mode mode = Mode::accelerated;
 };
 

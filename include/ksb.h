@@ -163,7 +163,8 @@ typedef struct {
     double tol;            /* relative residual (SolverOptions::tol, default 1e-9) */
     int max_iterations;    /* SolverOptions::max_iterations (default 20000) */
     int fixed_iterations;  /* >0: run exactly this many iterations, no stopping test (benchmark) */
-    int precond;           /* 0 = Jacobi (default) */
+    int precond;           /* 0 = Jacobi (default, fused); 1 = the reference's exact SGS (solver.cpp:50-55), level-scheduled
+                              triangular solves, host-driven iterations: parity runs, no fixed-iteration mode */
     int check_every;       /* host polls convergence flags every k iterations (default 8) */
 } ksb_cg_opts;
 
@@ -208,12 +209,15 @@ typedef struct {
     int nev_pad;        /* RunConfig::nev_scan_pad (4) */
     int check_every;    /* CG convergence poll interval */
     int fixed_sweeps;   /* > 0: inner loop runs exactly this many sweeps (diagnostics), else 0 */
+    int norm_l1;        /* density change in L1 instead of H1 (RunConfig::outer_norm_l1, runconfig.hpp:32) */
+    int precond;        /* 0: Jacobi orbital BVPs + multigrid Hartree (default); 1: the reference's exact SGS
+                           (solver.cpp:50-55) in every linear solve of the step -- parity runs */
 } ksb_step_opts;
 
 typedef struct {
     int inner_iterations;
     int hartree_iterations;
-    double delta; /* H1 norm of the density change (the outer stopping quantity) */
+    double delta; /* H1 (or, with norm_l1, L1) norm of the density change (the outer stopping quantity) */
     double ms_bvp, ms_hartree, ms_project, ms_inner, ms_total;
     int64_t cg_iterations; /* summed over orbitals and shift attempts */
 } ksb_step_log;
@@ -262,6 +266,7 @@ typedef struct {
     double mixing;       /* RunConfig::mixing (0.3) */
     int hartree_on, xc_on;
     double tol_eig;      /* Hartree solve tolerance (RunConfig::tol_eig, 1e-9) */
+    int norm_l1;         /* density change in L1 instead of H1 (scf::Options::norm_l1, scf.hpp:19) */
 } ksb_scf_opts;
 int ksb_scf_defaults(ksb_scf_opts* o);
 int ksb_coarse_scf(ksb_level* l, const ksb_scf_opts* o, double* h_lambda, double* d_Phi, int ld, double* d_rho_full,
@@ -330,6 +335,9 @@ int ksb_dorfler_mark(const double* h_eta, int64_t n_tets, double total_sq, doubl
                      int64_t* h_n_marked);
 /* l2_norm^2, h1_seminorm^2, h1_norm of a full-length nodal function (proj/src/assembly.cpp:251-287) */
 int ksb_norms(ksb_level* l, const double* d_f_full, double h_out[3]);
+/* fem::l1_norm of a full-length nodal function: integral of |f| by the Keast rule (proj/src/assembly.cpp:234-249,
+ * 289-291) */
+int ksb_l1_norm(ksb_level* l, const double* d_f_full, double* h_out);
 /* model::total_energy (proj/src/ks_model.cpp:107-143): kinetic, external, hartree, xc, total */
 int ksb_energy(ksb_level* l, const double* d_Phi, int N, int ld, const double* d_w_full, double h_out[5]);
 

@@ -65,6 +65,7 @@ _PROTO = {
     "orc_last_scf_history": (I, [P, DP, IP]),
     "orc_dorfler": (I, [DP, I64, D, D, IP, C.POINTER(C.c_int64)]),
     "orc_norms": (I, [P, I, DP, DP]),
+    "orc_l1_norm": (I, [P, I, DP, DP]),
     "orc_prolong_vec": (I, [P, I, I, DP, I, DP]),
     "orc_coarse_scf": (I, [P, D, I, D, D, DP, DP, DP, IP]),
     "orc_correction_step": (I, [P, I, DP, IP, DP, DP, DP, IP, DP]),
@@ -294,6 +295,11 @@ class Oracle:
         out = np.empty(3)
         _chk(lib.orc_norms(self._h, level, dp(f64(f)), dp(out)))
         return out
+
+    def l1_norm(self, level, f):
+        out = C.c_double()
+        _chk(lib.orc_l1_norm(self._h, level, dp(f64(f)), C.byref(out)))
+        return out.value
 
     def prolongation_matrix(self, frm, to):
         import scipy.sparse as sp

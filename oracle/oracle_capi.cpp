@@ -438,6 +438,13 @@ int orc_norms(orc_problem* p, int level, const double* f, double* out) {
         out[2] = h1_norm(V, x);
     });
 }
+/// fem::l1_norm (proj/src/assembly.cpp:289-291)
+int orc_l1_norm(orc_problem* p, int level, const double* f, double* out) {
+    return guard([&] {
+        const Space& V = p->p.space(level);
+        *out = l1_norm(V, Vec(f, f + V.n()));
+    });
+}
 int orc_prolong_vec(orc_problem* p, int from, int to, const double* in, int N, double* out) {
     return guard([&] {
         const auto cols = unpack(in, p->p.space(from).n(), N);

@@ -653,6 +653,22 @@ double h1_norm(const Space& V, const Vec& f) {
     return std::sqrt(a * a + b * b);
 }
 
+// proj/src/assembly.cpp:234-249 (integrate_of) with g = |v|, proj/src/assembly.cpp:289-291 (l1_norm)
+double l1_norm(const Space& V, const Vec& f) {
+    const Mesh& m = *V.mesh;
+    const auto& rule = keast();
+    double s = 0;
+    for (int t = 0; t < m.nt(); ++t) {
+        const Geo g = tet_geo(m, t);
+        const auto& v = m.tets[t];
+        for (const auto& q : rule) {
+            const double val = q.b[0] * f[v[0]] + q.b[1] * f[v[1]] + q.b[2] * f[v[2]] + q.b[3] * f[v[3]];
+            s += q.w * g.vol * std::abs(val);
+        }
+    }
+    return s;
+}
+
 // proj/src/assembly.cpp:311-324
 Csc interior_block(const Csc& A, const Space& V) {
     std::vector<Trip> t;

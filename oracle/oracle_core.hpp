@@ -130,6 +130,7 @@ Vec load_nodal(const Space& V, const Vec& f);
 double l2_norm(const Space& V, const Vec& f);
 double h1_seminorm(const Space& V, const Vec& f);
 double h1_norm(const Space& V, const Vec& f);
+double l1_norm(const Space& V, const Vec& f);
 Csc interior_block(const Csc& A, const Space& V);
 
 // ------------------------------------------------------------------ solver (proj/src/solver.cpp)

@@ -40,12 +40,13 @@ class CgStats(C.Structure):
 
 class StepOpts(C.Structure):
     _fields_ = [("tol_linear", D), ("tol_inner", D), ("score_floor", D), ("max_inner", I), ("nev_pad", I),
-                ("check_every", I), ("fixed_sweeps", I)]
+                ("check_every", I), ("fixed_sweeps", I), ("norm_l1", I),
+                ("precond", I)]
 
 
 class ScfOpts(C.Structure):
     _fields_ = [("tol", C.c_double), ("max_iterations", C.c_int), ("mixing", C.c_double), ("hartree_on", C.c_int),
-                ("xc_on", C.c_int), ("tol_eig", C.c_double)]
+                ("xc_on", C.c_int), ("tol_eig", C.c_double), ("norm_l1", C.c_int)]
 
 
 class StepLog(C.Structure):
@@ -134,6 +135,7 @@ PROTOTYPES = {
     "ksb_inner_scf": (I, [P, SOP, DP, DP, DP, DP, DP, DP, IP, DP, I]),
     "ksb_expand": (I, [P, P, I, P, P, P, P]),
     "ksb_norms": (I, [P, P, DP]),
+    "ksb_l1_norm": (I, [P, P, DP]),
     "ksb_energy": (I, [P, P, I, I, P, DP]),
 }
 

@@ -332,13 +332,15 @@ class Level:
         check(lib.ksb_spmm(self._h, mat, X.ptr, int(N), int(ldx or N), Y.ptr, int(ldy or N)))
 
     @staticmethod
-    def cg_options(tol=1e-9, max_iterations=20000, fixed_iterations=0, check_every=8) -> _N.CgOpts:
+    def cg_options(tol=1e-9, max_iterations=20000, fixed_iterations=0, check_every=8, precond=0) -> _N.CgOpts:
+        """precond 0: Jacobi (the fused production CG); 1: the reference's exact SGS (parity runs)"""
         o = _N.CgOpts()
         check(lib.ksb_cg_defaults(C.byref(o)))
         o.tol = tol
         o.max_iterations = max_iterations
         o.fixed_iterations = fixed_iterations
         o.check_every = check_every
+        o.precond = precond
         return o
 
     def cg_solve(self, mat: int, B: DeviceArray, X: DeviceArray, N: int, ld: int | None = None, opts=None,
@@ -398,12 +400,13 @@ class Level:
                 "ms_inner": lg.ms_inner, "ms_total": lg.ms_total, "cg_iterations": int(lg.cg_iterations),
                 "attempts": att.tolist(), "iterations": its.tolist()}
 
-    def coarse_scf(self, tol=1e-6, max_iterations=200, mixing=0.3, hartree=True, xc=True, tol_eig=1e-9):
+    def coarse_scf(self, tol=1e-6, max_iterations=200, mixing=0.3, hartree=True, xc=True, tol_eig=1e-9, norm_l1=False):
         """scf::self_consistent_solve on level 0 (proj/src/scf.cpp:22-90): (lambdas, Phi, rho, w, iterations, history)."""
         o = _N.ScfOpts()
         check(lib.ksb_scf_defaults(C.byref(o)))
         o.tol, o.max_iterations, o.mixing = float(tol), int(max_iterations), float(mixing)
         o.hartree_on, o.xc_on, o.tol_eig = int(hartree), int(xc), float(tol_eig)
+        o.norm_l1 = int(norm_l1)
         N = self.N
         ld = N if N == 1 else N + (N & 1)
         lam = np.empty(N)
@@ -555,6 +558,12 @@ class Level:
         out = np.empty(3)
         check(lib.ksb_norms(self._h, f.ptr, _dp(out)))
         return out
+
+    def l1_norm(self, f: DeviceArray) -> float:
+        """fem::l1_norm (proj/src/assembly.cpp:289-291) of a full-length nodal function"""
+        out = C.c_double()
+        check(lib.ksb_l1_norm(self._h, f.ptr, C.byref(out)))
+        return out.value
 
     def energy(self, Phi: DeviceArray, w: DeviceArray, N=None, ld=None) -> np.ndarray:
         out = np.empty(5)

@@ -578,9 +578,11 @@ int ksb_cg_defaults(ksb_cg_opts* o) {
 static void run_cg(ksb_level* l, int mat, int shift_mat, const double* h_sigma, const double* d_B, double* d_X, int N,
                    int ld, const ksb_cg_opts* o, ksb_cg_stats* h_stats) {
     need(l && d_B && d_X && o, "null argument");
-    if (o->precond != 0) ksb::raise(KSB_INVALID_ARGUMENT, "only the Jacobi preconditioner is available");
+    if (o->precond != 0 && o->precond != 1)
+        ksb::raise(KSB_INVALID_ARGUMENT, "precond must be 0 (Jacobi) or 1 (the reference's SGS)");
     if (mat < 0 || mat >= ksb::kMaxMats || (shift_mat >= ksb::kMaxMats)) ksb::raise(KSB_INVALID_ARGUMENT, "bad matrix id");
     ksb::CgOptions co;
+    co.precond = o->precond;
     co.tol = o->tol;
     co.max_iterations = o->max_iterations;
     co.fixed_iterations = o->fixed_iterations;
@@ -632,7 +634,9 @@ int ksb_solve(ksb_level* l, int mat, const double* d_b_full, const double* d_bc_
         if (mat < 0 || mat >= ksb::kMaxMats) ksb::raise(KSB_INVALID_ARGUMENT, "bad matrix id");
         ksb::CgOptions co;
         if (o) {
-            if (o->precond != 0) ksb::raise(KSB_INVALID_ARGUMENT, "only the Jacobi preconditioner is available");
+            if (o->precond != 0 && o->precond != 1)
+                ksb::raise(KSB_INVALID_ARGUMENT, "precond must be 0 (Jacobi) or 1 (the reference's SGS)");
+            co.precond = o->precond;
             co.tol = o->tol;
             co.max_iterations = o->max_iterations;
             co.fixed_iterations = o->fixed_iterations;
@@ -667,6 +671,9 @@ static ksb::StepOptions step_opts(const ksb_step_opts* o) {
         so.nev_pad = o->nev_pad;
         so.check_every = o->check_every;
         so.fixed_sweeps = o->fixed_sweeps;
+        so.norm_l1 = o->norm_l1 != 0;
+        if (o->precond < 0 || o->precond > 1) ksb::raise(KSB_INVALID_ARGUMENT, "precond must be 0 or 1");
+        so.precond = o->precond;
     }
     return so;
 }
@@ -707,6 +714,8 @@ int ksb_step_defaults(ksb_step_opts* o) {
         o->nev_pad = 4;
         o->check_every = 8;
         o->fixed_sweeps = 0;
+        o->norm_l1 = 0;
+        o->precond = 0;
     });
 }
 
@@ -749,6 +758,7 @@ int ksb_scf_defaults(ksb_scf_opts* o) {
         o->hartree_on = 1;
         o->xc_on = 1;
         o->tol_eig = 1e-9;
+        o->norm_l1 = 0;
     });
 }
 
@@ -765,6 +775,7 @@ int ksb_coarse_scf(ksb_level* l, const ksb_scf_opts* o, double* h_lambda, double
         p.hartree_on = o->hartree_on != 0;
         p.xc_on = o->xc_on != 0;
         p.tol_eig = o->tol_eig;
+        p.norm_l1 = o->norm_l1 != 0;
         ksb::ScfStats st;
         std::exception_ptr err;
         try {
@@ -1105,6 +1116,13 @@ int ksb_norms(ksb_level* l, const double* d_f, double out[3]) {
         out[1] = a[1];
         const double l2 = std::sqrt(std::max(0.0, a[0])), semi = std::sqrt(std::max(0.0, a[1]));
         out[2] = std::sqrt(l2 * l2 + semi * semi);
+    });
+}
+
+int ksb_l1_norm(ksb_level* l, const double* d_f, double* h_out) {
+    return guard([&] {
+        need(l && d_f && h_out, "null argument");
+        *h_out = ksb::l1_norm(l->L, d_f, l->corr().phys);
     });
 }
 

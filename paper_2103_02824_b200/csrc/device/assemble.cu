@@ -268,7 +268,9 @@ __global__ void k_dia_pack(int ni, DiaGeom dg, int D, int wg, const int32_t* __r
             for (int e = 0; e < D; ++e)
                 if (dg.off[e] == o) d = e;
             if (d >= 0)
-                out[wg == kDiaLine ? dia_line_pos(r, d, D, dg.n) : dia_pos(r, d, D, wg)] = csr[map ? map[k] : k];
+                out[wg == kDiaZT     ? dia_zt_pos(r, d, D, dg.n)
+                    : wg == kDiaLine ? dia_line_pos(r, d, D, dg.n)
+                                     : dia_pos(r, d, D, wg)] = csr[map ? map[k] : k];
         }
     }
 }
@@ -279,8 +281,11 @@ const double* Level::dia_values(int id, int wg) {
     if (dia_ng == 0) return nullptr;
     if (M.dia_version != M.version || M.dia_wg != wg) {
         const DiaGeom dg = dia_geom(*this);
-        if (wg == kDiaLine && dg.n == 0) raise(KSB_INTERNAL, "line-tiled stencil layout on a level without a grid");
-        const int64_t need = wg == kDiaLine ? dia_line_size(dg.n, dg.D) : dia_size(ni, dg.D, wg);
+        if ((wg == kDiaLine || wg == kDiaZT) && dg.n == 0)
+            raise(KSB_INTERNAL, "grid-tiled stencil layout on a level without a grid");
+        const int64_t need = wg == kDiaZT     ? dia_zt_size(dg.n, dg.D)
+                             : wg == kDiaLine ? dia_line_size(dg.n, dg.D)
+                                              : dia_size(ni, dg.D, wg);
         if (M.dia.n < need) M.dia.alloc(need);
         KSB_CUDA_CHECK(cudaMemsetAsync(M.dia.p, 0, sizeof(double) * need, ctx->stream));
         const int32_t* ptr = dia_lo ? lo_ptr.p : ii_ptr.p;

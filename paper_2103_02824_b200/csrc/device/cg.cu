@@ -1100,6 +1100,466 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_spmm_dia_z(int ni, Cols cc, D
     k1_epilogue(sm, N, cc, s);
 }
 
+// ---------------- K1 (stencil, TMA-staged z-marching, N = 16): the cfg2 kernel ----------------
+constexpr int kZtSlots = 4;                  // plane slots: z - 1, z, z + 1 in use, z + 2 in flight
+constexpr int kZtH = kZtT + 2;               // tile plus a one-row / one-line halo
+constexpr int kZtRows = kZtH * kZtH;
+
+inline size_t dia_zt_smem(int D) {
+    return sizeof(double) * (size_t(kZtSlots) * kZtRows * 16 + 2 * size_t(kZtT) * kZtT * D) + 8 * sizeof(uint64_t) +
+           sizeof(double) * 8 * 16;
+}
+
+/// Stencil SpMM for an N = 16 block (ld 16) on a cubic grid level, the block's planes staged by the TMA engine. A
+/// block of 8 warps owns a 16 x 16 (x, y) tile and marches it through kZtLz planes: every plane of X it touches
+/// (with a one-row / one-line halo, 18 x 18 rows x 128 B) arrives in shared memory by bulk async copies (18 line
+/// segments) into a ring of 4 plane slots, the tile's values by one bulk copy per plane into a ring of 2, all
+/// completing on mbarriers, so the loads of plane z + 2 are in flight while plane z is computed and no register or
+/// LSU slot waits on HBM. Lane group g of warp w computes 8 consecutive rows of line 2w + g / 2 with the per-run
+/// sliding windows of k_spmm_dia, reading the block rows from the staged planes. Each X row leaves HBM once and L2
+/// about 1.3 times (halo), instead of once per stencil run. Same accumulation order as k_spmm_dia.
+template <int NG, int LR>
+__global__ void __launch_bounds__(kThreads, 1) k_spmm_dia_zt(int ni, Cols cc, DiaGeom dg, int nzc,
+                                                           const double* __restrict__ dval,
+                                                           const double* __restrict__ P, double* __restrict__ AP,
+                                                           CgDev s) {
+    constexpr int L0 = 3, G = 8, CPL = 2;
+    constexpr int D = L0 + (NG - 1) * LR;
+    constexpr int SD = 4 * D, PAIRS = D / 2, TB = kZtT * kZtT * D;
+    extern __shared__ __align__(128) double dsm[];
+    double* xs = dsm;
+    double* vsm = xs + size_t(kZtSlots) * kZtRows * 16;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(vsm + 2 * TB);  // 0..3 planes, 4..5 values
+    double* sm = reinterpret_cast<double*>(bar + 8);
+    const int n = dg.n, nt = (n + kZtT - 1) / kZtT, ntile = nt * nt;
+    const int lz = (n + nzc - 1) / nzc;
+    const int nwork = ntile * nzc;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane / G, l = lane % G;
+    const int xoff = CPL * l;
+    const int yl = 2 * warp + g / 2, sg = g % 2;
+    double pd[CPL] = {0.0, 0.0};
+    // stale slot rows (halo outside the grid, never copied) must be finite: their value is 0, 0 * x must be 0
+    for (int i = threadIdx.x; i < kZtSlots * kZtRows * 16; i += blockDim.x) xs[i] = 0.0;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 6; ++i) mbar_init(bar + i, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    // One continuous stream per block over its work items (tile, z range): load j = plane z0 - 1 + k of the item it
+    // belongs to, into slot j % 4 (fill j / 4 of that slot); compute step c uses the three loads of planes z - 1, z,
+    // z + 1 and value block c % 2. Loads run ahead across item boundaries, so no item starts on a cold pipeline.
+    auto item_of = [&](int m, int& xt_, int& yt_, int& z0_, int& z1_) -> bool {
+        const int wi = blockIdx.x + m * gridDim.x;
+        if (wi >= nwork) return false;
+        const int tile = wi % ntile, zc = wi / ntile;
+        xt_ = tile % nt;
+        yt_ = tile / nt;
+        z0_ = zc * lz;
+        z1_ = min(n, z0_ + lz);
+        return true;
+    };
+    // load cursor
+    int lm = 0, lp = 0, lxt = 0, lyt = 0, lz0 = 0, lz1 = 0;
+    bool lvalid = item_of(0, lxt, lyt, lz0, lz1);
+    while (lvalid && lz0 >= lz1) lvalid = item_of(++lm, lxt, lyt, lz0, lz1);
+    if (lvalid) lp = lz0 - 1;
+    int jl = 0;  // next load index
+    auto issue_next = [&]() {
+        if (!lvalid) return;
+        const int sl = jl & 3;
+        if (warp == 0) {
+            const int x0 = lxt * kZtT, y0 = lyt * kZtT;
+            const bool pv = lp >= 0 && lp < n;
+            int lo = 0, hi = 0;
+            const int y = y0 - 1 + lane;
+            const int64_t start = int64_t(x0 - 1) + int64_t(n) * (int64_t(y) + int64_t(n) * lp);
+            if (pv && lane < kZtH && y >= 0 && y < n) {
+                lo = int(start > 0 ? start : int64_t(0));
+                hi = int(start + kZtH < int64_t(ni) ? start + kZtH : int64_t(ni));
+            }
+            int bytes = hi > lo ? (hi - lo) * 16 * int(sizeof(double)) : 0;
+            for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
+            if (lane == 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_expect_tx(bar + sl, uint32_t(bytes));
+            }
+            __syncwarp();
+            if (hi > lo)
+                bulk_g2s(xs + (size_t(sl) * kZtRows + size_t(lane) * kZtH + size_t(lo - start)) * 16,
+                         P + size_t(lo) * 16, uint32_t((hi - lo) * 16 * sizeof(double)), bar + sl);
+        }
+        ++jl;
+        if (++lp > lz1) {
+            do {
+                lvalid = item_of(++lm, lxt, lyt, lz0, lz1);
+            } while (lvalid && lz0 >= lz1);
+            if (lvalid) lp = lz0 - 1;
+        }
+    };
+    // value cursor (one block per compute step)
+    int vm = 0, vz = 0, vxt = 0, vyt = 0, vz0 = 0, vz1 = 0;
+    bool vvalid = item_of(0, vxt, vyt, vz0, vz1);
+    while (vvalid && vz0 >= vz1) vvalid = item_of(++vm, vxt, vyt, vz0, vz1);
+    if (vvalid) vz = vz0;
+    int jv = 0;
+    auto issue_vals = [&]() {
+        if (!vvalid) return;
+        const int vb = jv & 1;
+        if (threadIdx.x == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(bar + 4 + vb, uint32_t(TB * sizeof(double)));
+            bulk_g2s(vsm + size_t(vb) * TB, dval + ((size_t(vz) * nt + vyt) * nt + vxt) * TB,
+                     uint32_t(TB * sizeof(double)), bar + 4 + vb);
+        }
+        ++jv;
+        if (++vz >= vz1) {
+            do {
+                vvalid = item_of(++vm, vxt, vyt, vz0, vz1);
+            } while (vvalid && vz0 >= vz1);
+            if (vvalid) vz = vz0;
+        }
+    };
+    for (int k = 0; k < 4; ++k) issue_next();
+    issue_vals();
+    issue_vals();
+    int jbase = 0;  // load index of the current item's plane z0 - 1
+    int c = 0;      // compute step
+    int xt = 0, yt = 0, z0 = 0, z1 = 0;
+    for (int m = 0; item_of(m, xt, yt, z0, z1); ++m) {
+        if (z0 >= z1) continue;
+        const int x0 = xt * kZtT, y0 = yt * kZtT;
+        const int y = y0 + yl;
+        const int xs0 = x0 + 8 * sg;
+        for (int z = z0; z < z1; ++z, ++c) {
+            const int j0 = jbase + (z - z0);  // plane z - 1
+            const int vb = c & 1;
+            for (int t = 0; t < 3; ++t) mbar_wait(bar + ((j0 + t) & 3), ((j0 + t) >> 2) & 1);
+            mbar_wait(bar + 4 + vb, (c >> 1) & 1);
+            if (y < n) {
+                const int slot_of[3] = {j0 & 3, (j0 + 1) & 3, (j0 + 2) & 3};
+                auto xrow = [&](int dz, int dy, int col) -> const double* {
+                    return xs + (size_t(slot_of[dz + 1]) * kZtRows + size_t(yl + 1 + dy) * kZtH + col) * 16 + xoff;
+                };
+                auto lds = [&](const double* p, double (&x)[CPL]) {
+                    const double2 a = *reinterpret_cast<const double2*>(p);
+                    x[0] = a.x;
+                    x[1] = a.y;
+                };
+                const double* vbase = vsm + size_t(vb) * TB + size_t(warp) * 8 * SD;
+                double w0[L0 - 1][CPL];
+                double wr[NG - 1][LR - 1][CPL];
+                const int c0 = 8 * sg + 1;  // slot column of x = xs0
+#pragma unroll
+                for (int j = 0; j < L0 - 1; ++j) lds(xrow(0, 0, c0 - 1 + j), w0[j]);
+#pragma unroll
+                for (int q = 1; q < NG; ++q)
+#pragma unroll
+                    for (int j = 0; j < LR - 1; ++j) lds(xrow(dg.rdz[q], dg.rdy[q], c0 + dg.rdx[q] + j), wr[q - 1][j]);
+#pragma unroll 2
+                for (int st = 0; st < 8; ++st) {
+                    const double* vs = vbase + st * SD;
+                    double v[D];
+#pragma unroll
+                    for (int p = 0; p < PAIRS; ++p) {
+                        const double2 a = *reinterpret_cast<const double2*>(vs + 2 * (p * 4 + g));
+                        v[2 * p] = a.x;
+                        v[2 * p + 1] = a.y;
+                    }
+                    if constexpr (D & 1) v[D - 1] = vs[2 * PAIRS * 4 + g];
+                    double n0[CPL], nr[NG - 1][CPL];
+                    lds(xrow(0, 0, c0 + st + 1), n0);
+#pragma unroll
+                    for (int q = 1; q < NG; ++q) lds(xrow(dg.rdz[q], dg.rdy[q], c0 + st + dg.rdx[q] + LR - 1), nr[q - 1]);
+                    double acc[CPL];
+#pragma unroll
+                    for (int e = 0; e < CPL; ++e) {
+                        double a = v[0] * w0[0][e];
+                        a = fma(v[1], w0[1][e], a);
+                        a = fma(v[2], n0[e], a);
+                        acc[e] = a;
+                    }
+#pragma unroll
+                    for (int q = 1; q < NG; ++q) {
+                        const int d0 = L0 + (q - 1) * LR;
+#pragma unroll
+                        for (int j = 0; j < LR; ++j) {
+#pragma unroll
+                            for (int e = 0; e < CPL; ++e)
+                                acc[e] = fma(v[d0 + j], j < LR - 1 ? wr[q - 1][j][e] : nr[q - 1][e], acc[e]);
+                        }
+                    }
+                    if (xs0 + st < n) {
+#pragma unroll
+                        for (int e = 0; e < CPL; ++e) pd[e] = fma(w0[1][e], acc[e], pd[e]);
+                        const size_t r = size_t(xs0 + st) + size_t(n) * (size_t(y) + size_t(n) * z);
+                        *reinterpret_cast<double2*>(AP + r * 16 + xoff) = make_double2(acc[0], acc[1]);
+                    }
+#pragma unroll
+                    for (int e = 0; e < CPL; ++e) {
+                        w0[0][e] = w0[1][e];
+                        w0[1][e] = n0[e];
+                    }
+#pragma unroll
+                    for (int q = 1; q < NG; ++q) {
+#pragma unroll
+                        for (int j = 0; j + 1 < LR - 1; ++j)
+#pragma unroll
+                            for (int e = 0; e < CPL; ++e) wr[q - 1][j][e] = wr[q - 1][j + 1][e];
+#pragma unroll
+                        for (int e = 0; e < CPL; ++e) wr[q - 1][LR - 2][e] = nr[q - 1][e];
+                    }
+                }
+            }
+            __syncthreads();  // the loads below z's planes and value block c are free
+            // refill: keep loads up to the next step's first needed plane + 3 in flight
+            const int jnext = (z + 1 < z1) ? j0 + 1 : j0 + 3;  // next item starts 3 loads later (its own z0 - 1)
+            while (jl < jnext + 4 && lvalid) issue_next();
+            issue_vals();
+        }
+        jbase += (z1 - z0) + 2;
+    }
+#pragma unroll
+    for (int e = 0; e < CPL; ++e)
+        for (int o = 16; o >= G; o >>= 1) pd[e] += __shfl_xor_sync(0xffffffffu, pd[e], o);
+    const int N = cc.N;
+    if (lane < G) {
+#pragma unroll
+        for (int e = 0; e < CPL; ++e) sm[warp * N + xoff + e] = pd[e];
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < N; c += blockDim.x) {
+        double tt = 0.0;
+        for (int k = 0; k < int(blockDim.x >> 5); ++k) tt += sm[k * N + c];
+        s.part0[size_t(blockIdx.x) * N + c] = tt;
+    }
+    __syncthreads();
+    k1_epilogue(sm, N, cc, s);
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+constexpr int kZwThreads = 288;  // 8 compute warps + 1 producer warp
+
+/// k_spmm_dia_zt with a producer warp (warp specialisation): warp 8 issues the plane and value bulk copies as soon
+/// as the compute warps release a slot (per-slot "empty" mbarriers, one arrival per compute warp), so the compute
+/// warps never meet at a block barrier and a warp that finished plane z starts plane z + 1 as soon as its data has
+/// landed. Same work decomposition, layouts and accumulation order as k_spmm_dia_zt.
+template <int NG, int LR>
+__global__ void __launch_bounds__(kZwThreads, 1) k_spmm_dia_zw(int ni, Cols cc, DiaGeom dg, int nzc,
+                                                             const double* __restrict__ dval,
+                                                             const double* __restrict__ P, double* __restrict__ AP,
+                                                             CgDev s) {
+    constexpr int L0 = 3, G = 8, CPL = 2, NCW = 8;
+    constexpr int D = L0 + (NG - 1) * LR;
+    constexpr int SD = 4 * D, PAIRS = D / 2, TB = kZtT * kZtT * D;
+    extern __shared__ __align__(128) double dsm[];
+    double* xs = dsm;
+    double* vsm = xs + size_t(kZtSlots) * kZtRows * 16;
+    uint64_t* full = reinterpret_cast<uint64_t*>(vsm + 2 * TB);  // 0..3 planes, 4..5 values
+    uint64_t* empty = full + 6;                                  // 0..3 planes, 4..5 values
+    double* sm = reinterpret_cast<double*>(empty + 6);
+    const int n = dg.n, nt = (n + kZtT - 1) / kZtT, ntile = nt * nt;
+    const int lz = (n + nzc - 1) / nzc;
+    const int nwork = ntile * nzc;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < kZtSlots * kZtRows * 16; i += blockDim.x) xs[i] = 0.0;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 6; ++i) {
+            mbar_init(full + i, 1);
+            mbar_init(empty + i, NCW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto item_of = [&](int m, int& xt_, int& yt_, int& z0_, int& z1_) -> bool {
+        const int wi = blockIdx.x + m * gridDim.x;
+        if (wi >= nwork) return false;
+        const int tile = wi % ntile, zc = wi / ntile;
+        xt_ = tile % nt;
+        yt_ = tile / nt;
+        z0_ = zc * lz;
+        z1_ = min(n, z0_ + lz);
+        return true;
+    };
+    double pd[CPL] = {0.0, 0.0};
+    const int N = cc.N;
+    if (warp == NCW) {
+        // ---- producer: for every compute step, the plane loads it needs (up to z + 1) and its value block ----
+        int jl = 0, jv = 0;
+        auto load = [&](int xt, int yt, int p) {
+            const int sl = jl & 3;
+            if (jl >= 4) mbar_wait(empty + sl, ((jl >> 2) - 1) & 1);
+            const int x0 = xt * kZtT, y0 = yt * kZtT;
+            const bool pv = p >= 0 && p < n;
+            int lo = 0, hi = 0;
+            const int y = y0 - 1 + lane;
+            const int64_t start = int64_t(x0 - 1) + int64_t(n) * (int64_t(y) + int64_t(n) * p);
+            if (pv && lane < kZtH && y >= 0 && y < n) {
+                lo = int(start > 0 ? start : int64_t(0));
+                hi = int(start + kZtH < int64_t(ni) ? start + kZtH : int64_t(ni));
+            }
+            int bytes = hi > lo ? (hi - lo) * 16 * int(sizeof(double)) : 0;
+            for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
+            if (lane == 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_expect_tx(full + sl, uint32_t(bytes));
+            }
+            __syncwarp();
+            if (hi > lo)
+                bulk_g2s(xs + (size_t(sl) * kZtRows + size_t(lane) * kZtH + size_t(lo - start)) * 16,
+                         P + size_t(lo) * 16, uint32_t((hi - lo) * 16 * sizeof(double)), full + sl);
+            ++jl;
+        };
+        auto vals = [&](int xt, int yt, int p) {
+            const int vb = jv & 1;
+            if (jv >= 2) mbar_wait(empty + 4 + vb, ((jv >> 1) - 1) & 1);
+            if (lane == 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_expect_tx(full + 4 + vb, uint32_t(TB * sizeof(double)));
+                bulk_g2s(vsm + size_t(vb) * TB, dval + ((size_t(p) * nt + yt) * nt + xt) * TB,
+                         uint32_t(TB * sizeof(double)), full + 4 + vb);
+            }
+            __syncwarp();
+            ++jv;
+        };
+        int xt = 0, yt = 0, z0 = 0, z1 = 0;
+        for (int m = 0; item_of(m, xt, yt, z0, z1); ++m) {
+            if (z0 >= z1) continue;
+            load(xt, yt, z0 - 1);
+            load(xt, yt, z0);
+            for (int z = z0; z < z1; ++z) {
+                load(xt, yt, z + 1);
+                vals(xt, yt, z);
+            }
+        }
+    } else {
+        // ---- compute warps ----
+        const int g = lane / G, l = lane % G;
+        const int xoff = CPL * l;
+        const int yl = 2 * warp + g / 2, sg = g % 2;
+        int jbase = 0, c = 0;
+        int xt = 0, yt = 0, z0 = 0, z1 = 0;
+        for (int m = 0; item_of(m, xt, yt, z0, z1); ++m) {
+            if (z0 >= z1) continue;
+            const int x0 = xt * kZtT, y0 = yt * kZtT;
+            const int y = y0 + yl;
+            const int xs0 = x0 + 8 * sg;
+            for (int z = z0; z < z1; ++z, ++c) {
+                const int j0 = jbase + (z - z0);  // load of plane z - 1
+                const int vb = c & 1;
+                for (int t = 0; t < 3; ++t) mbar_wait(full + ((j0 + t) & 3), ((j0 + t) >> 2) & 1);
+                mbar_wait(full + 4 + vb, (c >> 1) & 1);
+                if (y < n) {
+                    const int slot_of[3] = {j0 & 3, (j0 + 1) & 3, (j0 + 2) & 3};
+                    auto xrow = [&](int dz, int dy, int col) -> const double* {
+                        return xs + (size_t(slot_of[dz + 1]) * kZtRows + size_t(yl + 1 + dy) * kZtH + col) * 16 + xoff;
+                    };
+                    auto lds = [&](const double* p, double (&x)[CPL]) {
+                        const double2 a = *reinterpret_cast<const double2*>(p);
+                        x[0] = a.x;
+                        x[1] = a.y;
+                    };
+                    const double* vbase = vsm + size_t(vb) * TB + size_t(warp) * 8 * SD;
+                    double w0[L0 - 1][CPL];
+                    double wr[NG - 1][LR - 1][CPL];
+                    const int c0 = 8 * sg + 1;  // slot column of x = xs0
+#pragma unroll
+                    for (int j = 0; j < L0 - 1; ++j) lds(xrow(0, 0, c0 - 1 + j), w0[j]);
+#pragma unroll
+                    for (int q = 1; q < NG; ++q)
+#pragma unroll
+                        for (int j = 0; j < LR - 1; ++j) lds(xrow(dg.rdz[q], dg.rdy[q], c0 + dg.rdx[q] + j), wr[q - 1][j]);
+#pragma unroll 2
+                    for (int st = 0; st < 8; ++st) {
+                        const double* vs = vbase + st * SD;
+                        double v[D];
+#pragma unroll
+                        for (int p = 0; p < PAIRS; ++p) {
+                            const double2 a = *reinterpret_cast<const double2*>(vs + 2 * (p * 4 + g));
+                            v[2 * p] = a.x;
+                            v[2 * p + 1] = a.y;
+                        }
+                        if constexpr (D & 1) v[D - 1] = vs[2 * PAIRS * 4 + g];
+                        double n0[CPL], nr[NG - 1][CPL];
+                        lds(xrow(0, 0, c0 + st + 1), n0);
+#pragma unroll
+                        for (int q = 1; q < NG; ++q)
+                            lds(xrow(dg.rdz[q], dg.rdy[q], c0 + st + dg.rdx[q] + LR - 1), nr[q - 1]);
+                        double acc[CPL];
+#pragma unroll
+                        for (int e = 0; e < CPL; ++e) {
+                            double a = v[0] * w0[0][e];
+                            a = fma(v[1], w0[1][e], a);
+                            a = fma(v[2], n0[e], a);
+                            acc[e] = a;
+                        }
+#pragma unroll
+                        for (int q = 1; q < NG; ++q) {
+                            const int d0 = L0 + (q - 1) * LR;
+#pragma unroll
+                            for (int j = 0; j < LR; ++j) {
+#pragma unroll
+                                for (int e = 0; e < CPL; ++e)
+                                    acc[e] = fma(v[d0 + j], j < LR - 1 ? wr[q - 1][j][e] : nr[q - 1][e], acc[e]);
+                            }
+                        }
+                        if (xs0 + st < n) {
+#pragma unroll
+                            for (int e = 0; e < CPL; ++e) pd[e] = fma(w0[1][e], acc[e], pd[e]);
+                            const size_t r = size_t(xs0 + st) + size_t(n) * (size_t(y) + size_t(n) * z);
+                            *reinterpret_cast<double2*>(AP + r * 16 + xoff) = make_double2(acc[0], acc[1]);
+                        }
+#pragma unroll
+                        for (int e = 0; e < CPL; ++e) {
+                            w0[0][e] = w0[1][e];
+                            w0[1][e] = n0[e];
+                        }
+#pragma unroll
+                        for (int q = 1; q < NG; ++q) {
+#pragma unroll
+                            for (int j = 0; j + 1 < LR - 1; ++j)
+#pragma unroll
+                                for (int e = 0; e < CPL; ++e) wr[q - 1][j][e] = wr[q - 1][j + 1][e];
+#pragma unroll
+                            for (int e = 0; e < CPL; ++e) wr[q - 1][LR - 2][e] = nr[q - 1][e];
+                        }
+                    }
+                }
+                // release: plane z - 1 (and at the item's end z, z + 1) and value block c
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(empty + (j0 & 3));
+                    if (z + 1 == z1) {
+                        mbar_arrive(empty + ((j0 + 1) & 3));
+                        mbar_arrive(empty + ((j0 + 2) & 3));
+                    }
+                    mbar_arrive(empty + 4 + vb);
+                }
+            }
+            jbase += (z1 - z0) + 2;
+        }
+#pragma unroll
+        for (int e = 0; e < CPL; ++e)
+            for (int o = 16; o >= G; o >>= 1) pd[e] += __shfl_xor_sync(0xffffffffu, pd[e], o);
+        if (lane < G) {
+#pragma unroll
+            for (int e = 0; e < CPL; ++e) sm[warp * N + xoff + e] = pd[e];
+        }
+    }
+    __syncthreads();
+    for (int cc2 = threadIdx.x; cc2 < N; cc2 += blockDim.x) {
+        double tt = 0.0;
+        for (int k = 0; k < NCW; ++k) tt += sm[k * N + cc2];
+        s.part0[size_t(blockIdx.x) * N + cc2] = tt;
+    }
+    __syncthreads();
+    k1_epilogue(sm, N, cc, s);
+}
+
 // ---------------- K1 (SELL-32 variant): one row per lane, all N <= 16 columns per lane ----------------
 template <int NC>
 __device__ __forceinline__ void load_row(const double* __restrict__ p, double (&x)[NC]) {
@@ -1774,6 +2234,7 @@ struct SellOps {
     const double* DIA = nullptr;              // tiled stencil values (dia.cuh) for dia_g lanes per row
     int dia_g = 0;
     int dia_z = 0;                            // > 0: z-marching kernel, lines per block
+    bool dia_zt = false;                      // TMA-staged z-marching kernel
     // CSR pattern the row kernels walk: the level's natural interior pattern, or its locality-ordered copy
     const int32_t *ptr = nullptr, *col = nullptr;
     int max_row = 0;
@@ -1837,9 +2298,75 @@ int dia_z(const Level& L, int N) {
     return std::atoi(env) == 8 ? 8 : 4;
 }
 
+/// TMA-staged z-marching kernel (default on cubic grid levels with an N = 16, ld = 16 block; KSB_DIA_ZT=0 keeps the
+/// band kernel)
+bool dia_zt(const Level& L, int N, int ld) {
+    const char* env = std::getenv("KSB_DIA_ZT");
+    const int D = L.dia_ng > 0 ? 3 + (L.dia_ng - 1) * L.dia_lr : 0;
+    // the plane and value rings must fit one block's shared memory (Kuhn 15-point: 222 KB; the 27-point box does not)
+    return N == 16 && ld == 16 && L.dia_n >= 3 && D > 0 && dia_zt_smem(D) <= 227 * 1024 && !(env && env[0] == '0');
+}
+
 bool try_dia(Ctx& c, const Level& L, const CgWork& w, const Cols& cc, const SellOps& so) {
     if (!so.DIA) return false;
     const DiaGeom dg = dia_geom(L);
+    if (so.dia_zt) {
+        auto go_zt = [&](auto kern) {
+            const size_t smt = dia_zt_smem(dg.D);
+            static std::map<const void*, bool> attr;
+            if (!attr[reinterpret_cast<const void*>(kern)]) {
+                KSB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smt)));
+                attr[reinterpret_cast<const void*>(kern)] = true;
+            }
+            const int n = dg.n, nt = ceil_div(n, kZtT);
+            const int res = std::max(1, std::min(resident_grid(c, kern, kThreads, smt), w.cap_blocks));
+            // z ranges: the length that balances the items over the resident blocks best (each item also loads two
+            // halo planes, from L2)
+            int nzc = 1;
+            double best = 1e30;
+            for (int lz = 3; lz <= std::min(n, 24); ++lz) {
+                const int zc = ceil_div(n, lz);
+                const double cost = double(ceil_div(int64_t(nt) * nt * zc, res)) * (lz + 0.5);
+                if (cost < best) {
+                    best = cost;
+                    nzc = zc;
+                }
+            }
+            const int grid = std::max(1, std::min(res, nt * nt * nzc));
+            launch(c, "spmm", kern, grid, kThreads, smt, L.ni, cc, dg, nzc, so.DIA, (const double*)w.P, w.AP, w.dev);
+            return true;
+        };
+        const char* zw = std::getenv("KSB_DIA_ZW");
+        if (!(zw && zw[0] == '0')) {  // warp-specialised producer (default)
+            auto kern = k_spmm_dia_zw<7, 2>;
+            const size_t smt = dia_zt_smem(dg.D) + 6 * sizeof(uint64_t);
+            static bool attr = false;
+            if (!attr) {
+                KSB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smt)));
+                attr = true;
+            }
+            const int n = dg.n, nt = ceil_div(n, kZtT);
+            const int res = std::max(1, std::min(resident_grid(c, kern, kZwThreads, smt), w.cap_blocks));
+            int nzc = 1;
+            double best = 1e30;
+            for (int lz = 3; lz <= std::min(n, 24); ++lz) {
+                const int zc = ceil_div(n, lz);
+                const double cost = double(ceil_div(int64_t(nt) * nt * zc, res)) * (lz + 0.5);
+                if (cost < best) {
+                    best = cost;
+                    nzc = zc;
+                }
+            }
+            const int grid = std::max(1, std::min(res, nt * nt * nzc));
+            if (L.dia_ng == 7) {
+                launch(c, "spmm", kern, grid, kZwThreads, smt, L.ni, cc, dg, nzc, so.DIA, (const double*)w.P, w.AP,
+                       w.dev);
+                return true;
+            }
+        }
+        if (L.dia_ng == 7) return go_zt(k_spmm_dia_zt<7, 2>);
+        if (L.dia_ng == 9) return go_zt(k_spmm_dia_zt<9, 3>);
+    }
     if (so.dia_z) {
         const size_t sm = sizeof(double) * std::max<size_t>(8 * size_t(cc.N), 2 * size_t(cc.N));
         auto go_z = [&](auto kern, int nw) {
@@ -2102,6 +2629,12 @@ void cg_solve(Ctx& c, Level& L, int mat, int shift_mat, const double* h_sigma, c
     if (!L.mats[mat].valid) raise(KSB_INVALID_ARGUMENT, "cg: operator not assembled");
     const bool shift = shift_mat >= 0;
     if (shift && !L.mats[shift_mat].valid) raise(KSB_INVALID_ARGUMENT, "cg: shift operator not assembled");
+    if (o.precond == 1) {  // the reference's exact SGS preconditioner (parity runs, sgs.cu)
+        if (o.fixed_iterations > 0) raise(KSB_INVALID_ARGUMENT, "cg: the SGS path has no fixed-iteration mode");
+        cg_solve_sgs(c, L, mat, shift_mat, h_sigma, d_B, d_X, N, ld, o, stats, w);
+        return;
+    }
+    if (o.precond != 0) raise(KSB_INVALID_ARGUMENT, "cg: precond must be 0 (Jacobi) or 1 (SGS)");
 
     const Plan p = plan_for(N);
     const int rows_per_block = kThreads / p.G;
@@ -2182,8 +2715,9 @@ void cg_solve(Ctx& c, Level& L, int mat, int shift_mat, const double* h_sigma, c
     if (!shift && L.dia_ng > 0 && L.dia_lo == int(lo) && dia_lanes(N) > 0 && !(dia_env && dia_env[0] == '0') &&
         ld % 2 == 0) {
         so.dia_g = dia_lanes(N);
-        so.dia_z = dia_z(L, N);
-        so.DIA = L.dia_values(mat, so.dia_z ? kDiaLine : 32 / so.dia_g);
+        so.dia_zt = dia_zt(L, N, ld);
+        so.dia_z = so.dia_zt ? 0 : dia_z(L, N);
+        so.DIA = L.dia_values(mat, so.dia_zt ? kDiaZT : so.dia_z ? kDiaLine : 32 / so.dia_g);
     }
     const int total = cc.fixed ? o.fixed_iterations : o.max_iterations;
     const int every = std::max(1, o.check_every);
@@ -2209,7 +2743,7 @@ void cg_solve(Ctx& c, Level& L, int mat, int shift_mat, const double* h_sigma, c
                                 d.diagA, d.diagB, so.ptr, so.col, so.T8, L.t8_col.p, L.sell_ptr.p, L.sell_col.p,
                                 L.ii_ptr.p, L.ii_col.p, L.lo_ptr.p, L.lo_col.p, so.DIA};
         std::memcpy(key.ptrs, ptrs, sizeof ptrs);
-        const int ints[10] = {mat, shift_mat, N, ld, chunk, grid_s, grid_e, cc.fixed, L.ni, L.nslices * 64 + so.dia_g * 2 + (so.dia_z > 0)};
+        const int ints[10] = {mat, shift_mat, N, ld, chunk, grid_s, grid_e, cc.fixed, L.ni, L.nslices * 64 + so.dia_g * 2 + (so.dia_z > 0) + (so.dia_zt ? 1 << 30 : 0)};
         std::memcpy(key.ints, ints, sizeof ints);
         key.tol = cc.tol;
         for (auto& g : w.graphs)

@@ -2,6 +2,7 @@
 #pragma once
 
 #include "level.cuh"
+#include "sgs.cuh"
 
 namespace ksb {
 
@@ -10,6 +11,7 @@ struct CgOptions {
     int max_iterations = 20000;
     int fixed_iterations = 0;
     int check_every = 8;
+    int precond = 0;  // 0: Jacobi (fused, production); 1: the reference's exact SGS (sgs.cu, parity runs)
 };
 
 struct CgColumnStats {
@@ -51,6 +53,7 @@ struct CgWork {
     int cap_cols = 0, cap_blocks = 0;
     CgDev dev{};
     std::vector<CgGraph> graphs;  // chunks of iterations captured as CUDA graphs (small FIFO cache)
+    SgsWork sgs;                  // blocks of the SGS parity path
     void ensure(int ni, int N, int ld, int max_blocks);
     /// drop the captured graphs of one level (ksb_level_destroy)
     void forget_level(uint64_t uid);
@@ -59,5 +62,8 @@ struct CgWork {
 
 void cg_solve(Ctx& c, Level& L, int mat, int shift_mat, const double* h_sigma, const double* d_B, double* d_X, int N,
               int ld, const CgOptions& o, CgColumnStats* stats, CgWork& w);
+/// EllipticSolver::pcg with apply_sgs (proj/src/solver.cpp:50-111) for N columns, host-driven (sgs.cu)
+void cg_solve_sgs(Ctx& c, Level& L, int mat, int shift_mat, const double* h_sigma, const double* d_B, double* d_X,
+                  int N, int ld, const CgOptions& o, CgColumnStats* stats, CgWork& w);
 
 } // namespace ksb

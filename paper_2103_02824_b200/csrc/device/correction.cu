@@ -265,6 +265,7 @@ void solve_orbitals(Level& L, Corrector& K, CgWork& cg, const StepOptions& o, co
     CgOptions co;
     co.tol = o.tol_linear;
     co.check_every = o.check_every;
+    co.precond = o.precond;
     std::vector<CgColumnStats> st(N);
     cg_solve(c, L, MAT_H, -1, nullptr, K.R0.p, d_PhiT, N, ld, co, st.data(), cg);
     if (ldT != ld) raise(KSB_INVALID_ARGUMENT, "solve_orbitals: ld mismatch");
@@ -327,7 +328,7 @@ void solve_orbitals(Level& L, Corrector& K, CgWork& cg, const StepOptions& o, co
 /// Jacobi CG. Same PCG contract either way (proj/src/solver.cpp:57-111).
 CgColumnStats stiffness_solve(Level& L, Corrector& K, CgWork& cg, const double* rhs, double* x, double tol) {
     static const char* env = std::getenv("KSB_STIFF_MG");
-    const bool use_mg = L.meshes.size() >= 2 && !(env && env[0] == '0') && K.coarse.CHi.n > 0;
+    const bool use_mg = K.precond == 0 && L.meshes.size() >= 2 && !(env && env[0] == '0') && K.coarse.CHi.n > 0;
     if (use_mg) {
         if (!K.mg.ready) mg_setup(L, K.mg, K.coarse.CHi.p);
         const CgColumnStats st = mg_pcg(L, K.mg, rhs, x, tol, 20000);
@@ -335,6 +336,7 @@ CgColumnStats stiffness_solve(Level& L, Corrector& K, CgWork& cg, const double* 
     }
     CgOptions co;
     co.tol = tol;
+    co.precond = K.precond;  // SGS parity runs: the reference's SGS-PCG on S (hartree.cpp:131-144)
     CgColumnStats st;
     cg_solve(*L.ctx, L, 0, -1, nullptr, rhs, x, 1, 1, co, &st, cg);
     return st;
@@ -373,6 +375,7 @@ void expand(Level& L, Corrector& K, const double* d_PhiT, int ldT, const double*
 void correction_step(Level& L, Corrector& K, CgWork& cg, const StepOptions& o, double* h_lambda, double* d_Phi, int ld,
                      double* d_w, StepLog* log) {
     Ctx& c = *L.ctx;
+    K.precond = o.precond;
     if (!K.ops_ready) level_ops(L, K);
     K.mlc_ld = 0;  // the step reuses the standard-MLC work buffers: a pending MLC level must be restarted
     const int N = K.sys.N, n = L.n, ni = L.ni;
@@ -434,9 +437,14 @@ void correction_step(Level& L, Corrector& K, CgWork& cg, const StepOptions& o, d
     rho_vxc(L, d_Phi, N, ld, K.sys.occ, K.sys.xc, K.rho_t.p, nullptr);
     launch(c, "elementwise", k_add, grid_of(c, n), kT, 0, int64_t(n), (const double*)K.rho_t.p, 1.0,
            (const double*)K.rho.p, -1.0, K.diff.p);
-    const auto nn = norms_sq(L, K.diff.p, K.phys);
-    const double l2 = std::sqrt(std::max(0.0, nn[0])), semi = std::sqrt(std::max(0.0, nn[1]));
-    lg.delta = std::sqrt(l2 * l2 + semi * semi);
+    // density_change (driver.cpp:56-60): H1, or L1 with RunConfig::outer_norm_l1
+    if (o.norm_l1) {
+        lg.delta = l1_norm(L, K.diff.p, K.phys);
+    } else {
+        const auto nn = norms_sq(L, K.diff.p, K.phys);
+        const double l2 = std::sqrt(std::max(0.0, nn[0])), semi = std::sqrt(std::max(0.0, nn[1]));
+        lg.delta = std::sqrt(l2 * l2 + semi * semi);
+    }
     KSB_CUDA_CHECK(cudaMemcpyAsync(h_lambda, K.inner.lamv[K.inner.cur].p, sizeof(double) * N, cudaMemcpyDeviceToHost,
                                    c.stream));
     tm.mark();
@@ -475,6 +483,7 @@ void hartree_of_density(Level& L, Corrector& K, CgWork& cg, const double* d_rho,
 void mlc_begin(Level& L, Corrector& K, CgWork& cg, const StepOptions& o, const double* h_lambda, const double* d_Phi,
                int ld, const double* d_w, StepLog* log) {
     Ctx& c = *L.ctx;
+    K.precond = o.precond;
     if (!K.ops_ready) level_ops(L, K);
     const int N = K.sys.N, n = L.n, ni = L.ni;
     for (auto* b : {&K.rho, &K.vxc, &K.what_full, &K.wt_full, &K.ell_full, &K.rho_t, &K.diff, &K.potf, &K.wscr})
@@ -512,6 +521,7 @@ void mlc_begin(Level& L, Corrector& K, CgWork& cg, const StepOptions& o, const d
 
 double mlc_sweep(Level& L, Corrector& K, CgWork& cg, const StepOptions& o, double* h_lambda, double* d_Phi, int ld) {
     Ctx& c = *L.ctx;
+    K.precond = o.precond;
     if (K.mlc_ld == 0) raise(KSB_INVALID_ARGUMENT, "mlc_sweep before mlc_begin");
     if (ld != K.mlc_ld) raise(KSB_INVALID_ARGUMENT, "mlc_sweep: ld differs from mlc_begin's");
     const int N = K.sys.N, n = L.n;
@@ -544,18 +554,21 @@ double mlc_sweep(Level& L, Corrector& K, CgWork& cg, const StepOptions& o, doubl
     rho_vxc(L, d_Phi, N, ld, K.sys.occ, K.sys.xc, K.rho_t.p, nullptr);
     launch(c, "elementwise", k_add, grid_of(c, n), kT, 0, int64_t(n), (const double*)K.rho_t.p, 1.0,
            (const double*)K.rho.p, -1.0, K.diff.p);
-    const auto nn = norms_sq(L, K.diff.p, K.phys);
+    const double l1 = o.norm_l1 ? l1_norm(L, K.diff.p, K.phys) : 0.0;
+    const auto nn = o.norm_l1 ? std::array<double, 2>{0.0, 0.0} : norms_sq(L, K.diff.p, K.phys);
     KSB_CUDA_CHECK(cudaMemcpyAsync(K.rho.p, K.rho_t.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream));
     KSB_CUDA_CHECK(cudaMemcpyAsync(h_lambda, K.inner.lamv[K.inner.cur].p, sizeof(double) * N, cudaMemcpyDeviceToHost,
                                    c.stream));
     KSB_CUDA_CHECK(cudaStreamSynchronize(c.stream));
     ++K.mlc_sweeps;
+    if (o.norm_l1) return l1;
     const double l2 = std::sqrt(std::max(0.0, nn[0])), semi = std::sqrt(std::max(0.0, nn[1]));
     return std::sqrt(l2 * l2 + semi * semi);
 }
 
 void mlc_finish(Level& L, Corrector& K, CgWork& cg, const StepOptions& o, double* d_w, double* d_rho) {
     Ctx& c = *L.ctx;
+    K.precond = o.precond;
     if (K.mlc_ld == 0) raise(KSB_INVALID_ARGUMENT, "mlc_finish before mlc_begin");
     const int n = L.n;
     if (K.sys.hartree_on)
@@ -603,8 +616,13 @@ ScfStats coarse_scf(Level& L, Corrector& K, CgWork& cg, const ScfParams& p, doub
         rho_vxc(L, d_Phi, N, ld, K.sys.occ, K.sys.xc, K.rho_t.p, nullptr);
         launch(c, "elementwise", k_add, grid_of(c, n), kT, 0, int64_t(n), (const double*)K.rho_t.p, 1.0,
                (const double*)d_rho, -1.0, K.diff.p);
-        const auto nn = norms_sq(L, K.diff.p, K.phys);
-        const double delta = std::sqrt(std::max(0.0, nn[0]) + std::max(0.0, nn[1]));
+        double delta;
+        if (p.norm_l1) {
+            delta = l1_norm(L, K.diff.p, K.phys);
+        } else {
+            const auto nn = norms_sq(L, K.diff.p, K.phys);
+            delta = std::sqrt(std::max(0.0, nn[0]) + std::max(0.0, nn[1]));
+        }
         st.history.push_back(delta);
         st.iterations = iter;
         const double mix = (p.hartree_on || p.xc_on) ? p.mixing : 1.0;

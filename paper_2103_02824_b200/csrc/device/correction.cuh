@@ -27,6 +27,8 @@ struct System {
 struct StepOptions {
     double tol_linear = 1e-9, tol_inner = 1e-8, score_floor = 1e-8;
     int max_inner = 400, nev_pad = 4, check_every = 8, fixed_sweeps = 0;
+    bool norm_l1 = false;  // density change in L1 instead of H1 (RunConfig::outer_norm_l1)
+    int precond = 0;       // 0: Jacobi BVPs + multigrid Hartree (production); 1: the reference's SGS everywhere
 };
 
 struct StepLog {
@@ -54,7 +56,8 @@ struct Corrector {
     DevBuf<double> colscale;    // per-column right-hand-side scales of the orbital solves
     DevBuf<double> potf, wscr;  // standard MLC: w + v_xc (full), scratch w of expand
     DevBuf<int> idx;
-    std::vector<double> scf_history;  // density changes of the last coarse_scf, kept when it fails (diagnostics)
+    std::vector<double> scf_history;
+    int precond = 0;  // preconditioner of the step in progress (StepOptions::precond)  // density changes of the last coarse_scf, kept when it fails (diagnostics)
     int ldT = 0;
     int mlc_ld = 0, mlc_sweeps = 0;  // standard MLC state: ld of PhiT, sweeps run
     EstimatorData est;
@@ -71,6 +74,7 @@ struct ScfParams {
     double mixing = 0.3;
     bool hartree_on = true, xc_on = true;
     double tol_eig = 1e-9;
+    bool norm_l1 = false;  // scf::Options::norm_l1 (proj/include/ksafem/scf.hpp:19)
 };
 struct ScfStats {
     int iterations = 0;

@@ -27,6 +27,7 @@ struct DiaGeom {
     int n;  // cubic grid dimension (rows = x + n (y + n z)), 0 when the level is not a grid
     int off[27];
     int first[9];
+    int rdx[9], rdy[9], rdz[9];  // grid levels: (dx, dy, dz) of the first offset of every run
 };
 
 inline DiaGeom dia_geom(const Level& L) {
@@ -39,6 +40,15 @@ inline DiaGeom dia_geom(const Level& L) {
         g.first[q] = L.dia_first[q];
         const int len = q == 0 ? 3 : L.dia_lr;
         for (int j = 0; j < len; ++j) g.off[g.D++] = L.dia_first[q] + j;
+        if (g.n > 0) {  // decode offset = dx + n (dy + n dz), |d| <= 1 (topology.cpp checked it)
+            const int o = L.dia_first[q], n = g.n;
+            const int dz = (o + n * n + (n * n) / 2) / (n * n) - 1;  // nearest multiple of n^2 (n >= 3)
+            const int rem = o - dz * n * n;
+            const int dy = (rem + n + n / 2) / n - 1;
+            g.rdz[q] = dz;
+            g.rdy[q] = dy;
+            g.rdx[q] = rem - dy * n;
+        }
     }
     return g;
 }
@@ -78,6 +88,28 @@ __host__ __device__ inline int64_t dia_line_pos(int r, int d, int D, int n) {
     const int xt = x / kDiaSeg, xin = x % kDiaSeg, g = xin / 8, s = xin % 8;
     const int64_t SD = dia_step_stride(D, 4);
     const int64_t base = ((int64_t(yz) * nxt + xt) * 8 + s) * SD;
+    const int pairs = D / 2;
+    return base + (d < 2 * pairs ? int64_t(2) * ((d / 2) * 4 + g) + (d & 1) : int64_t(2) * pairs * 4 + g);
+}
+
+// Plane-tiled layout (TMA-staged z-marching kernel k_spmm_dia_zt): the grid is cut into (x, y) tiles of kZtT x kZtT
+// rows; the values of one tile in one plane are one contiguous block of kZtT^2 D doubles, so a single bulk copy stages
+// them. Inside a block: warp w (lines 2w, 2w + 1 of the tile), step s (x = 8 (g % 2) + s), diagonal pairs of the 4
+// lane groups g (line 2w + g / 2) as in the band layout (wg = 4).
+constexpr int kDiaZT = 200;  // layout id
+constexpr int kZtT = 16;
+
+__host__ __device__ inline int64_t dia_zt_size(int n, int D) {
+    const int64_t nt = (n + kZtT - 1) / kZtT;
+    return nt * nt * n * kZtT * kZtT * D;
+}
+
+__host__ __device__ inline int64_t dia_zt_pos(int r, int d, int D, int n) {
+    const int x = r % n, y = (r / n) % n, z = r / (n * n);
+    const int nt = (n + kZtT - 1) / kZtT;
+    const int xt = x / kZtT, xl = x % kZtT, yt = y / kZtT, yl = y % kZtT;
+    const int w = yl / 2, g = (yl % 2) * 2 + xl / 8, s = xl % 8;
+    const int64_t base = ((int64_t(z) * nt + yt) * nt + xt) * (kZtT * kZtT * D) + int64_t(w) * 8 * 4 * D + s * 4 * D;
     const int pairs = D / 2;
     return base + (d < 2 * pairs ? int64_t(2) * ((d / 2) * 4 + g) + (d & 1) : int64_t(2) * pairs * 4 + g);
 }

@@ -56,6 +56,13 @@ struct Mat {
     bool valid = false;
 };
 
+/// dependency levels of the forward / backward triangular solves of a level's interior pattern (sgs.cu)
+struct SgsPlan {
+    DevBuf<int32_t> f_rows, b_rows;
+    std::vector<int> f_bounds, b_bounds;
+    bool ready = false;
+};
+
 struct Level {
     Ctx* ctx = nullptr;
     uint64_t uid = 0;  // process-unique id (never reused): keys the CG graph cache (cg.cu)
@@ -99,6 +106,7 @@ struct Level {
     DevBuf<double> scratch;   // term accumulation scratch (nnz_ii + nnz_ib)
     DevBuf<int> flag;         // device error flag (singular quadrature)
     Mat mats[kMaxMats];
+    SgsPlan sgs_plan;  // level sets of the SGS triangular solves (sgs.cu, built on first use)
     std::vector<MeshPtr> meshes;  // the hierarchy's meshes 0..level (coarser levels for the multigrid)
 
     Mat& mat(int id);

@@ -259,6 +259,23 @@ __global__ void k_norm_parts(int nt, const int32_t* __restrict__ tets, const dou
     block_sum_to<2>(acc, part);
 }
 
+// fem::l1_norm via integrate_of (reference proj/src/assembly.cpp:234-249,289-291): Keast rule, |f(x_q)|
+__global__ void k_l1_parts(int nt, const int32_t* __restrict__ tets, const double* __restrict__ xyz,
+                           const double* __restrict__ f, double* __restrict__ part) {
+    double acc[1] = {0};
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) {
+        const int4 v = reinterpret_cast<const int4*>(tets)[t];
+        TetG G;
+        tet_geometry(xyz, v, G);
+        const double fv[4] = {f[v.x], f[v.y], f[v.z], f[v.w]};
+        for (int q = 0; q < 11; ++q) {
+            const double val = g_qb[q][0] * fv[0] + g_qb[q][1] * fv[1] + g_qb[q][2] * fv[2] + g_qb[q][3] * fv[3];
+            acc[0] += g_qw[q] * G.vol * fabs(val);
+        }
+    }
+    block_sum_to<1>(acc, part);
+}
+
 __constant__ double c_atoms[4 * 256];
 
 __global__ void k_energy_parts(int nt, const int32_t* __restrict__ tets, const double* __restrict__ xyz,
@@ -412,6 +429,15 @@ std::array<double, 2> norms_sq(Level& L, const double* f_full, PhysWork& w) {
     const int g = grid_of(c, L.nt);
     launch(c, "norm", k_norm_parts, g, kT, 0, L.nt, (const int32_t*)L.tets.p, (const double*)L.xyz.p, f_full, w.part.p);
     return reduce_parts<2>(c, w.part, w.out, g);
+}
+
+double l1_norm(Level& L, const double* f_full, PhysWork& w) {
+    Ctx& c = *L.ctx;
+    ensure_rule(c.stream);
+    w.ensure(L);
+    const int g = grid_of(c, L.nt);
+    launch(c, "norm", k_l1_parts, g, kT, 0, L.nt, (const int32_t*)L.tets.p, (const double*)L.xyz.p, f_full, w.part.p);
+    return reduce_parts<1>(c, w.part, w.out, g)[0];
 }
 
 std::array<double, 5> energy(Level& L, const double* Phi, int N, int ld, const double* rho_full, const double* w_full,

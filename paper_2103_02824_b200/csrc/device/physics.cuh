@@ -46,6 +46,8 @@ double indicators(Level& L, EstimatorData& E, const std::vector<double>& atoms, 
 void lift(Level& L, int mat, const double* bcb, double* y_int);
 /// squared L2 norm and squared H1 seminorm of a full-length nodal function
 std::array<double, 2> norms_sq(Level& L, const double* f_full, PhysWork& w);
+/// fem::l1_norm (proj/src/assembly.cpp:289-291): integral of |f| by the Keast rule
+double l1_norm(Level& L, const double* f_full, PhysWork& w);
 /// kinetic, external, hartree, xc, total
 std::array<double, 5> energy(Level& L, const double* Phi, int N, int ld, const double* rho_full, const double* w_full,
                              const std::vector<double>& atoms, double occ, const XcParams& xc, PhysWork& w);

@@ -915,7 +915,6 @@ ScfResult self_consistent_solve(const model::MolecularSystem& sys, fem::SpacePtr
     sys.validate();
     if (!space || space->state()->level != 0 || space->n_interior() != space->state()->nH)
         fail("invalid-argument", "the device coarse solve runs on level 0 of a hierarchy");
-    if (opt.norm_l1) fail("invalid-argument", "only the H1 density-change norm is available on the device");
     const auto& V = *space;
     model::set_system(V, sys, opt.hartree_on, opt.xc_on && sys.xc.kind != model::XcKind::none);
     ksb_scf_opts o;
@@ -926,6 +925,7 @@ ScfResult self_consistent_solve(const model::MolecularSystem& sys, fem::SpacePtr
     o.hartree_on = opt.hartree_on ? 1 : 0;
     o.xc_on = opt.xc_on ? 1 : 0;
     o.tol_eig = opt.tol_eig;
+    o.norm_l1 = opt.norm_l1 ? 1 : 0;
     const int N = sys.n_pairs, ld = N == 1 ? 1 : N + (N & 1);
     auto& dev = V.device();
     b200::DeviceBuffer phi(dev, int64_t(V.n_interior()) * ld), rho(dev, int64_t(V.n_dofs())),
@@ -1015,8 +1015,8 @@ CorrectionState::CorrectionState(const LevelOps& ops, const model::MolecularSyst
 }
 
 StepLog CorrectionState::step() {
-    const auto o = corr::step_opts(opt_.tol_linear, opt_.tol_inner, opt_.max_inner, opt_.score_floor,
-                                   opt_.nev_scan_pad);
+    auto o = corr::step_opts(opt_.tol_linear, opt_.tol_inner, opt_.max_inner, opt_.score_floor, opt_.nev_scan_pad);
+    o.norm_l1 = opt_.norm_l1 ? 1 : 0;
     ksb_step_log lg{};
     StepLog out;
     out.attempts.assign(size_t(N_), 0);
@@ -1061,6 +1061,7 @@ RunLog run(const RunConfig& cfg) {
     // RunConfig::hartree_enabled / xc_enabled (proj/include/ksafem/runconfig.hpp:39-45)
     so.hartree = cfg.mode != Mode::linear;
     so.xc = cfg.mode != Mode::linear;
+    so.norm_l1 = cfg.outer_norm_l1;
     try {
         for (int level = 0; level < cfg.max_levels; ++level) {
             LevelRecord rec;
@@ -1082,6 +1083,7 @@ RunLog run(const RunConfig& cfg) {
                 opt.tol_eig = cfg.tol_eig;
                 opt.hartree_on = so.hartree;
                 opt.xc_on = so.xc;
+                opt.norm_l1 = cfg.outer_norm_l1;
                 const auto r = scf::initial_coarse_solve(sys, hier.space(0), cfg.tol_outer, opt);
                 rec.outer_iterations = r.iterations;
                 lam = r.lambdas;
@@ -1156,7 +1158,8 @@ LevelResult solve_level_mlc(const LevelOps& ops, const model::MolecularSystem& s
     b200::DeviceBuffer phi = fem::orbital_block(*space, orbitals, ld);
     fem::same_space(w, *space, "w lives on a different space");
     b200::DeviceBuffer wd(space->device(), w.coeffs);
-    const auto o = corr::step_opts(opt.tol_linear, opt.tol_inner, opt.max_inner, opt.score_floor, opt.nev_scan_pad);
+    auto o = corr::step_opts(opt.tol_linear, opt.tol_inner, opt.max_inner, opt.score_floor, opt.nev_scan_pad);
+    o.norm_l1 = opt.norm_l1 ? 1 : 0;
     VecX lam = lambdas;
     ksb_step_log lg{};
     std::vector<int> att(static_cast<size_t>(N)), its(static_cast<size_t>(N));

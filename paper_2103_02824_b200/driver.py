@@ -126,12 +126,13 @@ class RunLog:
 
 def run(ctx: api.Context, atoms, n_pairs: int, occupancy: float, xc: str, box: float, n_coarse: int, max_levels: int,
         refine: str = "adaptive", theta: float = 0.4, tol_outer: float = 1e-6, mixing: float = 0.3, max_scf: int = 200,
-        tol_eig: float = 1e-9, max_outer: int = 40, mode: str = "accelerated", **step_opts) -> RunLog:
+        tol_eig: float = 1e-9, max_outer: int = 40, mode: str = "accelerated", norm_l1: bool = False,
+        **step_opts) -> RunLog:
     """driver::run (proj/src/driver.cpp:306-435), all solves on the device; mode "accelerated" (the paper's
     corrected method, solve_level_corrected) or "standard_mlc" (solve_level_mlc, the comparison method): coarse SCF on
     level 0, then per level Doerfler marks of the residual indicators (or uniform refinement, as BASELINE's
     cfg1 prescribes), nested warm start, solve_level_corrected, indicators. Errors abort the run like the
-    reference (RunLog.aborted, abort_reason)."""
+    reference (RunLog.aborted, abort_reason). norm_l1 = RunConfig::outer_norm_l1 (density changes in L1)."""
     import time
 
     if mode not in ("accelerated", "linear", "standard_mlc"):
@@ -166,7 +167,7 @@ def run(ctx: api.Context, atoms, n_pairs: int, occupancy: float, xc: str, box: f
             t1 = time.perf_counter()
             if level == 0:
                 lam, Phi, rho, w, scf_it, _ = L.coarse_scf(tol=tol_outer, max_iterations=max_scf, mixing=mixing,
-                                                           hartree=hart, xc=xc_on, tol_eig=tol_eig)
+                                                           hartree=hart, xc=xc_on, tol_eig=tol_eig, norm_l1=norm_l1)
                 outer, inner = scf_it, []
             else:
                 # nested warm start on the device (proj/src/driver.cpp:367-371): orbitals as interior blocks
@@ -178,10 +179,10 @@ def run(ctx: api.Context, atoms, n_pairs: int, occupancy: float, xc: str, box: f
                 Phi, w = Phi_new, w_new
                 if mode == "standard_mlc":
                     res = solve_level_mlc(L, lam, Phi, w, tol_outer=tol_outer, max_scf=max_scf, level=level,
-                                          **step_opts)
+                                          norm_l1=int(norm_l1), **step_opts)
                 else:
                     res = solve_level_corrected(L, lam, Phi, w, tol_outer=tol_outer, max_outer=max_outer,
-                                                level=level, **step_opts)
+                                                level=level, norm_l1=int(norm_l1), **step_opts)
                 outer, inner = res.outer_iterations, res.inner_iterations
                 rho = ctx.empty((L.n,))
                 L.density(Phi, rho)

@@ -201,3 +201,20 @@ def test_correction_step_matches_oracle(ctx, xc, hartree):
         assert rel(P * sgn, orb_o[c.interior]) < 1e-6
         assert rel(w.download(), w_o) < 1e-6
         assert abs(lg["delta"] - lo["delta"]) <= 1e-6 * lo["delta"]
+
+
+def test_l1_density_change_option(ctx):
+    """RunConfig::outer_norm_l1 (proj/src/driver.cpp:56-60, proj/src/assembly.cpp:289-291): the step's delta is the
+    Keast-rule L1 norm of the density change, and ksb_l1_norm matches the oracle's fem::l1_norm"""
+    c = Case(ctx)
+    f = np.sin(np.arange(c.L.n) * 0.37) - 0.2
+    assert abs(c.L.l1_norm(c.dev(f)) - c.orc.l1_norm(c.lev, f)) <= 1e-12 * c.orc.l1_norm(c.lev, f)
+    lam_g = c.lam.copy()
+    Phi = c.dev(c.phi_block(c.orb))
+    w = c.dev(c.w)
+    rho0 = c.orc.density(c.orb)
+    lg = c.L.correction_step(lam_g, Phi, w, tol_linear=1e-12, norm_l1=1)
+    lam_o, orb_o, w_o, lo = c.orc.correction_step(c.lev, c.lam.copy(), c.orb.copy(), c.w.copy(), tol_linear=1e-12)
+    l1_o = c.orc.l1_norm(c.lev, c.orc.density(orb_o) - rho0)
+    assert abs(lg["delta"] - l1_o) <= 1e-6 * l1_o
+    assert lo["delta"] != pytest.approx(l1_o)  # the oracle's default stays H1
