@@ -43,8 +43,9 @@ def hierarchy(adaptive):
 def test_sgs_pcg_matches_oracle(ctx, adaptive):
     atoms, h, orc, lev = hierarchy(adaptive)
     L = kb.Level(ctx, h, lev)
-    L.assemble(kb.MAT_USER0, c_s=0.5, c_m=1.5, potential=(kb.POT_COULOMB, atoms))
-    op = orc.operator(lev, c_s=0.5, c_m=1.5, potential=(0, atoms), precond=0)  # oracle precond 0 = SGS
+    # 1/2 S + M_ext + 4 M: positive definite (the Z = 2 well binds at -2)
+    L.assemble(kb.MAT_USER0, c_s=0.5, c_m=4.0, potential=(kb.POT_COULOMB, atoms))
+    op = orc.operator(lev, c_s=0.5, c_m=4.0, potential=(0, atoms), precond=0)  # oracle precond 0 = SGS
     B = np.random.default_rng(5).standard_normal((L.ni, 3))
     B[:, 1] = 0.0
     X, st = L.cg_solve_host(kb.MAT_USER0, B, 3, opts=L.cg_options(tol=1e-10, precond=1))
