@@ -83,6 +83,12 @@ struct Level {
     // first chunk of coarse tet C; pj_n = number of chunks (== nct when no coarse tet is split)
     DevBuf<int32_t> pj_c, pj_b, pj_e, pj_ptr;
     int pj_n = 0;
+    // aggregated K-PROJ (GEMM form): compact chunks of each coarse tet's fine tets (topology.hpp ProjChunks), built
+    // on the first many-orbital projection
+    DevBuf<int32_t> pg_item_c, pg_item_ch, pg_cptr, pg_ch_t, pg_ch_v, pg_ch_e, pg_tets, pg_verts, pg_edges,
+        pg_vinc_ptr, pg_vinc, pg_einc_ptr, pg_einc;
+    int pg_items = 0;
+    bool pg_ready = false;
     DevBuf<int32_t> vinc_ptr, vinc;           // interior vertex -> incident (tet*4 + local)
     DevBuf<int32_t> bvinc_ptr, bvinc;         // boundary vertex -> incident (tet*4 + local)
     DevBuf<int32_t> cinc_ptr, cinc;           // coarse interior dof -> incident (coarse tet*4 + local)

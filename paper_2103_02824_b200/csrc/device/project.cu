@@ -8,6 +8,8 @@
 // deterministic coarse assembly (per coarse dof, ascending coarse tet) finishes the job.
 // No fine CSR matrix is formed for M_wt, M_xc, M_ell or the per-orbital M_phi.
 #include <algorithm>
+#include <cstdlib>
+#include <map>
 
 #include "geom.cuh"
 #include "project.cuh"
@@ -367,6 +369,286 @@ __global__ void k_coarse_scalar(int nct, int nvals, const double* __restrict__ p
     if (lane == 0) out[v] = s;
 }
 
+// ---------------- aggregated projection (GEMM form) for many orbitals ----------------
+// Every orbital-dependent ledger entry of a coarse tet is linear or quadratic in the orbital's nodal values, with
+// coefficients that do not depend on the orbital: per fine tet T and corner l,
+//   A_h4[ab] += phi_l (vol/120) (K_ab + mu_la (m_b + mu_lb) + mu_lb (m_a + mu_la)),  K_ab = m_a m_b + sum_j mu_ja mu_jb,
+//   b_X[a]   += phi_l sum_j mu_ja E^X[j][l]                (X = a_eff, w~, v_xc, 1, S: b_H1, b_H3, b_H4, c_Hh, d_phi),
+// and per vertex / edge of T
+//   rhs[a] += phi_l^2 (vol/120)(2 m_a + 4 mu_la) + phi_k phi_l (vol/60)(m_a + mu_ka + mu_la),
+//   beta_X += phi_l^2 E^X[l][l] + phi_k phi_l (E^X[k][l] + E^X[l][k])
+// (m_a = sum_j mu_ja; mass_elem's weights (vol/120) c_jk (1 + delta_jl + delta_kl)). Summing the coefficients over the
+// tets of a compact chunk first (per chunk vertex: R, 36 rows; per chunk vertex and edge: Q, 9 rows) turns the
+// orbital loop into two small GEMMs per chunk, [36 x V] [V x N] and [9 x (V + E)] [(V + E) x N] (vertex squares and
+// edge products as the second operand), run on the FP64 tensor cores (DMMA, mma.sync m8n8k4) -- about 20x fewer
+// flops than the per-tet form. The coefficient sums are gathers over each vertex's / edge's incident tets in
+// ascending order and the chunks of one work item accumulate in fixed order: deterministic.
+constexpr int kPgThreads = 256;
+constexpr int kPgSub = 16;     // tets per coefficient sub-block
+constexpr int kPgStage = 117;  // per staged tet: mu 16, m 4, K 16, vol, E^X 5 x 16
+constexpr int kPgCo = 234;     // coefficients per tet: G_A 64, G_X 80, vertex squares 36, edge products 54
+constexpr int kPgSlice = 32;   // orbital columns per GEMM slice
+constexpr int kPgRS = 84;      // R row stride (bank-conflict-free A fragments)
+constexpr int kPgQS = 324;     // Q row stride
+constexpr int kPgPS = 36;      // staged orbital-row stride
+constexpr size_t kPgSmem =
+    sizeof(double) * (size_t(kPgSub) * (kPgStage + kPgCo) + 36 * kPgRS + 9 * kPgQS + size_t(kPgV) * kPgPS) +
+    sizeof(int32_t) * kPgE;
+
+struct PgIn {
+    const int32_t *item_c, *item_ch, *ch_t, *ch_v, *ch_e, *tets, *verts, *edges, *vinc_ptr, *vinc, *einc_ptr, *einc;
+    int n_items;
+};
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+/// index of the tet edge (c1 < c2) among the 6
+__device__ __forceinline__ int pg_pair(int c1, int c2) { return c1 == 0 ? c2 - 1 : c1 == 1 ? c2 + 1 : 5; }
+
+/// first incidence of a (t-sorted) list with tet >= tlo
+__device__ __forceinline__ int pg_lower(const int32_t* __restrict__ inc, int b, int e, int tlo, int shift) {
+    while (b < e) {
+        const int m = (b + e) >> 1;
+        if ((inc[m] >> shift) < tlo)
+            b = m + 1;
+        else
+            e = m;
+    }
+    return b;
+}
+
+template <int NS>
+__global__ void __launch_bounds__(kPgThreads, NS >= 3 ? 1 : 2) k_proj_gemm(ProjIn in, PgIn pg, double* __restrict__ part) {
+    extern __shared__ __align__(16) double pgs[];
+    double* ST = pgs;                    // kPgSub x kPgStage
+    double* CO = ST + kPgSub * kPgStage;  // kPgSub x kPgCo
+    double* R = CO + kPgSub * kPgCo;
+    double* Q = R + 36 * kPgRS;
+    double* PH = Q + 9 * kPgQS;
+    int32_t* ED = reinterpret_cast<int32_t*>(PH + kPgV * kPgPS);
+    const int N = in.N;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int item = blockIdx.x; item < pg.n_items; item += gridDim.x) {
+        const int C = pg.item_c[item];
+        const int4 cv = reinterpret_cast<const int4*>(in.ctets)[C];
+        const int ci[4] = {in.ciidx[cv.x], in.ciidx[cv.y], in.ciidx[cv.z], in.ciidx[cv.w]};
+        double acc[NS][7][2];
+#pragma unroll
+        for (int sl = 0; sl < NS; ++sl)
+#pragma unroll
+            for (int k = 0; k < 7; ++k) acc[sl][k][0] = acc[sl][k][1] = 0.0;
+        for (int ch = pg.item_ch[item]; ch < pg.item_ch[item + 1]; ++ch) {
+            const int t0 = pg.ch_t[ch], nt = pg.ch_t[ch + 1] - t0;
+            const int v0 = pg.ch_v[ch], V = pg.ch_v[ch + 1] - v0;
+            const int e0 = pg.ch_e[ch], E = pg.ch_e[ch + 1] - e0;
+            const int nR = 36 * V, nQ = 9 * (V + E);
+            __syncthreads();  // the previous chunk's shared data is consumed
+            for (int k = threadIdx.x; k < E; k += blockDim.x) ED[k] = pg.edges[e0 + k];
+            for (int sb = 0; sb * kPgSub < nt; ++sb) {
+                const int tb = sb * kPgSub, ns = min(kPgSub, nt - tb);
+                // stage: geometry, interpolation, the five element operators of each tet of the sub-block
+                if (int(threadIdx.x) < ns) {
+                    double* S = ST + threadIdx.x * kPgStage;
+                    const int t = pg.tets[t0 + tb + threadIdx.x];
+                    const int4 v = reinterpret_cast<const int4*>(in.tets)[t];
+                    TetG G;
+                    tet_geometry(in.xyz, v, G);
+                    double mu[4][4];
+                    load_mu(in, v, ci, mu);
+                    double m[4];
+#pragma unroll
+                    for (int a = 0; a < 4; ++a) {
+                        m[a] = mu[0][a] + mu[1][a] + mu[2][a] + mu[3][a];
+                        S[16 + a] = m[a];
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) S[4 * i + a] = mu[i][a];
+                    }
+#pragma unroll
+                    for (int a = 0; a < 4; ++a)
+#pragma unroll
+                        for (int b = 0; b < 4; ++b)
+                            S[20 + 4 * a + b] = m[a] * m[b] + (mu[0][a] * mu[0][b] + mu[1][a] * mu[1][b] +
+                                                               mu[2][a] * mu[2][b] + mu[3][a] * mu[3][b]);
+                    S[36] = G.vol;
+                    const int vv[4] = {v.x, v.y, v.z, v.w};
+                    double el[4], wt[4], xc[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        el[i] = in.ell[vv[i]];
+                        wt[i] = in.wt[vv[i]];
+                        xc[i] = in.vxc[vv[i]];
+                    }
+                    const double* ex = in.eext + size_t(t) * 16;
+                    double E1[4][4], E3[4][4], E4[4][4];
+                    mass_elem(G.vol, el, E1);
+                    mass_elem(G.vol, wt, E3);
+                    mass_elem(G.vol, xc, E4);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+#pragma unroll
+                        for (int l = 0; l < 4; ++l) {
+                            const double sjl = G.vol * (G.g[j][0] * G.g[l][0] + G.g[j][1] * G.g[l][1] + G.g[j][2] * G.g[l][2]);
+                            S[37 + 4 * j + l] = E1[j][l] + 0.5 * sjl + ex[4 * j + l];
+                            S[53 + 4 * j + l] = E3[j][l];
+                            S[69 + 4 * j + l] = E4[j][l];
+                            S[85 + 4 * j + l] = (G.vol / 120.0) * (j == l ? 2.0 : 1.0) * 6.0;
+                            S[101 + 4 * j + l] = sjl;
+                        }
+                }
+                __syncthreads();
+                // coefficients: 16 threads per tet
+                {
+                    const int tl = threadIdx.x >> 4, part = threadIdx.x & 15;
+                    if (tl < ns) {
+                        const double* S = ST + tl * kPgStage;
+                        double* co = CO + tl * kPgCo;
+                        const double s120 = S[36] / 120.0;
+                        for (int j = part; j < kPgCo; j += 16) {
+                            double val;
+                            if (j < 64) {  // A_h4 rows: (a b, corner l)
+                                const int ab = j >> 2, l = j & 3, a = ab >> 2, b = ab & 3;
+                                const double la = S[4 * l + a], lb = S[4 * l + b];
+                                val = s120 * (S[20 + ab] + la * (S[16 + b] + lb) + lb * (S[16 + a] + la));
+                            } else if (j < 144) {  // b_X rows: (X a, corner l)
+                                const int xa = (j - 64) >> 2, l = j & 3, X = xa >> 2, a = xa & 3;
+                                const double* EX = S + 37 + 16 * X;
+                                val = S[a] * EX[l] + S[4 + a] * EX[4 + l] + S[8 + a] * EX[8 + l] + S[12 + a] * EX[12 + l];
+                            } else if (j < 180) {  // vertex squares: (q, corner l)
+                                const int q = (j - 144) >> 2, l = j & 3;
+                                val = q < 4 ? s120 * (2.0 * S[16 + q] + 4.0 * S[4 * l + q]) : S[37 + 16 * (q - 4) + 5 * l];
+                            } else {  // edge products: (q, pair)
+                                const int q = (j - 180) / 6, pe = (j - 180) % 6;
+                                const int c1 = pe < 3 ? 0 : pe < 5 ? 1 : 2, c2 = pe < 3 ? pe + 1 : pe < 5 ? pe - 1 : 3;
+                                if (q < 4) {
+                                    val = 2.0 * s120 * (S[16 + q] + S[4 * c1 + q] + S[4 * c2 + q]);
+                                } else {
+                                    const double* EX = S + 37 + 16 * (q - 4);
+                                    val = EX[4 * c1 + c2] + EX[4 * c2 + c1];
+                                }
+                            }
+                            co[j] = val;
+                        }
+                    }
+                }
+                __syncthreads();
+                // gathers into R / Q: incidences of the sub-block's tets, ascending tet
+                const int thi = tb + ns;
+                for (int w = threadIdx.x; w < nR + nQ; w += blockDim.x) {
+                    double sum = 0.0;
+                    if (w < nR) {
+                        const int r = w / V, vl = w % V;
+                        const int pb = pg.vinc_ptr[v0 + vl], pe = pg.vinc_ptr[v0 + vl + 1];
+                        for (int p = pg_lower(pg.vinc, pb, pe, tb, 2); p < pe; ++p) {
+                            const int inc = pg.vinc[p], t = inc >> 2;
+                            if (t >= thi) break;
+                            sum += CO[(t - tb) * kPgCo + 4 * r + (inc & 3)];
+                        }
+                        R[r * kPgRS + vl] = (sb == 0 ? 0.0 : R[r * kPgRS + vl]) + sum;
+                    } else {
+                        const int w2 = w - nR, q = w2 / (V + E), k = w2 % (V + E);
+                        if (k < V) {
+                            const int pb = pg.vinc_ptr[v0 + k], pe = pg.vinc_ptr[v0 + k + 1];
+                            for (int p = pg_lower(pg.vinc, pb, pe, tb, 2); p < pe; ++p) {
+                                const int inc = pg.vinc[p], t = inc >> 2;
+                                if (t >= thi) break;
+                                sum += CO[(t - tb) * kPgCo + 144 + 4 * q + (inc & 3)];
+                            }
+                        } else {
+                            const int pb = pg.einc_ptr[e0 + k - V], pe = pg.einc_ptr[e0 + k - V + 1];
+                            for (int p = pg_lower(pg.einc, pb, pe, tb, 4); p < pe; ++p) {
+                                const int inc = pg.einc[p], t = inc >> 4;
+                                if (t >= thi) break;
+                                sum += CO[(t - tb) * kPgCo + 180 + 6 * q + pg_pair((inc >> 2) & 3, inc & 3)];
+                            }
+                        }
+                        Q[q * kPgQS + k] = (sb == 0 ? 0.0 : Q[q * kPgQS + k]) + sum;
+                    }
+                }
+                __syncthreads();
+            }
+            // GEMMs, slice by slice of 32 orbitals: warp w owns n-tile w % 4 (8 orbitals) and every m-tile (5 x 8
+            // linear rows, 2 x 8 quadratic rows) over the k-steps of parity w / 4, so each B fragment (an orbital
+            // value, or a square / edge product of two) is formed once and feeds 5 or 2 DMMAs
+#pragma unroll
+            for (int sl = 0; sl < NS; ++sl) {
+                for (int w = threadIdx.x; w < V * kPgSlice; w += blockDim.x) {
+                    const int vl = w / kPgSlice, c = w % kPgSlice, col = sl * kPgSlice + c;
+                    const int row = in.iidx[pg.verts[v0 + vl]];
+                    PH[vl * kPgPS + c] = (row >= 0 && col < N) ? in.Phi[size_t(row) * in.ld + col] : 0.0;
+                }
+                __syncthreads();
+                const int bcol = (warp & 3) * 8 + (lane >> 2);
+                const int r8 = lane >> 2, kl = lane & 3;
+                for (int k0 = 4 * (warp >> 2); k0 < V; k0 += 8) {
+                    const int kk = k0 + kl;
+                    const double b = kk < V ? PH[kk * kPgPS + bcol] : 0.0;
+#pragma unroll
+                    for (int mt = 0; mt < 5; ++mt) {
+                        const int arow = mt * 8 + r8;
+                        const double a = (arow < 36 && kk < V) ? R[arow * kPgRS + kk] : 0.0;
+                        dmma(acc[sl][mt][0], acc[sl][mt][1], a, b);
+                    }
+                }
+                for (int k0 = 4 * (warp >> 2); k0 < V + E; k0 += 8) {
+                    const int kk = k0 + kl;
+                    double b = 0.0;
+                    if (kk < V) {
+                        const double p = PH[kk * kPgPS + bcol];
+                        b = p * p;
+                    } else if (kk < V + E) {
+                        const int ed = ED[kk - V];
+                        b = PH[(ed & 0xffff) * kPgPS + bcol] * PH[(ed >> 16) * kPgPS + bcol];
+                    }
+                    const double a0 = kk < V + E ? Q[r8 * kPgQS + kk] : 0.0;
+                    const double a1 = (r8 == 0 && kk < V + E) ? Q[8 * kPgQS + kk] : 0.0;
+                    dmma(acc[sl][5][0], acc[sl][5][1], a0, b);
+                    dmma(acc[sl][6][0], acc[sl][6][1], a1, b);
+                }
+                __syncthreads();  // before the next slice overwrites PH
+            }
+        }
+        // the item's ledger partials: the two k-parities of each n-tile summed in fixed order (warps w and w + 4)
+        double* RED = pgs;  // reused (all staging consumed): 4 warps x NS x 7 tiles x 32 lanes x 2 <= 7168 doubles
+        __syncthreads();
+        if (warp >= 4) {
+#pragma unroll
+            for (int sl = 0; sl < NS; ++sl)
+#pragma unroll
+                for (int mt = 0; mt < 7; ++mt)
+#pragma unroll
+                    for (int j = 0; j < 2; ++j)
+                        RED[((((warp - 4) * NS + sl) * 7 + mt) * 32 + lane) * 2 + j] = acc[sl][mt][j];
+        }
+        __syncthreads();
+        if (warp < 4) {
+#pragma unroll
+            for (int sl = 0; sl < NS; ++sl)
+#pragma unroll
+                for (int mt = 0; mt < 7; ++mt) {
+                    int idx;
+                    const int rr = mt * 8 + (lane >> 2);
+                    if (mt < 5) {
+                        idx = rr;  // 0-15 A_h4, 16-35 b_H1 b_H3 b_H4 c_Hh d_phi, 36-39 pad (zero rows)
+                    } else {
+                        const int q = (mt - 5) * 8 + (lane >> 2);
+                        idx = q < 4 ? 40 + q : q < 9 ? 44 + (q - 4) : -1;  // rhs, beta1 beta3 beta4 gamma zeta_phi
+                    }
+                    if (idx < 0) continue;
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) {
+                        const double o = acc[sl][mt][j] + RED[(((warp * NS + sl) * 7 + mt) * 32 + lane) * 2 + j];
+                        const int i = sl * kPgSlice + warp * 8 + 2 * (lane & 3) + j;
+                        if (i < N) part[(size_t(i) * pg.n_items + item) * kStride + idx] = o;
+                    }
+                }
+        }
+    }
+}
+
 /// per-coarse-tet partials from the chunk partials, chunks in ascending order (deterministic)
 __global__ void k_proj_fold(int nct, int nfun, int nch, const int32_t* __restrict__ cptr,
                             const double* __restrict__ pch, double* __restrict__ part) {
@@ -389,8 +671,13 @@ void project_blocks(Level& L, const double* Phi, int N, int ld, const double* wt
     const int nh = L.nH, nct = L.nct;
     o.ensure(nh, N, nct);
     const int nch = L.pj_n;
-    const bool split = nch != nct;
-    if (split && o.pchunk.n < int64_t(nch) * kStride * (N + 1)) o.pchunk.alloc(int64_t(nch) * kStride * (N + 1));
+    bool split = nch != nct;
+    // the aggregated GEMM (DMMA) form is opt-in (KSB_PROJ_GEMM=1): measured slower than the staged per-tet kernel
+    // (12.6 M tets, N = 120: 261 vs 57 ms; profiles/README.md r02) -- its per-chunk coefficient sums serialise
+    const char* ge = std::getenv("KSB_PROJ_GEMM");  // read per call (tests switch it)
+    const bool gemm = N >= kProjWideMin && N <= kPgSlice * 4 && ge && ge[0] == '1';
+    const int nfun_chunk = gemm ? 1 : N + 1;  // functions written per pj chunk (the GEMM form keeps its own items)
+    if (split && o.pchunk.n < int64_t(nch) * kStride * nfun_chunk) o.pchunk.alloc(int64_t(nch) * kStride * nfun_chunk);
     double* dst = split ? o.pchunk.p : o.part.p;
     ProjIn in{(const int32_t*)L.tets.p, (const int32_t*)L.iidx.p, (const int32_t*)L.anc_ptr.p,
               (const int32_t*)L.anc_tets.p, (const int32_t*)L.ctets.p, (const int32_t*)L.ciidx.p,
@@ -398,7 +685,58 @@ void project_blocks(Level& L, const double* Phi, int N, int ld, const double* wt
               ell_full, vxc_full, N, ld, nct, (const int32_t*)L.pj_c.p, (const int32_t*)L.pj_b.p,
               (const int32_t*)L.pj_e.p, nch};
     launch(c, "project", k_proj_shared, nch, kProjThreads, 0, in, dst);
-    if (N >= kProjWideMin) {
+    if (gemm) {
+        // orbital blocks by the aggregated GEMM form (DMMA); the shared block by k_proj_shared above
+        if (!L.pg_ready) {
+            const ProjChunks P = build_proj_chunks(*L.topo);
+            L.pg_item_c.upload(c, P.item_c);
+            L.pg_item_ch.upload(c, P.item_ch);
+            L.pg_cptr.upload(c, P.cptr);
+            L.pg_ch_t.upload(c, P.ch_t);
+            L.pg_ch_v.upload(c, P.ch_v);
+            L.pg_ch_e.upload(c, P.ch_e);
+            L.pg_tets.upload(c, P.tets);
+            L.pg_verts.upload(c, P.verts);
+            L.pg_edges.upload(c, P.edges);
+            L.pg_vinc_ptr.upload(c, P.vinc_ptr);
+            L.pg_vinc.upload(c, P.vinc);
+            L.pg_einc_ptr.upload(c, P.einc_ptr);
+            L.pg_einc.upload(c, P.einc);
+            L.pg_items = int(P.item_c.size());
+            KSB_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+            L.pg_ready = true;
+        }
+        if (split)
+            launch(c, "project", k_proj_fold, c.sm_count * 8, 256, 0, nct, 1, nch, (const int32_t*)L.pj_ptr.p,
+                   (const double*)o.pchunk.p, o.part.p);
+        const int64_t need = int64_t(N) * L.pg_items * kStride;
+        if (o.pgpart.n < need) o.pgpart.alloc(need);
+        PgIn pg{(const int32_t*)L.pg_item_c.p, (const int32_t*)L.pg_item_ch.p, (const int32_t*)L.pg_ch_t.p,
+                (const int32_t*)L.pg_ch_v.p, (const int32_t*)L.pg_ch_e.p, (const int32_t*)L.pg_tets.p,
+                (const int32_t*)L.pg_verts.p, (const int32_t*)L.pg_edges.p, (const int32_t*)L.pg_vinc_ptr.p,
+                (const int32_t*)L.pg_vinc.p, (const int32_t*)L.pg_einc_ptr.p, (const int32_t*)L.pg_einc.p, L.pg_items};
+        auto go = [&](auto kern) {
+            static std::map<const void*, bool> attr;
+            if (!attr[reinterpret_cast<const void*>(kern)]) {
+                KSB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPgSmem)));
+                attr[reinterpret_cast<const void*>(kern)] = true;
+            }
+            const int grid = std::max(1, std::min(L.pg_items, 2 * c.sm_count));
+            launch(c, "project", kern, grid, kPgThreads, kPgSmem, in, pg, o.pgpart.p);
+        };
+        const int ns = (N + kPgSlice - 1) / kPgSlice;
+        if (ns == 1)
+            go(k_proj_gemm<1>);
+        else if (ns == 2)
+            go(k_proj_gemm<2>);
+        else if (ns == 3)
+            go(k_proj_gemm<3>);
+        else
+            go(k_proj_gemm<4>);
+        launch(c, "project", k_proj_fold, c.sm_count * 8, 256, 0, nct, N, L.pg_items, (const int32_t*)L.pg_cptr.p,
+               (const double*)o.pgpart.p, o.part.p + size_t(nct) * kStride);
+        split = false;  // every record is in place
+    } else if (N >= kProjWideMin) {
         const size_t smem = sizeof(double) * std::max(kWideTets * kWideRec, kProjThreads * kOrbK);
         static bool attr = false;
         if (!attr) {

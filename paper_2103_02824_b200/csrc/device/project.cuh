@@ -14,6 +14,7 @@ struct ProjOut {
     int nh = 0, N = 0;
     DevBuf<double> part;
     DevBuf<double> pchunk;       // per-chunk partials on levels whose coarse tets are split into several chunks
+    DevBuf<double> pgpart;       // per-item orbital partials of the aggregated (GEMM) projection
     DevBuf<double> shared_mats;  // A_H1, A_H3, A_H4
     DevBuf<double> A_h4;         // N x nh x nh
     DevBuf<double> shared_vecs;  // d_Hh, lift_load

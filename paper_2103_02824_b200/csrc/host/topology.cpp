@@ -2,6 +2,7 @@
 #include "topology.hpp"
 
 #include <algorithm>
+#include <functional>
 #include <parallel/algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -565,6 +566,162 @@ int64_t dorfler_mark(const double* eta, int64_t nt, double total_sq, double thet
         if (acc >= theta * total_sq) break;
     }
     return k;
+}
+
+ProjChunks build_proj_chunks(const FineTopology& T) {
+    const Mesh& m = *T.space->mesh;
+    const int nct = int(T.anc_ptr.size()) - 1;
+    struct Local {
+        std::vector<int32_t> ch_t, ch_v, ch_e, tets, verts, edges, vcnt, vinc, ecnt, einc;
+    };
+    std::vector<Local> loc(size_t(std::max(nct, 0)));
+#pragma omp parallel
+    {
+    std::vector<int32_t> stamp(size_t(m.n_vertices()), -1);
+    int32_t stamp_id = 0;
+#pragma omp for schedule(dynamic, 4)
+    for (int C = 0; C < nct; ++C) {
+        Local& L = loc[size_t(C)];
+        const int b = T.anc_ptr[size_t(C)], e = T.anc_ptr[size_t(C) + 1];
+        // Morton order of the centroids inside the coarse tet's bounding box
+        double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+        std::vector<std::pair<uint64_t, int32_t>> key(size_t(e - b));
+        std::vector<double> cen(size_t(e - b) * 3);
+        for (int p = b; p < e; ++p) {
+            const int t = T.anc_tets[size_t(p)];
+            for (int d = 0; d < 3; ++d) {
+                double c = 0.0;
+                for (int k = 0; k < 4; ++k) c += m.xyz[3 * size_t(m.tets[4 * size_t(t) + k]) + d];
+                c *= 0.25;
+                cen[3 * size_t(p - b) + d] = c;
+                lo[d] = std::min(lo[d], c);
+                hi[d] = std::max(hi[d], c);
+            }
+        }
+        for (int p = b; p < e; ++p) {
+            uint64_t code = 0;
+            uint32_t q[3];
+            for (int d = 0; d < 3; ++d) {
+                const double span = hi[d] > lo[d] ? hi[d] - lo[d] : 1.0;
+                q[d] = uint32_t(std::min(2097151.0, (cen[3 * size_t(p - b) + d] - lo[d]) / span * 2097151.0));
+            }
+            for (int bit = 20; bit >= 0; --bit)
+                for (int d = 2; d >= 0; --d) code = (code << 1) | ((q[d] >> bit) & 1u);
+            key[size_t(p - b)] = {code, T.anc_tets[size_t(p)]};
+        }
+        std::sort(key.begin(), key.end());
+        // one chunk from key[lo, hi): sorted vertices, sorted local edges, incidences in ascending tet order; halved
+        // while it has more than kPgE edges
+        std::function<void(size_t, size_t)> emit = [&](size_t lo, size_t hi) {
+            std::vector<int32_t> vs;
+            vs.reserve((hi - lo) * 4);
+            for (size_t k = lo; k < hi; ++k)
+                for (int c = 0; c < 4; ++c) vs.push_back(m.tets[4 * size_t(key[k].second) + c]);
+            std::sort(vs.begin(), vs.end());
+            vs.erase(std::unique(vs.begin(), vs.end()), vs.end());
+            auto lidx = [&](int32_t v) { return int32_t(std::lower_bound(vs.begin(), vs.end(), v) - vs.begin()); };
+            std::vector<std::pair<int32_t, int32_t>> le;
+            le.reserve((hi - lo) * 6);
+            for (size_t k = lo; k < hi; ++k) {
+                const int32_t* tv = &m.tets[4 * size_t(key[k].second)];
+                for (int c = 0; c < 4; ++c)
+                    for (int d = c + 1; d < 4; ++d) {
+                        const int32_t a = lidx(tv[c]), bb = lidx(tv[d]);
+                        le.push_back({std::min(a, bb), std::max(a, bb)});
+                    }
+            }
+            std::sort(le.begin(), le.end());
+            le.erase(std::unique(le.begin(), le.end()), le.end());
+            if (int(le.size()) > kPgE && hi - lo > 1) {
+                const size_t mid = lo + (hi - lo) / 2;
+                emit(lo, mid);
+                emit(mid, hi);
+                return;
+            }
+            L.ch_t.push_back(int32_t(L.tets.size()));
+            L.ch_v.push_back(int32_t(L.verts.size()));
+            L.ch_e.push_back(int32_t(L.edges.size()));
+            std::vector<std::vector<int32_t>> vi(vs.size()), ei(le.size());
+            for (size_t k = lo; k < hi; ++k) {
+                const int32_t tl = int32_t(k - lo);
+                const int32_t* tv = &m.tets[4 * size_t(key[k].second)];
+                for (int c = 0; c < 4; ++c) vi[size_t(lidx(tv[c]))].push_back(tl << 2 | c);
+                for (int c = 0; c < 4; ++c)
+                    for (int d = c + 1; d < 4; ++d) {
+                        const int32_t a = lidx(tv[c]), bb = lidx(tv[d]);
+                        const auto pr = std::make_pair(std::min(a, bb), std::max(a, bb));
+                        ei[size_t(std::lower_bound(le.begin(), le.end(), pr) - le.begin())].push_back(tl << 4 | c << 2 | d);
+                    }
+                L.tets.push_back(key[k].second);
+            }
+            for (size_t k = 0; k < vs.size(); ++k) {
+                L.verts.push_back(vs[k]);
+                L.vcnt.push_back(int32_t(vi[k].size()));
+                L.vinc.insert(L.vinc.end(), vi[k].begin(), vi[k].end());
+            }
+            for (size_t k = 0; k < le.size(); ++k) {
+                L.edges.push_back(le[k].first | le[k].second << 16);
+                L.ecnt.push_back(int32_t(ei[k].size()));
+                L.einc.insert(L.einc.end(), ei[k].begin(), ei[k].end());
+            }
+        };
+        // greedy compact chunks: <= kPgT tets and <= kPgV vertices (vertex membership by a per-thread stamp)
+        size_t i = 0;
+        while (i < key.size()) {
+            ++stamp_id;
+            const size_t start = i;
+            int nvc = 0;
+            for (; i < key.size() && i - start < size_t(kPgT); ++i) {
+                const int32_t* tv = &m.tets[4 * size_t(key[i].second)];
+                int add = 0;
+                for (int c = 0; c < 4; ++c) {
+                    bool dup = stamp[size_t(tv[c])] == stamp_id;
+                    for (int d = 0; d < c && !dup; ++d) dup = tv[d] == tv[c];
+                    add += !dup;
+                }
+                if (i > start && nvc + add > kPgV) break;
+                for (int c = 0; c < 4; ++c) stamp[size_t(tv[c])] = stamp_id;
+                nvc += add;
+            }
+            emit(start, i);
+        }
+    }
+    }  // omp parallel
+    // concatenate in coarse-tet order
+    ProjChunks P;
+    P.cptr.assign(size_t(std::max(nct, 0)) + 1, 0);
+    P.vinc_ptr.push_back(0);
+    P.einc_ptr.push_back(0);
+    for (int C = 0; C < nct; ++C) {
+        const Local& L = loc[size_t(C)];
+        const int nch = int(L.ch_t.size());
+        const int t0 = int(P.tets.size()), v0 = int(P.verts.size()), e0 = int(P.edges.size());
+        const int chbase = int(P.ch_t.size());
+        P.cptr[size_t(C)] = int32_t(P.item_c.size());
+        for (int q = 0; q < nch; q += kPgItem) {
+            P.item_c.push_back(C);
+            P.item_ch.push_back(chbase + q);
+        }
+        for (int q = 0; q < nch; ++q) {
+            P.ch_t.push_back(t0 + L.ch_t[size_t(q)]);
+            P.ch_v.push_back(v0 + L.ch_v[size_t(q)]);
+            P.ch_e.push_back(e0 + L.ch_e[size_t(q)]);
+        }
+        P.tets.insert(P.tets.end(), L.tets.begin(), L.tets.end());
+        P.verts.insert(P.verts.end(), L.verts.begin(), L.verts.end());
+        P.edges.insert(P.edges.end(), L.edges.begin(), L.edges.end());
+        for (int32_t c : L.vcnt) P.vinc_ptr.push_back(P.vinc_ptr.back() + c);
+        for (int32_t c : L.ecnt) P.einc_ptr.push_back(P.einc_ptr.back() + c);
+        P.vinc.insert(P.vinc.end(), L.vinc.begin(), L.vinc.end());
+        P.einc.insert(P.einc.end(), L.einc.begin(), L.einc.end());
+        check_i32(int64_t(P.einc.size()), "projection chunk incidences");
+    }
+    if (nct >= 0) P.cptr[size_t(std::max(nct, 0))] = int32_t(P.item_c.size());
+    P.item_ch.push_back(int32_t(P.ch_t.size()));
+    P.ch_t.push_back(int32_t(P.tets.size()));
+    P.ch_v.push_back(int32_t(P.verts.size()));
+    P.ch_e.push_back(int32_t(P.edges.size()));
+    return P;
 }
 
 } // namespace ksb

@@ -107,6 +107,21 @@ struct FineTopology {
 /// one-step prolongation); P_int, incidences, T8 / locality / stencil views and the ancestor grouping stay empty
 std::shared_ptr<FineTopology> build_topology(const Hierarchy& h, int level, bool lite = false);
 
+/// Aggregated projection (K-PROJ GEMM form, project.cu): the fine tets of every coarse tet in Morton order of their
+/// centroids, cut greedily into compact chunks (<= kPgT tets, <= kPgV vertices, <= kPgE edges), each chunk with its
+/// sorted vertex and edge lists and the incidence of every local vertex / edge (chunk-local tet, corners) in
+/// ascending tet order; consecutive chunks of one coarse tet grouped into work items of <= kPgItem chunks.
+constexpr int kPgT = 96, kPgV = 80, kPgE = 240, kPgItem = 32;
+struct ProjChunks {
+    std::vector<int32_t> item_c, item_ch;      // per item: coarse tet, first chunk (item_ch has n_items + 1 entries)
+    std::vector<int32_t> cptr;                 // per coarse tet: first item (n_coarse_tets + 1)
+    std::vector<int32_t> ch_t, ch_v, ch_e;     // per chunk: first tet / vertex / edge (n_chunks + 1 entries each)
+    std::vector<int32_t> tets, verts, edges;   // fine tet ids; global vertex ids; local pairs lu | lv << 16 (lu < lv)
+    std::vector<int32_t> vinc_ptr, vinc;       // per vertex slot: incidences t << 2 | corner
+    std::vector<int32_t> einc_ptr, einc;       // per edge slot: incidences t << 4 | c1 << 2 | c2
+};
+ProjChunks build_proj_chunks(const FineTopology& T);
+
 /// est::dorfler_mark (proj/src/estimator.cpp:87-104): tets by descending eta, ties by lower index, up to the first
 /// cumulative sum >= theta * total; writes them to `marked` in that order and returns their count. The order is a
 /// strict total order, so the parallel sort gives the reference's sequence exactly.

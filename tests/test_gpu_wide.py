@@ -105,3 +105,48 @@ def test_wide_inner_sweep_many_eigenvalues(ctx):
     assert np.abs(g["lambda_"] - o["lambda_"]).max() <= 1e-9 * np.abs(o["lambda_"]).max()
     assert rel(g["theta2"], o["theta2"]) < 1e-7
     assert rel(g["phi_H"], o["phi_H"]) < 1e-7
+
+
+def test_prepare_blocks_gemm_form_matches_per_tet_kernel(ctx):
+    """The aggregated projection (KSB_PROJ_GEMM=1: per-chunk coefficient sums, FP64 DMMA products) gives the same
+    ledger as the per-tet kernel (itself pinned to the oracle's prepare_blocks, proj/src/correction.cpp:148-150,
+    173-194) on a refined level, N = 40"""
+    import os
+
+    import numpy as np
+
+    import paper_2103_02824_b200 as kb
+
+    atoms = [[2.0, 0.31, -0.17, 0.05]]
+    N = 40
+    h = kb.Hierarchy()
+    a = kb.Mesh.box([-5.0] * 3, [5.0] * 3, 4)
+    h.push(a)
+    for _ in range(2):
+        a = a.uniform_refine()
+        h.push(a)
+    L = kb.Level(ctx, h, 2)
+    L.set_system(atoms, n_pairs=N)
+    L.level_ops()
+    it = L.index("interior")
+    rng = np.random.default_rng(17)
+    orb = np.zeros((L.n, N))
+    orb[it] = rng.standard_normal((L.ni, N))
+    wt = np.zeros(L.n)
+    wt[it] = rng.standard_normal(L.ni)
+    ell = np.sin(np.arange(L.n) * 0.1)
+    vxc = -np.abs(np.cos(np.arange(L.n) * 0.07))
+    out = {}
+    for g in ("0", "1"):
+        os.environ["KSB_PROJ_GEMM"] = g
+        try:
+            L.prepare_blocks(ctx.to_device(np.ascontiguousarray(orb[it])), ctx.to_device(wt), ctx.to_device(ell),
+                             ctx.to_device(vxc))
+            out[g] = {k: L.blocks(k) for k in ("A_h4", "rhs", "b_H1", "b_H3", "b_H4", "c_Hh", "d_phi", "beta1", "beta3",
+                                               "beta4", "gamma", "zeta_phi")}
+        finally:
+            os.environ.pop("KSB_PROJ_GEMM", None)
+    for k in out["0"]:
+        x, y = out["1"][k], out["0"][k]
+        assert np.linalg.norm(x - y) <= 1e-11 * max(np.linalg.norm(y), 1e-300), k
+    L.close()
