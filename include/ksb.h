@@ -124,7 +124,12 @@ int ksb_level_sizes(const ksb_level* l, int64_t sizes[10]);
  * 11 stencil (DIA) view, 16 int32: {runs, centre run length 3, other run length, 1 if on the locality order,
  * first offset of each run (centre run first), [15] = n when the rows are an n^3 grid (else 0)}; runs = 0 when
  * the level has none (the solver's sliding-window
- * SpMM then does not apply) */
+ * SpMM then does not apply)
+ * 12 union-tile view sizes, 3 int32 {tiles, entries, rows per tile R} (tiles = 0 without the view); 13 tile rows
+ * (tiles*R ordered rows, -1 padded) 14 entry ptr (tiles+1) 15 entries (ordered column per entry, padding entries
+ * hold a valid row) 16 natural CSR slot of each of the R dense values per entry (entries*R, -1 = zero) -- the
+ * wide-block SpMM's tiling of the locality-ordered pattern; 17 natural CSR slot of each locality-ordered slot
+ * (nnz_ii) */
 int ksb_level_index(const ksb_level* l, int what, void* h_dst);
 
 /* ---------------- operators (interior blocks stored on the shared pattern) ----------------

@@ -300,7 +300,14 @@ class Level:
                 "interior": (4, np.int32, self.ni), "pint_col": (5, np.int32, self.ni * 4),
                 "pint_val": (6, np.float64, self.ni * 4), "t8_col": (7, np.int32, self.ni * 16), "lo_perm": (8, np.int32, self.ni),
                 "lo_ptr": (9, np.int32, self.ni + 1), "lo_col": (10, np.int32, self.nnz_ii),
-                "dia": (11, np.int32, 16)}[what]
+                "dia": (11, np.int32, 16), "ut_sizes": (12, np.int32, 3), "lo_map": (17, np.int32, self.nnz_ii)}
+        if what in ("ut_rows", "ut_eptr", "ut_ent", "ut_map"):
+            nt, ne, R = (int(x) for x in self.index("ut_sizes"))
+            spec["ut_rows"] = (13, np.int32, nt * R)
+            spec["ut_eptr"] = (14, np.int32, nt + 1)
+            spec["ut_ent"] = (15, np.int32, ne)
+            spec["ut_map"] = (16, np.int32, ne * R)
+        spec = spec[what]
         out = np.empty(spec[2], spec[1])
         check(lib.ksb_level_index(self._h, spec[0], out.ctypes.data_as(C.c_void_p)))
         return out

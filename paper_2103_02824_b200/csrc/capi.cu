@@ -511,6 +511,16 @@ int ksb_level_index(const ksb_level* l, int what, void* dst) {
                 std::memcpy(dst, info, sizeof info);
                 break;
             }
+            case 12: {  // union-tile view sizes: {tiles, entries, rows per tile} (3 int32; tiles = 0 without the view)
+                int32_t info[3] = {T.ut_nt, int32_t(T.ut_ent.size()), ksb::kUtR};
+                std::memcpy(dst, info, sizeof info);
+                break;
+            }
+            case 13: put(T.ut_rows); break;
+            case 14: put(T.ut_eptr); break;
+            case 15: put(T.ut_ent); break;
+            case 16: put(T.ut_map); break;
+            case 17: put(T.lo_map); break;
             default: ksb::raise(KSB_INVALID_ARGUMENT, "unknown index array");
         }
     });

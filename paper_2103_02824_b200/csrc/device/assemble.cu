@@ -312,6 +312,19 @@ const double* Level::lo_values(int id) {
     return M.lo.p;
 }
 
+const double* Level::ut_values(int id) {
+    Mat& M = mats[id];
+    if (!M.valid) raise(KSB_INVALID_ARGUMENT, "matrix not assembled");
+    if (ut_map.n == 0) return nullptr;
+    if (M.ut_version != M.version) {
+        if (M.ut.n < ut_map.n) M.ut.alloc(ut_map.n);
+        launch(*ctx, "lo_pack", k_sell_pack, grid_for(*ctx, ut_map.n, 256), 256, 0, int64_t(ut_map.n),
+               (const int32_t*)ut_map.p, (const double*)M.ii.p, M.ut.p);
+        M.ut_version = M.version;
+    }
+    return M.ut.p;
+}
+
 Mat& Level::mat(int id) {
     if (id < 0 || id >= kMaxMats) raise(KSB_INVALID_ARGUMENT, "matrix id out of range");
     Mat& m = mats[id];

@@ -18,6 +18,7 @@
 // K4: x, p, r in, x, p out) instead of 9 with the textbook x/r and p passes.
 #include <algorithm>
 #include <map>
+#include <type_traits>
 #include <cstdlib>
 #include <cstring>
 
@@ -1560,6 +1561,197 @@ __global__ void __launch_bounds__(kZwThreads, 1) k_spmm_dia_zw(int ni, Cols cc, 
     k1_epilogue(sm, N, cc, s);
 }
 
+// ---------------- K1 (union-tile variant, N > 16 on a locality order): G lanes per tile of <= kUtR rows ----------------
+/// Tiles of the level's union-tile view (host/topology.hpp). A group of G lanes (lane l owns the interleaved column
+/// pairs of the FULL layout, two 16-byte loads per row) walks the union of its tile's columns once: it gathers each
+/// X row once and feeds it from registers to all kUtR tile rows with the entry's dense value vector (zero where a row
+/// does not hold the column) -- k_spmm_dot gathers a row once per nonzero and broadcasts (col, val) by shuffles.
+/// No per-entry dispatch: the inner loop is loads and FMAs only. The tile's columns and values are staged in shared
+/// memory by bulk async copies one warp step ahead (two buffers per warp on mbarriers, 32 / G tiles per step) and
+/// read with broadcast loads. Per row the products are accumulated in ascending column order, as in k_spmm_dot (the
+/// zero products of the other rows' columns change nothing). With a shift operator the per-column coefficient
+/// a + sigma_j b is formed first, so one accumulator set serves (A + sigma_j B).
+inline size_t ut_tile_bytes(bool shift) { return size_t(kUtE) * 4 + size_t(kUtE) * kUtR * 8 * (shift ? 2 : 1); }
+inline size_t ut_smem(int G, int threads, bool shift) {
+    const size_t nw = threads / 32, tpw = 32 / G;
+    return nw * 4 * G * sizeof(double) + nw * 2 * tpw * ut_tile_bytes(shift) + nw * 2 * sizeof(uint64_t);
+}
+
+template <int G, bool SHIFT, int UB, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_spmm_ut(int nt, Cols cc, const int32_t* __restrict__ trows,
+                                                     const int32_t* __restrict__ eptr, const int32_t* __restrict__ ent,
+                                                     const double* __restrict__ A, const double* __restrict__ Bv,
+                                                     const double* __restrict__ P, double* __restrict__ AP, CgDev s) {
+    extern __shared__ double sm[];
+    constexpr int CPL = 4, R = kUtR, TPW = 32 / G, W = 4 * G;
+    constexpr int VS = SHIFT ? 2 : 1;
+    constexpr int TB = kUtE * 4 + kUtE * R * 8 * VS;  // staged bytes per tile
+    static_assert(R == 4, "the value loads below read 4 doubles per entry");
+    const int N = cc.N, ld = cc.ld;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nwb = NT / 32;
+    const int g = lane / G, l = lane % G;
+    char* stage = reinterpret_cast<char*>(sm) + size_t(nwb) * W * sizeof(double) + size_t(wib) * 2 * TPW * TB;
+    uint64_t* bars =
+        reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(sm) + size_t(nwb) * W * sizeof(double) + size_t(nwb) * 2 * TPW * TB) +
+        wib * 2;
+    // the lane's two column pairs (FULL layout); a pair that starts at or past N is clamped onto the block's last
+    // pair, so every gather is unconditional (same 128-byte lines as the neighbouring lanes); its products land in
+    // accumulators that are never stored or read
+    const int c0 = full_col<G>(l, 0), c1 = full_col<G>(l, 2);
+    const bool ok0 = c0 < N, ok1 = c1 < N;
+    const int cmax = (N - 1) & ~1;
+    const double* P0 = P + min(c0, cmax);
+    const double* P1 = P + min(c1, cmax);
+    const uint32_t uld = uint32_t(ld);
+    double pd[CPL], sg[CPL];
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) {
+        pd[q] = 0.0;
+        const int c = full_col<G>(l, q);
+        sg[q] = (SHIFT && c < N) ? s.sigma[c] : 0.0;
+    }
+    const TileWalk tw((nt + TPW - 1) / TPW);
+    const int ksteps = tw.t0 < tw.tend ? (tw.tend - tw.t0 + tw.step - 1) / tw.step : 0;
+    auto fetch = [&](int k) {  // group leaders: the group's tile of warp step k into buffer k & 1
+        if (l == 0 && k < ksteps) {
+            const int t = (tw.t0 + k * tw.step) * TPW + g;
+            uint64_t* bar = bars + (k & 1);
+            if (t < nt) {
+                const int e0 = __ldg(eptr + t), ne = __ldg(eptr + t + 1) - e0;
+                char* b = stage + size_t((k & 1) * TPW + g) * TB;
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_expect_tx(bar, uint32_t(ne * 4 + ne * R * 8 * VS));
+                bulk_g2s(b, ent + e0, uint32_t(ne * 4), bar);
+                bulk_g2s(b + kUtE * 4, A + size_t(e0) * R, uint32_t(ne * R * 8), bar);
+                if (SHIFT) bulk_g2s(b + kUtE * 4 + kUtE * R * 8, Bv + size_t(e0) * R, uint32_t(ne * R * 8), bar);
+            } else {
+                mbar_arrive(bar);
+            }
+        }
+    };
+    if (lane == 0) {
+        mbar_init(bars, TPW);
+        mbar_init(bars + 1, TPW);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    fetch(0);
+    for (int k = 0; k < ksteps; ++k) {
+        const int t = (tw.t0 + k * tw.step) * TPW + g;
+        const bool valid = t < nt;
+        __syncwarp();  // every lane is done with the buffer step k + 1 lands in (step k - 1's)
+        fetch(k + 1);
+        const int ne = valid ? __ldg(eptr + t + 1) - __ldg(eptr + t) : 0;
+        const int myrow = (valid && l < R) ? __ldg(trows + size_t(t) * R + l) : -1;
+        const char* b = stage + size_t((k & 1) * TPW + g) * TB;
+        const int32_t* sc = reinterpret_cast<const int32_t*>(b);
+        const double* sa = reinterpret_cast<const double*>(b + kUtE * 4);
+        const double* sb = reinterpret_cast<const double*>(b + kUtE * 4 + kUtE * R * 8);
+        double acc[R][CPL];
+#pragma unroll
+        for (int i = 0; i < R; ++i)
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) acc[i][q] = 0.0;
+        mbar_wait(bars + (k & 1), (k >> 1) & 1);
+        // batches of 4 entries (the entry count is a multiple of 4): the gathers of one batch, then its products.
+        // UB == 8: two batches' gathers at once; UB == 44: software-pipelined, the next batch's gathers are in flight
+        // during the current batch's products. The groups of a warp run their own trip counts (no warp-level
+        // operation inside).
+        auto gather = [&](int e, double2 (&x0)[4], double2 (&x1)[4]) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const size_t off = size_t(uint32_t(sc[e + u])) * uld;
+                x0[u] = __ldg(reinterpret_cast<const double2*>(P0 + off));
+                x1[u] = __ldg(reinterpret_cast<const double2*>(P1 + off));
+            }
+        };
+        auto products = [&](int e, const double2 (&x0)[4], const double2 (&x1)[4]) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const double2 a01 = *reinterpret_cast<const double2*>(sa + size_t(e + u) * R);
+                const double2 a23 = *reinterpret_cast<const double2*>(sa + size_t(e + u) * R + 2);
+                const double av[R] = {a01.x, a01.y, a23.x, a23.y};
+                const double xv[CPL] = {x0[u].x, x0[u].y, x1[u].x, x1[u].y};
+                if constexpr (SHIFT) {
+                    const double2 b01 = *reinterpret_cast<const double2*>(sb + size_t(e + u) * R);
+                    const double2 b23 = *reinterpret_cast<const double2*>(sb + size_t(e + u) * R + 2);
+                    const double bv[R] = {b01.x, b01.y, b23.x, b23.y};
+#pragma unroll
+                    for (int i = 0; i < R; ++i)
+#pragma unroll
+                        for (int q = 0; q < CPL; ++q) acc[i][q] = fma(fma(sg[q], bv[i], av[i]), xv[q], acc[i][q]);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < R; ++i)
+#pragma unroll
+                        for (int q = 0; q < CPL; ++q) acc[i][q] = fma(av[i], xv[q], acc[i][q]);
+                }
+            }
+        };
+        double2 xa0[4], xa1[4], xb0[4], xb1[4];
+        if constexpr (UB == 44) {
+            if (ne > 0) gather(0, xa0, xa1);
+            int e = 0;
+            for (; e + 8 <= ne; e += 8) {
+                gather(e + 4, xb0, xb1);
+                products(e, xa0, xa1);
+                if (e + 8 < ne) gather(e + 8, xa0, xa1);
+                products(e + 4, xb0, xb1);
+            }
+            if (e < ne) products(e, xa0, xa1);
+        } else if constexpr (UB == 8) {
+            int e = 0;
+            for (; e + 8 <= ne; e += 8) {
+                gather(e, xa0, xa1);
+                gather(e + 4, xb0, xb1);
+                products(e, xa0, xa1);
+                products(e + 4, xb0, xb1);
+            }
+            if (e < ne) {
+                gather(e, xa0, xa1);
+                products(e, xa0, xa1);
+            }
+        } else {
+            for (int e = 0; e < ne; e += 4) {
+                gather(e, xa0, xa1);
+                products(e, xa0, xa1);
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+            const int r = __shfl_sync(0xffffffffu, myrow, i, G);
+            if (r >= 0) {
+                const size_t off = size_t(uint32_t(r)) * uld;
+                const double2 p0 = __ldg(reinterpret_cast<const double2*>(P0 + off));
+                const double2 p1 = __ldg(reinterpret_cast<const double2*>(P1 + off));
+                if (ok0) __stcs(reinterpret_cast<double2*>(AP + off + c0), make_double2(acc[i][0], acc[i][1]));
+                if (ok1) __stcs(reinterpret_cast<double2*>(AP + off + c1), make_double2(acc[i][2], acc[i][3]));
+                pd[0] = fma(p0.x, acc[i][0], pd[0]);
+                pd[1] = fma(p0.y, acc[i][1], pd[1]);
+                pd[2] = fma(p1.x, acc[i][2], pd[2]);
+                pd[3] = fma(p1.y, acc[i][3], pd[3]);
+            }
+        }
+    }
+    // block reduce: groups with equal l hold the same columns -- xor tree over the groups of a warp, then a
+    // fixed-order sum over the warps (k_spmm_dot's epilogue)
+#pragma unroll
+    for (int q = 0; q < CPL; ++q)
+        for (int o = 16; o >= G; o >>= 1) pd[q] += __shfl_xor_sync(0xffffffffu, pd[q], o);
+    if (lane < G) {
+#pragma unroll
+        for (int q = 0; q < CPL; ++q) sm[wib * W + full_col<G>(l, q)] = pd[q];
+    }
+    __syncthreads();
+    if (threadIdx.x < N) {
+        double t = 0.0;
+        for (int k = 0; k < nwb; ++k) t += sm[k * W + threadIdx.x];
+        s.part0[size_t(blockIdx.x) * N + threadIdx.x] = t;
+    }
+    k1_epilogue(sm, N, cc, s);
+}
+
 // ---------------- K1 (SELL-32 variant): one row per lane, all N <= 16 columns per lane ----------------
 template <int NC>
 __device__ __forceinline__ void load_row(const double* __restrict__ p, double (&x)[NC]) {
@@ -2231,6 +2423,7 @@ Plan plan_for(int N) {
 struct SellOps {
     const double *A = nullptr, *B = nullptr;  // SELL-32 values (N <= 2)
     const double* T8 = nullptr;               // T8 values (N = 16, no shift, rows of <= 16 entries)
+    const double *UT = nullptr, *UTB = nullptr;  // union-tile values (wide blocks on a locality order), shift operator
     const double* DIA = nullptr;              // tiled stencil values (dia.cuh) for dia_g lanes per row
     int dia_g = 0;
     int dia_z = 0;                            // > 0: z-marching kernel, lines per block
@@ -2436,6 +2629,37 @@ bool try_dia(Ctx& c, const Level& L, const CgWork& w, const Cols& cc, const Sell
     return false;
 }
 
+/// union-tile SpMM (blocks of more than 16 columns on levels with the view; cg_solve sets so.UT)
+template <int G, bool SHIFT>
+bool try_ut(Ctx& c, const Level& L, const CgWork& w, const Cols& cc, const SellOps& so) {
+    if constexpr (G < 8) {
+        return false;
+    } else {
+        if (!so.UT || (SHIFT && !so.UTB)) return false;
+        // 8 tiles per block: 256 threads at G = 32, 128 at G = 16, 64 at G = 8 (the staging buffers are per tile)
+        constexpr int NT = 8 * G, MINB = 512 / NT;
+        if (cc.N > NT) return false;  // the epilogue folds one column per thread
+        const size_t smt = ut_smem(G, NT, SHIFT);
+        auto go = [&](auto kern) {
+            static bool attr = false;
+            if (!attr) {
+                KSB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smt)));
+                attr = true;
+            }
+            const int want = ceil_div(ceil_div(L.ut_nt, 32 / G), NT / 32);
+            const int grid = std::max(1, std::min({want, resident_grid(c, kern, NT, smt), w.cap_blocks}));
+            launch(c, "spmm", kern, grid, NT, smt, L.ut_nt, cc, (const int32_t*)L.ut_rows.p,
+                   (const int32_t*)L.ut_eptr.p, (const int32_t*)L.ut_ent.p, so.UT, so.UTB, (const double*)w.P, w.AP,
+                   w.dev);
+            return true;
+        };
+        static const char* ube = std::getenv("KSB_UT_UB");  // gathers in flight per lane group (experiments)
+        if (ube && std::atoi(ube) == 4) return go(k_spmm_ut<G, SHIFT, 4, NT, MINB>);
+        if (ube && std::atoi(ube) == 44) return go(k_spmm_ut<G, SHIFT, 44, NT, MINB>);
+        return go(k_spmm_ut<G, SHIFT, 8, NT, MINB>);
+    }
+}
+
 template <int G, int CPL, bool SHIFT, bool SPLIT, int FULL>
 void launch_iteration(Ctx& c, const Level& L, const CgWork& w, const Cols& cc, const double* A, const double* Bv,
                       const double* Bb, double* X, int grid_s, int grid_e, const SellOps& so) {
@@ -2445,6 +2669,7 @@ void launch_iteration(Ctx& c, const Level& L, const CgWork& w, const Cols& cc, c
     grid_e = std::min(grid_e, v2 ? resident_grid(c, k_update_r<2>, kThreads, sm_e)
                                  : resident_grid(c, k_update_r<1>, kThreads, sm_e));
     if (try_sell<SHIFT>(c, L, w, cc, so)) {
+    } else if (!SPLIT && try_ut<G, SHIFT>(c, L, w, cc, so)) {
     } else if (!SHIFT && try_dia(c, L, w, cc, so)) {
     } else {
         static const char* mb = std::getenv("KSB_SPMM_MINB");
@@ -2709,6 +2934,12 @@ void cg_solve(Ctx& c, Level& L, int mat, int shift_mat, const double* h_sigma, c
         so.B = shift ? L.sell_values(shift_mat) : nullptr;
     }
     if (N == 16 && !shift) so.T8 = L.t8_values(mat);
+    // blocks of more than 16 columns on a locality order: the union-tile SpMM (KSB_SPMM_UT=0 keeps the row kernel)
+    const char* ut_env = std::getenv("KSB_SPMM_UT");
+    if (lo && p.G >= 8 && L.ut_nt > 0 && ld % 2 == 0 && !(ut_env && ut_env[0] == '0')) {
+        so.UT = L.ut_values(mat);
+        so.UTB = shift ? L.ut_values(shift_mat) : nullptr;
+    }
     // stencil levels (cfg2's lexicographic box, uniformly refined levels in the locality order): the sliding-window
     // SpMM; KSB_SPMM_DIA=0 keeps the CSR / T8 kernels
     const char* dia_env = std::getenv("KSB_SPMM_DIA");
@@ -2739,9 +2970,10 @@ void cg_solve(Ctx& c, Level& L, int mat, int shift_mat, const double* h_sigma, c
         std::memset(&key, 0, sizeof key);
         key.level_uid = L.uid;
         // every pointer a captured kernel dereferences
-        const void* ptrs[25] = {A, Bv, d_B, d_X, so.A, so.B, w.R, w.P, w.AP, w.scal.p, w.parts.p, w.ints.p,
+        const void* ptrs[29] = {A, Bv, d_B, d_X, so.A, so.B, w.R, w.P, w.AP, w.scal.p, w.parts.p, w.ints.p,
                                 d.diagA, d.diagB, so.ptr, so.col, so.T8, L.t8_col.p, L.sell_ptr.p, L.sell_col.p,
-                                L.ii_ptr.p, L.ii_col.p, L.lo_ptr.p, L.lo_col.p, so.DIA};
+                                L.ii_ptr.p, L.ii_col.p, L.lo_ptr.p, L.lo_col.p, so.DIA, so.UT, so.UTB, L.ut_ent.p,
+                                L.ut_rows.p};
         std::memcpy(key.ptrs, ptrs, sizeof ptrs);
         const int ints[10] = {mat, shift_mat, N, ld, chunk, grid_s, grid_e, cc.fixed, L.ni, L.nslices * 64 + so.dia_g * 2 + (so.dia_z > 0) + (so.dia_zt ? 1 << 30 : 0)};
         std::memcpy(key.ints, ints, sizeof ints);

@@ -33,7 +33,7 @@ struct CgDev {
 /// identity of a captured chunk of CG iterations: every kernel argument that can differ between solves
 struct CgGraphKey {
     uint64_t level_uid;  // Level::uid: never reused, so a graph of a destroyed level can never match
-    const void* ptrs[25];
+    const void* ptrs[29];
     int ints[10];
     double tol;
 };

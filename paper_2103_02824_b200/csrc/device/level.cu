@@ -85,6 +85,11 @@ void upload_level(Ctx& cx, std::shared_ptr<FineTopology> topo, Level& L) {
     L.lo_map.upload(cx, T.lo_map);
     L.lo_dslot.upload(cx, T.lo_dslot);
     L.lo_max_row = T.lo_max_row;
+    L.ut_rows.upload(cx, T.ut_rows);
+    L.ut_eptr.upload(cx, T.ut_eptr);
+    L.ut_ent.upload(cx, T.ut_ent);
+    L.ut_map.upload(cx, T.ut_map);
+    L.ut_nt = T.ut_nt;
     L.dia_ng = T.dia_ng;
     L.dia_lr = T.dia_lr;
     L.dia_lo = T.dia_lo;

@@ -49,9 +49,10 @@ struct Mat {
     DevBuf<double> sell;         // ii values in the SELL-32 order (lazily converted)
     DevBuf<double> t8;           // ii values in the T8 order (lazily converted)
     DevBuf<double> lo;           // ii values on the locality-ordered pattern (lazily converted)
+    DevBuf<double> ut;           // ii values in the union-tile order (lazily converted)
     DevBuf<double> dia;          // ii values in the tiled stencil (DIA) layout (lazily converted, see dia_values)
     uint64_t version = 0, sell_version = ~uint64_t(0), t8_version = ~uint64_t(0), lo_version = ~uint64_t(0);
-    uint64_t dia_version = ~uint64_t(0);
+    uint64_t dia_version = ~uint64_t(0), ut_version = ~uint64_t(0);
     int dia_wg = 0;              // rows per warp step the DIA values were packed for
     bool valid = false;
 };
@@ -98,6 +99,8 @@ struct Level {
     DevBuf<int32_t> t8_col, t8_map;  // T8 view (empty when a row is longer than 16)
     DevBuf<int32_t> lo_perm, lo_ptr, lo_col, lo_map, lo_dslot;  // locality-ordered pattern (topology.hpp)
     int lo_max_row = 0;
+    DevBuf<int32_t> ut_rows, ut_eptr, ut_ent, ut_map;  // union-tile view of the ordered pattern (topology.hpp)
+    int ut_nt = 0;
     // stencil (DIA) view (topology.hpp): dia_ng runs, run 0 = {-1, 0, 1}, the others of length dia_lr starting at
     // dia_first[q]; on the natural order (dia_lo = 0) or the locality order (dia_lo = 1); dia_ng = 0 without one
     int dia_ng = 0, dia_lr = 0, dia_lo = 0, dia_n = 0;
@@ -123,6 +126,8 @@ struct Level {
     /// values of matrix id on the locality-ordered pattern (converted on first use after a change); null
     /// without a locality order
     const double* lo_values(int id);
+    /// values of matrix id in the union-tile order (converted on first use after a change); null without the view
+    const double* ut_values(int id);
     /// values of matrix id in the tiled stencil layout for wg rows per warp step (dia.cuh), converted on first use
     /// after a change; null without a stencil view
     const double* dia_values(int id, int wg);

@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <functional>
+#include <iterator>
 #include <parallel/algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -101,6 +102,123 @@ namespace {
 void check_i32(int64_t x, const char* what) {
     if (x > std::numeric_limits<int32_t>::max())
         raise(KSB_INVALID_ARGUMENT, std::string(what) + " exceeds the int32 index range");
+}
+
+/// 21 bits per axis interleaved (x lowest)
+uint64_t morton3(uint32_t x, uint32_t y, uint32_t z) {
+    auto spread = [](uint64_t v) {
+        v &= 0x1fffffull;
+        v = (v | v << 32) & 0x1f00000000ffffull;
+        v = (v | v << 16) & 0x1f0000ff0000ffull;
+        v = (v | v << 8) & 0x100f00f00f00f00full;
+        v = (v | v << 4) & 0x10c30c30c30c30c3ull;
+        v = (v | v << 2) & 0x1249249249249249ull;
+        return v;
+    };
+    return spread(x) | spread(y) << 1 | spread(z) << 2;
+}
+
+/// Union-tile view of the locality-ordered pattern (topology.hpp): ordered rows sorted by the Morton code of their
+/// vertex, cut greedily into tiles of <= kUtR rows with <= kUtE distinct columns.
+void build_union_tiles(FineTopology& T, const double* xyz, const int32_t* interior, int ni) {
+    const auto& perm = T.lo_perm;
+    const auto& ptr = T.lo_ptr;
+    const auto& col = T.lo_col;
+    double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+    for (int i = 0; i < ni; ++i) {
+        const double* p = xyz + 3 * size_t(interior[perm[i]]);
+        for (int d = 0; d < 3; ++d) {
+            lo[d] = std::min(lo[d], p[d]);
+            hi[d] = std::max(hi[d], p[d]);
+        }
+    }
+    double ext = 0.0;
+    for (int d = 0; d < 3; ++d) ext = std::max(ext, hi[d] - lo[d]);
+    if (!(ext > 0.0)) ext = 1.0;
+    std::vector<std::pair<uint64_t, int32_t>> key(ni);
+#pragma omp parallel for schedule(static)
+    for (int i = 0; i < ni; ++i) {
+        const double* p = xyz + 3 * size_t(interior[perm[i]]);
+        uint32_t q[3];
+        for (int d = 0; d < 3; ++d) q[d] = uint32_t(std::min(2097151.0, (p[d] - lo[d]) / ext * 2097151.0));
+        key[i] = {morton3(q[0], q[1], q[2]), i};
+    }
+    __gnu_parallel::sort(key.begin(), key.end());
+
+    // tile boundaries: independent greedy cuts inside fixed chunks of the Morton sequence
+    const int chunk = 1 << 14, nchunks = (ni + chunk - 1) / chunk;
+    std::vector<std::vector<int32_t>> starts(nchunks);
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int c = 0; c < nchunks; ++c) {
+        const int b = c * chunk, e = std::min(ni, b + chunk);
+        std::vector<int32_t> uni, tmp;
+        int rows = 0;
+        for (int k = b; k < e; ++k) {
+            const int r = key[k].second;
+            tmp.clear();
+            std::set_union(uni.begin(), uni.end(), col.begin() + ptr[r], col.begin() + ptr[r + 1], std::back_inserter(tmp));
+            if (rows == 0 || rows == kUtR || int(tmp.size()) > kUtE) {
+                starts[c].push_back(k);
+                uni.assign(col.begin() + ptr[r], col.begin() + ptr[r + 1]);
+                rows = 1;
+            } else {
+                uni.swap(tmp);
+                ++rows;
+            }
+        }
+    }
+    std::vector<int32_t> tstart;
+    for (auto& s : starts) tstart.insert(tstart.end(), s.begin(), s.end());
+    const int nt = int(tstart.size());
+    tstart.push_back(ni);
+
+    // sizes, then the fill
+    T.ut_nt = nt;
+    T.ut_rows.assign(size_t(nt) * kUtR, -1);
+    std::vector<int64_t> ecnt(size_t(nt) + 1, 0);
+#pragma omp parallel for schedule(static)
+    for (int t = 0; t < nt; ++t) {
+        const int k0 = tstart[t], nr = tstart[t + 1] - k0;
+        int32_t rows[16];  // (sized past kUtR: keeps the sort's insertion pass in bounds for the compiler)
+        for (int i = 0; i < nr; ++i) rows[i] = key[k0 + i].second;
+        std::sort(rows, rows + nr);
+        std::vector<int32_t> uni, tmp;
+        for (int i = 0; i < nr; ++i) {
+            T.ut_rows[size_t(t) * kUtR + i] = rows[i];
+            tmp.clear();
+            std::set_union(uni.begin(), uni.end(), col.begin() + ptr[rows[i]], col.begin() + ptr[rows[i] + 1],
+                           std::back_inserter(tmp));
+            uni.swap(tmp);
+        }
+        ecnt[t + 1] = (int64_t(uni.size()) + 3) / 4 * 4;
+    }
+    for (int t = 0; t < nt; ++t) ecnt[t + 1] += ecnt[t];
+    check_i32(ecnt[nt] * kUtR, "union-tile values");
+    T.ut_eptr.resize(size_t(nt) + 1);
+    for (int t = 0; t <= nt; ++t) T.ut_eptr[t] = int32_t(ecnt[t]);
+    T.ut_ent.assign(size_t(ecnt[nt]), 0);
+    T.ut_map.assign(size_t(ecnt[nt]) * kUtR, -1);
+#pragma omp parallel for schedule(static)
+    for (int t = 0; t < nt; ++t) {
+        const int32_t* rows = T.ut_rows.data() + size_t(t) * kUtR;
+        int head[kUtR], end[kUtR], nr = 0;
+        while (nr < kUtR && rows[nr] >= 0) {
+            head[nr] = ptr[rows[nr]];
+            end[nr] = ptr[rows[nr] + 1];
+            ++nr;
+        }
+        int64_t e = ecnt[t];
+        for (;;) {
+            int32_t cmin = std::numeric_limits<int32_t>::max();
+            for (int i = 0; i < nr; ++i)
+                if (head[i] < end[i]) cmin = std::min(cmin, col[head[i]]);
+            if (cmin == std::numeric_limits<int32_t>::max()) break;
+            for (int i = 0; i < nr; ++i)
+                if (head[i] < end[i] && col[head[i]] == cmin) T.ut_map[size_t(e) * kUtR + i] = T.lo_map[head[i]++];
+            T.ut_ent[e++] = cmin;
+        }
+        for (; e < ecnt[t + 1]; ++e) T.ut_ent[e] = rows[0];  // padding: a valid row to gather, all values zero
+    }
 }
 
 } // namespace
@@ -395,6 +513,9 @@ std::shared_ptr<FineTopology> build_topology(const Hierarchy& h, int level, bool
         }
         topo->lo_max_row = wmax;
     }
+
+    // union-tile view of the ordered pattern (wide blocks; topology.hpp)
+    if (!topo->lo_perm.empty() && topo->lo_max_row <= kUtE) build_union_tiles(*topo, m.xyz.data(), S.interior.data(), ni);
 
     // stencil (DIA) view: natural order first, else the locality order
     {

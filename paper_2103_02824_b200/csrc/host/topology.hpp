@@ -86,6 +86,17 @@ struct FineTopology {
     // slot. Empty when not built.
     std::vector<int32_t> lo_perm, lo_ptr, lo_col, lo_map, lo_dslot;
     int lo_max_row = 0;
+    // Union-tile ("UT") view of the locality-ordered pattern for blocks of more than 16 columns: tiles of <= kUtR
+    // ordered rows that are neighbours in space (consecutive in the Morton order of their vertices). A tile lists
+    // the union of its rows' columns once (ascending) and stores a dense kUtR-vector of values per column (zero
+    // where a row does not hold it), so the kernel gathers every distinct X row once per tile and feeds it to all
+    // tile rows from registers, with no per-entry dispatch (~2x fewer gathered rows than row by row, ~2x the
+    // multiply-adds). ut_rows[kUtR t + i] = ordered row of tile slot i (-1: none); entries
+    // [ut_eptr[t], ut_eptr[t+1]) = ordered columns, padded to a multiple of 4 with a valid row whose values are
+    // zero; values of entry e at [kUtR e, kUtR e + kUtR); ut_map = natural CSR slot of each value (-1: zero).
+    // A tile holds <= kUtE entries. Empty when not built (no locality order, or a row longer than kUtE).
+    std::vector<int32_t> ut_rows, ut_eptr, ut_ent, ut_map;
+    int ut_nt = 0;
     // Stencil (DIA) view: the interior rows are a uniform stencil in the natural numbering (dia_lo = 0; box meshes,
     // lexicographic) or in the locality order (dia_lo = 1; uniformly refined levels): every column offset
     // (col - row) lies in a set that splits into runs of consecutive offsets -- a centre run {-1, 0, 1} and
@@ -102,6 +113,10 @@ struct FineTopology {
     std::vector<int32_t> pstep_col, prev_iidx;
     std::vector<double> pstep_val;
 };
+
+/// union-tile view limits: rows per tile and entries (distinct columns) per tile (cg.cu stages a tile's columns
+/// and dense values in shared memory: kUtE * (4 + 8 kUtR) bytes per buffer)
+constexpr int kUtR = 4, kUtE = 64;
 
 /// lite: only what a multigrid level needs (interior / boundary patterns, assembly gathers, diagonal, SELL-32 view,
 /// one-step prolongation); P_int, incidences, T8 / locality / stencil views and the ancestor grouping stay empty

@@ -41,3 +41,23 @@ for k in range(2):
     print(json.dumps({"step": k, "wall_s": round(time.time() - t2, 2)} | {kk: lg[kk] for kk in
           ("ms_bvp", "ms_hartree", "ms_project", "ms_inner", "ms_total", "cg_iterations", "inner_iterations")}
           | {"attempts": lg["attempts"][:8]}), flush=True)
+
+# per-family CUDA-event times of one more step (the context's profiling counters; graphs are off while profiling)
+import os  # noqa: E402
+
+if os.environ.get("KSB_PROBE_FAMILIES", "1") != "0":
+    ctx.sync()
+    ctx.reset_counters()
+    ctx.set_profiling(True)
+    lg = L.correction_step(lam, Phi, w, ld=ld, fixed_sweeps=10)
+    ctx.sync()
+    ctx.set_profiling(False)
+    fam = {}
+    for nm in ("assemble", "axpby", "rho_vxc", "moments", "bc", "sqload", "lift", "elementwise", "cg_setup", "spmm",
+               "cg_update_r", "cg_update_px", "cg_trueres", "cg_coop", "mg", "project", "project_asm", "coarse",
+               "inner_tridiag", "expand", "norm", "energy", "reduce"):
+        ms, cnt = ctx.kernel_time(nm)
+        if cnt:
+            fam[nm] = {"ms": round(ms, 2), "launches": int(cnt), "avg_us": round(1e3 * ms / cnt, 1)}
+    print(json.dumps({"families": fam, "n_i": L.ni, "nnz": L.nnz_ii, "N": N, "ms_total": lg["ms_total"],
+                      "ms_bvp": lg["ms_bvp"]}), flush=True)
