@@ -1572,12 +1572,17 @@ __global__ void __launch_bounds__(kZwThreads, 1) k_spmm_dia_zw(int ni, Cols cc, 
 /// zero products of the other rows' columns change nothing). With a shift operator the per-column coefficient
 /// a + sigma_j b is formed first, so one accumulator set serves (A + sigma_j B).
 inline size_t ut_tile_bytes(bool shift) { return size_t(kUtE) * 4 + size_t(kUtE) * kUtR * 8 * (shift ? 2 : 1); }
-inline size_t ut_smem(int G, int threads, bool shift) {
+inline size_t ut_smem(int G, int threads, bool shift, bool vsm) {
     const size_t nw = threads / 32, tpw = 32 / G;
-    return nw * 4 * G * sizeof(double) + nw * 2 * tpw * ut_tile_bytes(shift) + nw * 2 * sizeof(uint64_t);
+    const size_t tile = vsm ? ut_tile_bytes(shift) : size_t(kUtE) * 4;
+    return nw * 4 * G * sizeof(double) + nw * 2 * tpw * tile + nw * 2 * sizeof(uint64_t);
 }
 
-template <int G, bool SHIFT, int UB, int NT, int MINB>
+/// VSM: the tile's values are staged in shared memory with its columns (one warp per tile: G = 32). !VSM: only the
+/// columns are staged (256 bytes per tile, so the staging no longer limits the resident warps) and each entry's four
+/// values are read from global memory with the entry's gathers (one broadcast 32-byte load per lane group) -- the
+/// narrow groups (G = 8, 16: four / two tiles per warp), whose value buffers would leave 6 warps per SM.
+template <int G, bool SHIFT, int UB, int NT, int MINB, bool VSM>
 __global__ void __launch_bounds__(NT, MINB) k_spmm_ut(int nt, Cols cc, const int32_t* __restrict__ trows,
                                                      const int32_t* __restrict__ eptr, const int32_t* __restrict__ ent,
                                                      const double* __restrict__ A, const double* __restrict__ Bv,
@@ -1585,8 +1590,9 @@ __global__ void __launch_bounds__(NT, MINB) k_spmm_ut(int nt, Cols cc, const int
     extern __shared__ double sm[];
     constexpr int CPL = 4, R = kUtR, TPW = 32 / G, W = 4 * G;
     constexpr int VS = SHIFT ? 2 : 1;
-    constexpr int TB = kUtE * 4 + kUtE * R * 8 * VS;  // staged bytes per tile
+    constexpr int TB = kUtE * 4 + (VSM ? kUtE * R * 8 * VS : 0);  // staged bytes per tile
     static_assert(R == 4, "the value loads below read 4 doubles per entry");
+    static_assert(VSM || UB == 4, "values from global memory: batches of 4 entries");
     const int N = cc.N, ld = cc.ld;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nwb = NT / 32;
     const int g = lane / G, l = lane % G;
@@ -1620,10 +1626,12 @@ __global__ void __launch_bounds__(NT, MINB) k_spmm_ut(int nt, Cols cc, const int
                 const int e0 = __ldg(eptr + t), ne = __ldg(eptr + t + 1) - e0;
                 char* b = stage + size_t((k & 1) * TPW + g) * TB;
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                mbar_expect_tx(bar, uint32_t(ne * 4 + ne * R * 8 * VS));
+                mbar_expect_tx(bar, uint32_t(ne * 4 + (VSM ? ne * R * 8 * VS : 0)));
                 bulk_g2s(b, ent + e0, uint32_t(ne * 4), bar);
-                bulk_g2s(b + kUtE * 4, A + size_t(e0) * R, uint32_t(ne * R * 8), bar);
-                if (SHIFT) bulk_g2s(b + kUtE * 4 + kUtE * R * 8, Bv + size_t(e0) * R, uint32_t(ne * R * 8), bar);
+                if constexpr (VSM) {
+                    bulk_g2s(b + kUtE * 4, A + size_t(e0) * R, uint32_t(ne * R * 8), bar);
+                    if (SHIFT) bulk_g2s(b + kUtE * 4 + kUtE * R * 8, Bv + size_t(e0) * R, uint32_t(ne * R * 8), bar);
+                }
             } else {
                 mbar_arrive(bar);
             }
@@ -1641,12 +1649,13 @@ __global__ void __launch_bounds__(NT, MINB) k_spmm_ut(int nt, Cols cc, const int
         const bool valid = t < nt;
         __syncwarp();  // every lane is done with the buffer step k + 1 lands in (step k - 1's)
         fetch(k + 1);
-        const int ne = valid ? __ldg(eptr + t + 1) - __ldg(eptr + t) : 0;
+        const int e0 = valid ? __ldg(eptr + t) : 0;
+        const int ne = valid ? __ldg(eptr + t + 1) - e0 : 0;
         const int myrow = (valid && l < R) ? __ldg(trows + size_t(t) * R + l) : -1;
         const char* b = stage + size_t((k & 1) * TPW + g) * TB;
         const int32_t* sc = reinterpret_cast<const int32_t*>(b);
-        const double* sa = reinterpret_cast<const double*>(b + kUtE * 4);
-        const double* sb = reinterpret_cast<const double*>(b + kUtE * 4 + kUtE * R * 8);
+        const double* sa = VSM ? reinterpret_cast<const double*>(b + kUtE * 4) : A + size_t(e0) * R;
+        const double* sb = VSM ? reinterpret_cast<const double*>(b + kUtE * 4 + kUtE * R * 8) : Bv + size_t(e0) * R;
         double acc[R][CPL];
 #pragma unroll
         for (int i = 0; i < R; ++i)
@@ -1654,27 +1663,49 @@ __global__ void __launch_bounds__(NT, MINB) k_spmm_ut(int nt, Cols cc, const int
             for (int q = 0; q < CPL; ++q) acc[i][q] = 0.0;
         mbar_wait(bars + (k & 1), (k >> 1) & 1);
         // batches of 4 entries (the entry count is a multiple of 4): the gathers of one batch, then its products.
-        // UB == 8: two batches' gathers at once; UB == 44: software-pipelined, the next batch's gathers are in flight
-        // during the current batch's products. The groups of a warp run their own trip counts (no warp-level
+        // UB == 8: two batches' gathers at once. The groups of a warp run their own trip counts (no warp-level
         // operation inside).
-        auto gather = [&](int e, double2 (&x0)[4], double2 (&x1)[4]) {
+        struct Vals {
+            double2 a[4][2], b[SHIFT ? 4 : 1][2];
+        };
+        auto gather = [&](int e, double2 (&x0)[4], double2 (&x1)[4], Vals& v) {
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const size_t off = size_t(uint32_t(sc[e + u])) * uld;
                 x0[u] = __ldg(reinterpret_cast<const double2*>(P0 + off));
                 x1[u] = __ldg(reinterpret_cast<const double2*>(P1 + off));
+                if constexpr (!VSM) {
+                    v.a[u][0] = __ldg(reinterpret_cast<const double2*>(sa + size_t(e + u) * R));
+                    v.a[u][1] = __ldg(reinterpret_cast<const double2*>(sa + size_t(e + u) * R + 2));
+                    if constexpr (SHIFT) {
+                        v.b[u][0] = __ldg(reinterpret_cast<const double2*>(sb + size_t(e + u) * R));
+                        v.b[u][1] = __ldg(reinterpret_cast<const double2*>(sb + size_t(e + u) * R + 2));
+                    }
+                }
             }
         };
-        auto products = [&](int e, const double2 (&x0)[4], const double2 (&x1)[4]) {
+        auto products = [&](int e, const double2 (&x0)[4], const double2 (&x1)[4], const Vals& v) {
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const double2 a01 = *reinterpret_cast<const double2*>(sa + size_t(e + u) * R);
-                const double2 a23 = *reinterpret_cast<const double2*>(sa + size_t(e + u) * R + 2);
+                double2 a01, a23, b01 = make_double2(0.0, 0.0), b23 = b01;
+                if constexpr (VSM) {
+                    a01 = *reinterpret_cast<const double2*>(sa + size_t(e + u) * R);
+                    a23 = *reinterpret_cast<const double2*>(sa + size_t(e + u) * R + 2);
+                    if constexpr (SHIFT) {
+                        b01 = *reinterpret_cast<const double2*>(sb + size_t(e + u) * R);
+                        b23 = *reinterpret_cast<const double2*>(sb + size_t(e + u) * R + 2);
+                    }
+                } else {
+                    a01 = v.a[u][0];
+                    a23 = v.a[u][1];
+                    if constexpr (SHIFT) {
+                        b01 = v.b[u][0];
+                        b23 = v.b[u][1];
+                    }
+                }
                 const double av[R] = {a01.x, a01.y, a23.x, a23.y};
                 const double xv[CPL] = {x0[u].x, x0[u].y, x1[u].x, x1[u].y};
                 if constexpr (SHIFT) {
-                    const double2 b01 = *reinterpret_cast<const double2*>(sb + size_t(e + u) * R);
-                    const double2 b23 = *reinterpret_cast<const double2*>(sb + size_t(e + u) * R + 2);
                     const double bv[R] = {b01.x, b01.y, b23.x, b23.y};
 #pragma unroll
                     for (int i = 0; i < R; ++i)
@@ -1688,33 +1719,25 @@ __global__ void __launch_bounds__(NT, MINB) k_spmm_ut(int nt, Cols cc, const int
                 }
             }
         };
-        double2 xa0[4], xa1[4], xb0[4], xb1[4];
-        if constexpr (UB == 44) {
-            if (ne > 0) gather(0, xa0, xa1);
+        double2 xa0[4], xa1[4];
+        Vals va;
+        if constexpr (UB == 8) {
+            double2 xb0[4], xb1[4];
             int e = 0;
             for (; e + 8 <= ne; e += 8) {
-                gather(e + 4, xb0, xb1);
-                products(e, xa0, xa1);
-                if (e + 8 < ne) gather(e + 8, xa0, xa1);
-                products(e + 4, xb0, xb1);
-            }
-            if (e < ne) products(e, xa0, xa1);
-        } else if constexpr (UB == 8) {
-            int e = 0;
-            for (; e + 8 <= ne; e += 8) {
-                gather(e, xa0, xa1);
-                gather(e + 4, xb0, xb1);
-                products(e, xa0, xa1);
-                products(e + 4, xb0, xb1);
+                gather(e, xa0, xa1, va);
+                gather(e + 4, xb0, xb1, va);
+                products(e, xa0, xa1, va);
+                products(e + 4, xb0, xb1, va);
             }
             if (e < ne) {
-                gather(e, xa0, xa1);
-                products(e, xa0, xa1);
+                gather(e, xa0, xa1, va);
+                products(e, xa0, xa1, va);
             }
         } else {
             for (int e = 0; e < ne; e += 4) {
-                gather(e, xa0, xa1);
-                products(e, xa0, xa1);
+                gather(e, xa0, xa1, va);
+                products(e, xa0, xa1, va);
             }
         }
         __syncwarp();
@@ -2636,11 +2659,10 @@ bool try_ut(Ctx& c, const Level& L, const CgWork& w, const Cols& cc, const SellO
         return false;
     } else {
         if (!so.UT || (SHIFT && !so.UTB)) return false;
-        // 8 tiles per block: 256 threads at G = 32, 128 at G = 16, 64 at G = 8 (the staging buffers are per tile)
-        constexpr int NT = 8 * G, MINB = 512 / NT;
-        if (cc.N > NT) return false;  // the epilogue folds one column per thread
-        const size_t smt = ut_smem(G, NT, SHIFT);
+        constexpr int NT = 256;
+        constexpr bool VSM = G == 32;  // one warp per tile: values staged with the columns
         auto go = [&](auto kern) {
+            const size_t smt = ut_smem(G, NT, SHIFT, VSM);
             static bool attr = false;
             if (!attr) {
                 KSB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smt)));
@@ -2653,10 +2675,14 @@ bool try_ut(Ctx& c, const Level& L, const CgWork& w, const Cols& cc, const SellO
                    w.dev);
             return true;
         };
-        static const char* ube = std::getenv("KSB_UT_UB");  // gathers in flight per lane group (experiments)
-        if (ube && std::atoi(ube) == 4) return go(k_spmm_ut<G, SHIFT, 4, NT, MINB>);
-        if (ube && std::atoi(ube) == 44) return go(k_spmm_ut<G, SHIFT, 44, NT, MINB>);
-        return go(k_spmm_ut<G, SHIFT, 8, NT, MINB>);
+        if constexpr (VSM) {
+            static const char* ube = std::getenv("KSB_UT_UB");  // gathers in flight per lane group (experiments)
+            if (ube && std::atoi(ube) == 4) return go(k_spmm_ut<G, SHIFT, 4, NT, 2, true>);
+            if (ube && std::atoi(ube) == 43) return go(k_spmm_ut<G, SHIFT, 4, NT, 3, true>);
+            return go(k_spmm_ut<G, SHIFT, 8, NT, 2, true>);
+        } else {
+            return go(k_spmm_ut<G, SHIFT, 4, NT, 2, false>);
+        }
     }
 }
 
@@ -2936,7 +2962,10 @@ void cg_solve(Ctx& c, Level& L, int mat, int shift_mat, const double* h_sigma, c
     if (N == 16 && !shift) so.T8 = L.t8_values(mat);
     // blocks of more than 16 columns on a locality order: the union-tile SpMM (KSB_SPMM_UT=0 keeps the row kernel)
     const char* ut_env = std::getenv("KSB_SPMM_UT");
-    if (lo && p.G >= 8 && L.ut_nt > 0 && ld % 2 == 0 && !(ut_env && ut_env[0] == '0')) {
+    // (measured on configs[3], N = 21: 8 lanes per tile run at 6 warps per SM and lose to the row kernel, 2.8 vs 2.3 ms
+    // per SpMM, so narrower blocks take the view only with KSB_SPMM_UT=2)
+    const int ut_min_g = (ut_env && ut_env[0] == '2') ? 8 : 32;
+    if (lo && p.G >= ut_min_g && L.ut_nt > 0 && ld % 2 == 0 && !(ut_env && ut_env[0] == '0')) {
         so.UT = L.ut_values(mat);
         so.UTB = shift ? L.ut_values(shift_mat) : nullptr;
     }

@@ -103,8 +103,7 @@ def test_ut_view_is_a_retiling_of_the_ordered_pattern(level):
 
 def solve(L, B, N, ut: bool, **kw):
     os.environ["KSB_CG_REORDER"] = "2"  # force the locality order (small blocks stay natural otherwise)
-    if not ut:
-        os.environ["KSB_SPMM_UT"] = "0"
+    os.environ["KSB_SPMM_UT"] = "2" if ut else "0"  # 2: also blocks of 17..64 columns (8 / 16 lanes per tile)
     try:
         return L.cg_solve_host(kb.MAT_USER0, B, N, **kw)
     finally:
