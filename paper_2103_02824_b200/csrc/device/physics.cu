@@ -193,8 +193,90 @@ __global__ void k_sqload_elem_warp(int nt, const int32_t* __restrict__ tets, con
     }
 }
 
+/// many orbitals, even leading dimension: eight lanes per tet (four tets per warp), the lanes stride the orbital
+/// pairs of the four vertex rows with 16-byte loads, the Gram entries are folded over 8 lanes (3 shuffle stages
+/// instead of 5 over a whole warp), and the Keast quadrature of the quadratic form is a constant 4 x 10 matrix
+/// built once per block: out_k = vol occ sum_m C[k][m] gm[m], C[k][(a,b)] = (2 - [a == b]) sum_q w_q b_qk b_qa b_qb
+/// (k_sqload_elem_warp spent ~550 of its ~900 warp instructions per tet on that quadrature in one lane).
+/// N = 120 at 12.6 M tets: 9.7 -> see profiles/README.md.
+__global__ void __launch_bounds__(256) k_sqload_elem_g8(int nt, const int32_t* __restrict__ tets,
+                                                        const double* __restrict__ xyz,
+                                                        const int32_t* __restrict__ iidx,
+                                                        const double* __restrict__ Phi, int N, int ld, double occ,
+                                                        double* __restrict__ E4) {
+    __shared__ double C[4][10];
+    if (threadIdx.x < 40) {
+        const int k = threadIdx.x / 10, m = threadIdx.x % 10;
+        int a = 0, b = 0;
+        for (int i = 0; i < 4; ++i)
+            for (int j = i; j < 4; ++j)
+                if (gram_idx(i, j) == m) {
+                    a = i;
+                    b = j;
+                }
+        double sum = 0.0;
+        for (int q = 0; q < 11; ++q) sum += g_qw[q] * g_qb[q][k] * g_qb[q][a] * g_qb[q][b];
+        C[k][m] = (a == b ? 1.0 : 2.0) * sum;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, g = lane >> 3, l = lane & 7;
+    const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    const int nsteps = (nt + 3) / 4;
+    for (int ws = w0; ws < nsteps; ws += nw) {
+        const int t = ws * 4 + g;
+        const bool valid = t < nt;
+        const int4 v = valid ? reinterpret_cast<const int4*>(tets)[t] : make_int4(0, 0, 0, 0);
+        int rr[4] = {-1, -1, -1, -1};
+        if (valid) {
+            rr[0] = iidx[v.x];
+            rr[1] = iidx[v.y];
+            rr[2] = iidx[v.z];
+            rr[3] = iidx[v.w];
+        }
+        double gm[10];
+#pragma unroll
+        for (int k = 0; k < 10; ++k) gm[k] = 0.0;
+        for (int c = 2 * l; c < N; c += 16) {
+            double2 f[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                f[k] = make_double2(0.0, 0.0);
+                if (rr[k] >= 0) f[k] = __ldg(reinterpret_cast<const double2*>(Phi + size_t(rr[k]) * ld + c));
+                if (c + 1 >= N) f[k].y = 0.0;  // odd N: the pad column is not an orbital
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+#pragma unroll
+                for (int j = k; j < 4; ++j)
+                    gm[gram_idx(k, j)] = fma(f[k].y, f[j].y, fma(f[k].x, f[j].x, gm[gram_idx(k, j)]));
+        }
+#pragma unroll
+        for (int k = 0; k < 10; ++k) {
+            gm[k] += __shfl_xor_sync(0xffffffffu, gm[k], 4);
+            gm[k] += __shfl_xor_sync(0xffffffffu, gm[k], 2);
+            gm[k] += __shfl_xor_sync(0xffffffffu, gm[k], 1);
+        }
+        if (l == 0 && valid) {
+            TetG G;
+            tet_geometry(xyz, v, G);
+            double out[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                double sum = 0.0;
+#pragma unroll
+                for (int m = 0; m < 10; ++m) sum = fma(C[k][m], gm[m], sum);
+                out[k] = G.vol * occ * sum;
+            }
+            reinterpret_cast<double4*>(E4)[t] = make_double4(out[0], out[1], out[2], out[3]);
+        }
+    }
+}
+
 void launch_sqload_elem(Ctx& c, Level& L, const double* Phi, int N, int ld, double occ, double* e4) {
-    if (N >= 32)
+    if (N >= 32 && ld % 2 == 0 && (reinterpret_cast<uintptr_t>(Phi) & 15) == 0)
+        launch(c, "sqload", k_sqload_elem_g8, grid_of(c, int64_t(L.nt) * 8, 256), 256, 0, L.nt,
+               (const int32_t*)L.tets.p, (const double*)L.xyz.p, (const int32_t*)L.iidx.p, Phi, N, ld, occ, e4);
+    else if (N >= 32)
         launch(c, "sqload", k_sqload_elem_warp, grid_of(c, int64_t(L.nt) * 32, 256), 256, 0, L.nt,
                (const int32_t*)L.tets.p, (const double*)L.xyz.p, (const int32_t*)L.iidx.p, Phi, N, ld, occ, e4);
     else
