@@ -300,15 +300,8 @@ __device__ __forceinline__ void row_product_pf(int r, RowChunk<G, SHIFT>& ch, co
 #pragma unroll
     for (int k = 0; k < CPL; ++k) acc[k] = accB[k] = 0.0;
     const int wmax = __reduce_max_sync(0xffffffffu, ch.re - ch.rb);
-    // rows longer than one super-chunk (common on adaptive levels: up to ~30 entries against SL = 16 at G = 8):
-    // the second super-chunk is requested before the first one's gathers, so its latency hides behind them
-    RowChunk<G, SHIFT> c2;
-    if (wmax > SL) c2.load(r, ch.rb + SL, ch.re, l, col, A, B);
     for (int k0 = 0; k0 < wmax; k0 += SL) {
-        if (k0 == SL)
-            ch = c2;
-        else if (k0 > SL)
-            ch.load(r, ch.rb + SL, ch.re, l, col, A, B);  // rare: very long rows
+        if (k0 > 0) ch.load(r, ch.rb + SL, ch.re, l, col, A, B);  // rows longer than one super-chunk
 #pragma unroll
         for (int s0 = 0; s0 < SL; s0 += UB) {
             if (s0 > 0 && k0 + s0 >= wmax) break;
