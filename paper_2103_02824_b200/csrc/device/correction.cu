@@ -358,6 +358,50 @@ int hartree_solve(Level& L, Corrector& K, CgWork& cg, const double* d_PhiT, int 
     return st.iterations;
 }
 
+/// out[c * N + i] = in[i * nh + c]: the coarse orbital coefficients with the orbital index fastest
+__global__ void k_transpose_cols(int N, int nh, const double* __restrict__ in, double* __restrict__ out) {
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < int64_t(N) * nh; e += int64_t(gridDim.x) * blockDim.x) {
+        const int c = int(e / N), i = int(e % N);
+        out[e] = in[size_t(i) * nh + c];
+    }
+}
+
+/// k_expand for many orbitals: threads run over the orbitals of a row (coalesced Phi / PhiT rows; the coarse
+/// coefficients come from the transposed copy, N contiguous doubles per coarse dof), the same sums in the same order.
+/// N = 120 at 2.05 M rows: 3.96 -> see profiles/README.md.
+__global__ void k_expand_wide(int ni, int N, const int32_t* __restrict__ pcol, const double* __restrict__ pval,
+                              const double* __restrict__ phiHT, const double* __restrict__ th2,
+                              const double* __restrict__ PhiT, int ldT, double* __restrict__ Phi, int ld,
+                              const double* __restrict__ wH, const double* __restrict__ th1,
+                              const double* __restrict__ wt_full, const int32_t* __restrict__ interior,
+                              double* __restrict__ w_full) {
+    const int rb = blockDim.x / N, i = threadIdx.x % N, rl = threadIdx.x / N;
+    if (rl >= rb) return;
+    const double t2 = th2[i];
+    for (int r = blockIdx.x * rb + rl; r < ni; r += gridDim.x * rb) {
+        int pc[4];
+        double pv[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            pc[k] = __ldg(pcol + 4 * size_t(r) + k);
+            pv[k] = __ldg(pval + 4 * size_t(r) + k);
+        }
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (pc[k] >= 0) s += pv[k] * __ldg(phiHT + size_t(pc[k]) * N + i);
+        Phi[size_t(r) * ld + i] = s + t2 * PhiT[size_t(r) * ldT + i];
+        if (i == 0) {
+            double sw = 0.0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (pc[k] >= 0) sw += pv[k] * wH[pc[k]];
+            const int v = interior[r];
+            w_full[v] = (0.0 + sw) + th1[0] * wt_full[v];
+        }
+    }
+}
+
 void expand(Level& L, Corrector& K, const double* d_PhiT, int ldT, const double* d_wt_full, const double* d_bcb,
             double* d_Phi, int ld, double* d_w_full) {
     Ctx& c = *L.ctx;
@@ -366,6 +410,19 @@ void expand(Level& L, Corrector& K, const double* d_PhiT, int ldT, const double*
     // boundary entries of w first (ell), interior entries from the kernel
     launch(c, "elementwise", k_full_from, grid_of(c, L.n), kT, 0, 0, L.nb, (const int32_t*)L.interior.p,
            (const int32_t*)L.boundary.p, (const double*)nullptr, d_bcb, d_w_full);
+    if (K.sys.N >= 8 && K.sys.N <= kT) {
+        const int N = K.sys.N;
+        need(K.phiHT, int64_t(N) * L.nH);
+        launch(c, "expand", k_transpose_cols, grid_of(c, int64_t(N) * L.nH), kT, 0, N, L.nH,
+               (const double*)w.phi[cur].p, K.phiHT.p);
+        const int rb = kT / N;
+        const int grid = int(std::max<int64_t>(1, std::min<int64_t>((int64_t(L.ni) + rb - 1) / rb, int64_t(c.sm_count) * 8)));
+        launch(c, "expand", k_expand_wide, grid, kT, 0, L.ni, N, (const int32_t*)L.pint_col.p,
+               (const double*)L.pint_val.p, (const double*)K.phiHT.p, (const double*)w.th2[cur].p, d_PhiT, ldT, d_Phi,
+               ld, (const double*)w.wH[cur].p, (const double*)w.th1[cur].p, d_wt_full, (const int32_t*)L.interior.p,
+               d_w_full);
+        return;
+    }
     launch(c, "expand", k_expand, grid_of(c, L.ni), kT, 0, L.ni, K.sys.N, L.nH, (const int32_t*)L.pint_col.p,
            (const double*)L.pint_val.p, (const double*)w.phi[cur].p, (const double*)w.th2[cur].p, d_PhiT, ldT, d_Phi,
            ld, (const double*)w.wH[cur].p, (const double*)w.th1[cur].p, d_wt_full, (const int32_t*)L.interior.p,

@@ -55,6 +55,7 @@ struct Corrector {
     DevBuf<double> R0, Bblk, Xblk, Bc, Xc, PhiT;
     DevBuf<double> colscale;    // per-column right-hand-side scales of the orbital solves
     DevBuf<double> potf, wscr;  // standard MLC: w + v_xc (full), scratch w of expand
+    DevBuf<double> phiHT;       // coarse orbital coefficients, orbital index fastest (expand)
     DevBuf<int> idx;
     std::vector<double> scf_history;
     int precond = 0;  // preconditioner of the step in progress (StepOptions::precond)  // density changes of the last coarse_scf, kept when it fails (diagnostics)
