@@ -1582,11 +1582,15 @@ inline size_t ut_smem(int G, int threads, bool shift, bool vsm) {
 /// columns are staged (256 bytes per tile, so the staging no longer limits the resident warps) and each entry's four
 /// values are read from global memory with the entry's gathers (one broadcast 32-byte load per lane group) -- the
 /// narrow groups (G = 8, 16: four / two tiles per warp), whose value buffers would leave 6 warps per SM.
-template <int G, bool SHIFT, int UB, int NT, int MINB, bool VSM>
+template <int G, bool SHIFT, int UB, int NT, int MINB, bool VSM, bool HINT = false>
 __global__ void __launch_bounds__(NT, MINB) k_spmm_ut(int nt, Cols cc, const int32_t* __restrict__ trows,
                                                      const int32_t* __restrict__ eptr, const int32_t* __restrict__ ent,
                                                      const double* __restrict__ A, const double* __restrict__ Bv,
-                                                     const double* __restrict__ P, double* __restrict__ AP, CgDev s) {
+                                                     const double* __restrict__ P, double* __restrict__ AP, CgDev s,
+                                                     int sync_every) {
+    // sync_every > 0 (cooperative launch): a grid barrier every sync_every warp steps keeps all warps inside one
+    // stretch of the Morton tile sequence, so the X rows that neighbouring tiles share are still in L2 when the
+    // next tile asks for them (without it the warps drift apart over the ~1200 steps of a 1e7-row level)
     extern __shared__ double sm[];
     constexpr int CPL = 4, R = kUtR, TPW = 32 / G, W = 4 * G;
     constexpr int VS = SHIFT ? 2 : 1;
@@ -1609,6 +1613,7 @@ __global__ void __launch_bounds__(NT, MINB) k_spmm_ut(int nt, Cols cc, const int
     const double* P0 = P + min(c0, cmax);
     const double* P1 = P + min(c1, cmax);
     const uint32_t uld = uint32_t(ld);
+    const uint64_t pol = HINT ? l2_policy_last() : 0;
     double pd[CPL], sg[CPL];
 #pragma unroll
     for (int q = 0; q < CPL; ++q) {
@@ -1644,7 +1649,10 @@ __global__ void __launch_bounds__(NT, MINB) k_spmm_ut(int nt, Cols cc, const int
     }
     __syncwarp();
     fetch(0);
-    for (int k = 0; k < ksteps; ++k) {
+    const int kall = (tw.tend + tw.step - 1) / tw.step;  // the same count for every warp of the grid
+    for (int k = 0; k < kall; ++k) {
+        if (sync_every > 0 && k > 0 && k % sync_every == 0) cooperative_groups::this_grid().sync();
+        if (k >= ksteps) continue;
         const int t = (tw.t0 + k * tw.step) * TPW + g;
         const bool valid = t < nt;
         __syncwarp();  // every lane is done with the buffer step k + 1 lands in (step k - 1's)
@@ -1672,8 +1680,13 @@ __global__ void __launch_bounds__(NT, MINB) k_spmm_ut(int nt, Cols cc, const int
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const size_t off = size_t(uint32_t(sc[e + u])) * uld;
-                x0[u] = __ldg(reinterpret_cast<const double2*>(P0 + off));
-                x1[u] = __ldg(reinterpret_cast<const double2*>(P1 + off));
+                if constexpr (HINT) {  // gathered rows evict-last in L2 (the matrix and output streams pass by)
+                    x0[u] = ldg2_hint(P0 + off, pol);
+                    x1[u] = ldg2_hint(P1 + off, pol);
+                } else {
+                    x0[u] = __ldg(reinterpret_cast<const double2*>(P0 + off));
+                    x1[u] = __ldg(reinterpret_cast<const double2*>(P1 + off));
+                }
                 if constexpr (!VSM) {
                     v.a[u][0] = __ldg(reinterpret_cast<const double2*>(sa + size_t(e + u) * R));
                     v.a[u][1] = __ldg(reinterpret_cast<const double2*>(sa + size_t(e + u) * R + 2));
@@ -2663,22 +2676,46 @@ bool try_ut(Ctx& c, const Level& L, const CgWork& w, const Cols& cc, const SellO
         constexpr bool VSM = G == 32;  // one warp per tile: values staged with the columns
         auto go = [&](auto kern) {
             const size_t smt = ut_smem(G, NT, SHIFT, VSM);
-            static bool attr = false;
-            if (!attr) {
+            static std::map<const void*, bool> attr;  // (the variants share one function-pointer type)
+            if (!attr[reinterpret_cast<const void*>(kern)]) {
                 KSB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smt)));
-                attr = true;
+                attr[reinterpret_cast<const void*>(kern)] = true;
             }
             const int want = ceil_div(ceil_div(L.ut_nt, 32 / G), NT / 32);
             const int grid = std::max(1, std::min({want, resident_grid(c, kern, NT, smt), w.cap_blocks}));
-            launch(c, "spmm", kern, grid, NT, smt, L.ut_nt, cc, (const int32_t*)L.ut_rows.p,
-                   (const int32_t*)L.ut_eptr.p, (const int32_t*)L.ut_ent.p, so.UT, so.UTB, (const double*)w.P, w.AP,
-                   w.dev);
+            const char* senv = std::getenv("KSB_UT_SYNC");  // read per launch (the probes switch it)
+            int se = senv ? std::atoi(senv) : 16;
+            if (se > 0) {  // resident grid: cooperative launch with the periodic grid barrier
+                int nt = L.ut_nt;
+                Cols ccv = cc;
+                const int32_t* rows = L.ut_rows.p;
+                const int32_t* ep = L.ut_eptr.p;
+                const int32_t* en = L.ut_ent.p;
+                const double* A = so.UT;
+                const double* Bv = so.UTB;
+                const double* Pp = w.P;
+                double* APp = w.AP;
+                CgDev dv = w.dev;
+                void* args[] = {&nt, &ccv, &rows, &ep, &en, &A, &Bv, &Pp, &APp, &dv, &se};
+                cudaEvent_t e0 = nullptr;
+                if (c.profiling) c.begin("spmm", &e0);
+                KSB_CUDA_CHECK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(grid), dim3(NT),
+                                                           args, smt, c.stream));
+                ++c.launches;
+                if (c.profiling) c.end("spmm", e0);
+            } else {
+                launch(c, "spmm", kern, grid, NT, smt, L.ut_nt, cc, (const int32_t*)L.ut_rows.p,
+                       (const int32_t*)L.ut_eptr.p, (const int32_t*)L.ut_ent.p, so.UT, so.UTB, (const double*)w.P,
+                       w.AP, w.dev, 0);
+            }
             return true;
         };
         if constexpr (VSM) {
             static const char* ube = std::getenv("KSB_UT_UB");  // gathers in flight per lane group (experiments)
             if (ube && std::atoi(ube) == 4) return go(k_spmm_ut<G, SHIFT, 4, NT, 2, true>);
             if (ube && std::atoi(ube) == 43) return go(k_spmm_ut<G, SHIFT, 4, NT, 3, true>);
+            const char* henv = std::getenv("KSB_UT_HINT");  // read per launch (probes)
+            if (henv && henv[0] == '1') return go(k_spmm_ut<G, SHIFT, 8, NT, 2, true, true>);
             return go(k_spmm_ut<G, SHIFT, 8, NT, 2, true>);
         } else {
             return go(k_spmm_ut<G, SHIFT, 4, NT, 2, false>);

@@ -45,7 +45,12 @@ for k in range(2):
 # per-family CUDA-event times of one more step (the context's profiling counters; graphs are off while profiling)
 import os  # noqa: E402
 
-if os.environ.get("KSB_PROBE_FAMILIES", "1") != "0":
+FAMS = ("assemble", "axpby", "rho_vxc", "moments", "bc", "sqload", "lift", "elementwise", "cg_setup", "spmm",
+        "cg_update_r", "cg_update_px", "cg_trueres", "cg_coop", "mg", "project", "project_asm", "coarse",
+        "inner_tridiag", "expand", "norm", "energy", "reduce")
+
+
+def families(tag):
     ctx.sync()
     ctx.reset_counters()
     ctx.set_profiling(True)
@@ -53,11 +58,21 @@ if os.environ.get("KSB_PROBE_FAMILIES", "1") != "0":
     ctx.sync()
     ctx.set_profiling(False)
     fam = {}
-    for nm in ("assemble", "axpby", "rho_vxc", "moments", "bc", "sqload", "lift", "elementwise", "cg_setup", "spmm",
-               "cg_update_r", "cg_update_px", "cg_trueres", "cg_coop", "mg", "project", "project_asm", "coarse",
-               "inner_tridiag", "expand", "norm", "energy", "reduce"):
+    for nm in FAMS:
         ms, cnt = ctx.kernel_time(nm)
         if cnt:
             fam[nm] = {"ms": round(ms, 2), "launches": int(cnt), "avg_us": round(1e3 * ms / cnt, 1)}
-    print(json.dumps({"families": fam, "n_i": L.ni, "nnz": L.nnz_ii, "N": N, "ms_total": lg["ms_total"],
+    print(json.dumps({"tag": tag, "families": fam, "n_i": L.ni, "nnz": L.nnz_ii, "N": N, "ms_total": lg["ms_total"],
                       "ms_bvp": lg["ms_bvp"]}), flush=True)
+
+
+if os.environ.get("KSB_PROBE_FAMILIES", "1") != "0":
+    # KSB_PROBE_AB="NAME=v1,v2,...": one profiled step per value of an environment switch the library reads per launch
+    ab = os.environ.get("KSB_PROBE_AB")
+    if ab:
+        name, vals = ab.split("=")
+        for v in vals.split(","):
+            os.environ[name] = v
+            families(f"{name}={v}")
+    else:
+        families("default")
