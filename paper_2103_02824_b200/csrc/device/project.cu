@@ -209,10 +209,16 @@ __global__ void __launch_bounds__(kProjThreads) k_proj_orbital(ProjIn in, double
 // consecutive threads from one row of Phi (coalesced). Each thread owns the 49 accumulators of its orbital;
 // tet slots are folded in fixed order at the end.
 constexpr int kWideTets = 64;   // fine tets per staged chunk
-constexpr int kWideRec = 104;   // doubles per staged tet: mu 16, E1 E3 E4 Eone S (5 x 16), vol, 4 rows (as int), pad
+constexpr int kWideRec0 = 104;  // record without the T_k block
+constexpr int kWideRec = 144;   // doubles per staged tet: mu 16, E1 E3 E4 Eone S (5 x 16), vol, 4 rows (as int), pad,
+                                // T_k = mu^T E^(k) mu for the four hat weights (4 x 10 unique entries) at 104
 
+/// TK: the orbital mass element through the precomputed T_k (many orbitals: the 4 x (element + mu^T E mu) per tet of
+/// the staging amortise over >= 64 orbitals; at N = 21 they cost more than they save, 32.6 -> 38.9 ms on configs[3])
+template <bool TK>
 __global__ void __launch_bounds__(kProjThreads) k_proj_orbital_wide(ProjIn in, double* __restrict__ part) {
-    extern __shared__ double st[];  // kWideTets * kWideRec, reused for the final fold
+    constexpr int REC = TK ? kWideRec : kWideRec0;
+    extern __shared__ double st[];  // kWideTets * REC, reused for the final fold
     const int ch = blockIdx.x;
     const int C = in.ch_c[ch];
     const int N = in.N;
@@ -232,7 +238,7 @@ __global__ void __launch_bounds__(kProjThreads) k_proj_orbital_wide(ProjIn in, d
         const int nc = min(kWideTets, pe - c0);
         __syncthreads();
         if (threadIdx.x < nc) {
-            double* R = st + threadIdx.x * kWideRec;
+            double* R = st + threadIdx.x * REC;
             const int t = in.anc_tets[c0 + threadIdx.x];
             const int4 v = reinterpret_cast<const int4*>(in.tets)[t];
             TetG G;
@@ -273,11 +279,29 @@ __global__ void __launch_bounds__(kProjThreads) k_proj_orbital_wide(ProjIn in, d
             ri[1] = in.iidx[v.y];
             ri[2] = in.iidx[v.z];
             ri[3] = in.iidx[v.w];
+            // the orbital mass element is linear in the orbital's vertex values: M_phi = sum_k phi_k E^(k) with E^(k)
+            // the element of the hat weight k, so mu^T M_phi mu = sum_k phi_k T_k with the orbital-independent
+            // T_k = mu^T E^(k) mu (symmetric: 10 entries), 40 multiply-adds per (orbital, tet) instead of 128 + the element
+#pragma unroll
+            for (int k = 0; TK && k < 4; ++k) {
+                double hat[4] = {0.0, 0.0, 0.0, 0.0};
+                hat[k] = 1.0;
+                mass_elem(G.vol, hat, E);
+                double T[16];
+#pragma unroll
+                for (int e = 0; e < 16; ++e) T[e] = 0.0;
+                acc_proj(mu, E, T);
+                int m = 0;
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+#pragma unroll
+                    for (int b = a; b < 4; ++b) R[104 + 10 * k + m++] = T[4 * a + b];
+            }
         }
         __syncthreads();
         if (act)
             for (int q = slot; q < nc; q += TS) {
-                const double* R = st + q * kWideRec;
+                const double* R = st + q * REC;
                 const int* ri = reinterpret_cast<const int*>(R + 97);
                 double ph[4];
 #pragma unroll
@@ -285,9 +309,27 @@ __global__ void __launch_bounds__(kProjThreads) k_proj_orbital_wide(ProjIn in, d
                 double mu[4][4], E[4][4];
 #pragma unroll
                 for (int k = 0; k < 16; ++k) mu[k / 4][k % 4] = R[k];
-                mass_elem(R[96], ph, E);  // M_phi
-                acc_proj(mu, E, acc + 0);
-                acc_vec(mu, E, ph, acc + 40);  // rhs = P^T (M_phi phi)
+                if constexpr (!TK) {
+                    mass_elem(R[96], ph, E);  // M_phi
+                    acc_proj(mu, E, acc + 0);
+                    acc_vec(mu, E, ph, acc + 40);  // rhs = P^T (M_phi phi)
+                } else {  // A_h4 += mu^T M_phi mu = sum_k phi_k T_k (upper triangle; mirrored after the tet loop)
+                    int m = 0;
+#pragma unroll
+                    for (int a = 0; a < 4; ++a)
+#pragma unroll
+                        for (int b = a; b < 4; ++b, ++m)
+                            acc[4 * a + b] += ph[0] * R[104 + m] + ph[1] * R[114 + m] + ph[2] * R[124 + m] + ph[3] * R[134 + m];
+                    // rhs += mu^T (M_phi phi), (M_phi phi)_i = |T| / 120 (W^2 + q + 2 phi_i (W + phi_i)), W = sum phi, q = sum phi^2
+                    const double W = ph[0] + ph[1] + ph[2] + ph[3];
+                    const double q = ph[0] * ph[0] + ph[1] * ph[1] + ph[2] * ph[2] + ph[3] * ph[3];
+                    const double sc = R[96] / 120.0, base = W * W + q;
+                    double y[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) y[i] = sc * (base + 2.0 * ph[i] * (W + ph[i]));
+#pragma unroll
+                    for (int a = 0; a < 4; ++a) acc[40 + a] += mu[0][a] * y[0] + mu[1][a] * y[1] + mu[2][a] * y[2] + mu[3][a] * y[3];
+                }
 #pragma unroll
                 for (int m = 0; m < 5; ++m) {
 #pragma unroll
@@ -296,6 +338,12 @@ __global__ void __launch_bounds__(kProjThreads) k_proj_orbital_wide(ProjIn in, d
                     acc[44 + m] += acc_vec(mu, E, ph, acc + 16 + 4 * m);
                 }
             }
+    }
+    if constexpr (TK) {
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = a + 1; b < 4; ++b) acc[4 * b + a] = acc[4 * a + b];
     }
     // fold the tet slots of each orbital in slot order
     __syncthreads();
@@ -737,13 +785,18 @@ void project_blocks(Level& L, const double* Phi, int N, int ld, const double* wt
                (const double*)o.pgpart.p, o.part.p + size_t(nct) * kStride);
         split = false;  // every record is in place
     } else if (N >= kProjWideMin) {
-        const size_t smem = sizeof(double) * std::max(kWideTets * kWideRec, kProjThreads * kOrbK);
+        const size_t smem = sizeof(double) * std::max(kWideTets * (N >= 64 ? kWideRec : kWideRec0), kProjThreads * kOrbK);
+        const size_t smem_max = sizeof(double) * std::max(kWideTets * kWideRec, kProjThreads * kOrbK);
         static bool attr = false;
         if (!attr) {
-            KSB_CUDA_CHECK(cudaFuncSetAttribute(k_proj_orbital_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            KSB_CUDA_CHECK(cudaFuncSetAttribute(k_proj_orbital_wide<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_max)));
+            KSB_CUDA_CHECK(cudaFuncSetAttribute(k_proj_orbital_wide<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_max)));
             attr = true;
         }
-        launch(c, "project", k_proj_orbital_wide, dim3(nch, ceil_div(N, kProjThreads)), kProjThreads, smem, in, dst);
+        if (N >= 64)
+            launch(c, "project", k_proj_orbital_wide<true>, dim3(nch, ceil_div(N, kProjThreads)), kProjThreads, smem, in, dst);
+        else
+            launch(c, "project", k_proj_orbital_wide<false>, dim3(nch, ceil_div(N, kProjThreads)), kProjThreads, smem, in, dst);
     } else if (N > 0) {
         launch(c, "project", k_proj_orbital, dim3(nch, N), kProjThreads, 0, in, dst);
     }

@@ -625,12 +625,13 @@ std::shared_ptr<FineTopology> build_topology(const Hierarchy& h, int level, bool
         if (!detect(ii.ptr, ii.col, 0) && !topo->lo_perm.empty()) detect(topo->lo_ptr, topo->lo_col, 1);
     }
 
-    // Levels whose (z, y, x) order is no stencil (adaptive levels) take the Morton order of the vertices instead: a
-    // row's neighbours are then close in every direction (median |i - j| ~13 against ~180 rows), so the gathered
-    // X rows of the wide SpMM stay in L1 / L2 / the TLB reach at 1e7 rows. KSB_LO_MORTON=0 keeps (z, y, x).
+    // Opt-in (KSB_LO_MORTON=1): levels whose (z, y, x) order is no stencil (adaptive levels) take the Morton order
+    // of the vertices instead (median |i - j| ~13 against ~180 rows, but a long tail across octant boundaries).
+    // Measured at the configs' sizes: N = 120 union-tile SpMM at 11.56 M rows 15.9 -> 15.8 ms, N = 21 row kernel at
+    // 4.4 M rows ~15 % slower (its far neighbours miss L2, which the (z, y, x) band keeps resident) -- so off.
     if (!topo->lo_perm.empty() && !(topo->dia_ng > 0 && topo->dia_lo == 1)) {
         const char* env = std::getenv("KSB_LO_MORTON");
-        if (!(env && env[0] == '0')) {
+        if (env && env[0] == '1') {
             morton_order(m.xyz.data(), S.interior.data(), ni, topo->lo_perm);
             build_lo();
         }
