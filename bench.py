@@ -351,7 +351,9 @@ ADAPTIVE_SWEEPS = 10  # inner sweeps per timed step: the work is defined whateve
 # parity / CPU-sample level: the finest level of the same hierarchy with at most this many vertices
 ADAPTIVE_SAMPLE_N = {"cfg3": 60000, "cfg4": 40000, "cfg5": 12000}
 ADAPTIVE_SAMPLE_SWEEPS = 3  # inner sweeps of the sample step (the oracle's dense bordered eigensolves dominate it)
-PROJ_FLOP_PER_TET_ORB = 500  # k_proj_orbital_wide: sum_k phi_k T_k (80), M_phi phi closed form + mu^T y (~60), five E x / mu^T y / x.y (360)
+# k_proj_orbital_wide per (orbital, fine tet). N >= 64 (T_k form): sum_k phi_k T_k (80), M_phi phi closed form +
+# mu^T y (~60), five E x / mu^T y / x.y (360). Below: M_phi element, P^T E P (256), six E x / mu^T y / x.y (432)
+PROJ_FLOP_PER_TET_ORB = {True: 500, False: 720}
 
 
 def fp64_peak():
@@ -414,7 +416,7 @@ def adaptive_case(name, args, ctx, stream, world, rank):
     bvp_bytes = block_its * (12 * L.nnz_ii + 4 * (L.ni + 1) + 16 * L.ni) + 88 * L.ni * int(its.sum())
     peak, peak_kind = measured_peak()
     fpk, fp_kind = fp64_peak()
-    proj_flop = PROJ_FLOP_PER_TET_ORB * N * L.nt
+    proj_flop = PROJ_FLOP_PER_TET_ORB[N >= 64] * N * L.nt
     rec.update({
         "ms_per_step": ms, "gpu_launches": launches,
         "phases_ms": {k: round(lg["ms_" + k], 3) for k in ("bvp", "hartree", "project", "inner")},
