@@ -266,9 +266,15 @@ void solve_orbitals(Level& L, Corrector& K, CgWork& cg, const StepOptions& o, co
     co.tol = o.tol_linear;
     co.check_every = o.check_every;
     co.precond = o.precond;
-    std::vector<CgColumnStats> st(N);
-    cg_solve(c, L, MAT_H, -1, nullptr, K.R0.p, d_PhiT, N, ld, co, st.data(), cg);
     if (ldT != ld) raise(KSB_INVALID_ARGUMENT, "solve_orbitals: ld mismatch");
+    // An odd block is solved with its pad column as one more right-hand side that is identically zero (converged
+    // at iteration 0, proj/src/solver.cpp:62-66): the columns are independent, and the even block takes the CG's
+    // paired 16-byte update passes (configs[3], N = 21: update_r 4.5 -> ~6 TB/s)
+    const int Ncg = (N > 1 && (N & 1) && ld > N && N < 128) ? N + 1 : N;
+    if (Ncg > N)
+        KSB_CUDA_CHECK(cudaMemset2DAsync(K.R0.p + N, sizeof(double) * ld, 0, sizeof(double), ni, c.stream));
+    std::vector<CgColumnStats> st(Ncg);
+    cg_solve(c, L, MAT_H, -1, nullptr, K.R0.p, d_PhiT, Ncg, ld, co, st.data(), cg);
     std::vector<int> attempt(N, -1), iters(N);
     std::vector<int> fail;
     for (int i = 0; i < N; ++i) {
@@ -294,8 +300,10 @@ void solve_orbitals(Level& L, Corrector& K, CgWork& cg, const StepOptions& o, co
         spmm(c, L, L.mats[1].ii.p, nullptr, nullptr, K.Xc.p, nf, ldc, K.Bc.p, ldc);  // (lambda + sigma) M phi
         launch(c, "elementwise", k_scale_cols, grid_of(c, int64_t(ni) * nf), kT, 0, ni, nf, (const double*)dsc, K.Bc.p,
                ldc);
-        std::vector<CgColumnStats> sst(nf);
-        cg_solve(c, L, MAT_H, 1, sig.data(), K.Bc.p, K.Xc.p, nf, ldc, co, sst.data(), cg);
+        const int nfc = nf > 1 ? ldc : nf;  // odd count: the zeroed pad column rides along (see above)
+        sig.resize(nfc, sigma);
+        std::vector<CgColumnStats> sst(nfc);
+        cg_solve(c, L, MAT_H, 1, sig.data(), K.Bc.p, K.Xc.p, nfc, ldc, co, sst.data(), cg);
         std::vector<int> take(nf), still;
         for (int j = 0; j < nf; ++j) {
             iters[fail[j]] += sst[j].iterations;
