@@ -2735,8 +2735,11 @@ void launch_iteration(Ctx& c, const Level& L, const CgWork& w, const Cols& cc, c
     } else if (!SPLIT && try_ut<G, SHIFT>(c, L, w, cc, so)) {
     } else if (!SHIFT && try_dia(c, L, w, cc, so)) {
     } else {
+        // resident blocks per SM the row kernel is compiled for. Lane groups of up to 16 (N <= 64) keep two (col, val)
+        // chunk sets of 16 / G x G slots in registers: at 64 registers (4 blocks) they spill 70-340 bytes, at 128
+        // (2 blocks) nothing -- configs[3] (N = 21, shifted): BVPs 1.98 -> 1.54 s. One row per warp (G = 32) keeps 4.
         static const char* mb = std::getenv("KSB_SPMM_MINB");
-        const int minb = mb ? std::atoi(mb) : KSB_SPMM_MINB;
+        const int minb = mb ? std::atoi(mb) : (G <= 16 ? 2 : KSB_SPMM_MINB);
         static const char* senv = std::getenv("KSB_SPMM_SYNC");
         static const char* denv = std::getenv("KSB_SPMM_DIE");
         const int die = denv ? std::atoi(denv) : 0;
@@ -2793,7 +2796,7 @@ void launch_iteration(Ctx& c, const Level& L, const CgWork& w, const Cols& cc, c
             go(k_spmm_dot<G, CPL, SHIFT, SPLIT, FULL, 5>);
         else if (FULL == 3 && minb == 3)
             go(k_spmm_dot<G, CPL, SHIFT, SPLIT, FULL, 3>);
-        else if (FULL && minb == 2)
+        else if (minb == 2)
             go(k_spmm_dot<G, CPL, SHIFT, SPLIT, FULL, 2>);
         else
             go(k_spmm_dot<G, CPL, SHIFT, SPLIT, FULL>);
